@@ -1,0 +1,313 @@
+"""Seeded synthetic inputs for the randomized Tucker/HOSVD hot path.
+
+This module serves BOTH the fp64 oracle (``oracle/``) and the CUDA path
+(``paper_2001_07124_b200``).  It holds none of the method's arithmetic: it only
+draws random numbers and assembles the *input* tensors and the random test
+matrices Omega that the method consumes (Omega is passed explicitly to both
+sides, so neither side draws random numbers of its own).
+
+Recipes (BASELINE.json configs):
+
+  * low multilinear rank tensor  X_s = [[G; U_1, ..., U_N]]  with a Gaussian core
+    and orthonormal factors (Q of a Gaussian matrix), §VIII "Random Low
+    Multilinear Rank Tensors" (the paper's factors are Gaussian, the
+    BASELINE configs ask for orthonormal ones);
+  * noise  X = X_s + gamma*N,  gamma = rho*||X_s||_F / ||N||_F  with the realized
+    ||N|| (PAPER.md Eq. noisytensor, SNR P:836-838; reading R11);
+  * cfg4's decaying core  G_ijk = N(0,1) / (i*j*k), 1-based (reading R14);
+  * Gaussian Omega_n in R^{J_n x K_n}, rows in the paper's j-index order
+    (PAPER.md Eq. proj, j-index P:99-105), generated in fp64 and
+    rounded to the working dtype (reading R15);
+  * Kronecker Omega_k^{(n)} in R^{d_k x L_k} (reading R3).
+
+Memory layout convention shared by both sides: a tensor with math shape
+(I_1, ..., I_N) is stored first-mode-fastest.  In numpy that is
+a Fortran-ordered array of shape (I_1..I_N); in torch it is a C-contiguous tensor
+of shape (I_N..I_1) (``to_device_layout``).
+
+Seeds: every random object draws from
+``numpy.random.SeedSequence([BASE_SEED, cfg, object, mode, slab])``.
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+from typing import Optional, Sequence
+
+import numpy as np
+
+BASE_SEED = 2001_07124
+
+# object ids inside the seed tuple
+_OBJ_CORE, _OBJ_FACTOR, _OBJ_NOISE, _OBJ_OMEGA, _OBJ_KRON = 1, 2, 3, 4, 5
+
+
+def rng_for(*key: int) -> np.random.Generator:
+    """Deterministic PCG64 stream for a key tuple (cfg, object, mode, slab, ...)."""
+    return np.random.default_rng(np.random.SeedSequence([BASE_SEED, *[int(k) for k in key]]))
+
+
+@dataclasses.dataclass(frozen=True)
+class Config:
+    """One BASELINE.json configuration (or a scaled-down variant of its recipe)."""
+    name: str
+    cfg_id: int
+    dims: tuple
+    dtype: str                      # "f64" | "f32"
+    core_dims: tuple                # multilinear rank of the signal
+    core_kind: str                  # "gauss" | "decay"
+    noise: str                      # "abs" | "rel" | "none"
+    noise_level: float
+    ranks: tuple                    # target multilinear rank R_n
+    p: int                          # oversampling
+    q: int                          # power iterations
+    algo: str                       # "hosvd" | "sthosvd"
+    omega: str                      # "gauss" | "kron"
+
+    @property
+    def order(self) -> int:
+        return len(self.dims)
+
+    @property
+    def np_dtype(self):
+        return np.float64 if self.dtype == "f64" else np.float32
+
+    @property
+    def nbytes(self) -> int:
+        return int(np.prod(self.dims)) * (8 if self.dtype == "f64" else 4)
+
+    def J(self, n: int) -> int:
+        return int(np.prod([d for k, d in enumerate(self.dims) if k != n]))
+
+    def K(self, n: int) -> int:
+        """Gaussian sketch width K_n = min(R_n + p, I_n, J_n) (reading R1)."""
+        return min(self.ranks[n] + self.p, self.dims[n], self.J(n))
+
+    def scaled(self, dims: Sequence[int], core_dims: Sequence[int], ranks: Sequence[int],
+               name: Optional[str] = None) -> "Config":
+        return dataclasses.replace(self, dims=tuple(dims), core_dims=tuple(core_dims),
+                                   ranks=tuple(ranks), name=name or self.name + "-small")
+
+
+# BASELINE.json configs[0..4]  (cfg1..cfg5)
+CONFIGS = {
+    "cfg1": Config("cfg1", 1, (64, 64, 64), "f64", (5, 5, 5), "gauss", "abs", 1e-6,
+                   (5, 5, 5), 5, 0, "hosvd", "gauss"),
+    "cfg2": Config("cfg2", 2, (500, 500, 500), "f32", (20, 20, 20), "gauss", "rel", 1e-2,
+                   (20, 20, 20), 10, 1, "hosvd", "gauss"),
+    "cfg3": Config("cfg3", 3, (128, 128, 128, 128), "f32", (16, 16, 16, 16), "gauss", "rel", 1e-3,
+                   (16, 16, 16, 16), 8, 0, "sthosvd", "kron"),
+    "cfg4": Config("cfg4", 4, (2048, 2048, 256), "f32", (200, 200, 100), "decay", "none", 0.0,
+                   (50, 50, 20), 10, 2, "hosvd", "gauss"),
+    "cfg5": Config("cfg5", 5, (2048, 2048, 2048), "f32", (64, 64, 64), "gauss", "rel", 1e-3,
+                   (64, 64, 64), 16, 1, "hosvd", "gauss"),
+}
+
+
+def orthonormal_factor(rng: np.random.Generator, rows: int, cols: int) -> np.ndarray:
+    """Q factor of a Gaussian rows x cols matrix (BASELINE.json: "U_n orthonormal from QR")."""
+    a = rng.standard_normal((rows, cols))
+    qm, _ = np.linalg.qr(a)
+    return qm
+
+
+def make_core(cfg: Config) -> np.ndarray:
+    """Signal core G (fp64, Fortran order)."""
+    g = rng_for(cfg.cfg_id, _OBJ_CORE).standard_normal(cfg.core_dims)
+    if cfg.core_kind == "decay":
+        # reading R14: G_ijk = N(0,1) / (i*j*k) with 1-based indices
+        for n, d in enumerate(cfg.core_dims):
+            shape = [1] * cfg.order
+            shape[n] = d
+            g = g / np.arange(1, d + 1, dtype=np.float64).reshape(shape)
+    return np.asfortranarray(g)
+
+
+def make_factors(cfg: Config) -> list:
+    return [orthonormal_factor(rng_for(cfg.cfg_id, _OBJ_FACTOR, n), cfg.dims[n], cfg.core_dims[n])
+            for n in range(cfg.order)]
+
+
+def _expand(core: np.ndarray, factors: Sequence[np.ndarray]) -> np.ndarray:
+    """[[core; U_1..U_N]] by successive tensordot (input assembly only)."""
+    t = core
+    for n, u in enumerate(factors):
+        # contract mode n of t with the columns of u, put the new axis back at n
+        t = np.moveaxis(np.tensordot(u, t, axes=([1], [n])), 0, n)
+    return np.asfortranarray(t)
+
+
+def make_tensor(cfg: Config, return_parts: bool = False):
+    """Host (numpy fp64 assembly, rounded to cfg dtype) input tensor X, Fortran order.
+
+    Returns X in cfg dtype; with ``return_parts`` also (X_signal_fp64, core, factors, gamma).
+    """
+    core = make_core(cfg)
+    factors = make_factors(cfg)
+    xs = _expand(core, factors)
+    gamma = 0.0
+    x = xs
+    if cfg.noise != "none":
+        nz = np.asfortranarray(rng_for(cfg.cfg_id, _OBJ_NOISE).standard_normal(cfg.dims))
+        if cfg.noise == "abs":
+            gamma = cfg.noise_level
+        else:  # reading R11: rho relative to ||X_s||_F with the realized ||N||_F
+            gamma = cfg.noise_level * np.linalg.norm(xs.ravel(order="K")) / np.linalg.norm(nz.ravel(order="K"))
+        x = np.asfortranarray(xs + gamma * nz)
+    out = np.asfortranarray(x.astype(cfg.np_dtype))
+    if return_parts:
+        return out, xs, core, factors, gamma
+    return out
+
+
+def gaussian_omega(cfg: Config, n: int, K: Optional[int] = None, rows: Optional[int] = None,
+                   row0: int = 0) -> np.ndarray:
+    """Gaussian Omega_n (J_n x K_n, C order = row-major, element (j,k) at j*K+k).
+
+    ``rows``/``row0`` select a contiguous block of rows (a slab's local rows), drawn
+    from the same stream as the full matrix so slabs and the whole agree bit-exactly.
+    """
+    K = cfg.K(n) if K is None else K
+    J = cfg.J(n)
+    rows = J - row0 if rows is None else rows
+    rng = rng_for(cfg.cfg_id, _OBJ_OMEGA, n)
+    if row0:
+        rng.standard_normal(row0 * K)  # advance the stream (row-major draw order)
+    om = rng.standard_normal((rows, K))
+    return np.ascontiguousarray(om.astype(cfg.np_dtype))
+
+
+def kron_widths(cfg: Config, n: int) -> list:
+    """Reading R3: uniform L = ceil((R_n+p)^(1/(N-1))) per other mode."""
+    L = int(math.ceil((cfg.ranks[n] + cfg.p) ** (1.0 / (cfg.order - 1)) - 1e-12))
+    return [L if k != n else 0 for k in range(cfg.order)]
+
+
+def kron_omegas(cfg: Config, n: int, cur_dims: Sequence[int], widths: Optional[Sequence[int]] = None) -> list:
+    """Kronecker sketch matrices Omega_k^{(n)} in R^{d_k x L_k} for k != n (None at k == n).
+
+    ``cur_dims`` are the current mode sizes of the tensor being sketched (for
+    STHOSVD, already-truncated modes have d_k = R_k).  C order (element (i,l) at i*L+l).
+    """
+    widths = kron_widths(cfg, n) if widths is None else widths
+    out = []
+    for k in range(cfg.order):
+        if k == n:
+            out.append(None)
+            continue
+        om = rng_for(cfg.cfg_id, _OBJ_KRON, n, k).standard_normal((cur_dims[k], widths[k]))
+        out.append(np.ascontiguousarray(om.astype(cfg.np_dtype)))
+    return out
+
+
+def sthosvd_dims_before(cfg: Config, n: int, order: Optional[Sequence[int]] = None) -> list:
+    """Mode sizes of the working tensor S when STHOSVD reaches mode n (Alg.8)."""
+    order = list(range(cfg.order)) if order is None else list(order)
+    d = list(cfg.dims)
+    for m in order:
+        if m == n:
+            break
+        d[m] = cfg.ranks[m]
+    return d
+
+
+def to_device_layout(x: np.ndarray):
+    """Numpy (I_1..I_N) Fortran array -> C-contiguous view of shape (I_N..I_1) (same bytes)."""
+    return np.ascontiguousarray(x.T)
+
+
+def compression_inverse(dims: Sequence[int], ranks: Sequence[int]) -> float:
+    """1/compression ratio S2/S1, S1 = prod I_n, S2 = prod R_n + sum I_n R_n."""
+    s1 = float(np.prod([float(d) for d in dims]))
+    s2 = float(np.prod([float(r) for r in ranks])) + float(sum(i * r for i, r in zip(dims, ranks)))
+    return s2 / s1
+
+
+# ---------------------------------------------------------------------------
+# Device-side assembly (torch) for configurations too large for host fp64
+# assembly (cfg5: 2048^3, 32 GiB fp32).  Same recipe; the random streams are
+# torch's Philox (seeded per slab from the same key tuple), so the bytes differ
+# from the numpy path -- such inputs are checked with sampled outputs and
+# size-independent properties.
+# ---------------------------------------------------------------------------
+
+def _torch_seed(*key: int) -> int:
+    return int(np.random.SeedSequence([BASE_SEED, *key]).generate_state(1, dtype=np.uint64)[0] & ((1 << 63) - 1))
+
+
+def make_tensor_device(cfg: Config, device, slab_modes: int = 64, last_range: Optional[tuple] = None):
+    """Assemble X on ``device`` (torch tensor of shape (I_N..I_1), cfg dtype).
+
+    Core and factors come from the numpy streams (small); the expansion runs in
+    fp64 slab by slab along the last mode; noise is torch Philox per slab with a
+    two-pass realized-norm scaling (reading R11).  ``last_range=(lo, hi)`` builds
+    only that slab of the last mode (multi-GPU: each rank builds its own slab).
+    Returns (X, info) with info = dict(core, factors, gamma).
+    """
+    import torch
+    core = make_core(cfg)
+    factors = make_factors(cfg)
+    N = cfg.order
+    I_last = cfg.dims[-1]
+    lo, hi = (0, I_last) if last_range is None else last_range
+    tdt = torch.float64 if cfg.dtype == "f64" else torch.float32
+    dev = torch.device(device)
+    g = torch.from_numpy(np.ascontiguousarray(core.T)).to(dev)          # shape (R_N..R_1)
+    us = [torch.from_numpy(u).to(dev) for u in factors]
+    # partial expansion over modes 0..N-2: W shape (R_N, I_{N-1}..I_1)
+    w = g
+    for n in range(N - 1):
+        ax = N - 1 - n                                              # torch axis of math mode n
+        w = torch.movedim(torch.tensordot(w, us[n], dims=([ax], [1])), -1, ax)
+    lead = int(np.prod(cfg.dims[:-1]))
+    w2 = w.reshape(w.shape[0], lead)                                # (R_N, J)
+    x = torch.empty((hi - lo,) + tuple(reversed(cfg.dims[:-1])), dtype=tdt, device=dev)
+    xf = x.view(hi - lo, lead)
+    gamma = 0.0
+    if cfg.noise == "rel":
+        # ||X_s||_F = ||G||_F exactly for orthonormal factors; realized ||N|| needs pass 1
+        nn2 = 0.0
+        for s0 in range(0, I_last, slab_modes):
+            s1 = min(I_last, s0 + slab_modes)
+            gen = torch.Generator(device=dev).manual_seed(_torch_seed(cfg.cfg_id, _OBJ_NOISE, s0))
+            nz = torch.randn((s1 - s0, lead), generator=gen, device=dev, dtype=torch.float64)
+            nn2 += float((nz * nz).sum())
+        gamma = cfg.noise_level * float(np.linalg.norm(core.ravel())) / math.sqrt(nn2)
+    elif cfg.noise == "abs":
+        gamma = cfg.noise_level
+    u_last = us[-1]
+    for s0 in range(0, I_last, slab_modes):
+        s1 = min(I_last, s0 + slab_modes)
+        a, b = max(s0, lo), min(s1, hi)
+        if a >= b:
+            continue
+        blk = u_last[a:b] @ w2                                          # (b-a, J) fp64
+        if cfg.noise != "none":
+            gen = torch.Generator(device=dev).manual_seed(_torch_seed(cfg.cfg_id, _OBJ_NOISE, s0))
+            nz = torch.randn((s1 - s0, lead), generator=gen, device=dev, dtype=torch.float64)
+            blk += gamma * nz[a - s0:b - s0]
+        xf[a - lo:b - lo] = blk.to(tdt)
+    return x, dict(core=core, factors=factors, gamma=gamma)
+
+
+def gaussian_omega_device(cfg: Config, n: int, device, K: Optional[int] = None,
+                          row0: int = 0, rows: Optional[int] = None, chunk_rows: int = 1 << 20):
+    """Gaussian Omega_n generated on device (torch Philox, seeded per 2^20-row chunk).
+
+    Row-major (J_n x K_n).  Row blocks are drawn chunk-wise so that any contiguous
+    row range (a slab's local rows) matches the full matrix bit-exactly.
+    """
+    import torch
+    K = cfg.K(n) if K is None else K
+    J = cfg.J(n)
+    rows = J - row0 if rows is None else rows
+    tdt = torch.float64 if cfg.dtype == "f64" else torch.float32
+    dev = torch.device(device)
+    out = torch.empty((rows, K), dtype=tdt, device=dev)
+    c0 = (row0 // chunk_rows) * chunk_rows
+    for c in range(c0, row0 + rows, chunk_rows):
+        gen = torch.Generator(device=dev).manual_seed(_torch_seed(cfg.cfg_id, _OBJ_OMEGA, n, c))
+        blk = torch.randn((min(chunk_rows, J - c), K), generator=gen, device=dev, dtype=torch.float64)
+        a, b = max(c, row0), min(c + blk.shape[0], row0 + rows)
+        out[a - row0:b - row0] = blk[a - c:b - c].to(tdt)
+    return out
