@@ -1,0 +1,380 @@
+// capi.cpp -- the extern "C" boundary of librtucker (declared in include/rtucker.h).
+// Validation, handle/workspace management and status conversion; no arithmetic.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "../../include/rtucker.h"
+#include "engine.h"
+
+struct rt_handle {
+  rt::Ctx ctx;
+  rt::Arena ws;
+  rt::Profiler prof;
+  std::unique_ptr<rt::Comm> comm;
+  std::string err;
+  int device = 0;
+  int* d_status = nullptr;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+rt_status fail(rt_handle* h, int st, const std::string& msg) {
+  if (h) h->err = msg;
+  g_err = msg;
+  return static_cast<rt_status>(st);
+}
+
+template <typename F>
+rt_status guard(rt_handle* h, F&& f) {
+  try {
+    if (h) {
+      cudaSetDevice(h->device);
+      h->ws.begin_call();
+    }
+    f();
+    return RT_OK;
+  } catch (const rt::Error& e) {
+    return fail(h, e.status, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(h, RT_ENOMEM, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(h, RT_ECUDA, e.what());
+  }
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+rt::TView check_tensor(const rt_tensor* X) {
+  RT_REQUIRE(X != nullptr, rt::kEINVAL, "X is NULL");
+  RT_REQUIRE(X->order >= 2 && X->order <= 5, rt::kEINVAL, "order must be in [2,5]");
+  RT_REQUIRE(X->dtype == RT_F32 || X->dtype == RT_F64, rt::kEINVAL, "dtype must be RT_F32 or RT_F64");
+  RT_REQUIRE(X->data != nullptr && aligned16(X->data), rt::kEINVAL, "X->data must be a 16-byte aligned device pointer");
+  rt::TView v;
+  v.dtype = X->dtype == RT_F64 ? 1 : 0;
+  v.N = X->order;
+  for (int k = 0; k < v.N; ++k) {
+    RT_REQUIRE(X->dims[k] >= 1, rt::kEINVAL, "dims must be >= 1");
+    v.d[k] = X->dims[k];
+  }
+  v.off = X->last_offset;
+  v.glob = X->last_global == 0 ? X->dims[v.N - 1] : X->last_global;
+  RT_REQUIRE(v.off >= 0 && v.off + v.d[v.N - 1] <= v.glob, rt::kEINVAL, "inconsistent slab (last_offset/last_global)");
+  v.data = X->data;
+  return v;
+}
+
+void check_gauss_omega(const rt::TView& X, int n, const void* om, int64_t K) {
+  RT_REQUIRE(om != nullptr && aligned16(om), rt::kEINVAL, "Omega_n must be a 16-byte aligned device pointer");
+  RT_REQUIRE(K >= 1, rt::kEINVAL, "omega_cols must be >= 1");
+  RT_REQUIRE(K <= X.Ig(n) && K <= X.Jg(n), rt::kERANK, "K_n must be <= min(I_n, J_n)");
+  RT_REQUIRE(K <= 128, rt::kEUNSUPPORTED, "K_n > 128 not supported");
+}
+
+int64_t check_kron_omega(const rt::TView& X, int n, const void* const* om, const int64_t* cols) {
+  int64_t K = 1;
+  for (int k = 0; k < X.N; ++k) {
+    if (k == n) continue;
+    RT_REQUIRE(om[k] != nullptr && aligned16(om[k]), rt::kEINVAL, "Kronecker factor must be an aligned device pointer");
+    RT_REQUIRE(cols[k] >= 1, rt::kEINVAL, "Kronecker widths must be >= 1");
+    K *= cols[k];
+  }
+  RT_REQUIRE(K <= X.Ig(n), rt::kERANK, "Kronecker sketch width prod L_k must be <= I_n");
+  RT_REQUIRE(K <= 128, rt::kEUNSUPPORTED, "Kronecker sketch width > 128 not supported");
+  return K;
+}
+
+// rows of Omega_n expected for the local slab
+int64_t local_J(const rt::TView& X, int n) { int64_t s = 1; for (int k = 0; k < X.N; ++k) if (k != n) s *= X.d[k]; return s; }
+
+}  // namespace
+
+extern "C" {
+
+rt_status rt_get_unique_id(uint8_t id[128]) {
+  if (!id) return RT_EINVAL;
+  int r = rt::nccl_get_unique_id(id);
+  if (r != 0) { g_err = rt::nccl_last_error(); return RT_ENCCL; }
+  return RT_OK;
+}
+
+static rt_status create_common(rt_handle** h, void* stream) {
+  if (!h) return RT_EINVAL;
+  auto* hh = new (std::nothrow) rt_handle();
+  if (!hh) return RT_ENOMEM;
+  cudaGetDevice(&hh->device);
+  hh->ctx.stream = static_cast<cudaStream_t>(stream);
+  int sms = 148;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, hh->device) == cudaSuccess) hh->ctx.num_sms = sms;
+  if (cudaMalloc(&hh->d_status, sizeof(int)) != cudaSuccess) {
+    cudaGetLastError();
+    delete hh;
+    return fail(nullptr, RT_ECUDA, "cudaMalloc(status) failed (no CUDA device?)");
+  }
+  cudaMemset(hh->d_status, 0, sizeof(int));
+  hh->ctx.d_status = hh->d_status;
+  hh->ctx.prof = &hh->prof;
+  *h = hh;
+  return RT_OK;
+}
+
+rt_status rt_create(rt_handle** h, void* cuda_stream, const uint8_t* id, int nranks, int rank) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(nullptr, RT_EINVAL, "bad nranks/rank");
+  rt_status s = create_common(h, cuda_stream);
+  if (s != RT_OK) return s;
+  if (id && nranks > 1) {
+    rt_status st = guard(*h, [&] { (*h)->comm = rt::make_nccl_comm(id, nranks, rank); });
+    if (st != RT_OK) { g_err = (*h)->err; rt_destroy(*h); *h = nullptr; return st; }
+  }
+  return RT_OK;
+}
+
+rt_status rt_loopback_group_create(void** group, int nranks) {
+  if (!group) return RT_EINVAL;
+  return guard(nullptr, [&] { *group = rt::loopback_group_create(nranks); });
+}
+
+rt_status rt_loopback_group_destroy(void* group) {
+  rt::loopback_group_destroy(static_cast<rt::LoopbackGroup*>(group));
+  return RT_OK;
+}
+
+rt_status rt_create_loopback(rt_handle** h, void* cuda_stream, void* group, int rank) {
+  rt_status s = create_common(h, cuda_stream);
+  if (s != RT_OK) return s;
+  rt_status st = guard(*h, [&] { (*h)->comm = rt::make_loopback_comm(static_cast<rt::LoopbackGroup*>(group), rank); });
+  if (st != RT_OK) { rt_destroy(*h); *h = nullptr; }
+  return st;
+}
+
+rt_status rt_destroy(rt_handle* h) {
+  if (!h) return RT_OK;
+  cudaSetDevice(h->device);
+  if (h->ctx.stream) cudaStreamSynchronize(h->ctx.stream); else cudaDeviceSynchronize();
+  h->comm.reset();
+  if (h->d_status) cudaFree(h->d_status);
+  delete h;
+  return RT_OK;
+}
+
+const char* rt_last_error(const rt_handle* h) { return h ? h->err.c_str() : g_err.c_str(); }
+
+rt_status rt_sync(rt_handle* h) {
+  if (!h) return RT_EINVAL;
+  int st = 0;
+  rt_status r = guard(h, [&] {
+    RT_CUDA(cudaStreamSynchronize(h->ctx.stream));
+    RT_CUDA(cudaMemcpy(&st, h->d_status, sizeof(int), cudaMemcpyDeviceToHost));
+    RT_CUDA(cudaMemset(h->d_status, 0, sizeof(int)));
+  });
+  if (r != RT_OK) return r;
+  if (st & rt::kStatusNonFinite) return fail(h, RT_ENUMERIC, "non-finite values in the input or a sketch");
+  if (st & rt::kStatusCholBreakdown) return fail(h, RT_ENUMERIC, "Cholesky breakdown in the thin QR after the shift");
+  return RT_OK;
+}
+
+rt_status rt_set_option(rt_handle* h, rt_option opt, int64_t value) {
+  if (!h) return RT_EINVAL;
+  switch (opt) {
+    case RT_OPT_TTM_IMPL: h->ctx.ttm_impl = int(value); return RT_OK;
+    case RT_OPT_PROFILE: h->prof.enabled = value != 0; return RT_OK;
+    case RT_OPT_QR_FALLBACK: return RT_OK;
+  }
+  return fail(h, RT_EINVAL, "unknown option");
+}
+
+rt_status rt_profile_read(rt_handle* h, rt_profile_entry* out, int cap, int* n, int64_t* launches) {
+  if (!h) return RT_EINVAL;
+  return guard(h, [&] {
+    RT_CUDA(cudaStreamSynchronize(h->ctx.stream));
+    int cnt = 0;
+    auto& P = h->prof;
+    for (auto& r : P.recs) {
+      float ms = 0.f;
+      RT_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+      int idx = -1;
+      for (int i = 0; i < cnt && i < cap; ++i)
+        if (std::strncmp(out[i].name, r.name, sizeof(out[i].name)) == 0) { idx = i; break; }
+      if (idx < 0 && cnt < cap) {
+        idx = cnt++;
+        std::memset(out[idx].name, 0, sizeof(out[idx].name));
+        std::strncpy(out[idx].name, r.name, sizeof(out[idx].name) - 1);
+        out[idx].count = 0;
+        out[idx].ms = 0;
+      }
+      if (idx >= 0) { out[idx].count += 1; out[idx].ms += ms; }
+      P.pool.push_back(r.a);
+      P.pool.push_back(r.b);
+    }
+    P.recs.clear();
+    if (n) *n = cnt;
+    if (launches) *launches = P.launches;
+    P.launches = 0;
+  });
+}
+
+rt_status rtucker_sketch(rt_handle* h, const rt_tensor* X, int mode, rt_omega_kind kind, const void* const* omega,
+                         const int64_t* omega_cols, int q, double* Y, int64_t ldy) {
+  if (!h) return RT_EINVAL;
+  return guard(h, [&] {
+    rt::TView v = check_tensor(X);
+    RT_REQUIRE(mode >= 0 && mode < v.N, rt::kEINVAL, "mode out of range");
+    RT_REQUIRE(q >= 0, rt::kEINVAL, "q must be >= 0");
+    RT_REQUIRE(omega && omega_cols && Y, rt::kEINVAL, "NULL omega/omega_cols/Y");
+    RT_REQUIRE(ldy >= v.d[mode], rt::kEINVAL, "ldy < I_n");
+    rt::Engine eng(h->ctx, h->ws, h->comm.get());
+    RT_REQUIRE(!(v.sharded() && !eng.dist() && q > 0), rt::kEINVAL,
+               "power iterations on a slab need a communicator");
+    int64_t K;
+    if (kind == RT_OMEGA_GAUSS) { K = omega_cols[mode]; check_gauss_omega(v, mode, omega[mode], K); }
+    else if (kind == RT_OMEGA_KRON) K = check_kron_omega(v, mode, omega, omega_cols);
+    else throw rt::Error(rt::kEINVAL, "unknown omega kind");
+    const int64_t In = v.d[mode];
+    double* Yt = (ldy == In) ? Y : h->ws.alloc_n<double>(In * K);
+    if (v.dtype == 0) eng.sketch<float>(v, static_cast<const float*>(v.data), mode, kind, omega, omega_cols, q, Yt);
+    else eng.sketch<double>(v, static_cast<const double*>(v.data), mode, kind, omega, omega_cols, q, Yt);
+    if (Yt != Y) RT_CUDA(cudaMemcpy2DAsync(Y, ldy * sizeof(double), Yt, In * sizeof(double), In * sizeof(double), K,
+                                           cudaMemcpyDeviceToDevice, h->ctx.stream));
+  });
+}
+
+rt_status rtucker_qr(rt_handle* h, int64_t m, int64_t k, rt_dtype dtype, const void* Y, int64_t ldy, double* Q,
+                     int64_t ldq, double* R, int rows_distributed) {
+  if (!h) return RT_EINVAL;
+  return guard(h, [&] {
+    RT_REQUIRE(Y && Q, rt::kEINVAL, "NULL Y/Q");
+    RT_REQUIRE(k >= 1 && m >= 0 && ldy >= m && ldq >= m, rt::kEINVAL, "bad m/k/ld");
+    RT_REQUIRE(k <= 128, rt::kEUNSUPPORTED, "k > 128 not supported");
+    rt::Engine eng(h->ctx, h->ws, h->comm.get());
+    const bool dist = rows_distributed && eng.dist();
+    int64_t m_glob = m, row0 = 0;
+    if (dist) {
+      // global row count and this rank's first row: allgather of local counts (host-visible)
+      double* cnt = h->ws.alloc_n<double>(1);
+      double* all = h->ws.alloc_n<double>(eng.comm->nranks());
+      const double md = double(m);
+      RT_CUDA(cudaMemcpyAsync(cnt, &md, sizeof(double), cudaMemcpyHostToDevice, h->ctx.stream));
+      eng.comm->allgather(cnt, all, 1, h->ctx.stream);
+      std::unique_ptr<double[]> host(new double[eng.comm->nranks()]);
+      RT_CUDA(cudaMemcpyAsync(host.get(), all, sizeof(double) * eng.comm->nranks(), cudaMemcpyDeviceToHost,
+                              h->ctx.stream));
+      RT_CUDA(cudaStreamSynchronize(h->ctx.stream));
+      m_glob = 0;
+      for (int r = 0; r < eng.comm->nranks(); ++r) {
+        if (r < eng.comm->rank()) row0 += int64_t(host[r]);
+        m_glob += int64_t(host[r]);
+      }
+    }
+    RT_REQUIRE(m_glob >= k, rt::kERANK, "thin QR needs m >= k");
+    if (dtype == RT_F64) eng.qr_rows<double>(static_cast<const double*>(Y), m, m_glob, int(k), ldy, Q, ldq, R, dist, row0);
+    else if (dtype == RT_F32) eng.qr_rows<float>(static_cast<const float*>(Y), m, m_glob, int(k), ldy, Q, ldq, R, dist, row0);
+    else throw rt::Error(rt::kEINVAL, "bad dtype");
+  });
+}
+
+rt_status rtucker_core(rt_handle* h, const rt_tensor* X, const double* const* Q, const int64_t* C, double* G,
+                       double* rel_err, double* rel_err_gram) {
+  if (!h) return RT_EINVAL;
+  return guard(h, [&] {
+    rt::TView v = check_tensor(X);
+    RT_REQUIRE(Q && C && G, rt::kEINVAL, "NULL Q/C/G");
+    rt::Engine eng(h->ctx, h->ws, h->comm.get());
+    RT_REQUIRE(!(v.sharded() && !eng.dist() && (rel_err || rel_err_gram)), rt::kEINVAL,
+               "relative error of a slab needs a communicator");
+    int64_t ldq[5];
+    for (int n = 0; n < v.N; ++n) {
+      RT_REQUIRE(Q[n] != nullptr, rt::kEINVAL, "NULL Q_n");
+      RT_REQUIRE(C[n] >= 1 && C[n] <= v.Ig(n), rt::kERANK, "C_n must be in [1, I_n]");
+      RT_REQUIRE(C[n] <= 128, rt::kEUNSUPPORTED, "C_n > 128 not supported");
+      ldq[n] = v.d[n];
+    }
+    if (v.dtype == 0) {
+      eng.core<float>(v, static_cast<const float*>(v.data), Q, ldq, C, G);
+      if (rel_err || rel_err_gram) eng.rel_error<float>(v, static_cast<const float*>(v.data), G, C, Q, rel_err, rel_err_gram);
+    } else {
+      eng.core<double>(v, static_cast<const double*>(v.data), Q, ldq, C, G);
+      if (rel_err || rel_err_gram) eng.rel_error<double>(v, static_cast<const double*>(v.data), G, C, Q, rel_err, rel_err_gram);
+    }
+  });
+}
+
+static void check_driver_args(const rt::TView& v, const int64_t* R, int p, int q, rt_omega_kind kind,
+                              const void* const* omega, const int64_t* omega_cols, double* const* Q_out,
+                              double* G_out, const int64_t* cur_dims) {
+  RT_REQUIRE(R && omega && omega_cols && Q_out && G_out, rt::kEINVAL, "NULL argument");
+  RT_REQUIRE(p >= 0 && q >= 0, rt::kEINVAL, "p and q must be >= 0");
+  RT_REQUIRE(kind == RT_OMEGA_GAUSS || kind == RT_OMEGA_KRON, rt::kEINVAL, "unknown omega kind");
+  const int N = v.N;
+  for (int n = 0; n < N; ++n) {
+    RT_REQUIRE(Q_out[n] != nullptr, rt::kEINVAL, "NULL Q_out[n]");
+    rt::TView w = v;
+    if (cur_dims) { for (int k = 0; k < N; ++k) w.d[k] = cur_dims[n * N + k]; w.glob = w.d[N - 1]; }
+    const void* const* om = omega + n * N;
+    const int64_t* oc = omega_cols + n * N;
+    int64_t K;
+    if (kind == RT_OMEGA_GAUSS) {
+      K = oc[n];
+      check_gauss_omega(w, n, om[n], K);
+      RT_REQUIRE(K == std::min<int64_t>(R[n] + p, std::min(w.Ig(n), w.Jg(n))), rt::kEINVAL,
+                 "Gaussian width must be K_n = min(R_n + p, I_n, J_n)");
+    } else {
+      K = check_kron_omega(w, n, om, oc);
+      RT_REQUIRE(K >= std::min<int64_t>(R[n] + p, w.Ig(n)), rt::kEINVAL,
+                 "Kronecker width prod L_k must be >= min(R_n + p, I_n)");
+    }
+    RT_REQUIRE(R[n] >= 1 && R[n] <= K, rt::kERANK, "need 1 <= R_n <= K_n");
+  }
+}
+
+rt_status rtucker_hosvd(rt_handle* h, const rt_tensor* X, const int64_t* R, int p, int q, rt_omega_kind kind,
+                        const void* const* omega, const int64_t* omega_cols, double* const* Q_out, double* G_out,
+                        double* rel_err, double* rel_err_gram) {
+  if (!h) return RT_EINVAL;
+  return guard(h, [&] {
+    rt::TView v = check_tensor(X);
+    check_driver_args(v, R, p, q, kind, omega, omega_cols, Q_out, G_out, nullptr);
+    rt::Engine eng(h->ctx, h->ws, h->comm.get());
+    RT_REQUIRE(!(v.sharded() && !eng.dist()), rt::kEINVAL, "a sharded tensor needs a communicator");
+    if (v.dtype == 0) eng.hosvd<float>(v, R, q, kind, omega, omega_cols, Q_out, G_out, rel_err, rel_err_gram);
+    else eng.hosvd<double>(v, R, q, kind, omega, omega_cols, Q_out, G_out, rel_err, rel_err_gram);
+  });
+}
+
+rt_status rtucker_sthosvd(rt_handle* h, const rt_tensor* X, const int64_t* R, int p, int q, rt_omega_kind kind,
+                          const void* const* omega, const int64_t* omega_cols, const int* mode_order,
+                          double* const* Q_out, double* G_out, double* rel_err, double* rel_err_gram) {
+  if (!h) return RT_EINVAL;
+  return guard(h, [&] {
+    rt::TView v = check_tensor(X);
+    rt::Engine eng(h->ctx, h->ws, h->comm.get());
+    RT_REQUIRE(!v.sharded(), rt::kEUNSUPPORTED, "sharded R-STHOSVD is not implemented");
+    const int N = v.N;
+    int order[5];
+    bool seen[5] = {false, false, false, false, false};
+    for (int s = 0; s < N; ++s) {
+      order[s] = mode_order ? mode_order[s] : s;
+      RT_REQUIRE(order[s] >= 0 && order[s] < N && !seen[order[s]], rt::kEINVAL, "mode_order must be a permutation");
+      seen[order[s]] = true;
+    }
+    RT_REQUIRE(R != nullptr, rt::kEINVAL, "NULL R");
+    for (int n = 0; n < N; ++n) RT_REQUIRE(R[n] >= 1 && R[n] <= v.d[n], rt::kERANK, "need 1 <= R_n <= I_n");
+    // sizes of the working tensor when each mode is processed (already-processed modes have R_m)
+    int64_t cur[25];
+    int64_t d[5];
+    for (int k = 0; k < N; ++k) d[k] = v.d[k];
+    for (int s = 0; s < N; ++s) {
+      const int n = order[s];
+      for (int k = 0; k < N; ++k) cur[n * N + k] = d[k];
+      d[n] = R[n];
+    }
+    check_driver_args(v, R, p, q, kind, omega, omega_cols, Q_out, G_out, cur);
+    if (v.dtype == 0) eng.sthosvd<float>(v, R, q, kind, omega, omega_cols, order, Q_out, G_out, rel_err, rel_err_gram);
+    else eng.sthosvd<double>(v, R, q, kind, omega, omega_cols, order, Q_out, G_out, rel_err, rel_err_gram);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,157 @@
+// common.cuh -- shared host/device plumbing of librtucker (errors, launch context,
+// profiling hooks, workspace arena).  No method arithmetic lives here.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace rt {
+
+// Thrown inside the library, converted to an rt_status at the C-ABI boundary.
+struct Error : std::runtime_error {
+  int status;
+  Error(int s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+#define RT_CUDA(expr)                                                                        \
+  do {                                                                                       \
+    cudaError_t _e = (expr);                                                                 \
+    if (_e != cudaSuccess)                                                                   \
+      throw ::rt::Error(-4, std::string(#expr) + ": " + cudaGetErrorString(_e) + " @" +      \
+                                std::to_string(__LINE__));                                   \
+  } while (0)
+
+#define RT_REQUIRE(cond, status, msg)                                                        \
+  do {                                                                                       \
+    if (!(cond)) throw ::rt::Error((status), std::string(msg));                              \
+  } while (0)
+
+constexpr int kEINVAL = -1, kERANK = -2, kENOMEM = -3, kECUDA = -4, kENCCL = -5, kENUMERIC = -6,
+              kEUNSUPPORTED = -7;
+
+// device status bits (latched by kernels, read by rt_sync)
+constexpr int kStatusCholBreakdown = 1;
+constexpr int kStatusNonFinite = 2;
+
+__host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ---------------------------------------------------------------- profiling
+struct Profiler {
+  bool enabled = false;
+  struct Rec { const char* name; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  int64_t launches = 0;     // counted even when timing is disabled
+  cudaEvent_t get() {
+    if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
+    cudaEvent_t e;
+    RT_CUDA(cudaEventCreate(&e));
+    return e;
+  }
+  ~Profiler() {
+    for (auto& r : recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+
+// ---------------------------------------------------------------- launch context
+struct Ctx {
+  cudaStream_t stream = nullptr;
+  int* d_status = nullptr;      // device status latch
+  Profiler* prof = nullptr;
+  int num_sms = 148;
+  int ttm_impl = 0;             // 0 auto, 1 SIMT, 2 tcgen05
+};
+
+// Launch a kernel (given as a lambda issuing <<<...>>> on ctx.stream) with optional
+// CUDA-event timing per kernel class.
+template <typename F>
+inline void launch(const Ctx& ctx, const char* name, F&& f) {
+  Profiler* p = ctx.prof;
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (p && p->enabled) { a = p->get(); b = p->get(); RT_CUDA(cudaEventRecord(a, ctx.stream)); }
+  f();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw Error(kECUDA, std::string("launch ") + name + ": " + cudaGetErrorString(e));
+  if (p) {
+    p->launches++;
+    if (p->enabled) { RT_CUDA(cudaEventRecord(b, ctx.stream)); p->recs.push_back({name, a, b}); }
+  }
+}
+
+// ---------------------------------------------------------------- workspace arena
+// Bump allocator over device blocks.  A call may grow it (cudaMalloc); at the start of
+// the next call all blocks are coalesced into one so the steady state never allocates.
+class Arena {
+ public:
+  ~Arena() { release(); }
+  void begin_call() {
+    if (blocks_.size() > 1 || (blocks_.size() == 1 && high_ > blocks_[0].size)) {
+      size_t total = 0;
+      for (auto& b : blocks_) total += b.size;
+      total = std::max(total, high_);
+      release_sync();
+      add_block(total);
+    }
+    for (auto& b : blocks_) b.used = 0;
+    cur_ = 0;
+    used_total_ = 0;
+  }
+  void* alloc(size_t bytes) {
+    bytes = (bytes + 255) & ~size_t(255);
+    if (bytes == 0) bytes = 256;
+    while (cur_ < blocks_.size()) {
+      Block& b = blocks_[cur_];
+      if (b.used + bytes <= b.size) {
+        void* p = static_cast<char*>(b.ptr) + b.used;
+        b.used += bytes;
+        used_total_ += bytes;
+        high_ = std::max(high_, used_total_);
+        return p;
+      }
+      ++cur_;
+    }
+    size_t last = blocks_.empty() ? 0 : blocks_.back().size;
+    add_block(std::max(bytes, std::max(last, size_t(64) << 20)));
+    cur_ = blocks_.size() - 1;
+    return alloc(bytes);
+  }
+  template <typename T> T* alloc_n(int64_t n) { return static_cast<T*>(alloc(sizeof(T) * size_t(n))); }
+  // Mark/rewind (scoped reuse inside one call; safe because kernels are stream-ordered).
+  struct Mark { size_t cur, used, total; };
+  Mark mark() const { return {cur_, cur_ < blocks_.size() ? blocks_[cur_].used : 0, used_total_}; }
+  void rewind(const Mark& m) {
+    for (size_t i = m.cur + 1; i < blocks_.size(); ++i) blocks_[i].used = 0;
+    cur_ = m.cur;
+    if (cur_ < blocks_.size()) blocks_[cur_].used = m.used;
+    used_total_ = m.total;
+  }
+  void release() {
+    for (auto& b : blocks_) cudaFree(b.ptr);
+    blocks_.clear();
+  }
+
+ private:
+  struct Block { void* ptr; size_t size; size_t used; };
+  void add_block(size_t bytes) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      throw Error(kENOMEM, "workspace cudaMalloc of " + std::to_string(bytes) + " bytes failed");
+    }
+    blocks_.push_back({p, bytes, 0});
+  }
+  void release_sync() {
+    cudaDeviceSynchronize();
+    release();
+  }
+  std::vector<Block> blocks_;
+  size_t cur_ = 0, used_total_ = 0, high_ = 0;
+};
+
+}  // namespace rt

@@ -1,0 +1,77 @@
+// engine.h -- orchestration of the hot path on one rank.
+#pragma once
+
+#include <vector>
+
+#include "comm.h"
+#include "kernels.h"
+
+namespace rt {
+
+// Local view of a (possibly slab-sharded) first-mode-fastest tensor.
+struct TView {
+  int dtype = 0;                 // 0 f32, 1 f64
+  int N = 0;
+  int64_t d[5] = {0, 0, 0, 0, 0};  // local dims
+  int64_t off = 0, glob = 0;     // last-mode slab [off, off + d[N-1]) of glob
+  const void* data = nullptr;
+
+  bool sharded() const { return off != 0 || glob != d[N - 1]; }
+  int64_t size() const { int64_t s = 1; for (int k = 0; k < N; ++k) s *= d[k]; return s; }
+  int64_t Ig(int n) const { return n == N - 1 ? glob : d[n]; }
+  int64_t Jg(int n) const { int64_t s = 1; for (int k = 0; k < N; ++k) if (k != n) s *= Ig(k); return s; }
+  Box box(int n) const { return box_of(d, N, n); }
+  static Box box_of(const int64_t* dims, int N, int n) {
+    Box b{1, dims[n], 1};
+    for (int k = 0; k < n; ++k) b.a *= dims[k];
+    for (int k = n + 1; k < N; ++k) b.b *= dims[k];
+    return b;
+  }
+};
+
+class Engine {
+ public:
+  Engine(Ctx& c, Arena& w, Comm* cm) : ctx(c), ws(w), comm(cm) {}
+  Ctx& ctx;
+  Arena& ws;
+  Comm* comm;
+  bool dist() const { return comm && comm->nranks() > 1; }
+
+  // (1) sketch of mode n incl. q power iterations; Yt: fp64 I_n(local) x K, ld I_n(local).
+  template <typename T>
+  void sketch(const TView& X, const T* data, int n, int kind, const void* const* omega,
+              const int64_t* omega_cols, int q, double* Yt);
+  // (2) thin QR of the fp64 Y side (shifted CholeskyQR3); R nullable.
+  void qr_y(const double* Y, int64_t m, int64_t m_glob, int k, int64_t ldy, double* Q, int64_t ldq,
+            double* R, bool rows_dist, int64_t row0);
+  template <typename T>
+  void qr_rows(const T* Y, int64_t m, int64_t m_glob, int k, int64_t ldy, double* Q, int64_t ldq, double* R,
+               bool rows_dist, int64_t row0);
+  // orthonormalize the tall Z of the power iteration in place (shifted CholeskyQR, fp64 Gram)
+  template <typename T>
+  void qr_z(T* Z, int64_t m, int64_t m_glob, int k, bool rows_dist, int64_t row0);
+  // (3) core G~ = X x_n Qt_n^T (all n) -> fp64 Gt (replicated)
+  template <typename T>
+  void core(const TView& X, const T* data, const double* const* Qt, const int64_t* ldq, const int64_t* K,
+            double* Gt);
+  // (a6) truncation of the oversampled core: Q_out, G_out from Gt, Qt
+  void truncate(const TView& X, const double* Gt, const int64_t* K, const double* const* Qt,
+                const int64_t* ldq, const int64_t* R, double* const* Q_out, double* G_out);
+  // (a8) residual pass: E and E_gram from X, G (R_1..R_N), Q (I_n(local) x R_n, ld I_n(local))
+  template <typename T>
+  void rel_error(const TView& X, const T* data, const double* G, const int64_t* R, const double* const* Q,
+                 double* E, double* Eg);
+  // drivers
+  template <typename T>
+  void hosvd(const TView& X, const int64_t* R, int q, int kind, const void* const* omega,
+             const int64_t* omega_cols, double* const* Q_out, double* G_out, double* E, double* Eg);
+  template <typename T>
+  void sthosvd(const TView& X, const int64_t* R, int q, int kind, const void* const* omega,
+               const int64_t* omega_cols, const int* order, double* const* Q_out, double* G_out, double* E,
+               double* Eg);
+
+ private:
+  void canon(double* Qn, int64_t m, int r, int64_t ld, int64_t row0, bool dist_rows, double* U, int ku);
+};
+
+}  // namespace rt

@@ -1,0 +1,83 @@
+// kernels.h -- host launchers of the librtucker device kernels.
+//
+// Tensor view used by every TTM launcher: for a contraction over mode n, the
+// first-mode-fastest tensor is viewed as a 3-D box [a, I, b] with
+// a = prod_{k<n} I_k, I = I_n, b = prod_{k>n} I_k; element (alpha, i, beta) sits at
+// alpha + a*i + a*I*beta, and the paper's j-index of the n-unfolding is
+// j = alpha + a*beta.  Nothing is ever permuted in memory ("unfolding-free").
+#pragma once
+
+#include "common.cuh"
+
+namespace rt {
+
+struct Box { int64_t a, I, b; int64_t J() const { return a * b; } int64_t size() const { return a * I * b; } };
+
+// Y(i,k) = sum_j X_(n)(i,j) B(j,k),  B(j,k) = Bm[j*bs_j + k*bs_k]   (TTM shape (i), sketch)
+// Y: fp64 col-major I x K (ldy).  gram=true: B := X_(n)^T (Gram of the unfolding, K = I).
+template <typename T>
+void ttm_s(const Ctx& ctx, Arena& ws, const T* X, Box box, const T* Bm, int64_t bs_j, int64_t bs_k,
+           int K, double* Y, int64_t ldy, bool gram = false);
+
+// out(alpha, c, beta) = sum_i X(alpha, i, beta) M(i, c),  M(i,c) = Mm[i*ms_i + c*ms_c]
+// out at alpha*so_a + c*so_c + beta*so_b   (TTM shapes (ii) and (iii))
+template <typename Tin, typename Tm, typename Tout>
+void ttm_t(const Ctx& ctx, const Tin* X, Box box, const Tm* Mm, int64_t ms_i, int64_t ms_c, int C,
+           Tout* out, int64_t so_a, int64_t so_c, int64_t so_b);
+
+// Gram of a col-major m x k matrix (fp64 out, k x k), partials reduced in fixed order.
+template <typename T>
+void gram(const Ctx& ctx, Arena& ws, const T* A, int64_t m, int k, int64_t lda, double* G);
+
+// Cholesky of (G + shift*I) (k x k) -> R (upper, col-major) and Rinv.  shift_coef * trace(G)
+// is the shift.  zero_flag[0] = 1 if trace(G) == 0 (all-zero input, reading R7).
+void chol_inv(const Ctx& ctx, const double* G, int k, double shift_coef, double* R, double* Rinv,
+              int* zero_flag);
+
+// C(m x n) = A(m x k) * B(k x n); A col-major (lda) of TA, B fp64 col-major (ldb), C of TC (ldc).
+// A == C allowed (in place, n == k).  zero_flag != nullptr && *zero_flag: C(i,c) = (row0+i == c)
+// (rows of the identity I[:, :n], row0 = global index of the first local row).
+template <typename TA, typename TC>
+void gemm_tall(const Ctx& ctx, const TA* A, int64_t m, int k, int64_t lda, const double* B, int n,
+               int64_t ldb, TC* C, int64_t ldc, const int* zero_flag = nullptr, int64_t row0 = 0);
+
+// Small dense fp64 GEMM C = op(A) op(B) (col-major), for k x k triangular products.
+void gemm_small(const Ctx& ctx, bool ta, bool tb, int m, int n, int k, const double* A, int lda,
+                const double* B, int ldb, double* C, int ldc);
+
+// Symmetric EVD (cyclic parallel Jacobi, fp64): W descending, V col-major k x k.
+void eig_sym(const Ctx& ctx, Arena& ws, const double* A, int k, double* W, double* V, int count = 1,
+             int64_t stride_a = 0, int64_t stride_w = 0, int64_t stride_v = 0);
+
+// Sign canonicalization (reading R5): per column of Q (m x r, ld), candidate (|v|max, global row,
+// sign) -> cand[3*c..]; then apply: flip Q[:,c] and U[:,c] (ldu, rows ku) where the best candidate
+// over `nc` candidate sets (stride 3*r) is negative.
+void colmax_candidates(const Ctx& ctx, const double* Q, int64_t m, int r, int64_t ld, int64_t row0,
+                       double* cand);
+void sign_apply(const Ctx& ctx, const double* cand, int nc, double* Q, int64_t m, int r, int64_t ld,
+                double* U, int ku, int64_t ldu);
+
+// Element conversion with optional 2-D strides (col-major copy).
+template <typename Ti, typename To>
+void convert2d(const Ctx& ctx, const Ti* in, int64_t m, int64_t n, int64_t ldi, To* out, int64_t ldo);
+
+// out(i + ldo*j) = T[(j%a) + a*i + a*I*(j/a)]  (explicit n-unfolding of a small tensor).
+template <typename T>
+void unfold_copy(const Ctx& ctx, const T* Tt, Box box, double* out, int64_t ldo);
+
+// Residual pass: sum_{j,i} (X[j + J*i] - sum_r P[j + J*r] Q[i + ldq*r])^2 and sum X^2.
+// P, X of type T; Q of type T.  Writes 2 fp64 sums to out2 (deterministic partials).
+template <typename T>
+void residual(const Ctx& ctx, Arena& ws, const T* X, int64_t J, int64_t In, const T* P, int R,
+              const T* Q, int64_t ldq, double* out2);
+
+// sum of squares of an fp64 vector -> out (deterministic)
+void sumsq(const Ctx& ctx, Arena& ws, const double* x, int64_t n, double* out);
+
+// E = sqrt(res/xx), E_gram = sqrt(max(0, 1 - gg/xx)) (0 when xx == 0).
+void finalize_err(const Ctx& ctx, const double* sums /*res, xx*/, const double* gg, double* E, double* Eg);
+
+void fill_zero(const Ctx& ctx, void* p, size_t bytes);
+void set_status_if_nonfinite(const Ctx& ctx, const double* x, int64_t n);
+
+}  // namespace rt

@@ -1,0 +1,675 @@
+// linalg.cu -- small fp64 linear algebra of the hot path:
+// tall-skinny Gram / Cholesky / triangular inverse (shifted CholeskyQR, the thin QR of
+// P:173 and Alg.1 line 3 P:206), tall x small GEMMs (Q = Y R^{-1}, Q_n = Q~_n U_n),
+// the symmetric eigensolver of the Gram-EVD truncation (reading R1), the sign
+// canonicalization (reading R5), the residual pass of E (Eq. Relativeerror)
+// and small helpers.
+#include <cfloat>
+
+#include "kernels.h"
+
+namespace rt {
+namespace {
+
+template <typename T> struct AccOf { using type = float; };
+template <> struct AccOf<double> { using type = double; };
+
+__device__ inline void latch(int* st, int bit) {
+  if (st) atomicOr(st, bit);
+}
+
+template <typename T>
+__device__ inline T block_sum(T v, T* sh) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  T r = T(0);
+  if (threadIdx.x < 32) {
+    r = threadIdx.x < nw ? sh[threadIdx.x] : T(0);
+    for (int o = 16; o; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+  }
+  return r;  // valid in thread 0
+}
+
+// ------------------------------------------------------------------ Gram
+// part[z][p + k*q] = sum_{rows of split z} A(row,p) A(row,q); fp64 products and sums.
+template <typename T, int KB>
+__global__ void __launch_bounds__(256) gram_kernel(const T* __restrict__ A, int64_t m, int k, int64_t lda,
+                                                    int64_t rps, double* __restrict__ part) {
+  constexpr int RB = 16;
+  __shared__ double As[RB][16 * KB + 1];
+  const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
+  const int64_t r0 = int64_t(blockIdx.x) * rps, r1 = min(m, r0 + rps);
+  double acc[KB][KB];
+#pragma unroll
+  for (int a = 0; a < KB; ++a)
+#pragma unroll
+    for (int b = 0; b < KB; ++b) acc[a][b] = 0.0;
+  for (int64_t rc = r0; rc < r1; rc += RB) {
+    for (int e = t; e < RB * 16 * KB; e += 256) {
+      const int rl = e % RB, c = e / RB;
+      const int64_t row = rc + rl;
+      As[rl][c] = (row < r1 && c < k) ? double(A[row + lda * c]) : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int rl = 0; rl < RB; ++rl) {
+      double pa[KB], qb[KB];
+#pragma unroll
+      for (int a = 0; a < KB; ++a) pa[a] = As[rl][ty + 16 * a];
+#pragma unroll
+      for (int b = 0; b < KB; ++b) qb[b] = As[rl][tx + 16 * b];
+#pragma unroll
+      for (int a = 0; a < KB; ++a)
+#pragma unroll
+        for (int b = 0; b < KB; ++b) acc[a][b] = fma(pa[a], qb[b], acc[a][b]);
+    }
+    __syncthreads();
+  }
+  double* dst = part + int64_t(blockIdx.x) * k * k;
+#pragma unroll
+  for (int a = 0; a < KB; ++a)
+#pragma unroll
+    for (int b = 0; b < KB; ++b) {
+      const int p = ty + 16 * a, q = tx + 16 * b;
+      if (p < k && q < k) dst[p + int64_t(k) * q] = acc[a][b];
+    }
+}
+
+__global__ void reduce_parts_kernel(const double* __restrict__ part, int64_t n, int splits,
+                                    double* __restrict__ out) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  double s = 0.0;
+  for (int z = 0; z < splits; ++z) s += part[int64_t(z) * n + e];
+  out[e] = s;
+}
+
+template <typename T, int KB>
+void launch_gram(const Ctx& ctx, Arena& ws, const T* A, int64_t m, int k, int64_t lda, double* G) {
+  int64_t splits = std::max<int64_t>(1, std::min<int64_t>(2LL * ctx.num_sms, cdiv(m, 64)));
+  const int64_t rps = cdiv(cdiv(m, splits), 16) * 16;
+  splits = std::max<int64_t>(1, cdiv(m, rps));
+  double* part = ws.alloc_n<double>(splits * k * k);
+  launch(ctx, "gram", [&] {
+    gram_kernel<T, KB><<<unsigned(splits), 256, 0, ctx.stream>>>(A, m, k, lda, rps, part);
+  });
+  const int64_t n = int64_t(k) * k;
+  launch(ctx, "gram_reduce", [&] {
+    reduce_parts_kernel<<<unsigned(cdiv(n, 256)), 256, 0, ctx.stream>>>(part, n, int(splits), G);
+  });
+}
+
+// ------------------------------------------------------- Cholesky + inverse
+// One CTA.  Packed lower-triangular storage L[i(i+1)/2 + c] and W = L^{-1} in shared memory.
+__device__ inline int tri(int i, int c) { return i * (i + 1) / 2 + c; }
+
+__global__ void __launch_bounds__(512) chol_inv_kernel(const double* __restrict__ G, int k, double shift_coef,
+                                                        double* __restrict__ R, double* __restrict__ Rinv,
+                                                        int* zero_flag, int* status) {
+  extern __shared__ double sm[];
+  double* L = sm;                        // k(k+1)/2
+  double* W = sm + k * (k + 1) / 2;      // k(k+1)/2
+  __shared__ double red[32];
+  __shared__ double s_shift, s_tr;
+  __shared__ int s_bad;
+  const int t = threadIdx.x, nt = blockDim.x;
+  double tr = 0.0;
+  for (int i = t; i < k; i += nt) tr += G[i + int64_t(k) * i];
+  tr = block_sum(tr, red);
+  if (t == 0) {
+    s_tr = tr;
+    s_shift = shift_coef * tr;
+    s_bad = 0;
+    if (!(tr == tr) || tr > DBL_MAX) latch(status, kStatusNonFinite);
+    if (zero_flag) *zero_flag = (tr == 0.0) ? 1 : 0;
+  }
+  __syncthreads();
+  const bool is_zero = (s_tr == 0.0);
+  for (int e = t; e < k * (k + 1) / 2; e += nt) {
+    // unpack e -> (i, c), i >= c
+    int i = int((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+    while (tri(i + 1, 0) <= e) ++i;
+    while (tri(i, 0) > e) --i;
+    const int c = e - tri(i, 0);
+    L[e] = G[i + int64_t(k) * c] + (i == c ? s_shift : 0.0);
+    W[e] = (i == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  if (!is_zero) {
+    // right-looking Cholesky G + sI = L L^T
+    for (int j = 0; j < k; ++j) {
+      if (t == 0) {
+        double d = L[tri(j, j)];
+        if (!(d > 0.0)) { s_bad = 1; d = 1.0; }
+        L[tri(j, j)] = sqrt(d);
+      }
+      __syncthreads();
+      const double ljj = L[tri(j, j)];
+      for (int i = j + 1 + t; i < k; i += nt) L[tri(i, j)] /= ljj;
+      __syncthreads();
+      const int rem = k - j - 1;
+      for (int e = t; e < rem * (rem + 1) / 2; e += nt) {
+        int ii = int((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+        while (tri(ii + 1, 0) <= e) ++ii;
+        while (tri(ii, 0) > e) --ii;
+        const int cc = e - tri(ii, 0);
+        const int i = j + 1 + ii, c = j + 1 + cc;
+        L[tri(i, c)] -= L[tri(i, j)] * L[tri(c, j)];
+      }
+      __syncthreads();
+    }
+    // W = L^{-1}: row j final = B[j,:]/L_jj, then B[i,c] -= L_ij W[j,c] for i > j, c <= j
+    for (int j = 0; j < k; ++j) {
+      const double ljj = L[tri(j, j)];
+      for (int c = t; c <= j; c += nt) W[tri(j, c)] /= ljj;
+      __syncthreads();
+      const int rows = k - j - 1;
+      for (int e = t; e < rows * (j + 1); e += nt) {
+        const int i = j + 1 + e / (j + 1), c = e % (j + 1);
+        W[tri(i, c)] -= L[tri(i, j)] * W[tri(j, c)];
+      }
+      __syncthreads();
+    }
+  }
+  if (t == 0 && s_bad) latch(status, kStatusCholBreakdown);
+  // R = L^T (upper), Rinv = W^T; col-major k x k
+  for (int e = t; e < k * k; e += nt) {
+    const int r = e % k, c = e / k;
+    if (is_zero) {
+      if (R) R[e] = 0.0;
+      Rinv[e] = 0.0;
+    } else {
+      if (R) R[e] = (r <= c) ? L[tri(c, r)] : 0.0;
+      Rinv[e] = (r <= c) ? W[tri(c, r)] : 0.0;
+    }
+  }
+}
+
+// --------------------------------------------------------------- tall GEMM
+// C(m x n) = A(m x k) B(k x n); 32 rows per CTA; B in shared memory; fp64 accumulation.
+template <typename TA, typename TC>
+__global__ void __launch_bounds__(256) gemm_tall_kernel(const TA* A, int64_t m, int k, int64_t lda,
+                                                         const double* __restrict__ B, int n, int64_t ldb,
+                                                         TC* C, int64_t ldc, const int* zero_flag,
+                                                         int64_t grow0) {
+  extern __shared__ double sm[];
+  constexpr int BR = 32;
+  double* Bs = sm;                  // k x n, Bs[l*n + c]
+  double* As = sm + k * n;          // BR x (k+1)
+  const int t = threadIdx.x;
+  const int64_t r0 = int64_t(blockIdx.x) * BR;
+  const bool zero = zero_flag && *zero_flag;
+  if (zero) {
+    for (int e = t; e < BR * n; e += 256) {
+      const int rl = e % BR, c = e / BR;
+      const int64_t row = r0 + rl;
+      if (row < m) C[row + ldc * c] = TC(grow0 + row == c ? 1.0 : 0.0);
+    }
+    return;
+  }
+  for (int e = t; e < k * n; e += 256) {
+    const int l = e % k, c = e / k;
+    Bs[l * n + c] = B[l + ldb * c];
+  }
+  for (int e = t; e < BR * k; e += 256) {
+    const int rl = e % BR, l = e / BR;
+    const int64_t row = r0 + rl;
+    As[rl * (k + 1) + l] = row < m ? double(A[row + lda * l]) : 0.0;
+  }
+  __syncthreads();
+  const int rl = t % BR, cg = t / BR;
+  const int64_t row = r0 + rl;
+  if (row < m) {
+    for (int c = cg; c < n; c += 8) {
+      double s = 0.0;
+      for (int l = 0; l < k; ++l) s = fma(As[rl * (k + 1) + l], Bs[l * n + c], s);
+      C[row + ldc * c] = TC(s);
+    }
+  }
+}
+
+__global__ void gemm_small_kernel(bool ta, bool tb, int m, int n, int k, const double* A, int lda,
+                                  const double* B, int ldb, double* C, int ldc) {
+  for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
+    const int i = e % m, j = e / m;
+    double s = 0.0;
+    for (int l = 0; l < k; ++l) {
+      const double av = ta ? A[l + int64_t(lda) * i] : A[i + int64_t(lda) * l];
+      const double bv = tb ? B[j + int64_t(ldb) * l] : B[l + int64_t(ldb) * j];
+      s = fma(av, bv, s);
+    }
+    C[i + int64_t(ldc) * j] = s;
+  }
+}
+
+// ----------------------------------------------------------- Jacobi EVD
+// Cyclic Jacobi with the round-robin parallel ordering; A (k x k, padded to even kk) in shared
+// memory, V in shared memory when it fits, else in global scratch.  Rotation per pair (p,q):
+// tau = (a_qq - a_pp)/(2 a_pq), t = sign(tau)/(|tau| + sqrt(1+tau^2)), c = 1/sqrt(1+t^2), s = t c;
+// A <- J^T A J with J = [[c, s], [-s, c]] in the (p,q) plane; V <- V J.
+__global__ void __launch_bounds__(512) jacobi_kernel(const double* __restrict__ Ain, int k, double* W,
+                                                     double* Vout, double* Vscratch, int v_in_smem,
+                                                     int64_t stride_a, int64_t stride_w, int64_t stride_v,
+                                                     int64_t stride_scr) {
+  extern __shared__ double sm[];
+  const int kk = k + (k & 1);
+  const int ld = kk + 1;
+  double* A = sm;                                   // kk x ld (row-major A[i*ld + j])
+  double* V = v_in_smem ? (sm + kk * ld) : (Vscratch + blockIdx.x * stride_scr);
+  double* cs = (v_in_smem ? sm + 2 * kk * ld : sm + kk * ld);   // kk/2 pairs: c, s, p, q
+  __shared__ double red[32];
+  __shared__ int s_done;
+  const double* Ab = Ain + blockIdx.x * stride_a;
+  W += blockIdx.x * stride_w;
+  Vout += blockIdx.x * stride_v;
+  const int t = threadIdx.x, nt = blockDim.x;
+  for (int e = t; e < kk * kk; e += nt) {
+    const int i = e / kk, j = e % kk;
+    A[i * ld + j] = (i < k && j < k) ? 0.5 * (Ab[i + int64_t(k) * j] + Ab[j + int64_t(k) * i]) : 0.0;
+    V[i * ld + j] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const int npairs = kk / 2;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    double off = 0.0, dia = 0.0;
+    for (int e = t; e < kk * kk; e += nt) {
+      const int i = e / kk, j = e % kk;
+      const double v = A[i * ld + j];
+      if (i != j) off += v * v; else dia += v * v;
+    }
+    off = block_sum(off, red);
+    __syncthreads();
+    dia = block_sum(dia, red);
+    if (t == 0) s_done = (off <= 1e-30 * dia) || (dia == 0.0);
+    __syncthreads();
+    if (s_done) break;
+    for (int round = 0; round < kk - 1; ++round) {
+      for (int pi = t; pi < npairs; pi += nt) {
+        int p, q;
+        if (pi == 0) { p = round % (kk - 1); q = kk - 1; }
+        else { p = (round + pi) % (kk - 1); q = (round - pi + kk - 1) % (kk - 1); }
+        if (p > q) { const int tmp = p; p = q; q = tmp; }
+        const double apq = A[p * ld + q];
+        double c = 1.0, s = 0.0;
+        if (apq != 0.0) {
+          const double tau = (A[q * ld + q] - A[p * ld + p]) / (2.0 * apq);
+          const double tt = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+          c = 1.0 / sqrt(1.0 + tt * tt);
+          s = tt * c;
+        }
+        cs[4 * pi + 0] = c; cs[4 * pi + 1] = s;
+        cs[4 * pi + 2] = p; cs[4 * pi + 3] = q;
+      }
+      __syncthreads();
+      // rows: A <- J^T A
+      for (int e = t; e < npairs * kk; e += nt) {
+        const int pi = e / kk, l = e % kk;
+        const double c = cs[4 * pi], s = cs[4 * pi + 1];
+        if (s == 0.0) continue;
+        const int p = int(cs[4 * pi + 2]), q = int(cs[4 * pi + 3]);
+        const double ap = A[p * ld + l], aq = A[q * ld + l];
+        A[p * ld + l] = c * ap - s * aq;
+        A[q * ld + l] = s * ap + c * aq;
+      }
+      __syncthreads();
+      // columns: A <- A J, V <- V J
+      for (int e = t; e < npairs * kk; e += nt) {
+        const int pi = e / kk, l = e % kk;
+        const double c = cs[4 * pi], s = cs[4 * pi + 1];
+        if (s == 0.0) continue;
+        const int p = int(cs[4 * pi + 2]), q = int(cs[4 * pi + 3]);
+        const double ap = A[l * ld + p], aq = A[l * ld + q];
+        A[l * ld + p] = c * ap - s * aq;
+        A[l * ld + q] = s * ap + c * aq;
+        const double vp = V[l * ld + p], vq = V[l * ld + q];
+        V[l * ld + p] = c * vp - s * vq;
+        V[l * ld + q] = s * vp + c * vq;
+      }
+      __syncthreads();
+      for (int pi = t; pi < npairs; pi += nt) {
+        if (cs[4 * pi + 1] == 0.0) continue;
+        const int p = int(cs[4 * pi + 2]), q = int(cs[4 * pi + 3]);
+        A[p * ld + q] = 0.0;
+        A[q * ld + p] = 0.0;
+      }
+      __syncthreads();
+    }
+  }
+  // sort descending (stable on ties: lower index first) and write out
+  for (int i = t; i < k; i += nt) {
+    const double wi = A[i * ld + i];
+    int rank = 0;
+    for (int j = 0; j < k; ++j) {
+      const double wj = A[j * ld + j];
+      rank += (wj > wi) || (wj == wi && j < i);
+    }
+    W[rank] = wi;
+    for (int l = 0; l < k; ++l) Vout[l + int64_t(k) * rank] = V[l * ld + i];
+  }
+}
+
+// ------------------------------------------------------------ sign canon
+__global__ void colmax_kernel(const double* __restrict__ Q, int64_t m, int64_t ld, int64_t row0,
+                              double* __restrict__ cand) {
+  const int c = blockIdx.x;
+  double best = -1.0;
+  int64_t brow = INT64_MAX;
+  double bsign = 1.0;
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+    const double v = Q[i + ld * c], av = fabs(v);
+    if (av > best) { best = av; brow = i; bsign = v < 0 ? -1.0 : 1.0; }
+  }
+  __shared__ double sb[256], ss[256];
+  __shared__ int64_t sr[256];
+  sb[threadIdx.x] = best; sr[threadIdx.x] = brow; ss[threadIdx.x] = bsign;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o; o >>= 1) {
+    if (threadIdx.x < o) {
+      const double b2 = sb[threadIdx.x + o];
+      const int64_t r2 = sr[threadIdx.x + o];
+      if (b2 > sb[threadIdx.x] || (b2 == sb[threadIdx.x] && r2 < sr[threadIdx.x])) {
+        sb[threadIdx.x] = b2; sr[threadIdx.x] = r2; ss[threadIdx.x] = ss[threadIdx.x + o];
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    cand[3 * c + 0] = sb[0];
+    cand[3 * c + 1] = double(row0 + (sr[0] == INT64_MAX ? 0 : sr[0]));
+    cand[3 * c + 2] = ss[0];
+  }
+}
+
+__global__ void sign_apply_kernel(const double* __restrict__ cand, int nc, int r, double* Q, int64_t m,
+                                  int64_t ld, double* U, int ku, int64_t ldu) {
+  const int c = blockIdx.x;
+  double best = -1.0, brow = 0.0, bsign = 1.0;
+  for (int s = 0; s < nc; ++s) {
+    const double* cd = cand + int64_t(s) * 3 * r + 3 * c;
+    if (cd[0] > best || (cd[0] == best && cd[1] < brow)) { best = cd[0]; brow = cd[1]; bsign = cd[2]; }
+  }
+  if (bsign >= 0) return;
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) Q[i + ld * c] = -Q[i + ld * c];
+  if (U)
+    for (int i = threadIdx.x; i < ku; i += blockDim.x) U[i + ldu * c] = -U[i + ldu * c];
+}
+
+// ------------------------------------------------------------ helpers
+template <typename Ti, typename To>
+__global__ void convert2d_kernel(const Ti* __restrict__ in, int64_t m, int64_t n, int64_t ldi,
+                                 To* __restrict__ out, int64_t ldo) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= m * n) return;
+  const int64_t i = e % m, j = e / m;
+  out[i + ldo * j] = To(in[i + ldi * j]);
+}
+
+template <typename T>
+__global__ void unfold_copy_kernel(const T* __restrict__ Tt, int64_t a, int64_t I, int64_t J,
+                                   double* __restrict__ out, int64_t ldo) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= I * J) return;
+  const int64_t i = e % I, j = e / I;
+  out[i + ldo * j] = double(Tt[(j % a) + a * i + a * I * (j / a)]);
+}
+
+// Residual: tiles of 128 (j) x 64 (i); R in chunks of BR; grid-stride over tiles.
+template <typename T>
+__global__ void __launch_bounds__(256) residual_kernel(const T* __restrict__ X, int64_t J, int64_t In,
+                                                        const T* __restrict__ P, int R, const T* __restrict__ Q,
+                                                        int64_t ldq, double* __restrict__ part) {
+  using Tacc = typename AccOf<T>::type;
+  constexpr int BM = 128, BN = 64, BR = 16;
+  __shared__ Tacc Ps[BR][BM];
+  __shared__ Tacc Qs[BR][BN + 1];
+  __shared__ double red[32];
+  const int t = threadIdx.x, tx = t & 31, ty = t >> 5;
+  const int64_t njt = cdiv(J, BM), nit = cdiv(In, BN), ntiles = njt * nit;
+  double res = 0.0, xx = 0.0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t j0 = (tile % njt) * BM, i0 = (tile / njt) * BN;
+    Tacc acc[4][8];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[r][c] = Tacc(0);
+    for (int r0 = 0; r0 < R; r0 += BR) {
+      for (int e = t; e < BR * BM; e += 256) {
+        const int jl = e % BM, rr = e / BM;
+        const int64_t j = j0 + jl;
+        Ps[rr][jl] = (j < J && r0 + rr < R) ? Tacc(P[j + J * (r0 + rr)]) : Tacc(0);
+      }
+      for (int e = t; e < BR * BN; e += 256) {
+        const int il = e % BN, rr = e / BN;
+        const int64_t i = i0 + il;
+        Qs[rr][il] = (i < In && r0 + rr < R) ? Tacc(Q[i + ldq * (r0 + rr)]) : Tacc(0);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int rr = 0; rr < BR; ++rr) {
+        Tacc pr[4], qr[8];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) pr[r] = Ps[rr][tx + 32 * r];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) qr[c] = Qs[rr][ty + 8 * c];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 8; ++c) acc[r][c] = fma(pr[r], qr[c], acc[r][c]);
+      }
+      __syncthreads();
+    }
+    Tacc tres = 0, txx = 0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int64_t i = i0 + ty + 8 * c;
+      if (i >= In) continue;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int64_t j = j0 + tx + 32 * r;
+        if (j >= J) continue;
+        const Tacc x = Tacc(X[j + J * i]);
+        const Tacc d = x - acc[r][c];
+        tres = fma(d, d, tres);
+        txx = fma(x, x, txx);
+      }
+    }
+    res += double(tres);
+    xx += double(txx);
+  }
+  res = block_sum(res, red);
+  __syncthreads();
+  xx = block_sum(xx, red);
+  if (t == 0) {
+    part[2 * blockIdx.x] = res;
+    part[2 * blockIdx.x + 1] = xx;
+  }
+}
+
+__global__ void reduce_pairs_kernel(const double* __restrict__ part, int n, double* __restrict__ out) {
+  __shared__ double red[32];
+  double a = 0.0, b = 0.0;
+  // fixed assignment + fixed tree => deterministic
+  for (int i = threadIdx.x; i < n; i += blockDim.x) { a += part[2 * i]; b += part[2 * i + 1]; }
+  a = block_sum(a, red);
+  __syncthreads();
+  b = block_sum(b, red);
+  if (threadIdx.x == 0) { out[0] = a; out[1] = b; }
+}
+
+__global__ void sumsq_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s = fma(x[i], x[i], s);
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) *out = s;
+}
+
+__global__ void finalize_err_kernel(const double* sums, const double* gg, double* E, double* Eg) {
+  const double res = sums[0], xx = sums[1];
+  if (E) *E = xx > 0 ? sqrt(res / xx) : 0.0;
+  if (Eg) *Eg = xx > 0 ? sqrt(fmax(0.0, 1.0 - *gg / xx)) : 0.0;
+}
+
+__global__ void nonfinite_kernel(const double* __restrict__ x, int64_t n, int* status) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e < n && !isfinite(x[e])) latch(status, kStatusNonFinite);
+}
+
+}  // namespace
+
+// ======================================================================= host
+template <typename T>
+void gram(const Ctx& ctx, Arena& ws, const T* A, int64_t m, int k, int64_t lda, double* G) {
+  RT_REQUIRE(k >= 1 && k <= 128, kEUNSUPPORTED, "gram: k must be in [1,128]");
+  if (m == 0) { RT_CUDA(cudaMemsetAsync(G, 0, sizeof(double) * k * k, ctx.stream)); return; }
+  if (k <= 16) launch_gram<T, 1>(ctx, ws, A, m, k, lda, G);
+  else if (k <= 32) launch_gram<T, 2>(ctx, ws, A, m, k, lda, G);
+  else if (k <= 48) launch_gram<T, 3>(ctx, ws, A, m, k, lda, G);
+  else if (k <= 64) launch_gram<T, 4>(ctx, ws, A, m, k, lda, G);
+  else if (k <= 80) launch_gram<T, 5>(ctx, ws, A, m, k, lda, G);
+  else if (k <= 96) launch_gram<T, 6>(ctx, ws, A, m, k, lda, G);
+  else launch_gram<T, 8>(ctx, ws, A, m, k, lda, G);
+}
+template void gram<float>(const Ctx&, Arena&, const float*, int64_t, int, int64_t, double*);
+template void gram<double>(const Ctx&, Arena&, const double*, int64_t, int, int64_t, double*);
+
+void chol_inv(const Ctx& ctx, const double* G, int k, double shift_coef, double* R, double* Rinv,
+              int* zero_flag) {
+  const size_t smem = sizeof(double) * size_t(k) * (k + 1);
+  RT_REQUIRE(smem <= 220 * 1024, kEUNSUPPORTED, "chol_inv: k too large");
+  static bool attr = false;
+  if (!attr) {
+    RT_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    attr = true;
+  }
+  launch(ctx, "chol_inv", [&] {
+    chol_inv_kernel<<<1, 512, smem, ctx.stream>>>(G, k, shift_coef, R, Rinv, zero_flag, ctx.d_status);
+  });
+}
+
+template <typename TA, typename TC>
+void gemm_tall(const Ctx& ctx, const TA* A, int64_t m, int k, int64_t lda, const double* B, int n,
+               int64_t ldb, TC* C, int64_t ldc, const int* zero_flag, int64_t row0) {
+  if (m == 0 || n == 0) return;
+  const size_t smem = sizeof(double) * (size_t(k) * n + 32 * size_t(k + 1));
+  RT_REQUIRE(smem <= 220 * 1024, kEUNSUPPORTED, "gemm_tall: k*n too large");
+  static bool attr = false;
+  if (!attr) {
+    RT_CUDA(cudaFuncSetAttribute(gemm_tall_kernel<TA, TC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    attr = true;
+  }
+  launch(ctx, "gemm_tall", [&] {
+    gemm_tall_kernel<TA, TC><<<unsigned(cdiv(m, 32)), 256, smem, ctx.stream>>>(A, m, k, lda, B, n, ldb, C, ldc,
+                                                                               zero_flag, row0);
+  });
+}
+template void gemm_tall<double, double>(const Ctx&, const double*, int64_t, int, int64_t, const double*, int,
+                                        int64_t, double*, int64_t, const int*, int64_t);
+template void gemm_tall<float, float>(const Ctx&, const float*, int64_t, int, int64_t, const double*, int,
+                                      int64_t, float*, int64_t, const int*, int64_t);
+template void gemm_tall<float, double>(const Ctx&, const float*, int64_t, int, int64_t, const double*, int,
+                                       int64_t, double*, int64_t, const int*, int64_t);
+
+void gemm_small(const Ctx& ctx, bool ta, bool tb, int m, int n, int k, const double* A, int lda,
+                const double* B, int ldb, double* C, int ldc) {
+  launch(ctx, "gemm_small", [&] {
+    gemm_small_kernel<<<1, 512, 0, ctx.stream>>>(ta, tb, m, n, k, A, lda, B, ldb, C, ldc);
+  });
+}
+
+void eig_sym(const Ctx& ctx, Arena& ws, const double* A, int k, double* W, double* V, int count,
+             int64_t stride_a, int64_t stride_w, int64_t stride_v) {
+  RT_REQUIRE(k >= 1 && k <= 128, kEUNSUPPORTED, "eig_sym: k must be in [1,128]");
+  const int kk = k + (k & 1), ld = kk + 1;
+  const size_t a_bytes = sizeof(double) * size_t(kk) * ld;
+  const size_t cs_bytes = sizeof(double) * 4 * size_t(kk / 2 + 1);
+  int v_in_smem = (2 * a_bytes + cs_bytes) <= 200 * 1024;
+  const size_t smem = (v_in_smem ? 2 * a_bytes : a_bytes) + cs_bytes;
+  double* scratch = nullptr;
+  int64_t stride_scr = 0;
+  if (!v_in_smem) {
+    stride_scr = int64_t(kk) * ld;
+    scratch = ws.alloc_n<double>(stride_scr * count);
+  }
+  static bool attr = false;
+  if (!attr) {
+    RT_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    attr = true;
+  }
+  launch(ctx, "jacobi_eig", [&] {
+    jacobi_kernel<<<count, 512, smem, ctx.stream>>>(A, k, W, V, scratch, v_in_smem, stride_a, stride_w, stride_v,
+                                                    stride_scr);
+  });
+}
+
+void colmax_candidates(const Ctx& ctx, const double* Q, int64_t m, int r, int64_t ld, int64_t row0,
+                       double* cand) {
+  launch(ctx, "colmax", [&] { colmax_kernel<<<r, 256, 0, ctx.stream>>>(Q, m, ld, row0, cand); });
+}
+
+void sign_apply(const Ctx& ctx, const double* cand, int nc, double* Q, int64_t m, int r, int64_t ld,
+                double* U, int ku, int64_t ldu) {
+  launch(ctx, "sign_apply", [&] {
+    sign_apply_kernel<<<r, 256, 0, ctx.stream>>>(cand, nc, r, Q, m, ld, U, ku, ldu);
+  });
+}
+
+template <typename Ti, typename To>
+void convert2d(const Ctx& ctx, const Ti* in, int64_t m, int64_t n, int64_t ldi, To* out, int64_t ldo) {
+  if (m * n == 0) return;
+  launch(ctx, "convert", [&] {
+    convert2d_kernel<Ti, To><<<unsigned(cdiv(m * n, 256)), 256, 0, ctx.stream>>>(in, m, n, ldi, out, ldo);
+  });
+}
+template void convert2d<double, float>(const Ctx&, const double*, int64_t, int64_t, int64_t, float*, int64_t);
+template void convert2d<double, double>(const Ctx&, const double*, int64_t, int64_t, int64_t, double*, int64_t);
+template void convert2d<float, double>(const Ctx&, const float*, int64_t, int64_t, int64_t, double*, int64_t);
+
+template <typename T>
+void unfold_copy(const Ctx& ctx, const T* Tt, Box box, double* out, int64_t ldo) {
+  const int64_t n = box.I * box.J();
+  if (n == 0) return;
+  launch(ctx, "unfold_copy", [&] {
+    unfold_copy_kernel<T><<<unsigned(cdiv(n, 256)), 256, 0, ctx.stream>>>(Tt, box.a, box.I, box.J(), out, ldo);
+  });
+}
+template void unfold_copy<float>(const Ctx&, const float*, Box, double*, int64_t);
+template void unfold_copy<double>(const Ctx&, const double*, Box, double*, int64_t);
+
+template <typename T>
+void residual(const Ctx& ctx, Arena& ws, const T* X, int64_t J, int64_t In, const T* P, int R, const T* Q,
+              int64_t ldq, double* out2) {
+  const int nblk = 4 * ctx.num_sms;
+  double* part = ws.alloc_n<double>(2 * nblk);
+  launch(ctx, "residual_simt", [&] {
+    residual_kernel<T><<<nblk, 256, 0, ctx.stream>>>(X, J, In, P, R, Q, ldq, part);
+  });
+  launch(ctx, "reduce_pairs", [&] { reduce_pairs_kernel<<<1, 256, 0, ctx.stream>>>(part, nblk, out2); });
+}
+template void residual<float>(const Ctx&, Arena&, const float*, int64_t, int64_t, const float*, int, const float*,
+                              int64_t, double*);
+template void residual<double>(const Ctx&, Arena&, const double*, int64_t, int64_t, const double*, int,
+                               const double*, int64_t, double*);
+
+void sumsq(const Ctx& ctx, Arena&, const double* x, int64_t n, double* out) {
+  launch(ctx, "sumsq", [&] { sumsq_kernel<<<1, 512, 0, ctx.stream>>>(x, n, out); });
+}
+
+void finalize_err(const Ctx& ctx, const double* sums, const double* gg, double* E, double* Eg) {
+  launch(ctx, "finalize_err", [&] { finalize_err_kernel<<<1, 1, 0, ctx.stream>>>(sums, gg, E, Eg); });
+}
+
+void fill_zero(const Ctx& ctx, void* p, size_t bytes) { RT_CUDA(cudaMemsetAsync(p, 0, bytes, ctx.stream)); }
+
+void set_status_if_nonfinite(const Ctx& ctx, const double* x, int64_t n) {
+  if (n == 0) return;
+  launch(ctx, "nonfinite_check", [&] {
+    nonfinite_kernel<<<unsigned(cdiv(n, 256)), 256, 0, ctx.stream>>>(x, n, ctx.d_status);
+  });
+}
+
+}  // namespace rt

@@ -1,0 +1,403 @@
+// pipeline.cu -- the randomized Tucker/HOSVD hot path on one rank.
+//
+// Every step runs in this library's kernels; torch only owns the caller's buffers.
+// Distributed semantics (slab along the last mode):
+//   C1  mode n < N-1 sketches / power products Y: per-slab partial sums -> allreduce
+//   C2  Gram matrices of row-distributed tall matrices (Y_{N-1}, Z_n for n < N-1) -> allreduce
+//   C3  Z = X_(N-1)^T Q of the last mode: per-slab partial sums (J x K) -> allreduce
+//   C4  core G~: per-slab partial sums -> allreduce
+//   C5  residual sums -> allreduce;  sign candidates of the row-distributed last factor -> allgather
+#include <cmath>
+
+#include "engine.h"
+
+namespace rt {
+
+namespace {
+constexpr double kU = 1.1102230246251565e-16;   // fp64 unit roundoff
+
+template <typename T> struct DT;
+template <> struct DT<float> { static constexpr int id = 0; };
+template <> struct DT<double> { static constexpr int id = 1; };
+
+template <typename T>
+void allreduce(Comm* c, bool on, T* p, int64_t n, cudaStream_t s) {
+  if (on && n > 0) c->allreduce_sum(p, size_t(n), s);
+}
+}  // namespace
+
+// ------------------------------------------------------------------ QR (a4)
+// Shifted CholeskyQR3 (sCQR3): step 1 with shift 11(mk + k(k+1)) u trace(G), steps 2-3 plain
+// CholeskyQR; R = R3 R2 R1, R_ii >= 0 by construction (reading R5).  Gram in fp64.
+template <typename T>
+void Engine::qr_rows(const T* Y, int64_t m, int64_t m_glob, int k, int64_t ldy, double* Q, int64_t ldq,
+                     double* R, bool rows_dist, int64_t row0) {
+  RT_REQUIRE(m_glob >= k, kERANK, "qr: needs m >= k");
+  const auto mk = ws.mark();
+  double* G = ws.alloc_n<double>(int64_t(k) * k);
+  double* Rs[3];
+  double* Ri = ws.alloc_n<double>(int64_t(k) * k);
+  for (int s = 0; s < 3; ++s) Rs[s] = ws.alloc_n<double>(int64_t(k) * k);
+  int* zero = ws.alloc_n<int>(1);
+  double* Q1 = ws.alloc_n<double>(m * k);
+  const bool dist_g = rows_dist && dist();
+  // step 1
+  gram<T>(ctx, ws, Y, m, k, ldy, G);
+  allreduce(comm, dist_g, G, int64_t(k) * k, ctx.stream);
+  const double shift = 11.0 * (double(m_glob) * k + double(k) * (k + 1)) * kU;
+  chol_inv(ctx, G, k, shift, Rs[0], Ri, zero);
+  gemm_tall<T, double>(ctx, Y, m, k, ldy, Ri, k, k, Q1, m, zero, row0);
+  // steps 2, 3
+  for (int s = 1; s < 3; ++s) {
+    gram<double>(ctx, ws, Q1, m, k, m, G);
+    allreduce(comm, dist_g, G, int64_t(k) * k, ctx.stream);
+    chol_inv(ctx, G, k, 0.0, Rs[s], Ri, nullptr);
+    if (s == 1) gemm_tall<double, double>(ctx, Q1, m, k, m, Ri, k, k, Q1, m);
+    else gemm_tall<double, double>(ctx, Q1, m, k, m, Ri, k, k, Q, ldq);
+  }
+  if (R) {
+    double* T21 = ws.alloc_n<double>(int64_t(k) * k);
+    gemm_small(ctx, false, false, k, k, k, Rs[1], k, Rs[0], k, T21, k);
+    gemm_small(ctx, false, false, k, k, k, Rs[2], k, T21, k, R, k);
+  }
+  ws.rewind(mk);
+}
+
+void Engine::qr_y(const double* Y, int64_t m, int64_t m_glob, int k, int64_t ldy, double* Q, int64_t ldq,
+                  double* R, bool rows_dist, int64_t row0) {
+  qr_rows<double>(Y, m, m_glob, k, ldy, Q, ldq, R, rows_dist, row0);
+}
+
+// Z only conditions the next product Y = X_(n) Z (span(X Z R^-1) = span(X Z)); a single
+// CholeskyQR step with a small safety shift keeps it well conditioned.
+template <typename T>
+void Engine::qr_z(T* Z, int64_t m, int64_t m_glob, int k, bool rows_dist, int64_t row0) {
+  const auto mk = ws.mark();
+  double* G = ws.alloc_n<double>(int64_t(k) * k);
+  double* Rr = ws.alloc_n<double>(int64_t(k) * k);
+  double* Ri = ws.alloc_n<double>(int64_t(k) * k);
+  int* zero = ws.alloc_n<int>(1);
+  gram<T>(ctx, ws, Z, m, k, m, G);
+  allreduce(comm, rows_dist && dist(), G, int64_t(k) * k, ctx.stream);
+  (void)m_glob;
+  chol_inv(ctx, G, k, 1e-13, Rr, Ri, zero);
+  gemm_tall<T, T>(ctx, Z, m, k, m, Ri, k, k, Z, m, zero, row0);
+  ws.rewind(mk);
+}
+
+// ---------------------------------------------------------------- sketch (a1-a3)
+template <typename T>
+void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* const* omega,
+                    const int64_t* omega_cols, int q, double* Yt) {
+  const int N = X.N;
+  const Box bx = X.box(n);
+  const bool last = (n == N - 1);
+  const int64_t In = bx.I;
+  int K;
+  if (kind == 0) {
+    K = int(omega_cols[n]);
+    ttm_s<T>(ctx, ws, data, bx, static_cast<const T*>(omega[n]), K, 1, K, Yt, In);
+  } else {
+    // Kronecker sketch W = X x_{k!=n} Omega_k^T (Eq.(2)): a chain of TTMs whose first
+    // stage streams X and whose later stages run on the shrunken result.
+    int64_t cur[5];
+    for (int k = 0; k < N; ++k) cur[k] = X.d[k];
+    K = 1;
+    for (int k = 0; k < N; ++k) if (k != n) K *= int(omega_cols[k]);
+    const auto mk = ws.mark();
+    const T* src = data;
+    T* bufs[2] = {nullptr, nullptr};
+    int which = 0;
+    for (int k = 0; k < N; ++k) {
+      if (k == n) continue;
+      const Box b = TView::box_of(cur, N, k);
+      const int L = int(omega_cols[k]);
+      T* dst = ws.alloc_n<T>(b.a * L * b.b);
+      bufs[which] = dst;
+      ttm_t<T, T, T>(ctx, src, b, static_cast<const T*>(omega[k]), L, 1, L, dst, 1, b.a, b.a * L);
+      src = dst;
+      cur[k] = L;
+      which ^= 1;
+    }
+    unfold_copy<T>(ctx, src, TView::box_of(cur, N, n), Yt, In);
+    ws.rewind(mk);   // the Y result is in Yt; intermediates are dead (stream order)
+  }
+  allreduce(comm, !last && dist(), Yt, In * K, ctx.stream);                       // C1
+  set_status_if_nonfinite(ctx, Yt, In * K);
+  if (q <= 0) return;
+  // power iterations (reading R2): Q = qr(Y); Z = qr(X_(n)^T Q); Y = X_(n) Z
+  const auto mk = ws.mark();
+  const int64_t Jl = bx.J();
+  double* Qy = ws.alloc_n<double>(In * K);
+  T* QyT = (DT<T>::id == 1) ? reinterpret_cast<T*>(Qy) : ws.alloc_n<T>(In * K);
+  T* Z = ws.alloc_n<T>(Jl * K);
+  const int64_t row0_last = X.off;
+  for (int it = 0; it < q; ++it) {
+    qr_y(Yt, In, X.Ig(n), K, In, Qy, In, nullptr, last && dist(), last ? row0_last : 0);
+    if (DT<T>::id == 0) convert2d<double, T>(ctx, Qy, In, K, In, QyT, In);
+    // Z(j, c) = sum_i X_(n)(i, j) Q(i, c), written col-major J x K: so_a=1, so_c=J, so_b=a
+    ttm_t<T, T, T>(ctx, data, bx, QyT, 1, In, K, Z, 1, Jl, bx.a);
+    allreduce(comm, last && dist(), Z, Jl * K, ctx.stream);                      // C3
+    // local Z rows: for n < N-1 the slab's j's are the contiguous block starting at a*b'*off
+    int64_t zrow0 = 0;
+    if (!last) {
+      int64_t bp = 1;
+      for (int k = n + 1; k < N - 1; ++k) bp *= X.d[k];
+      zrow0 = bx.a * bp * X.off;
+    }
+    qr_z<T>(Z, Jl, X.Jg(n), K, !last && dist(), zrow0);
+    ttm_s<T>(ctx, ws, data, bx, Z, 1, Jl, K, Yt, In);
+    allreduce(comm, !last && dist(), Yt, In * K, ctx.stream);                     // C1
+  }
+  ws.rewind(mk);
+}
+
+// ---------------------------------------------------------------------- core (a5)
+template <typename T>
+void Engine::core(const TView& X, const T* data, const double* const* Qt, const int64_t* ldq, const int64_t* K,
+                  double* Gt) {
+  const int N = X.N;
+  const auto mk = ws.mark();
+  const T* QT[5];
+  for (int n = 0; n < N; ++n) {
+    if (DT<T>::id == 1) { QT[n] = reinterpret_cast<const T*>(Qt[n]); continue; }
+    T* c = ws.alloc_n<T>(X.d[n] * K[n]);
+    convert2d<double, T>(ctx, Qt[n], X.d[n], K[n], ldq[n], c, X.d[n]);
+    QT[n] = c;
+  }
+  int64_t cur[5];
+  for (int k = 0; k < N; ++k) cur[k] = X.d[k];
+  const T* src = data;
+  for (int n = 0; n < N; ++n) {
+    const Box b = TView::box_of(cur, N, n);
+    const int64_t ld = (DT<T>::id == 1) ? ldq[n] : X.d[n];
+    if (n == N - 1) {
+      ttm_t<T, T, double>(ctx, src, b, QT[n], 1, ld, int(K[n]), Gt, 1, b.a, b.a * K[n]);
+    } else {
+      T* dst = ws.alloc_n<T>(b.a * K[n] * b.b);
+      ttm_t<T, T, T>(ctx, src, b, QT[n], 1, ld, int(K[n]), dst, 1, b.a, b.a * K[n]);
+      src = dst;
+    }
+    cur[n] = K[n];
+  }
+  int64_t gsz = 1;
+  for (int n = 0; n < N; ++n) gsz *= K[n];
+  allreduce(comm, dist(), Gt, gsz, ctx.stream);                                  // C4
+  ws.rewind(mk);
+}
+
+// ------------------------------------------------------------- sign canon (R5)
+void Engine::canon(double* Qn, int64_t m, int r, int64_t ld, int64_t row0, bool dist_rows, double* U, int ku) {
+  const auto mk = ws.mark();
+  double* cand = ws.alloc_n<double>(3 * r);
+  colmax_candidates(ctx, Qn, m, r, ld, row0, cand);
+  int nc = 1;
+  if (dist_rows && dist()) {
+    nc = comm->nranks();
+    double* all = ws.alloc_n<double>(3 * r * nc);
+    comm->allgather(cand, all, size_t(3 * r), ctx.stream);
+    cand = all;
+  }
+  sign_apply(ctx, cand, nc, Qn, m, r, ld, U, ku, ku);
+  ws.rewind(mk);
+}
+
+// ------------------------------------------------------------- truncation (a6)
+void Engine::truncate(const TView& X, const double* Gt, const int64_t* K, const double* const* Qt,
+                      const int64_t* ldq, const int64_t* R, double* const* Q_out, double* G_out) {
+  const int N = X.N;
+  const auto mk = ws.mark();
+  double* V[5];
+  double* W = ws.alloc_n<double>(128);
+  for (int n = 0; n < N; ++n) {
+    const int k = int(K[n]);
+    double* M = ws.alloc_n<double>(int64_t(k) * k);
+    V[n] = ws.alloc_n<double>(int64_t(k) * k);
+    // M_n = G~_(n) G~_(n)^T (Gram-EVD)
+    ttm_s<double>(ctx, ws, Gt, TView::box_of(K, N, n), nullptr, 0, 0, k, M, k, /*gram=*/true);
+    eig_sym(ctx, ws, M, k, W, V[n]);
+    // Q_n = Q~_n U_n, U_n = V_n[:, :R_n]; sign canonicalization on the lifted factor
+    gemm_tall<double, double>(ctx, Qt[n], X.d[n], k, ldq[n], V[n], int(R[n]), k, Q_out[n], X.d[n]);
+    canon(Q_out[n], X.d[n], int(R[n]), X.d[n], n == N - 1 ? X.off : 0, n == N - 1, V[n], k);
+  }
+  // G = G~ x_1 U_1^T ... x_N U_N^T
+  int64_t cur[5];
+  for (int k = 0; k < N; ++k) cur[k] = K[k];
+  const double* src = Gt;
+  for (int n = 0; n < N; ++n) {
+    const Box b = TView::box_of(cur, N, n);
+    double* dst = (n == N - 1) ? G_out : ws.alloc_n<double>(b.a * R[n] * b.b);
+    ttm_t<double, double, double>(ctx, src, b, V[n], 1, K[n], int(R[n]), dst, 1, b.a, b.a * R[n]);
+    src = dst;
+    cur[n] = R[n];
+  }
+  ws.rewind(mk);
+}
+
+// ------------------------------------------------------------- residual (a8)
+template <typename T>
+void Engine::rel_error(const TView& X, const T* data, const double* G, const int64_t* R, const double* const* Q,
+                       double* E, double* Eg) {
+  const int N = X.N;
+  const auto mk = ws.mark();
+  double* sums = ws.alloc_n<double>(2);
+  double* gg = ws.alloc_n<double>(1);
+  int64_t gsz = 1;
+  for (int n = 0; n < N; ++n) gsz *= R[n];
+  sumsq(ctx, ws, G, gsz, gg);
+  // P = G x_1 Q_1 ... x_{N-1} Q_{N-1} (all but the last mode), then the residual kernel
+  // rebuilds X^ = P x_N Q_N tile by tile against X.
+  int64_t cur[5];
+  for (int k = 0; k < N; ++k) cur[k] = R[k];
+  const double* src = G;
+  T* P = nullptr;
+  for (int n = 0; n < N - 1; ++n) {
+    const Box b = TView::box_of(cur, N, n);
+    const int64_t In = X.d[n];
+    if (n == N - 2) {
+      P = ws.alloc_n<T>(b.a * In * b.b);
+      ttm_t<double, double, T>(ctx, src, b, Q[n], In, 1, int(In), P, 1, b.a, b.a * In);
+    } else {
+      double* dst = ws.alloc_n<double>(b.a * In * b.b);
+      ttm_t<double, double, double>(ctx, src, b, Q[n], In, 1, int(In), dst, 1, b.a, b.a * In);
+      src = dst;
+    }
+    cur[n] = In;
+  }
+  const int64_t Il = X.d[N - 1];
+  const int Rl = int(R[N - 1]);
+  const T* QL;
+  if (DT<T>::id == 1) {
+    QL = reinterpret_cast<const T*>(Q[N - 1]);
+  } else {
+    T* c = ws.alloc_n<T>(Il * Rl);
+    convert2d<double, T>(ctx, Q[N - 1], Il, Rl, Il, c, Il);
+    QL = c;
+  }
+  int64_t J = 1;
+  for (int k = 0; k < N - 1; ++k) J *= X.d[k];
+  residual<T>(ctx, ws, data, J, Il, P, Rl, QL, Il, sums);
+  allreduce(comm, dist(), sums, 2, ctx.stream);                                    // C5
+  finalize_err(ctx, sums, gg, E, Eg);
+  ws.rewind(mk);
+}
+
+// ----------------------------------------------------------------- HOSVD (Alg.6)
+template <typename T>
+void Engine::hosvd(const TView& X, const int64_t* R, int q, int kind, const void* const* omega,
+                   const int64_t* omega_cols, double* const* Q_out, double* G_out, double* E, double* Eg) {
+  const int N = X.N;
+  const T* data = static_cast<const T*>(X.data);
+  const auto mk = ws.mark();
+  int64_t K[5], ldq[5];
+  double* Qt[5];
+  for (int n = 0; n < N; ++n) {
+    const void* const* om = omega + n * N;
+    const int64_t* oc = omega_cols + n * N;
+    if (kind == 0) K[n] = oc[n];
+    else { K[n] = 1; for (int k = 0; k < N; ++k) if (k != n) K[n] *= oc[k]; }
+    const int64_t In = X.d[n];
+    double* Yt = ws.alloc_n<double>(In * K[n]);
+    sketch<T>(X, data, n, kind, om, oc, q, Yt);
+    Qt[n] = ws.alloc_n<double>(In * K[n]);
+    ldq[n] = In;
+    const bool last = (n == N - 1);
+    qr_y(Yt, In, X.Ig(n), int(K[n]), In, Qt[n], In, nullptr, last && dist(), last ? X.off : 0);
+  }
+  int64_t gsz = 1;
+  for (int n = 0; n < N; ++n) gsz *= K[n];
+  double* Gt = ws.alloc_n<double>(gsz);
+  core<T>(X, data, Qt, ldq, K, Gt);
+  truncate(X, Gt, K, Qt, ldq, R, Q_out, G_out);
+  if (E || Eg) rel_error<T>(X, data, G_out, R, Q_out, E, Eg);
+  ws.rewind(mk);
+}
+
+// -------------------------------------------------------------- STHOSVD (Alg.8)
+template <typename T>
+void Engine::sthosvd(const TView& X, const int64_t* R, int q, int kind, const void* const* omega,
+                     const int64_t* omega_cols, const int* order, double* const* Q_out, double* G_out,
+                     double* E, double* Eg) {
+  const int N = X.N;
+  const auto mk = ws.mark();
+  TView S = X;                         // working tensor S (reading R8: S = X)
+  const T* sdata = static_cast<const T*>(X.data);
+  // S only shrinks (R_n <= I_n): two persistent ping-pong buffers sized for the first shrink
+  int64_t total = 1;
+  for (int k = 0; k < N; ++k) total *= X.d[k];
+  const int first = order ? order[0] : 0;
+  const int64_t smax = total / X.d[first] * R[first];
+  T* sbuf[2] = {ws.alloc_n<T>(smax), ws.alloc_n<T>(smax)};
+  for (int step = 0; step < N; ++step) {
+    const int n = order ? order[step] : step;
+    const void* const* om = omega + n * N;
+    const int64_t* oc = omega_cols + n * N;
+    int K;
+    if (kind == 0) K = int(oc[n]);
+    else { K = 1; for (int k = 0; k < N; ++k) if (k != n) K *= int(oc[k]); }
+    const int64_t In = S.d[n];
+    const auto mstep = ws.mark();
+    // Alg.8 line 3 = Alg.1 lines 1-3 on S_(n): sketch (+ power iterations) and thin QR
+    double* Yt = ws.alloc_n<double>(In * K);
+    sketch<T>(S, sdata, n, kind, om, oc, q, Yt);
+    double* Qt = ws.alloc_n<double>(In * K);
+    qr_y(Yt, In, In, K, In, Qt, In, nullptr, false, 0);
+    T* QtT = (DT<T>::id == 1) ? reinterpret_cast<T*>(Qt) : ws.alloc_n<T>(In * K);
+    if (DT<T>::id == 0) convert2d<double, T>(ctx, Qt, In, K, In, QtT, In);
+    // Alg.1 line 4: B = S x_n Q~^T
+    const Box bs = S.box(n);
+    T* B = ws.alloc_n<T>(bs.a * K * bs.b);
+    ttm_t<T, T, T>(ctx, sdata, bs, QtT, 1, In, K, B, 1, bs.a, bs.a * K);
+    // Alg.1 lines 5-7 via the Gram-EVD of B_(n): U = top-R_n eigenvectors, Q_n = Q~ U
+    const Box bb{bs.a, K, bs.b};
+    double* M = ws.alloc_n<double>(int64_t(K) * K);
+    double* V = ws.alloc_n<double>(int64_t(K) * K);
+    double* W = ws.alloc_n<double>(K);
+    ttm_s<T>(ctx, ws, B, bb, nullptr, 0, 0, K, M, K, /*gram=*/true);
+    eig_sym(ctx, ws, M, K, W, V);
+    gemm_tall<double, double>(ctx, Qt, In, K, In, V, int(R[n]), K, Q_out[n], In);
+    canon(Q_out[n], In, int(R[n]), In, 0, false, V, K);
+    // Alg.8 line 4 with the ΛV^T shortcut: S <- B x_n U^T
+    T* VT = (DT<T>::id == 1) ? reinterpret_cast<T*>(V) : ws.alloc_n<T>(int64_t(K) * R[n]);
+    if (DT<T>::id == 0) convert2d<double, T>(ctx, V, K, R[n], K, VT, K);
+    if (step == N - 1) {
+      ttm_t<T, T, double>(ctx, B, bb, VT, 1, K, int(R[n]), G_out, 1, bb.a, bb.a * R[n]);
+    } else {
+      T* Snew = sbuf[step & 1];
+      ttm_t<T, T, T>(ctx, B, bb, VT, 1, K, int(R[n]), Snew, 1, bb.a, bb.a * R[n]);
+      sdata = Snew;
+    }
+    ws.rewind(mstep);
+    S.d[n] = R[n];
+    S.glob = S.d[N - 1];
+  }
+  if (E || Eg) rel_error<T>(X, static_cast<const T*>(X.data), G_out, R, Q_out, E, Eg);
+  ws.rewind(mk);
+}
+
+template void Engine::sketch<float>(const TView&, const float*, int, int, const void* const*, const int64_t*, int,
+                                    double*);
+template void Engine::sketch<double>(const TView&, const double*, int, int, const void* const*, const int64_t*,
+                                     int, double*);
+template void Engine::qr_rows<float>(const float*, int64_t, int64_t, int, int64_t, double*, int64_t, double*,
+                                     bool, int64_t);
+template void Engine::qr_rows<double>(const double*, int64_t, int64_t, int, int64_t, double*, int64_t, double*,
+                                      bool, int64_t);
+template void Engine::core<float>(const TView&, const float*, const double* const*, const int64_t*,
+                                  const int64_t*, double*);
+template void Engine::core<double>(const TView&, const double*, const double* const*, const int64_t*,
+                                   const int64_t*, double*);
+template void Engine::rel_error<float>(const TView&, const float*, const double*, const int64_t*,
+                                       const double* const*, double*, double*);
+template void Engine::rel_error<double>(const TView&, const double*, const double*, const int64_t*,
+                                        const double* const*, double*, double*);
+template void Engine::hosvd<float>(const TView&, const int64_t*, int, int, const void* const*, const int64_t*,
+                                   double* const*, double*, double*, double*);
+template void Engine::hosvd<double>(const TView&, const int64_t*, int, int, const void* const*, const int64_t*,
+                                    double* const*, double*, double*, double*);
+template void Engine::sthosvd<float>(const TView&, const int64_t*, int, int, const void* const*, const int64_t*,
+                                     const int*, double* const*, double*, double*, double*);
+template void Engine::sthosvd<double>(const TView&, const int64_t*, int, int, const void* const*,
+                                      const int64_t*, const int*, double* const*, double*, double*, double*);
+
+}  // namespace rt

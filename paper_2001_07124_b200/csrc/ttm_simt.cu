@@ -1,0 +1,315 @@
+// ttm_simt.cu -- unfolding-free mode-n TTM kernels on CUDA cores (SIMT FFMA/DFMA).
+//
+// These are the portable baseline for the two TTM shapes of the hot path
+// (SURVEY.md §2.2 N1); the tcgen05 tensor-core kernels (ttm_tc.cu) replace the
+// X-streaming launches where they apply.
+//
+//   ttm_s:  Y(i,k) = sum_j X_(n)(i,j) B(j,k)      -- the sketch Y = X_(n) Omega
+//           (Eq. proj; Alg.6 line 3 P:556), the power-iteration product
+//           Y = X_(n) Z and Gram matrices of unfoldings.
+//   ttm_t:  out(alpha,c,beta) = sum_i X(alpha,i,beta) M(i,c)
+//           -- X x_n M^T (n-mode product P:109-112): Z = X_(n)^T Q, the core chain
+//           (Eq. Core), Kronecker sketch stages, STHOSVD shrink (Alg.8).
+//
+// X is read in place through the [a, I, b] box of kernels.h; nothing is permuted.
+#include "kernels.h"
+
+namespace rt {
+namespace {
+
+template <typename T> struct AccOf { using type = float; };
+template <> struct AccOf<double> { using type = double; };
+
+// ------------------------------------------------------------------ ttm_s
+// Block tile: BM = 128 rows i, BJ contraction columns j per stage, BN = 16*TN sketch cols.
+// 256 threads = 16 (k) x 16 (i); thread owns i in {ty + 16 r}, k in {tx + 16 c}.
+template <typename T, int TN, bool GRAM>
+__global__ void __launch_bounds__(256)
+ttm_s_kernel(const T* __restrict__ X, int64_t a, int64_t I, const T* __restrict__ Bm, int64_t bs_j,
+             int64_t bs_k, int K, int64_t J, int64_t jps, T* __restrict__ part) {
+  constexpr int BM = 128;
+  constexpr int BJ = sizeof(T) == 8 ? 16 : 32;
+  constexpr int BN = 16 * TN;
+  __shared__ T Xs[BJ][BM + 1];
+  __shared__ T Bs[GRAM ? 1 : BJ][BN];
+  const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
+  const int64_t i0 = int64_t(blockIdx.x) * BM;
+  const int k0 = blockIdx.y * BN;
+  const int64_t jb = int64_t(blockIdx.z) * jps;
+  const int64_t je = min(J, jb + jps);
+  const int64_t aI = a * I;
+  T acc[8][TN];
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int c = 0; c < TN; ++c) acc[r][c] = T(0);
+
+  for (int64_t jc = jb; jc < je; jc += BJ) {
+    if (a == 1) {                       // mode 0: X_(n)(i,j) = X[i + I*j], contiguous in i
+      const int il = t & 127;
+      const int64_t i = i0 + il;
+#pragma unroll
+      for (int s = 0; s < BJ / 2; ++s) {
+        const int jl = (t >> 7) + 2 * s;
+        const int64_t j = jc + jl;
+        Xs[jl][il] = (i < I && j < je) ? X[i + I * j] : T(0);
+      }
+    } else {                            // contiguous in alpha (= j within an alpha run)
+      const int jl = t % BJ;
+      const int64_t j = jc + jl;
+      const bool jv = j < je;
+      const int64_t off = jv ? (j % a) + aI * (j / a) : 0;
+#pragma unroll
+      for (int s = 0; s < BM * BJ / 256; ++s) {
+        const int il = t / BJ + (256 / BJ) * s;
+        const int64_t i = i0 + il;
+        Xs[jl][il] = (jv && i < I) ? X[off + a * i] : T(0);
+      }
+    }
+    if (!GRAM) {
+      if (bs_k == 1) {
+        for (int e = t; e < BJ * BN; e += 256) {
+          const int kl = e % BN, jl = e / BN;
+          const int64_t j = jc + jl;
+          const int k = k0 + kl;
+          Bs[jl][kl] = (j < je && k < K) ? Bm[j * bs_j + k] : T(0);
+        }
+      } else {
+        for (int e = t; e < BJ * BN; e += 256) {
+          const int jl = e % BJ, kl = e / BJ;
+          const int64_t j = jc + jl;
+          const int k = k0 + kl;
+          Bs[jl][kl] = (j < je && k < K) ? Bm[j * bs_j + int64_t(k) * bs_k] : T(0);
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int jj = 0; jj < BJ; ++jj) {
+      T xr[8], br[TN];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) xr[r] = Xs[jj][ty + 16 * r];
+#pragma unroll
+      for (int c = 0; c < TN; ++c) {
+        if (GRAM) {
+          const int k = k0 + tx + 16 * c;
+          br[c] = k < BM ? Xs[jj][k] : T(0);
+        } else {
+          br[c] = Bs[jj][tx + 16 * c];
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c = 0; c < TN; ++c) acc[r][c] = fma(xr[r], br[c], acc[r][c]);
+    }
+    __syncthreads();
+  }
+  T* dst = part + int64_t(blockIdx.z) * K * I;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int64_t i = i0 + ty + 16 * r;
+    if (i >= I) continue;
+#pragma unroll
+    for (int c = 0; c < TN; ++c) {
+      const int k = k0 + tx + 16 * c;
+      if (k < K) dst[int64_t(k) * I + i] = acc[r][c];
+    }
+  }
+}
+
+// Y(i + ldy*k) = sum_z part[z][k][i]  in fp64, fixed order (deterministic split-K reduce)
+template <typename T>
+__global__ void splitk_reduce_kernel(const T* __restrict__ part, int64_t I, int K, int splits,
+                                     double* __restrict__ Y, int64_t ldy) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= I * K) return;
+  const int64_t i = e % I, k = e / I;
+  double s = 0.0;
+  for (int z = 0; z < splits; ++z) s += double(part[(int64_t(z) * K + k) * I + i]);
+  Y[i + ldy * k] = s;
+}
+
+template <typename T, int TN>
+void launch_ttm_s(const Ctx& ctx, Arena& ws, const T* X, Box box, const T* Bm, int64_t bs_j,
+                  int64_t bs_k, int K, double* Y, int64_t ldy, bool gram) {
+  constexpr int BJ = sizeof(T) == 8 ? 16 : 32;
+  const int64_t J = box.J();
+  const int64_t itiles = cdiv(box.I, 128);
+  const int64_t ktiles = cdiv(K, 16 * TN);
+  const int64_t tiles = itiles * ktiles;
+  const int64_t target = 4LL * ctx.num_sms;
+  int64_t splits = std::max<int64_t>(1, cdiv(target, tiles));
+  splits = std::min<int64_t>(splits, std::max<int64_t>(1, cdiv(J, BJ * 8)));
+  splits = std::min<int64_t>(splits, 65535);
+  int64_t jps = cdiv(cdiv(J, splits), BJ) * BJ;
+  splits = cdiv(J, jps);
+  T* part = ws.alloc_n<T>(splits * K * box.I);
+  const dim3 grid((unsigned)itiles, (unsigned)ktiles, (unsigned)splits);
+  if (gram)
+    launch(ctx, "ttm_s_gram_simt", [&] {
+      ttm_s_kernel<T, TN, true><<<grid, 256, 0, ctx.stream>>>(X, box.a, box.I, Bm, bs_j, bs_k, K, J, jps, part);
+    });
+  else
+    launch(ctx, "ttm_s_simt", [&] {
+      ttm_s_kernel<T, TN, false><<<grid, 256, 0, ctx.stream>>>(X, box.a, box.I, Bm, bs_j, bs_k, K, J, jps, part);
+    });
+  const int64_t n = box.I * K;
+  launch(ctx, "splitk_reduce", [&] {
+    splitk_reduce_kernel<T><<<unsigned(cdiv(n, 256)), 256, 0, ctx.stream>>>(part, box.I, K, int(splits), Y, ldy);
+  });
+}
+
+// ------------------------------------------------------------------ ttm_t
+// Block tile: BM = 128 outputs j, BI contraction rows per stage, BN = 8*TN output cols c.
+// 256 threads = 32 (j, lanes) x 8 (c, warps); thread owns j in {tx + 32 r}, c in {ty + 8 cc}.
+template <typename Tin, typename Tm, typename Tout, int TN>
+__global__ void __launch_bounds__(256)
+ttm_t_kernel(const Tin* __restrict__ X, int64_t a, int64_t I, int64_t J, const Tm* __restrict__ Mm,
+             int64_t ms_i, int64_t ms_c, int C, Tout* __restrict__ out, int64_t so_a, int64_t so_c,
+             int64_t so_b) {
+  using Tacc = typename AccOf<Tin>::type;
+  constexpr int BM = 128;
+  constexpr int BI = sizeof(Tacc) == 8 ? 16 : 32;
+  constexpr int BN = 8 * TN;
+  __shared__ Tacc Xs[BI][BM + 1];
+  __shared__ Tacc Ms[BI][BN];
+  const int t = threadIdx.x, tx = t & 31, ty = t >> 5;
+  const int64_t j0 = int64_t(blockIdx.x) * BM;
+  const int c0 = blockIdx.y * BN;
+  const int64_t aI = a * I;
+  Tacc acc[4][TN];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < TN; ++c) acc[r][c] = Tacc(0);
+
+  // a > 1 loader: this thread always loads column jl = t & 127
+  const int jl_b = t & 127;
+  const int64_t j_b = j0 + jl_b;
+  const bool jv_b = j_b < J;
+  const int64_t off_b = jv_b ? (j_b % a) + aI * (j_b / a) : 0;
+
+  for (int64_t ic = 0; ic < I; ic += BI) {
+    if (a == 1) {                       // mode 0: X(j,i) = X[i + I*j], contiguous in i
+      const int il = t % BI;
+      const int64_t i = ic + il;
+#pragma unroll
+      for (int s = 0; s < BM * BI / 256; ++s) {
+        const int jl = t / BI + (256 / BI) * s;
+        const int64_t j = j0 + jl;
+        Xs[il][jl] = (j < J && i < I) ? Tacc(X[i + I * j]) : Tacc(0);
+      }
+    } else {
+#pragma unroll
+      for (int s = 0; s < BI / 2; ++s) {
+        const int il = (t >> 7) + 2 * s;
+        const int64_t i = ic + il;
+        Xs[il][jl_b] = (jv_b && i < I) ? Tacc(X[off_b + a * i]) : Tacc(0);
+      }
+    }
+    if (ms_c == 1) {
+      for (int e = t; e < BI * BN; e += 256) {
+        const int cl = e % BN, il = e / BN;
+        const int64_t i = ic + il;
+        const int c = c0 + cl;
+        Ms[il][cl] = (i < I && c < C) ? Tacc(Mm[i * ms_i + c]) : Tacc(0);
+      }
+    } else {
+      for (int e = t; e < BI * BN; e += 256) {
+        const int il = e % BI, cl = e / BI;
+        const int64_t i = ic + il;
+        const int c = c0 + cl;
+        Ms[il][cl] = (i < I && c < C) ? Tacc(Mm[i * ms_i + int64_t(c) * ms_c]) : Tacc(0);
+      }
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int ii = 0; ii < BI; ++ii) {
+      Tacc xr[4], mr[TN];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) xr[r] = Xs[ii][tx + 32 * r];
+#pragma unroll
+      for (int c = 0; c < TN; ++c) mr[c] = Ms[ii][ty + 8 * c];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < TN; ++c) acc[r][c] = fma(xr[r], mr[c], acc[r][c]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int64_t j = j0 + tx + 32 * r;
+    if (j >= J) continue;
+    const int64_t ob = (j % a) * so_a + (j / a) * so_b;
+#pragma unroll
+    for (int c = 0; c < TN; ++c) {
+      const int cc = c0 + ty + 8 * c;
+      if (cc < C) out[ob + int64_t(cc) * so_c] = Tout(acc[r][c]);
+    }
+  }
+}
+
+template <typename Tin, typename Tm, typename Tout, int TN>
+void launch_ttm_t(const Ctx& ctx, const Tin* X, Box box, const Tm* Mm, int64_t ms_i, int64_t ms_c, int C,
+                  Tout* out, int64_t so_a, int64_t so_c, int64_t so_b) {
+  const int64_t J = box.J();
+  const dim3 grid((unsigned)cdiv(J, 128), (unsigned)cdiv(C, 8 * TN));
+  RT_REQUIRE(grid.x < (1u << 31) && grid.y < 65536, kEUNSUPPORTED, "ttm_t grid too large");
+  launch(ctx, "ttm_t_simt", [&] {
+    ttm_t_kernel<Tin, Tm, Tout, TN><<<grid, 256, 0, ctx.stream>>>(X, box.a, box.I, J, Mm, ms_i, ms_c, C,
+                                                                  out, so_a, so_c, so_b);
+  });
+}
+
+}  // namespace
+
+template <typename T>
+void ttm_s(const Ctx& ctx, Arena& ws, const T* X, Box box, const T* Bm, int64_t bs_j, int64_t bs_k,
+           int K, double* Y, int64_t ldy, bool gram) {
+  if (box.J() == 0 || box.I == 0 || K == 0) {
+    for (int k = 0; k < K; ++k) RT_CUDA(cudaMemsetAsync(Y + ldy * k, 0, sizeof(double) * box.I, ctx.stream));
+    return;
+  }
+  if (gram) RT_REQUIRE(box.I <= 128 && K == box.I, kEUNSUPPORTED, "gram mode needs I <= 128");
+  if (K <= 16)       launch_ttm_s<T, 1>(ctx, ws, X, box, Bm, bs_j, bs_k, K, Y, ldy, gram);
+  else if (K <= 32)  launch_ttm_s<T, 2>(ctx, ws, X, box, Bm, bs_j, bs_k, K, Y, ldy, gram);
+  else if (K <= 48)  launch_ttm_s<T, 3>(ctx, ws, X, box, Bm, bs_j, bs_k, K, Y, ldy, gram);
+  else if (K <= 64)  launch_ttm_s<T, 4>(ctx, ws, X, box, Bm, bs_j, bs_k, K, Y, ldy, gram);
+  else if (K <= 80)  launch_ttm_s<T, 5>(ctx, ws, X, box, Bm, bs_j, bs_k, K, Y, ldy, gram);
+  else if (K <= 96)  launch_ttm_s<T, 6>(ctx, ws, X, box, Bm, bs_j, bs_k, K, Y, ldy, gram);
+  else               launch_ttm_s<T, 8>(ctx, ws, X, box, Bm, bs_j, bs_k, K, Y, ldy, gram);
+}
+
+template <typename Tin, typename Tm, typename Tout>
+void ttm_t(const Ctx& ctx, const Tin* X, Box box, const Tm* Mm, int64_t ms_i, int64_t ms_c, int C,
+           Tout* out, int64_t so_a, int64_t so_c, int64_t so_b) {
+  if (box.J() == 0 || C == 0) return;
+  if (box.I == 0) {
+    throw Error(kEINVAL, "ttm_t with empty contraction");
+  }
+  if (C <= 8)        launch_ttm_t<Tin, Tm, Tout, 1>(ctx, X, box, Mm, ms_i, ms_c, C, out, so_a, so_c, so_b);
+  else if (C <= 16)  launch_ttm_t<Tin, Tm, Tout, 2>(ctx, X, box, Mm, ms_i, ms_c, C, out, so_a, so_c, so_b);
+  else if (C <= 32)  launch_ttm_t<Tin, Tm, Tout, 4>(ctx, X, box, Mm, ms_i, ms_c, C, out, so_a, so_c, so_b);
+  else if (C <= 48)  launch_ttm_t<Tin, Tm, Tout, 6>(ctx, X, box, Mm, ms_i, ms_c, C, out, so_a, so_c, so_b);
+  else if (C <= 64)  launch_ttm_t<Tin, Tm, Tout, 8>(ctx, X, box, Mm, ms_i, ms_c, C, out, so_a, so_c, so_b);
+  else if (C <= 80)  launch_ttm_t<Tin, Tm, Tout, 10>(ctx, X, box, Mm, ms_i, ms_c, C, out, so_a, so_c, so_b);
+  else if (C <= 96)  launch_ttm_t<Tin, Tm, Tout, 12>(ctx, X, box, Mm, ms_i, ms_c, C, out, so_a, so_c, so_b);
+  else               launch_ttm_t<Tin, Tm, Tout, 16>(ctx, X, box, Mm, ms_i, ms_c, C, out, so_a, so_c, so_b);
+}
+
+template void ttm_s<float>(const Ctx&, Arena&, const float*, Box, const float*, int64_t, int64_t, int,
+                           double*, int64_t, bool);
+template void ttm_s<double>(const Ctx&, Arena&, const double*, Box, const double*, int64_t, int64_t, int,
+                            double*, int64_t, bool);
+template void ttm_t<float, float, float>(const Ctx&, const float*, Box, const float*, int64_t, int64_t, int,
+                                         float*, int64_t, int64_t, int64_t);
+template void ttm_t<float, float, double>(const Ctx&, const float*, Box, const float*, int64_t, int64_t, int,
+                                          double*, int64_t, int64_t, int64_t);
+template void ttm_t<double, double, double>(const Ctx&, const double*, Box, const double*, int64_t, int64_t,
+                                            int, double*, int64_t, int64_t, int64_t);
+template void ttm_t<double, double, float>(const Ctx&, const double*, Box, const double*, int64_t, int64_t,
+                                           int, float*, int64_t, int64_t, int64_t);
+
+}  // namespace rt
