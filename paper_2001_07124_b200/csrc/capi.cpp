@@ -68,14 +68,16 @@ rt::TView check_tensor(const rt_tensor* X) {
   return v;
 }
 
-void check_gauss_omega(const rt::TView& X, int n, const void* om, int64_t K) {
+// strict: K_n <= min(I_n, J_n) (needed by the thin QR); a bare sketch (q = 0) accepts any K <= 128
+void check_gauss_omega(const rt::TView& X, int n, const void* om, int64_t K, bool strict = true) {
   RT_REQUIRE(om != nullptr && aligned16(om), rt::kEINVAL, "Omega_n must be a 16-byte aligned device pointer");
   RT_REQUIRE(K >= 1, rt::kEINVAL, "omega_cols must be >= 1");
-  RT_REQUIRE(K <= X.Ig(n) && K <= X.Jg(n), rt::kERANK, "K_n must be <= min(I_n, J_n)");
+  RT_REQUIRE(!strict || (K <= X.Ig(n) && K <= X.Jg(n)), rt::kERANK, "K_n must be <= min(I_n, J_n)");
   RT_REQUIRE(K <= 128, rt::kEUNSUPPORTED, "K_n > 128 not supported");
 }
 
-int64_t check_kron_omega(const rt::TView& X, int n, const void* const* om, const int64_t* cols) {
+int64_t check_kron_omega(const rt::TView& X, int n, const void* const* om, const int64_t* cols,
+                         bool strict = true) {
   int64_t K = 1;
   for (int k = 0; k < X.N; ++k) {
     if (k == n) continue;
@@ -83,7 +85,7 @@ int64_t check_kron_omega(const rt::TView& X, int n, const void* const* om, const
     RT_REQUIRE(cols[k] >= 1, rt::kEINVAL, "Kronecker widths must be >= 1");
     K *= cols[k];
   }
-  RT_REQUIRE(K <= X.Ig(n), rt::kERANK, "Kronecker sketch width prod L_k must be <= I_n");
+  RT_REQUIRE(!strict || K <= X.Ig(n), rt::kERANK, "Kronecker sketch width prod L_k must be <= I_n");
   RT_REQUIRE(K <= 128, rt::kEUNSUPPORTED, "Kronecker sketch width > 128 not supported");
   return K;
 }
@@ -230,8 +232,8 @@ rt_status rtucker_sketch(rt_handle* h, const rt_tensor* X, int mode, rt_omega_ki
     RT_REQUIRE(!(v.sharded() && !eng.dist() && q > 0), rt::kEINVAL,
                "power iterations on a slab need a communicator");
     int64_t K;
-    if (kind == RT_OMEGA_GAUSS) { K = omega_cols[mode]; check_gauss_omega(v, mode, omega[mode], K); }
-    else if (kind == RT_OMEGA_KRON) K = check_kron_omega(v, mode, omega, omega_cols);
+    if (kind == RT_OMEGA_GAUSS) { K = omega_cols[mode]; check_gauss_omega(v, mode, omega[mode], K, q > 0); }
+    else if (kind == RT_OMEGA_KRON) K = check_kron_omega(v, mode, omega, omega_cols, q > 0);
     else throw rt::Error(rt::kEINVAL, "unknown omega kind");
     const int64_t In = v.d[mode];
     double* Yt = (ldy == In) ? Y : h->ws.alloc_n<double>(In * K);

@@ -316,8 +316,8 @@ def test_invalid_arguments(P, h):
     with pytest.raises(RtError) as e:
         P.rtucker_sketch(h, x, 3, om)
     assert e.value.status == -1
-    with pytest.raises(RtError) as e:            # K > I_n
-        P.rtucker_sketch(h, x, 0, om_dev(np.zeros((72, 11), dtype=np.float32)))
+    with pytest.raises(RtError) as e:            # K > I_n with power iterations (QR needs K <= I_n)
+        P.rtucker_sketch(h, x, 0, om_dev(np.zeros((72, 11), dtype=np.float32)), q=1)
     assert e.value.status == -2
     with pytest.raises(RtError) as e:            # R_n > K_n
         P.rtucker_hosvd(h, x, (6, 2, 2), 0, 0, [om, om_dev(np.zeros((80, 2), np.float32)),
