@@ -187,9 +187,10 @@ def rtucker_sketch(h: Handle, X: torch.Tensor, mode: int, omega, q: int = 0, kin
     if kind == "gauss":
         om = omega.contiguous()
         ptrs = [None] * N
-        ptrs[mode] = om
         cols = [0] * N
-        cols[mode] = om.shape[1]
+        if 0 <= mode < N:              # out-of-range modes are rejected by the library (RT_EINVAL)
+            ptrs[mode] = om
+            cols[mode] = om.shape[1]
         keep = [om]
         K = om.shape[1]
     else:
@@ -202,7 +203,7 @@ def rtucker_sketch(h: Handle, X: torch.Tensor, mode: int, omega, q: int = 0, kin
             ptrs[k] = o
             cols[k] = o.shape[1]
             K *= o.shape[1]
-    In = desc.dims[mode]
+    In = desc.dims[mode] if 0 <= mode < N else 1
     Y = new_colmajor(In, K, device=X.device)
     st = lib.rtucker_sketch(h.ptr, C.byref(desc), mode, _kind(kind), _ptr_array(ptrs), _i64_array(cols), q,
                             C.c_void_p(Y.data_ptr()), In)

@@ -253,7 +253,7 @@ def test_sthosvd_gauss_power_order(P, h):
 
 
 def test_hosvd_kron_power(P, h):
-    cfg = dataclasses.replace(synth.CONFIGS["cfg3"].scaled((30, 28, 26, 24), (5, 5, 5, 5), (5, 5, 5, 5)), q=1)
+    cfg = dataclasses.replace(synth.CONFIGS["cfg3"].scaled((34, 32, 30, 28), (5, 5, 5, 5), (5, 5, 5, 5)), q=1)
     x = synth.make_tensor(cfg)
     oms = _omegas_for(cfg, "kron")
     ref = oracle.hosvd(x, cfg.ranks, oms, q=1, kind="kron")
