@@ -177,6 +177,16 @@ def gaussian_omega(cfg: Config, n: int, K: Optional[int] = None, rows: Optional[
     return np.ascontiguousarray(om.astype(cfg.np_dtype))
 
 
+def round_tf32(a: np.ndarray) -> np.ndarray:
+    """Round fp32/fp64 values to the nearest tf32 value (10-bit mantissa, ties to even), returned
+    as float32.  Used to make Gaussian Omega tf32-exact BEFORE it is handed to both
+    the oracle and the CUDA path, which then skips the A_hi * Omega_lo product."""
+    u = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    lsb = (u >> np.uint64(13)) & np.uint64(1)
+    u = (u + np.uint64(0x0FFF) + lsb) & np.uint64(0xFFFFE000)
+    return u.astype(np.uint32).view(np.float32).reshape(np.shape(a))
+
+
 def kron_widths(cfg: Config, n: int) -> list:
     """Reading R3: uniform L = ceil((R_n+p)^(1/(N-1))) per other mode."""
     L = int(math.ceil((cfg.ranks[n] + cfg.p) ** (1.0 / (cfg.order - 1)) - 1e-12))

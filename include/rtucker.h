@@ -94,10 +94,14 @@ const char* rt_last_error(const rt_handle* h);
  * failure was latched since the last rt_sync (the latch is cleared). */
 rt_status rt_sync(rt_handle* h);
 
-/* Options (testing / A-B measurement).  RT_OPT_TTM_IMPL: 0 auto, 1 CUDA-core (SIMT)
- * TTM kernels, 2 tcgen05 tensor-core TTM kernels.  RT_OPT_PROFILE: 1 records a CUDA
- * event pair around every launch (read with rt_profile_read). */
-typedef enum { RT_OPT_TTM_IMPL = 0, RT_OPT_PROFILE = 1, RT_OPT_QR_FALLBACK = 2 } rt_option;
+/* Options.  RT_OPT_TTM_IMPL: 0 auto (tcgen05 where the shape fits the TMA path, else CUDA
+ * cores), 1 CUDA-core (SIMT) TTM kernels only, 2 tcgen05 only (RT_EUNSUPPORTED where it does
+ * not apply).  RT_OPT_PROFILE: 1 records a CUDA event pair around every launch (read with
+ * rt_profile_read).  RT_OPT_OMEGA_TF32: 1 = the caller guarantees every Gaussian Omega entry
+ * is exactly representable in tf32 (e.g. rounded on the host before it is given to both the
+ * oracle and this library); the sketch then skips the A_hi*Omega_lo product of the 3xTF32
+ * split.  RT_OPT_QR_FALLBACK is reserved. */
+typedef enum { RT_OPT_TTM_IMPL = 0, RT_OPT_PROFILE = 1, RT_OPT_QR_FALLBACK = 2, RT_OPT_OMEGA_TF32 = 3 } rt_option;
 rt_status rt_set_option(rt_handle* h, rt_option opt, int64_t value);
 
 /* Profile of the launches recorded since the last read (synchronizes the stream).

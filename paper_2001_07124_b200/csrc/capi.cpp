@@ -90,8 +90,6 @@ int64_t check_kron_omega(const rt::TView& X, int n, const void* const* om, const
   return K;
 }
 
-// rows of Omega_n expected for the local slab
-int64_t local_J(const rt::TView& X, int n) { int64_t s = 1; for (int k = 0; k < X.N; ++k) if (k != n) s *= X.d[k]; return s; }
 
 }  // namespace
 
@@ -185,6 +183,7 @@ rt_status rt_set_option(rt_handle* h, rt_option opt, int64_t value) {
     case RT_OPT_TTM_IMPL: h->ctx.ttm_impl = int(value); return RT_OK;
     case RT_OPT_PROFILE: h->prof.enabled = value != 0; return RT_OK;
     case RT_OPT_QR_FALLBACK: return RT_OK;
+    case RT_OPT_OMEGA_TF32: h->ctx.omega_tf32 = int(value != 0); return RT_OK;
   }
   return fail(h, RT_EINVAL, "unknown option");
 }

@@ -65,7 +65,8 @@ struct Ctx {
   int* d_status = nullptr;      // device status latch
   Profiler* prof = nullptr;
   int num_sms = 148;
-  int ttm_impl = 0;             // 0 auto, 1 SIMT, 2 tcgen05
+  int ttm_impl = 0;             // 0 auto, 1 SIMT, 2 tcgen05 (error if unavailable)
+  int omega_tf32 = 0;           // caller asserts Gaussian Omega entries are tf32-representable
 };
 
 // Launch a kernel (given as a lambda issuing <<<...>>> on ctx.stream) with optional

@@ -25,6 +25,16 @@ template <typename Tin, typename Tm, typename Tout>
 void ttm_t(const Ctx& ctx, const Tin* X, Box box, const Tm* Mm, int64_t ms_i, int64_t ms_c, int C,
            Tout* out, int64_t so_a, int64_t so_c, int64_t so_b);
 
+// tcgen05 tensor-core versions (ttm_tc.cu), fp32 only, 3xTF32 split.  Return false (nothing
+// launched) when the shape/alignment is outside the TMA path; callers then use the SIMT kernels.
+// B: row-major (element (j,k) at j*ldb + k, ldb % 4 == 0, pad columns zero) or col-major (element
+// (j,k) at j + ldb*k, ldb % 4 == 0, pad rows zero).  b_tf32_exact drops the A_hi*B_lo product.
+bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Bm, int64_t ldb, bool b_rowmajor,
+              bool b_tf32_exact, int K, double* Y, int64_t ldy);
+// out(alpha,c,beta) = sum_i X(alpha,i,beta) Q(i,c), Q col-major with ldq % 4 == 0 (pad rows zero)
+bool ttm_t_tc(const Ctx& ctx, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
+              int64_t so_a, int64_t so_c, int64_t so_b);
+
 // Gram of a col-major m x k matrix (fp64 out, k x k), partials reduced in fixed order.
 template <typename T>
 void gram(const Ctx& ctx, Arena& ws, const T* A, int64_t m, int k, int64_t lda, double* G);

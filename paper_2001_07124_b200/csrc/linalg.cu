@@ -628,6 +628,7 @@ void convert2d(const Ctx& ctx, const Ti* in, int64_t m, int64_t n, int64_t ldi, 
 template void convert2d<double, float>(const Ctx&, const double*, int64_t, int64_t, int64_t, float*, int64_t);
 template void convert2d<double, double>(const Ctx&, const double*, int64_t, int64_t, int64_t, double*, int64_t);
 template void convert2d<float, double>(const Ctx&, const float*, int64_t, int64_t, int64_t, double*, int64_t);
+template void convert2d<float, float>(const Ctx&, const float*, int64_t, int64_t, int64_t, float*, int64_t);
 
 template <typename T>
 void unfold_copy(const Ctx& ctx, const T* Tt, Box box, double* out, int64_t ldo) {

@@ -8,6 +8,7 @@
 //   C4  core G~: per-slab partial sums -> allreduce
 //   C5  residual sums -> allreduce;  sign candidates of the row-distributed last factor -> allgather
 #include <cmath>
+#include <type_traits>
 
 #include "engine.h"
 
@@ -23,6 +24,45 @@ template <> struct DT<double> { static constexpr int id = 1; };
 template <typename T>
 void allreduce(Comm* c, bool on, T* p, int64_t n, cudaStream_t s) {
   if (on && n > 0) c->allreduce_sum(p, size_t(n), s);
+}
+
+int64_t pad4(int64_t x) { return (x + 3) & ~int64_t(3); }
+
+// Y = X_(n) B: tcgen05 3xTF32 kernel for fp32 data when the shape fits the TMA path, else SIMT.
+void ttm_s_dispatch(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B, int64_t ldb, bool rowmajor,
+                    bool exact, int K, double* Y, int64_t ldy) {
+  if (ctx.ttm_impl != 1 && ttm_s_tc(ctx, ws, X, box, B, ldb, rowmajor, exact, K, Y, ldy)) return;
+  RT_REQUIRE(ctx.ttm_impl != 2, kEUNSUPPORTED, "tcgen05 ttm_s path unavailable for this shape");
+  ttm_s<float>(ctx, ws, X, box, B, rowmajor ? ldb : 1, rowmajor ? 1 : ldb, K, Y, ldy);
+}
+void ttm_s_dispatch(const Ctx& ctx, Arena& ws, const double* X, Box box, const double* B, int64_t ldb, bool rowmajor,
+                    bool, int K, double* Y, int64_t ldy) {
+  ttm_s<double>(ctx, ws, X, box, B, rowmajor ? ldb : 1, rowmajor ? 1 : ldb, K, Y, ldy);
+}
+// out(alpha,c,beta) = sum_i X(alpha,i,beta) Q(i,c), Q col-major (ldq)
+void ttm_t_dispatch(const Ctx& ctx, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
+                    int64_t so_a, int64_t so_c, int64_t so_b) {
+  if (ctx.ttm_impl != 1 && ttm_t_tc(ctx, X, box, Q, ldq, C, out, so_a, so_c, so_b)) return;
+  RT_REQUIRE(ctx.ttm_impl != 2, kEUNSUPPORTED, "tcgen05 ttm_t path unavailable for this shape");
+  ttm_t<float, float, float>(ctx, X, box, Q, 1, ldq, C, out, so_a, so_c, so_b);
+}
+void ttm_t_dispatch(const Ctx& ctx, const double* X, Box box, const double* Q, int64_t ldq, int C, double* out,
+                    int64_t so_a, int64_t so_c, int64_t so_b) {
+  ttm_t<double, double, double>(ctx, X, box, Q, 1, ldq, C, out, so_a, so_c, so_b);
+}
+
+// fp64 col-major m x k -> working-type copy with ld padded to a multiple of 4 (pad rows zero)
+template <typename T>
+T* working_copy(const Ctx& ctx, Arena& ws, const double* Q, int64_t m, int64_t k, int64_t ldq, int64_t& ld_out) {
+  if (std::is_same<T, double>::value) {
+    ld_out = ldq;
+    return const_cast<T*>(reinterpret_cast<const T*>(Q));
+  }
+  ld_out = pad4(m);
+  T* c = ws.alloc_n<T>(ld_out * k);
+  if (ld_out != m) fill_zero(ctx, c, sizeof(T) * ld_out * k);
+  convert2d<double, T>(ctx, Q, m, k, ldq, c, ld_out);
+  return c;
 }
 }  // namespace
 
@@ -71,17 +111,17 @@ void Engine::qr_y(const double* Y, int64_t m, int64_t m_glob, int k, int64_t ldy
 // Z only conditions the next product Y = X_(n) Z (span(X Z R^-1) = span(X Z)); a single
 // CholeskyQR step with a small safety shift keeps it well conditioned.
 template <typename T>
-void Engine::qr_z(T* Z, int64_t m, int64_t m_glob, int k, bool rows_dist, int64_t row0) {
+void Engine::qr_z(T* Z, int64_t m, int64_t ldz, int64_t m_glob, int k, bool rows_dist, int64_t row0) {
   const auto mk = ws.mark();
   double* G = ws.alloc_n<double>(int64_t(k) * k);
   double* Rr = ws.alloc_n<double>(int64_t(k) * k);
   double* Ri = ws.alloc_n<double>(int64_t(k) * k);
   int* zero = ws.alloc_n<int>(1);
-  gram<T>(ctx, ws, Z, m, k, m, G);
+  gram<T>(ctx, ws, Z, m, k, ldz, G);
   allreduce(comm, rows_dist && dist(), G, int64_t(k) * k, ctx.stream);
   (void)m_glob;
   chol_inv(ctx, G, k, 1e-13, Rr, Ri, zero);
-  gemm_tall<T, T>(ctx, Z, m, k, m, Ri, k, k, Z, m, zero, row0);
+  gemm_tall<T, T>(ctx, Z, m, k, ldz, Ri, k, k, Z, ldz, zero, row0);
   ws.rewind(mk);
 }
 
@@ -96,7 +136,17 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
   int K;
   if (kind == 0) {
     K = int(omega_cols[n]);
-    ttm_s<T>(ctx, ws, data, bx, static_cast<const T*>(omega[n]), K, 1, K, Yt, In);
+    const T* om = static_cast<const T*>(omega[n]);
+    int64_t ldo = K;
+    if (std::is_same<T, float>::value && (K % 4) && ctx.ttm_impl != 1) {
+      // TMA needs 16-byte row pitch: zero-padded copy of Omega_n (J x pad4(K), row-major)
+      ldo = pad4(K);
+      T* omp = ws.alloc_n<T>(bx.J() * ldo);
+      fill_zero(ctx, omp, sizeof(T) * bx.J() * ldo);
+      convert2d<T, T>(ctx, om, K, bx.J(), K, omp, ldo);
+      om = omp;
+    }
+    ttm_s_dispatch(ctx, ws, data, bx, om, ldo, /*rowmajor=*/true, ctx.omega_tf32 != 0, K, Yt, In);
   } else {
     // Kronecker sketch W = X x_{k!=n} Omega_k^T (Eq.(2)): a chain of TTMs whose first
     // stage streams X and whose later stages run on the shrunken result.
@@ -106,18 +156,14 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
     for (int k = 0; k < N; ++k) if (k != n) K *= int(omega_cols[k]);
     const auto mk = ws.mark();
     const T* src = data;
-    T* bufs[2] = {nullptr, nullptr};
-    int which = 0;
     for (int k = 0; k < N; ++k) {
       if (k == n) continue;
       const Box b = TView::box_of(cur, N, k);
       const int L = int(omega_cols[k]);
       T* dst = ws.alloc_n<T>(b.a * L * b.b);
-      bufs[which] = dst;
       ttm_t<T, T, T>(ctx, src, b, static_cast<const T*>(omega[k]), L, 1, L, dst, 1, b.a, b.a * L);
       src = dst;
       cur[k] = L;
-      which ^= 1;
     }
     unfold_copy<T>(ctx, src, TView::box_of(cur, N, n), Yt, In);
     ws.rewind(mk);   // the Y result is in Yt; intermediates are dead (stream order)
@@ -129,15 +175,19 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
   const auto mk = ws.mark();
   const int64_t Jl = bx.J();
   double* Qy = ws.alloc_n<double>(In * K);
-  T* QyT = (DT<T>::id == 1) ? reinterpret_cast<T*>(Qy) : ws.alloc_n<T>(In * K);
-  T* Z = ws.alloc_n<T>(Jl * K);
+  const int64_t ldz = pad4(Jl);            // 16-byte column pitch for the TMA path; pad rows zero
+  T* Z = ws.alloc_n<T>(ldz * K);
+  if (ldz != Jl) fill_zero(ctx, Z, sizeof(T) * ldz * K);
   const int64_t row0_last = X.off;
   for (int it = 0; it < q; ++it) {
     qr_y(Yt, In, X.Ig(n), K, In, Qy, In, nullptr, last && dist(), last ? row0_last : 0);
-    if (DT<T>::id == 0) convert2d<double, T>(ctx, Qy, In, K, In, QyT, In);
-    // Z(j, c) = sum_i X_(n)(i, j) Q(i, c), written col-major J x K: so_a=1, so_c=J, so_b=a
-    ttm_t<T, T, T>(ctx, data, bx, QyT, 1, In, K, Z, 1, Jl, bx.a);
-    allreduce(comm, last && dist(), Z, Jl * K, ctx.stream);                      // C3
+    const auto mq = ws.mark();
+    int64_t ldqt;
+    const T* QyT = working_copy<T>(ctx, ws, Qy, In, K, In, ldqt);
+    // Z(j, c) = sum_i X_(n)(i, j) Q(i, c), written col-major J x K: so_a=1, so_c=ldz, so_b=a
+    ttm_t_dispatch(ctx, data, bx, QyT, ldqt, K, Z, 1, ldz, bx.a);
+    ws.rewind(mq);
+    allreduce(comm, last && dist(), Z, ldz * K, ctx.stream);                     // C3
     // local Z rows: for n < N-1 the slab's j's are the contiguous block starting at a*b'*off
     int64_t zrow0 = 0;
     if (!last) {
@@ -145,8 +195,8 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
       for (int k = n + 1; k < N - 1; ++k) bp *= X.d[k];
       zrow0 = bx.a * bp * X.off;
     }
-    qr_z<T>(Z, Jl, X.Jg(n), K, !last && dist(), zrow0);
-    ttm_s<T>(ctx, ws, data, bx, Z, 1, Jl, K, Yt, In);
+    qr_z<T>(Z, Jl, ldz, X.Jg(n), K, !last && dist(), zrow0);
+    ttm_s_dispatch(ctx, ws, data, bx, Z, ldz, /*rowmajor=*/false, false, K, Yt, In);
     allreduce(comm, !last && dist(), Yt, In * K, ctx.stream);                     // C1
   }
   ws.rewind(mk);
@@ -159,23 +209,19 @@ void Engine::core(const TView& X, const T* data, const double* const* Qt, const 
   const int N = X.N;
   const auto mk = ws.mark();
   const T* QT[5];
-  for (int n = 0; n < N; ++n) {
-    if (DT<T>::id == 1) { QT[n] = reinterpret_cast<const T*>(Qt[n]); continue; }
-    T* c = ws.alloc_n<T>(X.d[n] * K[n]);
-    convert2d<double, T>(ctx, Qt[n], X.d[n], K[n], ldq[n], c, X.d[n]);
-    QT[n] = c;
-  }
+  int64_t ldt[5];
+  for (int n = 0; n < N; ++n) QT[n] = working_copy<T>(ctx, ws, Qt[n], X.d[n], K[n], ldq[n], ldt[n]);
   int64_t cur[5];
   for (int k = 0; k < N; ++k) cur[k] = X.d[k];
   const T* src = data;
   for (int n = 0; n < N; ++n) {
     const Box b = TView::box_of(cur, N, n);
-    const int64_t ld = (DT<T>::id == 1) ? ldq[n] : X.d[n];
+    const int64_t ld = ldt[n];
     if (n == N - 1) {
       ttm_t<T, T, double>(ctx, src, b, QT[n], 1, ld, int(K[n]), Gt, 1, b.a, b.a * K[n]);
     } else {
       T* dst = ws.alloc_n<T>(b.a * K[n] * b.b);
-      ttm_t<T, T, T>(ctx, src, b, QT[n], 1, ld, int(K[n]), dst, 1, b.a, b.a * K[n]);
+      ttm_t_dispatch(ctx, src, b, QT[n], ld, int(K[n]), dst, 1, b.a, b.a * K[n]);
       src = dst;
     }
     cur[n] = K[n];
@@ -342,12 +388,12 @@ void Engine::sthosvd(const TView& X, const int64_t* R, int q, int kind, const vo
     sketch<T>(S, sdata, n, kind, om, oc, q, Yt);
     double* Qt = ws.alloc_n<double>(In * K);
     qr_y(Yt, In, In, K, In, Qt, In, nullptr, false, 0);
-    T* QtT = (DT<T>::id == 1) ? reinterpret_cast<T*>(Qt) : ws.alloc_n<T>(In * K);
-    if (DT<T>::id == 0) convert2d<double, T>(ctx, Qt, In, K, In, QtT, In);
+    int64_t ldqt;
+    const T* QtT = working_copy<T>(ctx, ws, Qt, In, K, In, ldqt);
     // Alg.1 line 4: B = S x_n Q~^T
     const Box bs = S.box(n);
     T* B = ws.alloc_n<T>(bs.a * K * bs.b);
-    ttm_t<T, T, T>(ctx, sdata, bs, QtT, 1, In, K, B, 1, bs.a, bs.a * K);
+    ttm_t_dispatch(ctx, sdata, bs, QtT, ldqt, K, B, 1, bs.a, bs.a * K);
     // Alg.1 lines 5-7 via the Gram-EVD of B_(n): U = top-R_n eigenvectors, Q_n = Q~ U
     const Box bb{bs.a, K, bs.b};
     double* M = ws.alloc_n<double>(int64_t(K) * K);
@@ -379,6 +425,8 @@ template void Engine::sketch<float>(const TView&, const float*, int, int, const 
                                     double*);
 template void Engine::sketch<double>(const TView&, const double*, int, int, const void* const*, const int64_t*,
                                      int, double*);
+template void Engine::qr_z<float>(float*, int64_t, int64_t, int64_t, int, bool, int64_t);
+template void Engine::qr_z<double>(double*, int64_t, int64_t, int64_t, int, bool, int64_t);
 template void Engine::qr_rows<float>(const float*, int64_t, int64_t, int, int64_t, double*, int64_t, double*,
                                      bool, int64_t);
 template void Engine::qr_rows<double>(const double*, int64_t, int64_t, int, int64_t, double*, int64_t, double*,

@@ -1,0 +1,164 @@
+"""Parity of the tcgen05 (3xTF32, TMEM, TMA) TTM kernels, forced with RT_OPT_TTM_IMPL = 2,
+against the fp64 oracle.  Tolerances as in test_gpu_parity (BASELINE north_star 1e-5)."""
+import dataclasses
+
+import numpy as np
+import pytest
+
+import oracle
+from gen import synth
+from tests import _metrics as M
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2001_07124_b200 import api
+    return api
+
+
+def _handle(P, impl=2, omega_tf32=False):
+    from paper_2001_07124_b200 import _lib as L
+    h = P.Handle()
+    h.set_option(L.RT_OPT_TTM_IMPL, impl)
+    h.set_option(L.RT_OPT_OMEGA_TF32, int(omega_tf32))
+    return h
+
+
+@pytest.fixture(scope="module")
+def htc(P):
+    h = _handle(P, 2)
+    yield h
+    h.close()
+
+
+def dev(x):
+    return torch.from_numpy(synth.to_device_layout(x)).cuda()
+
+
+def om_dev(om):
+    return torch.from_numpy(np.ascontiguousarray(om)).cuda()
+
+
+def mat(t):
+    return t.detach().cpu().numpy()
+
+
+@pytest.mark.parametrize("dims,K", [((128, 96, 64), 80), ((500, 500, 40), 30), ((256, 36, 20, 12), 16),
+                                    ((1024, 200), 64), ((132, 68, 260), 128)])
+def test_tc_sketch_parity(P, htc, dims, K):
+    x = np.asfortranarray(np.random.default_rng(1).standard_normal(dims).astype(np.float32))
+    X = dev(x)
+    rng = np.random.default_rng(2)
+    for n in range(len(dims)):
+        J = x.size // dims[n]
+        om = rng.standard_normal((J, K)).astype(np.float32)
+        y = mat(P.rtucker_sketch(htc, X, n, om_dev(om)))
+        y0, _ = oracle.sketch_gauss(x, n, om, 0)
+        err = M.rel_fro(y, y0)
+        assert err <= 1e-5, (n, err)
+    htc.sync()
+
+
+def test_tc_sketch_tf32_exact_omega(P):
+    """RT_OPT_OMEGA_TF32: with a host-rounded (tf32-exact) Omega the 2-product path is exact to fp32."""
+    h = _handle(P, 2, omega_tf32=True)
+    dims = (256, 128, 96)
+    x = np.asfortranarray(np.random.default_rng(3).standard_normal(dims).astype(np.float32))
+    X = dev(x)
+    for n in range(3):
+        om = synth.round_tf32(np.random.default_rng(4 + n).standard_normal((x.size // dims[n], 80)))
+        y = mat(P.rtucker_sketch(h, X, n, om_dev(om)))
+        y0, _ = oracle.sketch_gauss(x, n, om, 0)
+        assert M.rel_fro(y, y0) <= 1e-5
+    h.sync()
+    h.close()
+
+
+def test_tc_long_contraction_precision(P, htc):
+    """Accumulation precision over a long contraction (J = 2^20): the TMEM fp32 accumulator is
+    drained every 1024 contraction elements into fp32 registers, split-K partials reduced in fp64."""
+    dims = (256, 1024, 1024)
+    x = np.asfortranarray(np.random.default_rng(5).standard_normal(dims).astype(np.float32))
+    X = dev(x)
+    for n in (0, 2):
+        J = x.size // dims[n]
+        om = np.random.default_rng(6).standard_normal((J, 80)).astype(np.float32)
+        y = mat(P.rtucker_sketch(htc, X, n, om_dev(om)))
+        y0 = oracle.unfold(x.astype(np.float64), n) @ om.astype(np.float64)
+        err = M.rel_fro(y, y0)
+        print(f"mode {n}: long-contraction rel err {err:.3e}")
+        assert err <= 2e-6
+    htc.sync()
+
+
+@pytest.mark.parametrize("q", [1, 2])
+def test_tc_power_iteration(P, htc, q):
+    cfg = synth.CONFIGS["cfg2"].scaled((128, 100, 84), (8, 8, 8), (8, 8, 8))
+    x = synth.make_tensor(cfg)
+    X = dev(x)
+    for n in range(3):
+        om = synth.gaussian_omega(cfg, n, K=16)
+        y = mat(P.rtucker_sketch(htc, X, n, om_dev(om), q=q))
+        _, yo = oracle.sketch_gauss(x, n, om, q)
+        ug = np.linalg.svd(y, full_matrices=False)[0][:, :8]
+        uo = np.linalg.svd(yo, full_matrices=False)[0][:, :8]
+        assert M.subspace(ug, uo) <= 1e-5
+    htc.sync()
+
+
+@pytest.mark.parametrize("dims,C", [((128, 96, 64), (80, 16, 32)), ((500, 500, 40), (30, 30, 20))])
+def test_tc_core_parity(P, htc, dims, C):
+    x = np.asfortranarray(np.random.default_rng(7).standard_normal(dims).astype(np.float32))
+    rng = np.random.default_rng(8)
+    qs = [np.linalg.qr(rng.standard_normal((d, c)))[0] for d, c in zip(dims, C)]
+    G, err = P.rtucker_core(htc, dev(x), [torch.from_numpy(q).cuda() for q in qs])
+    htc.sync()
+    go = oracle.core(x, qs)
+    assert M.rel_fro(P.core_to_numpy(G), go) <= 1e-5
+    assert abs(mat(err)[0] - oracle.rel_error(x, go, qs)) / oracle.rel_error(x, go, qs) <= 1e-5
+
+
+@pytest.mark.parametrize("name,dims,core,ranks", [
+    ("cfg5", (160, 152, 144), (40, 40, 40), (40, 40, 40)),
+    ("cfg4", (320, 288, 64), (100, 100, 50), (30, 30, 12)),
+    ("cfg2", (200, 180, 160), (20, 20, 20), (20, 20, 20)),
+])
+def test_tc_hosvd_parity(P, htc, name, dims, core, ranks):
+    cfg = synth.CONFIGS[name].scaled(dims, core, ranks)
+    x = synth.make_tensor(cfg)
+    oms = [synth.gaussian_omega(cfg, n) for n in range(3)]
+    ref = oracle.hosvd(x, cfg.ranks, oms, q=cfg.q)
+    res = P.rtucker_hosvd(htc, dev(x), cfg.ranks, cfg.p, cfg.q, [om_dev(o) for o in oms])
+    htc.sync()
+    qg = [mat(q) for q in res["Q"]]
+    gg = P.core_to_numpy(res["G"])
+    for n in range(3):
+        assert M.orth(qg[n]) <= 1e-12
+        assert M.subspace(qg[n], ref["Q"][n]) <= 1e-5, (n, M.subspace(qg[n], ref["Q"][n]))
+    assert M.core_in_oracle_basis(gg, qg, ref["G"], ref["Q"]) <= 1e-5
+    assert M.recon(gg, qg, ref["G"], ref["Q"]) <= 1e-5
+    e = mat(res["err"])[0]
+    assert abs(e - ref["E"]) / ref["E"] <= 1e-5
+
+
+def test_tc_sthosvd_shrink(P, htc):
+    cfg = dataclasses.replace(synth.CONFIGS["cfg2"].scaled((96, 80, 64), (8, 8, 8), (8, 8, 8)), q=0)
+    x = synth.make_tensor(cfg)
+    d = list(cfg.dims)
+    oms = []
+    for n in range(3):
+        J = int(np.prod([d[k] for k in range(3) if k != n]))
+        oms.append(np.ascontiguousarray(synth.rng_for(77, 1, n).standard_normal((J, 16)).astype(np.float32)))
+        d[n] = cfg.ranks[n]
+    ref = oracle.sthosvd(x, cfg.ranks, oms, q=0)
+    res = P.rtucker_sthosvd(htc, dev(x), cfg.ranks, 8, 0, [om_dev(o) for o in oms])
+    htc.sync()
+    qg = [mat(q) for q in res["Q"]]
+    for n in range(3):
+        assert M.subspace(qg[n], ref["Q"][n]) <= 1e-5
+    assert abs(mat(res["err"])[0] - ref["E"]) / ref["E"] <= 1e-5
