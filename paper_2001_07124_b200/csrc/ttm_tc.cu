@@ -10,7 +10,9 @@
 // issuer, warps 2-5 = "splitters" (one TMEM lane = one tile row each) that turn the raw fp32 X
 // tile (TMA -> smem) into hi/lo tf32 operands in TMEM (tcgen05.st) and split B in place, and that
 // drain the fp32 accumulators (tcgen05.ld) in the epilogue.  A comes from TMEM, B from shared
-// memory (SWIZZLE_NONE canonical layout written directly by permuted-stride TMA boxes).
+// memory in the K-major SWIZZLE_NONE canonical layout: written directly by a permuted-stride TMA
+// box when B is column-major (Z, Q), or transposed by the splitters from a row-major TMA tile
+// (Omega; MN-major tf32 B operands were measured not to work with A in TMEM, tools/tc_probe.cu).
 // Pipelines: NS-stage smem/TMEM ring (full -> ready -> consumed), double-buffered accumulators.
 #include <cstring>
 
@@ -21,21 +23,25 @@ namespace rt {
 namespace {
 using namespace tc;
 
-constexpr int NS = 4;            // pipeline depth
 constexpr int KC = 32;           // contraction elements per stage
 constexpr int BM = 128;          // tile rows = TMEM lanes
 constexpr int NTHREADS = 192;
 __host__ __device__ constexpr uint32_t kAccCol(int b) { return b ? 128u : 0u; }
 constexpr uint32_t kAStage = 256;  // A stage s: hi at kAStage + 64 s, lo at + 32
 
-template <int NPAD, bool BSPLIT>
+// Shared memory plan: per stage a raw X tile, the K-major B operand (hi), optionally B lo and
+// the raw row-major B tile (BRAW).  NS = 4 stages when they fit in ~200 KB, else 3.
+template <int NPAD, bool BSPLIT, bool BRAW>
 struct Smem {
   static constexpr size_t kX = size_t(BM) * KC * 4;          // 16 KB raw X tile
   static constexpr size_t kB = size_t(NPAD) * KC * 4;        // B tile
+  static constexpr size_t per_stage = kX + kB * (1 + (BSPLIT ? 1 : 0) + (BRAW ? 1 : 0));
+  static constexpr int NS = per_stage * 4 <= 200 * 1024 ? 4 : 3;
   static constexpr size_t off_x = 0;
   static constexpr size_t off_b = off_x + NS * kX;
   static constexpr size_t off_blo = off_b + NS * kB;
-  static constexpr size_t off_bar = off_blo + (BSPLIT ? NS * kB : 0);
+  static constexpr size_t off_braw = off_blo + (BSPLIT ? NS * kB : 0);
+  static constexpr size_t off_bar = off_braw + (BRAW ? NS * kB : 0);
   static constexpr size_t bytes = off_bar + 8 * (3 * NS + 4) + 16 + 1024;   // + alignment slack
 };
 
@@ -48,9 +54,9 @@ struct Bars {
   uint32_t* tmem_base;
 };
 
-template <int NPAD, bool BSPLIT>
+template <class L>
 __device__ __forceinline__ char* setup(char* raw, Bars& bars) {
-  using L = Smem<NPAD, BSPLIT>;
+  constexpr int NS = L::NS;
   char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
   uint64_t* b = reinterpret_cast<uint64_t*>(base + L::off_bar);
   bars.full = b;
@@ -62,12 +68,10 @@ __device__ __forceinline__ char* setup(char* raw, Bars& bars) {
   return base;
 }
 
-// B descriptor for k-step kk of stage buffer `saddr` (see tc_common.cuh for LBO/SBO meaning)
+// B descriptor for k-step kk of a stage buffer: K-major, element (n, k) at
+// (k/4)*(NPAD*16) + n*16 + (k%4)*4 bytes  (LBO = NPAD*16 between K-chunks, SBO = 128 between 8-row groups)
 template <int NPAD>
-__device__ __forceinline__ uint64_t bdesc(uint32_t saddr, int kk, int b_mn) {
-  if (b_mn)  // MN-major: element (n, k) at (n/4)*512 + k*16 + (n%4)*4
-    return sdesc(saddr + uint32_t(kk) * 128u, /*lbo*/ 128u, /*sbo*/ 512u);
-  // K-major: element (n, k) at (k/4)*(NPAD*16) + n*16 + (k%4)*4
+__device__ __forceinline__ uint64_t bdesc(uint32_t saddr, int kk) {
   return sdesc(saddr + uint32_t(kk) * 2u * NPAD * 16u, /*lbo*/ NPAD * 16u, /*sbo*/ 128u);
 }
 
@@ -115,17 +119,39 @@ __device__ __forceinline__ void split_b(float* b, float* blo, int t) {
   }
 }
 
+// Transpose the raw row-major B tile [KC j][NPAD n] into the K-major operand (+ optional hi/lo split).
+template <int NPAD, bool BSPLIT>
+__device__ __forceinline__ void transpose_b(const float* raw, float* bhi, float* blo, int t) {
+  for (int e = t; e < NPAD * (KC / 4); e += 128) {
+    const int n = e % NPAD, jg = e / NPAD;
+    float v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = raw[(4 * jg + q) * NPAD + n];
+    float4* dh = reinterpret_cast<float4*>(bhi) + (jg * NPAD + n);
+    if (BSPLIT) {
+      uint32_t h[4], l[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) split_tf32(v[q], h[q], l[q]);
+      *dh = make_float4(__uint_as_float(h[0]), __uint_as_float(h[1]), __uint_as_float(h[2]), __uint_as_float(h[3]));
+      *(reinterpret_cast<float4*>(blo) + (jg * NPAD + n)) =
+          make_float4(__uint_as_float(l[0]), __uint_as_float(l[1]), __uint_as_float(l[2]), __uint_as_float(l[3]));
+    } else {
+      *dh = make_float4(v[0], v[1], v[2], v[3]);
+    }
+  }
+}
+
 // MMA issue for one stage: 4 k-steps x (2 or 3) products into accumulator `acc`.
 template <int NPAD, bool BSPLIT>
 __device__ __forceinline__ void issue_stage(uint32_t tmem, uint32_t acc, int s, uint32_t b_saddr, uint32_t blo_saddr,
-                                            int b_mn, uint32_t idesc, bool first) {
+                                            uint32_t idesc, bool first) {
   const uint32_t a_hi = tmem + kAStage + 64u * s;
 #pragma unroll
   for (int kk = 0; kk < KC / 8; ++kk) {
-    const uint64_t bd = bdesc<NPAD>(b_saddr, kk, b_mn);
+    const uint64_t bd = bdesc<NPAD>(b_saddr, kk);
     mma_tf32_ts(tmem + acc, a_hi + 8 * kk, bd, idesc, (first && kk == 0) ? 0u : 1u);
     mma_tf32_ts(tmem + acc, a_hi + 32 + 8 * kk, bd, idesc, 1u);
-    if (BSPLIT) mma_tf32_ts(tmem + acc, a_hi + 8 * kk, bdesc<NPAD>(blo_saddr, kk, b_mn), idesc, 1u);
+    if (BSPLIT) mma_tf32_ts(tmem + acc, a_hi + 8 * kk, bdesc<NPAD>(blo_saddr, kk), idesc, 1u);
   }
 }
 
@@ -137,17 +163,18 @@ struct SParams {
   int64_t nchunks;    // total j-chunks
   int64_t cps;        // chunks per split (CTA)
   int seg;            // chunks per accumulator segment
-  int b_mn;           // 1: B row-major (MN-major), 0: B col-major (K-major)
   float* part;        // [split][K][I]
 };
 
-template <int NPAD, bool BSPLIT, bool AMN>
+// BRAW: B is row-major (Omega): TMA a [KC][NPAD] tile, splitters transpose it to K-major.
+template <int NPAD, bool BSPLIT, bool AMN, bool BRAW>
 __global__ void __launch_bounds__(NTHREADS, 1)
 ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb, const SParams p) {
-  using L = Smem<NPAD, BSPLIT>;
+  using L = Smem<NPAD, BSPLIT, BRAW>;
+  constexpr int NS = L::NS;
   extern __shared__ char smem_raw[];
   Bars bars;
-  char* sm = setup<NPAD, BSPLIT>(smem_raw, bars);
+  char* sm = setup<L>(smem_raw, bars);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t i0 = int64_t(blockIdx.x) * BM;
   const int64_t c_begin = int64_t(blockIdx.y) * p.cps;
@@ -184,7 +211,7 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
         const int64_t c = c_begin + it;
         mbar_expect_tx(&bars.full[s], bytes);
         float* xs = reinterpret_cast<float*>(sm + L::off_x + s * L::kX);
-        float* bs = reinterpret_cast<float*>(sm + L::off_b + s * L::kB);
+        float* bs = reinterpret_cast<float*>(sm + (BRAW ? L::off_braw : L::off_b) + s * L::kB);
         int64_t j0;
         if (AMN) {
           j0 = c * KC;
@@ -194,13 +221,13 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
           j0 = a0 + p.a * beta;
           tma_load_3d(xs, &tmx, &bars.full[s], int(a0), int(i0), int(beta));
         }
-        if (p.b_mn) tma_load_3d(bs, &tmb, &bars.full[s], 0, int(j0), 0);
+        if (BRAW) tma_load_2d(bs, &tmb, &bars.full[s], 0, int(j0));
         else tma_load_3d(bs, &tmb, &bars.full[s], 0, 0, int(j0 / 4));
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      const uint32_t idesc = idesc_tf32(BM, NPAD, p.b_mn);
+      const uint32_t idesc = idesc_tf32(BM, NPAD, 0);
       for (int it = 0; it < nch; ++it) {
         const int s = it % NS;
         const int u = it / p.seg;
@@ -211,7 +238,7 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
         mbar_wait(&bars.ready[s], (it / NS) & 1);
         tc_fence_after();
         issue_stage<NPAD, BSPLIT>(tmem, kAccCol(ab), s, smem_u32(sm + L::off_b + s * L::kB),
-                                  smem_u32(sm + L::off_blo + s * L::kB), p.b_mn, idesc, first);
+                                  smem_u32(sm + L::off_blo + s * L::kB), idesc, first);
         mma_commit(&bars.consumed[s]);
         if (last) mma_commit(&bars.acc_full[ab]);
       }
@@ -245,7 +272,11 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
       mbar_wait(&bars.full[s], (it / NS) & 1);
       const float* xs = reinterpret_cast<const float*>(sm + L::off_x + s * L::kX);
       split_row_to_tmem<AMN>(xs, r, lane_base + kAStage + 64u * s);
-      if (BSPLIT)
+      if (BRAW)
+        transpose_b<NPAD, BSPLIT>(reinterpret_cast<const float*>(sm + L::off_braw + s * L::kB),
+                                  reinterpret_cast<float*>(sm + L::off_b + s * L::kB),
+                                  reinterpret_cast<float*>(sm + L::off_blo + s * L::kB), t);
+      else if (BSPLIT)
         split_b<NPAD>(reinterpret_cast<float*>(sm + L::off_b + s * L::kB),
                       reinterpret_cast<float*>(sm + L::off_blo + s * L::kB), t);
       tmem_wait_st();
@@ -287,10 +318,11 @@ template <int NPAD, bool AKM>   // AKM: mode 0 (a == 1), X tile K-major [BM j][K
 __global__ void __launch_bounds__(NTHREADS, 1)
 ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb, const TParams p) {
   constexpr bool BSPLIT = true;
-  using L = Smem<NPAD, BSPLIT>;
+  using L = Smem<NPAD, BSPLIT, false>;
+  constexpr int NS = L::NS;
   extern __shared__ char smem_raw[];
   Bars bars;
-  char* sm = setup<NPAD, BSPLIT>(smem_raw, bars);
+  char* sm = setup<L>(smem_raw, bars);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t my_tiles = (p.ntiles > blockIdx.x) ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t total = my_tiles * p.nic;
@@ -351,7 +383,7 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
         mbar_wait(&bars.ready[s], uint32_t(it / NS) & 1);
         tc_fence_after();
         issue_stage<NPAD, BSPLIT>(tmem, kAccCol(ab), s, smem_u32(sm + L::off_b + s * L::kB),
-                                  smem_u32(sm + L::off_blo + s * L::kB), 0, idesc, first);
+                                  smem_u32(sm + L::off_blo + s * L::kB), idesc, first);
         mma_commit(&bars.consumed[s]);
         if (last) mma_commit(&bars.acc_full[ab]);
       }
@@ -452,25 +484,31 @@ void set_smem(K kernel, size_t bytes) {
   RT_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
 }
 
-template <int NPAD, bool BSPLIT, bool AMN>
+template <int NPAD, bool BSPLIT, bool AMN, bool BRAW>
 void launch_s(const Ctx& ctx, const CUtensorMap& tx, const CUtensorMap& tb, const SParams& p, dim3 grid) {
-  using L = Smem<NPAD, BSPLIT>;
+  using L = Smem<NPAD, BSPLIT, BRAW>;
   static bool attr = false;
-  if (!attr) { set_smem(ttm_s_tc_kernel<NPAD, BSPLIT, AMN>, L::bytes); attr = true; }
+  if (!attr) { set_smem(ttm_s_tc_kernel<NPAD, BSPLIT, AMN, BRAW>, L::bytes); attr = true; }
   launch(ctx, "ttm_s_tc", [&] {
-    ttm_s_tc_kernel<NPAD, BSPLIT, AMN><<<grid, NTHREADS, L::bytes, ctx.stream>>>(tx, tb, p);
+    ttm_s_tc_kernel<NPAD, BSPLIT, AMN, BRAW><<<grid, NTHREADS, L::bytes, ctx.stream>>>(tx, tb, p);
   });
 }
 
 template <int NPAD, bool BSPLIT>
-void dispatch_s(const Ctx& ctx, bool amn, const CUtensorMap& tx, const CUtensorMap& tb, const SParams& p, dim3 g) {
-  if (amn) launch_s<NPAD, BSPLIT, true>(ctx, tx, tb, p, g);
-  else launch_s<NPAD, BSPLIT, false>(ctx, tx, tb, p, g);
+void dispatch_s(const Ctx& ctx, bool amn, bool braw, const CUtensorMap& tx, const CUtensorMap& tb,
+                const SParams& p, dim3 g) {
+  if (amn) {
+    if (braw) launch_s<NPAD, BSPLIT, true, true>(ctx, tx, tb, p, g);
+    else launch_s<NPAD, BSPLIT, true, false>(ctx, tx, tb, p, g);
+  } else {
+    if (braw) launch_s<NPAD, BSPLIT, false, true>(ctx, tx, tb, p, g);
+    else launch_s<NPAD, BSPLIT, false, false>(ctx, tx, tb, p, g);
+  }
 }
 
 template <int NPAD, bool AKM>
 void launch_t(const Ctx& ctx, const CUtensorMap& tx, const CUtensorMap& tb, const TParams& p, dim3 grid) {
-  using L = Smem<NPAD, true>;
+  using L = Smem<NPAD, true, false>;
   static bool attr = false;
   if (!attr) { set_smem(ttm_t_tc_kernel<NPAD, AKM>, L::bytes); attr = true; }
   launch(ctx, "ttm_t_tc", [&] {
@@ -515,10 +553,10 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
     const uint32_t bx[3] = {KC, BM, 1};
     if (!make_map(&tx, X, 3, d, s, bx, true)) return false;
   }
-  if (b_rowmajor) {  // element (j, k) at j*ldb + k; canonical MN-major via box (4 k, 32 j, npad/4 k-groups)
-    const uint64_t d[3] = {4, uint64_t(J), uint64_t((K + 3) / 4)}, s[2] = {uint64_t(ldb) * 4, 16};
-    const uint32_t bx[3] = {4, KC, uint32_t(npad / 4)};
-    if (!make_map(&tb, Bm, 3, d, s, bx, false)) return false;
+  if (b_rowmajor) {  // element (j, k) at j*ldb + k: raw [KC j][npad k] tile, transposed in smem
+    const uint64_t d[2] = {uint64_t(K), uint64_t(J)}, s[1] = {uint64_t(ldb) * 4};
+    const uint32_t bx[2] = {uint32_t(npad), KC};
+    if (!make_map(&tb, Bm, 2, d, s, bx, false)) return false;
   } else {           // element (j, k) at j + ldb*k; canonical K-major via box (4 j, npad k, 8 j-groups)
     const uint64_t d[3] = {4, uint64_t(K), uint64_t((J + 3) / 4)}, s[2] = {uint64_t(ldb) * 4, 16};
     const uint32_t bx[3] = {4, uint32_t(npad), KC / 4};
@@ -528,7 +566,6 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
   p.a = box.a; p.I = box.I; p.b = box.b; p.K = K;
   p.cpb = amn ? 1 : cdiv(box.a, KC);
   p.nchunks = amn ? cdiv(box.b, KC) : p.cpb * box.b;
-  p.b_mn = b_rowmajor ? 1 : 0;
   const int64_t mtiles = cdiv(box.I, BM);
   int64_t splits = std::max<int64_t>(1, (int64_t(ctx.num_sms) * 4 + mtiles - 1) / mtiles);
   splits = std::min<int64_t>(splits, std::max<int64_t>(1, p.nchunks / 8));
@@ -541,8 +578,8 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
   const bool bsplit = !b_tf32_exact;
 #define RT_S_CASE(NP)                                                   \
   case NP:                                                              \
-    if (bsplit) dispatch_s<NP, true>(ctx, amn, tx, tb, p, grid);        \
-    else dispatch_s<NP, false>(ctx, amn, tx, tb, p, grid);              \
+    if (bsplit) dispatch_s<NP, true>(ctx, amn, b_rowmajor, tx, tb, p, grid);   \
+    else dispatch_s<NP, false>(ctx, amn, b_rowmajor, tx, tb, p, grid);         \
     break;
   switch (npad) {
     RT_S_CASE(16) RT_S_CASE(32) RT_S_CASE(48) RT_S_CASE(64) RT_S_CASE(80) RT_S_CASE(96) RT_S_CASE(128)
