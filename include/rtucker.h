@@ -94,14 +94,17 @@ const char* rt_last_error(const rt_handle* h);
  * failure was latched since the last rt_sync (the latch is cleared). */
 rt_status rt_sync(rt_handle* h);
 
-/* Options.  RT_OPT_TTM_IMPL: 0 auto (tcgen05 where the shape fits the TMA path, else CUDA
- * cores), 1 CUDA-core (SIMT) TTM kernels only, 2 tcgen05 only (RT_EUNSUPPORTED where it does
- * not apply).  RT_OPT_PROFILE: 1 records a CUDA event pair around every launch (read with
+/* Options.  RT_OPT_TTM_IMPL: 0 / 2 tcgen05 where the shape fits the TMA path (fp32 data,
+ * 16-byte aligned strides), CUDA-core (SIMT) kernels elsewhere; 1 CUDA-core TTM kernels only.  RT_OPT_PROFILE: 1 records a CUDA event pair around every launch (read with
  * rt_profile_read).  RT_OPT_OMEGA_TF32: 1 = the caller guarantees every Gaussian Omega entry
  * is exactly representable in tf32 (e.g. rounded on the host before it is given to both the
  * oracle and this library); the sketch then skips the A_hi*Omega_lo product of the 3xTF32
- * split.  RT_OPT_QR_FALLBACK is reserved. */
-typedef enum { RT_OPT_TTM_IMPL = 0, RT_OPT_PROFILE = 1, RT_OPT_QR_FALLBACK = 2, RT_OPT_OMEGA_TF32 = 3 } rt_option;
+ * split.  RT_OPT_TC_SEGMENT: contraction chunks (of 32) accumulated in TMEM before the fp32
+ * accumulator is drained to registers (default 4, i.e. 128 elements; the tensor core's fp32
+ * accumulation error grows with this length, tests/test_gpu_tc.py).  RT_OPT_QR_FALLBACK is
+ * reserved. */
+typedef enum { RT_OPT_TTM_IMPL = 0, RT_OPT_PROFILE = 1, RT_OPT_QR_FALLBACK = 2, RT_OPT_OMEGA_TF32 = 3,
+               RT_OPT_TC_SEGMENT = 4 } rt_option;
 rt_status rt_set_option(rt_handle* h, rt_option opt, int64_t value);
 
 /* Profile of the launches recorded since the last read (synchronizes the stream).

@@ -67,6 +67,7 @@ struct Ctx {
   int num_sms = 148;
   int ttm_impl = 0;             // 0 auto, 1 SIMT, 2 tcgen05 (error if unavailable)
   int omega_tf32 = 0;           // caller asserts Gaussian Omega entries are tf32-representable
+  int tc_seg = 4;               // tcgen05: 32-element chunks per TMEM accumulator segment (drained to fp32 regs)
 };
 
 // Launch a kernel (given as a lambda issuing <<<...>>> on ctx.stream) with optional

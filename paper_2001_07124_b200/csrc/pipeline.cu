@@ -32,7 +32,6 @@ int64_t pad4(int64_t x) { return (x + 3) & ~int64_t(3); }
 void ttm_s_dispatch(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B, int64_t ldb, bool rowmajor,
                     bool exact, int K, double* Y, int64_t ldy) {
   if (ctx.ttm_impl != 1 && ttm_s_tc(ctx, ws, X, box, B, ldb, rowmajor, exact, K, Y, ldy)) return;
-  RT_REQUIRE(ctx.ttm_impl != 2, kEUNSUPPORTED, "tcgen05 ttm_s path unavailable for this shape");
   ttm_s<float>(ctx, ws, X, box, B, rowmajor ? ldb : 1, rowmajor ? 1 : ldb, K, Y, ldy);
 }
 void ttm_s_dispatch(const Ctx& ctx, Arena& ws, const double* X, Box box, const double* B, int64_t ldb, bool rowmajor,
@@ -43,7 +42,6 @@ void ttm_s_dispatch(const Ctx& ctx, Arena& ws, const double* X, Box box, const d
 void ttm_t_dispatch(const Ctx& ctx, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
                     int64_t so_a, int64_t so_c, int64_t so_b) {
   if (ctx.ttm_impl != 1 && ttm_t_tc(ctx, X, box, Q, ldq, C, out, so_a, so_c, so_b)) return;
-  RT_REQUIRE(ctx.ttm_impl != 2, kEUNSUPPORTED, "tcgen05 ttm_t path unavailable for this shape");
   ttm_t<float, float, float>(ctx, X, box, Q, 1, ldq, C, out, so_a, so_c, so_b);
 }
 void ttm_t_dispatch(const Ctx& ctx, const double* X, Box box, const double* Q, int64_t ldq, int C, double* out,

@@ -310,6 +310,7 @@ struct TParams {
   int64_t tpb;        // tiles per beta (a > 1)
   int64_t ntiles;
   int nic;            // i-chunks per tile
+  int seg;            // i-chunks per accumulator segment (fp32 TMEM accumulation length)
   float* out;
   int64_t so_a, so_c, so_b;
 };
@@ -326,6 +327,7 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t my_tiles = (p.ntiles > blockIdx.x) ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t total = my_tiles * p.nic;
+  const int64_t nseg_t = (p.nic + p.seg - 1) / p.seg;     // segments per tile
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
@@ -375,11 +377,12 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
       const uint32_t idesc = idesc_tf32(BM, NPAD, 0);
       for (int64_t it = 0; it < total; ++it) {
         const int s = int(it % NS);
-        const int64_t u = it / p.nic;
-        const bool first = (it % p.nic) == 0;
-        const bool last = (it % p.nic) == p.nic - 1;
-        const int ab = int(u & 1);
-        if (first && u >= 2) mbar_wait(&bars.acc_empty[ab], uint32_t((u >> 1) - 1) & 1);
+        const int c = int(it % p.nic);
+        const int64_t g = (it / p.nic) * nseg_t + c / p.seg;     // global segment index
+        const bool first = (c % p.seg) == 0;
+        const bool last = (c % p.seg) == p.seg - 1 || c == p.nic - 1;
+        const int ab = int(g & 1);
+        if (first && g >= 2) mbar_wait(&bars.acc_empty[ab], uint32_t((g >> 1) - 1) & 1);
         mbar_wait(&bars.ready[s], uint32_t(it / NS) & 1);
         tc_fence_after();
         issue_stage<NPAD, BSPLIT>(tmem, kAccCol(ab), s, smem_u32(sm + L::off_b + s * L::kB),
@@ -393,32 +396,40 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
     const int r = 32 * q4 + lane;
     const uint32_t lane_base = tmem + (uint32_t(32 * q4) << 16);
     const int t = threadIdx.x - 64;
-    auto epilogue = [&](int64_t u) {
-      const int ab = int(u & 1);
-      const int64_t tile = blockIdx.x + u * gridDim.x;
-      int64_t a0, beta;
-      tile_coords(tile, a0, beta);
-      bool valid;
-      int64_t ob;
-      if (AKM) { const int64_t j = beta + r; valid = j < p.b; ob = j * p.so_b; }
-      else { const int64_t al = a0 + r; valid = al < p.a; ob = al * p.so_a + beta * p.so_b; }
-      mbar_wait(&bars.acc_full[ab], uint32_t(u >> 1) & 1);
+    float sums[NPAD];
+#pragma unroll
+    for (int k = 0; k < NPAD; ++k) sums[k] = 0.f;
+    // drain segment g into the register sums; after the last segment of a tile, store the tile
+    auto epilogue = [&](int64_t g) {
+      const int ab = int(g & 1);
+      mbar_wait(&bars.acc_full[ab], uint32_t(g >> 1) & 1);
       tc_fence_after();
 #pragma unroll
       for (int cb = 0; cb < NPAD / 16; ++cb) {
         uint32_t v[16];
         tmem_ld16(lane_base + kAccCol(ab) + 16 * cb, v);
         tmem_wait_ld();
-        if (valid) {
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const int c = 16 * cb + q;
-            if (c < p.C) p.out[ob + int64_t(c) * p.so_c] = __uint_as_float(v[q]);
-          }
-        }
+        for (int q = 0; q < 16; ++q) sums[16 * cb + q] += __uint_as_float(v[q]);
       }
       tc_fence_before();
       mbar_arrive(&bars.acc_empty[ab]);
+      if ((g % nseg_t) == nseg_t - 1) {
+        const int64_t tile = blockIdx.x + (g / nseg_t) * gridDim.x;
+        int64_t a0, beta;
+        tile_coords(tile, a0, beta);
+        bool valid;
+        int64_t ob;
+        if (AKM) { const int64_t j = beta + r; valid = j < p.b; ob = j * p.so_b; }
+        else { const int64_t al = a0 + r; valid = al < p.a; ob = al * p.so_a + beta * p.so_b; }
+        if (valid) {
+#pragma unroll
+          for (int k = 0; k < NPAD; ++k)
+            if (k < p.C) p.out[ob + int64_t(k) * p.so_c] = sums[k];
+        }
+#pragma unroll
+        for (int k = 0; k < NPAD; ++k) sums[k] = 0.f;
+      }
     };
     for (int64_t it = 0; it < total; ++it) {
       const int s = int(it % NS);
@@ -431,10 +442,12 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
       fence_proxy_async();
       tc_fence_before();
       mbar_arrive(&bars.ready[s]);
-      const int64_t u = it / p.nic;
-      if ((it % p.nic) == p.nic - 1 && u >= 1) epilogue(u - 1);
+      const int c = int(it % p.nic);
+      const bool last = (c % p.seg) == p.seg - 1 || c == p.nic - 1;
+      const int64_t g = (it / p.nic) * nseg_t + c / p.seg;
+      if (last && g >= 1) epilogue(g - 1);
     }
-    if (my_tiles >= 1) epilogue(my_tiles - 1);
+    if (my_tiles >= 1) epilogue(my_tiles * nseg_t - 1);
   }
   tc_fence_before();
   __syncthreads();
@@ -572,7 +585,7 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
   splits = std::min<int64_t>(splits, 65535);
   p.cps = cdiv(p.nchunks, splits);
   splits = cdiv(p.nchunks, p.cps);
-  p.seg = 32;
+  p.seg = std::max(1, ctx.tc_seg);
   p.part = ws.alloc_n<float>(splits * K * box.I);
   const dim3 grid{unsigned(mtiles), unsigned(splits), 1u};
   const bool bsplit = !b_tf32_exact;
@@ -622,6 +635,7 @@ bool ttm_t_tc(const Ctx& ctx, const float* X, Box box, const float* Q, int64_t l
   p.tpb = akm ? 1 : cdiv(box.a, BM);
   p.ntiles = akm ? cdiv(box.b, BM) : p.tpb * box.b;
   p.nic = int(cdiv(box.I, KC));
+  p.seg = std::max(1, ctx.tc_seg);
   p.out = out; p.so_a = so_a; p.so_c = so_c; p.so_b = so_b;
   const int64_t grid = std::min<int64_t>(p.ntiles, ctx.num_sms);
 #define RT_T_CASE(NP)                                                           \
