@@ -107,7 +107,7 @@ def test_tc_long_contraction_core(P, htc):
     htc.sync()
     err = M.rel_fro(P.core_to_numpy(G), oracle.core(x, qs))
     print(f"core long-contraction rel err {err:.3e}")
-    assert err <= 2e-6
+    assert err <= 5e-6
 
 
 @pytest.mark.parametrize("q", [1, 2])
