@@ -201,11 +201,12 @@ def run_gpu(args, cfg):
         for n in range(N):
             if n < N - 1:
                 a = int(np.prod(cfg.dims[:-1])) // cfg.dims[n]
-                oms.append(synth.gaussian_omega_device(cfg, n, dev, row0=a * lo, rows=a * (hi - lo)))
+                oms.append(synth.gaussian_omega_device(cfg, n, dev, row0=a * lo, rows=a * (hi - lo), tf32=True))
             else:
-                oms.append(synth.gaussian_omega_device(cfg, n, dev))
+                oms.append(synth.gaussian_omega_device(cfg, n, dev, tf32=True))
         torch.cuda.synchronize()
         h = P.Handle(stream=stream, nccl_id=nid, nranks=world, rank=rank)
+        h.set_option(3, 1)                  # RT_OPT_OMEGA_TF32: Omega is host/device-rounded to tf32
 
         def step():
             return P.rtucker_hosvd(h, X, cfg.ranks, cfg.p, cfg.q, oms, last_offset=lo, last_global=I_last)
@@ -241,7 +242,7 @@ def run_gpu(args, cfg):
         if not args.no_e2e:
             xh = torch.empty(X.shape, dtype=X.dtype, pin_memory=True)
             xh.copy_(X)
-            omh = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in oms]
+            omh = [torch.empty((o.shape[1], o.shape[0]), dtype=o.dtype, pin_memory=True).t() for o in oms]
             for a, b in zip(omh, oms):
                 a.copy_(b)
             torch.cuda.synchronize()
@@ -291,7 +292,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-elems", type=float, default=3.0e7)
+    ap.add_argument("--cpu-sample-elems", type=float, default=2.0e8)
     args = ap.parse_args()
     cfg = synth.CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))

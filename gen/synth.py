@@ -161,11 +161,12 @@ def make_tensor(cfg: Config, return_parts: bool = False):
 
 
 def gaussian_omega(cfg: Config, n: int, K: Optional[int] = None, rows: Optional[int] = None,
-                   row0: int = 0) -> np.ndarray:
-    """Gaussian Omega_n (J_n x K_n, C order = row-major, element (j,k) at j*K+k).
+                   row0: int = 0, tf32: bool = False) -> np.ndarray:
+    """Gaussian Omega_n as a (J_n, K_n) array (element (j,k) = Omega_n(j,k)).
 
     ``rows``/``row0`` select a contiguous block of rows (a slab's local rows), drawn
     from the same stream as the full matrix so slabs and the whole agree bit-exactly.
+    ``tf32``: round to tf32-exact values (``round_tf32``) before handing it to both sides.
     """
     K = cfg.K(n) if K is None else K
     J = cfg.J(n)
@@ -174,6 +175,8 @@ def gaussian_omega(cfg: Config, n: int, K: Optional[int] = None, rows: Optional[
     if row0:
         rng.standard_normal(row0 * K)  # advance the stream (row-major draw order)
     om = rng.standard_normal((rows, K))
+    if tf32 and cfg.dtype == "f32":
+        return np.ascontiguousarray(round_tf32(om))
     return np.ascontiguousarray(om.astype(cfg.np_dtype))
 
 
@@ -301,11 +304,13 @@ def make_tensor_device(cfg: Config, device, slab_modes: int = 64, last_range: Op
 
 
 def gaussian_omega_device(cfg: Config, n: int, device, K: Optional[int] = None,
-                          row0: int = 0, rows: Optional[int] = None, chunk_rows: int = 1 << 20):
+                          row0: int = 0, rows: Optional[int] = None, chunk_rows: int = 1 << 20,
+                          tf32: bool = False):
     """Gaussian Omega_n generated on device (torch Philox, seeded per 2^20-row chunk).
 
-    Row-major (J_n x K_n).  Row blocks are drawn chunk-wise so that any contiguous
-    row range (a slab's local rows) matches the full matrix bit-exactly.
+    Returned as a (rows, K_n) column-major view (the library's layout).  Row blocks are drawn
+    chunk-wise so that any contiguous row range (a slab's local rows) matches the full matrix
+    bit-exactly.  ``tf32``: round to nearest tf32 (same rule as ``round_tf32``).
     """
     import torch
     K = cfg.K(n) if K is None else K
@@ -313,11 +318,16 @@ def gaussian_omega_device(cfg: Config, n: int, device, K: Optional[int] = None,
     rows = J - row0 if rows is None else rows
     tdt = torch.float64 if cfg.dtype == "f64" else torch.float32
     dev = torch.device(device)
-    out = torch.empty((rows, K), dtype=tdt, device=dev)
+    out = torch.empty((K, rows), dtype=tdt, device=dev).t()
     c0 = (row0 // chunk_rows) * chunk_rows
     for c in range(c0, row0 + rows, chunk_rows):
         gen = torch.Generator(device=dev).manual_seed(_torch_seed(cfg.cfg_id, _OBJ_OMEGA, n, c))
         blk = torch.randn((min(chunk_rows, J - c), K), generator=gen, device=dev, dtype=torch.float64)
         a, b = max(c, row0), min(c + blk.shape[0], row0 + rows)
-        out[a - row0:b - row0] = blk[a - c:b - c].to(tdt)
+        v = blk[a - c:b - c].to(tdt)
+        if tf32 and tdt == torch.float32:
+            u = v.view(torch.int32)
+            u = (u + 0x0FFF + ((u >> 13) & 1)) & ~0x1FFF
+            v = u.view(torch.float32)
+        out[a - row0:b - row0] = v
     return out

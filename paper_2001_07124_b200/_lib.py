@@ -57,11 +57,12 @@ def _load():
         "rt_sync": (I, [P]),
         "rt_set_option": (I, [P, I, I64]),
         "rt_profile_read": (I, [P, C.POINTER(rt_profile_entry), I, C.POINTER(I), C.POINTER(I64)]),
-        "rtucker_sketch": (I, [P, C.POINTER(rt_tensor), I, I, PP, PI64, I, P, I64]),
+        "rtucker_sketch": (I, [P, C.POINTER(rt_tensor), I, I, PP, PI64, PI64, I, P, I64]),
         "rtucker_qr": (I, [P, I64, I64, I, P, I64, P, I64, P, I]),
         "rtucker_core": (I, [P, C.POINTER(rt_tensor), PP, PI64, P, P, P]),
-        "rtucker_hosvd": (I, [P, C.POINTER(rt_tensor), PI64, I, I, I, PP, PI64, PP, P, P, P]),
-        "rtucker_sthosvd": (I, [P, C.POINTER(rt_tensor), PI64, I, I, I, PP, PI64, C.POINTER(C.c_int), PP, P, P, P]),
+        "rtucker_hosvd": (I, [P, C.POINTER(rt_tensor), PI64, I, I, I, PP, PI64, PI64, PP, P, P, P]),
+        "rtucker_sthosvd": (I, [P, C.POINTER(rt_tensor), PI64, I, I, I, PP, PI64, PI64, C.POINTER(C.c_int), PP, P,
+                                P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

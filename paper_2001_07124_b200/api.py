@@ -7,7 +7,10 @@ device buffers and the stream.  Conventions:
     (I_N, ..., I_1) (first-mode-fastest memory, gen.synth.to_device_layout);
   * an m x k "col-major" matrix is a torch tensor M of shape (m, k) with strides (1, m)
     (i.e. ``t.T`` of a contiguous (k, m) tensor); results are returned that way;
-  * Gaussian Omega_n: C-contiguous (J_n, K_n); Kronecker factors: C-contiguous (d_k, L_k).
+  * Gaussian Omega_n (J_n, K_n) and Kronecker factors (d_k, L_k) are passed to the library
+    column-major; any (rows, cols) torch tensor is accepted (a strided column-major view such as
+    a slab's row block Omega[r0:r1, :] of a column-major Omega is used in place, otherwise a
+    column-major copy is made).
 """
 from __future__ import annotations
 
@@ -41,6 +44,17 @@ def colmajor(m: torch.Tensor) -> torch.Tensor:
     if m.stride(0) == 1 and (m.stride(1) == m.shape[0] or m.shape[1] == 1):
         return m
     return m.t().contiguous().t()
+
+
+def colmajor_ld(m: torch.Tensor):
+    """(tensor, ld): a column-major view (stride(0) == 1, stride(1) = ld >= rows) used in place,
+    else a packed column-major copy."""
+    if m.dim() != 2:
+        raise ValueError("expected a matrix")
+    if m.stride(0) == 1 and m.stride(1) >= m.shape[0]:
+        return m, (m.stride(1) if m.shape[1] > 1 else max(1, m.shape[0]))
+    c = m.t().contiguous().t()
+    return c, max(1, c.shape[0])
 
 
 def new_colmajor(m: int, k: int, dtype=torch.float64, device=None) -> torch.Tensor:
@@ -154,25 +168,21 @@ def _i64_array(vals) -> "C.Array":
 
 
 def _omega_table(N: int, omegas, kind: str):
-    """Flat N x N tables (pointer, cols) indexed [n*N + k] (include/rtucker.h)."""
+    """Flat N x N tables (pointer, cols, ld) indexed [n*N + k] (include/rtucker.h)."""
     ptrs = [None] * (N * N)
     cols = [0] * (N * N)
+    lds = [0] * (N * N)
     keep = []
     for n in range(N):
-        if kind == "gauss":
-            om = omegas[n].contiguous()
+        entries = [(n, omegas[n])] if kind == "gauss" else \
+            [(k, omegas[n][k]) for k in range(N) if k != n and omegas[n][k] is not None]
+        for k, om in entries:
+            om, ld = colmajor_ld(om)
             keep.append(om)
-            ptrs[n * N + n] = om
-            cols[n * N + n] = om.shape[1]
-        else:
-            for k in range(N):
-                if k == n or omegas[n][k] is None:
-                    continue
-                om = omegas[n][k].contiguous()
-                keep.append(om)
-                ptrs[n * N + k] = om
-                cols[n * N + k] = om.shape[1]
-    return _ptr_array(ptrs), _i64_array(cols), keep
+            ptrs[n * N + k] = om
+            cols[n * N + k] = om.shape[1]
+            lds[n * N + k] = ld
+    return _ptr_array(ptrs), _i64_array(cols), _i64_array(lds), keep
 
 
 def _kind(kind: str) -> int:
@@ -184,29 +194,26 @@ def rtucker_sketch(h: Handle, X: torch.Tensor, mode: int, omega, q: int = 0, kin
     """Y = X_(n) Omega (+ q power iterations); returns fp64 (I_n_local, K) col-major."""
     desc = tensor_desc(X, last_offset, last_global)
     N = desc.order
+    ptrs, cols, lds, keep = [None] * N, [0] * N, [0] * N, []
     if kind == "gauss":
-        om = omega.contiguous()
-        ptrs = [None] * N
-        cols = [0] * N
-        if 0 <= mode < N:              # out-of-range modes are rejected by the library (RT_EINVAL)
-            ptrs[mode] = om
-            cols[mode] = om.shape[1]
-        keep = [om]
+        om, ld = colmajor_ld(omega)
+        keep.append(om)
         K = om.shape[1]
+        if 0 <= mode < N:              # out-of-range modes are rejected by the library (RT_EINVAL)
+            ptrs[mode], cols[mode], lds[mode] = om, K, ld
     else:
-        keep, ptrs, cols, K = [], [None] * N, [0] * N, 1
+        K = 1
         for k in range(N):
             if k == mode:
                 continue
-            o = omega[k].contiguous()
+            o, ld = colmajor_ld(omega[k])
             keep.append(o)
-            ptrs[k] = o
-            cols[k] = o.shape[1]
+            ptrs[k], cols[k], lds[k] = o, o.shape[1], ld
             K *= o.shape[1]
     In = desc.dims[mode] if 0 <= mode < N else 1
     Y = new_colmajor(In, K, device=X.device)
-    st = lib.rtucker_sketch(h.ptr, C.byref(desc), mode, _kind(kind), _ptr_array(ptrs), _i64_array(cols), q,
-                            C.c_void_p(Y.data_ptr()), In)
+    st = lib.rtucker_sketch(h.ptr, C.byref(desc), mode, _kind(kind), _ptr_array(ptrs), _i64_array(cols),
+                            _i64_array(lds), q, C.c_void_p(Y.data_ptr()), In)
     h.keep(*keep)
     _check(h, st)
     return Y
@@ -245,12 +252,12 @@ def rtucker_core(h: Handle, X: torch.Tensor, Qs: Sequence[torch.Tensor], with_er
 def _driver(fn, h, X, ranks, p, q, omegas, kind, with_error, last_offset, last_global, mode_order=None):
     desc = tensor_desc(X, last_offset, last_global)
     N = desc.order
-    ptrs, cols, keep = _omega_table(N, omegas, kind)
+    ptrs, cols, lds, keep = _omega_table(N, omegas, kind)
     local = [desc.dims[n] for n in range(N)]
     Q = [new_colmajor(local[n], ranks[n], device=X.device) for n in range(N)]
     G = torch.empty(tuple(reversed(list(ranks))), dtype=torch.float64, device=X.device)
     err = torch.zeros(2, dtype=torch.float64, device=X.device) if with_error else None
-    args = [h.ptr, C.byref(desc), _i64_array(ranks), int(p), int(q), _kind(kind), ptrs, cols]
+    args = [h.ptr, C.byref(desc), _i64_array(ranks), int(p), int(q), _kind(kind), ptrs, cols, lds]
     if fn is lib.rtucker_sthosvd:
         if mode_order is None:
             args.append(None)

@@ -69,20 +69,29 @@ rt::TView check_tensor(const rt_tensor* X) {
 }
 
 // strict: K_n <= min(I_n, J_n) (needed by the thin QR); a bare sketch (q = 0) accepts any K <= 128
-void check_gauss_omega(const rt::TView& X, int n, const void* om, int64_t K, bool strict = true) {
-  RT_REQUIRE(om != nullptr && aligned16(om), rt::kEINVAL, "Omega_n must be a 16-byte aligned device pointer");
+int64_t local_rows(const rt::TView& X, int n) {
+  int64_t s = 1;
+  for (int k = 0; k < X.N; ++k) if (k != n) s *= X.d[k];
+  return s;
+}
+
+void check_gauss_omega(const rt::TView& X, int n, const void* om, int64_t K, int64_t ld, bool strict = true) {
+  RT_REQUIRE(om != nullptr && (reinterpret_cast<uintptr_t>(om) % (X.dtype ? 8 : 4)) == 0, rt::kEINVAL,
+             "Omega_n must be an aligned device pointer");
+  RT_REQUIRE(ld >= local_rows(X, n), rt::kEINVAL, "omega_ld must be >= the (local) row count J_n");
   RT_REQUIRE(K >= 1, rt::kEINVAL, "omega_cols must be >= 1");
   RT_REQUIRE(!strict || (K <= X.Ig(n) && K <= X.Jg(n)), rt::kERANK, "K_n must be <= min(I_n, J_n)");
   RT_REQUIRE(K <= 128, rt::kEUNSUPPORTED, "K_n > 128 not supported");
 }
 
-int64_t check_kron_omega(const rt::TView& X, int n, const void* const* om, const int64_t* cols,
+int64_t check_kron_omega(const rt::TView& X, int n, const void* const* om, const int64_t* cols, const int64_t* lds,
                          bool strict = true) {
   int64_t K = 1;
   for (int k = 0; k < X.N; ++k) {
     if (k == n) continue;
-    RT_REQUIRE(om[k] != nullptr && aligned16(om[k]), rt::kEINVAL, "Kronecker factor must be an aligned device pointer");
+    RT_REQUIRE(om[k] != nullptr, rt::kEINVAL, "Kronecker factor must be a device pointer");
     RT_REQUIRE(cols[k] >= 1, rt::kEINVAL, "Kronecker widths must be >= 1");
+    RT_REQUIRE(lds[k] >= X.d[k], rt::kEINVAL, "Kronecker factor ld must be >= d_k");
     K *= cols[k];
   }
   RT_REQUIRE(!strict || K <= X.Ig(n), rt::kERANK, "Kronecker sketch width prod L_k must be <= I_n");
@@ -220,25 +229,27 @@ rt_status rt_profile_read(rt_handle* h, rt_profile_entry* out, int cap, int* n, 
 }
 
 rt_status rtucker_sketch(rt_handle* h, const rt_tensor* X, int mode, rt_omega_kind kind, const void* const* omega,
-                         const int64_t* omega_cols, int q, double* Y, int64_t ldy) {
+                         const int64_t* omega_cols, const int64_t* omega_ld, int q, double* Y, int64_t ldy) {
   if (!h) return RT_EINVAL;
   return guard(h, [&] {
     rt::TView v = check_tensor(X);
     RT_REQUIRE(mode >= 0 && mode < v.N, rt::kEINVAL, "mode out of range");
     RT_REQUIRE(q >= 0, rt::kEINVAL, "q must be >= 0");
-    RT_REQUIRE(omega && omega_cols && Y, rt::kEINVAL, "NULL omega/omega_cols/Y");
+    RT_REQUIRE(omega && omega_cols && omega_ld && Y, rt::kEINVAL, "NULL omega/omega_cols/omega_ld/Y");
     RT_REQUIRE(ldy >= v.d[mode], rt::kEINVAL, "ldy < I_n");
     rt::Engine eng(h->ctx, h->ws, h->comm.get());
     RT_REQUIRE(!(v.sharded() && !eng.dist() && q > 0), rt::kEINVAL,
                "power iterations on a slab need a communicator");
     int64_t K;
-    if (kind == RT_OMEGA_GAUSS) { K = omega_cols[mode]; check_gauss_omega(v, mode, omega[mode], K, q > 0); }
-    else if (kind == RT_OMEGA_KRON) K = check_kron_omega(v, mode, omega, omega_cols, q > 0);
+    if (kind == RT_OMEGA_GAUSS) { K = omega_cols[mode]; check_gauss_omega(v, mode, omega[mode], K, omega_ld[mode], q > 0); }
+    else if (kind == RT_OMEGA_KRON) K = check_kron_omega(v, mode, omega, omega_cols, omega_ld, q > 0);
     else throw rt::Error(rt::kEINVAL, "unknown omega kind");
     const int64_t In = v.d[mode];
     double* Yt = (ldy == In) ? Y : h->ws.alloc_n<double>(In * K);
-    if (v.dtype == 0) eng.sketch<float>(v, static_cast<const float*>(v.data), mode, kind, omega, omega_cols, q, Yt);
-    else eng.sketch<double>(v, static_cast<const double*>(v.data), mode, kind, omega, omega_cols, q, Yt);
+    if (v.dtype == 0)
+      eng.sketch<float>(v, static_cast<const float*>(v.data), mode, kind, omega, omega_cols, omega_ld, q, Yt);
+    else
+      eng.sketch<double>(v, static_cast<const double*>(v.data), mode, kind, omega, omega_cols, omega_ld, q, Yt);
     if (Yt != Y) RT_CUDA(cudaMemcpy2DAsync(Y, ldy * sizeof(double), Yt, In * sizeof(double), In * sizeof(double), K,
                                            cudaMemcpyDeviceToDevice, h->ctx.stream));
   });
@@ -305,9 +316,9 @@ rt_status rtucker_core(rt_handle* h, const rt_tensor* X, const double* const* Q,
 }
 
 static void check_driver_args(const rt::TView& v, const int64_t* R, int p, int q, rt_omega_kind kind,
-                              const void* const* omega, const int64_t* omega_cols, double* const* Q_out,
-                              double* G_out, const int64_t* cur_dims) {
-  RT_REQUIRE(R && omega && omega_cols && Q_out && G_out, rt::kEINVAL, "NULL argument");
+                              const void* const* omega, const int64_t* omega_cols, const int64_t* omega_ld,
+                              double* const* Q_out, double* G_out, const int64_t* cur_dims) {
+  RT_REQUIRE(R && omega && omega_cols && omega_ld && Q_out && G_out, rt::kEINVAL, "NULL argument");
   RT_REQUIRE(p >= 0 && q >= 0, rt::kEINVAL, "p and q must be >= 0");
   RT_REQUIRE(kind == RT_OMEGA_GAUSS || kind == RT_OMEGA_KRON, rt::kEINVAL, "unknown omega kind");
   const int N = v.N;
@@ -317,14 +328,15 @@ static void check_driver_args(const rt::TView& v, const int64_t* R, int p, int q
     if (cur_dims) { for (int k = 0; k < N; ++k) w.d[k] = cur_dims[n * N + k]; w.glob = w.d[N - 1]; }
     const void* const* om = omega + n * N;
     const int64_t* oc = omega_cols + n * N;
+    const int64_t* ol = omega_ld + n * N;
     int64_t K;
     if (kind == RT_OMEGA_GAUSS) {
       K = oc[n];
-      check_gauss_omega(w, n, om[n], K);
+      check_gauss_omega(w, n, om[n], K, ol[n]);
       RT_REQUIRE(K == std::min<int64_t>(R[n] + p, std::min(w.Ig(n), w.Jg(n))), rt::kEINVAL,
                  "Gaussian width must be K_n = min(R_n + p, I_n, J_n)");
     } else {
-      K = check_kron_omega(w, n, om, oc);
+      K = check_kron_omega(w, n, om, oc, ol);
       RT_REQUIRE(K >= std::min<int64_t>(R[n] + p, w.Ig(n)), rt::kEINVAL,
                  "Kronecker width prod L_k must be >= min(R_n + p, I_n)");
     }
@@ -333,22 +345,23 @@ static void check_driver_args(const rt::TView& v, const int64_t* R, int p, int q
 }
 
 rt_status rtucker_hosvd(rt_handle* h, const rt_tensor* X, const int64_t* R, int p, int q, rt_omega_kind kind,
-                        const void* const* omega, const int64_t* omega_cols, double* const* Q_out, double* G_out,
-                        double* rel_err, double* rel_err_gram) {
+                        const void* const* omega, const int64_t* omega_cols, const int64_t* omega_ld,
+                        double* const* Q_out, double* G_out, double* rel_err, double* rel_err_gram) {
   if (!h) return RT_EINVAL;
   return guard(h, [&] {
     rt::TView v = check_tensor(X);
-    check_driver_args(v, R, p, q, kind, omega, omega_cols, Q_out, G_out, nullptr);
+    check_driver_args(v, R, p, q, kind, omega, omega_cols, omega_ld, Q_out, G_out, nullptr);
     rt::Engine eng(h->ctx, h->ws, h->comm.get());
     RT_REQUIRE(!(v.sharded() && !eng.dist()), rt::kEINVAL, "a sharded tensor needs a communicator");
-    if (v.dtype == 0) eng.hosvd<float>(v, R, q, kind, omega, omega_cols, Q_out, G_out, rel_err, rel_err_gram);
-    else eng.hosvd<double>(v, R, q, kind, omega, omega_cols, Q_out, G_out, rel_err, rel_err_gram);
+    if (v.dtype == 0) eng.hosvd<float>(v, R, q, kind, omega, omega_cols, omega_ld, Q_out, G_out, rel_err, rel_err_gram);
+    else eng.hosvd<double>(v, R, q, kind, omega, omega_cols, omega_ld, Q_out, G_out, rel_err, rel_err_gram);
   });
 }
 
 rt_status rtucker_sthosvd(rt_handle* h, const rt_tensor* X, const int64_t* R, int p, int q, rt_omega_kind kind,
-                          const void* const* omega, const int64_t* omega_cols, const int* mode_order,
-                          double* const* Q_out, double* G_out, double* rel_err, double* rel_err_gram) {
+                          const void* const* omega, const int64_t* omega_cols, const int64_t* omega_ld,
+                          const int* mode_order, double* const* Q_out, double* G_out, double* rel_err,
+                          double* rel_err_gram) {
   if (!h) return RT_EINVAL;
   return guard(h, [&] {
     rt::TView v = check_tensor(X);
@@ -373,9 +386,11 @@ rt_status rtucker_sthosvd(rt_handle* h, const rt_tensor* X, const int64_t* R, in
       for (int k = 0; k < N; ++k) cur[n * N + k] = d[k];
       d[n] = R[n];
     }
-    check_driver_args(v, R, p, q, kind, omega, omega_cols, Q_out, G_out, cur);
-    if (v.dtype == 0) eng.sthosvd<float>(v, R, q, kind, omega, omega_cols, order, Q_out, G_out, rel_err, rel_err_gram);
-    else eng.sthosvd<double>(v, R, q, kind, omega, omega_cols, order, Q_out, G_out, rel_err, rel_err_gram);
+    check_driver_args(v, R, p, q, kind, omega, omega_cols, omega_ld, Q_out, G_out, cur);
+    if (v.dtype == 0)
+      eng.sthosvd<float>(v, R, q, kind, omega, omega_cols, omega_ld, order, Q_out, G_out, rel_err, rel_err_gram);
+    else
+      eng.sthosvd<double>(v, R, q, kind, omega, omega_cols, omega_ld, order, Q_out, G_out, rel_err, rel_err_gram);
   });
 }
 

@@ -40,7 +40,7 @@ class Engine {
   // (1) sketch of mode n incl. q power iterations; Yt: fp64 I_n(local) x K, ld I_n(local).
   template <typename T>
   void sketch(const TView& X, const T* data, int n, int kind, const void* const* omega,
-              const int64_t* omega_cols, int q, double* Yt);
+              const int64_t* omega_cols, const int64_t* omega_ld, int q, double* Yt);
   // (2) thin QR of the fp64 Y side (shifted CholeskyQR3); R nullable.
   void qr_y(const double* Y, int64_t m, int64_t m_glob, int k, int64_t ldy, double* Q, int64_t ldq,
             double* R, bool rows_dist, int64_t row0);
@@ -64,11 +64,12 @@ class Engine {
   // drivers
   template <typename T>
   void hosvd(const TView& X, const int64_t* R, int q, int kind, const void* const* omega,
-             const int64_t* omega_cols, double* const* Q_out, double* G_out, double* E, double* Eg);
+             const int64_t* omega_cols, const int64_t* omega_ld, double* const* Q_out, double* G_out, double* E,
+             double* Eg);
   template <typename T>
   void sthosvd(const TView& X, const int64_t* R, int q, int kind, const void* const* omega,
-               const int64_t* omega_cols, const int* order, double* const* Q_out, double* G_out, double* E,
-               double* Eg);
+               const int64_t* omega_cols, const int64_t* omega_ld, const int* order, double* const* Q_out,
+               double* G_out, double* E, double* Eg);
 
  private:
   void canon(double* Qn, int64_t m, int r, int64_t ld, int64_t row0, bool dist_rows, double* U, int ku);

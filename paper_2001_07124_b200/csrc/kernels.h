@@ -27,11 +27,11 @@ void ttm_t(const Ctx& ctx, const Tin* X, Box box, const Tm* Mm, int64_t ms_i, in
 
 // tcgen05 tensor-core versions (ttm_tc.cu), fp32 only, 3xTF32 split.  Return false (nothing
 // launched) when the shape/alignment is outside the TMA path; callers then use the SIMT kernels.
-// B: row-major (element (j,k) at j*ldb + k, ldb % 4 == 0, pad columns zero) or col-major (element
-// (j,k) at j + ldb*k, ldb % 4 == 0, pad rows zero).  b_tf32_exact drops the A_hi*B_lo product.
-bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Bm, int64_t ldb, bool b_rowmajor,
-              bool b_tf32_exact, int K, double* Y, int64_t ldy);
-// out(alpha,c,beta) = sum_i X(alpha,i,beta) Q(i,c), Q col-major with ldq % 4 == 0 (pad rows zero)
+// B col-major (element (j,k) at j + ldb*k, ldb % 4 == 0, 16-byte aligned).  b_tf32_exact drops
+// the A_hi*B_lo product.
+bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Bm, int64_t ldb, bool b_tf32_exact,
+              int K, double* Y, int64_t ldy);
+// out(alpha,c,beta) = sum_i X(alpha,i,beta) Q(i,c), Q col-major with ldq % 4 == 0
 bool ttm_t_tc(const Ctx& ctx, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
               int64_t so_a, int64_t so_c, int64_t so_b);
 

@@ -28,15 +28,16 @@ void allreduce(Comm* c, bool on, T* p, int64_t n, cudaStream_t s) {
 
 int64_t pad4(int64_t x) { return (x + 3) & ~int64_t(3); }
 
-// Y = X_(n) B: tcgen05 3xTF32 kernel for fp32 data when the shape fits the TMA path, else SIMT.
-void ttm_s_dispatch(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B, int64_t ldb, bool rowmajor,
-                    bool exact, int K, double* Y, int64_t ldy) {
-  if (ctx.ttm_impl != 1 && ttm_s_tc(ctx, ws, X, box, B, ldb, rowmajor, exact, K, Y, ldy)) return;
-  ttm_s<float>(ctx, ws, X, box, B, rowmajor ? ldb : 1, rowmajor ? 1 : ldb, K, Y, ldy);
+// Y = X_(n) B (B col-major, ldb): tcgen05 3xTF32 kernel for fp32 data when the shape fits the
+// TMA path, else the SIMT kernel.
+void ttm_s_dispatch(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B, int64_t ldb, bool exact,
+                    int K, double* Y, int64_t ldy) {
+  if (ctx.ttm_impl != 1 && ttm_s_tc(ctx, ws, X, box, B, ldb, exact, K, Y, ldy)) return;
+  ttm_s<float>(ctx, ws, X, box, B, 1, ldb, K, Y, ldy);
 }
-void ttm_s_dispatch(const Ctx& ctx, Arena& ws, const double* X, Box box, const double* B, int64_t ldb, bool rowmajor,
-                    bool, int K, double* Y, int64_t ldy) {
-  ttm_s<double>(ctx, ws, X, box, B, rowmajor ? ldb : 1, rowmajor ? 1 : ldb, K, Y, ldy);
+void ttm_s_dispatch(const Ctx& ctx, Arena& ws, const double* X, Box box, const double* B, int64_t ldb, bool,
+                    int K, double* Y, int64_t ldy) {
+  ttm_s<double>(ctx, ws, X, box, B, 1, ldb, K, Y, ldy);
 }
 // out(alpha,c,beta) = sum_i X(alpha,i,beta) Q(i,c), Q col-major (ldq)
 void ttm_t_dispatch(const Ctx& ctx, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
@@ -126,7 +127,7 @@ void Engine::qr_z(T* Z, int64_t m, int64_t ldz, int64_t m_glob, int k, bool rows
 // ---------------------------------------------------------------- sketch (a1-a3)
 template <typename T>
 void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* const* omega,
-                    const int64_t* omega_cols, int q, double* Yt) {
+                    const int64_t* omega_cols, const int64_t* omega_ld, int q, double* Yt) {
   const int N = X.N;
   const Box bx = X.box(n);
   const bool last = (n == N - 1);
@@ -134,17 +135,7 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
   int K;
   if (kind == 0) {
     K = int(omega_cols[n]);
-    const T* om = static_cast<const T*>(omega[n]);
-    int64_t ldo = K;
-    if (std::is_same<T, float>::value && (K % 4) && ctx.ttm_impl != 1) {
-      // TMA needs 16-byte row pitch: zero-padded copy of Omega_n (J x pad4(K), row-major)
-      ldo = pad4(K);
-      T* omp = ws.alloc_n<T>(bx.J() * ldo);
-      fill_zero(ctx, omp, sizeof(T) * bx.J() * ldo);
-      convert2d<T, T>(ctx, om, K, bx.J(), K, omp, ldo);
-      om = omp;
-    }
-    ttm_s_dispatch(ctx, ws, data, bx, om, ldo, /*rowmajor=*/true, ctx.omega_tf32 != 0, K, Yt, In);
+    ttm_s_dispatch(ctx, ws, data, bx, static_cast<const T*>(omega[n]), omega_ld[n], ctx.omega_tf32 != 0, K, Yt, In);
   } else {
     // Kronecker sketch W = X x_{k!=n} Omega_k^T (Eq.(2)): a chain of TTMs whose first
     // stage streams X and whose later stages run on the shrunken result.
@@ -159,7 +150,7 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
       const Box b = TView::box_of(cur, N, k);
       const int L = int(omega_cols[k]);
       T* dst = ws.alloc_n<T>(b.a * L * b.b);
-      ttm_t<T, T, T>(ctx, src, b, static_cast<const T*>(omega[k]), L, 1, L, dst, 1, b.a, b.a * L);
+      ttm_t_dispatch(ctx, src, b, static_cast<const T*>(omega[k]), omega_ld[k], L, dst, 1, b.a, b.a * L);
       src = dst;
       cur[k] = L;
     }
@@ -194,7 +185,7 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
       zrow0 = bx.a * bp * X.off;
     }
     qr_z<T>(Z, Jl, ldz, X.Jg(n), K, !last && dist(), zrow0);
-    ttm_s_dispatch(ctx, ws, data, bx, Z, ldz, /*rowmajor=*/false, false, K, Yt, In);
+    ttm_s_dispatch(ctx, ws, data, bx, Z, ldz, false, K, Yt, In);
     allreduce(comm, !last && dist(), Yt, In * K, ctx.stream);                     // C1
   }
   ws.rewind(mk);
@@ -329,7 +320,8 @@ void Engine::rel_error(const TView& X, const T* data, const double* G, const int
 // ----------------------------------------------------------------- HOSVD (Alg.6)
 template <typename T>
 void Engine::hosvd(const TView& X, const int64_t* R, int q, int kind, const void* const* omega,
-                   const int64_t* omega_cols, double* const* Q_out, double* G_out, double* E, double* Eg) {
+                   const int64_t* omega_cols, const int64_t* omega_ld, double* const* Q_out, double* G_out, double* E,
+                   double* Eg) {
   const int N = X.N;
   const T* data = static_cast<const T*>(X.data);
   const auto mk = ws.mark();
@@ -338,11 +330,12 @@ void Engine::hosvd(const TView& X, const int64_t* R, int q, int kind, const void
   for (int n = 0; n < N; ++n) {
     const void* const* om = omega + n * N;
     const int64_t* oc = omega_cols + n * N;
+    const int64_t* ol = omega_ld + n * N;
     if (kind == 0) K[n] = oc[n];
     else { K[n] = 1; for (int k = 0; k < N; ++k) if (k != n) K[n] *= oc[k]; }
     const int64_t In = X.d[n];
     double* Yt = ws.alloc_n<double>(In * K[n]);
-    sketch<T>(X, data, n, kind, om, oc, q, Yt);
+    sketch<T>(X, data, n, kind, om, oc, ol, q, Yt);
     Qt[n] = ws.alloc_n<double>(In * K[n]);
     ldq[n] = In;
     const bool last = (n == N - 1);
@@ -360,8 +353,8 @@ void Engine::hosvd(const TView& X, const int64_t* R, int q, int kind, const void
 // -------------------------------------------------------------- STHOSVD (Alg.8)
 template <typename T>
 void Engine::sthosvd(const TView& X, const int64_t* R, int q, int kind, const void* const* omega,
-                     const int64_t* omega_cols, const int* order, double* const* Q_out, double* G_out,
-                     double* E, double* Eg) {
+                     const int64_t* omega_cols, const int64_t* omega_ld, const int* order, double* const* Q_out,
+                     double* G_out, double* E, double* Eg) {
   const int N = X.N;
   const auto mk = ws.mark();
   TView S = X;                         // working tensor S (reading R8: S = X)
@@ -376,6 +369,7 @@ void Engine::sthosvd(const TView& X, const int64_t* R, int q, int kind, const vo
     const int n = order ? order[step] : step;
     const void* const* om = omega + n * N;
     const int64_t* oc = omega_cols + n * N;
+    const int64_t* ol = omega_ld + n * N;
     int K;
     if (kind == 0) K = int(oc[n]);
     else { K = 1; for (int k = 0; k < N; ++k) if (k != n) K *= int(oc[k]); }
@@ -383,7 +377,7 @@ void Engine::sthosvd(const TView& X, const int64_t* R, int q, int kind, const vo
     const auto mstep = ws.mark();
     // Alg.8 line 3 = Alg.1 lines 1-3 on S_(n): sketch (+ power iterations) and thin QR
     double* Yt = ws.alloc_n<double>(In * K);
-    sketch<T>(S, sdata, n, kind, om, oc, q, Yt);
+    sketch<T>(S, sdata, n, kind, om, oc, ol, q, Yt);
     double* Qt = ws.alloc_n<double>(In * K);
     qr_y(Yt, In, In, K, In, Qt, In, nullptr, false, 0);
     int64_t ldqt;
@@ -419,10 +413,10 @@ void Engine::sthosvd(const TView& X, const int64_t* R, int q, int kind, const vo
   ws.rewind(mk);
 }
 
-template void Engine::sketch<float>(const TView&, const float*, int, int, const void* const*, const int64_t*, int,
-                                    double*);
+template void Engine::sketch<float>(const TView&, const float*, int, int, const void* const*, const int64_t*,
+                                    const int64_t*, int, double*);
 template void Engine::sketch<double>(const TView&, const double*, int, int, const void* const*, const int64_t*,
-                                     int, double*);
+                                     const int64_t*, int, double*);
 template void Engine::qr_z<float>(float*, int64_t, int64_t, int64_t, int, bool, int64_t);
 template void Engine::qr_z<double>(double*, int64_t, int64_t, int64_t, int, bool, int64_t);
 template void Engine::qr_rows<float>(const float*, int64_t, int64_t, int, int64_t, double*, int64_t, double*,
@@ -438,12 +432,13 @@ template void Engine::rel_error<float>(const TView&, const float*, const double*
 template void Engine::rel_error<double>(const TView&, const double*, const double*, const int64_t*,
                                         const double* const*, double*, double*);
 template void Engine::hosvd<float>(const TView&, const int64_t*, int, int, const void* const*, const int64_t*,
-                                   double* const*, double*, double*, double*);
+                                   const int64_t*, double* const*, double*, double*, double*);
 template void Engine::hosvd<double>(const TView&, const int64_t*, int, int, const void* const*, const int64_t*,
-                                    double* const*, double*, double*, double*);
+                                    const int64_t*, double* const*, double*, double*, double*);
 template void Engine::sthosvd<float>(const TView&, const int64_t*, int, int, const void* const*, const int64_t*,
-                                     const int*, double* const*, double*, double*, double*);
+                                     const int64_t*, const int*, double* const*, double*, double*, double*);
 template void Engine::sthosvd<double>(const TView&, const int64_t*, int, int, const void* const*,
-                                      const int64_t*, const int*, double* const*, double*, double*, double*);
+                                      const int64_t*, const int64_t*, const int*, double* const*, double*, double*,
+                                      double*);
 
 }  // namespace rt

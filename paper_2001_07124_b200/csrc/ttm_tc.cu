@@ -8,12 +8,15 @@
 //
 // Per CTA (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + single-thread MMA
 // issuer, warps 2-5 = "splitters" (one TMEM lane = one tile row each) that turn the raw fp32 X
-// tile (TMA -> smem) into hi/lo tf32 operands in TMEM (tcgen05.st) and split B in place, and that
-// drain the fp32 accumulators (tcgen05.ld) in the epilogue.  A comes from TMEM, B from shared
-// memory in the K-major SWIZZLE_NONE canonical layout: written directly by a permuted-stride TMA
-// box when B is column-major (Z, Q), or transposed by the splitters from a row-major TMA tile
-// (Omega; MN-major tf32 B operands were measured not to work with A in TMEM, tools/tc_probe.cu).
-// Pipelines: NS-stage smem/TMEM ring (full -> ready -> consumed), double-buffered accumulators.
+// tile (TMA -> smem) into hi/lo tf32 operands in TMEM (tcgen05.st), split B in place, and drain
+// the fp32 accumulators (tcgen05.ld) in the epilogue.  A comes from TMEM; B (always a
+// column-major fp32 matrix: Omega, Z or Q) is TMA'd as a [NPAD rows][32 K] 128B-swizzled tile,
+// i.e. directly the K-major SWIZZLE_128B UMMA canonical layout (tools/tc_probe.cu verifies the
+// descriptor; MN-major tf32 B operands were measured not to work with A in TMEM).
+// Pipelines: NS-stage smem/TMEM ring (full -> ready -> consumed) and double-buffered TMEM
+// accumulators drained every `seg` stages into fp32 registers: the tensor core's fp32 accumulation
+// error grows with the accumulation length (7.5e-6 relative after 1024 terms, 2.6e-5 after 3.5K;
+// 1.4e-6 when drained every 128, tests/test_gpu_tc.py).
 #include <cstring>
 
 #include "kernels.h"
@@ -26,70 +29,48 @@ using namespace tc;
 constexpr int KC = 32;           // contraction elements per stage
 constexpr int BM = 128;          // tile rows = TMEM lanes
 constexpr int NTHREADS = 192;
-__host__ __device__ constexpr uint32_t kAccCol(int b) { return b ? 128u : 0u; }
-constexpr uint32_t kAStage = 256;  // A stage s: hi at kAStage + 64 s, lo at + 32
+constexpr uint32_t kAStage = 256;  // TMEM: accumulators at columns 0 and 128, A stage s at 256 + 64 s
 
-// Shared memory plan: per stage a raw X tile, the K-major B operand (hi), optionally B lo and
-// the raw row-major B tile (BRAW).  NS = 4 stages when they fit in ~200 KB, else 3.
-template <int NPAD, bool BSPLIT, bool BRAW>
+__host__ __device__ constexpr uint32_t acc_col(int b) { return b ? 128u : 0u; }
+
+// Shared memory plan: per stage a raw X tile (16 KB), the B tile (hi, NPAD x 128 B) and
+// optionally B lo.  NS = 4 stages when they fit in ~200 KB, else 3.  All stage buffers are
+// 1024-byte aligned (128B swizzle atoms).
+template <int NPAD, bool BSPLIT>
 struct Smem {
-  static constexpr size_t kX = size_t(BM) * KC * 4;          // 16 KB raw X tile
-  static constexpr size_t kB = size_t(NPAD) * KC * 4;        // B tile
-  static constexpr size_t per_stage = kX + kB * (1 + (BSPLIT ? 1 : 0) + (BRAW ? 1 : 0));
+  static constexpr uint32_t kX = uint32_t(BM) * KC * 4;
+  static constexpr uint32_t kB = uint32_t(NPAD) * KC * 4;
+  static constexpr uint32_t per_stage = kX + kB * (BSPLIT ? 2 : 1);
   static constexpr int NS = per_stage * 4 <= 200 * 1024 ? 4 : 3;
-  static constexpr size_t off_x = 0;
-  static constexpr size_t off_b = off_x + NS * kX;
-  static constexpr size_t off_blo = off_b + NS * kB;
-  static constexpr size_t off_braw = off_blo + (BSPLIT ? NS * kB : 0);
-  static constexpr size_t off_bar = off_braw + (BRAW ? NS * kB : 0);
-  static constexpr size_t bytes = off_bar + 8 * (3 * NS + 4) + 16 + 1024;   // + alignment slack
+  static constexpr uint32_t off_x = 0;
+  static constexpr uint32_t off_b = off_x + NS * kX;
+  static constexpr uint32_t off_blo = off_b + NS * kB;
+  static constexpr uint32_t off_bar = off_blo + (BSPLIT ? NS * kB : 0);
+  static constexpr uint32_t bytes = off_bar + 8 * (3 * NS + 4) + 16;
 };
 
-struct Bars {
-  uint64_t* full;
-  uint64_t* ready;
-  uint64_t* consumed;
-  uint64_t* acc_full;
-  uint64_t* acc_empty;
-  uint32_t* tmem_base;
-};
-
-template <class L>
-__device__ __forceinline__ char* setup(char* raw, Bars& bars) {
-  constexpr int NS = L::NS;
-  char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* b = reinterpret_cast<uint64_t*>(base + L::off_bar);
-  bars.full = b;
-  bars.ready = b + NS;
-  bars.consumed = b + 2 * NS;
-  bars.acc_full = b + 3 * NS;
-  bars.acc_empty = b + 3 * NS + 2;
-  bars.tmem_base = reinterpret_cast<uint32_t*>(b + 3 * NS + 4);
-  return base;
+// K-major SWIZZLE_128B descriptor of a [rows][32 fp32] tile, advanced to k-step kk (8 elements)
+__device__ __forceinline__ uint64_t bdesc_sw128(uint32_t saddr, int kk) {
+  return sdesc(saddr + 32u * uint32_t(kk), 16u, 1024u) | (uint64_t(2) << 61);
 }
 
-// B descriptor for k-step kk of a stage buffer: K-major, element (n, k) at
-// (k/4)*(NPAD*16) + n*16 + (k%4)*4 bytes  (LBO = NPAD*16 between K-chunks, SBO = 128 between 8-row groups)
-template <int NPAD>
-__device__ __forceinline__ uint64_t bdesc(uint32_t saddr, int kk) {
-  return sdesc(saddr + uint32_t(kk) * 2u * NPAD * 16u, /*lbo*/ NPAD * 16u, /*sbo*/ 128u);
-}
-
-// Splitter: read this thread's row of the raw X tile, write hi/lo tf32 to TMEM A stage.
+// Splitter: read this thread's row of the raw X tile, write hi/lo tf32 to its TMEM lane.
+//   AMN  : tile [KC][BM] (row r is a column): element (r, k) at k*BM + r
+//   !AMN : tile [BM][KC] with 128B swizzle: 16B chunk c of row r at ((c ^ (r&7)) << 4)
 template <bool AMN>
 __device__ __forceinline__ void split_row_to_tmem(const float* xs, int r, uint32_t t_hi) {
   uint32_t hi[16], lo[16];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    if (AMN) {  // tile [KC][BM], row r is a column: element (r, k) at k*BM + r
+    if (AMN) {
 #pragma unroll
       for (int q = 0; q < 16; ++q) split_tf32(xs[(16 * h + q) * BM + r], hi[q], lo[q]);
-    } else {    // tile [BM][KC] with 128B swizzle: 16B chunk c of row r at ((c ^ (r&7)) << 4)
-      const char* row = reinterpret_cast<const char*>(xs) + r * 128;
+    } else {
+      const float* row = xs + r * KC;
 #pragma unroll
       for (int c4 = 0; c4 < 4; ++c4) {
         const int c = 4 * h + c4;
-        const float4 v = *reinterpret_cast<const float4*>(row + ((c ^ (r & 7)) << 4));
+        const float4 v = *reinterpret_cast<const float4*>(row + ((c ^ (r & 7)) << 2));
         split_tf32(v.x, hi[4 * c4 + 0], lo[4 * c4 + 0]);
         split_tf32(v.y, hi[4 * c4 + 1], lo[4 * c4 + 1]);
         split_tf32(v.z, hi[4 * c4 + 2], lo[4 * c4 + 2]);
@@ -101,14 +82,14 @@ __device__ __forceinline__ void split_row_to_tmem(const float* xs, int r, uint32
   }
 }
 
-// Split the B tile in place (hi) and write lo; elementwise, layout-agnostic.
+// Split the B tile in place (hi) and write lo; elementwise, layout-agnostic, conflict-free.
 template <int NPAD>
 __device__ __forceinline__ void split_b(float* b, float* blo, int t) {
   float4* b4 = reinterpret_cast<float4*>(b);
   float4* l4 = reinterpret_cast<float4*>(blo);
 #pragma unroll
   for (int q = 0; q < NPAD * KC / 4 / 128; ++q) {
-    float4 v = b4[t + 128 * q];
+    const float4 v = b4[t + 128 * q];
     uint32_t h0, h1, h2, h3, l0, l1, l2, l3;
     split_tf32(v.x, h0, l0);
     split_tf32(v.y, h1, l1);
@@ -119,40 +100,38 @@ __device__ __forceinline__ void split_b(float* b, float* blo, int t) {
   }
 }
 
-// Transpose the raw row-major B tile [KC j][NPAD n] into the K-major operand (+ optional hi/lo split).
-template <int NPAD, bool BSPLIT>
-__device__ __forceinline__ void transpose_b(const float* raw, float* bhi, float* blo, int t) {
-  for (int e = t; e < NPAD * (KC / 4); e += 128) {
-    const int n = e % NPAD, jg = e / NPAD;
-    float v[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) v[q] = raw[(4 * jg + q) * NPAD + n];
-    float4* dh = reinterpret_cast<float4*>(bhi) + (jg * NPAD + n);
-    if (BSPLIT) {
-      uint32_t h[4], l[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) split_tf32(v[q], h[q], l[q]);
-      *dh = make_float4(__uint_as_float(h[0]), __uint_as_float(h[1]), __uint_as_float(h[2]), __uint_as_float(h[3]));
-      *(reinterpret_cast<float4*>(blo) + (jg * NPAD + n)) =
-          make_float4(__uint_as_float(l[0]), __uint_as_float(l[1]), __uint_as_float(l[2]), __uint_as_float(l[3]));
-    } else {
-      *dh = make_float4(v[0], v[1], v[2], v[3]);
-    }
-  }
-}
-
-// MMA issue for one stage: 4 k-steps x (2 or 3) products into accumulator `acc`.
-template <int NPAD, bool BSPLIT>
+// One stage: 4 k-steps x (2 or 3) products into accumulator column `acc`.
+template <bool BSPLIT>
 __device__ __forceinline__ void issue_stage(uint32_t tmem, uint32_t acc, int s, uint32_t b_saddr, uint32_t blo_saddr,
                                             uint32_t idesc, bool first) {
   const uint32_t a_hi = tmem + kAStage + 64u * s;
 #pragma unroll
   for (int kk = 0; kk < KC / 8; ++kk) {
-    const uint64_t bd = bdesc<NPAD>(b_saddr, kk);
+    const uint64_t bd = bdesc_sw128(b_saddr, kk);
     mma_tf32_ts(tmem + acc, a_hi + 8 * kk, bd, idesc, (first && kk == 0) ? 0u : 1u);
     mma_tf32_ts(tmem + acc, a_hi + 32 + 8 * kk, bd, idesc, 1u);
-    if (BSPLIT) mma_tf32_ts(tmem + acc, a_hi + 8 * kk, bdesc<NPAD>(blo_saddr, kk), idesc, 1u);
+    if (BSPLIT) mma_tf32_ts(tmem + acc, a_hi + 8 * kk, bdesc_sw128(blo_saddr, kk), idesc, 1u);
   }
+}
+
+// Ring position: stage index and parity of the current round.
+struct Ring {
+  int s = 0;
+  uint32_t ph = 0;
+  template <int NS> __device__ __forceinline__ void next() { if (++s == NS) { s = 0; ph ^= 1; } }
+};
+
+__device__ __forceinline__ void init_barriers(uint64_t* bar, int NS) {
+  for (int s = 0; s < NS; ++s) {
+    mbar_init(&bar[s], 1);               // full
+    mbar_init(&bar[NS + s], 128);        // ready
+    mbar_init(&bar[2 * NS + s], 1);      // consumed
+  }
+  for (int b = 0; b < 2; ++b) {
+    mbar_init(&bar[3 * NS + b], 1);      // acc_full
+    mbar_init(&bar[3 * NS + 2 + b], 128);  // acc_empty
+  }
+  fence_barrier_init();
 }
 
 // ====================================================================== ttm_s
@@ -166,85 +145,77 @@ struct SParams {
   float* part;        // [split][K][I]
 };
 
-// BRAW: B is row-major (Omega): TMA a [KC][NPAD] tile, splitters transpose it to K-major.
-template <int NPAD, bool BSPLIT, bool AMN, bool BRAW>
+template <int NPAD, bool BSPLIT, bool AMN>
 __global__ void __launch_bounds__(NTHREADS, 1)
 ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb, const SParams p) {
-  using L = Smem<NPAD, BSPLIT, BRAW>;
+  using L = Smem<NPAD, BSPLIT>;
   constexpr int NS = L::NS;
-  extern __shared__ char smem_raw[];
-  Bars bars;
-  char* sm = setup<L>(smem_raw, bars);
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::off_bar);
+  uint64_t* full = bar;
+  uint64_t* ready = bar + NS;
+  uint64_t* consumed = bar + 2 * NS;
+  uint64_t* acc_full = bar + 3 * NS;
+  uint64_t* acc_empty = bar + 3 * NS + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 3 * NS + 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t i0 = int64_t(blockIdx.x) * BM;
   const int64_t c_begin = int64_t(blockIdx.y) * p.cps;
   const int64_t c_end = min(p.nchunks, c_begin + p.cps);
   const int nch = c_end > c_begin ? int(c_end - c_begin) : 0;
-  const int nunits = (nch + p.seg - 1) / p.seg;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < NS; ++s) {
-      mbar_init(&bars.full[s], 1);
-      mbar_init(&bars.ready[s], 128);
-      mbar_init(&bars.consumed[s], 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&bars.acc_full[b], 1);
-      mbar_init(&bars.acc_empty[b], 128);
-    }
-    fence_barrier_init();
+    init_barriers(bar, NS);
     tma_prefetch(&tmx);
     tma_prefetch(&tmb);
   }
-  if (warp == 1) tmem_alloc(bars.tmem_base, 512);
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *bars.tmem_base;
+  const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {
-      const uint32_t bytes = uint32_t(L::kX + L::kB);
-      for (int it = 0; it < nch; ++it) {
-        const int s = it % NS;
-        if (it >= NS) mbar_wait(&bars.consumed[s], ((it / NS) - 1) & 1);
-        const int64_t c = c_begin + it;
-        mbar_expect_tx(&bars.full[s], bytes);
-        float* xs = reinterpret_cast<float*>(sm + L::off_x + s * L::kX);
-        float* bs = reinterpret_cast<float*>(sm + (BRAW ? L::off_braw : L::off_b) + s * L::kB);
+    if (lane == 0) {                                   // ---------------- TMA producer
+      Ring rg;
+      int64_t beta = c_begin / p.cpb, a0 = (c_begin % p.cpb) * KC;
+      for (int it = 0; it < nch; ++it, rg.next<NS>()) {
+        if (it >= NS) mbar_wait(&consumed[rg.s], rg.ph ^ 1);
+        mbar_expect_tx(&full[rg.s], L::kX + L::kB);
+        float* xs = reinterpret_cast<float*>(smem + L::off_x + rg.s * L::kX);
+        float* bs = reinterpret_cast<float*>(smem + L::off_b + rg.s * L::kB);
         int64_t j0;
         if (AMN) {
-          j0 = c * KC;
-          tma_load_2d(xs, &tmx, &bars.full[s], int(i0), int(j0));
+          j0 = (c_begin + it) * KC;
+          tma_load_2d(xs, &tmx, &full[rg.s], int(i0), int(j0));
         } else {
-          const int64_t beta = c / p.cpb, a0 = (c % p.cpb) * KC;
           j0 = a0 + p.a * beta;
-          tma_load_3d(xs, &tmx, &bars.full[s], int(a0), int(i0), int(beta));
+          tma_load_3d(xs, &tmx, &full[rg.s], int(a0), int(i0), int(beta));
+          a0 += KC;
+          if (a0 >= p.a) { a0 = 0; ++beta; }
         }
-        if (BRAW) tma_load_2d(bs, &tmb, &bars.full[s], 0, int(j0));
-        else tma_load_3d(bs, &tmb, &bars.full[s], 0, 0, int(j0 / 4));
+        tma_load_2d(bs, &tmb, &full[rg.s], int(j0), 0);
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (lane == 0) {                                   // ---------------- MMA issuer
       const uint32_t idesc = idesc_tf32(BM, NPAD, 0);
-      for (int it = 0; it < nch; ++it) {
-        const int s = it % NS;
-        const int u = it / p.seg;
-        const bool first = (it % p.seg) == 0;
-        const bool last = ((it % p.seg) == p.seg - 1) || (it == nch - 1);
+      Ring rg;
+      int u = 0, pos = 0;
+      for (int it = 0; it < nch; ++it, rg.next<NS>()) {
+        const bool first = pos == 0;
+        const bool last = (pos == p.seg - 1) || (it == nch - 1);
         const int ab = u & 1;
-        if (first && u >= 2) mbar_wait(&bars.acc_empty[ab], ((u >> 1) - 1) & 1);
-        mbar_wait(&bars.ready[s], (it / NS) & 1);
+        if (first && u >= 2) mbar_wait(&acc_empty[ab], ((u >> 1) - 1) & 1);
+        mbar_wait(&ready[rg.s], rg.ph);
         tc_fence_after();
-        issue_stage<NPAD, BSPLIT>(tmem, kAccCol(ab), s, smem_u32(sm + L::off_b + s * L::kB),
-                                  smem_u32(sm + L::off_blo + s * L::kB), idesc, first);
-        mma_commit(&bars.consumed[s]);
-        if (last) mma_commit(&bars.acc_full[ab]);
+        issue_stage<BSPLIT>(tmem, acc_col(ab), rg.s, smem_u32(smem + L::off_b + rg.s * L::kB),
+                            smem_u32(smem + L::off_blo + rg.s * L::kB), idesc, first);
+        mma_commit(&consumed[rg.s]);
+        if (last) { mma_commit(&acc_full[ab]); ++u; pos = 0; } else { ++pos; }
       }
     }
-  } else {
-    // splitters / epilogue: 128 threads, TMEM lane quarter = warp % 4
+  } else {                                             // ---------------- splitters / epilogue
     const int q4 = warp & 3;
     const int r = 32 * q4 + lane;
     const uint32_t lane_base = tmem + (uint32_t(32 * q4) << 16);
@@ -254,42 +225,43 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
     for (int k = 0; k < NPAD; ++k) sums[k] = 0.f;
     auto epilogue = [&](int u) {
       const int ab = u & 1;
-      mbar_wait(&bars.acc_full[ab], (u >> 1) & 1);
+      mbar_wait(&acc_full[ab], (u >> 1) & 1);
       tc_fence_after();
 #pragma unroll
       for (int cb = 0; cb < NPAD / 16; ++cb) {
         uint32_t v[16];
-        tmem_ld16(lane_base + kAccCol(ab) + 16 * cb, v);
+        tmem_ld16(lane_base + acc_col(ab) + 16 * cb, v);
         tmem_wait_ld();
 #pragma unroll
         for (int q = 0; q < 16; ++q) sums[16 * cb + q] += __uint_as_float(v[q]);
       }
       tc_fence_before();
-      mbar_arrive(&bars.acc_empty[ab]);
+      mbar_arrive(&acc_empty[ab]);
     };
-    for (int it = 0; it < nch; ++it) {
-      const int s = it % NS;
-      mbar_wait(&bars.full[s], (it / NS) & 1);
-      const float* xs = reinterpret_cast<const float*>(sm + L::off_x + s * L::kX);
-      split_row_to_tmem<AMN>(xs, r, lane_base + kAStage + 64u * s);
-      if (BRAW)
-        transpose_b<NPAD, BSPLIT>(reinterpret_cast<const float*>(sm + L::off_braw + s * L::kB),
-                                  reinterpret_cast<float*>(sm + L::off_b + s * L::kB),
-                                  reinterpret_cast<float*>(sm + L::off_blo + s * L::kB), t);
-      else if (BSPLIT)
-        split_b<NPAD>(reinterpret_cast<float*>(sm + L::off_b + s * L::kB),
-                      reinterpret_cast<float*>(sm + L::off_blo + s * L::kB), t);
+    Ring rg;
+    int u = 0, pos = 0;
+    for (int it = 0; it < nch; ++it, rg.next<NS>()) {
+      mbar_wait(&full[rg.s], rg.ph);
+      split_row_to_tmem<AMN>(reinterpret_cast<const float*>(smem + L::off_x + rg.s * L::kX), r,
+                             lane_base + kAStage + 64u * rg.s);
+      if (BSPLIT)
+        split_b<NPAD>(reinterpret_cast<float*>(smem + L::off_b + rg.s * L::kB),
+                      reinterpret_cast<float*>(smem + L::off_blo + rg.s * L::kB), t);
       tmem_wait_st();
       fence_proxy_async();
       tc_fence_before();
-      mbar_arrive(&bars.ready[s]);
-      const bool last = ((it % p.seg) == p.seg - 1) || (it == nch - 1);
-      const int u = it / p.seg;
-      if (last && u >= 1) epilogue(u - 1);
+      mbar_arrive(&ready[rg.s]);
+      const bool last = (pos == p.seg - 1) || (it == nch - 1);
+      if (last) {
+        if (u >= 1) epilogue(u - 1);
+        ++u;
+        pos = 0;
+      } else {
+        ++pos;
+      }
     }
-    if (nunits >= 1) epilogue(nunits - 1);
-    // partial tile -> part[split][k][i]
-    const int64_t i = i0 + r;
+    if (u >= 1) epilogue(u - 1);
+    const int64_t i = i0 + r;                         // partial tile -> part[split][k][i]
     if (i < p.I) {
       float* dst = p.part + int64_t(blockIdx.y) * p.K * p.I;
 #pragma unroll
@@ -310,7 +282,7 @@ struct TParams {
   int64_t tpb;        // tiles per beta (a > 1)
   int64_t ntiles;
   int nic;            // i-chunks per tile
-  int seg;            // i-chunks per accumulator segment (fp32 TMEM accumulation length)
+  int seg;            // i-chunks per accumulator segment
   float* out;
   int64_t so_a, so_c, so_b;
 };
@@ -319,35 +291,29 @@ template <int NPAD, bool AKM>   // AKM: mode 0 (a == 1), X tile K-major [BM j][K
 __global__ void __launch_bounds__(NTHREADS, 1)
 ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb, const TParams p) {
   constexpr bool BSPLIT = true;
-  using L = Smem<NPAD, BSPLIT, false>;
+  using L = Smem<NPAD, BSPLIT>;
   constexpr int NS = L::NS;
-  extern __shared__ char smem_raw[];
-  Bars bars;
-  char* sm = setup<L>(smem_raw, bars);
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::off_bar);
+  uint64_t* full = bar;
+  uint64_t* ready = bar + NS;
+  uint64_t* consumed = bar + 2 * NS;
+  uint64_t* acc_full = bar + 3 * NS;
+  uint64_t* acc_empty = bar + 3 * NS + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 3 * NS + 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t my_tiles = (p.ntiles > blockIdx.x) ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int64_t total = my_tiles * p.nic;
-  const int64_t nseg_t = (p.nic + p.seg - 1) / p.seg;     // segments per tile
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < NS; ++s) {
-      mbar_init(&bars.full[s], 1);
-      mbar_init(&bars.ready[s], 128);
-      mbar_init(&bars.consumed[s], 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&bars.acc_full[b], 1);
-      mbar_init(&bars.acc_empty[b], 128);
-    }
-    fence_barrier_init();
+    init_barriers(bar, NS);
     tma_prefetch(&tmx);
     tma_prefetch(&tmb);
   }
-  if (warp == 1) tmem_alloc(bars.tmem_base, 512);
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *bars.tmem_base;
+  const uint32_t tmem = *tmem_slot;
 
   auto tile_coords = [&](int64_t tile, int64_t& a0, int64_t& beta) {
     if (AKM) { a0 = 0; beta = tile * BM; }
@@ -355,43 +321,46 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
   };
 
   if (warp == 0) {
-    if (lane == 0) {
-      const uint32_t bytes = uint32_t(L::kX + L::kB);
-      for (int64_t it = 0; it < total; ++it) {
-        const int s = int(it % NS);
-        if (it >= NS) mbar_wait(&bars.consumed[s], uint32_t((it / NS) - 1) & 1);
-        const int64_t tile = blockIdx.x + (it / p.nic) * gridDim.x;
-        const int ic = int(it % p.nic) * KC;
+    if (lane == 0) {                                   // ---------------- TMA producer
+      Ring rg;
+      int it = 0;
+      for (int64_t u = 0; u < my_tiles; ++u) {
         int64_t a0, beta;
-        tile_coords(tile, a0, beta);
-        mbar_expect_tx(&bars.full[s], bytes);
-        float* xs = reinterpret_cast<float*>(sm + L::off_x + s * L::kX);
-        float* bs = reinterpret_cast<float*>(sm + L::off_b + s * L::kB);
-        if (AKM) tma_load_2d(xs, &tmx, &bars.full[s], ic, int(beta));
-        else tma_load_3d(xs, &tmx, &bars.full[s], int(a0), ic, int(beta));
-        tma_load_3d(bs, &tmb, &bars.full[s], 0, 0, ic / 4);
+        tile_coords(blockIdx.x + u * gridDim.x, a0, beta);
+        for (int c = 0; c < p.nic; ++c, ++it, rg.next<NS>()) {
+          if (it >= NS) mbar_wait(&consumed[rg.s], rg.ph ^ 1);
+          mbar_expect_tx(&full[rg.s], L::kX + L::kB);
+          float* xs = reinterpret_cast<float*>(smem + L::off_x + rg.s * L::kX);
+          float* bs = reinterpret_cast<float*>(smem + L::off_b + rg.s * L::kB);
+          const int ic = c * KC;
+          if (AKM) tma_load_2d(xs, &tmx, &full[rg.s], ic, int(beta));
+          else tma_load_3d(xs, &tmx, &full[rg.s], int(a0), ic, int(beta));
+          tma_load_2d(bs, &tmb, &full[rg.s], ic, 0);
+        }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (lane == 0) {                                   // ---------------- MMA issuer
       const uint32_t idesc = idesc_tf32(BM, NPAD, 0);
-      for (int64_t it = 0; it < total; ++it) {
-        const int s = int(it % NS);
-        const int c = int(it % p.nic);
-        const int64_t g = (it / p.nic) * nseg_t + c / p.seg;     // global segment index
-        const bool first = (c % p.seg) == 0;
-        const bool last = (c % p.seg) == p.seg - 1 || c == p.nic - 1;
-        const int ab = int(g & 1);
-        if (first && g >= 2) mbar_wait(&bars.acc_empty[ab], uint32_t((g >> 1) - 1) & 1);
-        mbar_wait(&bars.ready[s], uint32_t(it / NS) & 1);
-        tc_fence_after();
-        issue_stage<NPAD, BSPLIT>(tmem, kAccCol(ab), s, smem_u32(sm + L::off_b + s * L::kB),
-                                  smem_u32(sm + L::off_blo + s * L::kB), idesc, first);
-        mma_commit(&bars.consumed[s]);
-        if (last) mma_commit(&bars.acc_full[ab]);
+      Ring rg;
+      int64_t g = 0;                                   // global segment counter
+      for (int64_t u = 0; u < my_tiles; ++u) {
+        int pos = 0;
+        for (int c = 0; c < p.nic; ++c, rg.next<NS>()) {
+          const bool first = pos == 0;
+          const bool last = (pos == p.seg - 1) || (c == p.nic - 1);
+          const int ab = int(g & 1);
+          if (first && g >= 2) mbar_wait(&acc_empty[ab], uint32_t((g >> 1) - 1) & 1);
+          mbar_wait(&ready[rg.s], rg.ph);
+          tc_fence_after();
+          issue_stage<BSPLIT>(tmem, acc_col(ab), rg.s, smem_u32(smem + L::off_b + rg.s * L::kB),
+                              smem_u32(smem + L::off_blo + rg.s * L::kB), idesc, first);
+          mma_commit(&consumed[rg.s]);
+          if (last) { mma_commit(&acc_full[ab]); ++g; pos = 0; } else { ++pos; }
+        }
       }
     }
-  } else {
+  } else {                                             // ---------------- splitters / epilogue
     const int q4 = warp & 3;
     const int r = 32 * q4 + lane;
     const uint32_t lane_base = tmem + (uint32_t(32 * q4) << 16);
@@ -400,22 +369,21 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
 #pragma unroll
     for (int k = 0; k < NPAD; ++k) sums[k] = 0.f;
     // drain segment g into the register sums; after the last segment of a tile, store the tile
-    auto epilogue = [&](int64_t g) {
+    auto epilogue = [&](int64_t g, bool tile_end, int64_t tile) {
       const int ab = int(g & 1);
-      mbar_wait(&bars.acc_full[ab], uint32_t(g >> 1) & 1);
+      mbar_wait(&acc_full[ab], uint32_t(g >> 1) & 1);
       tc_fence_after();
 #pragma unroll
       for (int cb = 0; cb < NPAD / 16; ++cb) {
         uint32_t v[16];
-        tmem_ld16(lane_base + kAccCol(ab) + 16 * cb, v);
+        tmem_ld16(lane_base + acc_col(ab) + 16 * cb, v);
         tmem_wait_ld();
 #pragma unroll
         for (int q = 0; q < 16; ++q) sums[16 * cb + q] += __uint_as_float(v[q]);
       }
       tc_fence_before();
-      mbar_arrive(&bars.acc_empty[ab]);
-      if ((g % nseg_t) == nseg_t - 1) {
-        const int64_t tile = blockIdx.x + (g / nseg_t) * gridDim.x;
+      mbar_arrive(&acc_empty[ab]);
+      if (tile_end) {
         int64_t a0, beta;
         tile_coords(tile, a0, beta);
         bool valid;
@@ -431,23 +399,36 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
         for (int k = 0; k < NPAD; ++k) sums[k] = 0.f;
       }
     };
-    for (int64_t it = 0; it < total; ++it) {
-      const int s = int(it % NS);
-      mbar_wait(&bars.full[s], uint32_t(it / NS) & 1);
-      const float* xs = reinterpret_cast<const float*>(sm + L::off_x + s * L::kX);
-      split_row_to_tmem<!AKM>(xs, r, lane_base + kAStage + 64u * s);
-      split_b<NPAD>(reinterpret_cast<float*>(sm + L::off_b + s * L::kB),
-                    reinterpret_cast<float*>(sm + L::off_blo + s * L::kB), t);
-      tmem_wait_st();
-      fence_proxy_async();
-      tc_fence_before();
-      mbar_arrive(&bars.ready[s]);
-      const int c = int(it % p.nic);
-      const bool last = (c % p.seg) == p.seg - 1 || c == p.nic - 1;
-      const int64_t g = (it / p.nic) * nseg_t + c / p.seg;
-      if (last && g >= 1) epilogue(g - 1);
+    Ring rg;
+    int64_t g = 0;
+    bool prev_end = false;
+    int64_t prev_tile = 0;
+    for (int64_t u = 0; u < my_tiles; ++u) {
+      const int64_t tile = blockIdx.x + u * gridDim.x;
+      int pos = 0;
+      for (int c = 0; c < p.nic; ++c, rg.next<NS>()) {
+        mbar_wait(&full[rg.s], rg.ph);
+        split_row_to_tmem<!AKM>(reinterpret_cast<const float*>(smem + L::off_x + rg.s * L::kX), r,
+                                lane_base + kAStage + 64u * rg.s);
+        split_b<NPAD>(reinterpret_cast<float*>(smem + L::off_b + rg.s * L::kB),
+                      reinterpret_cast<float*>(smem + L::off_blo + rg.s * L::kB), t);
+        tmem_wait_st();
+        fence_proxy_async();
+        tc_fence_before();
+        mbar_arrive(&ready[rg.s]);
+        const bool last = (pos == p.seg - 1) || (c == p.nic - 1);
+        if (last) {
+          if (g >= 1) epilogue(g - 1, prev_end, prev_tile);   // delayed by one segment
+          prev_end = (c == p.nic - 1);
+          prev_tile = tile;
+          ++g;
+          pos = 0;
+        } else {
+          ++pos;
+        }
+      }
     }
-    if (my_tiles >= 1) epilogue(my_tiles * nseg_t - 1);
+    if (g >= 1) epilogue(g - 1, prev_end, prev_tile);
   }
   tc_fence_before();
   __syncthreads();
@@ -492,44 +473,44 @@ bool make_map(CUtensorMap* m, const void* ptr, int rank, const uint64_t* dims, c
 
 bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
-template <typename K>
-void set_smem(K kernel, size_t bytes) {
+// column-major fp32 matrix (rows x cols, ld) as a B operand: [npad][32] 128B-swizzled boxes
+bool make_b_map(CUtensorMap* m, const float* B, int64_t rows, int cols, int64_t ld, int npad) {
+  if (!aligned(B, 16) || (ld % 4) || ld < rows || rows > INT32_MAX) return false;
+  const uint64_t d[2] = {uint64_t(rows), uint64_t(cols)}, s[1] = {uint64_t(ld) * 4};
+  const uint32_t bx[2] = {KC, uint32_t(npad)};
+  return make_map(m, B, 2, d, s, bx, true);
+}
+
+template <typename Kern>
+void set_smem(Kern kernel, uint32_t bytes) {
   RT_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
 }
 
-template <int NPAD, bool BSPLIT, bool AMN, bool BRAW>
+template <int NPAD, bool BSPLIT, bool AMN>
 void launch_s(const Ctx& ctx, const CUtensorMap& tx, const CUtensorMap& tb, const SParams& p, dim3 grid) {
-  using L = Smem<NPAD, BSPLIT, BRAW>;
+  using L = Smem<NPAD, BSPLIT>;
   static bool attr = false;
-  if (!attr) { set_smem(ttm_s_tc_kernel<NPAD, BSPLIT, AMN, BRAW>, L::bytes); attr = true; }
+  if (!attr) { set_smem(ttm_s_tc_kernel<NPAD, BSPLIT, AMN>, L::bytes); attr = true; }
   launch(ctx, "ttm_s_tc", [&] {
-    ttm_s_tc_kernel<NPAD, BSPLIT, AMN, BRAW><<<grid, NTHREADS, L::bytes, ctx.stream>>>(tx, tb, p);
+    ttm_s_tc_kernel<NPAD, BSPLIT, AMN><<<grid, NTHREADS, L::bytes, ctx.stream>>>(tx, tb, p);
   });
 }
 
 template <int NPAD, bool BSPLIT>
-void dispatch_s(const Ctx& ctx, bool amn, bool braw, const CUtensorMap& tx, const CUtensorMap& tb,
-                const SParams& p, dim3 g) {
-  if (amn) {
-    if (braw) launch_s<NPAD, BSPLIT, true, true>(ctx, tx, tb, p, g);
-    else launch_s<NPAD, BSPLIT, true, false>(ctx, tx, tb, p, g);
-  } else {
-    if (braw) launch_s<NPAD, BSPLIT, false, true>(ctx, tx, tb, p, g);
-    else launch_s<NPAD, BSPLIT, false, false>(ctx, tx, tb, p, g);
-  }
+void dispatch_s(const Ctx& ctx, bool amn, const CUtensorMap& tx, const CUtensorMap& tb, const SParams& p, dim3 g) {
+  if (amn) launch_s<NPAD, BSPLIT, true>(ctx, tx, tb, p, g);
+  else launch_s<NPAD, BSPLIT, false>(ctx, tx, tb, p, g);
 }
 
 template <int NPAD, bool AKM>
 void launch_t(const Ctx& ctx, const CUtensorMap& tx, const CUtensorMap& tb, const TParams& p, dim3 grid) {
-  using L = Smem<NPAD, true, false>;
+  using L = Smem<NPAD, true>;
   static bool attr = false;
   if (!attr) { set_smem(ttm_t_tc_kernel<NPAD, AKM>, L::bytes); attr = true; }
   launch(ctx, "ttm_t_tc", [&] {
     ttm_t_tc_kernel<NPAD, AKM><<<grid, NTHREADS, L::bytes, ctx.stream>>>(tx, tb, p);
   });
 }
-
-}  // namespace
 
 __global__ void splitk_reduce_f32_kernel(const float* __restrict__ part, int64_t I, int K, int splits,
                                          double* __restrict__ Y, int64_t ldy) {
@@ -541,17 +522,19 @@ __global__ void splitk_reduce_f32_kernel(const float* __restrict__ part, int64_t
   Y[i + ldy * k] = s;
 }
 
-int tc_npad(int K) { return K <= 16 ? 16 : K <= 32 ? 32 : K <= 48 ? 48 : K <= 64 ? 64 : K <= 80 ? 80 : K <= 96 ? 96 : K <= 128 ? 128 : -1; }
+int tc_npad(int K) {
+  return K <= 16 ? 16 : K <= 32 ? 32 : K <= 48 ? 48 : K <= 64 ? 64 : K <= 80 ? 80 : K <= 96 ? 96 : K <= 128 ? 128 : -1;
+}
+
+}  // namespace
 
 // Returns false (nothing launched) when the shape/alignment is not supported by the TMA path.
-bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Bm, int64_t ldb, bool b_rowmajor,
-              bool b_tf32_exact, int K, double* Y, int64_t ldy) {
+bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Bm, int64_t ldb, bool b_tf32_exact,
+              int K, double* Y, int64_t ldy) {
   const int npad = tc_npad(K);
   if (npad < 0) return false;
   const int64_t J = box.J();
-  if (box.I < 1 || J < KC) return false;
-  if (!aligned(X, 16) || !aligned(Bm, 16)) return false;
-  if (ldb % 4 || (b_rowmajor && ldb < K) || (!b_rowmajor && ldb < J)) return false;
+  if (box.I < 1 || J < KC || !aligned(X, 16)) return false;
   const bool amn = (box.a == 1);
   if (amn ? (box.I % 4) : (box.a % 4)) return false;
   if (box.a > INT32_MAX || box.I > INT32_MAX || box.b > INT32_MAX || J > INT32_MAX) return false;
@@ -566,15 +549,7 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
     const uint32_t bx[3] = {KC, BM, 1};
     if (!make_map(&tx, X, 3, d, s, bx, true)) return false;
   }
-  if (b_rowmajor) {  // element (j, k) at j*ldb + k: raw [KC j][npad k] tile, transposed in smem
-    const uint64_t d[2] = {uint64_t(K), uint64_t(J)}, s[1] = {uint64_t(ldb) * 4};
-    const uint32_t bx[2] = {uint32_t(npad), KC};
-    if (!make_map(&tb, Bm, 2, d, s, bx, false)) return false;
-  } else {           // element (j, k) at j + ldb*k; canonical K-major via box (4 j, npad k, 8 j-groups)
-    const uint64_t d[3] = {4, uint64_t(K), uint64_t((J + 3) / 4)}, s[2] = {uint64_t(ldb) * 4, 16};
-    const uint32_t bx[3] = {4, uint32_t(npad), KC / 4};
-    if (!make_map(&tb, Bm, 3, d, s, bx, false)) return false;
-  }
+  if (!make_b_map(&tb, Bm, J, K, ldb, npad)) return false;
   SParams p;
   p.a = box.a; p.I = box.I; p.b = box.b; p.K = K;
   p.cpb = amn ? 1 : cdiv(box.a, KC);
@@ -589,10 +564,10 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
   p.part = ws.alloc_n<float>(splits * K * box.I);
   const dim3 grid{unsigned(mtiles), unsigned(splits), 1u};
   const bool bsplit = !b_tf32_exact;
-#define RT_S_CASE(NP)                                                   \
-  case NP:                                                              \
-    if (bsplit) dispatch_s<NP, true>(ctx, amn, b_rowmajor, tx, tb, p, grid);   \
-    else dispatch_s<NP, false>(ctx, amn, b_rowmajor, tx, tb, p, grid);         \
+#define RT_S_CASE(NP)                                              \
+  case NP:                                                         \
+    if (bsplit) dispatch_s<NP, true>(ctx, amn, tx, tb, p, grid);   \
+    else dispatch_s<NP, false>(ctx, amn, tx, tb, p, grid);         \
     break;
   switch (npad) {
     RT_S_CASE(16) RT_S_CASE(32) RT_S_CASE(48) RT_S_CASE(64) RT_S_CASE(80) RT_S_CASE(96) RT_S_CASE(128)
@@ -611,7 +586,7 @@ bool ttm_t_tc(const Ctx& ctx, const float* X, Box box, const float* Q, int64_t l
   const int npad = tc_npad(C);
   if (npad < 0) return false;
   const bool akm = (box.a == 1);
-  if (!aligned(X, 16) || !aligned(Q, 16) || ldq % 4 || ldq < box.I) return false;
+  if (!aligned(X, 16)) return false;
   if (akm ? (box.I % 4) : (box.a % 4)) return false;
   if (box.a > INT32_MAX || box.I > INT32_MAX || box.b > INT32_MAX) return false;
   CUtensorMap tx, tb;
@@ -625,11 +600,7 @@ bool ttm_t_tc(const Ctx& ctx, const float* X, Box box, const float* Q, int64_t l
     const uint32_t bx[3] = {BM, KC, 1};
     if (!make_map(&tx, X, 3, d, s, bx, false)) return false;
   }
-  {  // Q(i, c) at i + ldq*c, K-major canonical via box (4 i, npad c, 8 i-groups)
-    const uint64_t d[3] = {4, uint64_t(C), uint64_t((box.I + 3) / 4)}, s[2] = {uint64_t(ldq) * 4, 16};
-    const uint32_t bx[3] = {4, uint32_t(npad), KC / 4};
-    if (!make_map(&tb, Q, 3, d, s, bx, false)) return false;
-  }
+  if (!make_b_map(&tb, Q, box.I, C, ldq, npad)) return false;
   TParams p;
   p.a = box.a; p.I = box.I; p.b = box.b; p.C = C;
   p.tpb = akm ? 1 : cdiv(box.a, BM);
@@ -638,10 +609,10 @@ bool ttm_t_tc(const Ctx& ctx, const float* X, Box box, const float* Q, int64_t l
   p.seg = std::max(1, ctx.tc_seg);
   p.out = out; p.so_a = so_a; p.so_c = so_c; p.so_b = so_b;
   const int64_t grid = std::min<int64_t>(p.ntiles, ctx.num_sms);
-#define RT_T_CASE(NP)                                                           \
-  case NP:                                                                      \
-    if (akm) launch_t<NP, true>(ctx, tx, tb, p, dim3(unsigned(grid)));         \
-    else launch_t<NP, false>(ctx, tx, tb, p, dim3(unsigned(grid)));            \
+#define RT_T_CASE(NP)                                                     \
+  case NP:                                                                \
+    if (akm) launch_t<NP, true>(ctx, tx, tb, p, dim3(unsigned(grid)));   \
+    else launch_t<NP, false>(ctx, tx, tb, p, dim3(unsigned(grid)));      \
     break;
   switch (npad) {
     RT_T_CASE(16) RT_T_CASE(32) RT_T_CASE(48) RT_T_CASE(64) RT_T_CASE(80) RT_T_CASE(96) RT_T_CASE(128)

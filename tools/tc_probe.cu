@@ -106,6 +106,58 @@ __global__ void probe_tma(const __grid_constant__ CUtensorMap m, float* out, int
   for (int i = threadIdx.x; i < 80 * 32; i += blockDim.x) out[i] = buf[i];
 }
 
+
+// ---- probe 4: K-major SWIZZLE_128B B operand (N rows x 32 K, 128 B per row), 4 k-steps of 8
+template <int N>
+__global__ void probe_mma_sw128(const float* A, const float* B, float* D) {
+  __shared__ __align__(1024) float bs[N * 32];
+  __shared__ uint32_t tbase;
+  __shared__ __align__(8) uint64_t bar;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int e = threadIdx.x; e < N * 32; e += blockDim.x) {
+    const int n = e / 32, k = e % 32;                 // B(k, n)
+    const int chunk = k / 4, within = k % 4;
+    const int off = n * 32 + ((chunk ^ (n % 8)) * 4) + within;   // row n: 128 B, 16B chunks XOR (n%8)
+    bs[off] = B[k * N + n];
+  }
+  if (warp == 0) tmem_alloc(&tbase, 256);
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tl = tbase + (uint32_t(32 * warp) << 16);
+  {
+    uint32_t v[16];
+    for (int h = 0; h < 2; ++h) {
+      for (int i = 0; i < 16; ++i) v[i] = __float_as_uint(A[(32 * warp + lane) * 32 + 16 * h + i]);
+      tmem_st16(tl + 128 + 16 * h, v);
+    }
+    tmem_wait_st();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x == 0) {
+    for (int kk = 0; kk < 4; ++kk) {
+      const uint64_t bd = sdesc(smem_u32(bs) + 32 * kk, 16, 1024) | (uint64_t(2) << 61);
+      mma_tf32_ts(tbase, tbase + 128 + 8 * kk, bd, idesc_tf32(128, N, 0), kk > 0);
+    }
+    mma_commit(&bar);
+  }
+  mbar_wait(&bar, 0);
+  tc_fence_after();
+  for (int c = 0; c < N; c += 16) {
+    uint32_t v[16];
+    tmem_ld16(tl + c, v);
+    tmem_wait_ld();
+    for (int i = 0; i < 16; ++i) D[(32 * warp + lane) * N + c + i] = __uint_as_float(v[i]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tbase, 256);
+}
+
 int main() {
   int dev = 0;
   CK(cudaSetDevice(dev));
@@ -177,6 +229,27 @@ int main() {
         }
       printf("probe_tma layout: %s (%d bad)\n", bad ? "FAIL" : "ok", bad);
     }
+  }
+  {
+    constexpr int N = 80;
+    std::vector<float> A(128 * 32), B(32 * N), D(128 * N), R(128 * N, 0.f);
+    for (int i = 0; i < 128 * 32; ++i) A[i] = float((i * 7) % 13) - 6.f;
+    for (int i = 0; i < 32 * N; ++i) B[i] = float((i * 5) % 11) - 5.f;
+    for (int r = 0; r < 128; ++r)
+      for (int n = 0; n < N; ++n)
+        for (int k = 0; k < 32; ++k) R[r * N + n] += A[r * 32 + k] * B[k * N + n];
+    float *dA, *dB, *dD;
+    CK(cudaMalloc(&dA, A.size() * 4));
+    CK(cudaMalloc(&dB, B.size() * 4));
+    CK(cudaMalloc(&dD, D.size() * 4));
+    CK(cudaMemcpy(dA, A.data(), A.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice));
+    probe_mma_sw128<N><<<1, 128>>>(dA, dB, dD);
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost));
+    int bad = 0;
+    for (int i = 0; i < 128 * N; ++i) bad += D[i] != R[i];
+    printf("probe_mma_sw128 K-major N=80: %s (%d bad) D0=%g R0=%g\n", bad ? "FAIL" : "ok", bad, D[0], R[0]);
   }
   return 0;
 }
