@@ -55,9 +55,11 @@ void gemm_tall(const Ctx& ctx, const TA* A, int64_t m, int k, int64_t lda, const
 void gemm_small(const Ctx& ctx, bool ta, bool tb, int m, int n, int k, const double* A, int lda,
                 const double* B, int ldb, double* C, int ldc);
 
-// Symmetric EVD (cyclic parallel Jacobi, fp64): W descending, V col-major k x k.
-void eig_sym(const Ctx& ctx, Arena& ws, const double* A, int k, double* W, double* V, int count = 1,
-             int64_t stride_a = 0, int64_t stride_w = 0, int64_t stride_v = 0);
+// Symmetric EVD (cyclic parallel Jacobi, fp64): W descending, V col-major k x k.  The batch form
+// solves up to 8 independent matrices (one CTA each) in one launch.
+void eig_sym(const Ctx& ctx, Arena& ws, const double* A, int k, double* W, double* V);
+void eig_sym_batch(const Ctx& ctx, Arena& ws, int count, const double* const* A, const int* k, double* const* W,
+                   double* const* V);
 
 // Sign canonicalization (reading R5): per column of Q (m x r, ld), candidate (|v|max, global row,
 // sign) -> cand[3*c..]; then apply: flip Q[:,c] and U[:,c] (ldu, rows ku) where the best candidate
@@ -80,6 +82,13 @@ void unfold_copy(const Ctx& ctx, const T* Tt, Box box, double* out, int64_t ldo)
 template <typename T>
 void residual(const Ctx& ctx, Arena& ws, const T* X, int64_t J, int64_t In, const T* P, int R,
               const T* Q, int64_t ldq, double* out2);
+
+// tcgen05 residual (ttm_tc.cu): same sums with Xhat = P Q^T built on the tensor cores (fp32 data,
+// R <= 64, J % 4 == 0, ldp % 4 == 0).  Returns false (nothing launched) when not applicable.
+bool residual_tc(const Ctx& ctx, Arena& ws, const float* X, int64_t J, int64_t In, const float* P, int64_t ldp,
+                 int R, const float* Q, int64_t ldq, double* out2);
+// out2 = fixed-order sums of n (a, b) pairs
+void reduce_pairs(const Ctx& ctx, const double* part, int n, double* out2);
 
 // sum of squares of an fp64 vector -> out (deterministic)
 void sumsq(const Ctx& ctx, Arena& ws, const double* x, int64_t n, double* out);

@@ -249,37 +249,45 @@ __global__ void gemm_small_kernel(bool ta, bool tb, int m, int n, int k, const d
 // Cyclic Jacobi with the round-robin parallel ordering; A (k x k, padded to even kk) in shared
 // memory, V in shared memory when it fits, else in global scratch.  Rotation per pair (p,q):
 // tau = (a_qq - a_pp)/(2 a_pq), t = sign(tau)/(|tau| + sqrt(1+tau^2)), c = 1/sqrt(1+t^2), s = t c;
-// A <- J^T A J with J = [[c, s], [-s, c]] in the (p,q) plane; V <- V J.
-__global__ void __launch_bounds__(512) jacobi_kernel(const double* __restrict__ Ain, int k, double* W,
-                                                     double* Vout, double* Vscratch, int v_in_smem,
-                                                     int64_t stride_a, int64_t stride_w, int64_t stride_v,
-                                                     int64_t stride_scr) {
+// A <- J^T A J with J = [[c, s], [-s, c]] in the (p,q) plane; V <- V J.  One CTA per matrix; a
+// launch handles a batch of independent matrices (the N modes of the truncation).
+struct EigBatch {
+  const double* A[8];
+  double* W[8];
+  double* V[8];
+  int k[8];
+};
+
+__global__ void __launch_bounds__(512) jacobi_kernel(EigBatch bt, double* Vscratch, int v_in_smem, int64_t stride_scr) {
   extern __shared__ double sm[];
+  const int k = bt.k[blockIdx.x];
   const int kk = k + (k & 1);
-  const int ld = kk + 1;
+  const int kmax = kk;  // smem carve-up uses this matrix's size
+  const int ld = kmax + 1;
   double* A = sm;                                   // kk x ld (row-major A[i*ld + j])
   double* V = v_in_smem ? (sm + kk * ld) : (Vscratch + blockIdx.x * stride_scr);
   double* cs = (v_in_smem ? sm + 2 * kk * ld : sm + kk * ld);   // kk/2 pairs: c, s, p, q
   __shared__ double red[32];
   __shared__ int s_done;
-  const double* Ab = Ain + blockIdx.x * stride_a;
-  W += blockIdx.x * stride_w;
-  Vout += blockIdx.x * stride_v;
+  const double* Ab = bt.A[blockIdx.x];
+  double* W = bt.W[blockIdx.x];
+  double* Vout = bt.V[blockIdx.x];
   const int t = threadIdx.x, nt = blockDim.x;
-  for (int e = t; e < kk * kk; e += nt) {
-    const int i = e / kk, j = e % kk;
-    A[i * ld + j] = (i < k && j < k) ? 0.5 * (Ab[i + int64_t(k) * j] + Ab[j + int64_t(k) * i]) : 0.0;
-    V[i * ld + j] = (i == j) ? 1.0 : 0.0;
-  }
+  const int warp = t >> 5, lane = t & 31, nw = nt >> 5;
+  for (int i = warp; i < kk; i += nw)
+    for (int j = lane; j < kk; j += 32) {
+      A[i * ld + j] = (i < k && j < k) ? 0.5 * (Ab[i + int64_t(k) * j] + Ab[j + int64_t(k) * i]) : 0.0;
+      V[i * ld + j] = (i == j) ? 1.0 : 0.0;
+    }
   __syncthreads();
   const int npairs = kk / 2;
   for (int sweep = 0; sweep < 40; ++sweep) {
     double off = 0.0, dia = 0.0;
-    for (int e = t; e < kk * kk; e += nt) {
-      const int i = e / kk, j = e % kk;
-      const double v = A[i * ld + j];
-      if (i != j) off += v * v; else dia += v * v;
-    }
+    for (int i = warp; i < kk; i += nw)
+      for (int j = lane; j < kk; j += 32) {
+        const double v = A[i * ld + j];
+        if (i != j) off += v * v; else dia += v * v;
+      }
     off = block_sum(off, red);
     __syncthreads();
     dia = block_sum(dia, red);
@@ -289,8 +297,11 @@ __global__ void __launch_bounds__(512) jacobi_kernel(const double* __restrict__ 
     for (int round = 0; round < kk - 1; ++round) {
       for (int pi = t; pi < npairs; pi += nt) {
         int p, q;
-        if (pi == 0) { p = round % (kk - 1); q = kk - 1; }
-        else { p = (round + pi) % (kk - 1); q = (round - pi + kk - 1) % (kk - 1); }
+        if (pi == 0) { p = round; q = kk - 1; }
+        else {
+          p = round + pi; if (p >= kk - 1) p -= kk - 1;
+          q = round - pi; if (q < 0) q += kk - 1;
+        }
         if (p > q) { const int tmp = p; p = q; q = tmp; }
         const double apq = A[p * ld + q];
         double c = 1.0, s = 0.0;
@@ -304,36 +315,32 @@ __global__ void __launch_bounds__(512) jacobi_kernel(const double* __restrict__ 
         cs[4 * pi + 2] = p; cs[4 * pi + 3] = q;
       }
       __syncthreads();
-      // rows: A <- J^T A
-      for (int e = t; e < npairs * kk; e += nt) {
-        const int pi = e / kk, l = e % kk;
+      // rows: A <- J^T A   (one warp per pair, lanes over columns)
+      for (int pi = warp; pi < npairs; pi += nw) {
         const double c = cs[4 * pi], s = cs[4 * pi + 1];
         if (s == 0.0) continue;
         const int p = int(cs[4 * pi + 2]), q = int(cs[4 * pi + 3]);
-        const double ap = A[p * ld + l], aq = A[q * ld + l];
-        A[p * ld + l] = c * ap - s * aq;
-        A[q * ld + l] = s * ap + c * aq;
+        for (int l = lane; l < kk; l += 32) {
+          const double ap = A[p * ld + l], aq = A[q * ld + l];
+          A[p * ld + l] = c * ap - s * aq;
+          A[q * ld + l] = s * ap + c * aq;
+        }
       }
       __syncthreads();
       // columns: A <- A J, V <- V J
-      for (int e = t; e < npairs * kk; e += nt) {
-        const int pi = e / kk, l = e % kk;
+      for (int pi = warp; pi < npairs; pi += nw) {
         const double c = cs[4 * pi], s = cs[4 * pi + 1];
         if (s == 0.0) continue;
         const int p = int(cs[4 * pi + 2]), q = int(cs[4 * pi + 3]);
-        const double ap = A[l * ld + p], aq = A[l * ld + q];
-        A[l * ld + p] = c * ap - s * aq;
-        A[l * ld + q] = s * ap + c * aq;
-        const double vp = V[l * ld + p], vq = V[l * ld + q];
-        V[l * ld + p] = c * vp - s * vq;
-        V[l * ld + q] = s * vp + c * vq;
-      }
-      __syncthreads();
-      for (int pi = t; pi < npairs; pi += nt) {
-        if (cs[4 * pi + 1] == 0.0) continue;
-        const int p = int(cs[4 * pi + 2]), q = int(cs[4 * pi + 3]);
-        A[p * ld + q] = 0.0;
-        A[q * ld + p] = 0.0;
+        for (int l = lane; l < kk; l += 32) {
+          const double ap = A[l * ld + p], aq = A[l * ld + q];
+          A[l * ld + p] = c * ap - s * aq;
+          A[l * ld + q] = s * ap + c * aq;
+          const double vp = V[l * ld + p], vq = V[l * ld + q];
+          V[l * ld + p] = c * vp - s * vq;
+          V[l * ld + q] = s * vp + c * vq;
+        }
+        if (lane == 0) { A[p * ld + q] = 0.0; A[q * ld + p] = 0.0; }
       }
       __syncthreads();
     }
@@ -581,13 +588,20 @@ void gemm_small(const Ctx& ctx, bool ta, bool tb, int m, int n, int k, const dou
   });
 }
 
-void eig_sym(const Ctx& ctx, Arena& ws, const double* A, int k, double* W, double* V, int count,
-             int64_t stride_a, int64_t stride_w, int64_t stride_v) {
-  RT_REQUIRE(k >= 1 && k <= 128, kEUNSUPPORTED, "eig_sym: k must be in [1,128]");
-  const int kk = k + (k & 1), ld = kk + 1;
+void eig_sym_batch(const Ctx& ctx, Arena& ws, int count, const double* const* A, const int* k, double* const* W,
+                   double* const* V) {
+  RT_REQUIRE(count >= 1 && count <= 8, kEUNSUPPORTED, "eig_sym_batch: 1..8 matrices");
+  EigBatch bt{};
+  int kmax = 0;
+  for (int i = 0; i < count; ++i) {
+    RT_REQUIRE(k[i] >= 1 && k[i] <= 128, kEUNSUPPORTED, "eig_sym: k must be in [1,128]");
+    bt.A[i] = A[i]; bt.W[i] = W[i]; bt.V[i] = V[i]; bt.k[i] = k[i];
+    kmax = std::max(kmax, k[i]);
+  }
+  const int kk = kmax + (kmax & 1), ld = kk + 1;
   const size_t a_bytes = sizeof(double) * size_t(kk) * ld;
   const size_t cs_bytes = sizeof(double) * 4 * size_t(kk / 2 + 1);
-  int v_in_smem = (2 * a_bytes + cs_bytes) <= 200 * 1024;
+  const int v_in_smem = (2 * a_bytes + cs_bytes) <= 200 * 1024;
   const size_t smem = (v_in_smem ? 2 * a_bytes : a_bytes) + cs_bytes;
   double* scratch = nullptr;
   int64_t stride_scr = 0;
@@ -601,9 +615,12 @@ void eig_sym(const Ctx& ctx, Arena& ws, const double* A, int k, double* W, doubl
     attr = true;
   }
   launch(ctx, "jacobi_eig", [&] {
-    jacobi_kernel<<<count, 512, smem, ctx.stream>>>(A, k, W, V, scratch, v_in_smem, stride_a, stride_w, stride_v,
-                                                    stride_scr);
+    jacobi_kernel<<<count, 512, smem, ctx.stream>>>(bt, scratch, v_in_smem, stride_scr);
   });
+}
+
+void eig_sym(const Ctx& ctx, Arena& ws, const double* A, int k, double* W, double* V) {
+  eig_sym_batch(ctx, ws, 1, &A, &k, &W, &V);
 }
 
 void colmax_candidates(const Ctx& ctx, const double* Q, int64_t m, int r, int64_t ld, int64_t row0,
@@ -655,6 +672,10 @@ template void residual<float>(const Ctx&, Arena&, const float*, int64_t, int64_t
                               int64_t, double*);
 template void residual<double>(const Ctx&, Arena&, const double*, int64_t, int64_t, const double*, int,
                                const double*, int64_t, double*);
+
+void reduce_pairs(const Ctx& ctx, const double* part, int n, double* out2) {
+  launch(ctx, "reduce_pairs", [&] { reduce_pairs_kernel<<<1, 256, 0, ctx.stream>>>(part, n, out2); });
+}
 
 void sumsq(const Ctx& ctx, Arena&, const double* x, int64_t n, double* out) {
   launch(ctx, "sumsq", [&] { sumsq_kernel<<<1, 512, 0, ctx.stream>>>(x, n, out); });

@@ -116,11 +116,28 @@ void Engine::qr_z(T* Z, int64_t m, int64_t ldz, int64_t m_glob, int k, bool rows
   double* Rr = ws.alloc_n<double>(int64_t(k) * k);
   double* Ri = ws.alloc_n<double>(int64_t(k) * k);
   int* zero = ws.alloc_n<int>(1);
-  gram<T>(ctx, ws, Z, m, k, ldz, G);
+  // fp32 Z on the tensor cores: view Z (ldz x k, pad rows zero) as a 2-way tensor [a=ldz, I=k]; its
+  // mode-1 "sketch" with B = Z is Z^T Z, and its mode-1 TTM with R^{-1} is Z R^{-1} (in place: every
+  // 128-row tile is read completely before it is written, by the one CTA that owns it).
+  const bool tc = std::is_same<T, float>::value && ctx.ttm_impl != 1;
+  const Box zb{ldz, k, 1};
+  bool done_gram = false;
+  if constexpr (std::is_same<T, float>::value) {
+    if (tc) done_gram = ttm_s_tc(ctx, ws, Z, zb, Z, ldz, false, k, G, k);
+  }
+  if (!done_gram) gram<T>(ctx, ws, Z, m, k, ldz, G);
   allreduce(comm, rows_dist && dist(), G, int64_t(k) * k, ctx.stream);
   (void)m_glob;
   chol_inv(ctx, G, k, 1e-13, Rr, Ri, zero);
-  gemm_tall<T, T>(ctx, Z, m, k, ldz, Ri, k, k, Z, ldz, zero, row0);
+  bool done_apply = false;
+  if constexpr (std::is_same<T, float>::value) {
+    if (tc) {
+      int64_t ldr;
+      const float* RiT = working_copy<float>(ctx, ws, Ri, k, k, k, ldr);
+      done_apply = ttm_t_tc(ctx, Z, zb, RiT, ldr, k, Z, 1, ldz, 0);
+    }
+  }
+  if (!done_apply) gemm_tall<T, T>(ctx, Z, m, k, ldz, Ri, k, k, Z, ldz, zero, row0);
   ws.rewind(mk);
 }
 
@@ -243,14 +260,20 @@ void Engine::truncate(const TView& X, const double* Gt, const int64_t* K, const 
   const int N = X.N;
   const auto mk = ws.mark();
   double* V[5];
-  double* W = ws.alloc_n<double>(128);
+  double* W[5];
+  double* M[5];
+  int kk[5];
   for (int n = 0; n < N; ++n) {
-    const int k = int(K[n]);
-    double* M = ws.alloc_n<double>(int64_t(k) * k);
-    V[n] = ws.alloc_n<double>(int64_t(k) * k);
+    kk[n] = int(K[n]);
+    M[n] = ws.alloc_n<double>(int64_t(kk[n]) * kk[n]);
+    V[n] = ws.alloc_n<double>(int64_t(kk[n]) * kk[n]);
+    W[n] = ws.alloc_n<double>(kk[n]);
     // M_n = G~_(n) G~_(n)^T (Gram-EVD)
-    ttm_s<double>(ctx, ws, Gt, TView::box_of(K, N, n), nullptr, 0, 0, k, M, k, /*gram=*/true);
-    eig_sym(ctx, ws, M, k, W, V[n]);
+    ttm_s<double>(ctx, ws, Gt, TView::box_of(K, N, n), nullptr, 0, 0, kk[n], M[n], kk[n], /*gram=*/true);
+  }
+  eig_sym_batch(ctx, ws, N, M, kk, W, V);
+  for (int n = 0; n < N; ++n) {
+    const int k = kk[n];
     // Q_n = Q~_n U_n, U_n = V_n[:, :R_n]; sign canonicalization on the lifted factor
     gemm_tall<double, double>(ctx, Qt[n], X.d[n], k, ldq[n], V[n], int(R[n]), k, Q_out[n], X.d[n]);
     canon(Q_out[n], X.d[n], int(R[n]), X.d[n], n == N - 1 ? X.off : 0, n == N - 1, V[n], k);
@@ -311,7 +334,9 @@ void Engine::rel_error(const TView& X, const T* data, const double* G, const int
   }
   int64_t J = 1;
   for (int k = 0; k < N - 1; ++k) J *= X.d[k];
-  residual<T>(ctx, ws, data, J, Il, P, Rl, QL, Il, sums);
+  bool done = false;
+  if constexpr (std::is_same<T, float>::value) done = residual_tc(ctx, ws, data, J, Il, P, J, Rl, QL, Il, sums);
+  if (!done) residual<T>(ctx, ws, data, J, Il, P, Rl, QL, Il, sums);
   allreduce(comm, dist(), sums, 2, ctx.stream);                                    // C5
   finalize_err(ctx, sums, gg, E, Eg);
   ws.rewind(mk);

@@ -623,3 +623,262 @@ bool ttm_t_tc(const Ctx& ctx, const float* X, Box box, const float* Q, int64_t l
 }
 
 }  // namespace rt
+
+// ============================================================ residual (a8)
+// sum_{j,i} (X[j + J i] - Xhat[j,i])^2 and sum X^2 with Xhat = P Q^T (P: J x R col-major, the core
+// expanded over all but the last mode; Q: the last factor).  Xhat tiles [128 j x 64 i] are built on
+// the tensor cores (A = P tile hi/lo in TMEM, B = Q^T hi / lo pre-split, 3 products, contraction R)
+// and compared with the X tile in the epilogue; nothing but two fp64 partial sums per CTA is written.
+namespace rt {
+namespace {
+using namespace tc;
+
+constexpr int RNB = 64;                      // i columns per block (MMA N)
+constexpr int RNS = 2;                       // block pipeline depth
+
+template <int RP>
+struct RSmem {
+  static constexpr uint32_t kP = uint32_t(RP) * BM * 4;          // raw P tile [RP r][128 j]
+  static constexpr uint32_t kQ = uint32_t(RNB) * KC * 4;         // one [64 i][32 r] swizzled B chunk
+  static constexpr uint32_t kXt = uint32_t(BM) * RNB * 4;        // X tile [64 i][128 j]
+  static constexpr uint32_t per_stage = 2 * (RP / KC) * kQ + kXt;
+  static constexpr uint32_t off_p = 0;
+  static constexpr uint32_t off_st = kP;
+  static constexpr uint32_t off_bar = off_st + RNS * per_stage;
+  static constexpr uint32_t bytes = off_bar + 8 * (2 * RNS + 8) + 16;
+};
+
+struct RParams {
+  int64_t J, In;
+  int R;
+  int64_t ntiles;     // j tiles of 128
+  int nblk;           // i blocks of 64
+  double* part;       // [grid][2]
+};
+
+template <int RP>
+__global__ void __launch_bounds__(NTHREADS, 1)
+residual_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmp,
+                   const __grid_constant__ CUtensorMap tqh, const __grid_constant__ CUtensorMap tql, const RParams p) {
+  using L = RSmem<RP>;
+  constexpr int NCH = RP / KC;                 // r chunks
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::off_bar);
+  uint64_t* st_full = bar;                     // [RNS] Q chunks + X tile landed
+  uint64_t* st_free = bar + RNS;               // [RNS] epilogue done with the stage (128 arrivals)
+  uint64_t* p_full = bar + 2 * RNS;            // P raw tile landed
+  uint64_t* p_free = bar + 2 * RNS + 1;        // splitter done reading P raw (128)
+  uint64_t* a_ready = bar + 2 * RNS + 2;       // A (hi/lo) in TMEM (128)
+  uint64_t* a_free = bar + 2 * RNS + 3;        // all MMAs of the tile done (commit)
+  uint64_t* acc_full = bar + 2 * RNS + 4;      // [2]
+  uint64_t* acc_empty = bar + 2 * RNS + 6;     // [2] (128)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2 * RNS + 8);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t my_tiles = (p.ntiles > blockIdx.x) ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  constexpr uint32_t kA = 2 * RNB;             // TMEM: acc at 0 / RNB, A hi at 128, A lo at 128 + RP
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < RNS; ++s) { mbar_init(&st_full[s], 1); mbar_init(&st_free[s], 128); }
+    mbar_init(p_full, 1);
+    mbar_init(p_free, 128);
+    mbar_init(a_ready, 128);
+    mbar_init(a_free, 1);
+    for (int b = 0; b < 2; ++b) { mbar_init(&acc_full[b], 1); mbar_init(&acc_empty[b], 128); }
+    fence_barrier_init();
+    tma_prefetch(&tmx); tma_prefetch(&tmp); tma_prefetch(&tqh); tma_prefetch(&tql);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {                                   // ---------------- TMA producer
+      Ring rg;
+      int it = 0;
+      for (int64_t u = 0; u < my_tiles; ++u) {
+        const int j0 = int((blockIdx.x + u * gridDim.x) * BM);
+        if (u >= 1) mbar_wait(p_free, uint32_t(u - 1) & 1);
+        mbar_expect_tx(p_full, L::kP);
+        for (int c = 0; c < NCH; ++c)
+          tma_load_2d(smem + L::off_p + c * (BM * KC * 4), &tmp, p_full, j0, c * KC);
+        for (int b = 0; b < p.nblk; ++b, ++it, rg.next<RNS>()) {
+          if (it >= RNS) mbar_wait(&st_free[rg.s], rg.ph ^ 1);
+          uint8_t* st = smem + L::off_st + rg.s * L::per_stage;
+          mbar_expect_tx(&st_full[rg.s], L::per_stage);
+          for (int c = 0; c < NCH; ++c) {
+            tma_load_2d(st + c * L::kQ, &tqh, &st_full[rg.s], c * KC, b * RNB);
+            tma_load_2d(st + (NCH + c) * L::kQ, &tql, &st_full[rg.s], c * KC, b * RNB);
+          }
+          tma_load_2d(st + 2 * NCH * L::kQ, &tmx, &st_full[rg.s], j0, b * RNB);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {                                   // ---------------- MMA issuer
+      const uint32_t idesc = idesc_tf32(BM, RNB, 0);
+      Ring rg;
+      int64_t g = 0;
+      for (int64_t u = 0; u < my_tiles; ++u) {
+        mbar_wait(a_ready, uint32_t(u) & 1);
+        tc_fence_after();
+        for (int b = 0; b < p.nblk; ++b, ++g, rg.next<RNS>()) {
+          const int ab = int(g & 1);
+          if (g >= 2) mbar_wait(&acc_empty[ab], uint32_t((g >> 1) - 1) & 1);
+          mbar_wait(&st_full[rg.s], rg.ph);
+          tc_fence_after();
+          const uint32_t st = smem_u32(smem + L::off_st + rg.s * L::per_stage);
+          const uint32_t acc = tmem + uint32_t(ab) * RNB;
+#pragma unroll
+          for (int c = 0; c < NCH; ++c)
+#pragma unroll
+            for (int kk = 0; kk < KC / 8; ++kk) {
+              const uint32_t a_hi = tmem + kA + c * KC + 8 * kk;
+              const uint32_t a_lo = a_hi + RP;
+              const uint64_t bh = bdesc_sw128(st + c * L::kQ, kk);
+              const uint64_t bl = bdesc_sw128(st + (NCH + c) * L::kQ, kk);
+              mma_tf32_ts(acc, a_hi, bh, idesc, (c == 0 && kk == 0) ? 0u : 1u);
+              mma_tf32_ts(acc, a_lo, bh, idesc, 1u);
+              mma_tf32_ts(acc, a_hi, bl, idesc, 1u);
+            }
+          mma_commit(&acc_full[ab]);
+        }
+        mma_commit(a_free);
+      }
+    }
+  } else {                                             // ---------------- split A / epilogue
+    const int q4 = warp & 3;
+    const int r = 32 * q4 + lane;
+    const uint32_t lane_base = tmem + (uint32_t(32 * q4) << 16);
+    double res = 0.0, xx = 0.0;
+    Ring rg;
+    int64_t g = 0;
+    for (int64_t u = 0; u < my_tiles; ++u) {
+      mbar_wait(p_full, uint32_t(u) & 1);
+      if (u >= 1) mbar_wait(a_free, uint32_t(u - 1) & 1);   // previous tile's MMAs done with A
+      tc_fence_after();
+      const float* ps = reinterpret_cast<const float*>(smem + L::off_p);
+#pragma unroll
+      for (int c = 0; c < NCH; ++c)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t hi[16], lo[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) split_tf32(ps[c * (BM * KC) + (16 * h + q) * BM + r], hi[q], lo[q]);
+          tmem_st16(lane_base + kA + c * KC + 16 * h, hi);
+          tmem_st16(lane_base + kA + RP + c * KC + 16 * h, lo);
+        }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(p_free);
+      mbar_arrive(a_ready);
+      for (int b = 0; b < p.nblk; ++b, ++g, rg.next<RNS>()) {
+        const int ab = int(g & 1);
+        mbar_wait(&st_full[rg.s], rg.ph);
+        mbar_wait(&acc_full[ab], uint32_t(g >> 1) & 1);
+        tc_fence_after();
+        const float* xt = reinterpret_cast<const float*>(smem + L::off_st + rg.s * L::per_stage + 2 * NCH * L::kQ);
+        float tr = 0.f, tx = 0.f;
+#pragma unroll
+        for (int cb = 0; cb < RNB / 16; ++cb) {
+          uint32_t v[16];
+          tmem_ld16(lane_base + uint32_t(ab) * RNB + 16 * cb, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const float x = xt[(16 * cb + q) * BM + r];
+            const float d = x - __uint_as_float(v[q]);
+            tr = fmaf(d, d, tr);
+            tx = fmaf(x, x, tx);
+          }
+        }
+        res += double(tr);
+        xx += double(tx);
+        tc_fence_before();
+        mbar_arrive(&acc_empty[ab]);
+        mbar_arrive(&st_free[rg.s]);
+      }
+    }
+    // CTA reduction of the 128 splitter threads -> part[blockIdx.x]
+    __shared__ double red[2][4];
+    for (int o = 16; o; o >>= 1) {
+      res += __shfl_xor_sync(0xffffffffu, res, o);
+      xx += __shfl_xor_sync(0xffffffffu, xx, o);
+    }
+    if (lane == 0) { red[0][q4] = res; red[1][q4] = xx; }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (threadIdx.x == 64) {
+      p.part[2 * blockIdx.x] = red[0][0] + red[0][1] + red[0][2] + red[0][3];
+      p.part[2 * blockIdx.x + 1] = red[1][0] + red[1][1] + red[1][2] + red[1][3];
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+template <int RP>
+void launch_r(const Ctx& ctx, const CUtensorMap& tx, const CUtensorMap& tp, const CUtensorMap& th,
+              const CUtensorMap& tl, const RParams& p, int grid) {
+  using L = RSmem<RP>;
+  static bool attr = false;
+  if (!attr) { set_smem(residual_tc_kernel<RP>, L::bytes); attr = true; }
+  launch(ctx, "residual_tc", [&] {
+    residual_tc_kernel<RP><<<grid, NTHREADS, L::bytes, ctx.stream>>>(tx, tp, th, tl, p);
+  });
+}
+
+__global__ void split_transpose_kernel(const float* __restrict__ Q, int64_t In, int R, int64_t ldq,
+                                       float* __restrict__ hi, float* __restrict__ lo, int ldt) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;   // element (r, i) of Q^T
+  if (e >= In * ldt) return;
+  const int64_t i = e / ldt;
+  const int r = int(e % ldt);
+  const float v = r < R ? Q[i + ldq * r] : 0.f;
+  uint32_t h, l;
+  split_tf32(v, h, l);
+  hi[e] = __uint_as_float(h);
+  lo[e] = __uint_as_float(l);
+}
+
+}  // namespace
+
+bool residual_tc(const Ctx& ctx, Arena& ws, const float* X, int64_t J, int64_t In, const float* P, int64_t ldp,
+                 int R, const float* Q, int64_t ldq, double* part_out2) {
+  if (ctx.ttm_impl == 1 || R < 1 || R > 64) return false;
+  if (!aligned(X, 16) || !aligned(P, 16) || (J % 4) || (ldp % 4) || J > INT32_MAX || In > INT32_MAX) return false;
+  const int rp = R <= 32 ? 32 : 64;
+  CUtensorMap tx, tp, th, tl;
+  {  // X(j, i) at j + J i: box (128 j, 64 i)
+    const uint64_t d[2] = {uint64_t(J), uint64_t(In)}, s[1] = {uint64_t(J) * 4};
+    const uint32_t bx[2] = {BM, RNB};
+    if (!make_map(&tx, X, 2, d, s, bx, false)) return false;
+  }
+  {  // P(j, r) at j + ldp r: box (128 j, 32 r) -> [32 r][128 j]
+    const uint64_t d[2] = {uint64_t(J), uint64_t(R)}, s[1] = {uint64_t(ldp) * 4};
+    const uint32_t bx[2] = {BM, KC};
+    if (!make_map(&tp, P, 2, d, s, bx, false)) return false;
+  }
+  // Q^T hi / lo, element (r, i) at r + rp*i (pad r >= R zero)
+  float* qh = ws.alloc_n<float>(In * rp);
+  float* ql = ws.alloc_n<float>(In * rp);
+  launch(ctx, "split_transpose", [&] {
+    split_transpose_kernel<<<unsigned(cdiv(In * rp, 256)), 256, 0, ctx.stream>>>(Q, In, R, ldq, qh, ql, rp);
+  });
+  if (!make_b_map(&th, qh, rp, int(In), rp, RNB) || !make_b_map(&tl, ql, rp, int(In), rp, RNB)) return false;
+  RParams p;
+  p.J = J; p.In = In; p.R = R;
+  p.ntiles = cdiv(J, BM);
+  p.nblk = int(cdiv(In, RNB));
+  const int grid = int(std::min<int64_t>(p.ntiles, ctx.num_sms));
+  p.part = ws.alloc_n<double>(2 * grid);
+  if (rp == 32) launch_r<32>(ctx, tx, tp, th, tl, p, grid);
+  else launch_r<64>(ctx, tx, tp, th, tl, p, grid);
+  // fixed-order final reduction of the per-CTA pairs
+  reduce_pairs(ctx, p.part, grid, part_out2);
+  return true;
+}
+
+}  // namespace rt
