@@ -128,7 +128,10 @@ void Engine::qr_z(T* Z, int64_t m, int64_t ldz, int64_t m_glob, int k, bool rows
   if (!done_gram) gram<T>(ctx, ws, Z, m, k, ldz, G);
   allreduce(comm, rows_dist && dist(), G, int64_t(k) * k, ctx.stream);
   (void)m_glob;
-  chol_inv(ctx, G, k, 1e-13, Rr, Ri, zero);
+  // Shift: the tensor-core Gram carries ~1e-6 relative error (3xTF32, fp32 TMEM segments), far
+  // above the fp64 Gram's; Z only conditions the next product (any invertible R keeps span(X Z)),
+  // so a shift that dominates that error keeps the Cholesky factor well defined (R2').
+  chol_inv(ctx, G, k, done_gram ? 1e-5 : 1e-13, Rr, Ri, zero);
   bool done_apply = false;
   if constexpr (std::is_same<T, float>::value) {
     if (tc) {
