@@ -28,26 +28,65 @@ using namespace tc;
 
 constexpr int KC = 32;           // contraction elements per stage
 constexpr int BM = 128;          // tile rows = TMEM lanes
-constexpr int NTHREADS = 192;
-constexpr uint32_t kAStage = 256;  // TMEM: accumulators at columns 0 and 128, A stage s at 256 + 64 s
+constexpr int NTHREADS = 192;    // residual kernel
+constexpr int NT_TTM = 224;      // TTM kernels: + a B-producer warp
+constexpr int NB = 4;            // B / TMEM-A ring depth
+constexpr uint32_t kAStage = 256;  // TMEM: accumulators at columns 0 and 128, A slot s at 256 + 64 s
 
 __host__ __device__ constexpr uint32_t acc_col(int b) { return b ? 128u : 0u; }
 
-// Shared memory plan: per stage a raw X tile (16 KB), the B tile (hi, NPAD x 128 B) and
-// optionally B lo.  NS = 4 stages when they fit in ~200 KB, else 3.  All stage buffers are
-// 1024-byte aligned (128B swizzle atoms).
+// Shared memory plan of the TTM kernels.  Two rings:
+//   X ring (NX stages of raw 16 KB X tiles): TMA -> splitter; a stage is released as soon as the
+//     splitters have copied it into TMEM, so the producer can run NX stages ahead (bytes in flight);
+//   B ring (NB stages of [NPAD][32] 128B-swizzled B tiles, + lo when split) paired with the NB TMEM A
+//     slots: TMA/splitter -> MMA, released by tcgen05.commit.
 template <int NPAD, bool BSPLIT>
 struct Smem {
   static constexpr uint32_t kX = uint32_t(BM) * KC * 4;
   static constexpr uint32_t kB = uint32_t(NPAD) * KC * 4;
-  static constexpr uint32_t per_stage = kX + kB * (BSPLIT ? 2 : 1);
-  static constexpr int NS = per_stage * 4 <= 200 * 1024 ? 4 : 3;
+  static constexpr uint32_t b_bytes = NB * kB * (BSPLIT ? 2 : 1);
+  static constexpr int NX_fit = int((212u * 1024u - b_bytes) / kX);
+  static constexpr int NX = NX_fit > 10 ? 10 : NX_fit;
   static constexpr uint32_t off_x = 0;
-  static constexpr uint32_t off_b = off_x + NS * kX;
-  static constexpr uint32_t off_blo = off_b + NS * kB;
-  static constexpr uint32_t off_bar = off_blo + (BSPLIT ? NS * kB : 0);
-  static constexpr uint32_t bytes = off_bar + 8 * (3 * NS + 4) + 16;
+  static constexpr uint32_t off_b = off_x + NX * kX;
+  static constexpr uint32_t off_blo = off_b + NB * kB;
+  static constexpr uint32_t off_bar = off_blo + (BSPLIT ? NB * kB : 0);
+  static constexpr int nbar = 2 * NX + 3 * NB + 4;
+  static constexpr uint32_t bytes = off_bar + 8 * nbar + 16;
+  static_assert(NX >= 4, "X ring too shallow");
 };
+
+struct Bars {
+  uint64_t *x_full, *x_free, *b_full, *ready, *consumed, *acc_full, *acc_empty;
+  uint32_t* tmem_slot;
+};
+
+template <class L>
+__device__ __forceinline__ Bars bars_of(uint8_t* smem) {
+  uint64_t* b = reinterpret_cast<uint64_t*>(smem + L::off_bar);
+  Bars r;
+  r.x_full = b;
+  r.x_free = b + L::NX;
+  r.b_full = b + 2 * L::NX;
+  r.ready = b + 2 * L::NX + NB;
+  r.consumed = b + 2 * L::NX + 2 * NB;
+  r.acc_full = b + 2 * L::NX + 3 * NB;
+  r.acc_empty = b + 2 * L::NX + 3 * NB + 2;
+  r.tmem_slot = reinterpret_cast<uint32_t*>(b + L::nbar);
+  return r;
+}
+
+template <class L>
+__device__ __forceinline__ void init_bars(const Bars& b) {
+  for (int s = 0; s < L::NX; ++s) { mbar_init(&b.x_full[s], 1); mbar_init(&b.x_free[s], 128); }
+  for (int s = 0; s < NB; ++s) {
+    mbar_init(&b.b_full[s], 1);
+    mbar_init(&b.ready[s], 128);
+    mbar_init(&b.consumed[s], 1);
+  }
+  for (int k = 0; k < 2; ++k) { mbar_init(&b.acc_full[k], 1); mbar_init(&b.acc_empty[k], 128); }
+  fence_barrier_init();
+}
 
 // K-major SWIZZLE_128B descriptor of a [rows][32 fp32] tile, advanced to k-step kk (8 elements)
 __device__ __forceinline__ uint64_t bdesc_sw128(uint32_t saddr, int kk) {
@@ -59,27 +98,26 @@ __device__ __forceinline__ uint64_t bdesc_sw128(uint32_t saddr, int kk) {
 //   !AMN : tile [BM][KC] with 128B swizzle: 16B chunk c of row r at ((c ^ (r&7)) << 4)
 template <bool AMN>
 __device__ __forceinline__ void split_row_to_tmem(const float* xs, int r, uint32_t t_hi) {
-  uint32_t hi[16], lo[16];
+  uint32_t hi[32], lo[32];
+  if (AMN) {
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    if (AMN) {
+    for (int q = 0; q < 32; ++q) split_tf32(xs[q * BM + r], hi[q], lo[q]);
+  } else {
+    const float* row = xs + r * KC;
 #pragma unroll
-      for (int q = 0; q < 16; ++q) split_tf32(xs[(16 * h + q) * BM + r], hi[q], lo[q]);
-    } else {
-      const float* row = xs + r * KC;
-#pragma unroll
-      for (int c4 = 0; c4 < 4; ++c4) {
-        const int c = 4 * h + c4;
-        const float4 v = *reinterpret_cast<const float4*>(row + ((c ^ (r & 7)) << 2));
-        split_tf32(v.x, hi[4 * c4 + 0], lo[4 * c4 + 0]);
-        split_tf32(v.y, hi[4 * c4 + 1], lo[4 * c4 + 1]);
-        split_tf32(v.z, hi[4 * c4 + 2], lo[4 * c4 + 2]);
-        split_tf32(v.w, hi[4 * c4 + 3], lo[4 * c4 + 3]);
-      }
+    for (int c = 0; c < 8; ++c) {
+      const float4 v = *reinterpret_cast<const float4*>(row + ((c ^ (r & 7)) << 2));
+      split_tf32(v.x, hi[4 * c + 0], lo[4 * c + 0]);
+      split_tf32(v.y, hi[4 * c + 1], lo[4 * c + 1]);
+      split_tf32(v.z, hi[4 * c + 2], lo[4 * c + 2]);
+      split_tf32(v.w, hi[4 * c + 3], lo[4 * c + 3]);
     }
-    tmem_st16(t_hi + 16 * h, hi);
-    tmem_st16(t_hi + 32 + 16 * h, lo);
   }
+  // all smem reads of the X stage are done once the values are in registers
+  tmem_st16(t_hi, *reinterpret_cast<const uint32_t(*)[16]>(&hi[0]));
+  tmem_st16(t_hi + 16, *reinterpret_cast<const uint32_t(*)[16]>(&hi[16]));
+  tmem_st16(t_hi + 32, *reinterpret_cast<const uint32_t(*)[16]>(&lo[0]));
+  tmem_st16(t_hi + 48, *reinterpret_cast<const uint32_t(*)[16]>(&lo[16]));
 }
 
 // Split the B tile in place (hi) and write lo; elementwise, layout-agnostic, conflict-free.
@@ -118,20 +156,25 @@ __device__ __forceinline__ void issue_stage(uint32_t tmem, uint32_t acc, int s, 
 struct Ring {
   int s = 0;
   uint32_t ph = 0;
-  template <int NS> __device__ __forceinline__ void next() { if (++s == NS) { s = 0; ph ^= 1; } }
+  template <int N> __device__ __forceinline__ void next() { if (++s == N) { s = 0; ph ^= 1; } }
 };
 
-__device__ __forceinline__ void init_barriers(uint64_t* bar, int NS) {
-  for (int s = 0; s < NS; ++s) {
-    mbar_init(&bar[s], 1);               // full
-    mbar_init(&bar[NS + s], 128);        // ready
-    mbar_init(&bar[2 * NS + s], 1);      // consumed
+// Drain accumulator buffer `ab` (use index u) into register sums; release the buffer.
+template <int NPAD>
+__device__ __forceinline__ void drain_acc(const Bars& b, uint32_t lane_base, int64_t u, float (&sums)[NPAD]) {
+  const int ab = int(u & 1);
+  mbar_wait(&b.acc_full[ab], uint32_t(u >> 1) & 1);
+  tc_fence_after();
+#pragma unroll
+  for (int cb = 0; cb < NPAD / 16; ++cb) {
+    uint32_t v[16];
+    tmem_ld16(lane_base + acc_col(ab) + 16 * cb, v);
+    tmem_wait_ld();
+#pragma unroll
+    for (int q = 0; q < 16; ++q) sums[16 * cb + q] += __uint_as_float(v[q]);
   }
-  for (int b = 0; b < 2; ++b) {
-    mbar_init(&bar[3 * NS + b], 1);      // acc_full
-    mbar_init(&bar[3 * NS + 2 + b], 128);  // acc_empty
-  }
-  fence_barrier_init();
+  tc_fence_before();
+  mbar_arrive(&b.acc_empty[ab]);
 }
 
 // ====================================================================== ttm_s
@@ -140,79 +183,83 @@ struct SParams {
   int K;
   int64_t cpb;        // chunks per beta (a > 1)
   int64_t nchunks;    // total j-chunks
-  int64_t cps;        // chunks per split (CTA)
   int seg;            // chunks per accumulator segment
   float* part;        // [split][K][I]
 };
 
+// chunk c -> X tile coordinates and first B row j0
+template <bool AMN>
+__device__ __forceinline__ void chunk_coords(const SParams& p, int64_t c, int64_t& a0, int64_t& beta, int64_t& j0) {
+  if (AMN) { a0 = 0; beta = c * KC; j0 = beta; }
+  else { beta = c / p.cpb; a0 = (c % p.cpb) * KC; j0 = a0 + p.a * beta; }
+}
+
+// grid (splits, mtiles): CTA (z, m) sums the chunks c = z, z + S, z + 2S, ... (S = splits) of M-tile
+// m.  Interleaving keeps all concurrently running CTAs of an M-tile inside a window of S chunks of
+// every row (DRAM-page / TLB locality for the long rows of the last mode).
 template <int NPAD, bool BSPLIT, bool AMN>
-__global__ void __launch_bounds__(NTHREADS, 1)
+__global__ void __launch_bounds__(NT_TTM, 1)
 ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb, const SParams p) {
   using L = Smem<NPAD, BSPLIT>;
-  constexpr int NS = L::NS;
+  constexpr int NX = L::NX;
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::off_bar);
-  uint64_t* full = bar;
-  uint64_t* ready = bar + NS;
-  uint64_t* consumed = bar + 2 * NS;
-  uint64_t* acc_full = bar + 3 * NS;
-  uint64_t* acc_empty = bar + 3 * NS + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 3 * NS + 4);
+  const Bars b = bars_of<L>(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t i0 = int64_t(blockIdx.x) * BM;
-  const int64_t c_begin = int64_t(blockIdx.y) * p.cps;
-  const int64_t c_end = min(p.nchunks, c_begin + p.cps);
-  const int nch = c_end > c_begin ? int(c_end - c_begin) : 0;
+  const int64_t z = blockIdx.x, S = gridDim.x;
+  const int64_t i0 = int64_t(blockIdx.y) * BM;
+  const int nch = z < p.nchunks ? int((p.nchunks - z + S - 1) / S) : 0;
 
   if (threadIdx.x == 0) {
-    init_barriers(bar, NS);
+    init_bars<L>(b);
     tma_prefetch(&tmx);
     tma_prefetch(&tmb);
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (warp == 1) tmem_alloc(b.tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = *b.tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {                                   // ---------------- TMA producer
-      Ring rg;
-      int64_t beta = c_begin / p.cpb, a0 = (c_begin % p.cpb) * KC;
-      for (int it = 0; it < nch; ++it, rg.next<NS>()) {
-        if (it >= NS) mbar_wait(&consumed[rg.s], rg.ph ^ 1);
-        mbar_expect_tx(&full[rg.s], L::kX + L::kB);
-        float* xs = reinterpret_cast<float*>(smem + L::off_x + rg.s * L::kX);
-        float* bs = reinterpret_cast<float*>(smem + L::off_b + rg.s * L::kB);
-        int64_t j0;
-        if (AMN) {
-          j0 = (c_begin + it) * KC;
-          tma_load_2d(xs, &tmx, &full[rg.s], int(i0), int(j0));
-        } else {
-          j0 = a0 + p.a * beta;
-          tma_load_3d(xs, &tmx, &full[rg.s], int(a0), int(i0), int(beta));
-          a0 += KC;
-          if (a0 >= p.a) { a0 = 0; ++beta; }
-        }
-        tma_load_2d(bs, &tmb, &full[rg.s], int(j0), 0);
+    if (lane == 0) {                                   // ---------------- X producer
+      Ring rx;
+      for (int it = 0; it < nch; ++it, rx.next<NX>()) {
+        if (it >= NX) mbar_wait(&b.x_free[rx.s], rx.ph ^ 1);
+        int64_t a0, beta, j0;
+        chunk_coords<AMN>(p, z + it * S, a0, beta, j0);
+        mbar_expect_tx(&b.x_full[rx.s], L::kX);
+        void* xs = smem + L::off_x + rx.s * L::kX;
+        if (AMN) tma_load_2d(xs, &tmx, &b.x_full[rx.s], int(i0), int(j0));
+        else tma_load_3d(xs, &tmx, &b.x_full[rx.s], int(a0), int(i0), int(beta));
+      }
+    }
+  } else if (warp == 6) {
+    if (lane == 0) {                                   // ---------------- B producer
+      Ring rb;
+      for (int it = 0; it < nch; ++it, rb.next<NB>()) {
+        if (it >= NB) mbar_wait(&b.consumed[rb.s], rb.ph ^ 1);
+        int64_t a0, beta, j0;
+        chunk_coords<AMN>(p, z + it * S, a0, beta, j0);
+        mbar_expect_tx(&b.b_full[rb.s], L::kB);
+        tma_load_2d(smem + L::off_b + rb.s * L::kB, &tmb, &b.b_full[rb.s], int(j0), 0);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {                                   // ---------------- MMA issuer
       const uint32_t idesc = idesc_tf32(BM, NPAD, 0);
-      Ring rg;
+      Ring rb;
       int u = 0, pos = 0;
-      for (int it = 0; it < nch; ++it, rg.next<NS>()) {
+      for (int it = 0; it < nch; ++it, rb.next<NB>()) {
         const bool first = pos == 0;
         const bool last = (pos == p.seg - 1) || (it == nch - 1);
         const int ab = u & 1;
-        if (first && u >= 2) mbar_wait(&acc_empty[ab], ((u >> 1) - 1) & 1);
-        mbar_wait(&ready[rg.s], rg.ph);
+        if (first && u >= 2) mbar_wait(&b.acc_empty[ab], ((u >> 1) - 1) & 1);
+        mbar_wait(&b.ready[rb.s], rb.ph);
         tc_fence_after();
-        issue_stage<BSPLIT>(tmem, acc_col(ab), rg.s, smem_u32(smem + L::off_b + rg.s * L::kB),
-                            smem_u32(smem + L::off_blo + rg.s * L::kB), idesc, first);
-        mma_commit(&consumed[rg.s]);
-        if (last) { mma_commit(&acc_full[ab]); ++u; pos = 0; } else { ++pos; }
+        issue_stage<BSPLIT>(tmem, acc_col(ab), rb.s, smem_u32(smem + L::off_b + rb.s * L::kB),
+                            smem_u32(smem + L::off_blo + rb.s * L::kB), idesc, first);
+        mma_commit(&b.consumed[rb.s]);
+        if (last) { mma_commit(&b.acc_full[ab]); ++u; pos = 0; } else { ++pos; }
       }
     }
   } else {                                             // ---------------- splitters / epilogue
@@ -223,47 +270,34 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
     float sums[NPAD];
 #pragma unroll
     for (int k = 0; k < NPAD; ++k) sums[k] = 0.f;
-    auto epilogue = [&](int u) {
-      const int ab = u & 1;
-      mbar_wait(&acc_full[ab], (u >> 1) & 1);
-      tc_fence_after();
-#pragma unroll
-      for (int cb = 0; cb < NPAD / 16; ++cb) {
-        uint32_t v[16];
-        tmem_ld16(lane_base + acc_col(ab) + 16 * cb, v);
-        tmem_wait_ld();
-#pragma unroll
-        for (int q = 0; q < 16; ++q) sums[16 * cb + q] += __uint_as_float(v[q]);
-      }
-      tc_fence_before();
-      mbar_arrive(&acc_empty[ab]);
-    };
-    Ring rg;
+    Ring rx, rb;
     int u = 0, pos = 0;
-    for (int it = 0; it < nch; ++it, rg.next<NS>()) {
-      mbar_wait(&full[rg.s], rg.ph);
-      split_row_to_tmem<AMN>(reinterpret_cast<const float*>(smem + L::off_x + rg.s * L::kX), r,
-                             lane_base + kAStage + 64u * rg.s);
+    for (int it = 0; it < nch; ++it, rx.next<NX>(), rb.next<NB>()) {
+      mbar_wait(&b.x_full[rx.s], rx.ph);
+      mbar_wait(&b.b_full[rb.s], rb.ph);              // implies TMEM slot rb.s is free (B producer waited)
+      split_row_to_tmem<AMN>(reinterpret_cast<const float*>(smem + L::off_x + rx.s * L::kX), r,
+                             lane_base + kAStage + 64u * rb.s);
+      mbar_arrive(&b.x_free[rx.s]);
       if (BSPLIT)
-        split_b<NPAD>(reinterpret_cast<float*>(smem + L::off_b + rg.s * L::kB),
-                      reinterpret_cast<float*>(smem + L::off_blo + rg.s * L::kB), t);
+        split_b<NPAD>(reinterpret_cast<float*>(smem + L::off_b + rb.s * L::kB),
+                      reinterpret_cast<float*>(smem + L::off_blo + rb.s * L::kB), t);
       tmem_wait_st();
-      fence_proxy_async();
+      if (BSPLIT) fence_proxy_async();
       tc_fence_before();
-      mbar_arrive(&ready[rg.s]);
+      mbar_arrive(&b.ready[rb.s]);
       const bool last = (pos == p.seg - 1) || (it == nch - 1);
       if (last) {
-        if (u >= 1) epilogue(u - 1);
+        if (u >= 1) drain_acc<NPAD>(b, lane_base, u - 1, sums);
         ++u;
         pos = 0;
       } else {
         ++pos;
       }
     }
-    if (u >= 1) epilogue(u - 1);
+    if (u >= 1) drain_acc<NPAD>(b, lane_base, u - 1, sums);
     const int64_t i = i0 + r;                         // partial tile -> part[split][k][i]
     if (i < p.I) {
-      float* dst = p.part + int64_t(blockIdx.y) * p.K * p.I;
+      float* dst = p.part + z * p.K * p.I;
 #pragma unroll
       for (int k = 0; k < NPAD; ++k)
         if (k < p.K) dst[int64_t(k) * p.I + i] = sums[k];
@@ -288,32 +322,26 @@ struct TParams {
 };
 
 template <int NPAD, bool AKM>   // AKM: mode 0 (a == 1), X tile K-major [BM j][KC i]
-__global__ void __launch_bounds__(NTHREADS, 1)
+__global__ void __launch_bounds__(NT_TTM, 1)
 ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb, const TParams p) {
   constexpr bool BSPLIT = true;
   using L = Smem<NPAD, BSPLIT>;
-  constexpr int NS = L::NS;
+  constexpr int NX = L::NX;
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::off_bar);
-  uint64_t* full = bar;
-  uint64_t* ready = bar + NS;
-  uint64_t* consumed = bar + 2 * NS;
-  uint64_t* acc_full = bar + 3 * NS;
-  uint64_t* acc_empty = bar + 3 * NS + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 3 * NS + 4);
+  const Bars b = bars_of<L>(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t my_tiles = (p.ntiles > blockIdx.x) ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
   if (threadIdx.x == 0) {
-    init_barriers(bar, NS);
+    init_bars<L>(b);
     tma_prefetch(&tmx);
     tma_prefetch(&tmb);
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (warp == 1) tmem_alloc(b.tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = *b.tmem_slot;
 
   auto tile_coords = [&](int64_t tile, int64_t& a0, int64_t& beta) {
     if (AKM) { a0 = 0; beta = tile * BM; }
@@ -321,42 +349,50 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
   };
 
   if (warp == 0) {
-    if (lane == 0) {                                   // ---------------- TMA producer
-      Ring rg;
+    if (lane == 0) {                                   // ---------------- X producer
+      Ring rx;
       int it = 0;
       for (int64_t u = 0; u < my_tiles; ++u) {
         int64_t a0, beta;
         tile_coords(blockIdx.x + u * gridDim.x, a0, beta);
-        for (int c = 0; c < p.nic; ++c, ++it, rg.next<NS>()) {
-          if (it >= NS) mbar_wait(&consumed[rg.s], rg.ph ^ 1);
-          mbar_expect_tx(&full[rg.s], L::kX + L::kB);
-          float* xs = reinterpret_cast<float*>(smem + L::off_x + rg.s * L::kX);
-          float* bs = reinterpret_cast<float*>(smem + L::off_b + rg.s * L::kB);
-          const int ic = c * KC;
-          if (AKM) tma_load_2d(xs, &tmx, &full[rg.s], ic, int(beta));
-          else tma_load_3d(xs, &tmx, &full[rg.s], int(a0), ic, int(beta));
-          tma_load_2d(bs, &tmb, &full[rg.s], ic, 0);
+        for (int c = 0; c < p.nic; ++c, ++it, rx.next<NX>()) {
+          if (it >= NX) mbar_wait(&b.x_free[rx.s], rx.ph ^ 1);
+          mbar_expect_tx(&b.x_full[rx.s], L::kX);
+          void* xs = smem + L::off_x + rx.s * L::kX;
+          if (AKM) tma_load_2d(xs, &tmx, &b.x_full[rx.s], c * KC, int(beta));
+          else tma_load_3d(xs, &tmx, &b.x_full[rx.s], int(a0), c * KC, int(beta));
         }
       }
+    }
+  } else if (warp == 6) {
+    if (lane == 0) {                                   // ---------------- B producer
+      Ring rb;
+      int it = 0;
+      for (int64_t u = 0; u < my_tiles; ++u)
+        for (int c = 0; c < p.nic; ++c, ++it, rb.next<NB>()) {
+          if (it >= NB) mbar_wait(&b.consumed[rb.s], rb.ph ^ 1);
+          mbar_expect_tx(&b.b_full[rb.s], L::kB);
+          tma_load_2d(smem + L::off_b + rb.s * L::kB, &tmb, &b.b_full[rb.s], c * KC, 0);
+        }
     }
   } else if (warp == 1) {
     if (lane == 0) {                                   // ---------------- MMA issuer
       const uint32_t idesc = idesc_tf32(BM, NPAD, 0);
-      Ring rg;
+      Ring rb;
       int64_t g = 0;                                   // global segment counter
       for (int64_t u = 0; u < my_tiles; ++u) {
         int pos = 0;
-        for (int c = 0; c < p.nic; ++c, rg.next<NS>()) {
+        for (int c = 0; c < p.nic; ++c, rb.next<NB>()) {
           const bool first = pos == 0;
           const bool last = (pos == p.seg - 1) || (c == p.nic - 1);
           const int ab = int(g & 1);
-          if (first && g >= 2) mbar_wait(&acc_empty[ab], uint32_t((g >> 1) - 1) & 1);
-          mbar_wait(&ready[rg.s], rg.ph);
+          if (first && g >= 2) mbar_wait(&b.acc_empty[ab], uint32_t((g >> 1) - 1) & 1);
+          mbar_wait(&b.ready[rb.s], rb.ph);
           tc_fence_after();
-          issue_stage<BSPLIT>(tmem, acc_col(ab), rg.s, smem_u32(smem + L::off_b + rg.s * L::kB),
-                              smem_u32(smem + L::off_blo + rg.s * L::kB), idesc, first);
-          mma_commit(&consumed[rg.s]);
-          if (last) { mma_commit(&acc_full[ab]); ++g; pos = 0; } else { ++pos; }
+          issue_stage<BSPLIT>(tmem, acc_col(ab), rb.s, smem_u32(smem + L::off_b + rb.s * L::kB),
+                              smem_u32(smem + L::off_blo + rb.s * L::kB), idesc, first);
+          mma_commit(&b.consumed[rb.s]);
+          if (last) { mma_commit(&b.acc_full[ab]); ++g; pos = 0; } else { ++pos; }
         }
       }
     }
@@ -370,19 +406,7 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
     for (int k = 0; k < NPAD; ++k) sums[k] = 0.f;
     // drain segment g into the register sums; after the last segment of a tile, store the tile
     auto epilogue = [&](int64_t g, bool tile_end, int64_t tile) {
-      const int ab = int(g & 1);
-      mbar_wait(&acc_full[ab], uint32_t(g >> 1) & 1);
-      tc_fence_after();
-#pragma unroll
-      for (int cb = 0; cb < NPAD / 16; ++cb) {
-        uint32_t v[16];
-        tmem_ld16(lane_base + acc_col(ab) + 16 * cb, v);
-        tmem_wait_ld();
-#pragma unroll
-        for (int q = 0; q < 16; ++q) sums[16 * cb + q] += __uint_as_float(v[q]);
-      }
-      tc_fence_before();
-      mbar_arrive(&acc_empty[ab]);
+      drain_acc<NPAD>(b, lane_base, g, sums);
       if (tile_end) {
         int64_t a0, beta;
         tile_coords(tile, a0, beta);
@@ -399,23 +423,25 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
         for (int k = 0; k < NPAD; ++k) sums[k] = 0.f;
       }
     };
-    Ring rg;
+    Ring rx, rb;
     int64_t g = 0;
     bool prev_end = false;
     int64_t prev_tile = 0;
     for (int64_t u = 0; u < my_tiles; ++u) {
       const int64_t tile = blockIdx.x + u * gridDim.x;
       int pos = 0;
-      for (int c = 0; c < p.nic; ++c, rg.next<NS>()) {
-        mbar_wait(&full[rg.s], rg.ph);
-        split_row_to_tmem<!AKM>(reinterpret_cast<const float*>(smem + L::off_x + rg.s * L::kX), r,
-                                lane_base + kAStage + 64u * rg.s);
-        split_b<NPAD>(reinterpret_cast<float*>(smem + L::off_b + rg.s * L::kB),
-                      reinterpret_cast<float*>(smem + L::off_blo + rg.s * L::kB), t);
+      for (int c = 0; c < p.nic; ++c, rx.next<NX>(), rb.next<NB>()) {
+        mbar_wait(&b.x_full[rx.s], rx.ph);
+        mbar_wait(&b.b_full[rb.s], rb.ph);
+        split_row_to_tmem<!AKM>(reinterpret_cast<const float*>(smem + L::off_x + rx.s * L::kX), r,
+                                lane_base + kAStage + 64u * rb.s);
+        mbar_arrive(&b.x_free[rx.s]);
+        split_b<NPAD>(reinterpret_cast<float*>(smem + L::off_b + rb.s * L::kB),
+                      reinterpret_cast<float*>(smem + L::off_blo + rb.s * L::kB), t);
         tmem_wait_st();
         fence_proxy_async();
         tc_fence_before();
-        mbar_arrive(&ready[rg.s]);
+        mbar_arrive(&b.ready[rb.s]);
         const bool last = (pos == p.seg - 1) || (c == p.nic - 1);
         if (last) {
           if (g >= 1) epilogue(g - 1, prev_end, prev_tile);   // delayed by one segment
@@ -492,7 +518,7 @@ void launch_s(const Ctx& ctx, const CUtensorMap& tx, const CUtensorMap& tb, cons
   static bool attr = false;
   if (!attr) { set_smem(ttm_s_tc_kernel<NPAD, BSPLIT, AMN>, L::bytes); attr = true; }
   launch(ctx, "ttm_s_tc", [&] {
-    ttm_s_tc_kernel<NPAD, BSPLIT, AMN><<<grid, NTHREADS, L::bytes, ctx.stream>>>(tx, tb, p);
+    ttm_s_tc_kernel<NPAD, BSPLIT, AMN><<<grid, NT_TTM, L::bytes, ctx.stream>>>(tx, tb, p);
   });
 }
 
@@ -508,7 +534,7 @@ void launch_t(const Ctx& ctx, const CUtensorMap& tx, const CUtensorMap& tb, cons
   static bool attr = false;
   if (!attr) { set_smem(ttm_t_tc_kernel<NPAD, AKM>, L::bytes); attr = true; }
   launch(ctx, "ttm_t_tc", [&] {
-    ttm_t_tc_kernel<NPAD, AKM><<<grid, NTHREADS, L::bytes, ctx.stream>>>(tx, tb, p);
+    ttm_t_tc_kernel<NPAD, AKM><<<grid, NT_TTM, L::bytes, ctx.stream>>>(tx, tb, p);
   });
 }
 
@@ -558,11 +584,9 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
   int64_t splits = std::max<int64_t>(1, (int64_t(ctx.num_sms) * 4 + mtiles - 1) / mtiles);
   splits = std::min<int64_t>(splits, std::max<int64_t>(1, p.nchunks / 8));
   splits = std::min<int64_t>(splits, 65535);
-  p.cps = cdiv(p.nchunks, splits);
-  splits = cdiv(p.nchunks, p.cps);
   p.seg = std::max(1, ctx.tc_seg);
   p.part = ws.alloc_n<float>(splits * K * box.I);
-  const dim3 grid{unsigned(mtiles), unsigned(splits), 1u};
+  const dim3 grid{unsigned(splits), unsigned(mtiles), 1u};
   const bool bsplit = !b_tf32_exact;
 #define RT_S_CASE(NP)                                              \
   case NP:                                                         \
