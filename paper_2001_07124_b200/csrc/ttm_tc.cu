@@ -35,29 +35,32 @@ constexpr uint32_t kAStage = 256;  // TMEM: accumulators at columns 0 and 128, A
 
 __host__ __device__ constexpr uint32_t acc_col(int b) { return b ? 128u : 0u; }
 
-// Shared memory plan of the TTM kernels.  Two rings:
+// Shared memory plan of the TTM kernels.  Three rings:
 //   X ring (NX stages of raw 16 KB X tiles): TMA -> splitter; a stage is released as soon as the
-//     splitters have copied it into TMEM, so the producer can run NX stages ahead (bytes in flight);
-//   B ring (NB stages of [NPAD][32] 128B-swizzled B tiles, + lo when split) paired with the NB TMEM A
-//     slots: TMA/splitter -> MMA, released by tcgen05.commit.
+//     splitters have copied it into TMEM, so the producer can run NX stages ahead;
+//   B ring (NBS stages of [NPAD][32] 128B-swizzled B tiles): TMA -> MMA (B hi is split in place),
+//     released by tcgen05.commit; deeper than the TMEM ring so B (L2 or DRAM) latency is hidden;
+//   TMEM A slots (NB = 4, 64 columns each: hi | lo) + B lo tiles (when split): splitter -> MMA.
 template <int NPAD, bool BSPLIT>
 struct Smem {
   static constexpr uint32_t kX = uint32_t(BM) * KC * 4;
   static constexpr uint32_t kB = uint32_t(NPAD) * KC * 4;
-  static constexpr uint32_t b_bytes = NB * kB * (BSPLIT ? 2 : 1);
-  static constexpr int NX_fit = int((212u * 1024u - b_bytes) / kX);
+  static constexpr uint32_t budget = 212u * 1024u;
+  static constexpr uint32_t lo_bytes = BSPLIT ? NB * kB : 0;
+  static constexpr int NBS = NPAD <= 96 ? 8 : 4;
+  static constexpr int NX_fit = int((budget - NBS * kB - lo_bytes) / kX);
   static constexpr int NX = NX_fit > 10 ? 10 : NX_fit;
   static constexpr uint32_t off_x = 0;
   static constexpr uint32_t off_b = off_x + NX * kX;
-  static constexpr uint32_t off_blo = off_b + NB * kB;
-  static constexpr uint32_t off_bar = off_blo + (BSPLIT ? NB * kB : 0);
-  static constexpr int nbar = 2 * NX + 3 * NB + 4;
+  static constexpr uint32_t off_blo = off_b + NBS * kB;
+  static constexpr uint32_t off_bar = off_blo + lo_bytes;
+  static constexpr int nbar = 2 * NX + 2 * NBS + 2 * NB + 4;
   static constexpr uint32_t bytes = off_bar + 8 * nbar + 16;
   static_assert(NX >= 4, "X ring too shallow");
 };
 
 struct Bars {
-  uint64_t *x_full, *x_free, *b_full, *ready, *consumed, *acc_full, *acc_empty;
+  uint64_t *x_full, *x_free, *b_full, *b_free, *ready, *tfree, *acc_full, *acc_empty;
   uint32_t* tmem_slot;
 };
 
@@ -68,10 +71,11 @@ __device__ __forceinline__ Bars bars_of(uint8_t* smem) {
   r.x_full = b;
   r.x_free = b + L::NX;
   r.b_full = b + 2 * L::NX;
-  r.ready = b + 2 * L::NX + NB;
-  r.consumed = b + 2 * L::NX + 2 * NB;
-  r.acc_full = b + 2 * L::NX + 3 * NB;
-  r.acc_empty = b + 2 * L::NX + 3 * NB + 2;
+  r.b_free = b + 2 * L::NX + L::NBS;
+  r.ready = b + 2 * L::NX + 2 * L::NBS;
+  r.tfree = b + 2 * L::NX + 2 * L::NBS + NB;
+  r.acc_full = b + 2 * L::NX + 2 * L::NBS + 2 * NB;
+  r.acc_empty = r.acc_full + 2;
   r.tmem_slot = reinterpret_cast<uint32_t*>(b + L::nbar);
   return r;
 }
@@ -79,11 +83,8 @@ __device__ __forceinline__ Bars bars_of(uint8_t* smem) {
 template <class L>
 __device__ __forceinline__ void init_bars(const Bars& b) {
   for (int s = 0; s < L::NX; ++s) { mbar_init(&b.x_full[s], 1); mbar_init(&b.x_free[s], 128); }
-  for (int s = 0; s < NB; ++s) {
-    mbar_init(&b.b_full[s], 1);
-    mbar_init(&b.ready[s], 128);
-    mbar_init(&b.consumed[s], 1);
-  }
+  for (int s = 0; s < L::NBS; ++s) { mbar_init(&b.b_full[s], 1); mbar_init(&b.b_free[s], 1); }
+  for (int s = 0; s < NB; ++s) { mbar_init(&b.ready[s], 128); mbar_init(&b.tfree[s], 1); }
   for (int k = 0; k < 2; ++k) { mbar_init(&b.acc_full[k], 1); mbar_init(&b.acc_empty[k], 128); }
   fence_barrier_init();
 }
@@ -194,9 +195,10 @@ __device__ __forceinline__ void chunk_coords(const SParams& p, int64_t c, int64_
   else { beta = c / p.cpb; a0 = (c % p.cpb) * KC; j0 = a0 + p.a * beta; }
 }
 
-// grid (splits, mtiles): CTA (z, m) sums the chunks c = z, z + S, z + 2S, ... (S = splits) of M-tile
-// m.  Interleaving keeps all concurrently running CTAs of an M-tile inside a window of S chunks of
-// every row (DRAM-page / TLB locality for the long rows of the last mode).
+// grid (mtiles, splits): CTA (m, z) sums the chunks c = z, z + S, z + 2S, ... (S = splits) of M-tile m.
+// The M-tiles of a split are adjacent in launch order, so the CTAs that share a B chunk (Omega / Z
+// rows) run in the same wave and in near lockstep: B comes from DRAM once and from L2 for the rest
+// (a split-major order re-read Omega once per wave: +16% DRAM traffic on cfg5, ncu).
 template <int NPAD, bool BSPLIT, bool AMN>
 __global__ void __launch_bounds__(NT_TTM, 1)
 ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb, const SParams p) {
@@ -205,8 +207,8 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
   extern __shared__ __align__(1024) uint8_t smem[];
   const Bars b = bars_of<L>(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t z = blockIdx.x, S = gridDim.x;
-  const int64_t i0 = int64_t(blockIdx.y) * BM;
+  const int64_t z = blockIdx.y, S = gridDim.y;
+  const int64_t i0 = int64_t(blockIdx.x) * BM;
   const int nch = z < p.nchunks ? int((p.nchunks - z + S - 1) / S) : 0;
 
   if (threadIdx.x == 0) {
@@ -236,8 +238,8 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
   } else if (warp == 6) {
     if (lane == 0) {                                   // ---------------- B producer
       Ring rb;
-      for (int it = 0; it < nch; ++it, rb.next<NB>()) {
-        if (it >= NB) mbar_wait(&b.consumed[rb.s], rb.ph ^ 1);
+      for (int it = 0; it < nch; ++it, rb.next<L::NBS>()) {
+        if (it >= L::NBS) mbar_wait(&b.b_free[rb.s], rb.ph ^ 1);
         int64_t a0, beta, j0;
         chunk_coords<AMN>(p, z + it * S, a0, beta, j0);
         mbar_expect_tx(&b.b_full[rb.s], L::kB);
@@ -247,18 +249,20 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
   } else if (warp == 1) {
     if (lane == 0) {                                   // ---------------- MMA issuer
       const uint32_t idesc = idesc_tf32(BM, NPAD, 0);
-      Ring rb;
+      Ring rt, rb;
       int u = 0, pos = 0;
-      for (int it = 0; it < nch; ++it, rb.next<NB>()) {
+      for (int it = 0; it < nch; ++it, rt.next<NB>(), rb.next<L::NBS>()) {
         const bool first = pos == 0;
         const bool last = (pos == p.seg - 1) || (it == nch - 1);
         const int ab = u & 1;
         if (first && u >= 2) mbar_wait(&b.acc_empty[ab], ((u >> 1) - 1) & 1);
-        mbar_wait(&b.ready[rb.s], rb.ph);
+        mbar_wait(&b.ready[rt.s], rt.ph);
+        if (!BSPLIT) mbar_wait(&b.b_full[rb.s], rb.ph);
         tc_fence_after();
-        issue_stage<BSPLIT>(tmem, acc_col(ab), rb.s, smem_u32(smem + L::off_b + rb.s * L::kB),
-                            smem_u32(smem + L::off_blo + rb.s * L::kB), idesc, first);
-        mma_commit(&b.consumed[rb.s]);
+        issue_stage<BSPLIT>(tmem, acc_col(ab), rt.s, smem_u32(smem + L::off_b + rb.s * L::kB),
+                            smem_u32(smem + L::off_blo + rt.s * L::kB), idesc, first);
+        mma_commit(&b.tfree[rt.s]);
+        mma_commit(&b.b_free[rb.s]);
         if (last) { mma_commit(&b.acc_full[ab]); ++u; pos = 0; } else { ++pos; }
       }
     }
@@ -270,21 +274,23 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
     float sums[NPAD];
 #pragma unroll
     for (int k = 0; k < NPAD; ++k) sums[k] = 0.f;
-    Ring rx, rb;
+    Ring rx, rt, rb;
     int u = 0, pos = 0;
-    for (int it = 0; it < nch; ++it, rx.next<NX>(), rb.next<NB>()) {
+    for (int it = 0; it < nch; ++it, rx.next<NX>(), rt.next<NB>(), rb.next<L::NBS>()) {
       mbar_wait(&b.x_full[rx.s], rx.ph);
-      mbar_wait(&b.b_full[rb.s], rb.ph);              // implies TMEM slot rb.s is free (B producer waited)
+      if (it >= NB) mbar_wait(&b.tfree[rt.s], rt.ph ^ 1);   // TMEM slot (and B lo) free
       split_row_to_tmem<AMN>(reinterpret_cast<const float*>(smem + L::off_x + rx.s * L::kX), r,
-                             lane_base + kAStage + 64u * rb.s);
+                             lane_base + kAStage + 64u * rt.s);
       mbar_arrive(&b.x_free[rx.s]);
-      if (BSPLIT)
+      if (BSPLIT) {
+        mbar_wait(&b.b_full[rb.s], rb.ph);
         split_b<NPAD>(reinterpret_cast<float*>(smem + L::off_b + rb.s * L::kB),
-                      reinterpret_cast<float*>(smem + L::off_blo + rb.s * L::kB), t);
+                      reinterpret_cast<float*>(smem + L::off_blo + rt.s * L::kB), t);
+      }
       tmem_wait_st();
       if (BSPLIT) fence_proxy_async();
       tc_fence_before();
-      mbar_arrive(&b.ready[rb.s]);
+      mbar_arrive(&b.ready[rt.s]);
       const bool last = (pos == p.seg - 1) || (it == nch - 1);
       if (last) {
         if (u >= 1) drain_acc<NPAD>(b, lane_base, u - 1, sums);
@@ -369,8 +375,8 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
       Ring rb;
       int it = 0;
       for (int64_t u = 0; u < my_tiles; ++u)
-        for (int c = 0; c < p.nic; ++c, ++it, rb.next<NB>()) {
-          if (it >= NB) mbar_wait(&b.consumed[rb.s], rb.ph ^ 1);
+        for (int c = 0; c < p.nic; ++c, ++it, rb.next<L::NBS>()) {
+          if (it >= L::NBS) mbar_wait(&b.b_free[rb.s], rb.ph ^ 1);
           mbar_expect_tx(&b.b_full[rb.s], L::kB);
           tma_load_2d(smem + L::off_b + rb.s * L::kB, &tmb, &b.b_full[rb.s], c * KC, 0);
         }
@@ -378,20 +384,21 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
   } else if (warp == 1) {
     if (lane == 0) {                                   // ---------------- MMA issuer
       const uint32_t idesc = idesc_tf32(BM, NPAD, 0);
-      Ring rb;
+      Ring rt, rb;
       int64_t g = 0;                                   // global segment counter
       for (int64_t u = 0; u < my_tiles; ++u) {
         int pos = 0;
-        for (int c = 0; c < p.nic; ++c, rb.next<NB>()) {
+        for (int c = 0; c < p.nic; ++c, rt.next<NB>(), rb.next<L::NBS>()) {
           const bool first = pos == 0;
           const bool last = (pos == p.seg - 1) || (c == p.nic - 1);
           const int ab = int(g & 1);
           if (first && g >= 2) mbar_wait(&b.acc_empty[ab], uint32_t((g >> 1) - 1) & 1);
-          mbar_wait(&b.ready[rb.s], rb.ph);
+          mbar_wait(&b.ready[rt.s], rt.ph);
           tc_fence_after();
-          issue_stage<BSPLIT>(tmem, acc_col(ab), rb.s, smem_u32(smem + L::off_b + rb.s * L::kB),
-                              smem_u32(smem + L::off_blo + rb.s * L::kB), idesc, first);
-          mma_commit(&b.consumed[rb.s]);
+          issue_stage<BSPLIT>(tmem, acc_col(ab), rt.s, smem_u32(smem + L::off_b + rb.s * L::kB),
+                              smem_u32(smem + L::off_blo + rt.s * L::kB), idesc, first);
+          mma_commit(&b.tfree[rt.s]);
+          mma_commit(&b.b_free[rb.s]);
           if (last) { mma_commit(&b.acc_full[ab]); ++g; pos = 0; } else { ++pos; }
         }
       }
@@ -423,25 +430,27 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
         for (int k = 0; k < NPAD; ++k) sums[k] = 0.f;
       }
     };
-    Ring rx, rb;
+    Ring rx, rt, rb;
     int64_t g = 0;
     bool prev_end = false;
     int64_t prev_tile = 0;
+    int it = 0;
     for (int64_t u = 0; u < my_tiles; ++u) {
       const int64_t tile = blockIdx.x + u * gridDim.x;
       int pos = 0;
-      for (int c = 0; c < p.nic; ++c, rx.next<NX>(), rb.next<NB>()) {
+      for (int c = 0; c < p.nic; ++c, ++it, rx.next<NX>(), rt.next<NB>(), rb.next<L::NBS>()) {
         mbar_wait(&b.x_full[rx.s], rx.ph);
-        mbar_wait(&b.b_full[rb.s], rb.ph);
+        if (it >= NB) mbar_wait(&b.tfree[rt.s], rt.ph ^ 1);
         split_row_to_tmem<!AKM>(reinterpret_cast<const float*>(smem + L::off_x + rx.s * L::kX), r,
-                                lane_base + kAStage + 64u * rb.s);
+                                lane_base + kAStage + 64u * rt.s);
         mbar_arrive(&b.x_free[rx.s]);
+        mbar_wait(&b.b_full[rb.s], rb.ph);
         split_b<NPAD>(reinterpret_cast<float*>(smem + L::off_b + rb.s * L::kB),
-                      reinterpret_cast<float*>(smem + L::off_blo + rb.s * L::kB), t);
+                      reinterpret_cast<float*>(smem + L::off_blo + rt.s * L::kB), t);
         tmem_wait_st();
         fence_proxy_async();
         tc_fence_before();
-        mbar_arrive(&b.ready[rb.s]);
+        mbar_arrive(&b.ready[rt.s]);
         const bool last = (pos == p.seg - 1) || (c == p.nic - 1);
         if (last) {
           if (g >= 1) epilogue(g - 1, prev_end, prev_tile);   // delayed by one segment
@@ -586,7 +595,7 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
   splits = std::min<int64_t>(splits, 65535);
   p.seg = std::max(1, ctx.tc_seg);
   p.part = ws.alloc_n<float>(splits * K * box.I);
-  const dim3 grid{unsigned(splits), unsigned(mtiles), 1u};
+  const dim3 grid{unsigned(mtiles), unsigned(splits), 1u};
   const bool bsplit = !b_tf32_exact;
 #define RT_S_CASE(NP)                                              \
   case NP:                                                         \
