@@ -68,6 +68,7 @@ struct Ctx {
   int ttm_impl = 0;             // 0 auto, 1 SIMT, 2 tcgen05 (error if unavailable)
   int omega_tf32 = 0;           // caller asserts Gaussian Omega entries are tf32-representable
   int tc_seg = 4;               // tcgen05: 32-element chunks per TMEM accumulator segment (drained to fp32 regs)
+  int tc_ablate = 0;            // profiling only (RT_OPT_TC_ABLATE): 1 no MMA, 2 no split; results invalid
 };
 
 // Launch a kernel (given as a lambda issuing <<<...>>> on ctx.stream) with optional

@@ -128,18 +128,15 @@ __global__ void __launch_bounds__(512) chol_inv_kernel(const double* __restrict_
   }
   __syncthreads();
   const bool is_zero = (s_tr == 0.0);
-  for (int e = t; e < k * (k + 1) / 2; e += nt) {
-    // unpack e -> (i, c), i >= c
-    int i = int((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
-    while (tri(i + 1, 0) <= e) ++i;
-    while (tri(i, 0) > e) --i;
-    const int c = e - tri(i, 0);
-    L[e] = G[i + int64_t(k) * c] + (i == c ? s_shift : 0.0);
-    W[e] = (i == c) ? 1.0 : 0.0;
-  }
+  const int warp = t >> 5, lane = t & 31, nw = nt >> 5;
+  for (int i = warp; i < k; i += nw)
+    for (int c = lane; c <= i; c += 32) {
+      L[tri(i, c)] = G[i + int64_t(k) * c] + (i == c ? s_shift : 0.0);
+      W[tri(i, c)] = (i == c) ? 1.0 : 0.0;
+    }
   __syncthreads();
   if (!is_zero) {
-    // right-looking Cholesky G + sI = L L^T
+    // right-looking Cholesky G + sI = L L^T (rows by warp, columns by lane)
     for (int j = 0; j < k; ++j) {
       if (t == 0) {
         double d = L[tri(j, j)];
@@ -147,29 +144,23 @@ __global__ void __launch_bounds__(512) chol_inv_kernel(const double* __restrict_
         L[tri(j, j)] = sqrt(d);
       }
       __syncthreads();
-      const double ljj = L[tri(j, j)];
-      for (int i = j + 1 + t; i < k; i += nt) L[tri(i, j)] /= ljj;
+      const double rjj = 1.0 / L[tri(j, j)];
+      for (int i = j + 1 + t; i < k; i += nt) L[tri(i, j)] *= rjj;
       __syncthreads();
-      const int rem = k - j - 1;
-      for (int e = t; e < rem * (rem + 1) / 2; e += nt) {
-        int ii = int((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
-        while (tri(ii + 1, 0) <= e) ++ii;
-        while (tri(ii, 0) > e) --ii;
-        const int cc = e - tri(ii, 0);
-        const int i = j + 1 + ii, c = j + 1 + cc;
-        L[tri(i, c)] -= L[tri(i, j)] * L[tri(c, j)];
+      for (int i = j + 1 + warp; i < k; i += nw) {
+        const double lij = L[tri(i, j)];
+        for (int c = j + 1 + lane; c <= i; c += 32) L[tri(i, c)] -= lij * L[tri(c, j)];
       }
       __syncthreads();
     }
     // W = L^{-1}: row j final = B[j,:]/L_jj, then B[i,c] -= L_ij W[j,c] for i > j, c <= j
     for (int j = 0; j < k; ++j) {
-      const double ljj = L[tri(j, j)];
-      for (int c = t; c <= j; c += nt) W[tri(j, c)] /= ljj;
+      const double rjj = 1.0 / L[tri(j, j)];
+      for (int c = t; c <= j; c += nt) W[tri(j, c)] *= rjj;
       __syncthreads();
-      const int rows = k - j - 1;
-      for (int e = t; e < rows * (j + 1); e += nt) {
-        const int i = j + 1 + e / (j + 1), c = e % (j + 1);
-        W[tri(i, c)] -= L[tri(i, j)] * W[tri(j, c)];
+      for (int i = j + 1 + warp; i < k; i += nw) {
+        const double lij = L[tri(i, j)];
+        for (int c = lane; c <= j; c += 32) W[tri(i, c)] -= lij * W[tri(j, c)];
       }
       __syncthreads();
     }

@@ -160,20 +160,20 @@ struct Ring {
   template <int N> __device__ __forceinline__ void next() { if (++s == N) { s = 0; ph ^= 1; } }
 };
 
-// Drain accumulator buffer `ab` (use index u) into register sums; release the buffer.
+// Drain accumulator buffer `ab` (use index u) into register sums; release the buffer.  All
+// tcgen05.ld are issued before a single wait::ld.
 template <int NPAD>
 __device__ __forceinline__ void drain_acc(const Bars& b, uint32_t lane_base, int64_t u, float (&sums)[NPAD]) {
   const int ab = int(u & 1);
   mbar_wait(&b.acc_full[ab], uint32_t(u >> 1) & 1);
   tc_fence_after();
+  uint32_t v[NPAD];
 #pragma unroll
-  for (int cb = 0; cb < NPAD / 16; ++cb) {
-    uint32_t v[16];
-    tmem_ld16(lane_base + acc_col(ab) + 16 * cb, v);
-    tmem_wait_ld();
+  for (int cb = 0; cb < NPAD / 16; ++cb)
+    tmem_ld16(lane_base + acc_col(ab) + 16 * cb, *reinterpret_cast<uint32_t(*)[16]>(&v[16 * cb]));
+  tmem_wait_ld();
 #pragma unroll
-    for (int q = 0; q < 16; ++q) sums[16 * cb + q] += __uint_as_float(v[q]);
-  }
+  for (int k = 0; k < NPAD; ++k) sums[k] += __uint_as_float(v[k]);
   tc_fence_before();
   mbar_arrive(&b.acc_empty[ab]);
 }
@@ -185,6 +185,7 @@ struct SParams {
   int64_t cpb;        // chunks per beta (a > 1)
   int64_t nchunks;    // total j-chunks
   int seg;            // chunks per accumulator segment
+  int ablate;         // profiling only: 1 = no MMA, 2 = no split work (results invalid)
   float* part;        // [split][K][I]
 };
 
@@ -259,8 +260,9 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
         mbar_wait(&b.ready[rt.s], rt.ph);
         if (!BSPLIT) mbar_wait(&b.b_full[rb.s], rb.ph);
         tc_fence_after();
-        issue_stage<BSPLIT>(tmem, acc_col(ab), rt.s, smem_u32(smem + L::off_b + rb.s * L::kB),
-                            smem_u32(smem + L::off_blo + rt.s * L::kB), idesc, first);
+        if (p.ablate != 1)
+          issue_stage<BSPLIT>(tmem, acc_col(ab), rt.s, smem_u32(smem + L::off_b + rb.s * L::kB),
+                              smem_u32(smem + L::off_blo + rt.s * L::kB), idesc, first);
         mma_commit(&b.tfree[rt.s]);
         mma_commit(&b.b_free[rb.s]);
         if (last) { mma_commit(&b.acc_full[ab]); ++u; pos = 0; } else { ++pos; }
@@ -279,8 +281,9 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
     for (int it = 0; it < nch; ++it, rx.next<NX>(), rt.next<NB>(), rb.next<L::NBS>()) {
       mbar_wait(&b.x_full[rx.s], rx.ph);
       if (it >= NB) mbar_wait(&b.tfree[rt.s], rt.ph ^ 1);   // TMEM slot (and B lo) free
-      split_row_to_tmem<AMN>(reinterpret_cast<const float*>(smem + L::off_x + rx.s * L::kX), r,
-                             lane_base + kAStage + 64u * rt.s);
+      if (p.ablate != 2)
+        split_row_to_tmem<AMN>(reinterpret_cast<const float*>(smem + L::off_x + rx.s * L::kX), r,
+                               lane_base + kAStage + 64u * rt.s);
       mbar_arrive(&b.x_free[rx.s]);
       if (BSPLIT) {
         mbar_wait(&b.b_full[rb.s], rb.ph);
@@ -594,6 +597,7 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
   splits = std::min<int64_t>(splits, std::max<int64_t>(1, p.nchunks / 8));
   splits = std::min<int64_t>(splits, 65535);
   p.seg = std::max(1, ctx.tc_seg);
+  p.ablate = ctx.tc_ablate;
   p.part = ws.alloc_n<float>(splits * K * box.I);
   const dim3 grid{unsigned(mtiles), unsigned(splits), 1u};
   const bool bsplit = !b_tf32_exact;

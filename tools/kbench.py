@@ -22,6 +22,7 @@ ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--impl", type=int, default=0)
 ap.add_argument("--seg", type=int, default=0)
 ap.add_argument("--tf32", type=int, default=0)
+ap.add_argument("--ablate", type=int, default=0)
 a = ap.parse_args()
 
 dims = a.dims
@@ -33,6 +34,8 @@ h.set_option(L.RT_OPT_TTM_IMPL, a.impl)
 h.set_option(L.RT_OPT_OMEGA_TF32, a.tf32)
 if a.seg:
     h.set_option(L.RT_OPT_TC_SEGMENT, a.seg)
+if a.ablate:
+    h.set_option(100, a.ablate)
 modes = range(N) if a.modes is None else a.modes
 for n in modes:
     J = X.numel() // dims[n]

@@ -251,5 +251,35 @@ int main() {
     for (int i = 0; i < 128 * N; ++i) bad += D[i] != R[i];
     printf("probe_mma_sw128 K-major N=80: %s (%d bad) D0=%g R0=%g\n", bad ? "FAIL" : "ok", bad, D[0], R[0]);
   }
+  {  // probe 5: how does kind::tf32 convert fp32 inputs?  D = A * I (A in TMEM, B = identity K-major)
+    constexpr int N = 32;
+    std::vector<float> A(128 * 8), B(8 * N, 0.f), D(128 * N);
+    for (int r = 0; r < 128; ++r)
+      for (int k = 0; k < 8; ++k) {
+        uint32_t u = 0x3F800000u + uint32_t((r * 8 + k) * 37 % 8192) + (uint32_t(r % 7) << 13);  // 1.x with low bits
+        float f; memcpy(&f, &u, 4);
+        A[r * 8 + k] = (r & 1) ? -f : f;
+      }
+    for (int k = 0; k < 8; ++k) B[k * N + k] = 1.f;
+    float *dA, *dB, *dD;
+    CK(cudaMalloc(&dA, A.size() * 4)); CK(cudaMalloc(&dB, B.size() * 4)); CK(cudaMalloc(&dD, D.size() * 4));
+    CK(cudaMemcpy(dA, A.data(), A.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice));
+    probe_mma<N><<<1, 128>>>(dA, dB, dD, 0);
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost));
+    int trunc_ok = 0, rn_ok = 0, tot = 0;
+    for (int r = 0; r < 128; ++r)
+      for (int k = 0; k < 8; ++k) {
+        float x = A[r * 8 + k], d = D[r * N + k];
+        uint32_t u; memcpy(&u, &x, 4);
+        uint32_t t = u & 0xFFFFE000u;
+        uint32_t lsb = (u >> 13) & 1;
+        uint32_t rn = (u + 0x0FFFu + lsb) & 0xFFFFE000u;
+        float ft, fr; memcpy(&ft, &t, 4); memcpy(&fr, &rn, 4);
+        trunc_ok += d == ft; rn_ok += d == fr; ++tot;
+      }
+    printf("probe_tf32_conversion: %d/%d match truncation, %d/%d match round-nearest-even\n", trunc_ok, tot, rn_ok, tot);
+  }
   return 0;
 }
