@@ -30,6 +30,7 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 from gen import synth  # noqa: E402
+from paper_2001_07124_b200 import partition  # noqa: E402
 
 BASELINE = json.load(open(os.path.join(ROOT, "BASELINE.json")))
 METRIC = BASELINE["metric"]
@@ -193,15 +194,15 @@ def run_gpu(args, cfg):
     I_last = cfg.dims[-1]
     if I_last % world:
         raise SystemExit(f"last mode {I_last} not divisible by {world} ranks")
-    lo, hi = rank * I_last // world, (rank + 1) * I_last // world
+    lo, hi = partition.slab_range(I_last, world, rank)
     stream = torch.cuda.Stream(device=dev)
     with torch.cuda.stream(stream):
         X, info = synth.make_tensor_device(cfg, dev, last_range=(lo, hi))
         oms = []
         for n in range(N):
-            if n < N - 1:
-                a = int(np.prod(cfg.dims[:-1])) // cfg.dims[n]
-                oms.append(synth.gaussian_omega_device(cfg, n, dev, row0=a * lo, rows=a * (hi - lo), tf32=True))
+            rows = partition.omega_rows(cfg.dims, n, lo, hi)
+            if rows is not None:
+                oms.append(synth.gaussian_omega_device(cfg, n, dev, row0=rows[0], rows=rows[1], tf32=True))
             else:
                 oms.append(synth.gaussian_omega_device(cfg, n, dev, tf32=True))
         torch.cuda.synchronize()
@@ -292,7 +293,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-elems", type=float, default=2.0e8)
+    ap.add_argument("--cpu-sample-elems", type=float, default=5.0e8)
     args = ap.parse_args()
     cfg = synth.CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -308,7 +309,7 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        target = 1.2e7
+        target = 6.0e7                  # ~391^3 cube: a few s per step, whole run within minutes
         scfg, nbytes, times = run_oracle_steps(cfg, args.steps, args.warmup, target)
         tot = sum(times)
         val = nbytes * len(times) / tot / 1e9
