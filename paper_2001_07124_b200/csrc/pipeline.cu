@@ -158,23 +158,27 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
     ttm_s_dispatch(ctx, ws, data, bx, static_cast<const T*>(omega[n]), omega_ld[n], ctx.omega_tf32 != 0, K, Yt, In);
   } else {
     // Kronecker sketch W = X x_{k!=n} Omega_k^T (Eq.(2)): a chain of TTMs whose first
-    // stage streams X and whose later stages run on the shrunken result.
+    // stage streams X and whose later stages run on the shrunken result.  The factors are narrow
+    // (L_k = 2-4), so every stage is an fp64-accumulating CUDA-core contraction with fp64
+    // intermediates (HBM-bound at these widths): the chain adds no fp32 rounding.
     int64_t cur[5];
     for (int k = 0; k < N; ++k) cur[k] = X.d[k];
     K = 1;
     for (int k = 0; k < N; ++k) if (k != n) K *= int(omega_cols[k]);
     const auto mk = ws.mark();
-    const T* src = data;
+    const double* src = nullptr;
     for (int k = 0; k < N; ++k) {
       if (k == n) continue;
       const Box b = TView::box_of(cur, N, k);
       const int L = int(omega_cols[k]);
-      T* dst = ws.alloc_n<T>(b.a * L * b.b);
-      ttm_t_dispatch(ctx, src, b, static_cast<const T*>(omega[k]), omega_ld[k], L, dst, 1, b.a, b.a * L);
+      double* dst = ws.alloc_n<double>(b.a * L * b.b);
+      const T* om = static_cast<const T*>(omega[k]);
+      if (src == nullptr) ttm_t<T, T, double>(ctx, data, b, om, 1, omega_ld[k], L, dst, 1, b.a, b.a * L);
+      else                ttm_t<double, T, double>(ctx, src, b, om, 1, omega_ld[k], L, dst, 1, b.a, b.a * L);
       src = dst;
       cur[k] = L;
     }
-    unfold_copy<T>(ctx, src, TView::box_of(cur, N, n), Yt, In);
+    unfold_copy<double>(ctx, src, TView::box_of(cur, N, n), Yt, In);
     ws.rewind(mk);   // the Y result is in Yt; intermediates are dead (stream order)
   }
   allreduce(comm, !last && dist(), Yt, In * K, ctx.stream);                       // C1
@@ -379,6 +383,9 @@ void Engine::hosvd(const TView& X, const int64_t* R, int q, int kind, const void
 }
 
 // -------------------------------------------------------------- STHOSVD (Alg.8)
+// S = X for the first step; every shrunken S (and every B = S x_n Q~^T) is kept in fp64: they
+// are at most R_1/I_1 of |X|, and an fp32 rounding of the intermediates would perturb the later
+// modes' subspaces (and through them E) beyond the 1e-5 parity bar (tests/test_gpu_fullsize.py).
 template <typename T>
 void Engine::sthosvd(const TView& X, const int64_t* R, int q, int kind, const void* const* omega,
                      const int64_t* omega_cols, const int64_t* omega_ld, const int* order, double* const* Q_out,
@@ -386,13 +393,12 @@ void Engine::sthosvd(const TView& X, const int64_t* R, int q, int kind, const vo
   const int N = X.N;
   const auto mk = ws.mark();
   TView S = X;                         // working tensor S (reading R8: S = X)
-  const T* sdata = static_cast<const T*>(X.data);
-  // S only shrinks (R_n <= I_n): two persistent ping-pong buffers sized for the first shrink
+  const double* sd = nullptr;          // fp64 S after the first shrink
   int64_t total = 1;
   for (int k = 0; k < N; ++k) total *= X.d[k];
   const int first = order ? order[0] : 0;
   const int64_t smax = total / X.d[first] * R[first];
-  T* sbuf[2] = {ws.alloc_n<T>(smax), ws.alloc_n<T>(smax)};
+  double* sbuf[2] = {ws.alloc_n<double>(smax), ws.alloc_n<double>(smax)};
   for (int step = 0; step < N; ++step) {
     const int n = order ? order[step] : step;
     const void* const* om = omega + n * N;
@@ -405,34 +411,43 @@ void Engine::sthosvd(const TView& X, const int64_t* R, int q, int kind, const vo
     const auto mstep = ws.mark();
     // Alg.8 line 3 = Alg.1 lines 1-3 on S_(n): sketch (+ power iterations) and thin QR
     double* Yt = ws.alloc_n<double>(In * K);
-    sketch<T>(S, sdata, n, kind, om, oc, ol, q, Yt);
+    if (step == 0) {
+      sketch<T>(S, static_cast<const T*>(X.data), n, kind, om, oc, ol, q, Yt);
+    } else {
+      // the test matrices are in the data type; the fp64 S needs fp64 copies (small: S has shrunk)
+      const void* om64[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+      int64_t ld64[5] = {0, 0, 0, 0, 0};
+      for (int k = 0; k < N; ++k) {
+        if (!om[k] || (kind == 0 && k != n) || (kind != 0 && k == n)) continue;
+        const int64_t rows = (kind == 0) ? S.box(n).J() : S.d[k];
+        if (DT<T>::id == 1) { om64[k] = om[k]; ld64[k] = ol[k]; continue; }
+        double* c = ws.alloc_n<double>(rows * oc[k]);
+        convert2d<float, double>(ctx, static_cast<const float*>(om[k]), rows, oc[k], ol[k], c, rows);
+        om64[k] = c;
+        ld64[k] = rows;
+      }
+      sketch<double>(S, sd, n, kind, om64, oc, ld64, q, Yt);
+    }
     double* Qt = ws.alloc_n<double>(In * K);
     qr_y(Yt, In, In, K, In, Qt, In, nullptr, false, 0);
-    int64_t ldqt;
-    const T* QtT = working_copy<T>(ctx, ws, Qt, In, K, In, ldqt);
-    // Alg.1 line 4: B = S x_n Q~^T
+    // Alg.1 line 4: B = S x_n Q~^T (fp64 accumulation and output)
     const Box bs = S.box(n);
-    T* B = ws.alloc_n<T>(bs.a * K * bs.b);
-    ttm_t_dispatch(ctx, sdata, bs, QtT, ldqt, K, B, 1, bs.a, bs.a * K);
+    double* B = ws.alloc_n<double>(bs.a * K * bs.b);
+    if (step == 0) ttm_t<T, double, double>(ctx, static_cast<const T*>(X.data), bs, Qt, 1, In, K, B, 1, bs.a, bs.a * K);
+    else           ttm_t<double, double, double>(ctx, sd, bs, Qt, 1, In, K, B, 1, bs.a, bs.a * K);
     // Alg.1 lines 5-7 via the Gram-EVD of B_(n): U = top-R_n eigenvectors, Q_n = Q~ U
     const Box bb{bs.a, K, bs.b};
     double* M = ws.alloc_n<double>(int64_t(K) * K);
     double* V = ws.alloc_n<double>(int64_t(K) * K);
     double* W = ws.alloc_n<double>(K);
-    ttm_s<T>(ctx, ws, B, bb, nullptr, 0, 0, K, M, K, /*gram=*/true);
+    ttm_s<double>(ctx, ws, B, bb, nullptr, 0, 0, K, M, K, /*gram=*/true);
     eig_sym(ctx, ws, M, K, W, V);
     gemm_tall<double, double>(ctx, Qt, In, K, In, V, int(R[n]), K, Q_out[n], In);
     canon(Q_out[n], In, int(R[n]), In, 0, false, V, K);
     // Alg.8 line 4 with the ΛV^T shortcut: S <- B x_n U^T
-    T* VT = (DT<T>::id == 1) ? reinterpret_cast<T*>(V) : ws.alloc_n<T>(int64_t(K) * R[n]);
-    if (DT<T>::id == 0) convert2d<double, T>(ctx, V, K, R[n], K, VT, K);
-    if (step == N - 1) {
-      ttm_t<T, T, double>(ctx, B, bb, VT, 1, K, int(R[n]), G_out, 1, bb.a, bb.a * R[n]);
-    } else {
-      T* Snew = sbuf[step & 1];
-      ttm_t<T, T, T>(ctx, B, bb, VT, 1, K, int(R[n]), Snew, 1, bb.a, bb.a * R[n]);
-      sdata = Snew;
-    }
+    double* Snew = (step == N - 1) ? G_out : sbuf[step & 1];
+    ttm_t<double, double, double>(ctx, B, bb, V, 1, K, int(R[n]), Snew, 1, bb.a, bb.a * R[n]);
+    sd = Snew;
     ws.rewind(mstep);
     S.d[n] = R[n];
     S.glob = S.d[N - 1];

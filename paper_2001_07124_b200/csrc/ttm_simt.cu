@@ -12,6 +12,7 @@
 //           (Eq. Core), Kronecker sketch stages, STHOSVD shrink (Alg.8).
 //
 // X is read in place through the [a, I, b] box of kernels.h; nothing is permuted.
+#include <type_traits>
 #include "kernels.h"
 
 namespace rt {
@@ -19,6 +20,13 @@ namespace {
 
 template <typename T> struct AccOf { using type = float; };
 template <> struct AccOf<double> { using type = double; };
+// ttm_t accumulates in fp64 as soon as any operand or the output is fp64 (fp32 x fp32 products
+// are exact in fp64): the Kronecker chain and the STHOSVD shrink keep fp64 intermediates.
+template <typename A, typename B, typename C> struct Acc3 {
+  using type = typename std::conditional<std::is_same<A, double>::value || std::is_same<B, double>::value ||
+                                             std::is_same<C, double>::value,
+                                         double, float>::type;
+};
 
 // ------------------------------------------------------------------ ttm_s
 // Block tile: BM = 128 rows i, BJ contraction columns j per stage, BN = 16*TN sketch cols.
@@ -168,7 +176,7 @@ __global__ void __launch_bounds__(256)
 ttm_t_kernel(const Tin* __restrict__ X, int64_t a, int64_t I, int64_t J, const Tm* __restrict__ Mm,
              int64_t ms_i, int64_t ms_c, int C, Tout* __restrict__ out, int64_t so_a, int64_t so_c,
              int64_t so_b) {
-  using Tacc = typename AccOf<Tin>::type;
+  using Tacc = typename Acc3<Tin, Tm, Tout>::type;
   constexpr int BM = 128;
   constexpr int BI = sizeof(Tacc) == 8 ? 16 : 32;
   constexpr int BN = 8 * TN;
@@ -309,6 +317,10 @@ template void ttm_t<float, float, double>(const Ctx&, const float*, Box, const f
                                           double*, int64_t, int64_t, int64_t);
 template void ttm_t<double, double, double>(const Ctx&, const double*, Box, const double*, int64_t, int64_t,
                                             int, double*, int64_t, int64_t, int64_t);
+template void ttm_t<float, double, double>(const Ctx&, const float*, Box, const double*, int64_t, int64_t, int,
+                                           double*, int64_t, int64_t, int64_t);
+template void ttm_t<double, float, double>(const Ctx&, const double*, Box, const float*, int64_t, int64_t, int,
+                                           double*, int64_t, int64_t, int64_t);
 template void ttm_t<double, double, float>(const Ctx&, const double*, Box, const double*, int64_t, int64_t,
                                            int, float*, int64_t, int64_t, int64_t);
 
