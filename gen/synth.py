@@ -308,7 +308,7 @@ def gaussian_omega_device(cfg: Config, n: int, device, K: Optional[int] = None,
                           tf32: bool = False):
     """Gaussian Omega_n generated on device (torch Philox, seeded per 2^20-row chunk).
 
-    Returned as a (rows, K_n) column-major view (the library's layout).  Row blocks are drawn
+    Returned as a (rows, K_n) row-major tensor (the library's layout for test matrices).  Row blocks are drawn
     chunk-wise so that any contiguous row range (a slab's local rows) matches the full matrix
     bit-exactly.  ``tf32``: round to nearest tf32 (same rule as ``round_tf32``).
     """
@@ -318,7 +318,7 @@ def gaussian_omega_device(cfg: Config, n: int, device, K: Optional[int] = None,
     rows = J - row0 if rows is None else rows
     tdt = torch.float64 if cfg.dtype == "f64" else torch.float32
     dev = torch.device(device)
-    out = torch.empty((K, rows), dtype=tdt, device=dev).t()
+    out = torch.empty((rows, K), dtype=tdt, device=dev)
     c0 = (row0 // chunk_rows) * chunk_rows
     for c in range(c0, row0 + rows, chunk_rows):
         gen = torch.Generator(device=dev).manual_seed(_torch_seed(cfg.cfg_id, _OBJ_OMEGA, n, c))

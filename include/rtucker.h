@@ -10,10 +10,12 @@
  *   - tensors are dense, first-mode-fastest (element (i_1..i_N) at
  *     i_1 + I_1*(i_2 + I_2*(...))), device memory, 16-byte aligned;
  *   - "col-major m x k, ld" means element (i,c) at i + ld*c;
- *   - Gaussian test matrices Omega_n are col-major J_n x K_n with leading dimension ld >= J_n
- *     (element (j,c) at j + ld*c), rows in the paper's j-index order, dtype of X;
- *   - Kronecker factors Omega_k^{(n)} are col-major d_k x L_k (element (i,l) at i + ld*l);
- *   - the tensor-core path needs ld % 4 == 0 and 16-byte aligned columns (else CUDA cores);
+ *   - "row-major m x k, ld" means element (i,c) at i*ld + c;
+ *   - Gaussian test matrices Omega_n are row-major J_n x K_n with row pitch ld >= K_n
+ *     (element (j,c) at j*ld + c), rows in the paper's j-index order, dtype of X (a slab's
+ *     local rows are one contiguous row block);
+ *   - Kronecker factors Omega_k^{(n)} are row-major d_k x L_k (element (i,l) at i*ld + l);
+ *   - the tensor-core path needs ld % 4 == 0 and 16-byte aligned rows (else CUDA cores);
  *   - factors and cores are returned in fp64.
  *
  * Execution: every call is stream-ordered on the handle's CUDA stream and only
@@ -105,7 +107,8 @@ rt_status rt_sync(rt_handle* h);
  * accumulation error grows with this length, tests/test_gpu_tc.py).  RT_OPT_QR_FALLBACK is
  * reserved. */
 typedef enum { RT_OPT_TTM_IMPL = 0, RT_OPT_PROFILE = 1, RT_OPT_QR_FALLBACK = 2, RT_OPT_OMEGA_TF32 = 3,
-               RT_OPT_TC_SEGMENT = 4, RT_OPT_TC_ABLATE = 100 /* profiling only: invalid results */ } rt_option;
+               RT_OPT_TC_SEGMENT = 4, RT_OPT_TC_SKEW = 5,
+               RT_OPT_TC_ABLATE = 100 /* profiling only: invalid results */ } rt_option;
 rt_status rt_set_option(rt_handle* h, rt_option opt, int64_t value);
 
 /* Profile of the launches recorded since the last read (synchronizes the stream).
@@ -119,10 +122,10 @@ rt_status rt_profile_read(rt_handle* h, rt_profile_entry* out, int cap, int* n, 
 /* (1) Mode-n sketch with q power iterations  (Alg.6 line 3; Eq. proj P:166-172;
  *     Alg.1 line 2 P:205; sequential orthonormalization P:212, reading R2):
  *       Y = X_(n) Omega;  q times:  Q = qr(Y); Z = qr(X_(n)^T Q); Y = X_(n) Z.
- * kind == GAUSS: omega[mode] is J_n x K (local rows if mode < N-1 on a slab),
- *                omega_cols[mode] = K, omega_ld[mode] = its leading dimension.
- * kind == KRON : omega[k] is d_k x L_k for k != mode (d_{N-1} local on a slab),
- *                omega_cols[k] = L_k, omega_ld[k] >= d_k, K = prod_{k!=mode} L_k (Eq.(2)).
+ * kind == GAUSS: omega[mode] is row-major J_n x K (local rows if mode < N-1 on a slab),
+ *                omega_cols[mode] = K, omega_ld[mode] = its row pitch (>= K).
+ * kind == KRON : omega[k] is row-major d_k x L_k for k != mode (d_{N-1} local on a slab),
+ *                omega_cols[k] = L_k, omega_ld[k] >= L_k, K = prod_{k!=mode} L_k (Eq.(2)).
  * Y: fp64 col-major I_n x K, ld ldy >= I_n (local rows for mode N-1 on a slab).
  * Requires 1 <= K <= min(I_n, J_n) (global sizes) and K <= 256. */
 rt_status rtucker_sketch(rt_handle* h, const rt_tensor* X, int mode, rt_omega_kind kind,
@@ -153,8 +156,8 @@ rt_status rtucker_core(rt_handle* h, const rt_tensor* X, const double* const* Q,
  *     (reading R1: M_n = G~_(n) G~_(n)^T, U_n = top-R_n eigenvectors, Q_n = Q~_n U_n,
  *     G = G~ x_n U_n^T; sign of each column of Q_n canonicalized, reading R5).
  * omega / omega_cols / omega_ld: flat N x N tables indexed [n*N + k].  GAUSS: entry [n*N+n] is
- *   Omega_n (J_n x K_n, col-major) and omega_cols[n*N+n] = K_n = min(R_n + p, I_n, J_n).
- *   KRON: entries [n*N+k], k != n, are Omega_k^{(n)} (I_k x L_k), omega_cols = L_k,
+ *   Omega_n (J_n x K_n, row-major) and omega_cols[n*N+n] = K_n = min(R_n + p, I_n, J_n).
+ *   KRON: entries [n*N+k], k != n, are Omega_k^{(n)} (I_k x L_k, row-major), omega_cols = L_k,
  *   K_n = prod_{k!=n} L_k >= min(R_n + p, I_n) and K_n <= I_n.
  * Q_out[n]: fp64 col-major I_n x R_n (ld I_n, local rows for n = N-1 on a slab).
  * G_out: fp64 R_1 x ... x R_N.  rel_err / rel_err_gram: device fp64 scalars, nullable. */

@@ -57,6 +57,17 @@ def colmajor_ld(m: torch.Tensor):
     return c, max(1, c.shape[0])
 
 
+def rowmajor_ld(m: torch.Tensor):
+    """(tensor, ld): a row-major view (stride(1) == 1, stride(0) = ld >= cols) used in place, else a
+    packed row-major copy (the layout of every test matrix Omega, include/rtucker.h)."""
+    if m.dim() != 2:
+        raise ValueError("expected a matrix")
+    if m.stride(1) == 1 and m.stride(0) >= m.shape[1]:
+        return m, (m.stride(0) if m.shape[0] > 1 else max(1, m.shape[1]))
+    c = m.contiguous()
+    return c, max(1, c.shape[1])
+
+
 def new_colmajor(m: int, k: int, dtype=torch.float64, device=None) -> torch.Tensor:
     return torch.empty((k, m), dtype=dtype, device=device).t()
 
@@ -177,7 +188,7 @@ def _omega_table(N: int, omegas, kind: str):
         entries = [(n, omegas[n])] if kind == "gauss" else \
             [(k, omegas[n][k]) for k in range(N) if k != n and omegas[n][k] is not None]
         for k, om in entries:
-            om, ld = colmajor_ld(om)
+            om, ld = rowmajor_ld(om)
             keep.append(om)
             ptrs[n * N + k] = om
             cols[n * N + k] = om.shape[1]
@@ -196,7 +207,7 @@ def rtucker_sketch(h: Handle, X: torch.Tensor, mode: int, omega, q: int = 0, kin
     N = desc.order
     ptrs, cols, lds, keep = [None] * N, [0] * N, [0] * N, []
     if kind == "gauss":
-        om, ld = colmajor_ld(omega)
+        om, ld = rowmajor_ld(omega)
         keep.append(om)
         K = om.shape[1]
         if 0 <= mode < N:              # out-of-range modes are rejected by the library (RT_EINVAL)
@@ -206,7 +217,7 @@ def rtucker_sketch(h: Handle, X: torch.Tensor, mode: int, omega, q: int = 0, kin
         for k in range(N):
             if k == mode:
                 continue
-            o, ld = colmajor_ld(omega[k])
+            o, ld = rowmajor_ld(omega[k])
             keep.append(o)
             ptrs[k], cols[k], lds[k] = o, o.shape[1], ld
             K *= o.shape[1]

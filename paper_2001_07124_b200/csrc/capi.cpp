@@ -78,8 +78,9 @@ int64_t local_rows(const rt::TView& X, int n) {
 void check_gauss_omega(const rt::TView& X, int n, const void* om, int64_t K, int64_t ld, bool strict = true) {
   RT_REQUIRE(om != nullptr && (reinterpret_cast<uintptr_t>(om) % (X.dtype ? 8 : 4)) == 0, rt::kEINVAL,
              "Omega_n must be an aligned device pointer");
-  RT_REQUIRE(ld >= local_rows(X, n), rt::kEINVAL, "omega_ld must be >= the (local) row count J_n");
   RT_REQUIRE(K >= 1, rt::kEINVAL, "omega_cols must be >= 1");
+  RT_REQUIRE(ld >= K, rt::kEINVAL, "omega_ld (row pitch of the row-major Omega_n) must be >= K_n");
+  (void)local_rows;
   RT_REQUIRE(!strict || (K <= X.Ig(n) && K <= X.Jg(n)), rt::kERANK, "K_n must be <= min(I_n, J_n)");
   RT_REQUIRE(K <= 128, rt::kEUNSUPPORTED, "K_n > 128 not supported");
 }
@@ -91,7 +92,7 @@ int64_t check_kron_omega(const rt::TView& X, int n, const void* const* om, const
     if (k == n) continue;
     RT_REQUIRE(om[k] != nullptr, rt::kEINVAL, "Kronecker factor must be a device pointer");
     RT_REQUIRE(cols[k] >= 1, rt::kEINVAL, "Kronecker widths must be >= 1");
-    RT_REQUIRE(lds[k] >= X.d[k], rt::kEINVAL, "Kronecker factor ld must be >= d_k");
+    RT_REQUIRE(lds[k] >= cols[k], rt::kEINVAL, "Kronecker factor ld (row pitch) must be >= its width L_k");
     K *= cols[k];
   }
   RT_REQUIRE(!strict || K <= X.Ig(n), rt::kERANK, "Kronecker sketch width prod L_k must be <= I_n");
@@ -195,6 +196,7 @@ rt_status rt_set_option(rt_handle* h, rt_option opt, int64_t value) {
     case RT_OPT_OMEGA_TF32: h->ctx.omega_tf32 = int(value != 0); return RT_OK;
     case RT_OPT_TC_SEGMENT: h->ctx.tc_seg = int(value > 0 ? value : 4); return RT_OK;
     case RT_OPT_TC_ABLATE: h->ctx.tc_ablate = int(value); return RT_OK;
+    case RT_OPT_TC_SKEW: h->ctx.tc_skew = int(value); return RT_OK;
   }
   return fail(h, RT_EINVAL, "unknown option");
 }

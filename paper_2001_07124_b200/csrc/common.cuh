@@ -69,10 +69,20 @@ struct Ctx {
   int omega_tf32 = 0;           // caller asserts Gaussian Omega entries are tf32-representable
   int tc_seg = 4;               // tcgen05: 32-element chunks per TMEM accumulator segment (drained to fp32 regs)
   int tc_ablate = 0;            // profiling only (RT_OPT_TC_ABLATE): 1 no MMA, 2 no split; results invalid
+  int tc_skew = -1;             // ttm_s_tc: chunk-order rotation per M-tile (-1 = default)
+  mutable const char* label = nullptr;   // profiler name override for the next TC launches
 };
 
 // Launch a kernel (given as a lambda issuing <<<...>>> on ctx.stream) with optional
 // CUDA-event timing per kernel class.
+// Scoped profiler label: TC TTM launches inside the scope are recorded under `name`.
+struct LabelScope {
+  const Ctx& c;
+  const char* prev;
+  LabelScope(const Ctx& ctx, const char* name) : c(ctx), prev(ctx.label) { ctx.label = name; }
+  ~LabelScope() { c.label = prev; }
+};
+
 template <typename F>
 inline void launch(const Ctx& ctx, const char* name, F&& f) {
   Profiler* p = ctx.prof;

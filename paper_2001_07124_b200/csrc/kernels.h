@@ -27,17 +27,18 @@ void ttm_t(const Ctx& ctx, const Tin* X, Box box, const Tm* Mm, int64_t ms_i, in
 
 // tcgen05 tensor-core versions (ttm_tc.cu), fp32 only, 3xTF32 split.  Return false (nothing
 // launched) when the shape/alignment is outside the TMA path; callers then use the SIMT kernels.
-// B col-major (element (j,k) at j + ldb*k, ldb % 4 == 0, 16-byte aligned).  b_tf32_exact drops
-// the A_hi*B_lo product.
+// ttm_s_tc: B row-major (element (j,k) at j*ldb + k, ldb % 4 == 0, 16-byte aligned), consumed as an
+// MN-major operand.  b_tf32_exact drops the A_hi*B_lo product.
 bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Bm, int64_t ldb, bool b_tf32_exact,
               int K, double* Y, int64_t ldy);
 // out(alpha,c,beta) = sum_i X(alpha,i,beta) Q(i,c), Q col-major with ldq % 4 == 0
 bool ttm_t_tc(const Ctx& ctx, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
               int64_t so_a, int64_t so_c, int64_t so_b);
 
-// Gram of a col-major m x k matrix (fp64 out, k x k), partials reduced in fixed order.
+// Gram A^T A of an m x k matrix (fp64 out, k x k), partials reduced in fixed order.  A col-major
+// (element (r,c) at r + lda*c) or, with rowmajor, at r*lda + c.
 template <typename T>
-void gram(const Ctx& ctx, Arena& ws, const T* A, int64_t m, int k, int64_t lda, double* G);
+void gram(const Ctx& ctx, Arena& ws, const T* A, int64_t m, int k, int64_t lda, double* G, bool rowmajor = false);
 
 // Cholesky of (G + shift*I) (k x k) -> R (upper, col-major) and Rinv.  shift_coef * trace(G)
 // is the shift.  zero_flag[0] = 1 if trace(G) == 0 (all-zero input, reading R7).
@@ -45,11 +46,13 @@ void chol_inv(const Ctx& ctx, const double* G, int k, double shift_coef, double*
               int* zero_flag);
 
 // C(m x n) = A(m x k) * B(k x n); A col-major (lda) of TA, B fp64 col-major (ldb), C of TC (ldc).
+// rowmajor: A and C are row-major (row pitches lda, ldc).
 // A == C allowed (in place, n == k).  zero_flag != nullptr && *zero_flag: C(i,c) = (row0+i == c)
 // (rows of the identity I[:, :n], row0 = global index of the first local row).
 template <typename TA, typename TC>
 void gemm_tall(const Ctx& ctx, const TA* A, int64_t m, int k, int64_t lda, const double* B, int n,
-               int64_t ldb, TC* C, int64_t ldc, const int* zero_flag = nullptr, int64_t row0 = 0);
+               int64_t ldb, TC* C, int64_t ldc, const int* zero_flag = nullptr, int64_t row0 = 0,
+               bool rowmajor = false);
 
 // Small dense fp64 GEMM C = op(A) op(B) (col-major), for k x k triangular products.
 void gemm_small(const Ctx& ctx, bool ta, bool tb, int m, int n, int k, const double* A, int lda,

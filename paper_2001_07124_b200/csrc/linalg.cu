@@ -37,7 +37,7 @@ __device__ inline T block_sum(T v, T* sh) {
 // part[z][p + k*q] = sum_{rows of split z} A(row,p) A(row,q); fp64 products and sums.
 template <typename T, int KB>
 __global__ void __launch_bounds__(256) gram_kernel(const T* __restrict__ A, int64_t m, int k, int64_t lda,
-                                                    int64_t rps, double* __restrict__ part) {
+                                                    int64_t rps, double* __restrict__ part, bool rm) {
   constexpr int RB = 16;
   __shared__ double As[RB][16 * KB + 1];
   const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
@@ -49,9 +49,9 @@ __global__ void __launch_bounds__(256) gram_kernel(const T* __restrict__ A, int6
     for (int b = 0; b < KB; ++b) acc[a][b] = 0.0;
   for (int64_t rc = r0; rc < r1; rc += RB) {
     for (int e = t; e < RB * 16 * KB; e += 256) {
-      const int rl = e % RB, c = e / RB;
+      const int rl = rm ? e / (16 * KB) : e % RB, c = rm ? e % (16 * KB) : e / RB;
       const int64_t row = rc + rl;
-      As[rl][c] = (row < r1 && c < k) ? double(A[row + lda * c]) : 0.0;
+      As[rl][c] = (row < r1 && c < k) ? double(rm ? A[row * lda + c] : A[row + lda * c]) : 0.0;
     }
     __syncthreads();
 #pragma unroll 4
@@ -88,13 +88,13 @@ __global__ void reduce_parts_kernel(const double* __restrict__ part, int64_t n, 
 }
 
 template <typename T, int KB>
-void launch_gram(const Ctx& ctx, Arena& ws, const T* A, int64_t m, int k, int64_t lda, double* G) {
+void launch_gram(const Ctx& ctx, Arena& ws, const T* A, int64_t m, int k, int64_t lda, double* G, bool rm) {
   int64_t splits = std::max<int64_t>(1, std::min<int64_t>(2LL * ctx.num_sms, cdiv(m, 64)));
   const int64_t rps = cdiv(cdiv(m, splits), 16) * 16;
   splits = std::max<int64_t>(1, cdiv(m, rps));
   double* part = ws.alloc_n<double>(splits * k * k);
   launch(ctx, "gram", [&] {
-    gram_kernel<T, KB><<<unsigned(splits), 256, 0, ctx.stream>>>(A, m, k, lda, rps, part);
+    gram_kernel<T, KB><<<unsigned(splits), 256, 0, ctx.stream>>>(A, m, k, lda, rps, part, rm);
   });
   const int64_t n = int64_t(k) * k;
   launch(ctx, "gram_reduce", [&] {
@@ -185,7 +185,9 @@ template <typename TA, typename TC>
 __global__ void __launch_bounds__(256) gemm_tall_kernel(const TA* A, int64_t m, int k, int64_t lda,
                                                          const double* __restrict__ B, int n, int64_t ldb,
                                                          TC* C, int64_t ldc, const int* zero_flag,
-                                                         int64_t grow0) {
+                                                         int64_t grow0, bool rm) {
+  // element (row, c): col-major at row + ld*c, row-major (rm) at row*ld + c
+  const int64_t ars = rm ? lda : 1, acs = rm ? 1 : lda, crs = rm ? ldc : 1, ccs = rm ? 1 : ldc;
   extern __shared__ double sm[];
   constexpr int BR = 32;
   double* Bs = sm;                  // k x n, Bs[l*n + c]
@@ -197,7 +199,7 @@ __global__ void __launch_bounds__(256) gemm_tall_kernel(const TA* A, int64_t m, 
     for (int e = t; e < BR * n; e += 256) {
       const int rl = e % BR, c = e / BR;
       const int64_t row = r0 + rl;
-      if (row < m) C[row + ldc * c] = TC(grow0 + row == c ? 1.0 : 0.0);
+      if (row < m) C[row * crs + ccs * c] = TC(grow0 + row == c ? 1.0 : 0.0);
     }
     return;
   }
@@ -208,7 +210,7 @@ __global__ void __launch_bounds__(256) gemm_tall_kernel(const TA* A, int64_t m, 
   for (int e = t; e < BR * k; e += 256) {
     const int rl = e % BR, l = e / BR;
     const int64_t row = r0 + rl;
-    As[rl * (k + 1) + l] = row < m ? double(A[row + lda * l]) : 0.0;
+    As[rl * (k + 1) + l] = row < m ? double(A[row * ars + acs * l]) : 0.0;
   }
   __syncthreads();
   const int rl = t % BR, cg = t / BR;
@@ -217,7 +219,7 @@ __global__ void __launch_bounds__(256) gemm_tall_kernel(const TA* A, int64_t m, 
     for (int c = cg; c < n; c += 8) {
       double s = 0.0;
       for (int l = 0; l < k; ++l) s = fma(As[rl * (k + 1) + l], Bs[l * n + c], s);
-      C[row + ldc * c] = TC(s);
+      C[row * crs + ccs * c] = TC(s);
     }
   }
 }
@@ -521,19 +523,19 @@ __global__ void nonfinite_kernel(const double* __restrict__ x, int64_t n, int* s
 
 // ======================================================================= host
 template <typename T>
-void gram(const Ctx& ctx, Arena& ws, const T* A, int64_t m, int k, int64_t lda, double* G) {
+void gram(const Ctx& ctx, Arena& ws, const T* A, int64_t m, int k, int64_t lda, double* G, bool rm) {
   RT_REQUIRE(k >= 1 && k <= 128, kEUNSUPPORTED, "gram: k must be in [1,128]");
   if (m == 0) { RT_CUDA(cudaMemsetAsync(G, 0, sizeof(double) * k * k, ctx.stream)); return; }
-  if (k <= 16) launch_gram<T, 1>(ctx, ws, A, m, k, lda, G);
-  else if (k <= 32) launch_gram<T, 2>(ctx, ws, A, m, k, lda, G);
-  else if (k <= 48) launch_gram<T, 3>(ctx, ws, A, m, k, lda, G);
-  else if (k <= 64) launch_gram<T, 4>(ctx, ws, A, m, k, lda, G);
-  else if (k <= 80) launch_gram<T, 5>(ctx, ws, A, m, k, lda, G);
-  else if (k <= 96) launch_gram<T, 6>(ctx, ws, A, m, k, lda, G);
-  else launch_gram<T, 8>(ctx, ws, A, m, k, lda, G);
+  if (k <= 16) launch_gram<T, 1>(ctx, ws, A, m, k, lda, G, rm);
+  else if (k <= 32) launch_gram<T, 2>(ctx, ws, A, m, k, lda, G, rm);
+  else if (k <= 48) launch_gram<T, 3>(ctx, ws, A, m, k, lda, G, rm);
+  else if (k <= 64) launch_gram<T, 4>(ctx, ws, A, m, k, lda, G, rm);
+  else if (k <= 80) launch_gram<T, 5>(ctx, ws, A, m, k, lda, G, rm);
+  else if (k <= 96) launch_gram<T, 6>(ctx, ws, A, m, k, lda, G, rm);
+  else launch_gram<T, 8>(ctx, ws, A, m, k, lda, G, rm);
 }
-template void gram<float>(const Ctx&, Arena&, const float*, int64_t, int, int64_t, double*);
-template void gram<double>(const Ctx&, Arena&, const double*, int64_t, int, int64_t, double*);
+template void gram<float>(const Ctx&, Arena&, const float*, int64_t, int, int64_t, double*, bool);
+template void gram<double>(const Ctx&, Arena&, const double*, int64_t, int, int64_t, double*, bool);
 
 void chol_inv(const Ctx& ctx, const double* G, int k, double shift_coef, double* R, double* Rinv,
               int* zero_flag) {
@@ -551,7 +553,7 @@ void chol_inv(const Ctx& ctx, const double* G, int k, double shift_coef, double*
 
 template <typename TA, typename TC>
 void gemm_tall(const Ctx& ctx, const TA* A, int64_t m, int k, int64_t lda, const double* B, int n,
-               int64_t ldb, TC* C, int64_t ldc, const int* zero_flag, int64_t row0) {
+               int64_t ldb, TC* C, int64_t ldc, const int* zero_flag, int64_t row0, bool rowmajor) {
   if (m == 0 || n == 0) return;
   const size_t smem = sizeof(double) * (size_t(k) * n + 32 * size_t(k + 1));
   RT_REQUIRE(smem <= 220 * 1024, kEUNSUPPORTED, "gemm_tall: k*n too large");
@@ -562,15 +564,15 @@ void gemm_tall(const Ctx& ctx, const TA* A, int64_t m, int k, int64_t lda, const
   }
   launch(ctx, "gemm_tall", [&] {
     gemm_tall_kernel<TA, TC><<<unsigned(cdiv(m, 32)), 256, smem, ctx.stream>>>(A, m, k, lda, B, n, ldb, C, ldc,
-                                                                               zero_flag, row0);
+                                                                               zero_flag, row0, rowmajor);
   });
 }
 template void gemm_tall<double, double>(const Ctx&, const double*, int64_t, int, int64_t, const double*, int,
-                                        int64_t, double*, int64_t, const int*, int64_t);
+                                        int64_t, double*, int64_t, const int*, int64_t, bool);
 template void gemm_tall<float, float>(const Ctx&, const float*, int64_t, int, int64_t, const double*, int,
-                                      int64_t, float*, int64_t, const int*, int64_t);
+                                      int64_t, float*, int64_t, const int*, int64_t, bool);
 template void gemm_tall<float, double>(const Ctx&, const float*, int64_t, int, int64_t, const double*, int,
-                                       int64_t, double*, int64_t, const int*, int64_t);
+                                       int64_t, double*, int64_t, const int*, int64_t, bool);
 
 void gemm_small(const Ctx& ctx, bool ta, bool tb, int m, int n, int k, const double* A, int lda,
                 const double* B, int ldb, double* C, int ldc) {

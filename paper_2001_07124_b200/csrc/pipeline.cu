@@ -28,16 +28,16 @@ void allreduce(Comm* c, bool on, T* p, int64_t n, cudaStream_t s) {
 
 int64_t pad4(int64_t x) { return (x + 3) & ~int64_t(3); }
 
-// Y = X_(n) B (B col-major, ldb): tcgen05 3xTF32 kernel for fp32 data when the shape fits the
-// TMA path, else the SIMT kernel.
+// Y = X_(n) B (B row-major, row pitch ldb: Omega or Z): tcgen05 3xTF32 kernel for fp32 data when
+// the shape fits the TMA path, else the SIMT kernel.
 void ttm_s_dispatch(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B, int64_t ldb, bool exact,
                     int K, double* Y, int64_t ldy) {
   if (ctx.ttm_impl != 1 && ttm_s_tc(ctx, ws, X, box, B, ldb, exact, K, Y, ldy)) return;
-  ttm_s<float>(ctx, ws, X, box, B, 1, ldb, K, Y, ldy);
+  ttm_s<float>(ctx, ws, X, box, B, ldb, 1, K, Y, ldy);
 }
 void ttm_s_dispatch(const Ctx& ctx, Arena& ws, const double* X, Box box, const double* B, int64_t ldb, bool,
                     int K, double* Y, int64_t ldy) {
-  ttm_s<double>(ctx, ws, X, box, B, 1, ldb, K, Y, ldy);
+  ttm_s<double>(ctx, ws, X, box, B, ldb, 1, K, Y, ldy);
 }
 // out(alpha,c,beta) = sum_i X(alpha,i,beta) Q(i,c), Q col-major (ldq)
 void ttm_t_dispatch(const Ctx& ctx, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
@@ -108,7 +108,8 @@ void Engine::qr_y(const double* Y, int64_t m, int64_t m_glob, int k, int64_t ldy
 }
 
 // Z only conditions the next product Y = X_(n) Z (span(X Z R^-1) = span(X Z)); a single
-// CholeskyQR step with a small safety shift keeps it well conditioned.
+// CholeskyQR step with a small safety shift keeps it well conditioned.  Z is row-major
+// (m x k, row pitch ldz).
 template <typename T>
 void Engine::qr_z(T* Z, int64_t m, int64_t ldz, int64_t m_glob, int k, bool rows_dist, int64_t row0) {
   const auto mk = ws.mark();
@@ -116,16 +117,19 @@ void Engine::qr_z(T* Z, int64_t m, int64_t ldz, int64_t m_glob, int k, bool rows
   double* Rr = ws.alloc_n<double>(int64_t(k) * k);
   double* Ri = ws.alloc_n<double>(int64_t(k) * k);
   int* zero = ws.alloc_n<int>(1);
-  // fp32 Z on the tensor cores: view Z (ldz x k, pad rows zero) as a 2-way tensor [a=ldz, I=k]; its
-  // mode-1 "sketch" with B = Z is Z^T Z, and its mode-1 TTM with R^{-1} is Z R^{-1} (in place: every
-  // 128-row tile is read completely before it is written, by the one CTA that owns it).
-  const bool tc = std::is_same<T, float>::value && ctx.ttm_impl != 1;
-  const Box zb{ldz, k, 1};
+  // fp32 Z on the tensor cores: view Z as the 2-way tensor [a=1, I=k, b=m] (element (c, j) at c + k j);
+  // its mode-0 "sketch" with B = Z is Z^T Z, and its mode-0 TTM with R^{-1} is Z R^{-1} (in place:
+  // every 128-row tile is read completely before it is written, by the one CTA that owns it).
+  const bool tc = std::is_same<T, float>::value && ctx.ttm_impl != 1 && ldz == k;
+  const Box zb{1, k, m};
   bool done_gram = false;
   if constexpr (std::is_same<T, float>::value) {
-    if (tc) done_gram = ttm_s_tc(ctx, ws, Z, zb, Z, ldz, false, k, G, k);
+    if (tc) {
+      LabelScope ls(ctx, "zgram_tc");
+      done_gram = ttm_s_tc(ctx, ws, Z, zb, Z, ldz, false, k, G, k);
+    }
   }
-  if (!done_gram) gram<T>(ctx, ws, Z, m, k, ldz, G);
+  if (!done_gram) gram<T>(ctx, ws, Z, m, k, ldz, G, /*rowmajor=*/true);
   allreduce(comm, rows_dist && dist(), G, int64_t(k) * k, ctx.stream);
   (void)m_glob;
   // Shift: the tensor-core Gram carries ~1e-6 relative error (3xTF32, fp32 TMEM segments), far
@@ -137,10 +141,11 @@ void Engine::qr_z(T* Z, int64_t m, int64_t ldz, int64_t m_glob, int k, bool rows
     if (tc) {
       int64_t ldr;
       const float* RiT = working_copy<float>(ctx, ws, Ri, k, k, k, ldr);
-      done_apply = ttm_t_tc(ctx, Z, zb, RiT, ldr, k, Z, 1, ldz, 0);
+      LabelScope ls(ctx, "zapply_tc");
+      done_apply = ttm_t_tc(ctx, Z, zb, RiT, ldr, k, Z, 0, 1, ldz);
     }
   }
-  if (!done_apply) gemm_tall<T, T>(ctx, Z, m, k, ldz, Ri, k, k, Z, ldz, zero, row0);
+  if (!done_apply) gemm_tall<T, T>(ctx, Z, m, k, ldz, Ri, k, k, Z, ldz, zero, row0, /*rowmajor=*/true);
   ws.rewind(mk);
 }
 
@@ -173,8 +178,9 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
       const int L = int(omega_cols[k]);
       double* dst = ws.alloc_n<double>(b.a * L * b.b);
       const T* om = static_cast<const T*>(omega[k]);
-      if (src == nullptr) ttm_t<T, T, double>(ctx, data, b, om, 1, omega_ld[k], L, dst, 1, b.a, b.a * L);
-      else                ttm_t<double, T, double>(ctx, src, b, om, 1, omega_ld[k], L, dst, 1, b.a, b.a * L);
+      // Omega_k row-major (d_k x L_k, row pitch omega_ld[k]): M(i, c) at i*ld + c
+      if (src == nullptr) ttm_t<T, T, double>(ctx, data, b, om, omega_ld[k], 1, L, dst, 1, b.a, b.a * L);
+      else                ttm_t<double, T, double>(ctx, src, b, om, omega_ld[k], 1, L, dst, 1, b.a, b.a * L);
       src = dst;
       cur[k] = L;
     }
@@ -188,19 +194,23 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
   const auto mk = ws.mark();
   const int64_t Jl = bx.J();
   double* Qy = ws.alloc_n<double>(In * K);
-  const int64_t ldz = pad4(Jl);            // 16-byte column pitch for the TMA path; pad rows zero
-  T* Z = ws.alloc_n<T>(ldz * K);
-  if (ldz != Jl) fill_zero(ctx, Z, sizeof(T) * ldz * K);
+  const int64_t ldz = pad4(K);             // Z row-major (Jl x K), 16-byte row pitch; pad columns zero
+  T* Z = ws.alloc_n<T>(Jl * ldz);
+  if (ldz != K) fill_zero(ctx, Z, sizeof(T) * Jl * ldz);
   const int64_t row0_last = X.off;
   for (int it = 0; it < q; ++it) {
     qr_y(Yt, In, X.Ig(n), K, In, Qy, In, nullptr, last && dist(), last ? row0_last : 0);
     const auto mq = ws.mark();
     int64_t ldqt;
     const T* QyT = working_copy<T>(ctx, ws, Qy, In, K, In, ldqt);
-    // Z(j, c) = sum_i X_(n)(i, j) Q(i, c), written col-major J x K: so_a=1, so_c=ldz, so_b=a
-    ttm_t_dispatch(ctx, data, bx, QyT, ldqt, K, Z, 1, ldz, bx.a);
+    // Z(j, c) = sum_i X_(n)(i, j) Q(i, c), written row-major J x K (j = alpha + a beta):
+    // so_a = ldz, so_c = 1, so_b = a ldz
+    {
+      LabelScope ls(ctx, "ttm_t_tc_pow");
+      ttm_t_dispatch(ctx, data, bx, QyT, ldqt, K, Z, ldz, 1, bx.a * ldz);
+    }
     ws.rewind(mq);
-    allreduce(comm, last && dist(), Z, ldz * K, ctx.stream);                     // C3
+    allreduce(comm, last && dist(), Z, Jl * ldz, ctx.stream);                    // C3
     // local Z rows: for n < N-1 the slab's j's are the contiguous block starting at a*b'*off
     int64_t zrow0 = 0;
     if (!last) {
@@ -209,7 +219,10 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
       zrow0 = bx.a * bp * X.off;
     }
     qr_z<T>(Z, Jl, ldz, X.Jg(n), K, !last && dist(), zrow0);
-    ttm_s_dispatch(ctx, ws, data, bx, Z, ldz, false, K, Yt, In);
+    {
+      LabelScope ls(ctx, "ttm_s_tc_pow");
+      ttm_s_dispatch(ctx, ws, data, bx, Z, ldz, false, K, Yt, In);
+    }
     allreduce(comm, !last && dist(), Yt, In * K, ctx.stream);                     // C1
   }
   ws.rewind(mk);
@@ -421,10 +434,11 @@ void Engine::sthosvd(const TView& X, const int64_t* R, int q, int kind, const vo
         if (!om[k] || (kind == 0 && k != n) || (kind != 0 && k == n)) continue;
         const int64_t rows = (kind == 0) ? S.box(n).J() : S.d[k];
         if (DT<T>::id == 1) { om64[k] = om[k]; ld64[k] = ol[k]; continue; }
+        // row-major rows x cols (pitch ld) == col-major cols x rows: convert, packed pitch = cols
         double* c = ws.alloc_n<double>(rows * oc[k]);
-        convert2d<float, double>(ctx, static_cast<const float*>(om[k]), rows, oc[k], ol[k], c, rows);
+        convert2d<float, double>(ctx, static_cast<const float*>(om[k]), oc[k], rows, ol[k], c, oc[k]);
         om64[k] = c;
-        ld64[k] = rows;
+        ld64[k] = oc[k];
       }
       sketch<double>(S, sd, n, kind, om64, oc, ld64, q, Yt);
     }

@@ -29,11 +29,24 @@ using namespace tc;
 constexpr int KC = 32;           // contraction elements per stage
 constexpr int BM = 128;          // tile rows = TMEM lanes
 constexpr int NTHREADS = 192;    // residual kernel
-constexpr int NT_TTM = 224;      // TTM kernels: + a B-producer warp
-constexpr int NB = 4;            // B / TMEM-A ring depth
-constexpr uint32_t kAStage = 256;  // TMEM: accumulators at columns 0 and 128, A slot s at 256 + 64 s
+constexpr int NT_TTM = 256;      // TTM kernels: producer, MMA issuer, 4 splitters, B producer, 2nd issuer
 
-__host__ __device__ constexpr uint32_t acc_col(int b) { return b ? 128u : 0u; }
+// MMA issue model (tools/mma_rate.cu): one thread's tcgen05.mma instructions complete one after
+// another (~110-160 cycles each, independent of N), while MMAs issued by different warps overlap.
+// The k-steps of every stage are therefore split between NI issuer warps, each accumulating into
+// its own (double-buffered) TMEM accumulator; the epilogue adds the NI partial accumulators.
+// TMEM (512 columns): accumulator (q, buffer) at column (2q + buffer) * NPAD, then NB A slots of 64
+// columns (hi | lo).
+template <int NPAD> struct TmemPlan {
+  static constexpr int NI = NPAD <= 96 ? 2 : 1;
+  static constexpr uint32_t acc_cols = uint32_t(2 * NI * NPAD);
+  static constexpr uint32_t a_base = (acc_cols + 63u) & ~63u;
+  static constexpr int NB_fit = int((512u - a_base) / 64u);
+  static constexpr int NB = NB_fit > 4 ? 4 : NB_fit;   // TMEM-A (and B lo) ring depth
+  static_assert(NB >= 2, "TMEM plan leaves fewer than two A slots");
+  __host__ __device__ static constexpr uint32_t acc(int q, int b) { return uint32_t((2 * q + b) * NPAD); }
+  __host__ __device__ static constexpr uint32_t a_slot(int s) { return a_base + 64u * uint32_t(s); }
+};
 
 // Shared memory plan of the TTM kernels.  Three rings:
 //   X ring (NX stages of raw 16 KB X tiles): TMA -> splitter; a stage is released as soon as the
@@ -41,10 +54,20 @@ __host__ __device__ constexpr uint32_t acc_col(int b) { return b ? 128u : 0u; }
 //   B ring (NBS stages of [NPAD][32] 128B-swizzled B tiles): TMA -> MMA (B hi is split in place),
 //     released by tcgen05.commit; deeper than the TMEM ring so B (L2 or DRAM) latency is hidden;
 //   TMEM A slots (NB = 4, 64 columns each: hi | lo) + B lo tiles (when split): splitter -> MMA.
-template <int NPAD, bool BSPLIT>
+// B tile bytes: K-major [NPAD][32] (128 B rows), or MN-major (row-major B in global memory, e.g.
+// Omega / Z): ceil(NPAD/32) atom columns of [32 k-rows][32 n] (4 KB each, SWIZZLE_128B_ATOM_32B).
+template <int NPAD, bool BMN>
+__host__ __device__ constexpr uint32_t b_tile_bytes() {
+  return BMN ? uint32_t((NPAD + 31) / 32) * 4096u : uint32_t(NPAD) * KC * 4;
+}
+
+template <int NPAD, bool BSPLIT, bool BMN = false>
 struct Smem {
+  using TP = TmemPlan<NPAD>;
+  static constexpr int NB = TP::NB;
+  static constexpr int NI = TP::NI;
   static constexpr uint32_t kX = uint32_t(BM) * KC * 4;
-  static constexpr uint32_t kB = uint32_t(NPAD) * KC * 4;
+  static constexpr uint32_t kB = b_tile_bytes<NPAD, BMN>();
   static constexpr uint32_t budget = 212u * 1024u;
   static constexpr uint32_t lo_bytes = BSPLIT ? NB * kB : 0;
   static constexpr int NBS = NPAD <= 96 ? 8 : 4;
@@ -54,7 +77,7 @@ struct Smem {
   static constexpr uint32_t off_b = off_x + NX * kX;
   static constexpr uint32_t off_blo = off_b + NBS * kB;
   static constexpr uint32_t off_bar = off_blo + lo_bytes;
-  static constexpr int nbar = 2 * NX + 2 * NBS + 2 * NB + 4;
+  static constexpr int nbar = 2 * NX + 2 * NBS + 2 * 4 + 4;
   static constexpr uint32_t bytes = off_bar + 8 * nbar + 16;
   static_assert(NX >= 4, "X ring too shallow");
 };
@@ -73,8 +96,8 @@ __device__ __forceinline__ Bars bars_of(uint8_t* smem) {
   r.b_full = b + 2 * L::NX;
   r.b_free = b + 2 * L::NX + L::NBS;
   r.ready = b + 2 * L::NX + 2 * L::NBS;
-  r.tfree = b + 2 * L::NX + 2 * L::NBS + NB;
-  r.acc_full = b + 2 * L::NX + 2 * L::NBS + 2 * NB;
+  r.tfree = b + 2 * L::NX + 2 * L::NBS + 4;
+  r.acc_full = b + 2 * L::NX + 2 * L::NBS + 2 * 4;
   r.acc_empty = r.acc_full + 2;
   r.tmem_slot = reinterpret_cast<uint32_t*>(b + L::nbar);
   return r;
@@ -83,15 +106,25 @@ __device__ __forceinline__ Bars bars_of(uint8_t* smem) {
 template <class L>
 __device__ __forceinline__ void init_bars(const Bars& b) {
   for (int s = 0; s < L::NX; ++s) { mbar_init(&b.x_full[s], 1); mbar_init(&b.x_free[s], 128); }
-  for (int s = 0; s < L::NBS; ++s) { mbar_init(&b.b_full[s], 1); mbar_init(&b.b_free[s], 1); }
-  for (int s = 0; s < NB; ++s) { mbar_init(&b.ready[s], 128); mbar_init(&b.tfree[s], 1); }
-  for (int k = 0; k < 2; ++k) { mbar_init(&b.acc_full[k], 1); mbar_init(&b.acc_empty[k], 128); }
+  for (int s = 0; s < L::NBS; ++s) { mbar_init(&b.b_full[s], 1); mbar_init(&b.b_free[s], L::NI); }
+  for (int s = 0; s < L::NB; ++s) { mbar_init(&b.ready[s], 128); mbar_init(&b.tfree[s], L::NI); }
+  for (int k = 0; k < 2; ++k) { mbar_init(&b.acc_full[k], L::NI); mbar_init(&b.acc_empty[k], 128); }
   fence_barrier_init();
 }
 
 // K-major SWIZZLE_128B descriptor of a [rows][32 fp32] tile, advanced to k-step kk (8 elements)
 __device__ __forceinline__ uint64_t bdesc_sw128(uint32_t saddr, int kk) {
   return sdesc(saddr + 32u * uint32_t(kk), 16u, 1024u) | (uint64_t(2) << 61);
+}
+// MN-major tf32 descriptor (layout SWIZZLE_128B_BASE32B, tools/mn_probe.cu): atoms of 4 k-rows x
+// 128 B; LBO = 4 KB between 32-wide N atom columns, SBO = 512 B between 4-row k groups; k-step kk
+// (8 rows) starts 1 KB further.
+__device__ __forceinline__ uint64_t bdesc_mn(uint32_t saddr, int kk) {
+  return sdesc(saddr + 1024u * uint32_t(kk), 4096u, 512u) | (uint64_t(1) << 61);
+}
+template <bool BMN>
+__device__ __forceinline__ uint64_t bdesc(uint32_t saddr, int kk) {
+  return BMN ? bdesc_mn(saddr, kk) : bdesc_sw128(saddr, kk);
 }
 
 // Splitter: read this thread's row of the raw X tile, write hi/lo tf32 to its TMEM lane.
@@ -122,12 +155,12 @@ __device__ __forceinline__ void split_row_to_tmem(const float* xs, int r, uint32
 }
 
 // Split the B tile in place (hi) and write lo; elementwise, layout-agnostic, conflict-free.
-template <int NPAD>
+template <uint32_t BYTES>
 __device__ __forceinline__ void split_b(float* b, float* blo, int t) {
   float4* b4 = reinterpret_cast<float4*>(b);
   float4* l4 = reinterpret_cast<float4*>(blo);
 #pragma unroll
-  for (int q = 0; q < NPAD * KC / 4 / 128; ++q) {
+  for (int q = 0; q < int(BYTES / 16 / 128); ++q) {
     const float4 v = b4[t + 128 * q];
     uint32_t h0, h1, h2, h3, l0, l1, l2, l3;
     split_tf32(v.x, h0, l0);
@@ -139,17 +172,19 @@ __device__ __forceinline__ void split_b(float* b, float* blo, int t) {
   }
 }
 
-// One stage: 4 k-steps x (2 or 3) products into accumulator column `acc`.
-template <bool BSPLIT>
-__device__ __forceinline__ void issue_stage(uint32_t tmem, uint32_t acc, int s, uint32_t b_saddr, uint32_t blo_saddr,
-                                            uint32_t idesc, bool first) {
-  const uint32_t a_hi = tmem + kAStage + 64u * s;
+// One stage, issuer q of NI: its share of the 4 k-steps x (2 or 3) products into accumulator `acc`.
+template <bool BSPLIT, int NI, bool BMN = false>
+__device__ __forceinline__ void issue_stage(uint32_t tmem, uint32_t acc, uint32_t a_col, int q, uint32_t b_saddr,
+                                            uint32_t blo_saddr, uint32_t idesc, bool first) {
+  const uint32_t a_hi = tmem + a_col;
+  constexpr int KPI = (KC / 8) / NI;
 #pragma unroll
-  for (int kk = 0; kk < KC / 8; ++kk) {
-    const uint64_t bd = bdesc_sw128(b_saddr, kk);
-    mma_tf32_ts(tmem + acc, a_hi + 8 * kk, bd, idesc, (first && kk == 0) ? 0u : 1u);
+  for (int k = 0; k < KPI; ++k) {
+    const int kk = q * KPI + k;
+    const uint64_t bd = bdesc<BMN>(b_saddr, kk);
+    mma_tf32_ts(tmem + acc, a_hi + 8 * kk, bd, idesc, (first && k == 0) ? 0u : 1u);
     mma_tf32_ts(tmem + acc, a_hi + 32 + 8 * kk, bd, idesc, 1u);
-    if (BSPLIT) mma_tf32_ts(tmem + acc, a_hi + 8 * kk, bdesc_sw128(blo_saddr, kk), idesc, 1u);
+    if (BSPLIT) mma_tf32_ts(tmem + acc, a_hi + 8 * kk, bdesc<BMN>(blo_saddr, kk), idesc, 1u);
   }
 }
 
@@ -164,16 +199,20 @@ struct Ring {
 // tcgen05.ld are issued before a single wait::ld.
 template <int NPAD>
 __device__ __forceinline__ void drain_acc(const Bars& b, uint32_t lane_base, int64_t u, float (&sums)[NPAD]) {
+  using TP = TmemPlan<NPAD>;
   const int ab = int(u & 1);
   mbar_wait(&b.acc_full[ab], uint32_t(u >> 1) & 1);
   tc_fence_after();
-  uint32_t v[NPAD];
 #pragma unroll
-  for (int cb = 0; cb < NPAD / 16; ++cb)
-    tmem_ld16(lane_base + acc_col(ab) + 16 * cb, *reinterpret_cast<uint32_t(*)[16]>(&v[16 * cb]));
-  tmem_wait_ld();
+  for (int q = 0; q < TP::NI; ++q) {
+    uint32_t v[NPAD];
 #pragma unroll
-  for (int k = 0; k < NPAD; ++k) sums[k] += __uint_as_float(v[k]);
+    for (int cb = 0; cb < NPAD / 16; ++cb)
+      tmem_ld16(lane_base + TP::acc(q, ab) + 16 * cb, *reinterpret_cast<uint32_t(*)[16]>(&v[16 * cb]));
+    tmem_wait_ld();
+#pragma unroll
+    for (int k = 0; k < NPAD; ++k) sums[k] += __uint_as_float(v[k]);
+  }
   tc_fence_before();
   mbar_arrive(&b.acc_empty[ab]);
 }
@@ -186,6 +225,7 @@ struct SParams {
   int64_t nchunks;    // total j-chunks
   int seg;            // chunks per accumulator segment
   int ablate;         // profiling only: 1 = no MMA, 2 = no split work (results invalid)
+  int skew;           // chunk-order rotation per M-tile (decorrelates the rows' DRAM addresses)
   float* part;        // [split][K][I]
 };
 
@@ -196,21 +236,28 @@ __device__ __forceinline__ void chunk_coords(const SParams& p, int64_t c, int64_
   else { beta = c / p.cpb; a0 = (c % p.cpb) * KC; j0 = a0 + p.a * beta; }
 }
 
-// grid (mtiles, splits): CTA (m, z) sums the chunks c = z, z + S, z + 2S, ... (S = splits) of M-tile m.
+// grid (mtiles, splits): CTA (m, z) sums the contiguous chunk range z*per .. (z+1)*per-1 of M-tile m.
 // The M-tiles of a split are adjacent in launch order, so the CTAs that share a B chunk (Omega / Z
 // rows) run in the same wave and in near lockstep: B comes from DRAM once and from L2 for the rest
 // (a split-major order re-read Omega once per wave: +16% DRAM traffic on cfg5, ncu).
 template <int NPAD, bool BSPLIT, bool AMN>
 __global__ void __launch_bounds__(NT_TTM, 1)
 ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb, const SParams p) {
-  using L = Smem<NPAD, BSPLIT>;
+  using L = Smem<NPAD, BSPLIT, true>;
+  constexpr int NBX = (NPAD + 31) / 32;                // 32-wide N atom columns of the B tile
   constexpr int NX = L::NX;
   extern __shared__ __align__(1024) uint8_t smem[];
   const Bars b = bars_of<L>(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t z = blockIdx.y, S = gridDim.y;
   const int64_t i0 = int64_t(blockIdx.x) * BM;
-  const int nch = z < p.nchunks ? int((p.nchunks - z + S - 1) / S) : 0;
+  // contiguous chunk range per split: consecutive TMA boxes of a CTA continue the same rows, which
+  // keeps DRAM pages (and 256 B L2 promotions) useful on the strided last-mode rows
+  const int64_t per = (p.nchunks + S - 1) / S;
+  const int64_t cbeg = z * per;
+  const int nch = cbeg < p.nchunks ? int(min(per, p.nchunks - cbeg)) : 0;
+  const int rot = nch ? int((int64_t(blockIdx.x) * p.skew) % nch) : 0;
+  auto chunk_of = [&](int it) { int c = it + rot; return cbeg + (c >= nch ? c - nch : c); };
 
   if (threadIdx.x == 0) {
     init_bars<L>(b);
@@ -226,33 +273,39 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
   if (warp == 0) {
     if (lane == 0) {                                   // ---------------- X producer
       Ring rx;
+      const uint64_t pol = policy_evict_first();
       for (int it = 0; it < nch; ++it, rx.next<NX>()) {
         if (it >= NX) mbar_wait(&b.x_free[rx.s], rx.ph ^ 1);
         int64_t a0, beta, j0;
-        chunk_coords<AMN>(p, z + it * S, a0, beta, j0);
+        chunk_coords<AMN>(p, chunk_of(it), a0, beta, j0);
         mbar_expect_tx(&b.x_full[rx.s], L::kX);
         void* xs = smem + L::off_x + rx.s * L::kX;
-        if (AMN) tma_load_2d(xs, &tmx, &b.x_full[rx.s], int(i0), int(j0));
-        else tma_load_3d(xs, &tmx, &b.x_full[rx.s], int(a0), int(i0), int(beta));
+        if (AMN) tma_load_2d_hint(xs, &tmx, &b.x_full[rx.s], int(i0), int(j0), pol);
+        else tma_load_3d_hint(xs, &tmx, &b.x_full[rx.s], int(a0), int(i0), int(beta), pol);
       }
     }
   } else if (warp == 6) {
     if (lane == 0) {                                   // ---------------- B producer
       Ring rb;
+      const uint64_t pol = policy_evict_last();
       for (int it = 0; it < nch; ++it, rb.next<L::NBS>()) {
         if (it >= L::NBS) mbar_wait(&b.b_free[rb.s], rb.ph ^ 1);
         int64_t a0, beta, j0;
-        chunk_coords<AMN>(p, z + it * S, a0, beta, j0);
+        chunk_coords<AMN>(p, chunk_of(it), a0, beta, j0);
         mbar_expect_tx(&b.b_full[rb.s], L::kB);
-        tma_load_2d(smem + L::off_b + rb.s * L::kB, &tmb, &b.b_full[rb.s], int(j0), 0);
+#pragma unroll
+        for (int x = 0; x < NBX; ++x)
+          tma_load_2d_hint(smem + L::off_b + rb.s * L::kB + x * 4096, &tmb, &b.b_full[rb.s], 32 * x, int(j0), pol);
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {                                   // ---------------- MMA issuer
-      const uint32_t idesc = idesc_tf32(BM, NPAD, 0);
+  } else if (warp == 1 || warp == 7) {
+    const int q = warp == 1 ? 0 : 1;
+    if (lane == 0 && q < L::NI) {                      // ---------------- MMA issuers
+      using TP = TmemPlan<NPAD>;
+      const uint32_t idesc = idesc_tf32(BM, NPAD, 1);
       Ring rt, rb;
       int u = 0, pos = 0;
-      for (int it = 0; it < nch; ++it, rt.next<NB>(), rb.next<L::NBS>()) {
+      for (int it = 0; it < nch; ++it, rt.next<L::NB>(), rb.next<L::NBS>()) {
         const bool first = pos == 0;
         const bool last = (pos == p.seg - 1) || (it == nch - 1);
         const int ab = u & 1;
@@ -261,8 +314,9 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
         if (!BSPLIT) mbar_wait(&b.b_full[rb.s], rb.ph);
         tc_fence_after();
         if (p.ablate != 1)
-          issue_stage<BSPLIT>(tmem, acc_col(ab), rt.s, smem_u32(smem + L::off_b + rb.s * L::kB),
-                              smem_u32(smem + L::off_blo + rt.s * L::kB), idesc, first);
+          issue_stage<BSPLIT, L::NI, true>(tmem, TP::acc(q, ab), TP::a_slot(rt.s), q,
+                                           smem_u32(smem + L::off_b + rb.s * L::kB),
+                                           smem_u32(smem + L::off_blo + rt.s * L::kB), idesc, first);
         mma_commit(&b.tfree[rt.s]);
         mma_commit(&b.b_free[rb.s]);
         if (last) { mma_commit(&b.acc_full[ab]); ++u; pos = 0; } else { ++pos; }
@@ -278,17 +332,17 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
     for (int k = 0; k < NPAD; ++k) sums[k] = 0.f;
     Ring rx, rt, rb;
     int u = 0, pos = 0;
-    for (int it = 0; it < nch; ++it, rx.next<NX>(), rt.next<NB>(), rb.next<L::NBS>()) {
+    for (int it = 0; it < nch; ++it, rx.next<NX>(), rt.next<L::NB>(), rb.next<L::NBS>()) {
       mbar_wait(&b.x_full[rx.s], rx.ph);
-      if (it >= NB) mbar_wait(&b.tfree[rt.s], rt.ph ^ 1);   // TMEM slot (and B lo) free
+      if (it >= L::NB) mbar_wait(&b.tfree[rt.s], rt.ph ^ 1);   // TMEM slot (and B lo) free
       if (p.ablate != 2)
         split_row_to_tmem<AMN>(reinterpret_cast<const float*>(smem + L::off_x + rx.s * L::kX), r,
-                               lane_base + kAStage + 64u * rt.s);
+                               lane_base + TmemPlan<NPAD>::a_slot(rt.s));
       mbar_arrive(&b.x_free[rx.s]);
       if (BSPLIT) {
         mbar_wait(&b.b_full[rb.s], rb.ph);
-        split_b<NPAD>(reinterpret_cast<float*>(smem + L::off_b + rb.s * L::kB),
-                      reinterpret_cast<float*>(smem + L::off_blo + rt.s * L::kB), t);
+        split_b<L::kB>(reinterpret_cast<float*>(smem + L::off_b + rb.s * L::kB),
+                       reinterpret_cast<float*>(smem + L::off_blo + rt.s * L::kB), t);
       }
       tmem_wait_st();
       if (BSPLIT) fence_proxy_async();
@@ -328,6 +382,7 @@ struct TParams {
   int seg;            // i-chunks per accumulator segment
   float* out;
   int64_t so_a, so_c, so_b;
+  bool vec4;          // so_c == 1 and every output row 16-byte aligned with C % 4 == 0
 };
 
 template <int NPAD, bool AKM>   // AKM: mode 0 (a == 1), X tile K-major [BM j][KC i]
@@ -360,6 +415,7 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
   if (warp == 0) {
     if (lane == 0) {                                   // ---------------- X producer
       Ring rx;
+      const uint64_t pol = policy_evict_first();
       int it = 0;
       for (int64_t u = 0; u < my_tiles; ++u) {
         int64_t a0, beta;
@@ -368,38 +424,42 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
           if (it >= NX) mbar_wait(&b.x_free[rx.s], rx.ph ^ 1);
           mbar_expect_tx(&b.x_full[rx.s], L::kX);
           void* xs = smem + L::off_x + rx.s * L::kX;
-          if (AKM) tma_load_2d(xs, &tmx, &b.x_full[rx.s], c * KC, int(beta));
-          else tma_load_3d(xs, &tmx, &b.x_full[rx.s], int(a0), c * KC, int(beta));
+          if (AKM) tma_load_2d_hint(xs, &tmx, &b.x_full[rx.s], c * KC, int(beta), pol);
+          else tma_load_3d_hint(xs, &tmx, &b.x_full[rx.s], int(a0), c * KC, int(beta), pol);
         }
       }
     }
   } else if (warp == 6) {
     if (lane == 0) {                                   // ---------------- B producer
       Ring rb;
+      const uint64_t pol = policy_evict_last();
       int it = 0;
       for (int64_t u = 0; u < my_tiles; ++u)
         for (int c = 0; c < p.nic; ++c, ++it, rb.next<L::NBS>()) {
           if (it >= L::NBS) mbar_wait(&b.b_free[rb.s], rb.ph ^ 1);
           mbar_expect_tx(&b.b_full[rb.s], L::kB);
-          tma_load_2d(smem + L::off_b + rb.s * L::kB, &tmb, &b.b_full[rb.s], c * KC, 0);
+          tma_load_2d_hint(smem + L::off_b + rb.s * L::kB, &tmb, &b.b_full[rb.s], c * KC, 0, pol);
         }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {                                   // ---------------- MMA issuer
+  } else if (warp == 1 || warp == 7) {
+    const int q = warp == 1 ? 0 : 1;
+    if (lane == 0 && q < L::NI) {                      // ---------------- MMA issuers
+      using TP = TmemPlan<NPAD>;
       const uint32_t idesc = idesc_tf32(BM, NPAD, 0);
       Ring rt, rb;
       int64_t g = 0;                                   // global segment counter
       for (int64_t u = 0; u < my_tiles; ++u) {
         int pos = 0;
-        for (int c = 0; c < p.nic; ++c, rt.next<NB>(), rb.next<L::NBS>()) {
+        for (int c = 0; c < p.nic; ++c, rt.next<L::NB>(), rb.next<L::NBS>()) {
           const bool first = pos == 0;
           const bool last = (pos == p.seg - 1) || (c == p.nic - 1);
           const int ab = int(g & 1);
           if (first && g >= 2) mbar_wait(&b.acc_empty[ab], uint32_t((g >> 1) - 1) & 1);
           mbar_wait(&b.ready[rt.s], rt.ph);
           tc_fence_after();
-          issue_stage<BSPLIT>(tmem, acc_col(ab), rt.s, smem_u32(smem + L::off_b + rb.s * L::kB),
-                              smem_u32(smem + L::off_blo + rt.s * L::kB), idesc, first);
+          issue_stage<BSPLIT, L::NI>(tmem, TP::acc(q, ab), TP::a_slot(rt.s), q,
+                                     smem_u32(smem + L::off_b + rb.s * L::kB),
+                                     smem_u32(smem + L::off_blo + rt.s * L::kB), idesc, first);
           mma_commit(&b.tfree[rt.s]);
           mma_commit(&b.b_free[rb.s]);
           if (last) { mma_commit(&b.acc_full[ab]); ++g; pos = 0; } else { ++pos; }
@@ -425,9 +485,16 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
         if (AKM) { const int64_t j = beta + r; valid = j < p.b; ob = j * p.so_b; }
         else { const int64_t al = a0 + r; valid = al < p.a; ob = al * p.so_a + beta * p.so_b; }
         if (valid) {
+          if (p.vec4) {                                        // row-major output rows: 16 B stores
+            float4* o4 = reinterpret_cast<float4*>(p.out + ob);
 #pragma unroll
-          for (int k = 0; k < NPAD; ++k)
-            if (k < p.C) p.out[ob + int64_t(k) * p.so_c] = sums[k];
+            for (int k = 0; k < NPAD / 4; ++k)
+              if (4 * k < p.C) o4[k] = make_float4(sums[4 * k], sums[4 * k + 1], sums[4 * k + 2], sums[4 * k + 3]);
+          } else {
+#pragma unroll
+            for (int k = 0; k < NPAD; ++k)
+              if (k < p.C) p.out[ob + int64_t(k) * p.so_c] = sums[k];
+          }
         }
 #pragma unroll
         for (int k = 0; k < NPAD; ++k) sums[k] = 0.f;
@@ -441,15 +508,15 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
     for (int64_t u = 0; u < my_tiles; ++u) {
       const int64_t tile = blockIdx.x + u * gridDim.x;
       int pos = 0;
-      for (int c = 0; c < p.nic; ++c, ++it, rx.next<NX>(), rt.next<NB>(), rb.next<L::NBS>()) {
+      for (int c = 0; c < p.nic; ++c, ++it, rx.next<NX>(), rt.next<L::NB>(), rb.next<L::NBS>()) {
         mbar_wait(&b.x_full[rx.s], rx.ph);
-        if (it >= NB) mbar_wait(&b.tfree[rt.s], rt.ph ^ 1);
+        if (it >= L::NB) mbar_wait(&b.tfree[rt.s], rt.ph ^ 1);
         split_row_to_tmem<!AKM>(reinterpret_cast<const float*>(smem + L::off_x + rx.s * L::kX), r,
-                                lane_base + kAStage + 64u * rt.s);
+                                lane_base + TmemPlan<NPAD>::a_slot(rt.s));
         mbar_arrive(&b.x_free[rx.s]);
         mbar_wait(&b.b_full[rb.s], rb.ph);
-        split_b<NPAD>(reinterpret_cast<float*>(smem + L::off_b + rb.s * L::kB),
-                      reinterpret_cast<float*>(smem + L::off_blo + rt.s * L::kB), t);
+        split_b<L::kB>(reinterpret_cast<float*>(smem + L::off_b + rb.s * L::kB),
+                       reinterpret_cast<float*>(smem + L::off_blo + rt.s * L::kB), t);
         tmem_wait_st();
         fence_proxy_async();
         tc_fence_before();
@@ -495,7 +562,7 @@ EncodeFn encode_fn() {
 }
 
 bool make_map(CUtensorMap* m, const void* ptr, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
-              const uint32_t* box, bool swz128) {
+              const uint32_t* box, bool swz128, CUtensorMapSwizzle swz_override = CU_TENSOR_MAP_SWIZZLE_NONE) {
   EncodeFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t d[5], s[4];
@@ -504,7 +571,9 @@ bool make_map(CUtensorMap* m, const void* ptr, int rank, const uint64_t* dims, c
   for (int i = 0; i < rank - 1; ++i) s[i] = strides_bytes[i];
   std::memset(m, 0, sizeof(*m));
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, cuuint32_t(rank), const_cast<void*>(ptr), d, s, b, e,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  swz_override != CU_TENSOR_MAP_SWIZZLE_NONE ? swz_override
+                                                             : (swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE),
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -519,6 +588,15 @@ bool make_b_map(CUtensorMap* m, const float* B, int64_t rows, int cols, int64_t 
   return make_map(m, B, 2, d, s, bx, true);
 }
 
+// row-major fp32 matrix (rows x cols, row pitch ld) as an MN-major B operand: (32 cols, 32 rows)
+// boxes with the 32 B-atom 128 B swizzle (columns >= cols read as zero)
+bool make_b_map_rm(CUtensorMap* m, const float* B, int64_t rows, int cols, int64_t ld) {
+  if (!aligned(B, 16) || (ld % 4) || ld < cols || rows > INT32_MAX) return false;
+  const uint64_t d[2] = {uint64_t(cols), uint64_t(rows)}, s[1] = {uint64_t(ld) * 4};
+  const uint32_t bx[2] = {32, KC};
+  return make_map(m, B, 2, d, s, bx, false, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+}
+
 template <typename Kern>
 void set_smem(Kern kernel, uint32_t bytes) {
   RT_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
@@ -526,10 +604,10 @@ void set_smem(Kern kernel, uint32_t bytes) {
 
 template <int NPAD, bool BSPLIT, bool AMN>
 void launch_s(const Ctx& ctx, const CUtensorMap& tx, const CUtensorMap& tb, const SParams& p, dim3 grid) {
-  using L = Smem<NPAD, BSPLIT>;
+  using L = Smem<NPAD, BSPLIT, true>;
   static bool attr = false;
   if (!attr) { set_smem(ttm_s_tc_kernel<NPAD, BSPLIT, AMN>, L::bytes); attr = true; }
-  launch(ctx, "ttm_s_tc", [&] {
+  launch(ctx, ctx.label ? ctx.label : "ttm_s_tc", [&] {
     ttm_s_tc_kernel<NPAD, BSPLIT, AMN><<<grid, NT_TTM, L::bytes, ctx.stream>>>(tx, tb, p);
   });
 }
@@ -545,7 +623,7 @@ void launch_t(const Ctx& ctx, const CUtensorMap& tx, const CUtensorMap& tb, cons
   using L = Smem<NPAD, true>;
   static bool attr = false;
   if (!attr) { set_smem(ttm_t_tc_kernel<NPAD, AKM>, L::bytes); attr = true; }
-  launch(ctx, "ttm_t_tc", [&] {
+  launch(ctx, ctx.label ? ctx.label : "ttm_t_tc", [&] {
     ttm_t_tc_kernel<NPAD, AKM><<<grid, NT_TTM, L::bytes, ctx.stream>>>(tx, tb, p);
   });
 }
@@ -587,7 +665,7 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
     const uint32_t bx[3] = {KC, BM, 1};
     if (!make_map(&tx, X, 3, d, s, bx, true)) return false;
   }
-  if (!make_b_map(&tb, Bm, J, K, ldb, npad)) return false;
+  if (!make_b_map_rm(&tb, Bm, J, K, ldb)) return false;
   SParams p;
   p.a = box.a; p.I = box.I; p.b = box.b; p.K = K;
   p.cpb = amn ? 1 : cdiv(box.a, KC);
@@ -598,6 +676,7 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
   splits = std::min<int64_t>(splits, 65535);
   p.seg = std::max(1, ctx.tc_seg);
   p.ablate = ctx.tc_ablate;
+  p.skew = ctx.tc_skew >= 0 ? ctx.tc_skew : 0;
   p.part = ws.alloc_n<float>(splits * K * box.I);
   const dim3 grid{unsigned(mtiles), unsigned(splits), 1u};
   const bool bsplit = !b_tf32_exact;
@@ -645,6 +724,7 @@ bool ttm_t_tc(const Ctx& ctx, const float* X, Box box, const float* Q, int64_t l
   p.nic = int(cdiv(box.I, KC));
   p.seg = std::max(1, ctx.tc_seg);
   p.out = out; p.so_a = so_a; p.so_c = so_c; p.so_b = so_b;
+  p.vec4 = so_c == 1 && (so_a % 4) == 0 && (so_b % 4) == 0 && (C % 4) == 0 && aligned(out, 16);
   const int64_t grid = std::min<int64_t>(p.ntiles, ctx.num_sms);
 #define RT_T_CASE(NP)                                                     \
   case NP:                                                                \

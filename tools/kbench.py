@@ -23,6 +23,7 @@ ap.add_argument("--impl", type=int, default=0)
 ap.add_argument("--seg", type=int, default=0)
 ap.add_argument("--tf32", type=int, default=0)
 ap.add_argument("--ablate", type=int, default=0)
+ap.add_argument("--skew", type=int, default=-1)
 a = ap.parse_args()
 
 dims = a.dims
@@ -36,6 +37,8 @@ if a.seg:
     h.set_option(L.RT_OPT_TC_SEGMENT, a.seg)
 if a.ablate:
     h.set_option(100, a.ablate)
+if a.skew >= 0:
+    h.set_option(L.RT_OPT_TC_SKEW, a.skew)
 modes = range(N) if a.modes is None else a.modes
 for n in modes:
     J = X.numel() // dims[n]
