@@ -103,9 +103,9 @@ rt_status rt_sync(rt_handle* h);
  * is exactly representable in tf32 (e.g. rounded on the host before it is given to both the
  * oracle and this library); the sketch then skips the A_hi*Omega_lo product of the 3xTF32
  * split.  RT_OPT_TC_SEGMENT: contraction chunks (of 32) accumulated in TMEM before the fp32
- * accumulator is drained to registers (default 4, i.e. 128 elements; the tensor core's fp32
- * accumulation error grows with this length, tests/test_gpu_tc.py).  RT_OPT_QR_FALLBACK is
- * reserved. */
+ * accumulator is drained to registers (default 8, i.e. 256 elements; the tensor core's fp32
+ * accumulation error grows with this length, tests/test_gpu_tc.py).  RT_OPT_TC_SKEW: tuning of
+ * the split-K chunk order (rotation per row tile; default 0).  RT_OPT_QR_FALLBACK is reserved. */
 typedef enum { RT_OPT_TTM_IMPL = 0, RT_OPT_PROFILE = 1, RT_OPT_QR_FALLBACK = 2, RT_OPT_OMEGA_TF32 = 3,
                RT_OPT_TC_SEGMENT = 4, RT_OPT_TC_SKEW = 5,
                RT_OPT_TC_ABLATE = 100 /* profiling only: invalid results */ } rt_option;

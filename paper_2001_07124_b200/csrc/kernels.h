@@ -29,11 +29,19 @@ void ttm_t(const Ctx& ctx, const Tin* X, Box box, const Tm* Mm, int64_t ms_i, in
 // launched) when the shape/alignment is outside the TMA path; callers then use the SIMT kernels.
 // ttm_s_tc: B row-major (element (j,k) at j*ldb + k, ldb % 4 == 0, 16-byte aligned), consumed as an
 // MN-major operand.  b_tf32_exact drops the A_hi*B_lo product.
+// b_presplit: B holds rows [B_hi (tc_split_width(K) columns, zero padded) | B_lo (same)] written by
+// ttm_t_tc(split_out) -- no split work in the kernel.
 bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Bm, int64_t ldb, bool b_tf32_exact,
-              int K, double* Y, int64_t ldy);
-// out(alpha,c,beta) = sum_i X(alpha,i,beta) Q(i,c), Q col-major with ldq % 4 == 0
-bool ttm_t_tc(const Ctx& ctx, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
-              int64_t so_a, int64_t so_c, int64_t so_b);
+              int K, double* Y, int64_t ldy, bool b_presplit = false);
+// whether ttm_s_tc would run (same shape/alignment rules, no launch)
+bool ttm_s_tc_ok(const Ctx& ctx, const float* X, Box box, int K);
+int tc_npad(int K);
+int tc_split_width(int K);
+// out(alpha,c,beta) = sum_i X(alpha,i,beta) Q(i,c), Q col-major (any ld; split into a [hi | lo]
+// workspace copy).  split_out: each output row (so_c == 1) is written as [hi | lo] halves of
+// tc_split_width(C) columns each (the pre-split B operand of ttm_s_tc).
+bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
+              int64_t so_a, int64_t so_c, int64_t so_b, bool split_out = false);
 
 // Gram A^T A of an m x k matrix (fp64 out, k x k), partials reduced in fixed order.  A col-major
 // (element (r,c) at r + lda*c) or, with rowmajor, at r*lda + c.

@@ -40,12 +40,12 @@ void ttm_s_dispatch(const Ctx& ctx, Arena& ws, const double* X, Box box, const d
   ttm_s<double>(ctx, ws, X, box, B, ldb, 1, K, Y, ldy);
 }
 // out(alpha,c,beta) = sum_i X(alpha,i,beta) Q(i,c), Q col-major (ldq)
-void ttm_t_dispatch(const Ctx& ctx, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
+void ttm_t_dispatch(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
                     int64_t so_a, int64_t so_c, int64_t so_b) {
-  if (ctx.ttm_impl != 1 && ttm_t_tc(ctx, X, box, Q, ldq, C, out, so_a, so_c, so_b)) return;
+  if (ctx.ttm_impl != 1 && ttm_t_tc(ctx, ws, X, box, Q, ldq, C, out, so_a, so_c, so_b)) return;
   ttm_t<float, float, float>(ctx, X, box, Q, 1, ldq, C, out, so_a, so_c, so_b);
 }
-void ttm_t_dispatch(const Ctx& ctx, const double* X, Box box, const double* Q, int64_t ldq, int C, double* out,
+void ttm_t_dispatch(const Ctx& ctx, Arena&, const double* X, Box box, const double* Q, int64_t ldq, int C, double* out,
                     int64_t so_a, int64_t so_c, int64_t so_b) {
   ttm_t<double, double, double>(ctx, X, box, Q, 1, ldq, C, out, so_a, so_c, so_b);
 }
@@ -111,7 +111,8 @@ void Engine::qr_y(const double* Y, int64_t m, int64_t m_glob, int k, int64_t ldy
 // CholeskyQR step with a small safety shift keeps it well conditioned.  Z is row-major
 // (m x k, row pitch ldz).
 template <typename T>
-void Engine::qr_z(T* Z, int64_t m, int64_t ldz, int64_t m_glob, int k, bool rows_dist, int64_t row0) {
+bool Engine::qr_z(T* Z, int64_t m, int64_t ldz, int64_t m_glob, int k, bool rows_dist, int64_t row0, T* Z2,
+                  int64_t ldz2) {
   const auto mk = ws.mark();
   double* G = ws.alloc_n<double>(int64_t(k) * k);
   double* Rr = ws.alloc_n<double>(int64_t(k) * k);
@@ -142,11 +143,14 @@ void Engine::qr_z(T* Z, int64_t m, int64_t ldz, int64_t m_glob, int k, bool rows
       int64_t ldr;
       const float* RiT = working_copy<float>(ctx, ws, Ri, k, k, k, ldr);
       LabelScope ls(ctx, "zapply_tc");
-      done_apply = ttm_t_tc(ctx, Z, zb, RiT, ldr, k, Z, 0, 1, ldz);
+      // Z2 requested: Z R^{-1} written as the pre-split [hi | lo] operand of the next product
+      if (Z2) done_apply = ttm_t_tc(ctx, ws, Z, zb, RiT, ldr, k, Z2, 0, 1, ldz2, /*split_out=*/true);
+      else done_apply = ttm_t_tc(ctx, ws, Z, zb, RiT, ldr, k, Z, 0, 1, ldz);
     }
   }
   if (!done_apply) gemm_tall<T, T>(ctx, Z, m, k, ldz, Ri, k, k, Z, ldz, zero, row0, /*rowmajor=*/true);
   ws.rewind(mk);
+  return done_apply && Z2 != nullptr;
 }
 
 // ---------------------------------------------------------------- sketch (a1-a3)
@@ -160,7 +164,19 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
   int K;
   if (kind == 0) {
     K = int(omega_cols[n]);
-    ttm_s_dispatch(ctx, ws, data, bx, static_cast<const T*>(omega[n]), omega_ld[n], ctx.omega_tf32 != 0, K, Yt, In);
+    const T* om = static_cast<const T*>(omega[n]);
+    int64_t ld = omega_ld[n];
+    const auto mo = ws.mark();
+    if (std::is_same<T, float>::value && ctx.ttm_impl != 1 && (ld % 4) != 0) {
+      // the TMA path needs a 16-byte row pitch: repack Omega (J x K, small next to X) with ld = pad4(K)
+      const int64_t ldp = pad4(K);
+      T* c = ws.alloc_n<T>(bx.J() * ldp);
+      convert2d<T, T>(ctx, om, K, bx.J(), ld, c, ldp);
+      om = c;
+      ld = ldp;
+    }
+    ttm_s_dispatch(ctx, ws, data, bx, om, ld, ctx.omega_tf32 != 0, K, Yt, In);
+    ws.rewind(mo);
   } else {
     // Kronecker sketch W = X x_{k!=n} Omega_k^T (Eq.(2)): a chain of TTMs whose first
     // stage streams X and whose later stages run on the shrunken result.  The factors are narrow
@@ -197,6 +213,16 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
   const int64_t ldz = pad4(K);             // Z row-major (Jl x K), 16-byte row pitch; pad columns zero
   T* Z = ws.alloc_n<T>(Jl * ldz);
   if (ldz != K) fill_zero(ctx, Z, sizeof(T) * Jl * ldz);
+  // fp32 on the tensor cores: the orthonormalized Z is written once in the pre-split [hi | lo] form
+  // (row pitch 2 * tc_split_width(K)) so the product Y = X_(n) Z does no split work per tile
+  T* Z2 = nullptr;
+  int64_t ldz2 = 0;
+  if constexpr (std::is_same<T, float>::value) {
+    if (ttm_s_tc_ok(ctx, data, bx, K) && ldz == K) {
+      ldz2 = 2 * int64_t(tc_split_width(K));
+      Z2 = ws.alloc_n<T>(Jl * ldz2);
+    }
+  }
   const int64_t row0_last = X.off;
   for (int it = 0; it < q; ++it) {
     qr_y(Yt, In, X.Ig(n), K, In, Qy, In, nullptr, last && dist(), last ? row0_last : 0);
@@ -207,7 +233,7 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
     // so_a = ldz, so_c = 1, so_b = a ldz
     {
       LabelScope ls(ctx, "ttm_t_tc_pow");
-      ttm_t_dispatch(ctx, data, bx, QyT, ldqt, K, Z, ldz, 1, bx.a * ldz);
+      ttm_t_dispatch(ctx, ws, data, bx, QyT, ldqt, K, Z, ldz, 1, bx.a * ldz);
     }
     ws.rewind(mq);
     allreduce(comm, last && dist(), Z, Jl * ldz, ctx.stream);                    // C3
@@ -218,10 +244,15 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
       for (int k = n + 1; k < N - 1; ++k) bp *= X.d[k];
       zrow0 = bx.a * bp * X.off;
     }
-    qr_z<T>(Z, Jl, ldz, X.Jg(n), K, !last && dist(), zrow0);
+    const bool pre = qr_z<T>(Z, Jl, ldz, X.Jg(n), K, !last && dist(), zrow0, Z2, ldz2);
     {
       LabelScope ls(ctx, "ttm_s_tc_pow");
-      ttm_s_dispatch(ctx, ws, data, bx, Z, ldz, false, K, Yt, In);
+      bool done = false;
+      if constexpr (std::is_same<T, float>::value) {
+        if (pre) done = ttm_s_tc(ctx, ws, data, bx, Z2, ldz2, false, K, Yt, In, /*b_presplit=*/true);
+      }
+      RT_REQUIRE(!pre || done, kEUNSUPPORTED, "pre-split power product not launched");
+      if (!done) ttm_s_dispatch(ctx, ws, data, bx, Z, ldz, false, K, Yt, In);
     }
     allreduce(comm, !last && dist(), Yt, In * K, ctx.stream);                     // C1
   }
@@ -247,7 +278,7 @@ void Engine::core(const TView& X, const T* data, const double* const* Qt, const 
       ttm_t<T, T, double>(ctx, src, b, QT[n], 1, ld, int(K[n]), Gt, 1, b.a, b.a * K[n]);
     } else {
       T* dst = ws.alloc_n<T>(b.a * K[n] * b.b);
-      ttm_t_dispatch(ctx, src, b, QT[n], ld, int(K[n]), dst, 1, b.a, b.a * K[n]);
+      ttm_t_dispatch(ctx, ws, src, b, QT[n], ld, int(K[n]), dst, 1, b.a, b.a * K[n]);
       src = dst;
     }
     cur[n] = K[n];
@@ -474,8 +505,8 @@ template void Engine::sketch<float>(const TView&, const float*, int, int, const 
                                     const int64_t*, int, double*);
 template void Engine::sketch<double>(const TView&, const double*, int, int, const void* const*, const int64_t*,
                                      const int64_t*, int, double*);
-template void Engine::qr_z<float>(float*, int64_t, int64_t, int64_t, int, bool, int64_t);
-template void Engine::qr_z<double>(double*, int64_t, int64_t, int64_t, int, bool, int64_t);
+template bool Engine::qr_z<float>(float*, int64_t, int64_t, int64_t, int, bool, int64_t, float*, int64_t);
+template bool Engine::qr_z<double>(double*, int64_t, int64_t, int64_t, int, bool, int64_t, double*, int64_t);
 template void Engine::qr_rows<float>(const float*, int64_t, int64_t, int, int64_t, double*, int64_t, double*,
                                      bool, int64_t);
 template void Engine::qr_rows<double>(const double*, int64_t, int64_t, int, int64_t, double*, int64_t, double*,

@@ -17,7 +17,9 @@
 // accumulators drained every `seg` stages into fp32 registers: the tensor core's fp32 accumulation
 // error grows with the accumulation length (7.5e-6 relative after 1024 terms, 2.6e-5 after 3.5K;
 // 1.4e-6 when drained every 128, tests/test_gpu_tc.py).
+#include <cstdio>
 #include <cstring>
+#include <vector>
 
 #include "kernels.h"
 #include "tc_common.cuh"
@@ -29,54 +31,54 @@ using namespace tc;
 constexpr int KC = 32;           // contraction elements per stage
 constexpr int BM = 128;          // tile rows = TMEM lanes
 constexpr int NTHREADS = 192;    // residual kernel
-constexpr int NT_TTM = 256;      // TTM kernels: producer, MMA issuer, 4 splitters, B producer, 2nd issuer
+constexpr int NT_TTM = 384;      // TTM kernels: X producer, MMA issuer, 4 splitters, B producer, 2nd issuer,
+                                 // 4 epilogue warps (warp w accesses TMEM lanes 32 (w % 4) ..)
 
 // MMA issue model (tools/mma_rate.cu): one thread's tcgen05.mma instructions complete one after
-// another (~110-160 cycles each, independent of N), while MMAs issued by different warps overlap.
-// The k-steps of every stage are therefore split between NI issuer warps, each accumulating into
-// its own (double-buffered) TMEM accumulator; the epilogue adds the NI partial accumulators.
-// TMEM (512 columns): accumulator (q, buffer) at column (2q + buffer) * NPAD, then NB A slots of 64
-// columns (hi | lo).
-template <int NPAD> struct TmemPlan {
-  static constexpr int NI = NPAD <= 96 ? 2 : 1;
-  static constexpr uint32_t acc_cols = uint32_t(2 * NI * NPAD);
+// another (~110-160 cycles each whatever N <= 256), while MMAs issued by different warps overlap.
+// So the work of a stage is spread over two issuer warps and made of as few, as wide instructions
+// as possible:
+//   !BSPLIT (B tf32-exact, e.g. a host-rounded Omega): D += A_hi B + A_lo B; the 4 k-steps are split
+//     between NI issuers, each with its own double-buffered accumulator of NPAD columns;
+//   BSPLIT: B = B_hi + B_lo is split in shared memory into one slot [B_hi | B_lo] that is a single
+//     operand of N = NH + NPAD columns, so issuer 0 runs D0 += A_hi [B_hi | B_lo] and issuer 1 runs
+//     D1 += A_lo B_hi (2 instructions per k-step instead of 3; single-buffered accumulators).
+//     D0's hi block only accumulates A_hi B_hi, the correction terms land in their own columns,
+//     so the fp32 accumulation error per segment is a third of the 3-products-in-one form.
+// TMEM (512 columns): accumulators first, then NB A slots of 64 columns (hi | lo).
+// Shared memory rings:
+//   X ring (NX stages of raw 16 KB X tiles): TMA -> splitter, released right after the split;
+//   B ring (NBS slots): TMA -> (splitter: B_lo) -> MMA, released by tcgen05.commit.
+// B tile: K-major [NPAD][32] (128 B rows, SWIZZLE_128B), or MN-major (row-major B in global
+// memory: Omega / Z) as ceil(NPAD/32) atom columns of [32 k-rows][32 n] (4 KB each,
+// SWIZZLE_128B_ATOM_32B); NH = N width of the hi part (MN-major: padded to 32).
+template <int NPAD, bool BSPLIT, bool BMN>
+struct Plan {
+  static constexpr int NBX = (NPAD + 31) / 32;
+  static constexpr int NH = BMN ? NBX * 32 : NPAD;
+  static constexpr uint32_t kB = BMN ? uint32_t(NBX) * 4096u : uint32_t(NPAD) * KC * 4u;
+  static constexpr uint32_t kBS = BSPLIT ? 2u * kB : kB;
+  static constexpr int NI = BSPLIT ? 2 : (NPAD <= 96 ? 2 : 1);
+  static constexpr int NBUF = BSPLIT ? 1 : 2;
+  static constexpr uint32_t acc_cols = BSPLIT ? uint32_t(NH + 2 * NPAD) : uint32_t(2 * NI * NPAD);
   static constexpr uint32_t a_base = (acc_cols + 63u) & ~63u;
   static constexpr int NB_fit = int((512u - a_base) / 64u);
-  static constexpr int NB = NB_fit > 4 ? 4 : NB_fit;   // TMEM-A (and B lo) ring depth
+  static constexpr int NB = NB_fit > 4 ? 4 : NB_fit;
   static_assert(NB >= 2, "TMEM plan leaves fewer than two A slots");
-  __host__ __device__ static constexpr uint32_t acc(int q, int b) { return uint32_t((2 * q + b) * NPAD); }
+  static_assert(!BSPLIT || NH + NPAD <= 256, "concatenated B operand wider than 256");
+  __host__ __device__ static constexpr uint32_t acc(int q, int b) {
+    return BSPLIT ? (q == 0 ? 0u : uint32_t(NH + NPAD)) : uint32_t((2 * q + b) * NPAD);
+  }
   __host__ __device__ static constexpr uint32_t a_slot(int s) { return a_base + 64u * uint32_t(s); }
-};
-
-// Shared memory plan of the TTM kernels.  Three rings:
-//   X ring (NX stages of raw 16 KB X tiles): TMA -> splitter; a stage is released as soon as the
-//     splitters have copied it into TMEM, so the producer can run NX stages ahead;
-//   B ring (NBS stages of [NPAD][32] 128B-swizzled B tiles): TMA -> MMA (B hi is split in place),
-//     released by tcgen05.commit; deeper than the TMEM ring so B (L2 or DRAM) latency is hidden;
-//   TMEM A slots (NB = 4, 64 columns each: hi | lo) + B lo tiles (when split): splitter -> MMA.
-// B tile bytes: K-major [NPAD][32] (128 B rows), or MN-major (row-major B in global memory, e.g.
-// Omega / Z): ceil(NPAD/32) atom columns of [32 k-rows][32 n] (4 KB each, SWIZZLE_128B_ATOM_32B).
-template <int NPAD, bool BMN>
-__host__ __device__ constexpr uint32_t b_tile_bytes() {
-  return BMN ? uint32_t((NPAD + 31) / 32) * 4096u : uint32_t(NPAD) * KC * 4;
-}
-
-template <int NPAD, bool BSPLIT, bool BMN = false>
-struct Smem {
-  using TP = TmemPlan<NPAD>;
-  static constexpr int NB = TP::NB;
-  static constexpr int NI = TP::NI;
+  // shared memory
   static constexpr uint32_t kX = uint32_t(BM) * KC * 4;
-  static constexpr uint32_t kB = b_tile_bytes<NPAD, BMN>();
-  static constexpr uint32_t budget = 212u * 1024u;
-  static constexpr uint32_t lo_bytes = BSPLIT ? NB * kB : 0;
-  static constexpr int NBS = NPAD <= 96 ? 8 : 4;
-  static constexpr int NX_fit = int((budget - NBS * kB - lo_bytes) / kX);
+  static constexpr uint32_t budget = 224u * 1024u;
+  static constexpr int NBS = BSPLIT ? (kBS <= 24u * 1024u ? 6 : 4) : (NPAD <= 96 ? 8 : 4);
+  static constexpr int NX_fit = int((budget - NBS * kBS) / kX);
   static constexpr int NX = NX_fit > 10 ? 10 : NX_fit;
   static constexpr uint32_t off_x = 0;
   static constexpr uint32_t off_b = off_x + NX * kX;
-  static constexpr uint32_t off_blo = off_b + NBS * kB;
-  static constexpr uint32_t off_bar = off_blo + lo_bytes;
+  static constexpr uint32_t off_bar = off_b + NBS * kBS;
   static constexpr int nbar = 2 * NX + 2 * NBS + 2 * 4 + 4;
   static constexpr uint32_t bytes = off_bar + 8 * nbar + 16;
   static_assert(NX >= 4, "X ring too shallow");
@@ -172,19 +174,29 @@ __device__ __forceinline__ void split_b(float* b, float* blo, int t) {
   }
 }
 
-// One stage, issuer q of NI: its share of the 4 k-steps x (2 or 3) products into accumulator `acc`.
-template <bool BSPLIT, int NI, bool BMN = false>
-__device__ __forceinline__ void issue_stage(uint32_t tmem, uint32_t acc, uint32_t a_col, int q, uint32_t b_saddr,
-                                            uint32_t blo_saddr, uint32_t idesc, bool first) {
+// One stage (4 k-steps) of issuer q into accumulator buffer ab (see Plan).
+template <class P, bool BSPLIT, bool BMN>
+__device__ __forceinline__ void issue_stage(uint32_t tmem, int q, int ab, uint32_t a_col, uint32_t b_saddr,
+                                            uint32_t idesc0, uint32_t idesc1, bool first) {
   const uint32_t a_hi = tmem + a_col;
-  constexpr int KPI = (KC / 8) / NI;
+  if constexpr (BSPLIT) {
+    const uint32_t d = tmem + P::acc(q, 0);
 #pragma unroll
-  for (int k = 0; k < KPI; ++k) {
-    const int kk = q * KPI + k;
-    const uint64_t bd = bdesc<BMN>(b_saddr, kk);
-    mma_tf32_ts(tmem + acc, a_hi + 8 * kk, bd, idesc, (first && k == 0) ? 0u : 1u);
-    mma_tf32_ts(tmem + acc, a_hi + 32 + 8 * kk, bd, idesc, 1u);
-    if (BSPLIT) mma_tf32_ts(tmem + acc, a_hi + 8 * kk, bdesc<BMN>(blo_saddr, kk), idesc, 1u);
+    for (int kk = 0; kk < KC / 8; ++kk) {
+      const uint64_t bd = bdesc<BMN>(b_saddr, kk);      // [B_hi | B_lo] (issuer 0) or B_hi (issuer 1)
+      if (q == 0) mma_tf32_ts_w(d, a_hi + 8 * kk, bd, idesc0, (first && kk == 0) ? 0u : 1u);
+      else mma_tf32_ts_w(d, a_hi + 32 + 8 * kk, bd, idesc1, (first && kk == 0) ? 0u : 1u);
+    }
+  } else {
+    const uint32_t d = tmem + P::acc(q, ab);
+    constexpr int KPI = (KC / 8) / P::NI;
+#pragma unroll
+    for (int k = 0; k < KPI; ++k) {
+      const int kk = q * KPI + k;
+      const uint64_t bd = bdesc<BMN>(b_saddr, kk);
+      mma_tf32_ts_w(d, a_hi + 8 * kk, bd, idesc0, (first && k == 0) ? 0u : 1u);
+      mma_tf32_ts_w(d, a_hi + 32 + 8 * kk, bd, idesc0, 1u);
+    }
   }
 }
 
@@ -195,23 +207,46 @@ struct Ring {
   template <int N> __device__ __forceinline__ void next() { if (++s == N) { s = 0; ph ^= 1; } }
 };
 
-// Drain accumulator buffer `ab` (use index u) into register sums; release the buffer.  All
-// tcgen05.ld are issued before a single wait::ld.
+template <class P>
+__device__ __forceinline__ int acc_buf(int64_t u) { return P::NBUF == 2 ? int(u & 1) : 0; }
+template <class P>
+__device__ __forceinline__ uint32_t acc_par(int64_t u) { return uint32_t(P::NBUF == 2 ? (u >> 1) : u) & 1u; }
+
+// Issuer side: before the first stage of segment u, wait until the epilogue has drained the
+// accumulator buffer it reuses.
+template <class P>
+__device__ __forceinline__ void wait_acc_free(const Bars& b, int64_t u) {
+  if (u >= P::NBUF) mbar_wait(&b.acc_empty[acc_buf<P>(u)], acc_par<P>(u - P::NBUF));
+}
+
 template <int NPAD>
-__device__ __forceinline__ void drain_acc(const Bars& b, uint32_t lane_base, int64_t u, float (&sums)[NPAD]) {
-  using TP = TmemPlan<NPAD>;
-  const int ab = int(u & 1);
-  mbar_wait(&b.acc_full[ab], uint32_t(u >> 1) & 1);
-  tc_fence_after();
+__device__ __forceinline__ void add_cols(uint32_t taddr, float (&sums)[NPAD]) {
+  // 32 columns per tcgen05.ld batch keeps the epilogue warps under the 384-thread register budget
 #pragma unroll
-  for (int q = 0; q < TP::NI; ++q) {
-    uint32_t v[NPAD];
-#pragma unroll
-    for (int cb = 0; cb < NPAD / 16; ++cb)
-      tmem_ld16(lane_base + TP::acc(q, ab) + 16 * cb, *reinterpret_cast<uint32_t(*)[16]>(&v[16 * cb]));
+  for (int c0 = 0; c0 < NPAD; c0 += 32) {
+    uint32_t v[32];
+    tmem_ld16(taddr + c0, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+    if (c0 + 16 < NPAD) tmem_ld16(taddr + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
     tmem_wait_ld();
 #pragma unroll
-    for (int k = 0; k < NPAD; ++k) sums[k] += __uint_as_float(v[k]);
+    for (int k = 0; k < 32; ++k)
+      if (c0 + k < NPAD) sums[c0 + k] += __uint_as_float(v[k]);
+  }
+}
+
+// Drain segment u's accumulators into the register sums and release them.
+template <class P, int NPAD, bool BSPLIT>
+__device__ __forceinline__ void drain_acc(const Bars& b, uint32_t lane_base, int64_t u, float (&sums)[NPAD]) {
+  const int ab = acc_buf<P>(u);
+  mbar_wait(&b.acc_full[ab], acc_par<P>(u));
+  tc_fence_after();
+  if constexpr (BSPLIT) {
+    add_cols<NPAD>(lane_base + P::acc(0, 0), sums);             // A_hi B_hi
+    add_cols<NPAD>(lane_base + P::acc(0, 0) + P::NH, sums);     // A_hi B_lo
+    add_cols<NPAD>(lane_base + P::acc(1, 0), sums);             // A_lo B_hi
+  } else {
+#pragma unroll
+    for (int q = 0; q < P::NI; ++q) add_cols<NPAD>(lane_base + P::acc(q, ab), sums);
   }
   tc_fence_before();
   mbar_arrive(&b.acc_empty[ab]);
@@ -227,7 +262,21 @@ struct SParams {
   int ablate;         // profiling only: 1 = no MMA, 2 = no split work (results invalid)
   int skew;           // chunk-order rotation per M-tile (decorrelates the rows' DRAM addresses)
   float* part;        // [split][K][I]
+  unsigned long long* tim;   // diagnostics (RT_OPT_TC_ABLATE = 1000): per-CTA role wait cycles, else null
 };
+
+// diagnostics: accumulate the cycles spent in `body` into slot k of this CTA's timing record
+#define RT_TIMED(tim, k, ...)                                                                   \
+  do {                                                                                           \
+    if (tim) {                                                                                   \
+      const long long t0_ = clock64();                                                           \
+      __VA_ARGS__;                                                                               \
+      if ((threadIdx.x & 31) == 0)                                                               \
+        atomicAdd(&(tim)[(blockIdx.y * gridDim.x + blockIdx.x) * 24 + (k)], (unsigned long long)(clock64() - t0_)); \
+    } else {                                                                                     \
+      __VA_ARGS__;                                                                               \
+    }                                                                                            \
+  } while (0)
 
 // chunk c -> X tile coordinates and first B row j0
 template <bool AMN>
@@ -238,13 +287,14 @@ __device__ __forceinline__ void chunk_coords(const SParams& p, int64_t c, int64_
 
 // grid (mtiles, splits): CTA (m, z) sums the contiguous chunk range z*per .. (z+1)*per-1 of M-tile m.
 // The M-tiles of a split are adjacent in launch order, so the CTAs that share a B chunk (Omega / Z
-// rows) run in the same wave and in near lockstep: B comes from DRAM once and from L2 for the rest
-// (a split-major order re-read Omega once per wave: +16% DRAM traffic on cfg5, ncu).
-template <int NPAD, bool BSPLIT, bool AMN>
+// rows) run in the same wave and in near lockstep: B comes from DRAM once and from L2 for the rest.
+// BPRE (with BSPLIT): B is pre-split in global memory, row j = [hi (NH columns) | lo (NH columns)],
+// and is loaded as the whole [B_hi | B_lo] slot; nothing is split in the kernel.
+template <int NPAD, bool BSPLIT, bool AMN, bool BPRE>
 __global__ void __launch_bounds__(NT_TTM, 1)
 ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb, const SParams p) {
-  using L = Smem<NPAD, BSPLIT, true>;
-  constexpr int NBX = (NPAD + 31) / 32;                // 32-wide N atom columns of the B tile
+  static_assert(!BPRE || BSPLIT, "pre-split B implies the split product form");
+  using L = Plan<NPAD, BSPLIT, true>;
   constexpr int NX = L::NX;
   extern __shared__ __align__(1024) uint8_t smem[];
   const Bars b = bars_of<L>(smem);
@@ -275,7 +325,7 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
       Ring rx;
       const uint64_t pol = policy_evict_first();
       for (int it = 0; it < nch; ++it, rx.next<NX>()) {
-        if (it >= NX) mbar_wait(&b.x_free[rx.s], rx.ph ^ 1);
+        if (it >= NX) RT_TIMED(p.tim, 0, mbar_wait(&b.x_free[rx.s], rx.ph ^ 1));
         int64_t a0, beta, j0;
         chunk_coords<AMN>(p, chunk_of(it), a0, beta, j0);
         mbar_expect_tx(&b.x_full[rx.s], L::kX);
@@ -285,79 +335,90 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
       }
     }
   } else if (warp == 6) {
-    if (lane == 0) {                                   // ---------------- B producer
+    if (lane == 0) {                                   // ---------------- B producer (hi tile)
       Ring rb;
       const uint64_t pol = policy_evict_last();
       for (int it = 0; it < nch; ++it, rb.next<L::NBS>()) {
-        if (it >= L::NBS) mbar_wait(&b.b_free[rb.s], rb.ph ^ 1);
+        if (it >= L::NBS) RT_TIMED(p.tim, 1, mbar_wait(&b.b_free[rb.s], rb.ph ^ 1));
         int64_t a0, beta, j0;
         chunk_coords<AMN>(p, chunk_of(it), a0, beta, j0);
-        mbar_expect_tx(&b.b_full[rb.s], L::kB);
+        constexpr int nbox = BPRE ? 2 * L::NBX : L::NBX;
+        mbar_expect_tx(&b.b_full[rb.s], nbox * 4096);
 #pragma unroll
-        for (int x = 0; x < NBX; ++x)
-          tma_load_2d_hint(smem + L::off_b + rb.s * L::kB + x * 4096, &tmb, &b.b_full[rb.s], 32 * x, int(j0), pol);
+        for (int x = 0; x < nbox; ++x)
+          tma_load_2d_hint(smem + L::off_b + rb.s * L::kBS + x * 4096, &tmb, &b.b_full[rb.s], 32 * x, int(j0), pol);
       }
     }
   } else if (warp == 1 || warp == 7) {
     const int q = warp == 1 ? 0 : 1;
-    if (lane == 0 && q < L::NI) {                      // ---------------- MMA issuers
-      using TP = TmemPlan<NPAD>;
-      const uint32_t idesc = idesc_tf32(BM, NPAD, 1);
+    if (q < L::NI) {                                   // ---------------- MMA issuers (whole warp)
+      unsigned long long* tim = p.tim;
+      const uint32_t idesc0 = idesc_tf32(BM, BSPLIT ? L::NH + NPAD : NPAD, 1);
+      const uint32_t idesc1 = idesc_tf32(BM, NPAD, 1);
       Ring rt, rb;
-      int u = 0, pos = 0;
+      int64_t u = 0;
+      int pos = 0;
+      const long long tl0 = clock64();
       for (int it = 0; it < nch; ++it, rt.next<L::NB>(), rb.next<L::NBS>()) {
         const bool first = pos == 0;
         const bool last = (pos == p.seg - 1) || (it == nch - 1);
-        const int ab = u & 1;
-        if (first && u >= 2) mbar_wait(&b.acc_empty[ab], ((u >> 1) - 1) & 1);
-        mbar_wait(&b.ready[rt.s], rt.ph);
-        if (!BSPLIT) mbar_wait(&b.b_full[rb.s], rb.ph);
-        tc_fence_after();
-        if (p.ablate != 1)
-          issue_stage<BSPLIT, L::NI, true>(tmem, TP::acc(q, ab), TP::a_slot(rt.s), q,
-                                           smem_u32(smem + L::off_b + rb.s * L::kB),
-                                           smem_u32(smem + L::off_blo + rt.s * L::kB), idesc, first);
-        mma_commit(&b.tfree[rt.s]);
-        mma_commit(&b.b_free[rb.s]);
-        if (last) { mma_commit(&b.acc_full[ab]); ++u; pos = 0; } else { ++pos; }
+        if (first) RT_TIMED(tim, 2 + 4 * q, wait_acc_free<L>(b, u));
+        RT_TIMED(tim, 3 + 4 * q, mbar_wait(&b.ready[rt.s], rt.ph));
+        if (!BSPLIT || BPRE) RT_TIMED(tim, 4 + 4 * q, mbar_wait(&b.b_full[rb.s], rb.ph));
+        RT_TIMED(tim, 20 + q, tc_fence_after());
+        RT_TIMED(tim, 5 + 4 * q, {
+          if (p.ablate != 1)
+            issue_stage<L, BSPLIT, true>(tmem, q, acc_buf<L>(u), L::a_slot(rt.s),
+                                         smem_u32(smem + L::off_b + rb.s * L::kBS), idesc0, idesc1, first);
+        });
+        RT_TIMED(tim, 16 + q, {
+          mma_commit_w(&b.tfree[rt.s]);
+          mma_commit_w(&b.b_free[rb.s]);
+        });
+        if (last) { mma_commit_w(&b.acc_full[acc_buf<L>(u)]); ++u; pos = 0; } else { ++pos; }
       }
+      if (tim && lane == 0)
+        atomicAdd(&tim[(blockIdx.y * gridDim.x + blockIdx.x) * 24 + 18 + q], (unsigned long long)(clock64() - tl0));
     }
-  } else {                                             // ---------------- splitters / epilogue
+  } else if (warp >= 2 && warp <= 5) {                 // ---------------- splitters
     const int q4 = warp & 3;
     const int r = 32 * q4 + lane;
     const uint32_t lane_base = tmem + (uint32_t(32 * q4) << 16);
     const int t = threadIdx.x - 64;
+    unsigned long long* tim = (warp == 2) ? p.tim : nullptr;   // warp-uniform (aligned tcgen05 ops inside)
+    const long long tstart = clock64();
+    Ring rx, rt, rb;
+    for (int it = 0; it < nch; ++it, rx.next<NX>(), rt.next<L::NB>(), rb.next<L::NBS>()) {
+      RT_TIMED(tim, 10, mbar_wait(&b.x_full[rx.s], rx.ph));
+      if (it >= L::NB) RT_TIMED(tim, 11, mbar_wait(&b.tfree[rt.s], rt.ph ^ 1));   // TMEM slot free
+      RT_TIMED(tim, 12, {
+        if (p.ablate != 2)
+          split_row_to_tmem<AMN>(reinterpret_cast<const float*>(smem + L::off_x + rx.s * L::kX), r,
+                                 lane_base + L::a_slot(rt.s));
+      });
+      mbar_arrive(&b.x_free[rx.s]);
+      if (BSPLIT && !BPRE) {
+        RT_TIMED(tim, 13, mbar_wait(&b.b_full[rb.s], rb.ph));
+        float* bs = reinterpret_cast<float*>(smem + L::off_b + rb.s * L::kBS);
+        split_b<L::kB>(bs, bs + L::kB / 4, t);
+      }
+      tmem_wait_st();
+      if (BSPLIT && !BPRE) fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(&b.ready[rt.s]);
+    }
+    if (tim && lane == 0)
+      atomicAdd(&tim[(blockIdx.y * gridDim.x + blockIdx.x) * 24 + 15], (unsigned long long)(clock64() - tstart));
+  } else if (warp >= 8) {                              // ---------------- epilogue: drain segments
+    const int q4 = warp & 3;
+    const int r = 32 * q4 + lane;
+    const uint32_t lane_base = tmem + (uint32_t(32 * q4) << 16);
+    unsigned long long* tim = (warp == 8) ? p.tim : nullptr;
     float sums[NPAD];
 #pragma unroll
     for (int k = 0; k < NPAD; ++k) sums[k] = 0.f;
-    Ring rx, rt, rb;
-    int u = 0, pos = 0;
-    for (int it = 0; it < nch; ++it, rx.next<NX>(), rt.next<L::NB>(), rb.next<L::NBS>()) {
-      mbar_wait(&b.x_full[rx.s], rx.ph);
-      if (it >= L::NB) mbar_wait(&b.tfree[rt.s], rt.ph ^ 1);   // TMEM slot (and B lo) free
-      if (p.ablate != 2)
-        split_row_to_tmem<AMN>(reinterpret_cast<const float*>(smem + L::off_x + rx.s * L::kX), r,
-                               lane_base + TmemPlan<NPAD>::a_slot(rt.s));
-      mbar_arrive(&b.x_free[rx.s]);
-      if (BSPLIT) {
-        mbar_wait(&b.b_full[rb.s], rb.ph);
-        split_b<L::kB>(reinterpret_cast<float*>(smem + L::off_b + rb.s * L::kB),
-                       reinterpret_cast<float*>(smem + L::off_blo + rt.s * L::kB), t);
-      }
-      tmem_wait_st();
-      if (BSPLIT) fence_proxy_async();
-      tc_fence_before();
-      mbar_arrive(&b.ready[rt.s]);
-      const bool last = (pos == p.seg - 1) || (it == nch - 1);
-      if (last) {
-        if (u >= 1) drain_acc<NPAD>(b, lane_base, u - 1, sums);
-        ++u;
-        pos = 0;
-      } else {
-        ++pos;
-      }
-    }
-    if (u >= 1) drain_acc<NPAD>(b, lane_base, u - 1, sums);
+    const int64_t nseg = (nch + p.seg - 1) / p.seg;
+    for (int64_t u = 0; u < nseg; ++u) RT_TIMED(tim, 14, drain_acc<L, NPAD, BSPLIT>(b, lane_base, u, sums));
     const int64_t i = i0 + r;                         // partial tile -> part[split][k][i]
     if (i < p.I) {
       float* dst = p.part + z * p.K * p.I;
@@ -383,13 +444,14 @@ struct TParams {
   float* out;
   int64_t so_a, so_c, so_b;
   bool vec4;          // so_c == 1 and every output row 16-byte aligned with C % 4 == 0
+  bool split_out;     // write each output row as [hi (NHO) | lo (NHO)] tf32 halves (vec4 layout)
 };
 
 template <int NPAD, bool AKM>   // AKM: mode 0 (a == 1), X tile K-major [BM j][KC i]
 __global__ void __launch_bounds__(NT_TTM, 1)
 ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb, const TParams p) {
-  constexpr bool BSPLIT = true;
-  using L = Smem<NPAD, BSPLIT>;
+  constexpr bool BSPLIT = true;                        // Q (fp64 basis) is never tf32-exact
+  using L = Plan<NPAD, BSPLIT, false>;
   constexpr int NX = L::NX;
   extern __shared__ __align__(1024) uint8_t smem[];
   const Bars b = bars_of<L>(smem);
@@ -430,22 +492,22 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
       }
     }
   } else if (warp == 6) {
-    if (lane == 0) {                                   // ---------------- B producer
+    if (lane == 0) {                                   // ---------------- B producer ([Q_hi | Q_lo])
       Ring rb;
       const uint64_t pol = policy_evict_last();
       int it = 0;
       for (int64_t u = 0; u < my_tiles; ++u)
         for (int c = 0; c < p.nic; ++c, ++it, rb.next<L::NBS>()) {
           if (it >= L::NBS) mbar_wait(&b.b_free[rb.s], rb.ph ^ 1);
-          mbar_expect_tx(&b.b_full[rb.s], L::kB);
-          tma_load_2d_hint(smem + L::off_b + rb.s * L::kB, &tmb, &b.b_full[rb.s], c * KC, 0, pol);
+          mbar_expect_tx(&b.b_full[rb.s], L::kBS);
+          tma_load_2d_hint(smem + L::off_b + rb.s * L::kBS, &tmb, &b.b_full[rb.s], c * KC, 0, pol);
         }
     }
   } else if (warp == 1 || warp == 7) {
     const int q = warp == 1 ? 0 : 1;
-    if (lane == 0 && q < L::NI) {                      // ---------------- MMA issuers
-      using TP = TmemPlan<NPAD>;
-      const uint32_t idesc = idesc_tf32(BM, NPAD, 0);
+    if (q < L::NI) {                                   // ---------------- MMA issuers (whole warp)
+      const uint32_t idesc0 = idesc_tf32(BM, L::NH + NPAD, 0);
+      const uint32_t idesc1 = idesc_tf32(BM, NPAD, 0);
       Ring rt, rb;
       int64_t g = 0;                                   // global segment counter
       for (int64_t u = 0; u < my_tiles; ++u) {
@@ -453,87 +515,82 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
         for (int c = 0; c < p.nic; ++c, rt.next<L::NB>(), rb.next<L::NBS>()) {
           const bool first = pos == 0;
           const bool last = (pos == p.seg - 1) || (c == p.nic - 1);
-          const int ab = int(g & 1);
-          if (first && g >= 2) mbar_wait(&b.acc_empty[ab], uint32_t((g >> 1) - 1) & 1);
+          if (first) wait_acc_free<L>(b, g);
           mbar_wait(&b.ready[rt.s], rt.ph);
+          mbar_wait(&b.b_full[rb.s], rb.ph);
           tc_fence_after();
-          issue_stage<BSPLIT, L::NI>(tmem, TP::acc(q, ab), TP::a_slot(rt.s), q,
-                                     smem_u32(smem + L::off_b + rb.s * L::kB),
-                                     smem_u32(smem + L::off_blo + rt.s * L::kB), idesc, first);
-          mma_commit(&b.tfree[rt.s]);
-          mma_commit(&b.b_free[rb.s]);
-          if (last) { mma_commit(&b.acc_full[ab]); ++g; pos = 0; } else { ++pos; }
+          issue_stage<L, BSPLIT, false>(tmem, q, acc_buf<L>(g), L::a_slot(rt.s),
+                                        smem_u32(smem + L::off_b + rb.s * L::kBS), idesc0, idesc1, first);
+          mma_commit_w(&b.tfree[rt.s]);
+          mma_commit_w(&b.b_free[rb.s]);
+          if (last) { mma_commit_w(&b.acc_full[acc_buf<L>(g)]); ++g; pos = 0; } else { ++pos; }
         }
       }
     }
-  } else {                                             // ---------------- splitters / epilogue
+  } else if (warp >= 2 && warp <= 5) {                 // ---------------- splitters
     const int q4 = warp & 3;
     const int r = 32 * q4 + lane;
     const uint32_t lane_base = tmem + (uint32_t(32 * q4) << 16);
-    const int t = threadIdx.x - 64;
-    float sums[NPAD];
-#pragma unroll
-    for (int k = 0; k < NPAD; ++k) sums[k] = 0.f;
-    // drain segment g into the register sums; after the last segment of a tile, store the tile
-    auto epilogue = [&](int64_t g, bool tile_end, int64_t tile) {
-      drain_acc<NPAD>(b, lane_base, g, sums);
-      if (tile_end) {
-        int64_t a0, beta;
-        tile_coords(tile, a0, beta);
-        bool valid;
-        int64_t ob;
-        if (AKM) { const int64_t j = beta + r; valid = j < p.b; ob = j * p.so_b; }
-        else { const int64_t al = a0 + r; valid = al < p.a; ob = al * p.so_a + beta * p.so_b; }
-        if (valid) {
-          if (p.vec4) {                                        // row-major output rows: 16 B stores
-            float4* o4 = reinterpret_cast<float4*>(p.out + ob);
-#pragma unroll
-            for (int k = 0; k < NPAD / 4; ++k)
-              if (4 * k < p.C) o4[k] = make_float4(sums[4 * k], sums[4 * k + 1], sums[4 * k + 2], sums[4 * k + 3]);
-          } else {
-#pragma unroll
-            for (int k = 0; k < NPAD; ++k)
-              if (k < p.C) p.out[ob + int64_t(k) * p.so_c] = sums[k];
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < NPAD; ++k) sums[k] = 0.f;
-      }
-    };
-    Ring rx, rt, rb;
-    int64_t g = 0;
-    bool prev_end = false;
-    int64_t prev_tile = 0;
+    Ring rx, rt;
     int it = 0;
     for (int64_t u = 0; u < my_tiles; ++u) {
-      const int64_t tile = blockIdx.x + u * gridDim.x;
-      int pos = 0;
-      for (int c = 0; c < p.nic; ++c, ++it, rx.next<NX>(), rt.next<L::NB>(), rb.next<L::NBS>()) {
+      for (int c = 0; c < p.nic; ++c, ++it, rx.next<NX>(), rt.next<L::NB>()) {
         mbar_wait(&b.x_full[rx.s], rx.ph);
         if (it >= L::NB) mbar_wait(&b.tfree[rt.s], rt.ph ^ 1);
         split_row_to_tmem<!AKM>(reinterpret_cast<const float*>(smem + L::off_x + rx.s * L::kX), r,
-                                lane_base + TmemPlan<NPAD>::a_slot(rt.s));
+                                lane_base + L::a_slot(rt.s));
         mbar_arrive(&b.x_free[rx.s]);
-        mbar_wait(&b.b_full[rb.s], rb.ph);
-        split_b<L::kB>(reinterpret_cast<float*>(smem + L::off_b + rb.s * L::kB),
-                       reinterpret_cast<float*>(smem + L::off_blo + rt.s * L::kB), t);
         tmem_wait_st();
-        fence_proxy_async();
         tc_fence_before();
         mbar_arrive(&b.ready[rt.s]);
-        const bool last = (pos == p.seg - 1) || (c == p.nic - 1);
-        if (last) {
-          if (g >= 1) epilogue(g - 1, prev_end, prev_tile);   // delayed by one segment
-          prev_end = (c == p.nic - 1);
-          prev_tile = tile;
-          ++g;
-          pos = 0;
-        } else {
-          ++pos;
-        }
       }
     }
-    if (g >= 1) epilogue(g - 1, prev_end, prev_tile);
+  } else if (warp >= 8) {                              // ---------------- epilogue: drain, store tiles
+    const int q4 = warp & 3;
+    const int r = 32 * q4 + lane;
+    const uint32_t lane_base = tmem + (uint32_t(32 * q4) << 16);
+    float sums[NPAD];
+#pragma unroll
+    for (int k = 0; k < NPAD; ++k) sums[k] = 0.f;
+    const int segs_per_tile = (p.nic + p.seg - 1) / p.seg;
+    int64_t g = 0;
+    for (int64_t u = 0; u < my_tiles; ++u) {
+      const int64_t tile = blockIdx.x + u * gridDim.x;
+      for (int sgi = 0; sgi < segs_per_tile; ++sgi, ++g) drain_acc<L, NPAD, BSPLIT>(b, lane_base, g, sums);
+      int64_t a0, beta;
+      tile_coords(tile, a0, beta);
+      bool valid;
+      int64_t ob;
+      if (AKM) { const int64_t j = beta + r; valid = j < p.b; ob = j * p.so_b; }
+      else { const int64_t al = a0 + r; valid = al < p.a; ob = al * p.so_a + beta * p.so_b; }
+      if (valid) {
+        if (p.split_out) {                                   // [hi | lo] rows for a pre-split B operand
+          constexpr int NHO = ((NPAD + 31) / 32) * 32;
+          float4* oh = reinterpret_cast<float4*>(p.out + ob);
+          float4* ol = reinterpret_cast<float4*>(p.out + ob + NHO);
+#pragma unroll
+          for (int k = 0; k < NHO / 4; ++k) {
+            uint32_t h[4], l[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) split_tf32((4 * k + e < NPAD && 4 * k + e < p.C) ? sums[(4 * k + e) % NPAD] : 0.f,
+                                                   h[e], l[e]);
+            oh[k] = make_float4(__uint_as_float(h[0]), __uint_as_float(h[1]), __uint_as_float(h[2]), __uint_as_float(h[3]));
+            ol[k] = make_float4(__uint_as_float(l[0]), __uint_as_float(l[1]), __uint_as_float(l[2]), __uint_as_float(l[3]));
+          }
+        } else if (p.vec4) {                                 // row-major output rows: 16 B stores
+          float4* o4 = reinterpret_cast<float4*>(p.out + ob);
+#pragma unroll
+          for (int k = 0; k < NPAD / 4; ++k)
+            if (4 * k < p.C) o4[k] = make_float4(sums[4 * k], sums[4 * k + 1], sums[4 * k + 2], sums[4 * k + 3]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < NPAD; ++k)
+            if (k < p.C) p.out[ob + int64_t(k) * p.so_c] = sums[k];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < NPAD; ++k) sums[k] = 0.f;
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -602,25 +659,28 @@ void set_smem(Kern kernel, uint32_t bytes) {
   RT_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
 }
 
-template <int NPAD, bool BSPLIT, bool AMN>
+template <int NPAD, bool BSPLIT, bool AMN, bool BPRE>
 void launch_s(const Ctx& ctx, const CUtensorMap& tx, const CUtensorMap& tb, const SParams& p, dim3 grid) {
-  using L = Smem<NPAD, BSPLIT, true>;
+  using L = Plan<NPAD, BSPLIT, true>;
   static bool attr = false;
-  if (!attr) { set_smem(ttm_s_tc_kernel<NPAD, BSPLIT, AMN>, L::bytes); attr = true; }
+  if (!attr) { set_smem(ttm_s_tc_kernel<NPAD, BSPLIT, AMN, BPRE>, L::bytes); attr = true; }
   launch(ctx, ctx.label ? ctx.label : "ttm_s_tc", [&] {
-    ttm_s_tc_kernel<NPAD, BSPLIT, AMN><<<grid, NT_TTM, L::bytes, ctx.stream>>>(tx, tb, p);
+    ttm_s_tc_kernel<NPAD, BSPLIT, AMN, BPRE><<<grid, NT_TTM, L::bytes, ctx.stream>>>(tx, tb, p);
   });
 }
 
-template <int NPAD, bool BSPLIT>
-void dispatch_s(const Ctx& ctx, bool amn, const CUtensorMap& tx, const CUtensorMap& tb, const SParams& p, dim3 g) {
-  if (amn) launch_s<NPAD, BSPLIT, true>(ctx, tx, tb, p, g);
-  else launch_s<NPAD, BSPLIT, false>(ctx, tx, tb, p, g);
+// b: 0 tf32-exact B, 1 split in the kernel, 2 pre-split in global memory
+template <int NPAD>
+void dispatch_s(const Ctx& ctx, bool amn, int bmode, const CUtensorMap& tx, const CUtensorMap& tb, const SParams& p,
+                dim3 g) {
+  if (bmode == 0) { if (amn) launch_s<NPAD, false, true, false>(ctx, tx, tb, p, g); else launch_s<NPAD, false, false, false>(ctx, tx, tb, p, g); }
+  else if (bmode == 1) { if (amn) launch_s<NPAD, true, true, false>(ctx, tx, tb, p, g); else launch_s<NPAD, true, false, false>(ctx, tx, tb, p, g); }
+  else { if (amn) launch_s<NPAD, true, true, true>(ctx, tx, tb, p, g); else launch_s<NPAD, true, false, true>(ctx, tx, tb, p, g); }
 }
 
 template <int NPAD, bool AKM>
 void launch_t(const Ctx& ctx, const CUtensorMap& tx, const CUtensorMap& tb, const TParams& p, dim3 grid) {
-  using L = Smem<NPAD, true>;
+  using L = Plan<NPAD, true, false>;
   static bool attr = false;
   if (!attr) { set_smem(ttm_t_tc_kernel<NPAD, AKM>, L::bytes); attr = true; }
   launch(ctx, ctx.label ? ctx.label : "ttm_t_tc", [&] {
@@ -638,15 +698,43 @@ __global__ void splitk_reduce_f32_kernel(const float* __restrict__ part, int64_t
   Y[i + ldy * k] = s;
 }
 
-int tc_npad(int K) {
-  return K <= 16 ? 16 : K <= 32 ? 32 : K <= 48 ? 48 : K <= 64 ? 64 : K <= 80 ? 80 : K <= 96 ? 96 : K <= 128 ? 128 : -1;
+// Q (I x C, col-major ldq) -> Q2 (I x 2 npad, col-major ld2): columns [0, C) = tf32 hi, columns
+// [npad, npad + C) = lo, the rest zero (the pre-split [B_hi | B_lo] operand of ttm_t_tc)
+__global__ void split_q_kernel(const float* __restrict__ Q, int64_t I, int C, int64_t ldq, int npad,
+                               float* __restrict__ Q2, int64_t ld2) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= ld2 * npad) return;
+  const int64_t i = e % ld2;
+  const int c = int(e / ld2);
+  const float v = (i < I && c < C) ? Q[i + ldq * c] : 0.f;
+  uint32_t h, l;
+  split_tf32(v, h, l);
+  Q2[i + ld2 * c] = __uint_as_float(h);
+  Q2[i + ld2 * (npad + c)] = __uint_as_float(l);
 }
 
 }  // namespace
 
+int tc_npad(int K) {
+  return K <= 16 ? 16 : K <= 32 ? 32 : K <= 48 ? 48 : K <= 64 ? 64 : K <= 80 ? 80 : K <= 96 ? 96 : K <= 128 ? 128 : -1;
+}
+int tc_split_width(int K) {
+  const int np = tc_npad(K);
+  return np < 0 ? -1 : ((np + 31) / 32) * 32;
+}
+
+bool ttm_s_tc_ok(const Ctx& ctx, const float* X, Box box, int K) {
+  if (ctx.ttm_impl == 1 || tc_npad(K) < 0) return false;
+  const int64_t J = box.J();
+  if (box.I < 1 || J < KC || !aligned(X, 16)) return false;
+  const bool amn = (box.a == 1);
+  if (amn ? (box.I % 4) : (box.a % 4)) return false;
+  return !(box.a > INT32_MAX || box.I > INT32_MAX || box.b > INT32_MAX || J > INT32_MAX);
+}
+
 // Returns false (nothing launched) when the shape/alignment is not supported by the TMA path.
 bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Bm, int64_t ldb, bool b_tf32_exact,
-              int K, double* Y, int64_t ldy) {
+              int K, double* Y, int64_t ldy, bool b_presplit) {
   const int npad = tc_npad(K);
   if (npad < 0) return false;
   const int64_t J = box.J();
@@ -654,6 +742,7 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
   const bool amn = (box.a == 1);
   if (amn ? (box.I % 4) : (box.a % 4)) return false;
   if (box.a > INT32_MAX || box.I > INT32_MAX || box.b > INT32_MAX || J > INT32_MAX) return false;
+  const int nh = tc_split_width(K);
   CUtensorMap tx, tb;
   if (amn) {
     const uint64_t d[2] = {uint64_t(box.I), uint64_t(box.b)}, s[1] = {uint64_t(box.I) * 4};
@@ -665,7 +754,7 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
     const uint32_t bx[3] = {KC, BM, 1};
     if (!make_map(&tx, X, 3, d, s, bx, true)) return false;
   }
-  if (!make_b_map_rm(&tb, Bm, J, K, ldb)) return false;
+  if (!make_b_map_rm(&tb, Bm, J, b_presplit ? 2 * nh : K, ldb)) return false;
   SParams p;
   p.a = box.a; p.I = box.I; p.b = box.b; p.K = K;
   p.cpb = amn ? 1 : cdiv(box.a, KC);
@@ -678,18 +767,39 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
   p.ablate = ctx.tc_ablate;
   p.skew = ctx.tc_skew >= 0 ? ctx.tc_skew : 0;
   p.part = ws.alloc_n<float>(splits * K * box.I);
+  p.tim = nullptr;
   const dim3 grid{unsigned(mtiles), unsigned(splits), 1u};
-  const bool bsplit = !b_tf32_exact;
-#define RT_S_CASE(NP)                                              \
-  case NP:                                                         \
-    if (bsplit) dispatch_s<NP, true>(ctx, amn, tx, tb, p, grid);   \
-    else dispatch_s<NP, false>(ctx, amn, tx, tb, p, grid);         \
+  if (ctx.tc_ablate == 1000) {
+    p.tim = ws.alloc_n<unsigned long long>(mtiles * splits * 24);
+    RT_CUDA(cudaMemsetAsync(p.tim, 0, sizeof(unsigned long long) * mtiles * splits * 24, ctx.stream));
+  }
+  const int bmode = b_presplit ? 2 : (b_tf32_exact ? 0 : 1);
+#define RT_S_CASE(NP)                                       \
+  case NP:                                                  \
+    dispatch_s<NP>(ctx, amn, bmode, tx, tb, p, grid);       \
     break;
   switch (npad) {
     RT_S_CASE(16) RT_S_CASE(32) RT_S_CASE(48) RT_S_CASE(64) RT_S_CASE(80) RT_S_CASE(96) RT_S_CASE(128)
     default: return false;
   }
 #undef RT_S_CASE
+  if (p.tim) {   // diagnostics: mean cycles per CTA spent in each role's waits / work
+    std::vector<unsigned long long> h(size_t(mtiles * splits * 24));
+    RT_CUDA(cudaMemcpyAsync(h.data(), p.tim, h.size() * 8, cudaMemcpyDeviceToHost, ctx.stream));
+    RT_CUDA(cudaStreamSynchronize(ctx.stream));
+    static const char* nm[22] = {"x_prod:wait_free", "b_prod:wait_free", "iss0:acc_empty", "iss0:ready", "iss0:b_full",
+                                 "iss0:mma", "iss1:acc_empty", "iss1:ready", "iss1:b_full", "iss1:mma",
+                                 "split:x_full", "split:tfree", "split:split", "split:b_full", "split:drain", "total",
+                                 "iss0:commits", "iss1:commits", "iss0:loop", "iss1:loop", "iss0:fence", "iss1:fence"};
+    std::fprintf(stderr, "[ttm_s_tc diag] %s npad=%d bmode=%d grid=%lldx%lld chunks/cta=%lld\n",
+                 ctx.label ? ctx.label : "ttm_s_tc", npad, bmode, (long long)mtiles, (long long)splits,
+                 (long long)((p.nchunks + splits - 1) / splits));
+    for (int k = 0; k < 22; ++k) {
+      double sum = 0;
+      for (int64_t c = 0; c < mtiles * splits; ++c) sum += double(h[size_t(c * 24 + k)]);
+      std::fprintf(stderr, "   %-18s %12.0f cycles/CTA\n", nm[k], sum / double(mtiles * splits));
+    }
+  }
   const int64_t n = box.I * K;
   launch(ctx, "splitk_reduce", [&] {
     splitk_reduce_f32_kernel<<<unsigned(cdiv(n, 256)), 256, 0, ctx.stream>>>(p.part, box.I, K, int(splits), Y, ldy);
@@ -697,8 +807,8 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
   return true;
 }
 
-bool ttm_t_tc(const Ctx& ctx, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
-              int64_t so_a, int64_t so_c, int64_t so_b) {
+bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
+              int64_t so_a, int64_t so_c, int64_t so_b, bool split_out) {
   const int npad = tc_npad(C);
   if (npad < 0) return false;
   const bool akm = (box.a == 1);
@@ -716,7 +826,13 @@ bool ttm_t_tc(const Ctx& ctx, const float* X, Box box, const float* Q, int64_t l
     const uint32_t bx[3] = {BM, KC, 1};
     if (!make_map(&tx, X, 3, d, s, bx, false)) return false;
   }
-  if (!make_b_map(&tb, Q, box.I, C, ldq, npad)) return false;
+  // pre-split [Q_hi | Q_lo] (I x 2 npad): the kernel loads it as one [2 npad][32] K-major slot
+  const int64_t ld2 = (box.I + 3) & ~int64_t(3);
+  float* Q2 = ws.alloc_n<float>(ld2 * 2 * npad);
+  if (!make_b_map(&tb, Q2, box.I, 2 * npad, ld2, 2 * npad)) return false;
+  launch(ctx, "split_q", [&] {
+    split_q_kernel<<<unsigned(cdiv(ld2 * npad, 256)), 256, 0, ctx.stream>>>(Q, box.I, C, ldq, npad, Q2, ld2);
+  });
   TParams p;
   p.a = box.a; p.I = box.I; p.b = box.b; p.C = C;
   p.tpb = akm ? 1 : cdiv(box.a, BM);
@@ -725,6 +841,9 @@ bool ttm_t_tc(const Ctx& ctx, const float* X, Box box, const float* Q, int64_t l
   p.seg = std::max(1, ctx.tc_seg);
   p.out = out; p.so_a = so_a; p.so_c = so_c; p.so_b = so_b;
   p.vec4 = so_c == 1 && (so_a % 4) == 0 && (so_b % 4) == 0 && (C % 4) == 0 && aligned(out, 16);
+  p.split_out = split_out;
+  RT_REQUIRE(!split_out || (so_c == 1 && (so_a % 4) == 0 && (so_b % 4) == 0 && aligned(out, 16)), kEINVAL,
+             "split output needs 16-byte aligned row-major rows");
   const int64_t grid = std::min<int64_t>(p.ntiles, ctx.num_sms);
 #define RT_T_CASE(NP)                                                     \
   case NP:                                                                \
