@@ -59,15 +59,17 @@ struct Plan {
   static constexpr uint32_t kB = BMN ? uint32_t(NBX) * 4096u : uint32_t(NPAD) * KC * 4u;
   static constexpr uint32_t kBS = BSPLIT ? 2u * kB : kB;
   static constexpr int NI = BSPLIT ? 2 : (NPAD <= 96 ? 2 : 1);
-  static constexpr int NBUF = BSPLIT ? 1 : 2;
-  static constexpr uint32_t acc_cols = BSPLIT ? uint32_t(NH + 2 * NPAD) : uint32_t(2 * NI * NPAD);
+  // single-buffered accumulators: the dedicated epilogue warps drain a segment in a few hundred
+  // cycles, and the TMEM saved buys A slots (a deeper splitter -> MMA ring)
+  static constexpr int NBUF = 1;
+  static constexpr uint32_t acc_cols = BSPLIT ? uint32_t(NH + 2 * NPAD) : uint32_t(NI * NPAD);
   static constexpr uint32_t a_base = (acc_cols + 63u) & ~63u;
   static constexpr int NB_fit = int((512u - a_base) / 64u);
-  static constexpr int NB = NB_fit > 4 ? 4 : NB_fit;
+  static constexpr int NB = NB_fit > 6 ? 6 : NB_fit;
   static_assert(NB >= 2, "TMEM plan leaves fewer than two A slots");
   static_assert(!BSPLIT || NH + NPAD <= 256, "concatenated B operand wider than 256");
   __host__ __device__ static constexpr uint32_t acc(int q, int b) {
-    return BSPLIT ? (q == 0 ? 0u : uint32_t(NH + NPAD)) : uint32_t((2 * q + b) * NPAD);
+    return BSPLIT ? (q == 0 ? 0u : uint32_t(NH + NPAD)) : uint32_t((NBUF * q + b) * NPAD);
   }
   __host__ __device__ static constexpr uint32_t a_slot(int s) { return a_base + 64u * uint32_t(s); }
   // shared memory
@@ -79,7 +81,7 @@ struct Plan {
   static constexpr uint32_t off_x = 0;
   static constexpr uint32_t off_b = off_x + NX * kX;
   static constexpr uint32_t off_bar = off_b + NBS * kBS;
-  static constexpr int nbar = 2 * NX + 2 * NBS + 2 * 4 + 4;
+  static constexpr int nbar = 2 * NX + 2 * NBS + 2 * 8 + 4;
   static constexpr uint32_t bytes = off_bar + 8 * nbar + 16;
   static_assert(NX >= 4, "X ring too shallow");
 };
@@ -98,8 +100,8 @@ __device__ __forceinline__ Bars bars_of(uint8_t* smem) {
   r.b_full = b + 2 * L::NX;
   r.b_free = b + 2 * L::NX + L::NBS;
   r.ready = b + 2 * L::NX + 2 * L::NBS;
-  r.tfree = b + 2 * L::NX + 2 * L::NBS + 4;
-  r.acc_full = b + 2 * L::NX + 2 * L::NBS + 2 * 4;
+  r.tfree = b + 2 * L::NX + 2 * L::NBS + 8;
+  r.acc_full = b + 2 * L::NX + 2 * L::NBS + 2 * 8;
   r.acc_empty = r.acc_full + 2;
   r.tmem_slot = reinterpret_cast<uint32_t*>(b + L::nbar);
   return r;
