@@ -194,8 +194,11 @@ rt_status rt_set_option(rt_handle* h, rt_option opt, int64_t value) {
     case RT_OPT_PROFILE: h->prof.enabled = value != 0; return RT_OK;
     case RT_OPT_QR_FALLBACK: return RT_OK;
     case RT_OPT_OMEGA_TF32: h->ctx.omega_tf32 = int(value != 0); return RT_OK;
-    case RT_OPT_TC_SEGMENT: h->ctx.tc_seg = int(value > 0 ? value : 8); return RT_OK;
-    case RT_OPT_TC_ABLATE: h->ctx.tc_ablate = int(value); return RT_OK;
+    case RT_OPT_TC_SEGMENT: h->ctx.tc_seg = int(value > 0 ? value : 16); return RT_OK;
+    case RT_OPT_TC_ABLATE:
+      if (value == 200 || value == 201) { h->ctx.tc_presplit_z = int(value == 201); return RT_OK; }
+      h->ctx.tc_ablate = int(value);
+      return RT_OK;
     case RT_OPT_TC_SKEW: h->ctx.tc_skew = int(value); return RT_OK;
   }
   return fail(h, RT_EINVAL, "unknown option");

@@ -67,10 +67,11 @@ struct Ctx {
   int num_sms = 148;
   int ttm_impl = 0;             // 0 auto, 1 SIMT, 2 tcgen05 (error if unavailable)
   int omega_tf32 = 0;           // caller asserts Gaussian Omega entries are tf32-representable
-  int tc_seg = 8;               // tcgen05: 32-element chunks per TMEM accumulator segment (drained to fp32 regs)
+  int tc_seg = 16;              // tcgen05: 32-element chunks per TMEM accumulator segment (drained to fp32 regs)
   int tc_ablate = 0;            // profiling only (RT_OPT_TC_ABLATE): 1 no MMA, 2 no split; results invalid
   int tc_skew = -1;             // ttm_s_tc: chunk-order rotation per M-tile (-1 = default)
   mutable const char* label = nullptr;   // profiler name override for the next TC launches
+  int tc_presplit_z = 0;        // power iteration: write Z R^-1 pre-split [hi | lo] (ablation 200 toggles)
 };
 
 // Launch a kernel (given as a lambda issuing <<<...>>> on ctx.stream) with optional

@@ -284,7 +284,10 @@ __global__ void __launch_bounds__(512) jacobi_kernel(EigBatch bt, double* Vscrat
     off = block_sum(off, red);
     __syncthreads();
     dia = block_sum(dia, red);
-    if (t == 0) s_done = (off <= 1e-30 * dia) || (dia == 0.0);
+    // converged when ||offdiag||_F <= k u ||diag||_F (u = 2^-53): below this the rotations only
+    // shuffle rounding noise
+    const double tol = double(k) * 1.1102230246251565e-16;
+    if (t == 0) s_done = (off <= tol * tol * dia) || (dia == 0.0);
     __syncthreads();
     if (s_done) break;
     for (int round = 0; round < kk - 1; ++round) {

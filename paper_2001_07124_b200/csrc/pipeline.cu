@@ -218,7 +218,7 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
   T* Z2 = nullptr;
   int64_t ldz2 = 0;
   if constexpr (std::is_same<T, float>::value) {
-    if (ttm_s_tc_ok(ctx, data, bx, K) && ldz == K) {
+    if (ctx.tc_presplit_z && ttm_s_tc_ok(ctx, data, bx, K) && ldz == K) {
       ldz2 = 2 * int64_t(tc_split_width(K));
       Z2 = ws.alloc_n<T>(Jl * ldz2);
     }
@@ -275,6 +275,7 @@ void Engine::core(const TView& X, const T* data, const double* const* Qt, const 
     const Box b = TView::box_of(cur, N, n);
     const int64_t ld = ldt[n];
     if (n == N - 1) {
+      LabelScope ls(ctx, "core_last_simt");
       ttm_t<T, T, double>(ctx, src, b, QT[n], 1, ld, int(K[n]), Gt, 1, b.a, b.a * K[n]);
     } else {
       T* dst = ws.alloc_n<T>(b.a * K[n] * b.b);
@@ -336,6 +337,7 @@ void Engine::truncate(const TView& X, const double* Gt, const int64_t* K, const 
   for (int n = 0; n < N; ++n) {
     const Box b = TView::box_of(cur, N, n);
     double* dst = (n == N - 1) ? G_out : ws.alloc_n<double>(b.a * R[n] * b.b);
+    LabelScope ls(ctx, "trunc_simt");
     ttm_t<double, double, double>(ctx, src, b, V[n], 1, K[n], int(R[n]), dst, 1, b.a, b.a * R[n]);
     src = dst;
     cur[n] = R[n];
@@ -363,6 +365,7 @@ void Engine::rel_error(const TView& X, const T* data, const double* G, const int
   for (int n = 0; n < N - 1; ++n) {
     const Box b = TView::box_of(cur, N, n);
     const int64_t In = X.d[n];
+    LabelScope ls(ctx, "pchain_simt");
     if (n == N - 2) {
       P = ws.alloc_n<T>(b.a * In * b.b);
       ttm_t<double, double, T>(ctx, src, b, Q[n], In, 1, int(In), P, 1, b.a, b.a * In);

@@ -265,7 +265,7 @@ void launch_ttm_t(const Ctx& ctx, const Tin* X, Box box, const Tm* Mm, int64_t m
   const int64_t J = box.J();
   const dim3 grid((unsigned)cdiv(J, 128), (unsigned)cdiv(C, 8 * TN));
   RT_REQUIRE(grid.x < (1u << 31) && grid.y < 65536, kEUNSUPPORTED, "ttm_t grid too large");
-  launch(ctx, "ttm_t_simt", [&] {
+  launch(ctx, ctx.label ? ctx.label : "ttm_t_simt", [&] {
     ttm_t_kernel<Tin, Tm, Tout, TN><<<grid, 256, 0, ctx.stream>>>(X, box.a, box.I, J, Mm, ms_i, ms_c, C,
                                                                   out, so_a, so_c, so_b);
   });

@@ -75,7 +75,9 @@ struct Plan {
   // shared memory
   static constexpr uint32_t kX = uint32_t(BM) * KC * 4;
   static constexpr uint32_t budget = 224u * 1024u;
-  static constexpr int NBS = BSPLIT ? (kBS <= 24u * 1024u ? 6 : 4) : (NPAD <= 96 ? 8 : 4);
+  // One stage = one A slot + one B slot, released together by a single tcgen05.commit per issuer
+  // (every commit stalls the issuing warp's MMA stream, so there is one per stage).
+  static constexpr int NBS = NB;
   static constexpr int NX_fit = int((budget - NBS * kBS) / kX);
   static constexpr int NX = NX_fit > 10 ? 10 : NX_fit;
   static constexpr uint32_t off_x = 0;
@@ -98,7 +100,7 @@ __device__ __forceinline__ Bars bars_of(uint8_t* smem) {
   r.x_full = b;
   r.x_free = b + L::NX;
   r.b_full = b + 2 * L::NX;
-  r.b_free = b + 2 * L::NX + L::NBS;
+  r.b_free = b + 2 * L::NX + 2 * L::NBS + 8;   // == tfree: a stage's A and B slots are released together
   r.ready = b + 2 * L::NX + 2 * L::NBS;
   r.tfree = b + 2 * L::NX + 2 * L::NBS + 8;
   r.acc_full = b + 2 * L::NX + 2 * L::NBS + 2 * 8;
@@ -110,7 +112,7 @@ __device__ __forceinline__ Bars bars_of(uint8_t* smem) {
 template <class L>
 __device__ __forceinline__ void init_bars(const Bars& b) {
   for (int s = 0; s < L::NX; ++s) { mbar_init(&b.x_full[s], 1); mbar_init(&b.x_free[s], 128); }
-  for (int s = 0; s < L::NBS; ++s) { mbar_init(&b.b_full[s], 1); mbar_init(&b.b_free[s], L::NI); }
+  for (int s = 0; s < L::NBS; ++s) mbar_init(&b.b_full[s], 1);
   for (int s = 0; s < L::NB; ++s) { mbar_init(&b.ready[s], 128); mbar_init(&b.tfree[s], L::NI); }
   for (int k = 0; k < 2; ++k) { mbar_init(&b.acc_full[k], L::NI); mbar_init(&b.acc_empty[k], 128); }
   fence_barrier_init();
@@ -365,18 +367,14 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
         const bool first = pos == 0;
         const bool last = (pos == p.seg - 1) || (it == nch - 1);
         if (first) RT_TIMED(tim, 2 + 4 * q, wait_acc_free<L>(b, u));
-        RT_TIMED(tim, 3 + 4 * q, mbar_wait(&b.ready[rt.s], rt.ph));
-        if (!BSPLIT || BPRE) RT_TIMED(tim, 4 + 4 * q, mbar_wait(&b.b_full[rb.s], rb.ph));
+        RT_TIMED(tim, 3 + 4 * q, mbar_wait(&b.ready[rt.s], rt.ph));   // A split and B landed
         RT_TIMED(tim, 20 + q, tc_fence_after());
         RT_TIMED(tim, 5 + 4 * q, {
           if (p.ablate != 1)
             issue_stage<L, BSPLIT, true>(tmem, q, acc_buf<L>(u), L::a_slot(rt.s),
                                          smem_u32(smem + L::off_b + rb.s * L::kBS), idesc0, idesc1, first);
         });
-        RT_TIMED(tim, 16 + q, {
-          mma_commit_w(&b.tfree[rt.s]);
-          mma_commit_w(&b.b_free[rb.s]);
-        });
+        RT_TIMED(tim, 16 + q, mma_commit_w(&b.tfree[rt.s]));
         if (last) { mma_commit_w(&b.acc_full[acc_buf<L>(u)]); ++u; pos = 0; } else { ++pos; }
       }
       if (tim && lane == 0)
@@ -399,8 +397,8 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
                                  lane_base + L::a_slot(rt.s));
       });
       mbar_arrive(&b.x_free[rx.s]);
+      RT_TIMED(tim, 13, mbar_wait(&b.b_full[rb.s], rb.ph));
       if (BSPLIT && !BPRE) {
-        RT_TIMED(tim, 13, mbar_wait(&b.b_full[rb.s], rb.ph));
         float* bs = reinterpret_cast<float*>(smem + L::off_b + rb.s * L::kBS);
         split_b<L::kB>(bs, bs + L::kB / 4, t);
       }
@@ -518,13 +516,11 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
           const bool first = pos == 0;
           const bool last = (pos == p.seg - 1) || (c == p.nic - 1);
           if (first) wait_acc_free<L>(b, g);
-          mbar_wait(&b.ready[rt.s], rt.ph);
-          mbar_wait(&b.b_full[rb.s], rb.ph);
+          mbar_wait(&b.ready[rt.s], rt.ph);                // A split and B landed
           tc_fence_after();
           issue_stage<L, BSPLIT, false>(tmem, q, acc_buf<L>(g), L::a_slot(rt.s),
                                         smem_u32(smem + L::off_b + rb.s * L::kBS), idesc0, idesc1, first);
           mma_commit_w(&b.tfree[rt.s]);
-          mma_commit_w(&b.b_free[rb.s]);
           if (last) { mma_commit_w(&b.acc_full[acc_buf<L>(g)]); ++g; pos = 0; } else { ++pos; }
         }
       }
@@ -542,6 +538,7 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
         split_row_to_tmem<!AKM>(reinterpret_cast<const float*>(smem + L::off_x + rx.s * L::kX), r,
                                 lane_base + L::a_slot(rt.s));
         mbar_arrive(&b.x_free[rx.s]);
+        mbar_wait(&b.b_full[rt.s], rt.ph);
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&b.ready[rt.s]);
@@ -913,7 +910,10 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constan
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2 * RNS + 8);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t my_tiles = (p.ntiles > blockIdx.x) ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  constexpr uint32_t kA = 2 * RNB;             // TMEM: acc at 0 / RNB, A hi at 128, A lo at 128 + RP
+  // TMEM: accumulator buffers at 0 / 2 RNB, each [hi.hi | hi.lo + lo.hi] (2 RNB columns: the B
+  // operand of the wide MMA is the concatenated [Q_hi | Q_lo] chunk); A hi at kA, A lo at kA + RP
+  constexpr uint32_t kAcc = 2 * RNB;
+  constexpr uint32_t kA = 2 * kAcc;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < RNS; ++s) { mbar_init(&st_full[s], 1); mbar_init(&st_free[s], 128); }
@@ -945,45 +945,42 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constan
           if (it >= RNS) mbar_wait(&st_free[rg.s], rg.ph ^ 1);
           uint8_t* st = smem + L::off_st + rg.s * L::per_stage;
           mbar_expect_tx(&st_full[rg.s], L::per_stage);
-          for (int c = 0; c < NCH; ++c) {
-            tma_load_2d(st + c * L::kQ, &tqh, &st_full[rg.s], c * KC, b * RNB);
-            tma_load_2d(st + (NCH + c) * L::kQ, &tql, &st_full[rg.s], c * KC, b * RNB);
+          for (int c = 0; c < NCH; ++c) {      // [Q_hi c | Q_lo c] adjacent: one N = 2 RNB operand
+            tma_load_2d(st + (2 * c) * L::kQ, &tqh, &st_full[rg.s], c * KC, b * RNB);
+            tma_load_2d(st + (2 * c + 1) * L::kQ, &tql, &st_full[rg.s], c * KC, b * RNB);
           }
           tma_load_2d(st + 2 * NCH * L::kQ, &tmx, &st_full[rg.s], j0, b * RNB);
         }
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {                                   // ---------------- MMA issuer
-      const uint32_t idesc = idesc_tf32(BM, RNB, 0);
-      Ring rg;
-      int64_t g = 0;
-      for (int64_t u = 0; u < my_tiles; ++u) {
-        mbar_wait(a_ready, uint32_t(u) & 1);
+  } else if (warp == 1) {                             // ---------------- MMA issuer (whole warp)
+    const uint32_t idesc_w = idesc_tf32(BM, 2 * RNB, 0);   // A_hi [Q_hi | Q_lo]
+    const uint32_t idesc_n = idesc_tf32(BM, RNB, 0);       // A_lo Q_hi -> correction columns
+    Ring rg;
+    int64_t g = 0;
+    for (int64_t u = 0; u < my_tiles; ++u) {
+      mbar_wait(a_ready, uint32_t(u) & 1);
+      tc_fence_after();
+      for (int b = 0; b < p.nblk; ++b, ++g, rg.next<RNS>()) {
+        const int ab = int(g & 1);
+        if (g >= 2) mbar_wait(&acc_empty[ab], uint32_t((g >> 1) - 1) & 1);
+        mbar_wait(&st_full[rg.s], rg.ph);
         tc_fence_after();
-        for (int b = 0; b < p.nblk; ++b, ++g, rg.next<RNS>()) {
-          const int ab = int(g & 1);
-          if (g >= 2) mbar_wait(&acc_empty[ab], uint32_t((g >> 1) - 1) & 1);
-          mbar_wait(&st_full[rg.s], rg.ph);
-          tc_fence_after();
-          const uint32_t st = smem_u32(smem + L::off_st + rg.s * L::per_stage);
-          const uint32_t acc = tmem + uint32_t(ab) * RNB;
+        const uint32_t st = smem_u32(smem + L::off_st + rg.s * L::per_stage);
+        const uint32_t acc = tmem + uint32_t(ab) * kAcc;
 #pragma unroll
-          for (int c = 0; c < NCH; ++c)
+        for (int c = 0; c < NCH; ++c)
 #pragma unroll
-            for (int kk = 0; kk < KC / 8; ++kk) {
-              const uint32_t a_hi = tmem + kA + c * KC + 8 * kk;
-              const uint32_t a_lo = a_hi + RP;
-              const uint64_t bh = bdesc_sw128(st + c * L::kQ, kk);
-              const uint64_t bl = bdesc_sw128(st + (NCH + c) * L::kQ, kk);
-              mma_tf32_ts(acc, a_hi, bh, idesc, (c == 0 && kk == 0) ? 0u : 1u);
-              mma_tf32_ts(acc, a_lo, bh, idesc, 1u);
-              mma_tf32_ts(acc, a_hi, bl, idesc, 1u);
-            }
-          mma_commit(&acc_full[ab]);
-        }
-        mma_commit(a_free);
+          for (int kk = 0; kk < KC / 8; ++kk) {
+            const uint32_t a_hi = tmem + kA + c * KC + 8 * kk;
+            const uint32_t a_lo = a_hi + RP;
+            const uint64_t bq = bdesc_sw128(st + (2 * c) * L::kQ, kk);
+            mma_tf32_ts_w(acc, a_hi, bq, idesc_w, (c == 0 && kk == 0) ? 0u : 1u);
+            mma_tf32_ts_w(acc + RNB, a_lo, bq, idesc_n, 1u);
+          }
+        mma_commit_w(&acc_full[ab]);
       }
+      mma_commit_w(a_free);
     }
   } else {                                             // ---------------- split A / epilogue
     const int q4 = warp & 3;
@@ -1020,13 +1017,14 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constan
         float tr = 0.f, tx = 0.f;
 #pragma unroll
         for (int cb = 0; cb < RNB / 16; ++cb) {
-          uint32_t v[16];
-          tmem_ld16(lane_base + uint32_t(ab) * RNB + 16 * cb, v);
+          uint32_t v[16], w[16];
+          tmem_ld16(lane_base + uint32_t(ab) * kAcc + 16 * cb, v);           // A_hi Q_hi
+          tmem_ld16(lane_base + uint32_t(ab) * kAcc + RNB + 16 * cb, w);     // A_hi Q_lo + A_lo Q_hi
           tmem_wait_ld();
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
             const float x = xt[(16 * cb + q) * BM + r];
-            const float d = x - __uint_as_float(v[q]);
+            const float d = x - (__uint_as_float(v[q]) + __uint_as_float(w[q]));
             tr = fmaf(d, d, tr);
             tx = fmaf(x, x, tx);
           }
