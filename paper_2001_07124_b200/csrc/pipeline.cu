@@ -368,7 +368,17 @@ void Engine::rel_error(const TView& X, const T* data, const double* G, const int
     LabelScope ls(ctx, "pchain_simt");
     if (n == N - 2) {
       P = ws.alloc_n<T>(b.a * In * b.b);
-      ttm_t<double, double, T>(ctx, src, b, Q[n], In, 1, int(In), P, 1, b.a, b.a * In);
+      if constexpr (std::is_same<T, float>::value) {
+        // the widest stage (|P| = |X| R_N / I_N outputs): fp32 operands and accumulation (P is
+        // consumed in fp32 by the residual kernel; R_n-term dot products)
+        float* sf = ws.alloc_n<float>(b.a * b.I * b.b);
+        float* qf = ws.alloc_n<float>(In * b.I);
+        convert2d<double, float>(ctx, src, b.a * b.I * b.b, 1, b.a * b.I * b.b, sf, b.a * b.I * b.b);
+        convert2d<double, float>(ctx, Q[n], In, b.I, In, qf, In);
+        ttm_t<float, float, float>(ctx, sf, b, qf, In, 1, int(In), P, 1, b.a, b.a * In);
+      } else {
+        ttm_t<double, double, T>(ctx, src, b, Q[n], In, 1, int(In), P, 1, b.a, b.a * In);
+      }
     } else {
       double* dst = ws.alloc_n<double>(b.a * In * b.b);
       ttm_t<double, double, double>(ctx, src, b, Q[n], In, 1, int(In), dst, 1, b.a, b.a * In);
