@@ -52,8 +52,23 @@ constexpr int NT_TTM = 384;      // TTM kernels: X producer, MMA issuer, 4 split
 // B tile: K-major [NPAD][32] (128 B rows, SWIZZLE_128B), or MN-major (row-major B in global
 // memory: Omega / Z) as ceil(NPAD/32) atom columns of [32 k-rows][32 n] (4 KB each,
 // SWIZZLE_128B_ATOM_32B); NH = N width of the hi part (MN-major: padded to 32).
+// chunks per stage for the sketch kernel: 2 when two 128-column A stages still fit next to the
+// accumulators, else 1
 template <int NPAD, bool BSPLIT, bool BMN>
+constexpr int sketch_cps() {
+  constexpr int nbx = (NPAD + 31) / 32, nh = BMN ? nbx * 32 : NPAD;
+  constexpr int ni = BSPLIT ? 2 : (NPAD <= 96 ? 2 : 1);
+  constexpr int acc = BSPLIT ? nh + 2 * NPAD : ni * NPAD;
+  constexpr int abase = (acc + 63) & ~63;
+  return (512 - abase) / 128 >= 2 ? 2 : 1;
+}
+
+template <int NPAD, bool BSPLIT, bool BMN, int CPS_ = 1>
 struct Plan {
+  // CPS chunks (of KC contraction elements) per pipeline stage: one ready wait, one commit and
+  // one A slot of 64 CPS columns per stage -- the issuer warps' per-stage overhead (barrier wait,
+  // commit, loop bookkeeping: ~450 cycles measured) is paid once per CPS chunks
+  static constexpr int CPS = CPS_;
   static constexpr int NBX = (NPAD + 31) / 32;
   static constexpr int NH = BMN ? NBX * 32 : NPAD;
   static constexpr uint32_t kB = BMN ? uint32_t(NBX) * 4096u : uint32_t(NPAD) * KC * 4u;
@@ -64,20 +79,20 @@ struct Plan {
   static constexpr int NBUF = 1;
   static constexpr uint32_t acc_cols = BSPLIT ? uint32_t(NH + 2 * NPAD) : uint32_t(NI * NPAD);
   static constexpr uint32_t a_base = (acc_cols + 63u) & ~63u;
-  static constexpr int NB_fit = int((512u - a_base) / 64u);
-  static constexpr int NB = NB_fit > 6 ? 6 : NB_fit;
-  static_assert(NB >= 2, "TMEM plan leaves fewer than two A slots");
+  static constexpr int NB_fit = int((512u - a_base) / (64u * CPS));
+  static constexpr int NB = NB_fit > 6 ? 6 : NB_fit;   // stages in the TMEM A ring
+  static_assert(NB >= 2, "TMEM plan leaves fewer than two A stages");
   static_assert(!BSPLIT || NH + NPAD <= 256, "concatenated B operand wider than 256");
   __host__ __device__ static constexpr uint32_t acc(int q, int b) {
     return BSPLIT ? (q == 0 ? 0u : uint32_t(NH + NPAD)) : uint32_t((NBUF * q + b) * NPAD);
   }
-  __host__ __device__ static constexpr uint32_t a_slot(int s) { return a_base + 64u * uint32_t(s); }
+  __host__ __device__ static constexpr uint32_t a_slot(int s) { return a_base + 64u * CPS * uint32_t(s); }
   // shared memory
   static constexpr uint32_t kX = uint32_t(BM) * KC * 4;
   static constexpr uint32_t budget = 224u * 1024u;
   // One stage = one A slot + one B slot, released together by a single tcgen05.commit per issuer
   // (every commit stalls the issuing warp's MMA stream, so there is one per stage).
-  static constexpr int NBS = NB;
+  static constexpr int NBS = NB * CPS;                  // B slots (one per chunk)
   static constexpr int NX_fit = int((budget - NBS * kBS) / kX);
   static constexpr int NX = NX_fit > 10 ? 10 : NX_fit;
   static constexpr uint32_t off_x = 0;
@@ -267,9 +282,31 @@ struct SParams {
   int skew;           // chunk-order rotation per M-tile (decorrelates the rows' DRAM addresses)
   float* part;        // [split][K][I]
   unsigned long long* tim;   // diagnostics (RT_OPT_TC_ABLATE = 1000): per-CTA role wait cycles, else null
+  long long* trace;          // diagnostics (RT_OPT_TC_ABLATE = 2000): per-chunk event clocks of CTA (0,0)
 };
+#if RT_TC_DIAG
+#define RT_TRACE(p, it, k)                                                                         \
+  do {                                                                                             \
+    if ((p).trace && blockIdx.x == 0 && blockIdx.y == 0 && (it) < 512 && (threadIdx.x & 31) == 0) \
+      (p).trace[(it) * 8 + (k)] = clock64();                                                       \
+  } while (0)
+#else
+#define RT_TRACE(p, it, k) do { } while (0)
+#endif
 
 // diagnostics: accumulate the cycles spent in `body` into slot k of this CTA's timing record
+// RT_TC_DIAG=1 (make diag build) compiles the per-role timers / traces in; the normal build has
+// none of their instructions in the issue loops.
+#ifndef RT_TC_DIAG
+#define RT_TC_DIAG 0
+#endif
+#if !RT_TC_DIAG
+#define RT_TIMED(tim, k, ...) \
+  do {                        \
+    (void)(tim);              \
+    __VA_ARGS__;              \
+  } while (0)
+#else
 #define RT_TIMED(tim, k, ...)                                                                   \
   do {                                                                                           \
     if (tim) {                                                                                   \
@@ -281,6 +318,7 @@ struct SParams {
       __VA_ARGS__;                                                                               \
     }                                                                                            \
   } while (0)
+#endif
 
 // chunk c -> X tile coordinates and first B row j0
 template <bool AMN>
@@ -298,8 +336,8 @@ template <int NPAD, bool BSPLIT, bool AMN, bool BPRE>
 __global__ void __launch_bounds__(NT_TTM, 1)
 ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb, const SParams p) {
   static_assert(!BPRE || BSPLIT, "pre-split B implies the split product form");
-  using L = Plan<NPAD, BSPLIT, true>;
-  constexpr int NX = L::NX;
+  using L = Plan<NPAD, BSPLIT, true, sketch_cps<NPAD, BSPLIT, true>()>;
+  constexpr int NX = L::NX, CPS = L::CPS, NB = L::NB;
   extern __shared__ __align__(1024) uint8_t smem[];
   const Bars b = bars_of<L>(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -310,8 +348,12 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
   const int64_t per = (p.nchunks + S - 1) / S;
   const int64_t cbeg = z * per;
   const int nch = cbeg < p.nchunks ? int(min(per, p.nchunks - cbeg)) : 0;
+  const int nst = (nch + CPS - 1) / CPS;               // stages
   const int rot = nch ? int((int64_t(blockIdx.x) * p.skew) % nch) : 0;
   auto chunk_of = [&](int it) { int c = it + rot; return cbeg + (c >= nch ? c - nch : c); };
+  // stage g -> ring slot and round parity
+  auto st_slot = [](int g) { return g % NB; };
+  auto st_par = [](int g) { return uint32_t(g / NB) & 1u; };
 
   if (threadIdx.x == 0) {
     init_bars<L>(b);
@@ -339,18 +381,18 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
       }
     }
   } else if (warp == 6) {
-    if (lane == 0) {                                   // ---------------- B producer (hi tile)
-      Ring rb;
+    if (lane == 0) {                                   // ---------------- B producer (one slot per chunk)
       const uint64_t pol = policy_evict_last();
-      for (int it = 0; it < nch; ++it, rb.next<L::NBS>()) {
-        if (it >= L::NBS) RT_TIMED(p.tim, 1, mbar_wait(&b.b_free[rb.s], rb.ph ^ 1));
+      for (int it = 0; it < nch; ++it) {
+        const int g = it / CPS, bs = it % L::NBS;
+        if (g >= NB) RT_TIMED(p.tim, 1, mbar_wait(&b.tfree[st_slot(g)], st_par(g) ^ 1));   // stage g - NB done
         int64_t a0, beta, j0;
         chunk_coords<AMN>(p, chunk_of(it), a0, beta, j0);
         constexpr int nbox = BPRE ? 2 * L::NBX : L::NBX;
-        mbar_expect_tx(&b.b_full[rb.s], nbox * 4096);
+        mbar_expect_tx(&b.b_full[bs], nbox * 4096);
 #pragma unroll
         for (int x = 0; x < nbox; ++x)
-          tma_load_2d_hint(smem + L::off_b + rb.s * L::kBS + x * 4096, &tmb, &b.b_full[rb.s], 32 * x, int(j0), pol);
+          tma_load_2d_hint(smem + L::off_b + bs * L::kBS + x * 4096, &tmb, &b.b_full[bs], 32 * x, int(j0), pol);
       }
     }
   } else if (warp == 1 || warp == 7) {
@@ -359,26 +401,30 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
       unsigned long long* tim = p.tim;
       const uint32_t idesc0 = idesc_tf32(BM, BSPLIT ? L::NH + NPAD : NPAD, 1);
       const uint32_t idesc1 = idesc_tf32(BM, NPAD, 1);
-      Ring rt, rb;
+      const int spg = (p.seg + CPS - 1) / CPS;        // stages per accumulator segment
       int64_t u = 0;
       int pos = 0;
-      const long long tl0 = clock64();
-      for (int it = 0; it < nch; ++it, rt.next<L::NB>(), rb.next<L::NBS>()) {
+      for (int g = 0; g < nst; ++g) {
         const bool first = pos == 0;
-        const bool last = (pos == p.seg - 1) || (it == nch - 1);
+        const bool last = (pos == spg - 1) || (g == nst - 1);
+        const int sl = st_slot(g);
         if (first) RT_TIMED(tim, 2 + 4 * q, wait_acc_free<L>(b, u));
-        RT_TIMED(tim, 3 + 4 * q, mbar_wait(&b.ready[rt.s], rt.ph));   // A split and B landed
-        RT_TIMED(tim, 20 + q, tc_fence_after());
-        RT_TIMED(tim, 5 + 4 * q, {
-          if (p.ablate != 1)
-            issue_stage<L, BSPLIT, true>(tmem, q, acc_buf<L>(u), L::a_slot(rt.s),
-                                         smem_u32(smem + L::off_b + rb.s * L::kBS), idesc0, idesc1, first);
-        });
-        RT_TIMED(tim, 16 + q, mma_commit_w(&b.tfree[rt.s]));
+        RT_TIMED(tim, 3 + 4 * q, mbar_wait(&b.ready[sl], st_par(g)));   // A split and B landed
+        RT_TRACE(p, g, 3 + 2 * q);
+        tc_fence_after();
+        const int c0 = g * CPS;
+        const int cn = (nch - c0) < CPS ? (nch - c0) : CPS;
+#pragma unroll
+        for (int c = 0; c < CPS; ++c) {
+          if (c < cn && p.ablate != 1)
+            issue_stage<L, BSPLIT, true>(tmem, q, acc_buf<L>(u), L::a_slot(sl) + 64u * c,
+                                         smem_u32(smem + L::off_b + ((c0 + c) % L::NBS) * L::kBS), idesc0, idesc1,
+                                         first && c == 0);
+        }
+        mma_commit_w(&b.tfree[sl]);
+        RT_TRACE(p, g, 4 + 2 * q);
         if (last) { mma_commit_w(&b.acc_full[acc_buf<L>(u)]); ++u; pos = 0; } else { ++pos; }
       }
-      if (tim && lane == 0)
-        atomicAdd(&tim[(blockIdx.y * gridDim.x + blockIdx.x) * 24 + 18 + q], (unsigned long long)(clock64() - tl0));
     }
   } else if (warp >= 2 && warp <= 5) {                 // ---------------- splitters
     const int q4 = warp & 3;
@@ -386,29 +432,29 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
     const uint32_t lane_base = tmem + (uint32_t(32 * q4) << 16);
     const int t = threadIdx.x - 64;
     unsigned long long* tim = (warp == 2) ? p.tim : nullptr;   // warp-uniform (aligned tcgen05 ops inside)
-    const long long tstart = clock64();
-    Ring rx, rt, rb;
-    for (int it = 0; it < nch; ++it, rx.next<NX>(), rt.next<L::NB>(), rb.next<L::NBS>()) {
+    Ring rx;
+    for (int it = 0; it < nch; ++it, rx.next<NX>()) {
+      const int g = it / CPS, c = it % CPS, sl = st_slot(g), bs = it % L::NBS;
       RT_TIMED(tim, 10, mbar_wait(&b.x_full[rx.s], rx.ph));
-      if (it >= L::NB) RT_TIMED(tim, 11, mbar_wait(&b.tfree[rt.s], rt.ph ^ 1));   // TMEM slot free
+      if (c == 0 && g >= NB) RT_TIMED(tim, 11, mbar_wait(&b.tfree[sl], st_par(g) ^ 1));   // stage's TMEM slot free
       RT_TIMED(tim, 12, {
         if (p.ablate != 2)
           split_row_to_tmem<AMN>(reinterpret_cast<const float*>(smem + L::off_x + rx.s * L::kX), r,
-                                 lane_base + L::a_slot(rt.s));
+                                 lane_base + L::a_slot(sl) + 64u * c);
       });
       mbar_arrive(&b.x_free[rx.s]);
-      RT_TIMED(tim, 13, mbar_wait(&b.b_full[rb.s], rb.ph));
+      RT_TIMED(tim, 13, mbar_wait(&b.b_full[bs], uint32_t(it / L::NBS) & 1u));
       if (BSPLIT && !BPRE) {
-        float* bs = reinterpret_cast<float*>(smem + L::off_b + rb.s * L::kBS);
-        split_b<L::kB>(bs, bs + L::kB / 4, t);
+        float* bsp = reinterpret_cast<float*>(smem + L::off_b + bs * L::kBS);
+        split_b<L::kB>(bsp, bsp + L::kB / 4, t);
       }
-      tmem_wait_st();
-      if (BSPLIT && !BPRE) fence_proxy_async();
-      tc_fence_before();
-      mbar_arrive(&b.ready[rt.s]);
+      if (c == CPS - 1 || it == nch - 1) {             // stage complete
+        tmem_wait_st();
+        if (BSPLIT && !BPRE) fence_proxy_async();
+        tc_fence_before();
+        mbar_arrive(&b.ready[sl]);
+      }
     }
-    if (tim && lane == 0)
-      atomicAdd(&tim[(blockIdx.y * gridDim.x + blockIdx.x) * 24 + 15], (unsigned long long)(clock64() - tstart));
   } else if (warp >= 8) {                              // ---------------- epilogue: drain segments
     const int q4 = warp & 3;
     const int r = 32 * q4 + lane;
@@ -417,7 +463,8 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
     float sums[NPAD];
 #pragma unroll
     for (int k = 0; k < NPAD; ++k) sums[k] = 0.f;
-    const int64_t nseg = (nch + p.seg - 1) / p.seg;
+    const int spg = (p.seg + CPS - 1) / CPS;
+    const int64_t nseg = (nst + spg - 1) / spg;
     for (int64_t u = 0; u < nseg; ++u) RT_TIMED(tim, 14, drain_acc<L, NPAD, BSPLIT>(b, lane_base, u, sums));
     const int64_t i = i0 + r;                         // partial tile -> part[split][k][i]
     if (i < p.I) {
@@ -660,7 +707,7 @@ void set_smem(Kern kernel, uint32_t bytes) {
 
 template <int NPAD, bool BSPLIT, bool AMN, bool BPRE>
 void launch_s(const Ctx& ctx, const CUtensorMap& tx, const CUtensorMap& tb, const SParams& p, dim3 grid) {
-  using L = Plan<NPAD, BSPLIT, true>;
+  using L = Plan<NPAD, BSPLIT, true, sketch_cps<NPAD, BSPLIT, true>()>;
   static bool attr = false;
   if (!attr) { set_smem(ttm_s_tc_kernel<NPAD, BSPLIT, AMN, BPRE>, L::bytes); attr = true; }
   launch(ctx, ctx.label ? ctx.label : "ttm_s_tc", [&] {
@@ -767,7 +814,12 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
   p.skew = ctx.tc_skew >= 0 ? ctx.tc_skew : 0;
   p.part = ws.alloc_n<float>(splits * K * box.I);
   p.tim = nullptr;
+  p.trace = nullptr;
   const dim3 grid{unsigned(mtiles), unsigned(splits), 1u};
+  if (ctx.tc_ablate == 2000) {
+    p.trace = ws.alloc_n<long long>(512 * 8);
+    RT_CUDA(cudaMemsetAsync(p.trace, 0, sizeof(long long) * 512 * 8, ctx.stream));
+  }
   if (ctx.tc_ablate == 1000) {
     p.tim = ws.alloc_n<unsigned long long>(mtiles * splits * 24);
     RT_CUDA(cudaMemsetAsync(p.tim, 0, sizeof(unsigned long long) * mtiles * splits * 24, ctx.stream));
@@ -782,6 +834,19 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
     default: return false;
   }
 #undef RT_S_CASE
+  if (p.trace) {   // diagnostics: event clocks of chunks 200..231 of CTA (0,0), relative to chunk 200 start
+    std::vector<long long> h(512 * 8);
+    RT_CUDA(cudaMemcpyAsync(h.data(), p.trace, h.size() * 8, cudaMemcpyDeviceToHost, ctx.stream));
+    RT_CUDA(cudaStreamSynchronize(ctx.stream));
+    const long long t0 = h[200 * 8 + 0];
+    std::fprintf(stderr, "[ttm_s_tc trace] %s bmode=%d: it  x_full  slot  ready | iss0 go  done | iss1 go  done | drain\n",
+                 ctx.label ? ctx.label : "ttm_s_tc", bmode);
+    for (int it = 200; it < 232; ++it) {
+      std::fprintf(stderr, "   %3d", it);
+      for (int e = 0; e < 8; ++e) std::fprintf(stderr, " %7lld", h[it * 8 + e] ? h[it * 8 + e] - t0 : -1LL);
+      std::fprintf(stderr, "\n");
+    }
+  }
   if (p.tim) {   // diagnostics: mean cycles per CTA spent in each role's waits / work
     std::vector<unsigned long long> h(size_t(mtiles * splits * 24));
     RT_CUDA(cudaMemcpyAsync(h.data(), p.tim, h.size() * 8, cudaMemcpyDeviceToHost, ctx.stream));
