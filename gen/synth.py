@@ -39,7 +39,7 @@ import numpy as np
 BASE_SEED = 2001_07124
 
 # object ids inside the seed tuple
-_OBJ_CORE, _OBJ_FACTOR, _OBJ_NOISE, _OBJ_OMEGA, _OBJ_KRON = 1, 2, 3, 4, 5
+_OBJ_CORE, _OBJ_FACTOR, _OBJ_NOISE, _OBJ_OMEGA, _OBJ_KRON, _OBJ_OMEGA_TILDE = 1, 2, 3, 4, 5, 6
 
 
 def rng_for(*key: int) -> np.random.Generator:
@@ -178,6 +178,19 @@ def gaussian_omega(cfg: Config, n: int, K: Optional[int] = None, rows: Optional[
     if tf32 and cfg.dtype == "f32":
         return np.ascontiguousarray(round_tf32(om))
     return np.ascontiguousarray(om.astype(cfg.np_dtype))
+
+
+def pet_sizes(cfg: Config, K: Optional[Sequence[int]] = None) -> tuple:
+    """R-PET sketch sizes (Alg.9): K_n = min(R_n + p, I_n, J_n) and S_n = min(2 K_n + 1, I_n)."""
+    ks = [cfg.K(n) for n in range(cfg.order)] if K is None else list(K)
+    ss = [min(2 * k + 1, cfg.dims[n]) for n, k in enumerate(ks)]
+    return ks, ss
+
+
+def omega_tilde(cfg: Config, n: int, S: int) -> np.ndarray:
+    """Gaussian Omega~_n in R^{S_n x I_n} of R-PET line 3, dtype of the tensor."""
+    rng = rng_for(cfg.cfg_id, _OBJ_OMEGA_TILDE, n)
+    return np.ascontiguousarray(rng.standard_normal((S, cfg.dims[n])).astype(cfg.np_dtype))
 
 
 def round_tf32(a: np.ndarray) -> np.ndarray:

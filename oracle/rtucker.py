@@ -220,6 +220,37 @@ def sthosvd(x: np.ndarray, ranks: Sequence[int], omegas, q: int = 0, kind: str =
     return out
 
 
+def pet(x: np.ndarray, ranks: Sequence[int], omegas, omega_tildes, with_error: bool = True) -> dict:
+    """Alg.9 R-PET, the randomized pass-efficient Tucker algorithm:
+
+      Y_n = X_(n) Omega_n                     (line 1; Omega_n: J_n x K_n)
+      [Q^(n), ~] = QR(Y_n)                    (line 2; qr+ of reading R5)
+      H = X x_1 Omega~_1 x_2 ... x_N Omega~_N (line 3; Omega~_n: S_n x I_n, R_n <= K_n <= S_n)
+      S = H x_n (Omega~_n Q^(n))^dagger       (line 4; Moore-Penrose pseudo-inverse, numpy.linalg.pinv)
+      truncate S, Q^(n) to (R_1..R_N)         (line 5; reading R1: the small HOSVD of S, as in hosvd)
+
+    Every sketch of lines 1 and 3 reads X only (no product depends on another): one pass.
+    """
+    x64 = np.asarray(x, dtype=np.float64)
+    if fro(x64) == 0.0:
+        return _zero_result(x64.shape, ranks)
+    N = x64.ndim
+    y0s, qts = [], []
+    for n in range(N):
+        y0 = unfold(x64, n) @ np.asarray(omegas[n], dtype=np.float64)
+        qt, _ = qr_plus(y0)
+        y0s.append(y0)
+        qts.append(qt)
+    h = multi_ttm(x64, [np.asarray(o, dtype=np.float64) for o in omega_tildes])
+    s = multi_ttm(h, [np.linalg.pinv(np.asarray(o, dtype=np.float64) @ qt) for o, qt in zip(omega_tildes, qts)])
+    g, qs = truncate_hosvd(s, qts, ranks)
+    out = dict(Q=qs, G=g, Qt=qts, Gt=s, H=h, Y0=y0s)
+    if with_error:
+        out["E"] = rel_error(x64, g, qs)
+        out["E_gram"] = rel_error_gram(x64, g)
+    return out
+
+
 # ------------------------------------------------------ deterministic references
 def thosvd(x: np.ndarray, ranks: Sequence[int]) -> dict:
     """Deterministic truncated HOSVD via full SVD of each unfolding (Eq. UnfoldHOSVD
@@ -262,6 +293,6 @@ def hooi(x: np.ndarray, ranks: Sequence[int], iters: int = 50) -> dict:
     return dict(Q=qs, G=g, E=rel_error(x64, g, qs))
 
 
-__all__ = ["qr_plus", "sketch_gauss", "sketch_kron", "sketch", "core", "rel_error",
+__all__ = ["qr_plus", "sketch_gauss", "sketch_kron", "sketch", "core", "rel_error", "pet",
            "rel_error_gram", "eig_desc", "canon_sign", "truncate_hosvd", "hosvd", "sthosvd",
            "thosvd", "sthosvd_det", "hooi", "unfold", "fold", "ttm", "multi_ttm", "reconstruct", "fro"]

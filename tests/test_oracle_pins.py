@@ -436,3 +436,56 @@ def test_generators_deterministic_and_slab_consistent():
     om = synth.gaussian_omega(cfg, 1)
     part = synth.gaussian_omega(cfg, 1, rows=20, row0=13)
     assert np.array_equal(om[13:33], part)
+
+
+# ----------------------------------------------------------------- R-PET (Alg.9)
+def _lowrank(seed, dims, r):
+    rng = np.random.default_rng(seed)
+    g = rng.standard_normal((r,) * len(dims))
+    us = [np.linalg.qr(rng.standard_normal((d, r)))[0] for d in dims]
+    return oracle.reconstruct(g, us), us
+
+
+def test_P21_pet_exact_rank_recovery():
+    """Alg.9 with K = 2R, S = 2K + 1 recovers an exact multilinear-rank-R tensor."""
+    dims, r = (30, 28, 26), 4
+    x, us = _lowrank(21, dims, r)
+    rng = np.random.default_rng(22)
+    ks = [2 * r] * 3
+    ss = [2 * k + 1 for k in ks]
+    oms = [rng.standard_normal((x.size // d, k)) for d, k in zip(dims, ks)]
+    omt = [rng.standard_normal((s_, d)) for s_, d in zip(ss, dims)]
+    out = oracle.pet(x, (r,) * 3, oms, omt)
+    assert out["E"] < 1e-8
+    for n in range(3):
+        assert np.linalg.norm(out["Q"][n].T @ out["Q"][n] - np.eye(r)) < 1e-12
+        p = out["Q"][n] @ out["Q"][n].T
+        assert np.linalg.norm(p @ us[n] - us[n]) < 1e-8            # captured the true factor
+
+
+def test_P22_pet_core_recovery_inverts_the_core_sketch():
+    """Line 4: if X = C x_n Q_n (X inside span(Q)), S = H x_n (Omega~_n Q_n)^+ returns C exactly
+    (the pseudo-inverse of a full-column-rank Omega~_n Q_n is a left inverse)."""
+    dims, k = (12, 11, 10), 3
+    rng = np.random.default_rng(23)
+    c = rng.standard_normal((k, k, k))
+    qs = [np.linalg.qr(rng.standard_normal((d, k)))[0] for d in dims]
+    x = oracle.reconstruct(c, qs)
+    omt = [rng.standard_normal((2 * k + 1, d)) for d in dims]
+    h = oracle.multi_ttm(x, omt)
+    s = oracle.multi_ttm(h, [np.linalg.pinv(o @ q) for o, q in zip(omt, qs)])
+    assert np.linalg.norm(s - c) <= 1e-12 * np.linalg.norm(c)
+
+
+def test_P23_pet_identity_core_sketch_reduces_to_rp_hosvd():
+    """With Omega~_n = I_{I_n} (S_n = I_n) line 4 is S = X x_n Q_n^+ = X x_n Q_n^T (orthonormal
+    Q), the RP-HOSVD core of Alg.6: R-PET then equals hosvd() on the same Omega_n."""
+    cfg = synth.CONFIGS["cfg2"].scaled((20, 18, 16), (3, 3, 3), (3, 3, 3))
+    x = synth.make_tensor(cfg)
+    oms = [synth.gaussian_omega(cfg, n) for n in range(3)]
+    a = oracle.pet(x, cfg.ranks, oms, [np.eye(d) for d in cfg.dims])
+    b = oracle.hosvd(x, cfg.ranks, oms, q=0)
+    for n in range(3):
+        assert np.linalg.norm(a["Q"][n] - b["Q"][n]) < 1e-10
+    assert np.linalg.norm(a["G"] - b["G"]) < 1e-10 * np.linalg.norm(b["G"])
+    assert abs(a["E"] - b["E"]) < 1e-12
