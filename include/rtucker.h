@@ -179,6 +179,23 @@ rt_status rtucker_sthosvd(rt_handle* h, const rt_tensor* X, const int64_t* R, in
                           const int64_t* omega_ld, const int* mode_order, double* const* Q_out, double* G_out,
                           double* rel_err, double* rel_err_gram);
 
+/* (6) Randomized pass-efficient Tucker = Alg.9 R-PET (single-pass formulas P:224-233):
+ *       Y_n = X_(n) Omega_n, [Q^(n), ~] = QR(Y_n)                 (lines 1-2)
+ *       H = X x_1 Omega~_1 x_2 ... x_N Omega~_N                    (line 3)
+ *       S = H x_n (Omega~_n Q^(n))^+  (pseudo-inverse of the full-column-rank S_n x K_n matrix)
+ *       truncation of S, Q^(n) to (R_1..R_N) as in (4)             (line 5, reading R1)
+ *     Every sketch reads only X (the algorithm is single-pass; this implementation streams X once
+ *     per sketch).
+ * omega / omega_cols / omega_ld: Gaussian tables as in (4): entry [n*N+n] is Omega_n (J_n x K_n,
+ *   row-major), R_n <= K_n <= min(I_n, J_n).
+ * omega_tilde[n]: Omega~_n, S_n x I_n row-major with row pitch omega_tilde_ld[n] >= I_n, dtype of X,
+ *   K_n <= S_n (a slab holds the S_{N-1} x I_{N-1,local} block of its last-mode columns).
+ * Q_out / G_out / rel_err / rel_err_gram as in (4). */
+rt_status rtucker_pet(rt_handle* h, const rt_tensor* X, const int64_t* R, const void* const* omega,
+                      const int64_t* omega_cols, const int64_t* omega_ld, const void* const* omega_tilde,
+                      const int64_t* S, const int64_t* omega_tilde_ld, double* const* Q_out, double* G_out,
+                      double* rel_err, double* rel_err_gram);
+
 #ifdef __cplusplus
 }
 #endif

@@ -297,6 +297,34 @@ def rtucker_sthosvd(h: Handle, X: torch.Tensor, ranks: Sequence[int], p: int, q:
     return _driver(lib.rtucker_sthosvd, h, X, ranks, p, q, omegas, kind, with_error, 0, None, mode_order)
 
 
+def rtucker_pet(h: Handle, X: torch.Tensor, ranks: Sequence[int], omegas, omega_tildes, with_error: bool = True,
+                last_offset: int = 0, last_global: Optional[int] = None) -> dict:
+    """Randomized pass-efficient Tucker (Alg.9 R-PET).  omegas[n]: Omega_n (J_n x K_n);
+    omega_tildes[n]: Omega~_n (S_n x I_n, local columns of the last mode on a slab).
+    Returns dict(Q, G, err) as rtucker_hosvd."""
+    desc = tensor_desc(X, last_offset, last_global)
+    N = desc.order
+    ptrs, cols, lds, keep = _omega_table(N, omegas, "gauss")
+    tl, tp, tld = [], [], []
+    for o in omega_tildes:
+        o, ld = rowmajor_ld(o)
+        tl.append(o)
+        tp.append(o)
+        tld.append(ld)
+    S = [int(o.shape[0]) for o in tl]
+    local = [desc.dims[n] for n in range(N)]
+    Q = [new_colmajor(local[n], ranks[n], device=X.device) for n in range(N)]
+    G = torch.empty(tuple(reversed(list(ranks))), dtype=torch.float64, device=X.device)
+    err = torch.zeros(2, dtype=torch.float64, device=X.device) if with_error else None
+    st = lib.rtucker_pet(h.ptr, C.byref(desc), _i64_array(ranks), ptrs, cols, lds, _ptr_array(tp), _i64_array(S),
+                         _i64_array(tld), _ptr_array(Q), C.c_void_p(G.data_ptr()),
+                         C.c_void_p(err.data_ptr()) if with_error else None,
+                         C.c_void_p(err.data_ptr() + 8) if with_error else None)
+    h.keep(*keep, *tl)
+    _check(h, st)
+    return dict(Q=Q, G=G, err=err)
+
+
 def core_to_numpy(G: torch.Tensor):
     """Device-layout core (R_N..R_1) -> numpy array indexed G[r_1, ..., r_N]."""
     return G.detach().cpu().numpy().T

@@ -400,4 +400,39 @@ rt_status rtucker_sthosvd(rt_handle* h, const rt_tensor* X, const int64_t* R, in
   });
 }
 
+rt_status rtucker_pet(rt_handle* h, const rt_tensor* X, const int64_t* R, const void* const* omega,
+                      const int64_t* omega_cols, const int64_t* omega_ld, const void* const* omega_tilde,
+                      const int64_t* S, const int64_t* omega_tilde_ld, double* const* Q_out, double* G_out,
+                      double* rel_err, double* rel_err_gram) {
+  if (!h) return RT_EINVAL;
+  return guard(h, [&] {
+    rt::TView v = check_tensor(X);
+    RT_REQUIRE(R && omega && omega_cols && omega_ld && omega_tilde && S && omega_tilde_ld && Q_out && G_out,
+               rt::kEINVAL, "NULL argument");
+    const int N = v.N;
+    rt::Engine eng(h->ctx, h->ws, h->comm.get());
+    RT_REQUIRE(!(v.sharded() && !eng.dist()), rt::kEINVAL, "a sharded tensor needs a communicator");
+    int64_t hsz = 1;
+    for (int n = 0; n < N; ++n) {
+      const rt::TView w = v;
+      const int64_t K = omega_cols[n * N + n];
+      check_gauss_omega(w, n, omega[n * N + n], K, omega_ld[n * N + n]);
+      RT_REQUIRE(R[n] >= 1 && R[n] <= K, rt::kERANK, "need 1 <= R_n <= K_n");
+      RT_REQUIRE(S[n] >= K, rt::kERANK, "need K_n <= S_n");
+      RT_REQUIRE(omega_tilde[n] != nullptr && (reinterpret_cast<uintptr_t>(omega_tilde[n]) % (v.dtype ? 8 : 4)) == 0,
+                 rt::kEINVAL, "Omega~_n must be an aligned device pointer");
+      RT_REQUIRE(omega_tilde_ld[n] >= v.d[n], rt::kEINVAL, "Omega~_n row pitch must be >= I_n (local)");
+      RT_REQUIRE(Q_out[n] != nullptr, rt::kEINVAL, "NULL Q_out");
+      hsz *= S[n];
+    }
+    RT_REQUIRE(hsz <= (int64_t(1) << 31), rt::kEUNSUPPORTED, "core sketch H too large");
+    if (v.dtype == 0)
+      eng.pet<float>(v, R, omega, omega_cols, omega_ld, omega_tilde, S, omega_tilde_ld, Q_out, G_out, rel_err,
+                     rel_err_gram);
+    else
+      eng.pet<double>(v, R, omega, omega_cols, omega_ld, omega_tilde, S, omega_tilde_ld, Q_out, G_out, rel_err,
+                      rel_err_gram);
+  });
+}
+
 }  // extern "C"

@@ -71,6 +71,10 @@ class Engine {
   void sthosvd(const TView& X, const int64_t* R, int q, int kind, const void* const* omega,
                const int64_t* omega_cols, const int64_t* omega_ld, const int* order, double* const* Q_out,
                double* G_out, double* E, double* Eg);
+  template <typename T>
+  void pet(const TView& X, const int64_t* R, const void* const* omega, const int64_t* omega_cols,
+           const int64_t* omega_ld, const void* const* omega_tilde, const int64_t* S, const int64_t* omega_tilde_ld,
+           double* const* Q_out, double* G_out, double* E, double* Eg);
 
  private:
   void canon(double* Qn, int64_t m, int r, int64_t ld, int64_t row0, bool dist_rows, double* U, int ku);

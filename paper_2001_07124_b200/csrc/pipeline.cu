@@ -514,6 +514,81 @@ void Engine::sthosvd(const TView& X, const int64_t* R, int q, int kind, const vo
   ws.rewind(mk);
 }
 
+// --------------------------------------------------------------- R-PET (Alg.9)
+// Y_n = X_(n) Omega_n, Q^(n) = qr(Y_n) (lines 1-2); H = X x_1 Omega~_1 ... x_N Omega~_N (line 3, the
+// core kernel chain with Omega~_n^T in place of Q~_n); S = H x_n (Omega~_n Q^(n))^+ (line 4) with
+// A^+ = (A^T A)^{-1} A^T for the full-column-rank A = Omega~_n Q^(n) (S_n x K_n, S_n >= K_n; fp64,
+// Cholesky of A^T A); truncation (line 5) and error as in hosvd (reading R1).  Every sketch of
+// lines 1 and 3 reads only X.
+template <typename T>
+void Engine::pet(const TView& X, const int64_t* R, const void* const* omega, const int64_t* omega_cols,
+                 const int64_t* omega_ld, const void* const* omega_tilde, const int64_t* S,
+                 const int64_t* omega_tilde_ld, double* const* Q_out, double* G_out, double* E, double* Eg) {
+  const int N = X.N;
+  const T* data = static_cast<const T*>(X.data);
+  const auto mk = ws.mark();
+  int64_t K[5], ldq[5], ldw[5];
+  double* Qt[5];
+  double* Wt[5];
+  for (int n = 0; n < N; ++n) {
+    const void* const* om = omega + n * N;
+    const int64_t* oc = omega_cols + n * N;
+    const int64_t* ol = omega_ld + n * N;
+    K[n] = oc[n];
+    const int64_t In = X.d[n];
+    const bool last = (n == N - 1);
+    double* Yt = ws.alloc_n<double>(In * K[n]);
+    sketch<T>(X, data, n, 0, om, oc, ol, 0, Yt);                                  // line 1 (C1)
+    Qt[n] = ws.alloc_n<double>(In * K[n]);
+    ldq[n] = In;
+    qr_y(Yt, In, X.Ig(n), int(K[n]), In, Qt[n], In, nullptr, last && dist(), last ? X.off : 0);   // line 2
+    // Omega~_n (S_n x I_n row-major, pitch ld) is Omega~_n^T as a col-major I_n x S_n matrix
+    Wt[n] = ws.alloc_n<double>(In * S[n]);
+    ldw[n] = In;
+    convert2d<T, double>(ctx, static_cast<const T*>(omega_tilde[n]), In, S[n], omega_tilde_ld[n], Wt[n], In);
+  }
+  int64_t hsz = 1;
+  for (int n = 0; n < N; ++n) hsz *= S[n];
+  double* H = ws.alloc_n<double>(hsz);
+  core<T>(X, data, Wt, ldw, S, H);                                                 // line 3 (C4)
+  // line 4: S = H x_n (Omega~_n Q^(n))^+
+  int64_t cur[5];
+  for (int k = 0; k < N; ++k) cur[k] = S[k];
+  const double* src = H;
+  double* Sc = nullptr;
+  for (int n = 0; n < N; ++n) {
+    const int s = int(S[n]), k = int(K[n]);
+    double* A = ws.alloc_n<double>(int64_t(s) * k);
+    gemm_small(ctx, true, false, s, k, int(X.d[n]), Wt[n], int(ldw[n]), Qt[n], int(ldq[n]), A, s);
+    allreduce(comm, n == N - 1 && dist(), A, int64_t(s) * k, ctx.stream);            // rows of the last mode
+    double* G = ws.alloc_n<double>(int64_t(k) * k);
+    double* Rc = ws.alloc_n<double>(int64_t(k) * k);
+    double* Ri = ws.alloc_n<double>(int64_t(k) * k);
+    double* T1 = ws.alloc_n<double>(int64_t(s) * k);
+    double* M = ws.alloc_n<double>(int64_t(s) * k);
+    gemm_small(ctx, true, false, k, k, s, A, s, A, s, G, k);                      // A^T A
+    chol_inv(ctx, G, k, 0.0, Rc, Ri, nullptr);                                    // A^T A = Rc^T Rc
+    gemm_small(ctx, false, false, s, k, k, A, s, Ri, k, T1, s);                   // A Rc^-1
+    gemm_small(ctx, false, true, s, k, k, T1, s, Ri, k, M, s);                    // (A^+)^T = A (A^T A)^-1
+    const Box b = TView::box_of(cur, N, n);
+    double* dst = ws.alloc_n<double>(b.a * k * b.b);
+    LabelScope ls(ctx, "pet_recover");
+    ttm_t<double, double, double>(ctx, src, b, M, 1, s, k, dst, 1, b.a, b.a * k);
+    src = dst;
+    Sc = dst;
+    cur[n] = k;
+  }
+  truncate(X, Sc, K, Qt, ldq, R, Q_out, G_out);                                   // line 5 (R1)
+  if (E || Eg) rel_error<T>(X, data, G_out, R, Q_out, E, Eg);
+  ws.rewind(mk);
+}
+
+template void Engine::pet<float>(const TView&, const int64_t*, const void* const*, const int64_t*, const int64_t*,
+                                 const void* const*, const int64_t*, const int64_t*, double* const*, double*, double*,
+                                 double*);
+template void Engine::pet<double>(const TView&, const int64_t*, const void* const*, const int64_t*, const int64_t*,
+                                  const void* const*, const int64_t*, const int64_t*, double* const*, double*, double*,
+                                  double*);
 template void Engine::sketch<float>(const TView&, const float*, int, int, const void* const*, const int64_t*,
                                     const int64_t*, int, double*);
 template void Engine::sketch<double>(const TView&, const double*, int, int, const void* const*, const int64_t*,

@@ -1,0 +1,165 @@
+"""GPU parity of R-PET (Alg.9) through the C-ABI
+(`rtucker_pet`) against the fp64 oracle `oracle.pet` on the same seeded inputs.  Metrics and
+tolerances as for the HOSVD path (M2, M4-M7 <= 1e-5; orthonormality <= 1e-12)."""
+import dataclasses
+import threading
+
+import numpy as np
+import pytest
+
+import oracle
+from gen import synth
+from tests import _metrics as M
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2001_07124_b200 import api
+    return api
+
+
+@pytest.fixture(scope="module")
+def h(P):
+    hh = P.Handle()
+    yield hh
+    hh.close()
+
+
+def _dev(x):
+    return torch.from_numpy(synth.to_device_layout(x)).cuda()
+
+
+def _t(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _inputs(cfg):
+    ks, ss = synth.pet_sizes(cfg)
+    oms = [synth.gaussian_omega(cfg, n, K=ks[n]) for n in range(cfg.order)]
+    omt = [synth.omega_tilde(cfg, n, ss[n]) for n in range(cfg.order)]
+    return oms, omt
+
+
+def _check(P, res, ref, tol=1e-5):
+    qg = [q.cpu().numpy() for q in res["Q"]]
+    gg = P.core_to_numpy(res["G"])
+    for n, q in enumerate(qg):
+        assert M.orth(q) <= 1e-12
+        assert M.subspace(q, ref["Q"][n]) <= tol, ("M2", n, M.subspace(q, ref["Q"][n]))
+    assert M.core_in_oracle_basis(gg, qg, ref["G"], ref["Q"]) <= tol
+    assert M.recon(gg, qg, ref["G"], ref["Q"]) <= tol
+    e = float(res["err"][0])
+    assert abs(e - ref["E"]) / ref["E"] <= tol, (e, ref["E"])
+
+
+CASES = {
+    "cfg2s": synth.CONFIGS["cfg2"].scaled((150, 140, 130), (12, 12, 12), (12, 12, 12)),
+    "cfg5s": synth.CONFIGS["cfg5"].scaled((160, 150, 140), (24, 24, 24), (24, 24, 24)),
+    "cfg4s": synth.CONFIGS["cfg4"].scaled((300, 280, 64), (100, 100, 50), (30, 30, 12)),
+    "ragged": synth.CONFIGS["cfg2"].scaled((37, 50, 29), (5, 5, 5), (5, 5, 5)),
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_pet_parity(P, h, name):
+    cfg = CASES[name]
+    x = synth.make_tensor(cfg)
+    oms, omt = _inputs(cfg)
+    ref = oracle.pet(x, cfg.ranks, oms, omt)
+    res = P.rtucker_pet(h, _dev(x), cfg.ranks, [_t(o) for o in oms], [_t(o) for o in omt])
+    h.sync()
+    _check(P, res, ref)
+
+
+def test_pet_exact_rank_fp64(P, h):
+    """Exact multilinear rank R, K = 2R, S = 2K + 1: fp64 data recovers X (E < 1e-10)."""
+    cfg = dataclasses.replace(synth.CONFIGS["cfg1"].scaled((40, 36, 32), (4, 4, 4), (4, 4, 4)), noise="none", p=4)
+    x = synth.make_tensor(cfg)
+    oms, omt = _inputs(cfg)
+    res = P.rtucker_pet(h, _dev(x), cfg.ranks, [_t(o) for o in oms], [_t(o) for o in omt])
+    h.sync()
+    assert float(res["err"][0]) < 1e-10
+    # the K - R surplus sketch columns are pure rounding noise here (exact rank, no noise): the
+    # shifted CholeskyQR orthonormalizes them only to ~sqrt(u), which bounds the factor agreement
+    ref = oracle.pet(x, cfg.ranks, oms, omt)
+    for n in range(3):
+        assert M.subspace(res["Q"][n].cpu().numpy(), ref["Q"][n]) <= 1e-7
+
+
+def test_pet_identity_core_sketch_equals_hosvd(P, h):
+    """Omega~_n = I (S_n = I_n): R-PET is RP-HOSVD (q = 0) on the same Omega_n (pin P23 on the GPU)."""
+    cfg = synth.CONFIGS["cfg2"].scaled((64, 60, 56), (6, 6, 6), (6, 6, 6))
+    x = synth.make_tensor(cfg)
+    oms = [synth.gaussian_omega(cfg, n) for n in range(3)]
+    eye = [np.eye(d, dtype=np.float32) for d in cfg.dims]
+    a = P.rtucker_pet(h, _dev(x), cfg.ranks, [_t(o) for o in oms], [_t(e) for e in eye])
+    b = P.rtucker_hosvd(h, _dev(x), cfg.ranks, cfg.p, 0, [_t(o) for o in oms])
+    h.sync()
+    for n in range(3):
+        assert M.subspace(a["Q"][n].cpu().numpy(), b["Q"][n].cpu().numpy()) <= 1e-6
+    assert abs(float(a["err"][0]) - float(b["err"][0])) <= 1e-6 * float(b["err"][0])
+
+
+def test_pet_invalid_arguments(P, h):
+    from paper_2001_07124_b200 import _lib as L
+    cfg = CASES["ragged"]
+    x = _dev(synth.make_tensor(cfg))
+    oms, omt = _inputs(cfg)
+    bad = [_t(o[: cfg.K(n) - 1]) for n, o in enumerate(omt)]             # S_n < K_n
+    with pytest.raises(L.RtError):
+        P.rtucker_pet(h, x, cfg.ranks, [_t(o) for o in oms], bad)
+    h.sync()
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_pet_loopback_multirank(P, nranks):
+    """Slab-parallel R-PET on one GPU (loopback communicator): the line-1 sketches of modes
+    n < N-1, the core sketch H and Omega~_{N-1} Q^(N-1) are slab partial sums (allreduced), the
+    last factor is row-distributed; the gathered result equals the oracle."""
+    cfg = synth.CONFIGS["cfg5"].scaled((48, 40, 36), (6, 6, 6), (6, 6, 6))
+    x = synth.make_tensor(cfg)
+    oms, omt = _inputs(cfg)
+    ref = oracle.pet(x, cfg.ranks, oms, omt)
+    cuts = np.linspace(0, cfg.dims[2], nranks + 1).astype(int)
+    grp = P.LoopbackGroup(nranks)
+    out = [None] * nranks
+    errs = []
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                hh = P.Handle(stream=s, loopback_group=grp, rank=r)
+                lo, hi = int(cuts[r]), int(cuts[r + 1])
+                xs = _dev(np.asfortranarray(x[:, :, lo:hi]))
+                # local rows of Omega_0 / Omega_1 (j = alpha + a beta: the slab's beta block), full Omega_2
+                loc = [_t(oms[0][cfg.dims[1] * lo:cfg.dims[1] * hi]), _t(oms[1][cfg.dims[0] * lo:cfg.dims[0] * hi]),
+                       _t(oms[2])]
+                tl = [_t(omt[0]), _t(omt[1]), _t(np.ascontiguousarray(omt[2][:, lo:hi]))]
+                res = P.rtucker_pet(hh, xs, cfg.ranks, loc, tl, last_offset=lo, last_global=cfg.dims[2])
+                hh.sync()
+                out[r] = dict(Q=[q.cpu().numpy() for q in res["Q"]], G=P.core_to_numpy(res["G"]),
+                              err=res["err"].cpu().numpy())
+                hh.close()
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    ts = [threading.Thread(target=worker, args=(r,)) for r in range(nranks)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=300)
+    assert not errs, errs
+    q_last = np.concatenate([out[r]["Q"][2] for r in range(nranks)], axis=0)
+    qg = out[0]["Q"][:2] + [q_last]
+    for n in range(3):
+        assert M.subspace(qg[n], ref["Q"][n]) <= 1e-5
+    assert M.recon(out[0]["G"], qg, ref["G"], ref["Q"]) <= 1e-5
+    assert abs(out[0]["err"][0] - ref["E"]) / ref["E"] <= 1e-5
