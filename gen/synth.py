@@ -39,7 +39,7 @@ import numpy as np
 BASE_SEED = 2001_07124
 
 # object ids inside the seed tuple
-_OBJ_CORE, _OBJ_FACTOR, _OBJ_NOISE, _OBJ_OMEGA, _OBJ_KRON, _OBJ_OMEGA_TILDE = 1, 2, 3, 4, 5, 6
+_OBJ_CORE, _OBJ_FACTOR, _OBJ_NOISE, _OBJ_OMEGA, _OBJ_KRON, _OBJ_OMEGA_TILDE, _OBJ_KR = 1, 2, 3, 4, 5, 6, 7
 
 
 def rng_for(*key: int) -> np.random.Generator:
@@ -178,6 +178,17 @@ def gaussian_omega(cfg: Config, n: int, K: Optional[int] = None, rows: Optional[
     if tf32 and cfg.dtype == "f32":
         return np.ascontiguousarray(round_tf32(om))
     return np.ascontiguousarray(om.astype(cfg.np_dtype))
+
+
+def kr_omegas(cfg: Config, n: int, cur_dims: Sequence[int], K: Optional[int] = None) -> list:
+    """Khatri-Rao factors of the mode-n sketch: Omega_k in R^{d_k x K_n} (row-major) for k != n,
+    K_n = min(R_n + p, I_n, J_n) of the current sizes; None at k = n."""
+    N = len(cur_dims)
+    J = int(np.prod([cur_dims[k] for k in range(N) if k != n]))
+    K = min(cfg.ranks[n] + cfg.p, cur_dims[n], J) if K is None else K
+    return [None if k == n else np.ascontiguousarray(
+        rng_for(cfg.cfg_id, _OBJ_KR, n, k).standard_normal((cur_dims[k], K)).astype(cfg.np_dtype))
+        for k in range(N)]
 
 
 def pet_sizes(cfg: Config, K: Optional[Sequence[int]] = None) -> tuple:

@@ -59,7 +59,7 @@ typedef enum { RT_F32 = 0, RT_F64 = 1 } rt_dtype;
 
 /* Sketch operator of the range finder: dense Gaussian Omega_n (Eq. proj, P:162-172;
  * Alg.6 line 3) or the Kronecker-structured X x_{k!=n} Omega_k^T. */
-typedef enum { RT_OMEGA_GAUSS = 0, RT_OMEGA_KRON = 1 } rt_omega_kind;
+typedef enum { RT_OMEGA_GAUSS = 0, RT_OMEGA_KRON = 1, RT_OMEGA_KR = 2 } rt_omega_kind;
 
 typedef struct rt_handle rt_handle;
 
@@ -126,6 +126,9 @@ rt_status rt_profile_read(rt_handle* h, rt_profile_entry* out, int cap, int* n, 
  *                omega_cols[mode] = K, omega_ld[mode] = its row pitch (>= K).
  * kind == KRON : omega[k] is row-major d_k x L_k for k != mode (d_{N-1} local on a slab),
  *                omega_cols[k] = L_k, omega_ld[k] >= L_k, K = prod_{k!=mode} L_k (Eq.(2)).
+ * kind == KR   : Khatri-Rao sketch (P:510 footnote; KR product P:317):
+ *                Y = X_(n) (Omega_N (.) ... (.) Omega_1, without n); omega[k] is row-major d_k x K
+ *                for every k != mode (same K, d_{N-1} local on a slab), omega_ld[k] >= K, K <= 128.
  * Y: fp64 col-major I_n x K, ld ldy >= I_n (local rows for mode N-1 on a slab).
  * Requires 1 <= K <= min(I_n, J_n) (global sizes) and K <= 256. */
 rt_status rtucker_sketch(rt_handle* h, const rt_tensor* X, int mode, rt_omega_kind kind,
@@ -159,6 +162,7 @@ rt_status rtucker_core(rt_handle* h, const rt_tensor* X, const double* const* Q,
  *   Omega_n (J_n x K_n, row-major) and omega_cols[n*N+n] = K_n = min(R_n + p, I_n, J_n).
  *   KRON: entries [n*N+k], k != n, are Omega_k^{(n)} (I_k x L_k, row-major), omega_cols = L_k,
  *   K_n = prod_{k!=n} L_k >= min(R_n + p, I_n) and K_n <= I_n.
+ *   KR: entries [n*N+k], k != n, are Omega_k^{(n)} (I_k x K_n, row-major), K_n = min(R_n + p, I_n, J_n).
  * Q_out[n]: fp64 col-major I_n x R_n (ld I_n, local rows for n = N-1 on a slab).
  * G_out: fp64 R_1 x ... x R_N.  rel_err / rel_err_gram: device fp64 scalars, nullable. */
 rt_status rtucker_hosvd(rt_handle* h, const rt_tensor* X, const int64_t* R, int p, int q,

@@ -80,11 +80,40 @@ def sketch_kron(x: np.ndarray, n: int, omegas: Sequence[Optional[np.ndarray]], q
     return y0, y
 
 
+def khatri_rao(mats: Sequence[np.ndarray]) -> np.ndarray:
+    """Column-wise Kronecker product A_1 (.) A_2 (.) ... (Eq. KHM): column c is
+    kron(A_1[:, c], A_2[:, c], ...)."""
+    k = mats[0].shape[1]
+    out = np.ones((1, k))
+    for m in mats:
+        out = np.einsum("ic,jc->ijc", out, np.asarray(m, dtype=np.float64)).reshape(-1, k)
+    return out
+
+
+def sketch_kr(x: np.ndarray, n: int, omegas: Sequence[Optional[np.ndarray]], q: int = 0):
+    """Khatri-Rao-structured mode-n sketch (P:510 footnote):
+    Y0 = X_(n) (Omega_N (.) ... (.) Omega_1, without n), every Omega_k in R^{I_k x K}, in the
+    Kronecker ordering of Eq.(2) so that the j-index of the unfolding matches.
+    Power iterations (q > 0) continue with dense Z as in ``sketch_gauss``."""
+    x64 = np.asarray(x, dtype=np.float64)
+    xn = unfold(x64, n)
+    kr = khatri_rao([omegas[k] for k in reversed(range(x64.ndim)) if k != n])
+    y0 = xn @ kr
+    y = y0
+    for _ in range(q):
+        qy, _ = qr_plus(y)
+        z, _ = qr_plus(xn.T @ qy)
+        y = xn @ z
+    return y0, y
+
+
 def sketch(x, n, kind, omega, q=0):
     if kind == "gauss":
         return sketch_gauss(x, n, omega, q)
     if kind == "kron":
         return sketch_kron(x, n, omega, q)
+    if kind == "kr":
+        return sketch_kr(x, n, omega, q)
     raise ValueError(kind)
 
 
@@ -293,6 +322,6 @@ def hooi(x: np.ndarray, ranks: Sequence[int], iters: int = 50) -> dict:
     return dict(Q=qs, G=g, E=rel_error(x64, g, qs))
 
 
-__all__ = ["qr_plus", "sketch_gauss", "sketch_kron", "sketch", "core", "rel_error", "pet",
+__all__ = ["qr_plus", "sketch_gauss", "sketch_kron", "sketch_kr", "khatri_rao", "sketch", "core", "rel_error", "pet",
            "rel_error_gram", "eig_desc", "canon_sign", "truncate_hosvd", "hosvd", "sthosvd",
            "thosvd", "sthosvd_det", "hooi", "unfold", "fold", "ttm", "multi_ttm", "reconstruct", "fro"]

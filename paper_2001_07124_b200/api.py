@@ -197,7 +197,7 @@ def _omega_table(N: int, omegas, kind: str):
 
 
 def _kind(kind: str) -> int:
-    return {"gauss": L.RT_OMEGA_GAUSS, "kron": L.RT_OMEGA_KRON}[kind]
+    return {"gauss": L.RT_OMEGA_GAUSS, "kron": L.RT_OMEGA_KRON, "kr": L.RT_OMEGA_KR}[kind]
 
 
 def rtucker_sketch(h: Handle, X: torch.Tensor, mode: int, omega, q: int = 0, kind: str = "gauss",
@@ -220,7 +220,7 @@ def rtucker_sketch(h: Handle, X: torch.Tensor, mode: int, omega, q: int = 0, kin
             o, ld = rowmajor_ld(omega[k])
             keep.append(o)
             ptrs[k], cols[k], lds[k] = o, o.shape[1], ld
-            K *= o.shape[1]
+            K = o.shape[1] if kind == "kr" else K * o.shape[1]     # Khatri-Rao: shared width
     In = desc.dims[mode] if 0 <= mode < N else 1
     Y = new_colmajor(In, K, device=X.device)
     st = lib.rtucker_sketch(h.ptr, C.byref(desc), mode, _kind(kind), _ptr_array(ptrs), _i64_array(cols),

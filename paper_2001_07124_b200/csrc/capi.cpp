@@ -85,6 +85,22 @@ void check_gauss_omega(const rt::TView& X, int n, const void* om, int64_t K, int
   RT_REQUIRE(K <= 128, rt::kEUNSUPPORTED, "K_n > 128 not supported");
 }
 
+// Khatri-Rao factors: every Omega_k (k != n) is I_k x K row-major with the same K
+int64_t check_kr_omega(const rt::TView& X, int n, const void* const* om, const int64_t* cols, const int64_t* lds,
+                       bool strict = true) {
+  const int k0 = n == 0 ? 1 : 0;
+  const int64_t K = cols[k0];
+  RT_REQUIRE(K >= 1 && K <= 128, rt::kEUNSUPPORTED, "Khatri-Rao width must be in [1, 128]");
+  for (int k = 0; k < X.N; ++k) {
+    if (k == n) continue;
+    RT_REQUIRE(om[k] != nullptr, rt::kEINVAL, "Khatri-Rao factor must be a device pointer");
+    RT_REQUIRE(cols[k] == K, rt::kEINVAL, "Khatri-Rao factors must share their column count K_n");
+    RT_REQUIRE(lds[k] >= K, rt::kEINVAL, "Khatri-Rao factor row pitch must be >= K_n");
+  }
+  RT_REQUIRE(!strict || (K <= X.Ig(n) && K <= X.Jg(n)), rt::kERANK, "K_n must be <= min(I_n, J_n)");
+  return K;
+}
+
 int64_t check_kron_omega(const rt::TView& X, int n, const void* const* om, const int64_t* cols, const int64_t* lds,
                          bool strict = true) {
   int64_t K = 1;
@@ -249,6 +265,7 @@ rt_status rtucker_sketch(rt_handle* h, const rt_tensor* X, int mode, rt_omega_ki
     int64_t K;
     if (kind == RT_OMEGA_GAUSS) { K = omega_cols[mode]; check_gauss_omega(v, mode, omega[mode], K, omega_ld[mode], q > 0); }
     else if (kind == RT_OMEGA_KRON) K = check_kron_omega(v, mode, omega, omega_cols, omega_ld, q > 0);
+    else if (kind == RT_OMEGA_KR) K = check_kr_omega(v, mode, omega, omega_cols, omega_ld, q > 0);
     else throw rt::Error(rt::kEINVAL, "unknown omega kind");
     const int64_t In = v.d[mode];
     double* Yt = (ldy == In) ? Y : h->ws.alloc_n<double>(In * K);
@@ -326,7 +343,8 @@ static void check_driver_args(const rt::TView& v, const int64_t* R, int p, int q
                               double* const* Q_out, double* G_out, const int64_t* cur_dims) {
   RT_REQUIRE(R && omega && omega_cols && omega_ld && Q_out && G_out, rt::kEINVAL, "NULL argument");
   RT_REQUIRE(p >= 0 && q >= 0, rt::kEINVAL, "p and q must be >= 0");
-  RT_REQUIRE(kind == RT_OMEGA_GAUSS || kind == RT_OMEGA_KRON, rt::kEINVAL, "unknown omega kind");
+  RT_REQUIRE(kind == RT_OMEGA_GAUSS || kind == RT_OMEGA_KRON || kind == RT_OMEGA_KR, rt::kEINVAL,
+             "unknown omega kind");
   const int N = v.N;
   for (int n = 0; n < N; ++n) {
     RT_REQUIRE(Q_out[n] != nullptr, rt::kEINVAL, "NULL Q_out[n]");
@@ -341,6 +359,10 @@ static void check_driver_args(const rt::TView& v, const int64_t* R, int p, int q
       check_gauss_omega(w, n, om[n], K, ol[n]);
       RT_REQUIRE(K == std::min<int64_t>(R[n] + p, std::min(w.Ig(n), w.Jg(n))), rt::kEINVAL,
                  "Gaussian width must be K_n = min(R_n + p, I_n, J_n)");
+    } else if (kind == RT_OMEGA_KR) {
+      K = check_kr_omega(w, n, om, oc, ol);
+      RT_REQUIRE(K == std::min<int64_t>(R[n] + p, std::min(w.Ig(n), w.Jg(n))), rt::kEINVAL,
+                 "Khatri-Rao width must be K_n = min(R_n + p, I_n, J_n)");
     } else {
       K = check_kron_omega(w, n, om, oc, ol);
       RT_REQUIRE(K >= std::min<int64_t>(R[n] + p, w.Ig(n)), rt::kEINVAL,

@@ -25,6 +25,12 @@ template <typename Tin, typename Tm, typename Tout>
 void ttm_t(const Ctx& ctx, const Tin* X, Box box, const Tm* Mm, int64_t ms_i, int64_t ms_c, int C,
            Tout* out, int64_t so_a, int64_t so_c, int64_t so_b);
 
+// Khatri-Rao sketch stage: out[alpha + a beta] = sum_i W(alpha, i, beta) Om[i*ld + c] with the KR
+// column c = ((c_in_a ? alpha : beta) / c_stride) % K  (W viewed as [a, I, b] for the contracted mode)
+template <typename Tw, typename To>
+void kr_ttv(const Ctx& ctx, const Tw* W, Box box, const To* Om, int64_t ld, int K, bool c_in_a, int64_t c_stride,
+            double* out);
+
 // tcgen05 tensor-core versions (ttm_tc.cu), fp32 only, 3xTF32 split.  Return false (nothing
 // launched) when the shape/alignment is outside the TMA path; callers then use the SIMT kernels.
 // ttm_s_tc: B row-major (element (j,k) at j*ldb + k, ldb % 4 == 0, 16-byte aligned), consumed as an
@@ -87,6 +93,9 @@ void convert2d(const Ctx& ctx, const Ti* in, int64_t m, int64_t n, int64_t ldi, 
 // out(i + ldo*j) = T[(j%a) + a*i + a*I*(j/a)]  (explicit n-unfolding of a small tensor).
 template <typename T>
 void unfold_copy(const Ctx& ctx, const T* Tt, Box box, double* out, int64_t ldo);
+// row-major m x n (row pitch ldi) -> col-major m x n (ldo)
+template <typename T>
+void transpose_copy(const Ctx& ctx, const T* in, int64_t m, int64_t n, int64_t ldi, T* out, int64_t ldo);
 
 // Residual pass: sum_{j,i} (X[j + J*i] - sum_r P[j + J*r] Q[i + ldq*r])^2 and sum X^2.
 // P, X of type T; Q of type T.  Writes 2 fp64 sums to out2 (deterministic partials).

@@ -638,6 +638,24 @@ void convert2d(const Ctx& ctx, const Ti* in, int64_t m, int64_t n, int64_t ldi, 
     convert2d_kernel<Ti, To><<<unsigned(cdiv(m * n, 256)), 256, 0, ctx.stream>>>(in, m, n, ldi, out, ldo);
   });
 }
+template <typename T>
+__global__ void transpose_copy_kernel(const T* __restrict__ in, int64_t m, int64_t n, int64_t ldi, T* __restrict__ out,
+                                      int64_t ldo) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= m * n) return;
+  const int64_t i = e % m, j = e / m;
+  out[i + ldo * j] = in[i * ldi + j];
+}
+template <typename T>
+void transpose_copy(const Ctx& ctx, const T* in, int64_t m, int64_t n, int64_t ldi, T* out, int64_t ldo) {
+  if (m * n == 0) return;
+  launch(ctx, "transpose_copy", [&] {
+    transpose_copy_kernel<T><<<unsigned(cdiv(m * n, 256)), 256, 0, ctx.stream>>>(in, m, n, ldi, out, ldo);
+  });
+}
+template void transpose_copy<float>(const Ctx&, const float*, int64_t, int64_t, int64_t, float*, int64_t);
+template void transpose_copy<double>(const Ctx&, const double*, int64_t, int64_t, int64_t, double*, int64_t);
+
 template void convert2d<double, float>(const Ctx&, const double*, int64_t, int64_t, int64_t, float*, int64_t);
 template void convert2d<double, double>(const Ctx&, const double*, int64_t, int64_t, int64_t, double*, int64_t);
 template void convert2d<float, double>(const Ctx&, const float*, int64_t, int64_t, int64_t, double*, int64_t);

@@ -177,6 +177,51 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
     }
     ttm_s_dispatch(ctx, ws, data, bx, om, ld, ctx.omega_tf32 != 0, K, Yt, In);
     ws.rewind(mo);
+  } else if (kind == 2) {
+    // Khatri-Rao sketch (P:510 footnote): Y[:, c] = X x_{k!=n} Omega_k[:, c]^T.  One TTM with the
+    // first factor (Omega_k0: I_k0 x K, row-major) streams X; each further mode is a TTV whose
+    // vector is the KR column c carried by the k0 coordinate (fp64 sums).
+    int k0 = (n == 0) ? 1 : 0;
+    K = int(omega_cols[k0]);
+    int64_t cur[5];
+    for (int k = 0; k < N; ++k) cur[k] = X.d[k];
+    const auto mk = ws.mark();
+    const Box b0 = TView::box_of(cur, N, k0);
+    T* W0 = ws.alloc_n<T>(b0.a * K * b0.b);
+    {
+      // ttm_t_dispatch takes a col-major Q (I x K); Omega_k0 is row-major -> transposed copy
+      const int64_t ldo = pad4(cur[k0]);
+      T* qc = ws.alloc_n<T>(ldo * K);
+      if (ldo != cur[k0]) fill_zero(ctx, qc, sizeof(T) * ldo * K);
+      transpose_copy<T>(ctx, static_cast<const T*>(omega[k0]), cur[k0], K, omega_ld[k0], qc, ldo);
+      ttm_t_dispatch(ctx, ws, data, b0, qc, ldo, K, W0, 1, b0.a, b0.a * K);
+    }
+    cur[k0] = K;
+    const void* src = W0;
+    bool src_is_T = true;
+    for (int m = 0; m < N; ++m) {
+      if (m == n || m == k0) continue;
+      const Box bm = TView::box_of(cur, N, m);
+      int64_t cs = 1;
+      const bool c_in_a = k0 < m;
+      if (c_in_a) { for (int k = 0; k < k0; ++k) cs *= cur[k]; }
+      else { for (int k = m + 1; k < k0; ++k) cs *= cur[k]; }
+      double* dst = ws.alloc_n<double>(bm.a * bm.b);
+      const T* om = static_cast<const T*>(omega[m]);
+      if (src_is_T) kr_ttv<T, T>(ctx, static_cast<const T*>(src), bm, om, omega_ld[m], K, c_in_a, cs, dst);
+      else kr_ttv<double, T>(ctx, static_cast<const double*>(src), bm, om, omega_ld[m], K, c_in_a, cs, dst);
+      src = dst;
+      src_is_T = false;
+      cur[m] = 1;
+    }
+    if (src_is_T) {   // order-2 tensor: no TTV stage; widen W0 to fp64
+      double* w64 = ws.alloc_n<double>(b0.a * K * b0.b);
+      convert2d<T, double>(ctx, static_cast<const T*>(src), b0.a * K * b0.b, 1, b0.a * K * b0.b, w64,
+                           b0.a * K * b0.b);
+      src = w64;
+    }
+    unfold_copy<double>(ctx, static_cast<const double*>(src), TView::box_of(cur, N, n), Yt, In);
+    ws.rewind(mk);
   } else {
     // Kronecker sketch W = X x_{k!=n} Omega_k^T (Eq.(2)): a chain of TTMs whose first
     // stage streams X and whose later stages run on the shrunken result.  The factors are narrow
@@ -421,6 +466,7 @@ void Engine::hosvd(const TView& X, const int64_t* R, int q, int kind, const void
     const int64_t* oc = omega_cols + n * N;
     const int64_t* ol = omega_ld + n * N;
     if (kind == 0) K[n] = oc[n];
+    else if (kind == 2) K[n] = oc[n == 0 ? 1 : 0];
     else { K[n] = 1; for (int k = 0; k < N; ++k) if (k != n) K[n] *= oc[k]; }
     const int64_t In = X.d[n];
     double* Yt = ws.alloc_n<double>(In * K[n]);
@@ -463,6 +509,7 @@ void Engine::sthosvd(const TView& X, const int64_t* R, int q, int kind, const vo
     const int64_t* ol = omega_ld + n * N;
     int K;
     if (kind == 0) K = int(oc[n]);
+    else if (kind == 2) K = int(oc[n == 0 ? 1 : 0]);
     else { K = 1; for (int k = 0; k < N; ++k) if (k != n) K *= int(oc[k]); }
     const int64_t In = S.d[n];
     const auto mstep = ws.mark();

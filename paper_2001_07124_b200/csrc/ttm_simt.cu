@@ -307,6 +307,40 @@ void ttm_t(const Ctx& ctx, const Tin* X, Box box, const Tm* Mm, int64_t ms_i, in
   else               launch_ttm_t<Tin, Tm, Tout, 16>(ctx, X, box, Mm, ms_i, ms_c, C, out, so_a, so_c, so_b);
 }
 
+// ------------------------------------------------------------- Khatri-Rao TTV
+// out[alpha + a beta] = sum_i W[alpha + a i + a I beta] Om[i ld + c], the KR column c read from the
+// alpha (c_in_a) or beta index: c = (alpha / c_stride) % K  or  (beta / c_stride) % K.  fp64 sums.
+namespace {
+template <typename Tw, typename To>
+__global__ void kr_ttv_kernel(const Tw* __restrict__ W, int64_t a, int64_t I, int64_t b, const To* __restrict__ Om,
+                              int64_t ld, int K, bool c_in_a, int64_t c_stride, double* __restrict__ out) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= a * b) return;
+  const int64_t al = e % a, be = e / a;
+  const int c = int(((c_in_a ? al : be) / c_stride) % K);
+  const Tw* w = W + al + a * I * be;
+  double s = 0.0;
+  for (int64_t i = 0; i < I; ++i) s = fma(double(w[a * i]), double(Om[i * ld + c]), s);
+  out[e] = s;
+}
+
+}  // namespace
+
+template <typename Tw, typename To>
+void kr_ttv(const Ctx& ctx, const Tw* W, Box box, const To* Om, int64_t ld, int K, bool c_in_a, int64_t c_stride,
+            double* out) {
+  const int64_t n = box.a * box.b;
+  if (n == 0) return;
+  launch(ctx, "kr_ttv", [&] {
+    kr_ttv_kernel<Tw, To><<<unsigned(cdiv(n, 256)), 256, 0, ctx.stream>>>(W, box.a, box.I, box.b, Om, ld, K, c_in_a,
+                                                                          c_stride, out);
+  });
+}
+template void kr_ttv<float, float>(const Ctx&, const float*, Box, const float*, int64_t, int, bool, int64_t, double*);
+template void kr_ttv<double, float>(const Ctx&, const double*, Box, const float*, int64_t, int, bool, int64_t, double*);
+template void kr_ttv<double, double>(const Ctx&, const double*, Box, const double*, int64_t, int, bool, int64_t,
+                                     double*);
+
 template void ttm_s<float>(const Ctx&, Arena&, const float*, Box, const float*, int64_t, int64_t, int,
                            double*, int64_t, bool);
 template void ttm_s<double>(const Ctx&, Arena&, const double*, Box, const double*, int64_t, int64_t, int,

@@ -489,3 +489,38 @@ def test_P23_pet_identity_core_sketch_reduces_to_rp_hosvd():
         assert np.linalg.norm(a["Q"][n] - b["Q"][n]) < 1e-10
     assert np.linalg.norm(a["G"] - b["G"]) < 1e-10 * np.linalg.norm(b["G"])
     assert abs(a["E"] - b["E"]) < 1e-12
+
+
+# ------------------------------------------------------------- Khatri-Rao sketch
+def test_P24_khatri_rao_sketch_is_explicit_brute_force():
+    """sketch_kr equals X_(n) times the explicit Khatri-Rao matrix built entry by entry:
+    row j (first-mode-fastest over k != n, reading R6) of column c is prod_k Omega_k[i_k, c]."""
+    dims = (4, 3, 5)
+    rng = np.random.default_rng(24)
+    x = rng.standard_normal(dims)
+    K = 2
+    for n in range(3):
+        oms = [None if k == n else rng.standard_normal((dims[k], K)) for k in range(3)]
+        others = [k for k in range(3) if k != n]
+        J = int(np.prod([dims[k] for k in others]))
+        kr = np.zeros((J, K))
+        for c in range(K):
+            for idx in np.ndindex(*[dims[k] for k in reversed(others)]):
+                sub = dict(zip(reversed(others), idx))
+                j = 0
+                stride = 1
+                for k in others:                       # first-mode-fastest linearization
+                    j += sub[k] * stride
+                    stride *= dims[k]
+                kr[j, c] = np.prod([oms[k][sub[k], c] for k in others])
+        y0, _ = oracle.sketch_kr(x, n, oms)
+        brute = np.zeros((dims[n], K))
+        for i in range(dims[n]):
+            row = np.moveaxis(x, n, 0)[i]
+            for c in range(K):
+                w = row.copy()
+                for pos, k in reversed(list(enumerate(others))):
+                    w = np.tensordot(w, oms[k][:, c], axes=([pos], [0]))
+                brute[i, c] = w
+        assert np.allclose(y0, oracle.unfold(x, n) @ kr, rtol=0, atol=1e-12)
+        assert np.allclose(y0, brute, rtol=0, atol=1e-12)
