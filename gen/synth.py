@@ -39,7 +39,7 @@ import numpy as np
 BASE_SEED = 2001_07124
 
 # object ids inside the seed tuple
-_OBJ_CORE, _OBJ_FACTOR, _OBJ_NOISE, _OBJ_OMEGA, _OBJ_KRON, _OBJ_OMEGA_TILDE, _OBJ_KR = 1, 2, 3, 4, 5, 6, 7
+_OBJ_CORE, _OBJ_FACTOR, _OBJ_NOISE, _OBJ_OMEGA, _OBJ_KRON, _OBJ_OMEGA_TILDE, _OBJ_KR, _OBJ_HOOI = 1, 2, 3, 4, 5, 6, 7, 8
 
 
 def rng_for(*key: int) -> np.random.Generator:
@@ -189,6 +189,19 @@ def kr_omegas(cfg: Config, n: int, cur_dims: Sequence[int], K: Optional[int] = N
     return [None if k == n else np.ascontiguousarray(
         rng_for(cfg.cfg_id, _OBJ_KR, n, k).standard_normal((cur_dims[k], K)).astype(cfg.np_dtype))
         for k in range(N)]
+
+
+def hooi_omegas(cfg: Config, sweeps: int) -> list:
+    """RP-HOOI test matrices Omega^(n) in R^{prod_{p!=n} R_p x R_n} (fp64, row-major), per sweep."""
+    N = cfg.order
+    out = []
+    for it in range(sweeps):
+        row = []
+        for n in range(N):
+            rows = int(np.prod([cfg.ranks[p] for p in range(N) if p != n]))
+            row.append(np.ascontiguousarray(rng_for(cfg.cfg_id, _OBJ_HOOI, it, n).standard_normal((rows, cfg.ranks[n]))))
+        out.append(row)
+    return out
 
 
 def pet_sizes(cfg: Config, K: Optional[Sequence[int]] = None) -> tuple:

@@ -280,6 +280,35 @@ def pet(x: np.ndarray, ranks: Sequence[int], omegas, omega_tildes, with_error: b
     return out
 
 
+def rp_hooi(x: np.ndarray, ranks: Sequence[int], q_init: Sequence[np.ndarray], omegas, with_error: bool = True) -> dict:
+    """Alg.7 RP-HOOI, len(omegas) sweeps (reading R24: the stopping criterion is a
+    fixed sweep count; the Gaussian Omega^(n) of every sweep and mode are inputs):
+
+      for each sweep, for n = 1..N:
+        S = X x_{p != n} Q^(p)T                     (line 4, the latest factors)
+        W^(n) = S_(n) Omega^(n),  Omega^(n) in R^{prod_{p!=n} R_p x R_n}   (line 5)
+        Q^(n) = orthonormal basis of W^(n) (qr+)      (line 6)
+      S = S x_N Q^(N)T                               (line 7: the core of the last factors)
+
+    Q^(n) are then sign-canonicalized (reading R5) and the core is X x_n Q^(n)T of those factors.
+    """
+    x64 = np.asarray(x, dtype=np.float64)
+    N = x64.ndim
+    qs = [np.asarray(q, dtype=np.float64) for q in q_init]
+    for sweep in omegas:
+        for n in range(N):
+            s = multi_ttm(x64, qs, transpose=True, skip=[n])
+            w = unfold(s, n) @ np.asarray(sweep[n], dtype=np.float64)
+            qs[n], _ = qr_plus(w)
+    qs = [canon_sign(q, np.zeros((1, q.shape[1])))[0] for q in qs]
+    g = core(x64, qs)
+    out = dict(Q=qs, G=g)
+    if with_error:
+        out["E"] = rel_error(x64, g, qs)
+        out["E_gram"] = rel_error_gram(x64, g)
+    return out
+
+
 # ------------------------------------------------------ deterministic references
 def thosvd(x: np.ndarray, ranks: Sequence[int]) -> dict:
     """Deterministic truncated HOSVD via full SVD of each unfolding (Eq. UnfoldHOSVD
@@ -323,5 +352,6 @@ def hooi(x: np.ndarray, ranks: Sequence[int], iters: int = 50) -> dict:
 
 
 __all__ = ["qr_plus", "sketch_gauss", "sketch_kron", "sketch_kr", "khatri_rao", "sketch", "core", "rel_error", "pet",
+           "rp_hooi",
            "rel_error_gram", "eig_desc", "canon_sign", "truncate_hosvd", "hosvd", "sthosvd",
            "thosvd", "sthosvd_det", "hooi", "unfold", "fold", "ttm", "multi_ttm", "reconstruct", "fro"]

@@ -12,6 +12,7 @@ import pytest
 
 import oracle
 from gen import synth
+from tests import _metrics as M
 
 
 def _rng(seed):
@@ -524,3 +525,43 @@ def test_P24_khatri_rao_sketch_is_explicit_brute_force():
                 brute[i, c] = w
         assert np.allclose(y0, oracle.unfold(x, n) @ kr, rtol=0, atol=1e-12)
         assert np.allclose(y0, brute, rtol=0, atol=1e-12)
+
+
+# ----------------------------------------------------------------- RP-HOOI (Alg.7)
+def test_P25_rp_hooi_exact_rank_from_random_start():
+    """Alg.7 from random orthonormal starting factors recovers an exact multilinear-rank-R
+    tensor in one sweep (S_(n) has rank R_n, so orth(S_(n) Omega) spans it): E <= 1e-10."""
+    dims, r = (20, 18, 16), 3
+    x, us = _lowrank(25, dims, r)
+    rng = np.random.default_rng(26)
+    q0 = [np.linalg.qr(rng.standard_normal((d, r)))[0] for d in dims]
+    oms = [[rng.standard_normal((r * r, r)) for _ in range(3)] for _ in range(2)]
+    out = oracle.rp_hooi(x, (r,) * 3, q0, oms)
+    assert out["E"] <= 1e-10
+    for n in range(3):
+        assert np.linalg.norm(out["Q"][n].T @ out["Q"][n] - np.eye(r)) < 1e-12
+
+
+def test_P26_rp_hooi_matrix_identity_sketch_is_subspace_iteration():
+    """N = 2, R_1 = R_2 = R, Omega^(n) = I_R: line 5 is W = S_(n) = X Q^(2) (resp. X^T Q^(1)), so a
+    sweep is one step of orthogonal (subspace) iteration, i.e. the HOOI update for matrices."""
+    rng = np.random.default_rng(27)
+    x = rng.standard_normal((30, 25))
+    r = 4
+    q1, q2 = (np.linalg.qr(rng.standard_normal((d, r)))[0] for d in x.shape)
+    out = oracle.rp_hooi(x, (r, r), [q1, q2], [[np.eye(r), np.eye(r)]])
+    e1 = np.linalg.qr(x @ q2)[0]
+    e2 = np.linalg.qr(x.T @ e1)[0]
+    # (the projector-distance metric has a ~1e-8 floor: sqrt of an fp64 cancellation)
+    assert M.subspace(out["Q"][0], e1) < 1e-7 and M.subspace(out["Q"][1], e2) < 1e-7
+
+
+def test_P27_rp_hooi_above_the_hooi_optimum():
+    """No orthonormal factors beat the (converged) HOOI fit: E_rphooi >= E_hooi (1 - 1e-9)."""
+    cfg = synth.CONFIGS["cfg2"].scaled((24, 22, 20), (4, 4, 4), (4, 4, 4))
+    x = synth.make_tensor(cfg)
+    oms = [synth.gaussian_omega(cfg, n) for n in range(3)]
+    a = oracle.hosvd(x, cfg.ranks, oms, q=0)
+    b = oracle.rp_hooi(x, cfg.ranks, a["Q"], synth.hooi_omegas(cfg, 3))
+    c = oracle.hooi(x, cfg.ranks)
+    assert c["E"] * (1 - 1e-9) <= b["E"]
