@@ -200,6 +200,18 @@ rt_status rtucker_pet(rt_handle* h, const rt_tensor* X, const int64_t* R, const 
                       const int64_t* S, const int64_t* omega_tilde_ld, double* const* Q_out, double* G_out,
                       double* rel_err, double* rel_err_gram);
 
+/* (7) Random projection HOOI = Alg.7 RP-HOOI, `sweeps` sweeps (reading R24: fixed sweep
+ *     count; every Omega is an input):  for n = 1..N:  S = X x_{p!=n} Q^(p)T (latest factors),
+ *     W = S_(n) Omega^(n), Q^(n) = qr(W);  then signs canonicalized (R5) and G = X x_n Q^(n)T.
+ * Q_init[n]: starting factors (device fp64 col-major I_n x R_n, ld I_n; local rows for the last mode
+ *   on a slab; e.g. the output of (4)); may alias Q_out[n].
+ * omega[it*N + n], omega_ld[it*N + n]: Omega^(n) of sweep it, device fp64 row-major
+ *   (prod_{p!=n} R_p) x R_n with row pitch >= R_n; rows in the first-mode-fastest j order of S_(n).
+ * Q_out / G_out / rel_err / rel_err_gram as in (4).  R_n <= 128. */
+rt_status rtucker_rp_hooi(rt_handle* h, const rt_tensor* X, const int64_t* R, int sweeps,
+                          const double* const* Q_init, const double* const* omega, const int64_t* omega_ld,
+                          double* const* Q_out, double* G_out, double* rel_err, double* rel_err_gram);
+
 #ifdef __cplusplus
 }
 #endif

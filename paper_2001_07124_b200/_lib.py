@@ -20,7 +20,7 @@ RT_OPT_TTM_IMPL, RT_OPT_PROFILE, RT_OPT_QR_FALLBACK, RT_OPT_OMEGA_TF32, RT_OPT_T
 
 EXPORTS = ["rt_get_unique_id", "rt_create", "rt_loopback_group_create", "rt_loopback_group_destroy",
            "rt_create_loopback", "rt_destroy", "rt_last_error", "rt_sync", "rt_set_option", "rt_profile_read",
-           "rtucker_sketch", "rtucker_qr", "rtucker_core", "rtucker_hosvd", "rtucker_sthosvd", "rtucker_pet"]
+           "rtucker_sketch", "rtucker_qr", "rtucker_core", "rtucker_hosvd", "rtucker_sthosvd", "rtucker_pet", "rtucker_rp_hooi"]
 
 
 class rt_tensor(C.Structure):
@@ -64,6 +64,7 @@ def _load():
         "rtucker_sthosvd": (I, [P, C.POINTER(rt_tensor), PI64, I, I, I, PP, PI64, PI64, C.POINTER(C.c_int), PP, P,
                                 P, P]),
         "rtucker_pet": (I, [P, C.POINTER(rt_tensor), PI64, PP, PI64, PI64, PP, PI64, PI64, PP, P, P, P]),
+        "rtucker_rp_hooi": (I, [P, C.POINTER(rt_tensor), PI64, I, PP, PP, PI64, PP, P, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -15,6 +15,7 @@ device buffers and the stream.  Conventions:
 from __future__ import annotations
 
 import ctypes as C
+import math
 from typing import List, Optional, Sequence
 
 import torch
@@ -321,6 +322,41 @@ def rtucker_pet(h: Handle, X: torch.Tensor, ranks: Sequence[int], omegas, omega_
                          C.c_void_p(err.data_ptr()) if with_error else None,
                          C.c_void_p(err.data_ptr() + 8) if with_error else None)
     h.keep(*keep, *tl)
+    _check(h, st)
+    return dict(Q=Q, G=G, err=err)
+
+
+def rtucker_rp_hooi(h: Handle, X: torch.Tensor, ranks: Sequence[int], q_init, omegas, with_error: bool = True,
+                    last_offset: int = 0, last_global: Optional[int] = None) -> dict:
+    """Random projection HOOI (Alg.7).  q_init[n]: fp64 (I_n_local, R_n) starting factors;
+    omegas[sweep][n]: fp64 (prod_{p!=n} R_p, R_n).  Returns dict(Q, G, err) as rtucker_hosvd."""
+    desc = tensor_desc(X, last_offset, last_global)
+    N = desc.order
+    q0 = [colmajor(q.to(torch.float64)) for q in q_init]
+    for n, q in enumerate(q0):
+        if q.stride(1) != q.shape[0] and q.shape[1] > 1:
+            raise ValueError("q_init must be packed column-major")
+    flat, lds, keep = [], [], list(q0)
+    for sweep in omegas:
+        if len(sweep) != N:
+            raise ValueError("each sweep needs N test matrices")
+        for n, o in enumerate(sweep):
+            rows = math.prod(int(ranks[p]) for p in range(N) if p != n)
+            if tuple(o.shape) != (rows, ranks[n]):
+                raise ValueError(f"Omega^({n}) must be ({rows}, {ranks[n]}), got {tuple(o.shape)}")
+            o, ld = rowmajor_ld(o.to(torch.float64))
+            keep.append(o)
+            flat.append(o)
+            lds.append(ld)
+    local = [desc.dims[n] for n in range(N)]
+    Q = [new_colmajor(local[n], ranks[n], device=X.device) for n in range(N)]
+    G = torch.empty(tuple(reversed(list(ranks))), dtype=torch.float64, device=X.device)
+    err = torch.zeros(2, dtype=torch.float64, device=X.device) if with_error else None
+    st = lib.rtucker_rp_hooi(h.ptr, C.byref(desc), _i64_array(ranks), len(omegas), _ptr_array(q0),
+                             _ptr_array(flat) if flat else None, _i64_array(lds) if lds else None, _ptr_array(Q),
+                             C.c_void_p(G.data_ptr()), C.c_void_p(err.data_ptr()) if with_error else None,
+                             C.c_void_p(err.data_ptr() + 8) if with_error else None)
+    h.keep(*keep)
     _check(h, st)
     return dict(Q=Q, G=G, err=err)
 

@@ -457,4 +457,31 @@ rt_status rtucker_pet(rt_handle* h, const rt_tensor* X, const int64_t* R, const 
   });
 }
 
+rt_status rtucker_rp_hooi(rt_handle* h, const rt_tensor* X, const int64_t* R, int sweeps,
+                          const double* const* Q_init, const double* const* omega, const int64_t* omega_ld,
+                          double* const* Q_out, double* G_out, double* rel_err, double* rel_err_gram) {
+  if (!h) return RT_EINVAL;
+  return guard(h, [&] {
+    rt::TView v = check_tensor(X);
+    RT_REQUIRE(R && Q_init && Q_out && G_out && (sweeps == 0 || (omega && omega_ld)), rt::kEINVAL, "NULL argument");
+    RT_REQUIRE(sweeps >= 0, rt::kEINVAL, "sweeps must be >= 0");
+    const int N = v.N;
+    rt::Engine eng(h->ctx, h->ws, h->comm.get());
+    RT_REQUIRE(!(v.sharded() && !eng.dist()), rt::kEINVAL, "a sharded tensor needs a communicator");
+    for (int n = 0; n < N; ++n) {
+      RT_REQUIRE(R[n] >= 1 && R[n] <= v.Ig(n) && R[n] <= 128, rt::kERANK, "need 1 <= R_n <= min(I_n, 128)");
+      RT_REQUIRE(Q_init[n] && Q_out[n], rt::kEINVAL, "NULL factor pointer");
+      int64_t rows = 1;
+      for (int p = 0; p < N; ++p) if (p != n) rows *= R[p];
+      RT_REQUIRE(rows >= R[n], rt::kERANK, "need prod_{p!=n} R_p >= R_n");
+      for (int it = 0; it < sweeps; ++it) {
+        RT_REQUIRE(omega[it * N + n] != nullptr, rt::kEINVAL, "NULL Omega");
+        RT_REQUIRE(omega_ld[it * N + n] >= R[n], rt::kEINVAL, "Omega row pitch must be >= R_n");
+      }
+    }
+    if (v.dtype == 0) eng.rp_hooi<float>(v, R, sweeps, Q_init, omega, omega_ld, Q_out, G_out, rel_err, rel_err_gram);
+    else eng.rp_hooi<double>(v, R, sweeps, Q_init, omega, omega_ld, Q_out, G_out, rel_err, rel_err_gram);
+  });
+}
+
 }  // extern "C"

@@ -75,6 +75,14 @@ class Engine {
   void pet(const TView& X, const int64_t* R, const void* const* omega, const int64_t* omega_cols,
            const int64_t* omega_ld, const void* const* omega_tilde, const int64_t* S, const int64_t* omega_tilde_ld,
            double* const* Q_out, double* G_out, double* E, double* Eg);
+  template <typename T>
+  void rp_hooi(const TView& X, const int64_t* R, int sweeps, const double* const* Q_init, const double* const* omega,
+               const int64_t* omega_ld, double* const* Q_out, double* G_out, double* E, double* Eg);
+  // X x_{p != skip} Q_p^T in ascending mode order -> fp64 tensor (R_p for p != skip, X.d[skip] at skip);
+  // slab partial sums are allreduced when the last mode is contracted
+  template <typename T>
+  void multi_ttm_skip(const TView& X, const T* data, const double* const* Q, const int64_t* ldq, const int64_t* C,
+                      int skip, double* out);
 
  private:
   void canon(double* Qn, int64_t m, int r, int64_t ld, int64_t row0, bool dist_rows, double* U, int ku);

@@ -630,6 +630,84 @@ void Engine::pet(const TView& X, const int64_t* R, const void* const* omega, con
   ws.rewind(mk);
 }
 
+// ------------------------------------------------------------- RP-HOOI (Alg.7)
+// Reading R25: every stage accumulates in fp64 (CUDA cores) with fp64 intermediates and the fp64
+// factors as stored.  W = S_(n) Omega^(n) has no oversampling, so span(W) is conditioned by
+// kappa(W) ~ 1e1-1e2 and the fp32-accumulated tensor-core chain moved E by ~2e-5 on cfg2-small.
+template <typename T>
+void Engine::multi_ttm_skip(const TView& X, const T* data, const double* const* Q, const int64_t* ldq,
+                            const int64_t* C, int skip, double* out) {
+  const int N = X.N;
+  const auto mk = ws.mark();
+  int ps[5], np_ = 0;
+  for (int p = 0; p < N; ++p) if (p != skip) ps[np_++] = p;
+  int64_t cur[5];
+  for (int k = 0; k < N; ++k) cur[k] = X.d[k];
+  const double* src = nullptr;
+  for (int i = 0; i < np_; ++i) {
+    const int p = ps[i];
+    const Box b = TView::box_of(cur, N, p);
+    double* dst = (i == np_ - 1) ? out : ws.alloc_n<double>(b.a * C[p] * b.b);
+    if (i == 0)
+      ttm_t<T, double, double>(ctx, data, b, Q[p], 1, ldq[p], int(C[p]), dst, 1, b.a, b.a * C[p]);
+    else
+      ttm_t<double, double, double>(ctx, src, b, Q[p], 1, ldq[p], int(C[p]), dst, 1, b.a, b.a * C[p]);
+    src = dst;
+    cur[p] = C[p];
+  }
+  int64_t sz = 1;
+  for (int k = 0; k < N; ++k) sz *= cur[k];
+  allreduce(comm, dist() && skip != N - 1, out, sz, ctx.stream);            // last mode contracted: partial sums
+  ws.rewind(mk);
+}
+
+// Alg.7: sweeps over n of  S = X x_{p!=n} Q^(p)T (latest factors),  W = S_(n) Omega^(n),
+// Q^(n) = qr(W); then R5 signs and the core of the final factors (line 7) and E.
+template <typename T>
+void Engine::rp_hooi(const TView& X, const int64_t* R, int sweeps, const double* const* Q_init,
+                     const double* const* omega, const int64_t* omega_ld, double* const* Q_out, double* G_out,
+                     double* E, double* Eg) {
+  const int N = X.N;
+  const T* data = static_cast<const T*>(X.data);
+  const auto mk = ws.mark();
+  int64_t ldq[5];
+  for (int n = 0; n < N; ++n) {
+    ldq[n] = X.d[n];
+    if (Q_out[n] != Q_init[n])
+      RT_CUDA(cudaMemcpyAsync(Q_out[n], Q_init[n], sizeof(double) * X.d[n] * R[n], cudaMemcpyDeviceToDevice,
+                              ctx.stream));
+  }
+  for (int it = 0; it < sweeps; ++it) {
+    for (int n = 0; n < N; ++n) {
+      const auto ms = ws.mark();
+      int64_t cur[5];
+      for (int k = 0; k < N; ++k) cur[k] = (k == n) ? X.d[k] : R[k];
+      int64_t sz = 1;
+      for (int k = 0; k < N; ++k) sz *= cur[k];
+      double* S = ws.alloc_n<double>(sz);
+      multi_ttm_skip<T>(X, data, Q_out, ldq, R, n, S);                                   // line 4
+      const int64_t In = X.d[n];
+      double* W = ws.alloc_n<double>(In * R[n]);
+      ttm_s<double>(ctx, ws, S, TView::box_of(cur, N, n), omega[it * N + n], omega_ld[it * N + n], 1, int(R[n]), W,
+                    In);                                                                  // line 5
+      const bool last = (n == N - 1);
+      qr_y(W, In, X.Ig(n), int(R[n]), In, Q_out[n], In, nullptr, last && dist(), last ? X.off : 0);   // line 6
+      ws.rewind(ms);
+    }
+  }
+  for (int n = 0; n < N; ++n) {                                                         // reading R5
+    double* U = ws.alloc_n<double>(R[n] * R[n]);
+    canon(Q_out[n], X.d[n], int(R[n]), X.d[n], n == N - 1 ? X.off : 0, n == N - 1, U, int(R[n]));
+  }
+  core<T>(X, data, Q_out, ldq, R, G_out);                                                // line 7
+  if (E || Eg) rel_error<T>(X, data, G_out, R, Q_out, E, Eg);
+  ws.rewind(mk);
+}
+
+template void Engine::rp_hooi<float>(const TView&, const int64_t*, int, const double* const*, const double* const*,
+                                     const int64_t*, double* const*, double*, double*, double*);
+template void Engine::rp_hooi<double>(const TView&, const int64_t*, int, const double* const*, const double* const*,
+                                      const int64_t*, double* const*, double*, double*, double*);
 template void Engine::pet<float>(const TView&, const int64_t*, const void* const*, const int64_t*, const int64_t*,
                                  const void* const*, const int64_t*, const int64_t*, double* const*, double*, double*,
                                  double*);

@@ -78,6 +78,21 @@ def test_cfg2_full_vs_oracle(P, hb):
     _check_vs_oracle(P, res, ref)
 
 
+def test_cfg2_full_rp_hooi_vs_oracle(P, hb):
+    """RP-HOOI (Alg.7) at cfg2's full size: 2 sweeps from the oracle's RP-HOSVD
+    factors, elementwise metrics against oracle.rp_hooi (reading R25)."""
+    cfg = synth.CONFIGS["cfg2"]
+    x = synth.make_tensor(cfg)
+    oms = [synth.gaussian_omega(cfg, n) for n in range(3)]
+    q0 = oracle.hosvd(x, cfg.ranks, oms, q=0)["Q"]
+    hs = synth.hooi_omegas(cfg, 2)
+    ref = oracle.rp_hooi(x, cfg.ranks, q0, hs)
+    res = P.rtucker_rp_hooi(hb, _dev(x), cfg.ranks, [torch.from_numpy(q).cuda() for q in q0],
+                            [[torch.from_numpy(o).cuda() for o in sw] for sw in hs])
+    hb.sync()
+    _check_vs_oracle(P, res, ref)
+
+
 def test_cfg3_full_sthosvd_kron_vs_oracle(P, hb):
     cfg = synth.CONFIGS["cfg3"]
     x = synth.make_tensor(cfg)
