@@ -40,6 +40,7 @@ BASE_SEED = 2001_07124
 
 # object ids inside the seed tuple
 _OBJ_CORE, _OBJ_FACTOR, _OBJ_NOISE, _OBJ_OMEGA, _OBJ_KRON, _OBJ_OMEGA_TILDE, _OBJ_KR, _OBJ_HOOI = 1, 2, 3, 4, 5, 6, 7, 8
+_OBJ_COUNT = 9
 
 
 def rng_for(*key: int) -> np.random.Generator:
@@ -202,6 +203,19 @@ def hooi_omegas(cfg: Config, sweeps: int) -> list:
             row.append(np.ascontiguousarray(rng_for(cfg.cfg_id, _OBJ_HOOI, it, n).standard_normal((rows, cfg.ranks[n]))))
         out.append(row)
     return out
+
+
+def count_codes(cfg: Config, n: int, K: Optional[int] = None, J: Optional[int] = None, step: int = 0) -> tuple:
+    """Count-sketch operand (codes, K) for mode n: label h_j uniform on [0, K) and
+    Rademacher sign s_j per column j of the (J_n-column) unfolding, packed as the int32 code
+    s_j (h_j + 1).  ``J`` defaults to J_n of X (STHOSVD passes the shrunken size, ``step`` keys
+    the stream)."""
+    K = cfg.K(n) if K is None else int(K)
+    J = cfg.J(n) if J is None else int(J)
+    rng = rng_for(cfg.cfg_id, _OBJ_COUNT, n, step)
+    h = rng.integers(0, K, size=J, dtype=np.int64)
+    s = rng.integers(0, 2, size=J, dtype=np.int64) * 2 - 1
+    return (s * (h + 1)).astype(np.int32), K
 
 
 def pet_sizes(cfg: Config, K: Optional[Sequence[int]] = None) -> tuple:

@@ -107,6 +107,38 @@ def sketch_kr(x: np.ndarray, n: int, omegas: Sequence[Optional[np.ndarray]], q: 
     return y0, y
 
 
+def count_decode(codes):
+    """Split the caller-drawn codes code_j = s_j (h_j + 1) into the hash labels h_j in [0, K)
+    and the Rademacher signs s_j (include/rtucker.h)."""
+    c = np.asarray(codes, dtype=np.int64)
+    if np.any(c == 0):
+        raise ValueError("count-sketch code 0 is invalid")
+    return np.abs(c) - 1, np.sign(c).astype(np.float64)
+
+
+def sketch_count(x: np.ndarray, n: int, omega, q: int = 0):
+    """Count-sketch mode-n sketch, the paper's three steps
+    on the columns of X_(n): (1) hashing -- column j carries the label h_j in 1..K (here 0..K-1);
+    (2) grouping the columns with the same label; (3) signing (s_j = +-1, footnote P:309) and
+    summing each group into its representative column Y0[:, c].  omega = (codes, K).
+    Power iterations (q > 0) continue with dense Z as in ``sketch_gauss``."""
+    codes, K = omega
+    xn = unfold(np.asarray(x, dtype=np.float64), n)
+    h, s = count_decode(codes)
+    if h.shape[0] != xn.shape[1] or np.any(h >= K):
+        raise ValueError("count-sketch codes do not match the unfolding")
+    y0 = np.zeros((xn.shape[0], K))
+    for c in range(K):
+        group = np.nonzero(h == c)[0]                       # step 2
+        y0[:, c] = xn[:, group] @ s[group]                  # step 3: signed column sum
+    y = y0
+    for _ in range(q):
+        qy, _ = qr_plus(y)
+        z, _ = qr_plus(xn.T @ qy)
+        y = xn @ z
+    return y0, y
+
+
 def sketch(x, n, kind, omega, q=0):
     if kind == "gauss":
         return sketch_gauss(x, n, omega, q)
@@ -114,6 +146,8 @@ def sketch(x, n, kind, omega, q=0):
         return sketch_kron(x, n, omega, q)
     if kind == "kr":
         return sketch_kr(x, n, omega, q)
+    if kind == "count":
+        return sketch_count(x, n, omega, q)
     raise ValueError(kind)
 
 
@@ -351,7 +385,7 @@ def hooi(x: np.ndarray, ranks: Sequence[int], iters: int = 50) -> dict:
     return dict(Q=qs, G=g, E=rel_error(x64, g, qs))
 
 
-__all__ = ["qr_plus", "sketch_gauss", "sketch_kron", "sketch_kr", "khatri_rao", "sketch", "core", "rel_error", "pet",
+__all__ = ["qr_plus", "sketch_gauss", "sketch_kron", "sketch_kr", "sketch_count", "count_decode", "khatri_rao", "sketch", "core", "rel_error", "pet",
            "rp_hooi",
            "rel_error_gram", "eig_desc", "canon_sign", "truncate_hosvd", "hosvd", "sthosvd",
            "thosvd", "sthosvd_det", "hooi", "unfold", "fold", "ttm", "multi_ttm", "reconstruct", "fro"]

@@ -565,3 +565,71 @@ def test_P27_rp_hooi_above_the_hooi_optimum():
     b = oracle.rp_hooi(x, cfg.ranks, a["Q"], synth.hooi_omegas(cfg, 3))
     c = oracle.hooi(x, cfg.ranks)
     assert c["E"] * (1 - 1e-9) <= b["E"]
+
+
+# ------------------------------------------------------------ count sketch
+def _explicit_count_matrix(codes, K):
+    """S in {0, +-1}^{J x K} written out entry by entry: S[j, h_j] = s_j."""
+    S = np.zeros((len(codes), K))
+    for j, v in enumerate(codes):
+        S[j, abs(int(v)) - 1] = 1.0 if v > 0 else -1.0
+    return S
+
+
+def test_P28_count_sketch_equals_explicit_sign_hash_matrix():
+    """The three-step count sketch (hash, group, signed sum) equals X_(n) S for the explicit
+    one-nonzero-per-row sign/hash matrix S, every mode, order 3 and 4, ragged sizes."""
+    for dims in [(7, 5, 6), (4, 3, 5, 2)]:
+        rng = np.random.default_rng(sum(dims))
+        x = rng.standard_normal(dims)
+        for n in range(len(dims)):
+            J = int(np.prod(dims)) // dims[n]
+            K = 3
+            codes = ((rng.integers(0, K, J) + 1) * (2 * rng.integers(0, 2, J) - 1)).astype(np.int32)
+            y0, _ = oracle.sketch(x, n, "count", (codes, K))
+            # X_(n)(i, j) with the Kolda j-index (P:99-105), written as loops over the entries
+            xn = np.zeros((dims[n], J))
+            for idx in np.ndindex(*dims):
+                j, stride = 0, 1
+                for k in range(len(dims)):
+                    if k == n:
+                        continue
+                    j += idx[k] * stride
+                    stride *= dims[k]
+                xn[idx[n], j] = x[idx]
+            assert np.allclose(y0, xn @ _explicit_count_matrix(codes, K), atol=1e-13, rtol=0)
+
+
+def test_P29_count_sketch_permutation_is_column_permutation():
+    """K = J with distinct labels and all signs +: Y0 is X_(n) with its columns permuted."""
+    rng = np.random.default_rng(29)
+    x = rng.standard_normal((6, 4, 5))
+    J = 20
+    perm = rng.permutation(J)
+    y0, _ = oracle.sketch(x, 0, "count", ((perm + 1).astype(np.int32), J))
+    xn = x.reshape(6, J, order="F")
+    assert np.array_equal(y0[:, perm], xn)
+
+
+def test_P30_count_sketch_norm_unbiased():
+    """E[S S^T] = I for Rademacher signs (footnote P:309): the mean of ||Y0||_F^2 over draws is
+    ||X||_F^2 (a dropped sign gives cross terms and fails this by far)."""
+    rng = np.random.default_rng(30)
+    x = rng.standard_normal((8, 6, 5)) + 1.0                  # non-zero mean: cross terms matter
+    J, K, draws = 30, 4, 3000
+    acc = 0.0
+    for _ in range(draws):
+        codes = ((rng.integers(0, K, J) + 1) * (2 * rng.integers(0, 2, J) - 1)).astype(np.int32)
+        acc += np.sum(oracle.sketch(x, 0, "count", (codes, K))[0] ** 2)
+    assert abs(acc / draws / np.sum(x ** 2) - 1.0) < 0.03
+
+
+def test_P31_count_sketch_hosvd_exact_rank_recovery():
+    """RP-HOSVD with count-sketch operators (K_n = R + p) recovers an exact multilinear-rank
+    tensor: the sketch X_(n) S spans range(X_(n)) for generic labels/signs; E < 1e-10."""
+    dims, r = (24, 22, 20), 3
+    x, _ = _lowrank(31, dims, r)
+    cfg = synth.CONFIGS["cfg1"].scaled(dims, (r,) * 3, (r,) * 3)
+    oms = [synth.count_codes(cfg, n, K=r + 3) for n in range(3)]
+    out = oracle.hosvd(x, (r,) * 3, oms, q=0, kind="count")
+    assert out["E"] < 1e-10
