@@ -59,7 +59,7 @@ typedef enum { RT_F32 = 0, RT_F64 = 1 } rt_dtype;
 
 /* Sketch operator of the range finder: dense Gaussian Omega_n (Eq. proj, P:162-172;
  * Alg.6 line 3) or the Kronecker-structured X x_{k!=n} Omega_k^T. */
-typedef enum { RT_OMEGA_GAUSS = 0, RT_OMEGA_KRON = 1, RT_OMEGA_KR = 2 } rt_omega_kind;
+typedef enum { RT_OMEGA_GAUSS = 0, RT_OMEGA_KRON = 1, RT_OMEGA_KR = 2, RT_OMEGA_COUNT = 3 } rt_omega_kind;
 
 typedef struct rt_handle rt_handle;
 
@@ -129,8 +129,14 @@ rt_status rt_profile_read(rt_handle* h, rt_profile_entry* out, int cap, int* n, 
  * kind == KR   : Khatri-Rao sketch (P:510 footnote; KR product P:317):
  *                Y = X_(n) (Omega_N (.) ... (.) Omega_1, without n); omega[k] is row-major d_k x K
  *                for every k != mode (same K, d_{N-1} local on a slab), omega_ld[k] >= K, K <= 128.
+ * kind == COUNT: count sketch: Y = X_(n) S with S in {0,+-1}^{J_n x K}, one nonzero
+ *                per row; omega[mode] is a device int32 array of J_n codes (local columns if
+ *                mode < N-1 on a slab, in the j order of X_(n)), code_j = s_j (h_j + 1) with the
+ *                group h_j in [0, K) and the sign s_j = +-1 drawn by the caller;
+ *                omega_cols[mode] = K, omega_ld ignored.  A code outside [-K,-1] U [1,K] makes
+ *                rt_sync return RT_EINVAL (the element is skipped).
  * Y: fp64 col-major I_n x K, ld ldy >= I_n (local rows for mode N-1 on a slab).
- * Requires 1 <= K <= min(I_n, J_n) (global sizes) and K <= 256. */
+ * Requires 1 <= K <= min(I_n, J_n) (global sizes) and K <= 128. */
 rt_status rtucker_sketch(rt_handle* h, const rt_tensor* X, int mode, rt_omega_kind kind,
                          const void* const* omega, const int64_t* omega_cols, const int64_t* omega_ld, int q,
                          double* Y, int64_t ldy);
@@ -163,6 +169,8 @@ rt_status rtucker_core(rt_handle* h, const rt_tensor* X, const double* const* Q,
  *   KRON: entries [n*N+k], k != n, are Omega_k^{(n)} (I_k x L_k, row-major), omega_cols = L_k,
  *   K_n = prod_{k!=n} L_k >= min(R_n + p, I_n) and K_n <= I_n.
  *   KR: entries [n*N+k], k != n, are Omega_k^{(n)} (I_k x K_n, row-major), K_n = min(R_n + p, I_n, J_n).
+ *   COUNT: entry [n*N+n] is the int32 code array of mode n (J_n codes, see (1)), omega_cols[n*N+n]
+ *   = K_n = min(R_n + p, I_n, J_n).
  * Q_out[n]: fp64 col-major I_n x R_n (ld I_n, local rows for n = N-1 on a slab).
  * G_out: fp64 R_1 x ... x R_N.  rel_err / rel_err_gram: device fp64 scalars, nullable. */
 rt_status rtucker_hosvd(rt_handle* h, const rt_tensor* X, const int64_t* R, int p, int q,
@@ -176,7 +184,7 @@ rt_status rtucker_hosvd(rt_handle* h, const rt_tensor* X, const int64_t* R, int 
  *     S = B x_n U^T (ΛV^T shortcut).  G = S.
  * mode_order: permutation of 0..N-1, NULL = ascending.  Omega tables as in
  *   (4) but sized for the working tensor: when mode n is processed, already-processed
- *   modes m have size R_m (GAUSS: J_n = prod of current sizes; KRON: d_k current).
+ *   modes m have size R_m (GAUSS/COUNT: J_n = prod of current sizes; KRON: d_k current).
  * Single-GPU only for now (RT_EUNSUPPORTED on a sharded tensor with a communicator). */
 rt_status rtucker_sthosvd(rt_handle* h, const rt_tensor* X, const int64_t* R, int p, int q,
                           rt_omega_kind kind, const void* const* omega, const int64_t* omega_cols,

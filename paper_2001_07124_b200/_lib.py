@@ -15,7 +15,7 @@ RT_OK, RT_EINVAL, RT_ERANK, RT_ENOMEM, RT_ECUDA, RT_ENCCL, RT_ENUMERIC, RT_EUNSU
 STATUS_NAMES = {0: "RT_OK", -1: "RT_EINVAL", -2: "RT_ERANK", -3: "RT_ENOMEM", -4: "RT_ECUDA", -5: "RT_ENCCL",
                 -6: "RT_ENUMERIC", -7: "RT_EUNSUPPORTED"}
 RT_F32, RT_F64 = 0, 1
-RT_OMEGA_GAUSS, RT_OMEGA_KRON, RT_OMEGA_KR = 0, 1, 2
+RT_OMEGA_GAUSS, RT_OMEGA_KRON, RT_OMEGA_KR, RT_OMEGA_COUNT = 0, 1, 2, 3
 RT_OPT_TTM_IMPL, RT_OPT_PROFILE, RT_OPT_QR_FALLBACK, RT_OPT_OMEGA_TF32, RT_OPT_TC_SEGMENT, RT_OPT_TC_SKEW = 0, 1, 2, 3, 4, 5
 
 EXPORTS = ["rt_get_unique_id", "rt_create", "rt_loopback_group_create", "rt_loopback_group_destroy",

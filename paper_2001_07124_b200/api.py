@@ -186,6 +186,11 @@ def _omega_table(N: int, omegas, kind: str):
     lds = [0] * (N * N)
     keep = []
     for n in range(N):
+        if kind == "count":
+            codes, K = _count_codes(omegas[n])
+            keep.append(codes)
+            ptrs[n * N + n], cols[n * N + n], lds[n * N + n] = codes, K, 1
+            continue
         entries = [(n, omegas[n])] if kind == "gauss" else \
             [(k, omegas[n][k]) for k in range(N) if k != n and omegas[n][k] is not None]
         for k, om in entries:
@@ -198,7 +203,16 @@ def _omega_table(N: int, omegas, kind: str):
 
 
 def _kind(kind: str) -> int:
-    return {"gauss": L.RT_OMEGA_GAUSS, "kron": L.RT_OMEGA_KRON, "kr": L.RT_OMEGA_KR}[kind]
+    return {"gauss": L.RT_OMEGA_GAUSS, "kron": L.RT_OMEGA_KRON, "kr": L.RT_OMEGA_KR,
+            "count": L.RT_OMEGA_COUNT}[kind]
+
+
+def _count_codes(entry):
+    """Count-sketch operand (codes, K): codes = int32 device vector, code_j = s_j (h_j + 1)."""
+    codes, K = entry
+    if codes.dtype != torch.int32 or codes.dim() != 1:
+        raise ValueError("count-sketch codes must be a 1-D int32 tensor")
+    return codes.contiguous(), int(K)
 
 
 def rtucker_sketch(h: Handle, X: torch.Tensor, mode: int, omega, q: int = 0, kind: str = "gauss",
@@ -207,7 +221,12 @@ def rtucker_sketch(h: Handle, X: torch.Tensor, mode: int, omega, q: int = 0, kin
     desc = tensor_desc(X, last_offset, last_global)
     N = desc.order
     ptrs, cols, lds, keep = [None] * N, [0] * N, [0] * N, []
-    if kind == "gauss":
+    if kind == "count":
+        codes, K = _count_codes(omega)
+        keep.append(codes)
+        if 0 <= mode < N:
+            ptrs[mode], cols[mode], lds[mode] = codes, K, 1
+    elif kind == "gauss":
         om, ld = rowmajor_ld(omega)
         keep.append(om)
         K = om.shape[1]

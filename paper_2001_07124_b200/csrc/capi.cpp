@@ -101,6 +101,15 @@ int64_t check_kr_omega(const rt::TView& X, int n, const void* const* om, const i
   return K;
 }
 
+// count sketch: one int32 code per (local) column of X_(n), K_n groups
+void check_count_omega(const rt::TView& X, int n, const void* om, int64_t K, bool strict = true) {
+  RT_REQUIRE(om != nullptr && (reinterpret_cast<uintptr_t>(om) % 4) == 0, rt::kEINVAL,
+             "count-sketch codes must be an aligned device pointer");
+  RT_REQUIRE(K >= 1, rt::kEINVAL, "omega_cols (number of count-sketch groups) must be >= 1");
+  RT_REQUIRE(!strict || (K <= X.Ig(n) && K <= X.Jg(n)), rt::kERANK, "K_n must be <= min(I_n, J_n)");
+  RT_REQUIRE(K <= 128, rt::kEUNSUPPORTED, "K_n > 128 not supported");
+}
+
 int64_t check_kron_omega(const rt::TView& X, int n, const void* const* om, const int64_t* cols, const int64_t* lds,
                          bool strict = true) {
   int64_t K = 1;
@@ -199,6 +208,7 @@ rt_status rt_sync(rt_handle* h) {
   });
   if (r != RT_OK) return r;
   if (st & rt::kStatusNonFinite) return fail(h, RT_ENUMERIC, "non-finite values in the input or a sketch");
+  if (st & rt::kStatusBadHash) return fail(h, RT_EINVAL, "count-sketch code outside [-K, -1] U [1, K]");
   if (st & rt::kStatusCholBreakdown) return fail(h, RT_ENUMERIC, "Cholesky breakdown in the thin QR after the shift");
   return RT_OK;
 }
@@ -266,6 +276,7 @@ rt_status rtucker_sketch(rt_handle* h, const rt_tensor* X, int mode, rt_omega_ki
     if (kind == RT_OMEGA_GAUSS) { K = omega_cols[mode]; check_gauss_omega(v, mode, omega[mode], K, omega_ld[mode], q > 0); }
     else if (kind == RT_OMEGA_KRON) K = check_kron_omega(v, mode, omega, omega_cols, omega_ld, q > 0);
     else if (kind == RT_OMEGA_KR) K = check_kr_omega(v, mode, omega, omega_cols, omega_ld, q > 0);
+    else if (kind == RT_OMEGA_COUNT) { K = omega_cols[mode]; check_count_omega(v, mode, omega[mode], K, q > 0); }
     else throw rt::Error(rt::kEINVAL, "unknown omega kind");
     const int64_t In = v.d[mode];
     double* Yt = (ldy == In) ? Y : h->ws.alloc_n<double>(In * K);
@@ -343,7 +354,7 @@ static void check_driver_args(const rt::TView& v, const int64_t* R, int p, int q
                               double* const* Q_out, double* G_out, const int64_t* cur_dims) {
   RT_REQUIRE(R && omega && omega_cols && omega_ld && Q_out && G_out, rt::kEINVAL, "NULL argument");
   RT_REQUIRE(p >= 0 && q >= 0, rt::kEINVAL, "p and q must be >= 0");
-  RT_REQUIRE(kind == RT_OMEGA_GAUSS || kind == RT_OMEGA_KRON || kind == RT_OMEGA_KR, rt::kEINVAL,
+  RT_REQUIRE(kind == RT_OMEGA_GAUSS || kind == RT_OMEGA_KRON || kind == RT_OMEGA_KR || kind == RT_OMEGA_COUNT, rt::kEINVAL,
              "unknown omega kind");
   const int N = v.N;
   for (int n = 0; n < N; ++n) {
@@ -359,6 +370,11 @@ static void check_driver_args(const rt::TView& v, const int64_t* R, int p, int q
       check_gauss_omega(w, n, om[n], K, ol[n]);
       RT_REQUIRE(K == std::min<int64_t>(R[n] + p, std::min(w.Ig(n), w.Jg(n))), rt::kEINVAL,
                  "Gaussian width must be K_n = min(R_n + p, I_n, J_n)");
+    } else if (kind == RT_OMEGA_COUNT) {
+      K = oc[n];
+      check_count_omega(w, n, om[n], K);
+      RT_REQUIRE(K == std::min<int64_t>(R[n] + p, std::min(w.Ig(n), w.Jg(n))), rt::kEINVAL,
+                 "count-sketch width must be K_n = min(R_n + p, I_n, J_n)");
     } else if (kind == RT_OMEGA_KR) {
       K = check_kr_omega(w, n, om, oc, ol);
       RT_REQUIRE(K == std::min<int64_t>(R[n] + p, std::min(w.Ig(n), w.Jg(n))), rt::kEINVAL,

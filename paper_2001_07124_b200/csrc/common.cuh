@@ -37,6 +37,7 @@ constexpr int kEINVAL = -1, kERANK = -2, kENOMEM = -3, kECUDA = -4, kENCCL = -5,
 // device status bits (latched by kernels, read by rt_sync)
 constexpr int kStatusCholBreakdown = 1;
 constexpr int kStatusNonFinite = 2;
+constexpr int kStatusBadHash = 4;     // count-sketch code outside [-K, -1] U [1, K]
 
 __host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

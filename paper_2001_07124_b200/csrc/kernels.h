@@ -31,6 +31,11 @@ template <typename Tw, typename To>
 void kr_ttv(const Ctx& ctx, const Tw* W, Box box, const To* Om, int64_t ld, int K, bool c_in_a, int64_t c_stride,
             double* out);
 
+// Count sketch: Y(i, c) = sum_{j: |code_j| = c+1} sign(code_j) X_(n)(i, j); Y fp64 col-major
+// I x K (ldy), zeroed here.  Out-of-range codes latch kStatusBadHash (reported by rt_sync).
+template <typename T>
+void count_sketch(const Ctx& ctx, const T* X, Box box, const int32_t* code, int K, double* Y, int64_t ldy);
+
 // tcgen05 tensor-core versions (ttm_tc.cu), fp32 only, 3xTF32 split.  Return false (nothing
 // launched) when the shape/alignment is outside the TMA path; callers then use the SIMT kernels.
 // ttm_s_tc: B row-major (element (j,k) at j*ldb + k, ldb % 4 == 0, 16-byte aligned), consumed as an

@@ -177,6 +177,10 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
     }
     ttm_s_dispatch(ctx, ws, data, bx, om, ld, ctx.omega_tf32 != 0, K, Yt, In);
     ws.rewind(mo);
+  } else if (kind == 3) {
+    // count sketch: hash, group, sign and sum the columns of X_(n); no multiplications
+    K = int(omega_cols[n]);
+    count_sketch<T>(ctx, data, bx, static_cast<const int32_t*>(omega[n]), K, Yt, In);
   } else if (kind == 2) {
     // Khatri-Rao sketch (P:510 footnote): Y[:, c] = X x_{k!=n} Omega_k[:, c]^T.  One TTM with the
     // first factor (Omega_k0: I_k0 x K, row-major) streams X; each further mode is a TTV whose
@@ -465,7 +469,7 @@ void Engine::hosvd(const TView& X, const int64_t* R, int q, int kind, const void
     const void* const* om = omega + n * N;
     const int64_t* oc = omega_cols + n * N;
     const int64_t* ol = omega_ld + n * N;
-    if (kind == 0) K[n] = oc[n];
+    if (kind == 0 || kind == 3) K[n] = oc[n];
     else if (kind == 2) K[n] = oc[n == 0 ? 1 : 0];
     else { K[n] = 1; for (int k = 0; k < N; ++k) if (k != n) K[n] *= oc[k]; }
     const int64_t In = X.d[n];
@@ -508,7 +512,7 @@ void Engine::sthosvd(const TView& X, const int64_t* R, int q, int kind, const vo
     const int64_t* oc = omega_cols + n * N;
     const int64_t* ol = omega_ld + n * N;
     int K;
-    if (kind == 0) K = int(oc[n]);
+    if (kind == 0 || kind == 3) K = int(oc[n]);
     else if (kind == 2) K = int(oc[n == 0 ? 1 : 0]);
     else { K = 1; for (int k = 0; k < N; ++k) if (k != n) K *= int(oc[k]); }
     const int64_t In = S.d[n];
@@ -522,6 +526,7 @@ void Engine::sthosvd(const TView& X, const int64_t* R, int q, int kind, const vo
       const void* om64[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
       int64_t ld64[5] = {0, 0, 0, 0, 0};
       for (int k = 0; k < N; ++k) {
+        if (kind == 3) { om64[k] = om[k]; ld64[k] = ol[k]; continue; }     // int32 codes: no conversion
         if (!om[k] || (kind == 0 && k != n) || (kind != 0 && k == n)) continue;
         const int64_t rows = (kind == 0) ? S.box(n).J() : S.d[k];
         if (DT<T>::id == 1) { om64[k] = om[k]; ld64[k] = ol[k]; continue; }
