@@ -34,7 +34,7 @@ void kr_ttv(const Ctx& ctx, const Tw* W, Box box, const To* Om, int64_t ld, int 
 // Count sketch: Y(i, c) = sum_{j: |code_j| = c+1} sign(code_j) X_(n)(i, j); Y fp64 col-major
 // I x K (ldy), zeroed here.  Out-of-range codes latch kStatusBadHash (reported by rt_sync).
 template <typename T>
-void count_sketch(const Ctx& ctx, const T* X, Box box, const int32_t* code, int K, double* Y, int64_t ldy);
+void count_sketch(const Ctx& ctx, Arena& ws, const T* X, Box box, const int32_t* code, int K, double* Y, int64_t ldy);
 
 // tcgen05 tensor-core versions (ttm_tc.cu), fp32 only, 3xTF32 split.  Return false (nothing
 // launched) when the shape/alignment is outside the TMA path; callers then use the SIMT kernels.

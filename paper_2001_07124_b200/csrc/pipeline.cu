@@ -180,7 +180,7 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
   } else if (kind == 3) {
     // count sketch: hash, group, sign and sum the columns of X_(n); no multiplications
     K = int(omega_cols[n]);
-    count_sketch<T>(ctx, data, bx, static_cast<const int32_t*>(omega[n]), K, Yt, In);
+    count_sketch<T>(ctx, ws, data, bx, static_cast<const int32_t*>(omega[n]), K, Yt, In);
   } else if (kind == 2) {
     // Khatri-Rao sketch (P:510 footnote): Y[:, c] = X x_{k!=n} Omega_k[:, c]^T.  One TTM with the
     // first factor (Omega_k0: I_k0 x K, row-major) streams X; each further mode is a TTV whose

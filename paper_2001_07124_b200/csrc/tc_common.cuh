@@ -190,5 +190,9 @@ __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) 
   lo = __float_as_uint(x - __uint_as_float(h));
 }
 
+// host: fp32 tiled tensor map (ttm_tc.cu); false if the driver rejects it
+bool encode_f32_map(CUtensorMap* m, const void* ptr, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+                    const uint32_t* box, bool swz128);
+
 }  // namespace tc
 }  // namespace rt

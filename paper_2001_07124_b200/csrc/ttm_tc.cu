@@ -761,6 +761,13 @@ __global__ void split_q_kernel(const float* __restrict__ Q, int64_t I, int C, in
 
 }  // namespace
 
+namespace tc {
+bool encode_f32_map(CUtensorMap* m, const void* ptr, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+                    const uint32_t* box, bool swz128) {
+  return make_map(m, ptr, rank, dims, strides_bytes, box, swz128);
+}
+}  // namespace tc
+
 int tc_npad(int K) {
   return K <= 16 ? 16 : K <= 32 ? 32 : K <= 48 ? 48 : K <= 64 ? 64 : K <= 80 ? 80 : K <= 96 ? 96 : K <= 128 ? 128 : -1;
 }
