@@ -42,7 +42,23 @@ void ttm_s_dispatch(const Ctx& ctx, Arena& ws, const double* X, Box box, const d
 // out(alpha,c,beta) = sum_i X(alpha,i,beta) Q(i,c), Q col-major (ldq)
 void ttm_t_dispatch(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
                     int64_t so_a, int64_t so_c, int64_t so_b) {
-  if (ctx.ttm_impl != 1 && ttm_t_tc(ctx, ws, X, box, Q, ldq, C, out, so_a, so_c, so_b)) return;
+  if (ctx.ttm_impl != 1) {
+    if (C <= 128) {
+      if (ttm_t_tc(ctx, ws, X, box, Q, ldq, C, out, so_a, so_c, so_b)) return;
+    } else {
+      // wider than one TMEM tile (e.g. the R-PET core sketch, S_n = 2K_n + 1): balanced column
+      // chunks of <= 128, one X pass each, each writing its slice of the output
+      const int nch = int(cdiv(C, 128));
+      const int cw = int(cdiv(C, nch) + 3) & ~3;
+      if (ttm_t_tc(ctx, ws, X, box, Q, ldq, cw, out, so_a, so_c, so_b)) {
+        for (int c0 = cw; c0 < C; c0 += cw)
+          RT_REQUIRE(ttm_t_tc(ctx, ws, X, box, Q + int64_t(c0) * ldq, ldq, std::min(cw, C - c0), out + c0 * so_c, so_a,
+                              so_c, so_b),
+                     kEINVAL, "ttm_t: tensor-core chunk rejected after the first");   // same shape: unreachable
+        return;
+      }
+    }
+  }
   ttm_t<float, float, float>(ctx, X, box, Q, 1, ldq, C, out, so_a, so_c, so_b);
 }
 void ttm_t_dispatch(const Ctx& ctx, Arena&, const double* X, Box box, const double* Q, int64_t ldq, int C, double* out,
@@ -579,7 +595,7 @@ void Engine::pet(const TView& X, const int64_t* R, const void* const* omega, con
   const int N = X.N;
   const T* data = static_cast<const T*>(X.data);
   const auto mk = ws.mark();
-  int64_t K[5], ldq[5], ldw[5];
+  int64_t K[5], ldq[5], ldw[5], Sp[5];
   double* Qt[5];
   double* Wt[5];
   for (int n = 0; n < N; ++n) {
@@ -594,34 +610,68 @@ void Engine::pet(const TView& X, const int64_t* R, const void* const* omega, con
     Qt[n] = ws.alloc_n<double>(In * K[n]);
     ldq[n] = In;
     qr_y(Yt, In, X.Ig(n), int(K[n]), In, Qt[n], In, nullptr, last && dist(), last ? X.off : 0);   // line 2
-    // Omega~_n (S_n x I_n row-major, pitch ld) is Omega~_n^T as a col-major I_n x S_n matrix
-    Wt[n] = ws.alloc_n<double>(In * S[n]);
+    // Omega~_n (S_n x I_n row-major, pitch ld) is Omega~_n^T as a col-major I_n x S_n matrix.
+    // Sp_n = S_n rounded up to a multiple of 4 with zero rows: the core-sketch intermediates then
+    // keep 16-byte rows (tensor-core TTM for the later stages); the zero slices of H meet zero
+    // rows of A = Omega~_n Q^(n) in line 4, so S is unchanged.
+    Sp[n] = pad4(S[n]);
+    Wt[n] = ws.alloc_n<double>(In * Sp[n]);
     ldw[n] = In;
+    if (Sp[n] != S[n]) fill_zero(ctx, Wt[n], sizeof(double) * In * Sp[n]);
     convert2d<T, double>(ctx, static_cast<const T*>(omega_tilde[n]), In, S[n], omega_tilde_ld[n], Wt[n], In);
   }
   int64_t hsz = 1;
-  for (int n = 0; n < N; ++n) hsz *= S[n];
+  for (int n = 0; n < N; ++n) hsz *= Sp[n];
   double* H = ws.alloc_n<double>(hsz);
-  core<T>(X, data, Wt, ldw, S, H);                                                 // line 3 (C4)
+  {
+    // line 3 (C4): H = X x_1 Omega~_1 ... x_N Omega~_N.  The first stage streams X (tensor cores
+    // for fp32); the later stages accumulate in fp64 with fp64 intermediates: line 4 does not
+    // project, so E is first-order sensitive to H (reading R26)
+    const auto mh = ws.mark();
+    int64_t cur[5];
+    for (int k = 0; k < N; ++k) cur[k] = X.d[k];
+    const Box b0 = TView::box_of(cur, N, 0);
+    int64_t ld0;
+    const T* w0 = working_copy<T>(ctx, ws, Wt[0], X.d[0], Sp[0], ldw[0], ld0);
+    T* h1 = ws.alloc_n<T>(b0.a * Sp[0] * b0.b);
+    ttm_t_dispatch(ctx, ws, data, b0, w0, ld0, int(Sp[0]), h1, 1, b0.a, b0.a * Sp[0]);
+    cur[0] = Sp[0];
+    const double* src = nullptr;
+    for (int n = 1; n < N; ++n) {
+      const Box b = TView::box_of(cur, N, n);
+      double* dst = (n == N - 1) ? H : ws.alloc_n<double>(b.a * Sp[n] * b.b);
+      LabelScope ls(ctx, "pet_hchain");
+      if (n == 1) ttm_t<T, double, double>(ctx, h1, b, Wt[n], 1, ldw[n], int(Sp[n]), dst, 1, b.a, b.a * Sp[n]);
+      else ttm_t<double, double, double>(ctx, src, b, Wt[n], 1, ldw[n], int(Sp[n]), dst, 1, b.a, b.a * Sp[n]);
+      src = dst;
+      cur[n] = Sp[n];
+    }
+    allreduce(comm, dist(), H, hsz, ctx.stream);
+    ws.rewind(mh);
+  }
   // line 4: S = H x_n (Omega~_n Q^(n))^+
   int64_t cur[5];
-  for (int k = 0; k < N; ++k) cur[k] = S[k];
+  for (int k = 0; k < N; ++k) cur[k] = Sp[k];
   const double* src = H;
   double* Sc = nullptr;
   for (int n = 0; n < N; ++n) {
-    const int s = int(S[n]), k = int(K[n]);
+    const int s = int(Sp[n]), k = int(K[n]);
     double* A = ws.alloc_n<double>(int64_t(s) * k);
-    gemm_small(ctx, true, false, s, k, int(X.d[n]), Wt[n], int(ldw[n]), Qt[n], int(ldq[n]), A, s);
+    // A = Omega~_n Q^(n) = W^T Q: the col-major I_n x S_n matrix W viewed as the mode-1 box
+    // [a = I_n, I = S_n, b = 1] of a sketch with B = Q (row j, column c at j + ldq c)
+    ttm_s<double>(ctx, ws, Wt[n], Box{X.d[n], s, 1}, Qt[n], 1, ldq[n], k, A, s);
     allreduce(comm, n == N - 1 && dist(), A, int64_t(s) * k, ctx.stream);            // rows of the last mode
     double* G = ws.alloc_n<double>(int64_t(k) * k);
     double* Rc = ws.alloc_n<double>(int64_t(k) * k);
     double* Ri = ws.alloc_n<double>(int64_t(k) * k);
+    double* RiT = ws.alloc_n<double>(int64_t(k) * k);
     double* T1 = ws.alloc_n<double>(int64_t(s) * k);
     double* M = ws.alloc_n<double>(int64_t(s) * k);
-    gemm_small(ctx, true, false, k, k, s, A, s, A, s, G, k);                      // A^T A
+    gram<double>(ctx, ws, A, s, k, s, G);                                         // A^T A
     chol_inv(ctx, G, k, 0.0, Rc, Ri, nullptr);                                    // A^T A = Rc^T Rc
-    gemm_small(ctx, false, false, s, k, k, A, s, Ri, k, T1, s);                   // A Rc^-1
-    gemm_small(ctx, false, true, s, k, k, T1, s, Ri, k, M, s);                    // (A^+)^T = A (A^T A)^-1
+    gemm_tall<double, double>(ctx, A, s, k, s, Ri, k, k, T1, s);                  // A Rc^-1
+    transpose_copy<double>(ctx, Ri, k, k, k, RiT, k);                             // Rc^-T (col-major)
+    gemm_tall<double, double>(ctx, T1, s, k, s, RiT, k, k, M, s);                 // (A^+)^T = A (A^T A)^-1
     const Box b = TView::box_of(cur, N, n);
     double* dst = ws.alloc_n<double>(b.a * k * b.b);
     LabelScope ls(ctx, "pet_recover");
