@@ -739,9 +739,18 @@ __global__ void splitk_reduce_f32_kernel(const float* __restrict__ part, int64_t
   const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (e >= I * K) return;
   const int64_t i = e % I, k = e / I;
-  double s = 0.0;
-  for (int z = 0; z < splits; ++z) s += double(part[(int64_t(z) * K + k) * I + i]);
-  Y[i + ldy * k] = s;
+  // 8 independent loads in flight per thread (the split count is ~37: a dependent chain of
+  // global loads would make this tiny reduction latency-bound); fixed summation order
+  const float* pp = part + k * I + i;
+  const int64_t zs = int64_t(K) * I;
+  double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int z = 0;
+  for (; z + 8 <= splits; z += 8) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s[u] += double(__ldg(pp + (z + u) * zs));
+  }
+  for (int u = 0; z < splits; ++z, ++u) s[u] += double(__ldg(pp + z * zs));
+  Y[i + ldy * k] = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
 }
 
 // Q (I x C, col-major ldq) -> Q2 (I x 2 npad, col-major ld2): columns [0, C) = tf32 hi, columns
