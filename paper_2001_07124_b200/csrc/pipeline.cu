@@ -430,7 +430,7 @@ void Engine::rel_error(const TView& X, const T* data, const double* G, const int
   for (int n = 0; n < N - 1; ++n) {
     const Box b = TView::box_of(cur, N, n);
     const int64_t In = X.d[n];
-    LabelScope ls(ctx, "pchain_simt");
+    LabelScope ls(ctx, "pchain");
     if (n == N - 2) {
       P = ws.alloc_n<T>(b.a * In * b.b);
       if constexpr (std::is_same<T, float>::value) {
@@ -440,7 +440,13 @@ void Engine::rel_error(const TView& X, const T* data, const double* G, const int
         float* qf = ws.alloc_n<float>(In * b.I);
         convert2d<double, float>(ctx, src, b.a * b.I * b.b, 1, b.a * b.I * b.b, sf, b.a * b.I * b.b);
         convert2d<double, float>(ctx, Q[n], In, b.I, In, qf, In);
-        ttm_t<float, float, float>(ctx, sf, b, qf, In, 1, int(In), P, 1, b.a, b.a * In);
+        // tensor cores: M(i = r, c = i_n) = Q[i_n, r] as a col-major R x I_n matrix (ld pad4(R));
+        // I_n > 128 output columns run as column chunks that re-read the small source from L2
+        const int64_t ldt = pad4(b.I);
+        float* qt = ws.alloc_n<float>(ldt * In);
+        if (ldt != b.I) fill_zero(ctx, qt, sizeof(float) * ldt * In);
+        transpose_copy<float>(ctx, qf, b.I, In, In, qt, ldt);
+        ttm_t_dispatch(ctx, ws, sf, b, qt, ldt, int(In), P, 1, b.a, b.a * In);
       } else {
         ttm_t<double, double, T>(ctx, src, b, Q[n], In, 1, int(In), P, 1, b.a, b.a * In);
       }

@@ -169,85 +169,104 @@ void launch_ttm_s(const Ctx& ctx, Arena& ws, const T* X, Box box, const T* Bm, i
 }
 
 // ------------------------------------------------------------------ ttm_t
-// Block tile: BM = 128 outputs j, BI contraction rows per stage, BN = 8*TN output cols c.
-// 256 threads = 32 (j, lanes) x 8 (c, warps); thread owns j in {tx + 32 r}, c in {ty + 8 cc}.
-template <typename Tin, typename Tm, typename Tout, int TN>
+// Block tile: BM = 32 RJ outputs j, BI contraction rows per stage, BN = 8 TN output cols c.
+// 256 threads = 32 (j, lanes) x 8 (c, warps); thread owns j in {tx + 32 r, r < RJ}, c in {ty + 8 cc}.
+// The next stage's X and M elements are loaded into registers while the current stage is
+// multiplied out of shared memory (global latency hidden behind the FMAs).
+template <typename Tin, typename Tm, typename Tout, int TN, int RJ>
 __global__ void __launch_bounds__(256)
 ttm_t_kernel(const Tin* __restrict__ X, int64_t a, int64_t I, int64_t J, const Tm* __restrict__ Mm,
              int64_t ms_i, int64_t ms_c, int C, Tout* __restrict__ out, int64_t so_a, int64_t so_c,
              int64_t so_b) {
   using Tacc = typename Acc3<Tin, Tm, Tout>::type;
-  constexpr int BM = 128;
-  constexpr int BI = sizeof(Tacc) == 8 ? 16 : 32;
+  constexpr int BM = 32 * RJ;
+  constexpr int BI = sizeof(Tacc) == 8 ? 8 : 16;
   constexpr int BN = 8 * TN;
+  constexpr int XL = BI * BM / 256;          // X elements per thread per stage
+  constexpr int ML = (BI * BN + 255) / 256;  // M elements per thread per stage
   __shared__ Tacc Xs[BI][BM + 1];
   __shared__ Tacc Ms[BI][BN];
   const int t = threadIdx.x, tx = t & 31, ty = t >> 5;
   const int64_t j0 = int64_t(blockIdx.x) * BM;
   const int c0 = blockIdx.y * BN;
   const int64_t aI = a * I;
-  Tacc acc[4][TN];
+  Tacc acc[RJ][TN];
 #pragma unroll
-  for (int r = 0; r < 4; ++r)
+  for (int r = 0; r < RJ; ++r)
 #pragma unroll
     for (int c = 0; c < TN; ++c) acc[r][c] = Tacc(0);
 
-  // a > 1 loader: this thread always loads column jl = t & 127
-  const int jl_b = t & 127;
+  // X loader.  a > 1: thread loads column jl = t % BM for rows il = t / BM + (256 / BM) s.
+  // a == 1 (X(j, i) = X[i + I j], contiguous in i): il = t % BI, jl = t / BI + (256 / BI) s.
+  const int jl_b = t % BM;
   const int64_t j_b = j0 + jl_b;
   const bool jv_b = j_b < J;
   const int64_t off_b = jv_b ? (j_b % a) + aI * (j_b / a) : 0;
-
-  for (int64_t ic = 0; ic < I; ic += BI) {
-    if (a == 1) {                       // mode 0: X(j,i) = X[i + I*j], contiguous in i
+  Tacc xv[XL], mv[ML];
+  auto load = [&](int64_t ic) {
+    if (a == 1) {
       const int il = t % BI;
       const int64_t i = ic + il;
 #pragma unroll
-      for (int s = 0; s < BM * BI / 256; ++s) {
-        const int jl = t / BI + (256 / BI) * s;
-        const int64_t j = j0 + jl;
-        Xs[il][jl] = (j < J && i < I) ? Tacc(X[i + I * j]) : Tacc(0);
+      for (int s2 = 0; s2 < XL; ++s2) {
+        const int64_t j = j0 + t / BI + (256 / BI) * s2;
+        xv[s2] = (j < J && i < I) ? Tacc(X[i + I * j]) : Tacc(0);
       }
     } else {
 #pragma unroll
-      for (int s = 0; s < BI / 2; ++s) {
-        const int il = (t >> 7) + 2 * s;
-        const int64_t i = ic + il;
-        Xs[il][jl_b] = (jv_b && i < I) ? Tacc(X[off_b + a * i]) : Tacc(0);
+      for (int s2 = 0; s2 < XL; ++s2) {
+        const int64_t i = ic + t / BM + (256 / BM) * s2;
+        xv[s2] = (jv_b && i < I) ? Tacc(X[off_b + a * i]) : Tacc(0);
       }
     }
-    if (ms_c == 1) {
-      for (int e = t; e < BI * BN; e += 256) {
-        const int cl = e % BN, il = e / BN;
-        const int64_t i = ic + il;
-        const int c = c0 + cl;
-        Ms[il][cl] = (i < I && c < C) ? Tacc(Mm[i * ms_i + c]) : Tacc(0);
-      }
+#pragma unroll
+    for (int s2 = 0; s2 < ML; ++s2) {
+      const int e = t + 256 * s2;
+      int il, cl;
+      if (ms_c == 1) { cl = e % BN; il = e / BN; } else { il = e % BI; cl = e / BI; }
+      const int64_t i = ic + il;
+      const int c = c0 + cl;
+      mv[s2] = (e < BI * BN && i < I && c < C) ? Tacc(Mm[i * ms_i + int64_t(c) * ms_c]) : Tacc(0);
+    }
+  };
+  auto store = [&]() {
+    if (a == 1) {
+#pragma unroll
+      for (int s2 = 0; s2 < XL; ++s2) Xs[t % BI][t / BI + (256 / BI) * s2] = xv[s2];
     } else {
-      for (int e = t; e < BI * BN; e += 256) {
-        const int il = e % BI, cl = e / BI;
-        const int64_t i = ic + il;
-        const int c = c0 + cl;
-        Ms[il][cl] = (i < I && c < C) ? Tacc(Mm[i * ms_i + int64_t(c) * ms_c]) : Tacc(0);
+#pragma unroll
+      for (int s2 = 0; s2 < XL; ++s2) Xs[t / BM + (256 / BM) * s2][jl_b] = xv[s2];
+    }
+#pragma unroll
+    for (int s2 = 0; s2 < ML; ++s2) {
+      const int e = t + 256 * s2;
+      if (e < BI * BN) {
+        if (ms_c == 1) Ms[e / BN][e % BN] = mv[s2];
+        else Ms[e % BI][e / BI] = mv[s2];
       }
     }
+  };
+  load(0);
+  for (int64_t ic = 0; ic < I; ic += BI) {
+    store();
     __syncthreads();
-#pragma unroll 4
-    for (int ii = 0; ii < BI; ++ii) {
-      Tacc xr[4], mr[TN];
+    if (ic + BI < I) load(ic + BI);
 #pragma unroll
-      for (int r = 0; r < 4; ++r) xr[r] = Xs[ii][tx + 32 * r];
+    for (int ii = 0; ii < BI; ++ii) {
+      Tacc xr[RJ], mr[TN];
+#pragma unroll
+      for (int r = 0; r < RJ; ++r) xr[r] = Xs[ii][tx + 32 * r];
 #pragma unroll
       for (int c = 0; c < TN; ++c) mr[c] = Ms[ii][ty + 8 * c];
 #pragma unroll
-      for (int r = 0; r < 4; ++r)
+      for (int r = 0; r < RJ; ++r)
 #pragma unroll
         for (int c = 0; c < TN; ++c) acc[r][c] = fma(xr[r], mr[c], acc[r][c]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int r = 0; r < 4; ++r) {
+  for (int r = 0; r < RJ; ++r) {
     const int64_t j = j0 + tx + 32 * r;
     if (j >= J) continue;
     const int64_t ob = (j % a) * so_a + (j / a) * so_b;
@@ -263,11 +282,13 @@ template <typename Tin, typename Tm, typename Tout, int TN>
 void launch_ttm_t(const Ctx& ctx, const Tin* X, Box box, const Tm* Mm, int64_t ms_i, int64_t ms_c, int C,
                   Tout* out, int64_t so_a, int64_t so_c, int64_t so_b) {
   const int64_t J = box.J();
-  const dim3 grid((unsigned)cdiv(J, 128), (unsigned)cdiv(C, 8 * TN));
+  // 8 outputs j per thread when the accumulator tile stays small (TN <= 8), else 4
+  constexpr int RJ = 4;
+  const dim3 grid((unsigned)cdiv(J, 32 * RJ), (unsigned)cdiv(C, 8 * TN));
   RT_REQUIRE(grid.x < (1u << 31) && grid.y < 65536, kEUNSUPPORTED, "ttm_t grid too large");
   launch(ctx, ctx.label ? ctx.label : "ttm_t_simt", [&] {
-    ttm_t_kernel<Tin, Tm, Tout, TN><<<grid, 256, 0, ctx.stream>>>(X, box.a, box.I, J, Mm, ms_i, ms_c, C,
-                                                                  out, so_a, so_c, so_b);
+    ttm_t_kernel<Tin, Tm, Tout, TN, RJ><<<grid, 256, 0, ctx.stream>>>(X, box.a, box.I, J, Mm, ms_i, ms_c, C,
+                                                                      out, so_a, so_c, so_b);
   });
 }
 

@@ -46,6 +46,17 @@ def _inputs(cfg):
     return oms, omt
 
 
+# Reading R28: R-PET's core is not the projection core, so E is first-order sensitive to the
+# fp32-accumulated X passes (sketch H, residual); its error is bounded in absolute terms by a few
+# fp32 unit roundoffs (E is relative to ||X||), not relative to a small E.  Measured (cfg5-scaled,
+# E = 1.5e-3): |E_gpu - E_exact(gpu factors)| = 2.1e-8, |E_exact - E_oracle| = 1.8e-8 (~0.3 u).
+U32 = 2.0 ** -24
+
+
+def _e_ok(e, e_ref, tol=1e-5):
+    return abs(e - e_ref) <= max(tol * e_ref, 4 * U32)
+
+
 def _check(P, res, ref, tol=1e-5):
     qg = [q.cpu().numpy() for q in res["Q"]]
     gg = P.core_to_numpy(res["G"])
@@ -55,7 +66,7 @@ def _check(P, res, ref, tol=1e-5):
     assert M.core_in_oracle_basis(gg, qg, ref["G"], ref["Q"]) <= tol
     assert M.recon(gg, qg, ref["G"], ref["Q"]) <= tol
     e = float(res["err"][0])
-    assert abs(e - ref["E"]) / ref["E"] <= tol, (e, ref["E"])
+    assert _e_ok(e, ref["E"], tol), (e, ref["E"])
 
 
 CASES = {
@@ -162,4 +173,4 @@ def test_pet_loopback_multirank(P, nranks):
     for n in range(3):
         assert M.subspace(qg[n], ref["Q"][n]) <= 1e-5
     assert M.recon(out[0]["G"], qg, ref["G"], ref["Q"]) <= 1e-5
-    assert abs(out[0]["err"][0] - ref["E"]) / ref["E"] <= 1e-5
+    assert _e_ok(out[0]["err"][0], ref["E"]), (out[0]["err"][0], ref["E"])
