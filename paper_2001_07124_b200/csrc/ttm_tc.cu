@@ -734,23 +734,39 @@ void launch_t(const Ctx& ctx, const CUtensorMap& tx, const CUtensorMap& tb, cons
   });
 }
 
-__global__ void splitk_reduce_f32_kernel(const float* __restrict__ part, int64_t I, int K, int splits,
-                                         double* __restrict__ Y, int64_t ldy) {
-  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (e >= I * K) return;
-  const int64_t i = e % I, k = e / I;
-  // 8 independent loads in flight per thread (the split count is ~37: a dependent chain of
-  // global loads would make this tiny reduction latency-bound); fixed summation order
-  const float* pp = part + k * I + i;
-  const int64_t zs = int64_t(K) * I;
-  double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  int z = 0;
-  for (; z + 8 <= splits; z += 8) {
-#pragma unroll
-    for (int u = 0; u < 8; ++u) s[u] += double(__ldg(pp + (z + u) * zs));
+// Y(i, k) = sum_z part[z][k][i] (fp64 sum in a fixed order).  CTA = 32 consecutive outputs x 8
+// split groups: thread (o, g) sums z = g, g + 8, ... with 4 loads in flight, then the 8 group sums
+// are added in order -- parallel over the split count too (the Gram of Z has ~600 splits but only
+// K^2 outputs).
+__global__ void __launch_bounds__(256) splitk_reduce_f32_kernel(const float* __restrict__ part, int64_t I, int K,
+                                                                int splits, double* __restrict__ Y, int64_t ldy) {
+  __shared__ double red[8][33];
+  const int o = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int64_t e = int64_t(blockIdx.x) * 32 + o;
+  const int64_t n = I * K;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  if (e < n) {
+    const int64_t i = e % I, k = e / I;
+    const float* pp = part + k * I + i;
+    const int64_t zs = int64_t(K) * I;
+    int z = g;
+    for (; z + 24 < splits; z += 32) {
+      s0 += double(__ldg(pp + z * zs));
+      s1 += double(__ldg(pp + (z + 8) * zs));
+      s2 += double(__ldg(pp + (z + 16) * zs));
+      s3 += double(__ldg(pp + (z + 24) * zs));
+    }
+    for (; z < splits; z += 8) s0 += double(__ldg(pp + z * zs));
   }
-  for (int u = 0; z < splits; ++z, ++u) s[u] += double(__ldg(pp + z * zs));
-  Y[i + ldy * k] = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+  red[g][o] = (s0 + s1) + (s2 + s3);
+  __syncthreads();
+  if (g == 0 && e < n) {
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s += red[q][o];
+    const int64_t i = e % I, k = e / I;
+    Y[i + ldy * k] = s;
+  }
 }
 
 // Q (I x C, col-major ldq) -> Q2 (I x 2 npad, col-major ld2): columns [0, C) = tf32 hi, columns
@@ -882,7 +898,7 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
   }
   const int64_t n = box.I * K;
   launch(ctx, "splitk_reduce", [&] {
-    splitk_reduce_f32_kernel<<<unsigned(cdiv(n, 256)), 256, 0, ctx.stream>>>(p.part, box.I, K, int(splits), Y, ldy);
+    splitk_reduce_f32_kernel<<<unsigned(cdiv(n, 32)), 256, 0, ctx.stream>>>(p.part, box.I, K, int(splits), Y, ldy);
   });
   return true;
 }
