@@ -78,8 +78,11 @@ def work_model(cfg, nranks=1):
     r_bytes = xl * esz + (xl // dims_l[-1]) * cfg.ranks[-1] * esz
     r_flops = 2 * xl * cfg.ranks[-1]
     total_flops = s_flops + t_flops + r_flops
+    # hardware tensor flops of the ttm_s class: the Omega sketch runs 2 tf32 products (tf32-exact
+    # Omega, reading R18), the power product Y = X Z 3 (3xTF32)
+    s_hw = sum(2 * xl * K[n] * (2 + 3 * cfg.q) for n in range(N))
     return {"ttm_s": (s_bytes, s_flops, s_n), "ttm_t": (t_bytes, t_flops, t_n), "residual": (r_bytes, r_flops, 1),
-            "total_flops": total_flops, "x_bytes_local": xl * esz}
+            "total_flops": total_flops, "x_bytes_local": xl * esz, "ttm_s_hw_flops": s_hw}
 
 
 # --------------------------------------------------------------------- clocks
@@ -313,6 +316,15 @@ def run_gpu(args, cfg):
     return out
 
 
+def _pipeline(prof, ms, steps, xbytes):
+    """throughput of sketch+QR+core (first sketch to truncated G) with the
+    residual pass (a8: P chain + residual kernel) timed and reported separately."""
+    res_ms = sum(t for nm, _, t in prof if nm in ("residual_tc", "residual_simt", "pchain", "reduce_pairs",
+                                                   "finalize_err", "sumsq")) / steps
+    pm = ms - res_ms
+    return {"value": xbytes / (pm * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": pm, "residual_ms": res_ms}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -382,12 +394,20 @@ def main():
                 "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
                 "share_of_step": per_step_ms / ms,
                 "tflops": f / (per_step_ms * 1e-3) / 1e12}
+        if cls == "ttm_s":
+            # tensor pipe: hardware tf32 flops against the tf32 peak = measured bf16 peak x 1/2
+            # (nominal tf32:bf16 ratio, B200_PROFILING.md); the class is co-limited by both
+            tf32_peak = bf16 / 2.0
+            hw = wm["ttm_s_hw_flops"] / (per_step_ms * 1e-3) / 1e12
+            roof["tensor"] = {"hw_tflops": hw, "peak_tflops": tf32_peak, "frac": hw / tf32_peak,
+                              "peak_source": f"{peak_src} bf16 x 1/2"}
     line = {"metric": METRIC, "value": value * 1.0, "unit": UNIT, "n_gpus": r["world"], "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config,
             "ttm_tflops": wm["total_flops"] * r["world"] / (ms * 1e-3) / 1e12,
             "rel_err": r["E"], "rel_err_gram": r["Eg"], "roofline": roof,
             "kernels": [{"name": n, "count": c, "ms_per_step": t / args.steps} for n, c, t in prof[:12]],
+            "pipeline": _pipeline(prof, ms, args.steps, xbytes),
             "gpu_launches": int(r["launches"]), "clocks": r["clocks"]}
     if r["e2e"]:
         em, h2d, d2h = r["e2e"]
