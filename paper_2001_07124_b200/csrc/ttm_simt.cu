@@ -292,6 +292,131 @@ void launch_ttm_t(const Ctx& ctx, const Tin* X, Box box, const Tm* Mm, int64_t m
   });
 }
 
+// ------------------------------------------------------------ ttm_t, fp64 accumulate on DMMA
+// out(j, c) = sum_i X(j, i) M(i, c) with fp64 products and sums on the fp64 warp MMA
+// (mma.sync m8n8k4 f64; tools/dmma_rate.cu: 37 TF/s vs 34 for DFMA, with 4x less operand traffic
+// per FMA: the SIMT kernel is bound by shared-memory bandwidth at ~15 TF/s).  Block tile 128 j x
+// 64 c, 16 contraction rows per stage (4 MMA k-steps), register-prefetched stages as above.  Warp w
+// owns j in [32 (w % 4), +32) x c in [32 (w / 4), +32): 4 x 4 m8n8 tiles, 16 MMAs per k-step.
+// Fragments (PTX m8n8k4 .f64): A[r][k] at lane 4 r + k; B[k][n] at lane 4 n + k; C[r][2 q + e] at
+// lane 4 r + q.  Shared pitches = 8 mod 16 doubles: the 4 k-rows of a fragment hit disjoint banks.
+template <typename Tin, typename Tm, typename Tout>
+__global__ void __launch_bounds__(256)
+ttm_t_dmma_kernel(const Tin* __restrict__ X, int64_t a, int64_t I, int64_t J, const Tm* __restrict__ Mm,
+                  int64_t ms_i, int64_t ms_c, int C, Tout* __restrict__ out, int64_t so_a, int64_t so_c,
+                  int64_t so_b) {
+  constexpr int BM = 128, BN = 64, BI = 16;
+  constexpr int PX = BM + 8, PM = BN + 8;
+  constexpr int XL = BI * BM / 256, ML = BI * BN / 256;
+  __shared__ double Xs[BI][PX];
+  __shared__ double Ms[BI][PM];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int64_t j0 = int64_t(blockIdx.x) * BM;
+  const int c0 = blockIdx.y * BN;
+  const int64_t aI = a * I;
+  const int jw = 32 * (w & 3), cw = 32 * (w >> 2);
+  const int fr = lane >> 2, fk = lane & 3;
+  double acc[4][4][2];
+#pragma unroll
+  for (int m = 0; m < 4; ++m)
+#pragma unroll
+    for (int n = 0; n < 4; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+
+  const int jl_b = t % BM;
+  const int64_t j_b = j0 + jl_b;
+  const bool jv_b = j_b < J;
+  const int64_t off_b = jv_b ? (j_b % a) + aI * (j_b / a) : 0;
+  double xv[XL], mv[ML];
+  auto load = [&](int64_t ic) {
+    if (a == 1) {
+      const int il = t % BI;
+      const int64_t i = ic + il;
+#pragma unroll
+      for (int s2 = 0; s2 < XL; ++s2) {
+        const int64_t j = j0 + t / BI + (256 / BI) * s2;
+        xv[s2] = (j < J && i < I) ? double(X[i + I * j]) : 0.0;
+      }
+    } else {
+#pragma unroll
+      for (int s2 = 0; s2 < XL; ++s2) {
+        const int64_t i = ic + t / BM + (256 / BM) * s2;
+        xv[s2] = (jv_b && i < I) ? double(X[off_b + a * i]) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int s2 = 0; s2 < ML; ++s2) {
+      const int e = t + 256 * s2;
+      int il, cl;
+      if (ms_c == 1) { cl = e % BN; il = e / BN; } else { il = e % BI; cl = e / BI; }
+      const int64_t i = ic + il;
+      const int c = c0 + cl;
+      mv[s2] = (i < I && c < C) ? double(Mm[i * ms_i + int64_t(c) * ms_c]) : 0.0;
+    }
+  };
+  auto store = [&]() {
+    if (a == 1) {
+#pragma unroll
+      for (int s2 = 0; s2 < XL; ++s2) Xs[t % BI][t / BI + (256 / BI) * s2] = xv[s2];
+    } else {
+#pragma unroll
+      for (int s2 = 0; s2 < XL; ++s2) Xs[t / BM + (256 / BM) * s2][jl_b] = xv[s2];
+    }
+#pragma unroll
+    for (int s2 = 0; s2 < ML; ++s2) {
+      const int e = t + 256 * s2;
+      if (ms_c == 1) Ms[e / BN][e % BN] = mv[s2];
+      else Ms[e % BI][e / BI] = mv[s2];
+    }
+  };
+  load(0);
+  for (int64_t ic = 0; ic < I; ic += BI) {
+    store();
+    __syncthreads();
+    if (ic + BI < I) load(ic + BI);
+#pragma unroll
+    for (int kk = 0; kk < BI / 4; ++kk) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) af[m] = Xs[4 * kk + fk][jw + 8 * m + fr];
+#pragma unroll
+      for (int n = 0; n < 4; ++n) bf[n] = Ms[4 * kk + fk][cw + 8 * n + fr];
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int n = 0; n < 4; ++n)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(acc[m][n][0]), "+d"(acc[m][n][1])
+                       : "d"(af[m]), "d"(bf[n]));
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int64_t j = j0 + jw + 8 * m + fr;
+    if (j >= J) continue;
+    const int64_t ob = (j % a) * so_a + (j / a) * so_b;
+#pragma unroll
+    for (int n = 0; n < 4; ++n)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = c0 + cw + 8 * n + 2 * fk + e;
+        if (c < C) out[ob + int64_t(c) * so_c] = Tout(acc[m][n][e]);
+      }
+  }
+}
+
+template <typename Tin, typename Tm, typename Tout>
+void launch_ttm_t_dmma(const Ctx& ctx, const Tin* X, Box box, const Tm* Mm, int64_t ms_i, int64_t ms_c, int C,
+                       Tout* out, int64_t so_a, int64_t so_c, int64_t so_b) {
+  const int64_t J = box.J();
+  const dim3 grid((unsigned)cdiv(J, 128), (unsigned)cdiv(C, 64));
+  RT_REQUIRE(grid.x < (1u << 31) && grid.y < 65536, kEUNSUPPORTED, "ttm_t grid too large");
+  launch(ctx, ctx.label ? ctx.label : "ttm_t_dmma", [&] {
+    ttm_t_dmma_kernel<Tin, Tm, Tout><<<grid, 256, 0, ctx.stream>>>(X, box.a, box.I, J, Mm, ms_i, ms_c, C, out,
+                                                                    so_a, so_c, so_b);
+  });
+}
+
 }  // namespace
 
 template <typename T>
@@ -317,6 +442,12 @@ void ttm_t(const Ctx& ctx, const Tin* X, Box box, const Tm* Mm, int64_t ms_i, in
   if (box.J() == 0 || C == 0) return;
   if (box.I == 0) {
     throw Error(kEINVAL, "ttm_t with empty contraction");
+  }
+  using Tacc = typename Acc3<Tin, Tm, Tout>::type;
+  if (std::is_same<Tacc, double>::value && C > 16 && ctx.ttm_impl != 1) {
+    // fp64 accumulation: the fp64 warp MMA (fewer shared-memory operand reads per FMA)
+    launch_ttm_t_dmma<Tin, Tm, Tout>(ctx, X, box, Mm, ms_i, ms_c, C, out, so_a, so_c, so_b);
+    return;
   }
   if (C <= 8)        launch_ttm_t<Tin, Tm, Tout, 1>(ctx, X, box, Mm, ms_i, ms_c, C, out, so_a, so_c, so_b);
   else if (C <= 16)  launch_ttm_t<Tin, Tm, Tout, 2>(ctx, X, box, Mm, ms_i, ms_c, C, out, so_a, so_c, so_b);
