@@ -296,19 +296,22 @@ void launch_ttm_t(const Ctx& ctx, const Tin* X, Box box, const Tm* Mm, int64_t m
 // out(j, c) = sum_i X(j, i) M(i, c) with fp64 products and sums on the fp64 warp MMA
 // (mma.sync m8n8k4 f64; tools/dmma_rate.cu: 37 TF/s vs 34 for DFMA, with 4x less operand traffic
 // per FMA: the SIMT kernel is bound by shared-memory bandwidth at ~15 TF/s).  Block tile 128 j x
-// 64 c, 16 contraction rows per stage (4 MMA k-steps), register-prefetched stages as above.  Warp w
+// 64 c, 32 (fp32 X) or 16 (fp64 X) contraction rows per stage, register-prefetched stages as above.  Warp w
 // owns j in [32 (w % 4), +32) x c in [32 (w / 4), +32): 4 x 4 m8n8 tiles, 16 MMAs per k-step.
 // Fragments (PTX m8n8k4 .f64): A[r][k] at lane 4 r + k; B[k][n] at lane 4 n + k; C[r][2 q + e] at
-// lane 4 r + q.  Shared pitches = 8 mod 16 doubles: the 4 k-rows of a fragment hit disjoint banks.
+// lane 4 r + q.  fp64 pitches = 8 mod 16 doubles: the 4 k-rows of a fragment hit disjoint banks.
 template <typename Tin, typename Tm, typename Tout>
 __global__ void __launch_bounds__(256)
 ttm_t_dmma_kernel(const Tin* __restrict__ X, int64_t a, int64_t I, int64_t J, const Tm* __restrict__ Mm,
                   int64_t ms_i, int64_t ms_c, int C, Tout* __restrict__ out, int64_t so_a, int64_t so_c,
                   int64_t so_b) {
-  constexpr int BM = 128, BN = 64, BI = 16;
-  constexpr int PX = BM + 8, PM = BN + 8;
+  // fp32 X is staged as fp32 (converted when a fragment is read): 32 contraction rows per stage,
+  // pitch 132 floats (stores along i and the 4-row fragment reads are at most 2-way conflicted)
+  using TX = typename std::conditional<std::is_same<Tin, float>::value, float, double>::type;
+  constexpr int BM = 128, BN = 64, BI = sizeof(TX) == 4 ? 32 : 16;
+  constexpr int PX = sizeof(TX) == 4 ? BM + 4 : BM + 8, PM = BN + 8;
   constexpr int XL = BI * BM / 256, ML = BI * BN / 256;
-  __shared__ double Xs[BI][PX];
+  __shared__ TX Xs[BI][PX];
   __shared__ double Ms[BI][PM];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const int64_t j0 = int64_t(blockIdx.x) * BM;
@@ -326,7 +329,8 @@ ttm_t_dmma_kernel(const Tin* __restrict__ X, int64_t a, int64_t I, int64_t J, co
   const int64_t j_b = j0 + jl_b;
   const bool jv_b = j_b < J;
   const int64_t off_b = jv_b ? (j_b % a) + aI * (j_b / a) : 0;
-  double xv[XL], mv[ML];
+  TX xv[XL];
+  double mv[ML];
   auto load = [&](int64_t ic) {
     if (a == 1) {
       const int il = t % BI;
@@ -334,13 +338,13 @@ ttm_t_dmma_kernel(const Tin* __restrict__ X, int64_t a, int64_t I, int64_t J, co
 #pragma unroll
       for (int s2 = 0; s2 < XL; ++s2) {
         const int64_t j = j0 + t / BI + (256 / BI) * s2;
-        xv[s2] = (j < J && i < I) ? double(X[i + I * j]) : 0.0;
+        xv[s2] = (j < J && i < I) ? TX(X[i + I * j]) : TX(0);
       }
     } else {
 #pragma unroll
       for (int s2 = 0; s2 < XL; ++s2) {
         const int64_t i = ic + t / BM + (256 / BM) * s2;
-        xv[s2] = (jv_b && i < I) ? double(X[off_b + a * i]) : 0.0;
+        xv[s2] = (jv_b && i < I) ? TX(X[off_b + a * i]) : TX(0);
       }
     }
 #pragma unroll
@@ -377,7 +381,7 @@ ttm_t_dmma_kernel(const Tin* __restrict__ X, int64_t a, int64_t I, int64_t J, co
     for (int kk = 0; kk < BI / 4; ++kk) {
       double af[4], bf[4];
 #pragma unroll
-      for (int m = 0; m < 4; ++m) af[m] = Xs[4 * kk + fk][jw + 8 * m + fr];
+      for (int m = 0; m < 4; ++m) af[m] = double(Xs[4 * kk + fk][jw + 8 * m + fr]);
 #pragma unroll
       for (int n = 0; n < 4; ++n) bf[n] = Ms[4 * kk + fk][cw + 8 * n + fr];
 #pragma unroll
