@@ -301,7 +301,7 @@ void launch_ttm_t(const Ctx& ctx, const Tin* X, Box box, const Tm* Mm, int64_t m
 // Fragments (PTX m8n8k4 .f64): A[r][k] at lane 4 r + k; B[k][n] at lane 4 n + k; C[r][2 q + e] at
 // lane 4 r + q.  fp64 pitches = 8 mod 16 doubles: the 4 k-rows of a fragment hit disjoint banks.
 template <typename Tin, typename Tm, typename Tout>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 2)
 ttm_t_dmma_kernel(const Tin* __restrict__ X, int64_t a, int64_t I, int64_t J, const Tm* __restrict__ Mm,
                   int64_t ms_i, int64_t ms_c, int C, Tout* __restrict__ out, int64_t so_a, int64_t so_c,
                   int64_t so_b) {

@@ -1,5 +1,8 @@
 """Time the count-sketch operator per mode on a device-generated BASELINE config (CUDA events)."""
 import argparse
+import os
+import sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 from gen import synth

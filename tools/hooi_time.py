@@ -1,5 +1,8 @@
 """Time RP-HOOI sweeps on a device-generated BASELINE config (default cfg5) with CUDA events."""
 import argparse
+import os
+import sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from gen import synth
 from paper_2001_07124_b200 import api
