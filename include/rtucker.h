@@ -185,7 +185,9 @@ rt_status rtucker_hosvd(rt_handle* h, const rt_tensor* X, const int64_t* R, int 
  * mode_order: permutation of 0..N-1, NULL = ascending.  Omega tables as in
  *   (4) but sized for the working tensor: when mode n is processed, already-processed
  *   modes m have size R_m (GAUSS/COUNT: J_n = prod of current sizes; KRON: d_k current).
- * Single-GPU only for now (RT_EUNSUPPORTED on a sharded tensor with a communicator). */
+ * Slab-parallel (sharded X): the slab mode N-1 must come last in mode_order
+ *   (RT_EUNSUPPORTED otherwise); Omega rows of modes n < N-1 are the slab's (local J_n), the
+ *   Kronecker factor of mode N-1 holds its local rows; Q_out[N-1] gets the local rows. */
 rt_status rtucker_sthosvd(rt_handle* h, const rt_tensor* X, const int64_t* R, int p, int q,
                           rt_omega_kind kind, const void* const* omega, const int64_t* omega_cols,
                           const int64_t* omega_ld, const int* mode_order, double* const* Q_out, double* G_out,

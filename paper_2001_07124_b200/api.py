@@ -312,9 +312,12 @@ def rtucker_hosvd(h: Handle, X: torch.Tensor, ranks: Sequence[int], p: int, q: i
 
 
 def rtucker_sthosvd(h: Handle, X: torch.Tensor, ranks: Sequence[int], p: int, q: int, omegas, kind: str = "gauss",
-                    mode_order: Optional[Sequence[int]] = None, with_error: bool = True) -> dict:
-    """Randomized STHOSVD (Alg.8).  omegas sized for the shrinking working tensor."""
-    return _driver(lib.rtucker_sthosvd, h, X, ranks, p, q, omegas, kind, with_error, 0, None, mode_order)
+                    mode_order: Optional[Sequence[int]] = None, with_error: bool = True, last_offset: int = 0,
+                    last_global: Optional[int] = None) -> dict:
+    """Randomized STHOSVD (Alg.8).  omegas sized for the shrinking working tensor (local rows of
+    the slab for modes processed before the slab mode, which must come last when sharded)."""
+    return _driver(lib.rtucker_sthosvd, h, X, ranks, p, q, omegas, kind, with_error, last_offset, last_global,
+                   mode_order)
 
 
 def rtucker_pet(h: Handle, X: torch.Tensor, ranks: Sequence[int], omegas, omega_tildes, with_error: bool = True,

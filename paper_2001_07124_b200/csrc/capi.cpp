@@ -360,7 +360,11 @@ static void check_driver_args(const rt::TView& v, const int64_t* R, int p, int q
   for (int n = 0; n < N; ++n) {
     RT_REQUIRE(Q_out[n] != nullptr, rt::kEINVAL, "NULL Q_out[n]");
     rt::TView w = v;
-    if (cur_dims) { for (int k = 0; k < N; ++k) w.d[k] = cur_dims[n * N + k]; w.glob = w.d[N - 1]; }
+    if (cur_dims) {
+      for (int k = 0; k < N; ++k) w.d[k] = cur_dims[n * N + k];
+      // the slab mode keeps its global size until it is processed (it is last when sharded)
+      if (w.d[N - 1] != v.d[N - 1] || !v.sharded()) { w.glob = w.d[N - 1]; w.off = 0; }
+    }
     const void* const* om = omega + n * N;
     const int64_t* oc = omega_cols + n * N;
     const int64_t* ol = omega_ld + n * N;
@@ -410,7 +414,7 @@ rt_status rtucker_sthosvd(rt_handle* h, const rt_tensor* X, const int64_t* R, in
   return guard(h, [&] {
     rt::TView v = check_tensor(X);
     rt::Engine eng(h->ctx, h->ws, h->comm.get());
-    RT_REQUIRE(!v.sharded(), rt::kEUNSUPPORTED, "sharded R-STHOSVD is not implemented");
+    RT_REQUIRE(!(v.sharded() && !eng.dist()), rt::kEINVAL, "a sharded tensor needs a communicator");
     const int N = v.N;
     int order[5];
     bool seen[5] = {false, false, false, false, false};
@@ -419,8 +423,10 @@ rt_status rtucker_sthosvd(rt_handle* h, const rt_tensor* X, const int64_t* R, in
       RT_REQUIRE(order[s] >= 0 && order[s] < N && !seen[order[s]], rt::kEINVAL, "mode_order must be a permutation");
       seen[order[s]] = true;
     }
+    RT_REQUIRE(!v.sharded() || order[N - 1] == N - 1, rt::kEUNSUPPORTED,
+               "sharded R-STHOSVD processes the slab mode last (mode_order[N-1] == N-1)");
     RT_REQUIRE(R != nullptr, rt::kEINVAL, "NULL R");
-    for (int n = 0; n < N; ++n) RT_REQUIRE(R[n] >= 1 && R[n] <= v.d[n], rt::kERANK, "need 1 <= R_n <= I_n");
+    for (int n = 0; n < N; ++n) RT_REQUIRE(R[n] >= 1 && R[n] <= v.Ig(n), rt::kERANK, "need 1 <= R_n <= I_n");
     // sizes of the working tensor when each mode is processed (already-processed modes have R_m)
     int64_t cur[25];
     int64_t d[5];

@@ -560,29 +560,36 @@ void Engine::sthosvd(const TView& X, const int64_t* R, int q, int kind, const vo
       }
       sketch<double>(S, sd, n, kind, om64, oc, ld64, q, Yt);
     }
+    // slab-parallel: while the last mode is still a slab, S is local, the sketches
+    // of modes n < N-1 and the Grams of B_(n) are partial sums (allreduced); the last mode comes last,
+    // its sketch rows and factor rows stay local and B = S x_{N-1} Q~^T is allreduced
+    const bool dist_last = dist() && n == N - 1 && S.sharded();
+    const bool dist_slab = dist() && n != N - 1 && S.sharded();
     double* Qt = ws.alloc_n<double>(In * K);
-    qr_y(Yt, In, In, K, In, Qt, In, nullptr, false, 0);
+    qr_y(Yt, In, S.Ig(n), K, In, Qt, In, nullptr, dist_last, dist_last ? S.off : 0);
     // Alg.1 line 4: B = S x_n Q~^T (fp64 accumulation and output)
     const Box bs = S.box(n);
     double* B = ws.alloc_n<double>(bs.a * K * bs.b);
     if (step == 0) ttm_t<T, double, double>(ctx, static_cast<const T*>(X.data), bs, Qt, 1, In, K, B, 1, bs.a, bs.a * K);
     else           ttm_t<double, double, double>(ctx, sd, bs, Qt, 1, In, K, B, 1, bs.a, bs.a * K);
+    allreduce(comm, dist_last, B, bs.a * K * bs.b, ctx.stream);
     // Alg.1 lines 5-7 via the Gram-EVD of B_(n): U = top-R_n eigenvectors, Q_n = Q~ U
     const Box bb{bs.a, K, bs.b};
     double* M = ws.alloc_n<double>(int64_t(K) * K);
     double* V = ws.alloc_n<double>(int64_t(K) * K);
     double* W = ws.alloc_n<double>(K);
     ttm_s<double>(ctx, ws, B, bb, nullptr, 0, 0, K, M, K, /*gram=*/true);
+    allreduce(comm, dist_slab, M, int64_t(K) * K, ctx.stream);
     eig_sym(ctx, ws, M, K, W, V);
     gemm_tall<double, double>(ctx, Qt, In, K, In, V, int(R[n]), K, Q_out[n], In);
-    canon(Q_out[n], In, int(R[n]), In, 0, false, V, K);
+    canon(Q_out[n], In, int(R[n]), In, dist_last ? S.off : 0, dist_last, V, K);
     // Alg.8 line 4 with the ΛV^T shortcut: S <- B x_n U^T
     double* Snew = (step == N - 1) ? G_out : sbuf[step & 1];
     ttm_t<double, double, double>(ctx, B, bb, V, 1, K, int(R[n]), Snew, 1, bb.a, bb.a * R[n]);
     sd = Snew;
     ws.rewind(mstep);
     S.d[n] = R[n];
-    S.glob = S.d[N - 1];
+    if (n == N - 1) { S.glob = R[n]; S.off = 0; }      // the last mode is now replicated
   }
   if (E || Eg) rel_error<T>(X, static_cast<const T*>(X.data), G_out, R, Q_out, E, Eg);
   ws.rewind(mk);
