@@ -108,6 +108,7 @@ rt_status rt_sync(rt_handle* h);
  * the split-K chunk order (rotation per row tile; default 0).  RT_OPT_QR_FALLBACK is reserved. */
 typedef enum { RT_OPT_TTM_IMPL = 0, RT_OPT_PROFILE = 1, RT_OPT_QR_FALLBACK = 2, RT_OPT_OMEGA_TF32 = 3,
                RT_OPT_TC_SEGMENT = 4, RT_OPT_TC_SKEW = 5,
+               RT_OPT_FORCE_COLLECTIVES = 6 /* tests: run the slab exchanges even on a 1-rank communicator */,
                RT_OPT_TC_ABLATE = 100 /* profiling only: invalid results */ } rt_option;
 rt_status rt_set_option(rt_handle* h, rt_option opt, int64_t value);
 

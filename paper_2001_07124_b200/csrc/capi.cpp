@@ -161,7 +161,7 @@ rt_status rt_create(rt_handle** h, void* cuda_stream, const uint8_t* id, int nra
   if (nranks < 1 || rank < 0 || rank >= nranks) return fail(nullptr, RT_EINVAL, "bad nranks/rank");
   rt_status s = create_common(h, cuda_stream);
   if (s != RT_OK) return s;
-  if (id && nranks > 1) {
+  if (id) {                              // a 1-rank NCCL communicator is allowed (tests)
     rt_status st = guard(*h, [&] { (*h)->comm = rt::make_nccl_comm(id, nranks, rank); });
     if (st != RT_OK) { g_err = (*h)->err; rt_destroy(*h); *h = nullptr; return st; }
   }
@@ -226,6 +226,7 @@ rt_status rt_set_option(rt_handle* h, rt_option opt, int64_t value) {
       h->ctx.tc_ablate = int(value);
       return RT_OK;
     case RT_OPT_TC_SKEW: h->ctx.tc_skew = int(value); return RT_OK;
+    case RT_OPT_FORCE_COLLECTIVES: h->ctx.force_dist = int(value != 0); return RT_OK;
   }
   return fail(h, RT_EINVAL, "unknown option");
 }

@@ -71,6 +71,7 @@ struct Ctx {
   int tc_seg = 16;              // tcgen05: 32-element chunks per TMEM accumulator segment (drained to fp32 regs)
   int tc_ablate = 0;            // profiling only (RT_OPT_TC_ABLATE): 1 no MMA, 2 no split; results invalid
   int tc_skew = -1;             // ttm_s_tc: chunk-order rotation per M-tile (-1 = default)
+  int force_dist = 0;           // run the slab exchanges on a 1-rank communicator (tests)
   mutable const char* label = nullptr;   // profiler name override for the next TC launches
   int tc_presplit_z = 0;        // power iteration: write Z R^-1 pre-split [hi | lo] (ablation 200 toggles)
 };

@@ -35,7 +35,7 @@ class Engine {
   Ctx& ctx;
   Arena& ws;
   Comm* comm;
-  bool dist() const { return comm && comm->nranks() > 1; }
+  bool dist() const { return comm && (comm->nranks() > 1 || ctx.force_dist); }
 
   // (1) sketch of mode n incl. q power iterations; Yt: fp64 I_n(local) x K, ld I_n(local).
   template <typename T>
