@@ -147,3 +147,63 @@ def test_slab_parallel_matches_unsharded_oracle():
             np.testing.assert_allclose(out["q"][n], ref["Q"][n], rtol=0, atol=1e-9)
         np.testing.assert_allclose(out["g"], ref["G"], rtol=0, atol=1e-9 * np.abs(ref["G"]).max())
         assert abs(out["e"] - ref["E"]) <= 1e-9 * ref["E"]
+
+
+# ------------------------------------------------ slab-parallel R-STHOSVD (slab mode last)
+def _sthosvd_worker(rank, world, port, ranks, x, omegas, ret):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        N = x.ndim
+        lo, hi = partition.slab_range(x.shape[-1], world, rank)
+        s = x[..., lo:hi]
+        qs = []
+        for n in range(N):
+            sn = unfold(s, n)
+            if n < N - 1:
+                a = int(np.prod([s.shape[k] for k in range(N - 1) if k != n]))
+                y = _allreduce(sn @ omegas[n][a * lo:a * hi])               # C1 (slab's Omega rows)
+                qt, _ = orc.qr_plus(y)
+                b = orc.fold(qt.T @ sn, n, tuple(qt.shape[1] if k == n else s.shape[k] for k in range(N)))
+                bn = unfold(b, n)
+                m = _allreduce(bn @ bn.T)                                    # Gram of B_(n): partial sums
+                _, v = orc.eig_desc(m)
+                u = v[:, :ranks[n]]
+                qn, u = orc.canon_sign(qt @ u, u)
+                qs.append(qn)
+            else:
+                y = sn @ omegas[n]                                           # local rows of the slab mode
+                qt = _cholqr_rows(y)                                         # C2
+                b = _allreduce(qt.T @ sn)                                    # B = S x_{N-1} Q~^T (C4-like)
+                _, v = orc.eig_desc(b @ b.T)
+                u = v[:, :ranks[n]]
+                lifted = _allgather_rows(qt @ u)
+                qn, u = orc.canon_sign(lifted, u)
+                qs.append(qn[lo:hi])
+                b = orc.fold(b, n, tuple(b.shape[0] if k == n else s.shape[k] for k in range(N)))
+            s = orc.ttm(b, u.T, n)
+        sums = _allreduce(np.array([fro(x[..., lo:hi] - multi_ttm(s, qs)) ** 2, fro(x[..., lo:hi]) ** 2]))
+        ret[rank] = dict(q=qs[:-1] + [_allgather_rows(qs[-1])], g=s, e=float(np.sqrt(sums[0] / sums[1])))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_slab_parallel_sthosvd_matches_unsharded_oracle():
+    cfg = _cfg()
+    x = np.asarray(synth.make_tensor(cfg), dtype=np.float64)
+    rng = np.random.default_rng(90)
+    omegas, d = [], list(x.shape)
+    for n in range(x.ndim):
+        J = int(np.prod(d)) // d[n]
+        omegas.append(rng.standard_normal((J, min(cfg.ranks[n] + cfg.p, d[n], J))))
+        d[n] = cfg.ranks[n]
+    ref = orc.sthosvd(x, cfg.ranks, omegas, q=0)
+    mgr = mp.Manager()
+    ret = mgr.dict()
+    mp.spawn(_sthosvd_worker, args=(2, _free_port(), cfg.ranks, x, omegas, ret), nprocs=2, join=True)
+    for r in range(2):
+        out = ret[r]
+        for n in range(x.ndim):
+            np.testing.assert_allclose(out["q"][n], ref["Q"][n], rtol=0, atol=1e-9)
+        np.testing.assert_allclose(out["g"], ref["G"], rtol=0, atol=1e-9 * np.abs(ref["G"]).max())
+        assert abs(out["e"] - ref["E"]) <= 1e-9 * ref["E"]
