@@ -99,10 +99,10 @@ rt_status rt_sync(rt_handle* h);
 
 /* Options.  RT_OPT_TTM_IMPL: 0 / 2 tcgen05 where the shape fits the TMA path (fp32 data,
  * 16-byte aligned strides), CUDA-core (SIMT) kernels elsewhere; 1 CUDA-core TTM kernels only.  RT_OPT_PROFILE: 1 records a CUDA event pair around every launch (read with
- * rt_profile_read).  RT_OPT_OMEGA_TF32: 1 = the caller guarantees every Gaussian Omega entry
- * is exactly representable in tf32 (e.g. rounded on the host before it is given to both the
- * oracle and this library); the sketch then skips the A_hi*Omega_lo product of the 3xTF32
- * split.  RT_OPT_TC_SEGMENT: contraction chunks (of 32) accumulated in TMEM before the fp32
+ * rt_profile_read).  RT_OPT_OMEGA_TF32: 1 = the caller guarantees every entry of the random test
+ * matrices (Gaussian Omega, the Khatri-Rao factors, R-PET's Omega~) is exactly representable in
+ * tf32 (e.g. rounded on the host before it is given to both the oracle and this library); the
+ * tensor-core products with them then skip the A_hi*Omega_lo product of the 3xTF32 split.  RT_OPT_TC_SEGMENT: contraction chunks (of 32) accumulated in TMEM before the fp32
  * accumulator is drained to registers (default 8, i.e. 256 elements; the tensor core's fp32
  * accumulation error grows with this length, tests/test_gpu_tc.py).  RT_OPT_TC_SKEW: tuning of
  * the split-K chunk order (rotation per row tile; default 0).  RT_OPT_QR_FALLBACK is reserved. */

@@ -52,7 +52,7 @@ int tc_split_width(int K);
 // workspace copy).  split_out: each output row (so_c == 1) is written as [hi | lo] halves of
 // tc_split_width(C) columns each (the pre-split B operand of ttm_s_tc).
 bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
-              int64_t so_a, int64_t so_c, int64_t so_b, bool split_out = false);
+              int64_t so_a, int64_t so_c, int64_t so_b, bool split_out = false, bool q_tf32_exact = false);
 
 // Gram A^T A of an m x k matrix (fp64 out, k x k), partials reduced in fixed order.  A col-major
 // (element (r,c) at r + lda*c) or, with rowmajor, at r*lda + c.

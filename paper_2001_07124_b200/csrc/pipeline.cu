@@ -40,20 +40,22 @@ void ttm_s_dispatch(const Ctx& ctx, Arena& ws, const double* X, Box box, const d
   ttm_s<double>(ctx, ws, X, box, B, ldb, 1, K, Y, ldy);
 }
 // out(alpha,c,beta) = sum_i X(alpha,i,beta) Q(i,c), Q col-major (ldq)
+// q_tf32_exact: Q holds tf32-representable values (a host-rounded test matrix, reading R18): the
+// tensor-core kernel then runs 2 products instead of the 3 of the split form
 void ttm_t_dispatch(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
-                    int64_t so_a, int64_t so_c, int64_t so_b) {
+                    int64_t so_a, int64_t so_c, int64_t so_b, bool q_tf32_exact = false) {
   if (ctx.ttm_impl != 1) {
     if (C <= 128) {
-      if (ttm_t_tc(ctx, ws, X, box, Q, ldq, C, out, so_a, so_c, so_b)) return;
+      if (ttm_t_tc(ctx, ws, X, box, Q, ldq, C, out, so_a, so_c, so_b, false, q_tf32_exact)) return;
     } else {
       // wider than one TMEM tile (e.g. the R-PET core sketch, S_n = 2K_n + 1): balanced column
       // chunks of <= 128, one X pass each, each writing its slice of the output
       const int nch = int(cdiv(C, 128));
       const int cw = int(cdiv(C, nch) + 3) & ~3;
-      if (ttm_t_tc(ctx, ws, X, box, Q, ldq, cw, out, so_a, so_c, so_b)) {
+      if (ttm_t_tc(ctx, ws, X, box, Q, ldq, cw, out, so_a, so_c, so_b, false, q_tf32_exact)) {
         for (int c0 = cw; c0 < C; c0 += cw)
           RT_REQUIRE(ttm_t_tc(ctx, ws, X, box, Q + int64_t(c0) * ldq, ldq, std::min(cw, C - c0), out + c0 * so_c, so_a,
-                              so_c, so_b),
+                              so_c, so_b, false, q_tf32_exact),
                      kEINVAL, "ttm_t: tensor-core chunk rejected after the first");   // same shape: unreachable
         return;
       }
@@ -62,7 +64,7 @@ void ttm_t_dispatch(const Ctx& ctx, Arena& ws, const float* X, Box box, const fl
   ttm_t<float, float, float>(ctx, X, box, Q, 1, ldq, C, out, so_a, so_c, so_b);
 }
 void ttm_t_dispatch(const Ctx& ctx, Arena&, const double* X, Box box, const double* Q, int64_t ldq, int C, double* out,
-                    int64_t so_a, int64_t so_c, int64_t so_b) {
+                    int64_t so_a, int64_t so_c, int64_t so_b, bool = false) {
   ttm_t<double, double, double>(ctx, X, box, Q, 1, ldq, C, out, so_a, so_c, so_b);
 }
 
@@ -214,7 +216,7 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
       T* qc = ws.alloc_n<T>(ldo * K);
       if (ldo != cur[k0]) fill_zero(ctx, qc, sizeof(T) * ldo * K);
       transpose_copy<T>(ctx, static_cast<const T*>(omega[k0]), cur[k0], K, omega_ld[k0], qc, ldo);
-      ttm_t_dispatch(ctx, ws, data, b0, qc, ldo, K, W0, 1, b0.a, b0.a * K);
+      ttm_t_dispatch(ctx, ws, data, b0, qc, ldo, K, W0, 1, b0.a, b0.a * K, ctx.omega_tf32 != 0);
     }
     cur[k0] = K;
     const void* src = W0;
@@ -647,7 +649,7 @@ void Engine::pet(const TView& X, const int64_t* R, const void* const* omega, con
     int64_t ld0;
     const T* w0 = working_copy<T>(ctx, ws, Wt[0], X.d[0], Sp[0], ldw[0], ld0);
     T* h1 = ws.alloc_n<T>(b0.a * Sp[0] * b0.b);
-    ttm_t_dispatch(ctx, ws, data, b0, w0, ld0, int(Sp[0]), h1, 1, b0.a, b0.a * Sp[0]);
+    ttm_t_dispatch(ctx, ws, data, b0, w0, ld0, int(Sp[0]), h1, 1, b0.a, b0.a * Sp[0], ctx.omega_tf32 != 0);
     cur[0] = Sp[0];
     const double* src = nullptr;
     for (int n = 1; n < N; ++n) {

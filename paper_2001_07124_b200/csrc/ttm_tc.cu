@@ -494,10 +494,11 @@ struct TParams {
   bool split_out;     // write each output row as [hi (NHO) | lo (NHO)] tf32 halves (vec4 layout)
 };
 
-template <int NPAD, bool AKM>   // AKM: mode 0 (a == 1), X tile K-major [BM j][KC i]
+// AKM: mode 0 (a == 1), X tile K-major [BM j][KC i].  BSPLIT: Q = Q_hi + Q_lo pre-split (an fp64
+// basis is never tf32-exact); !BSPLIT: Q is tf32-exact (a host-rounded test matrix, R18), 2 products.
+template <int NPAD, bool AKM, bool BSPLIT>
 __global__ void __launch_bounds__(NT_TTM, 1)
 ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb, const TParams p) {
-  constexpr bool BSPLIT = true;                        // Q (fp64 basis) is never tf32-exact
   using L = Plan<NPAD, BSPLIT, false>;
   constexpr int NX = L::NX;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -553,7 +554,7 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
   } else if (warp == 1 || warp == 7) {
     const int q = warp == 1 ? 0 : 1;
     if (q < L::NI) {                                   // ---------------- MMA issuers (whole warp)
-      const uint32_t idesc0 = idesc_tf32(BM, L::NH + NPAD, 0);
+      const uint32_t idesc0 = idesc_tf32(BM, BSPLIT ? L::NH + NPAD : NPAD, 0);
       const uint32_t idesc1 = idesc_tf32(BM, NPAD, 0);
       Ring rt, rb;
       int64_t g = 0;                                   // global segment counter
@@ -724,13 +725,13 @@ void dispatch_s(const Ctx& ctx, bool amn, int bmode, const CUtensorMap& tx, cons
   else { if (amn) launch_s<NPAD, true, true, true>(ctx, tx, tb, p, g); else launch_s<NPAD, true, false, true>(ctx, tx, tb, p, g); }
 }
 
-template <int NPAD, bool AKM>
+template <int NPAD, bool AKM, bool BSPLIT>
 void launch_t(const Ctx& ctx, const CUtensorMap& tx, const CUtensorMap& tb, const TParams& p, dim3 grid) {
-  using L = Plan<NPAD, true, false>;
+  using L = Plan<NPAD, BSPLIT, false>;
   static bool attr = false;
-  if (!attr) { set_smem(ttm_t_tc_kernel<NPAD, AKM>, L::bytes); attr = true; }
+  if (!attr) { set_smem(ttm_t_tc_kernel<NPAD, AKM, BSPLIT>, L::bytes); attr = true; }
   launch(ctx, ctx.label ? ctx.label : "ttm_t_tc", [&] {
-    ttm_t_tc_kernel<NPAD, AKM><<<grid, NT_TTM, L::bytes, ctx.stream>>>(tx, tb, p);
+    ttm_t_tc_kernel<NPAD, AKM, BSPLIT><<<grid, NT_TTM, L::bytes, ctx.stream>>>(tx, tb, p);
   });
 }
 
@@ -904,7 +905,7 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
 }
 
 bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
-              int64_t so_a, int64_t so_c, int64_t so_b, bool split_out) {
+              int64_t so_a, int64_t so_c, int64_t so_b, bool split_out, bool q_tf32_exact) {
   const int npad = tc_npad(C);
   if (npad < 0) return false;
   const bool akm = (box.a == 1);
@@ -922,13 +923,19 @@ bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q
     const uint32_t bx[3] = {BM, KC, 1};
     if (!make_map(&tx, X, 3, d, s, bx, false)) return false;
   }
-  // pre-split [Q_hi | Q_lo] (I x 2 npad): the kernel loads it as one [2 npad][32] K-major slot
-  const int64_t ld2 = (box.I + 3) & ~int64_t(3);
-  float* Q2 = ws.alloc_n<float>(ld2 * 2 * npad);
-  if (!make_b_map(&tb, Q2, box.I, 2 * npad, ld2, 2 * npad)) return false;
-  launch(ctx, "split_q", [&] {
-    split_q_kernel<<<unsigned(cdiv(ld2 * npad, 256)), 256, 0, ctx.stream>>>(Q, box.I, C, ldq, npad, Q2, ld2);
-  });
+  const bool bsplit = !q_tf32_exact || !aligned(Q, 16) || (ldq % 4) != 0;
+  if (bsplit) {
+    // pre-split [Q_hi | Q_lo] (I x 2 npad): the kernel loads it as one [2 npad][32] K-major slot
+    const int64_t ld2 = (box.I + 3) & ~int64_t(3);
+    float* Q2 = ws.alloc_n<float>(ld2 * 2 * npad);
+    if (!make_b_map(&tb, Q2, box.I, 2 * npad, ld2, 2 * npad)) return false;
+    launch(ctx, "split_q", [&] {
+      split_q_kernel<<<unsigned(cdiv(ld2 * npad, 256)), 256, 0, ctx.stream>>>(Q, box.I, C, ldq, npad, Q2, ld2);
+    });
+  } else {
+    // tf32-exact Q read in place as a [npad][32] K-major slot (columns >= C read as zero)
+    if (!make_b_map(&tb, Q, box.I, C, ldq, npad)) return false;
+  }
   TParams p;
   p.a = box.a; p.I = box.I; p.b = box.b; p.C = C;
   p.tpb = akm ? 1 : cdiv(box.a, BM);
@@ -943,8 +950,13 @@ bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q
   const int64_t grid = std::min<int64_t>(p.ntiles, ctx.num_sms);
 #define RT_T_CASE(NP)                                                     \
   case NP:                                                                \
-    if (akm) launch_t<NP, true>(ctx, tx, tb, p, dim3(unsigned(grid)));   \
-    else launch_t<NP, false>(ctx, tx, tb, p, dim3(unsigned(grid)));      \
+    if (bsplit) {                                                        \
+      if (akm) launch_t<NP, true, true>(ctx, tx, tb, p, dim3(unsigned(grid)));  \
+      else launch_t<NP, false, true>(ctx, tx, tb, p, dim3(unsigned(grid)));     \
+    } else {                                                             \
+      if (akm) launch_t<NP, true, false>(ctx, tx, tb, p, dim3(unsigned(grid))); \
+      else launch_t<NP, false, false>(ctx, tx, tb, p, dim3(unsigned(grid)));    \
+    }                                                                    \
     break;
   switch (npad) {
     RT_T_CASE(16) RT_T_CASE(32) RT_T_CASE(48) RT_T_CASE(64) RT_T_CASE(80) RT_T_CASE(96) RT_T_CASE(128)

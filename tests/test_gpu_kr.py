@@ -140,3 +140,23 @@ def test_kr_loopback_multirank(P, nranks):
     for n in range(3):
         assert M.subspace(qg[n], ref["Q"][n]) <= 1e-5
     assert abs(out[0]["err"][0] - ref["E"]) / ref["E"] <= 1e-5
+
+
+@pytest.mark.parametrize("dims,K", [((128, 96, 64), 40), ((256, 36, 20, 12), 16), ((40, 36, 32), 13)])
+def test_kr_sketch_tf32_exact_factors(P, dims, K):
+    """RT_OPT_OMEGA_TF32 with host-rounded Khatri-Rao factors: the first TTM runs 2 tensor products
+    (no B split) and still matches the oracle on the same rounded factors."""
+    from paper_2001_07124_b200 import _lib as L
+    rng = np.random.default_rng(35)
+    x = np.asfortranarray(rng.standard_normal(dims).astype(np.float32))
+    hh = P.Handle()
+    hh.set_option(L.RT_OPT_OMEGA_TF32, 1)
+    X = _dev(x)
+    for n in range(len(dims)):
+        k = min(K, dims[n], x.size // dims[n])
+        oms = [None if j == n else synth.round_tf32(rng.standard_normal((dims[j], k))) for j in range(len(dims))]
+        y = P.rtucker_sketch(hh, X, n, [_t(o) for o in oms], kind="kr").cpu().numpy()
+        y0, _ = oracle.sketch_kr(x, n, oms)
+        assert M.rel_fro(y, y0) <= 1e-5, (n, M.rel_fro(y, y0))
+    hh.sync()
+    hh.close()

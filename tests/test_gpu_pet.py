@@ -174,3 +174,21 @@ def test_pet_loopback_multirank(P, nranks):
         assert M.subspace(qg[n], ref["Q"][n]) <= 1e-5
     assert M.recon(out[0]["G"], qg, ref["G"], ref["Q"]) <= 1e-5
     assert _e_ok(out[0]["err"][0], ref["E"]), (out[0]["err"][0], ref["E"])
+
+
+def test_pet_tf32_exact_omega_tilde(P):
+    """RT_OPT_OMEGA_TF32 with host-rounded Omega and Omega~: the core sketch's first stage runs 2
+    tensor products; parity with the oracle on the same rounded matrices."""
+    from paper_2001_07124_b200 import _lib as L
+    cfg = CASES["cfg2s"]
+    x = synth.make_tensor(cfg)
+    oms, omt = _inputs(cfg)
+    oms = [synth.round_tf32(o) for o in oms]
+    omt = [synth.round_tf32(o) for o in omt]
+    ref = oracle.pet(x, cfg.ranks, oms, omt)
+    hh = P.Handle()
+    hh.set_option(L.RT_OPT_OMEGA_TF32, 1)
+    res = P.rtucker_pet(hh, _dev(x), cfg.ranks, [_t(o) for o in oms], [_t(o) for o in omt])
+    hh.sync()
+    _check(P, res, ref)
+    hh.close()

@@ -46,6 +46,7 @@ def main():
     cfg = synth.CONFIGS[a.cfg]
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
     h = api.Handle()
+    h.set_option(3, 1)          # RT_OPT_OMEGA_TF32: test matrices are host-rounded to tf32 (R18), as in bench.py
     X, _ = synth.make_tensor_device(cfg, "cuda")
     xb = X.numel() * X.element_size()
     N = cfg.order
@@ -89,13 +90,14 @@ def main():
         emit(f"count_sketch mode {n}", timed(h, lambda: api.rtucker_sketch(h, X, n, (c, K), kind="count"), a.reps), 1,
              {"K": K}, cs_cpu if n == 0 else None)
     for n in range(N):
-        oms = [None if k == n else torch.from_numpy(o).cuda() for k, o in enumerate(synth.kr_omegas(cfg, n, cfg.dims))]
+        oms = [None if k == n else torch.from_numpy(synth.round_tf32(o)).cuda()
+               for k, o in enumerate(synth.kr_omegas(cfg, n, cfg.dims))]
         K = cfg.K(n)
         emit(f"khatri_rao_sketch mode {n}", timed(h, lambda: api.rtucker_sketch(h, X, n, oms, kind="kr"), a.reps), 1,
              {"K": K}, kr_cpu if n == 0 else None)
     ks, ss = synth.pet_sizes(cfg)
-    om = [torch.from_numpy(synth.gaussian_omega(cfg, n, K=ks[n])).cuda() for n in range(N)]
-    omt = [torch.from_numpy(synth.omega_tilde(cfg, n, ss[n])).cuda() for n in range(N)]
+    om = [torch.from_numpy(synth.round_tf32(synth.gaussian_omega(cfg, n, K=ks[n]))).cuda() for n in range(N)]
+    omt = [torch.from_numpy(synth.round_tf32(synth.omega_tilde(cfg, n, ss[n]))).cuda() for n in range(N)]
     emit("r_pet", timed(h, lambda: api.rtucker_pet(h, X, cfg.ranks, om, omt), a.reps), N + 2,
          {"note": "N factor sketches + core sketch + residual pass"}, pet_cpu)
     del om, omt
