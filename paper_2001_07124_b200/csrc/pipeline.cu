@@ -337,12 +337,20 @@ void Engine::core(const TView& X, const T* data, const double* const* Qt, const 
   for (int n = 0; n < N; ++n) QT[n] = working_copy<T>(ctx, ws, Qt[n], X.d[n], K[n], ldq[n], ldt[n]);
   int64_t cur[5];
   for (int k = 0; k < N; ++k) cur[k] = X.d[k];
+  // contraction order 0, N-1, N-2, ..., 1 (the core is multilinear; any order gives G): the first
+  // stage streams X, and the second then contracts the slowest mode of the shrunken tensor, whose
+  // rows (a = K_0 I_1 ... I_{N-2}) fill whole 128-row tiles; contracting mode 1 second would
+  // leave a = K_0 < 128 rows per tile (2/3 of each tile empty at K_0 = 80).
+  int ord[5];
+  ord[0] = 0;
+  for (int s2 = 1; s2 < N; ++s2) ord[s2] = N - s2;
   const T* src = data;
-  for (int n = 0; n < N; ++n) {
+  for (int s2 = 0; s2 < N; ++s2) {
+    const int n = ord[s2];
     const Box b = TView::box_of(cur, N, n);
     const int64_t ld = ldt[n];
-    if (n == N - 1) {
-      LabelScope ls(ctx, "core_last_simt");
+    if (s2 == N - 1) {
+      LabelScope ls(ctx, "core_last");
       ttm_t<T, T, double>(ctx, src, b, QT[n], 1, ld, int(K[n]), Gt, 1, b.a, b.a * K[n]);
     } else {
       T* dst = ws.alloc_n<T>(b.a * K[n] * b.b);
