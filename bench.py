@@ -376,7 +376,7 @@ def main():
     # dominant kernel class by measured device time: the X-streaming launches of one TTM shape
     # (ttm_s_tc = Omega sketch + power product Y = X Z; ttm_t_tc = Z = X^T Q + first core stage)
     prof = sorted(r["prof"], key=lambda e: -e[2])
-    classes = {"ttm_s": ("ttm_s_tc", "ttm_s_tc_pow"), "ttm_t": ("ttm_t_tc", "ttm_t_tc_pow"),
+    classes = {"ttm_s": ("ttm_s_tc", "ttm_s_tc_pow"), "ttm_t": ("ttm_t_tc", "ttm_t_tc_pow", "core_first"),
                "residual": ("residual_tc",)}
     cls_ms = {c: sum(t for nm, _, t in prof if nm in names) for c, names in classes.items()}
     cls = max(cls_ms, key=cls_ms.get) if prof else None

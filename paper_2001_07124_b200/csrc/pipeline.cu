@@ -354,6 +354,7 @@ void Engine::core(const TView& X, const T* data, const double* const* Qt, const 
       ttm_t<T, T, double>(ctx, src, b, QT[n], 1, ld, int(K[n]), Gt, 1, b.a, b.a * K[n]);
     } else {
       T* dst = ws.alloc_n<T>(b.a * K[n] * b.b);
+      LabelScope ls(ctx, s2 == 0 ? "core_first" : "core_mid");
       ttm_t_dispatch(ctx, ws, src, b, QT[n], ld, int(K[n]), dst, 1, b.a, b.a * K[n]);
       src = dst;
     }
