@@ -63,7 +63,7 @@ constexpr int sketch_cps() {
   return (512 - abase) / 128 >= 2 ? 2 : 1;
 }
 
-template <int NPAD, bool BSPLIT, bool BMN, int CPS_ = 1>
+template <int NPAD, bool BSPLIT, bool BMN, int CPS_ = 1, uint32_t OUTB = 0>
 struct Plan {
   // CPS chunks (of KC contraction elements) per pipeline stage: one ready wait, one commit and
   // one A slot of 64 CPS columns per stage -- the issuer warps' per-stage overhead (barrier wait,
@@ -93,11 +93,12 @@ struct Plan {
   // One stage = one A slot + one B slot, released together by a single tcgen05.commit per issuer
   // (every commit stalls the issuing warp's MMA stream, so there is one per stage).
   static constexpr int NBS = NB * CPS;                  // B slots (one per chunk)
-  static constexpr int NX_fit = int((budget - NBS * kBS) / kX);
+  static constexpr int NX_fit = int((budget - NBS * kBS - OUTB) / kX);
   static constexpr int NX = NX_fit > 10 ? 10 : NX_fit;
   static constexpr uint32_t off_x = 0;
   static constexpr uint32_t off_b = off_x + NX * kX;
-  static constexpr uint32_t off_bar = off_b + NBS * kBS;
+  static constexpr uint32_t off_o = off_b + NBS * kBS;  // output staging (1024-aligned), OUTB bytes
+  static constexpr uint32_t off_bar = off_o + OUTB;
   static constexpr int nbar = 2 * NX + 2 * NBS + 2 * 8 + 4;
   static constexpr uint32_t bytes = off_bar + 8 * nbar + 16;
   static_assert(NX >= 4, "X ring too shallow");
@@ -492,14 +493,21 @@ struct TParams {
   int64_t so_a, so_c, so_b;
   bool vec4;          // so_c == 1 and every output row 16-byte aligned with C % 4 == 0
   bool split_out;     // write each output row as [hi (NHO) | lo (NHO)] tf32 halves (vec4 layout)
+  bool tma_out;       // output tiles staged in shared memory and written by TMA stores (tmo)
 };
 
 // AKM: mode 0 (a == 1), X tile K-major [BM j][KC i].  BSPLIT: Q = Q_hi + Q_lo pre-split (an fp64
 // basis is never tf32-exact); !BSPLIT: Q is tf32-exact (a host-rounded test matrix, R18), 2 products.
+// Output rows (so_c == 1) are staged in shared memory as 128 B-swizzled [128 rows][32 cols] boxes
+// and written by TMA stores (tmo): one contiguous tile per store instead of 16-byte row pieces.
+template <int NPAD>
+constexpr uint32_t t_outb() { return uint32_t(BM) * ((NPAD + 31) / 32) * 128u; }
+
 template <int NPAD, bool AKM, bool BSPLIT>
 __global__ void __launch_bounds__(NT_TTM, 1)
-ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb, const TParams p) {
-  using L = Plan<NPAD, BSPLIT, false>;
+ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb,
+                const __grid_constant__ CUtensorMap tmo, const TParams p) {
+  using L = Plan<NPAD, BSPLIT, false, 1, t_outb<NPAD>()>;
   constexpr int NX = L::NX;
   extern __shared__ __align__(1024) uint8_t smem[];
   const Bars b = bars_of<L>(smem);
@@ -610,7 +618,31 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
       int64_t ob;
       if (AKM) { const int64_t j = beta + r; valid = j < p.b; ob = j * p.so_b; }
       else { const int64_t al = a0 + r; valid = al < p.a; ob = al * p.so_a + beta * p.so_b; }
-      if (valid) {
+      if (p.tma_out) {
+        constexpr int NBX = (NPAD + 31) / 32;
+        uint8_t* stage = smem + L::off_o;
+        if (u > 0 && r == 0) bulk_wait_read0();              // the previous tile's stores have read it
+        named_bar(1, 128);
+#pragma unroll
+        for (int bx = 0; bx < NBX; ++bx)
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int c = 32 * bx + 4 * q;
+            const float4 v = make_float4(c < NPAD ? sums[c % NPAD] : 0.f, c + 1 < NPAD ? sums[(c + 1) % NPAD] : 0.f,
+                                         c + 2 < NPAD ? sums[(c + 2) % NPAD] : 0.f,
+                                         c + 3 < NPAD ? sums[(c + 3) % NPAD] : 0.f);
+            *reinterpret_cast<float4*>(stage + bx * (BM * 128) + r * 128 + ((q ^ (r & 7)) << 4)) = v;
+          }
+        fence_proxy_async();
+        named_bar(1, 128);
+        if (r == 0) {
+          const int row0 = AKM ? int(beta) : int(a0 + p.a * beta);
+#pragma unroll
+          for (int bx = 0; bx < NBX; ++bx)
+            if (32 * bx < p.C) tma_store_2d(&tmo, stage + bx * (BM * 128), 32 * bx, row0);
+          bulk_commit();
+        }
+      } else if (valid) {
         if (p.split_out) {                                   // [hi | lo] rows for a pre-split B operand
           constexpr int NHO = ((NPAD + 31) / 32) * 32;
           float4* oh = reinterpret_cast<float4*>(p.out + ob);
@@ -638,6 +670,7 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
 #pragma unroll
       for (int k = 0; k < NPAD; ++k) sums[k] = 0.f;
     }
+    if (p.tma_out && r == 0) bulk_wait0();
   }
   tc_fence_before();
   __syncthreads();
@@ -726,12 +759,13 @@ void dispatch_s(const Ctx& ctx, bool amn, int bmode, const CUtensorMap& tx, cons
 }
 
 template <int NPAD, bool AKM, bool BSPLIT>
-void launch_t(const Ctx& ctx, const CUtensorMap& tx, const CUtensorMap& tb, const TParams& p, dim3 grid) {
-  using L = Plan<NPAD, BSPLIT, false>;
+void launch_t(const Ctx& ctx, const CUtensorMap& tx, const CUtensorMap& tb, const CUtensorMap& to, const TParams& p,
+              dim3 grid) {
+  using L = Plan<NPAD, BSPLIT, false, 1, t_outb<NPAD>()>;
   static bool attr = false;
   if (!attr) { set_smem(ttm_t_tc_kernel<NPAD, AKM, BSPLIT>, L::bytes); attr = true; }
   launch(ctx, ctx.label ? ctx.label : "ttm_t_tc", [&] {
-    ttm_t_tc_kernel<NPAD, AKM, BSPLIT><<<grid, NT_TTM, L::bytes, ctx.stream>>>(tx, tb, p);
+    ttm_t_tc_kernel<NPAD, AKM, BSPLIT><<<grid, NT_TTM, L::bytes, ctx.stream>>>(tx, tb, to, p);
   });
 }
 
@@ -947,15 +981,31 @@ bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q
   p.split_out = split_out;
   RT_REQUIRE(!split_out || (so_c == 1 && (so_a % 4) == 0 && (so_b % 4) == 0 && aligned(out, 16)), kEINVAL,
              "split output needs 16-byte aligned row-major rows");
+  // TMA-stored output tiles: row-major rows (so_c == 1) with one row pitch across the whole
+  // output (mode 0: rows j = beta, pitch so_b; a > 1: rows alpha + a beta with so_b = a so_a and
+  // whole 128-row tiles per beta)
+  CUtensorMap to;
+  std::memset(&to, 0, sizeof(to));
+  p.tma_out = false;
+  if (p.vec4 && !split_out && !getenv("RT_TC_NO_TMA_OUT")) {
+    const int64_t pitch = akm ? so_b : so_a;
+    const int64_t rows = akm ? box.b : box.a * box.b;
+    const bool rowsok = akm || (box.a % BM == 0 && so_b == box.a * so_a);
+    if (rowsok && rows <= INT32_MAX) {
+      const uint64_t d[2] = {uint64_t(C), uint64_t(rows)}, st[1] = {uint64_t(pitch) * 4};
+      const uint32_t bx[2] = {32, uint32_t(BM)};
+      p.tma_out = make_map(&to, out, 2, d, st, bx, true);
+    }
+  }
   const int64_t grid = std::min<int64_t>(p.ntiles, ctx.num_sms);
 #define RT_T_CASE(NP)                                                     \
   case NP:                                                                \
     if (bsplit) {                                                        \
-      if (akm) launch_t<NP, true, true>(ctx, tx, tb, p, dim3(unsigned(grid)));  \
-      else launch_t<NP, false, true>(ctx, tx, tb, p, dim3(unsigned(grid)));     \
+      if (akm) launch_t<NP, true, true>(ctx, tx, tb, to, p, dim3(unsigned(grid)));  \
+      else launch_t<NP, false, true>(ctx, tx, tb, to, p, dim3(unsigned(grid)));     \
     } else {                                                             \
-      if (akm) launch_t<NP, true, false>(ctx, tx, tb, p, dim3(unsigned(grid))); \
-      else launch_t<NP, false, false>(ctx, tx, tb, p, dim3(unsigned(grid)));    \
+      if (akm) launch_t<NP, true, false>(ctx, tx, tb, to, p, dim3(unsigned(grid))); \
+      else launch_t<NP, false, false>(ctx, tx, tb, to, p, dim3(unsigned(grid)));    \
     }                                                                    \
     break;
   switch (npad) {

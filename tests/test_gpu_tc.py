@@ -152,7 +152,10 @@ def test_tc_hosvd_parity(P, htc, name, dims, core, ranks):
     htc.sync()
     htc.set_option(1, 0)
     names = {n for n, _, _ in htc.profile_read()[0]}
-    assert "ttm_s_tc" in names and (cfg.q == 0 or "ttm_t_tc" in names), names
+    # the X-streaming launches ran on the tensor cores: the sketches, the power products and the
+    # first core stage (labels of csrc/pipeline.cu)
+    assert "ttm_s_tc" in names and "core_first" in names, names
+    assert cfg.q == 0 or ("ttm_t_tc_pow" in names and "ttm_s_tc_pow" in names), names
     qg = [mat(q) for q in res["Q"]]
     gg = P.core_to_numpy(res["G"])
     for n in range(3):
