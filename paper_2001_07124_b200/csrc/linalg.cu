@@ -6,6 +6,7 @@
 // and small helpers.
 #include <cfloat>
 
+#include <cstdlib>
 #include "kernels.h"
 
 namespace rt {
@@ -175,6 +176,145 @@ __global__ void __launch_bounds__(512) chol_inv_kernel(const double* __restrict_
     } else {
       if (R) R[e] = (r <= c) ? L[tri(c, r)] : 0.0;
       Rinv[e] = (r <= c) ? W[tri(c, r)] : 0.0;
+    }
+  }
+}
+
+// Blocked variant (k <= 128): panels of NBK = 16 columns, so the barrier count is per panel, not
+// per column.  A (k x ld, ld = k + 1, lower part) is factored in place into L; W = L^{-1}.
+//   per panel p:  warp 0 factors the diagonal block (column by column, __syncwarp only);
+//                 L21 = A21 L11^{-T} (one thread per row, forward substitution over the panel);
+//                 A22 -= L21 L21^T (lower part, all threads).
+//   inverse:      D_p = L_pp^{-1} for every diagonal block (one warp each), then row blocks
+//                 p = 1..: W_pq = -D_p sum_{r=q}^{p-1} L_pr W_rq for all q < p at once.
+constexpr int NBK = 16;
+
+__global__ void __launch_bounds__(256) chol_inv_blk_kernel(const double* __restrict__ G, int k, double shift_coef,
+                                                           double* __restrict__ R, double* __restrict__ Rinv,
+                                                           int* zero_flag, int* status) {
+  extern __shared__ double sm[];
+  const int ld = k + 1;
+  double* A = sm;                          // k x ld, L in the lower part
+  double* W = sm + size_t(k) * ld;         // k x ld, W = L^{-1} (lower part)
+  double* T = W + size_t(k) * ld;          // k x NBK scratch (sum_r L_pr W_rq for the current row block)
+  double* rl = T + size_t(k) * NBK;        // 1 / L_jj (fp64 divisions are long dependent sequences)
+  __shared__ double red[32];
+  __shared__ double s_shift, s_tr;
+  __shared__ int s_bad;
+  const int t = threadIdx.x, nt = blockDim.x;
+  const int warp = t >> 5, lane = t & 31, nw = nt >> 5;
+  double tr = 0.0;
+  for (int i = t; i < k; i += nt) tr += G[i + int64_t(k) * i];
+  tr = block_sum(tr, red);
+  if (t == 0) {
+    s_tr = tr;
+    s_shift = shift_coef * tr;
+    s_bad = 0;
+    if (!(tr == tr) || tr > DBL_MAX) latch(status, kStatusNonFinite);
+    if (zero_flag) *zero_flag = (tr == 0.0) ? 1 : 0;
+  }
+  __syncthreads();
+  const bool is_zero = (s_tr == 0.0);
+  for (int e = t; e < k * k; e += nt) {
+    const int i = e / k, c = e % k;
+    A[i * ld + c] = (c <= i) ? G[i + int64_t(k) * c] + (i == c ? s_shift : 0.0) : 0.0;
+    W[i * ld + c] = 0.0;
+  }
+  __syncthreads();
+  const int np = (k + NBK - 1) / NBK;
+  if (!is_zero) {
+    for (int pb = 0; pb < np; ++pb) {
+      const int c0 = pb * NBK, nb = min(NBK, k - c0);
+      if (warp == 0) {                               // diagonal block, unblocked (lane = row)
+        for (int jj = 0; jj < nb; ++jj) {
+          const int j = c0 + jj;
+          double d = A[j * ld + j];
+          if (!(d > 0.0)) { if (lane == 0) s_bad = 1; d = 1.0; }
+          const double sd = sqrt(d), rsd = 1.0 / sd;
+          __syncwarp();
+          const int i = c0 + lane;
+          if (lane < nb && lane > jj) A[i * ld + j] *= rsd;
+          __syncwarp();
+          if (lane == jj) { A[j * ld + j] = sd; rl[j] = rsd; }
+          if (lane < nb && lane > jj) {
+            const double lij = A[i * ld + j];
+            for (int c = jj + 1; c <= lane; ++c) A[i * ld + c0 + c] -= lij * A[(c0 + c) * ld + j];
+          }
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+      // L21 = A21 L11^{-T}: rows below the panel, one thread per row
+      for (int i = c0 + nb + t; i < k; i += nt) {
+        double* ai = A + i * ld;
+        for (int jj = 0; jj < nb; ++jj) {
+          const int j = c0 + jj;
+          double v = ai[j];
+          for (int m = 0; m < jj; ++m) v -= ai[c0 + m] * A[j * ld + c0 + m];
+          ai[j] = v * rl[j];
+        }
+      }
+      __syncthreads();
+      // A22 -= L21 L21^T (lower part); warp per row, lanes over columns
+      for (int i = c0 + nb + warp; i < k; i += nw) {
+        const double* li = A + i * ld + c0;
+        for (int c = c0 + nb + lane; c <= i; c += 32) {
+          const double* lc = A + c * ld + c0;
+          double v = 0.0;
+#pragma unroll
+          for (int m = 0; m < NBK; ++m) if (m < nb) v = fma(li[m], lc[m], v);
+          A[i * ld + c] -= v;
+        }
+      }
+      __syncthreads();
+    }
+    // D_p = L_pp^{-1} into W's diagonal blocks: warp per block, lane = column of the block
+    for (int pb = warp; pb < np; pb += nw) {
+      const int c0 = pb * NBK, nb = min(NBK, k - c0);
+      if (lane < nb) {
+        const int c = c0 + lane;
+        W[c * ld + c] = rl[c];
+        for (int j = c + 1; j < c0 + nb; ++j) {
+          double v = 0.0;
+          for (int m = c; m < j; ++m) v = fma(A[j * ld + m], W[m * ld + c], v);
+          W[j * ld + c] = -v * rl[j];
+        }
+      }
+    }
+    __syncthreads();
+    // off-diagonal blocks, row block by row block: W_pq = -D_p (sum_{r=q}^{p-1} L_pr W_rq)
+    for (int pb = 1; pb < np; ++pb) {
+      const int r0 = pb * NBK, nr = min(NBK, k - r0);
+      // T[i][c] = sum_{m < r0} L[r0 + i][m] W[m][c] for all c < r0 (lower-triangular W: m >= c)
+      for (int e = t; e < nr * r0; e += nt) {
+        const int i = e / r0, c = e % r0;
+        const double* li = A + (r0 + i) * ld;
+        double v0 = 0.0, v1 = 0.0;
+        int m = c;
+        for (; m + 1 < r0; m += 2) { v0 = fma(li[m], W[m * ld + c], v0); v1 = fma(li[m + 1], W[(m + 1) * ld + c], v1); }
+        if (m < r0) v0 = fma(li[m], W[m * ld + c], v0);
+        T[i * k + c] = v0 + v1;
+      }
+      __syncthreads();
+      for (int e = t; e < nr * r0; e += nt) {
+        const int i = e / r0, c = e % r0;
+        double v = 0.0;
+        for (int m = 0; m <= i; ++m) v = fma(W[(r0 + i) * ld + r0 + m], T[m * k + c], v);
+        W[(r0 + i) * ld + c] = -v;
+      }
+      __syncthreads();
+    }
+  }
+  if (t == 0 && s_bad) latch(status, kStatusCholBreakdown);
+  // R = L^T (upper), Rinv = W^T; col-major k x k
+  for (int e = t; e < k * k; e += nt) {
+    const int r = e % k, c = e / k;
+    if (is_zero) {
+      if (R) R[e] = 0.0;
+      Rinv[e] = 0.0;
+    } else {
+      if (R) R[e] = (r <= c) ? A[c * ld + r] : 0.0;
+      Rinv[e] = (r <= c) ? W[c * ld + r] : 0.0;
     }
   }
 }
@@ -544,13 +684,18 @@ void chol_inv(const Ctx& ctx, const double* G, int k, double shift_coef, double*
               int* zero_flag) {
   const size_t smem = sizeof(double) * size_t(k) * (k + 1);
   RT_REQUIRE(smem <= 220 * 1024, kEUNSUPPORTED, "chol_inv: k too large");
+  const size_t smem_blk = sizeof(double) * (2 * size_t(k) * (k + 1) + size_t(k) * NBK + size_t(k));
   static bool attr = false;
   if (!attr) {
     RT_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    RT_CUDA(cudaFuncSetAttribute(chol_inv_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     attr = true;
   }
   launch(ctx, "chol_inv", [&] {
-    chol_inv_kernel<<<1, 512, smem, ctx.stream>>>(G, k, shift_coef, R, Rinv, zero_flag, ctx.d_status);
+    if (smem_blk <= 220 * 1024 && !getenv("RT_CHOL_UNBLOCKED"))
+      chol_inv_blk_kernel<<<1, 256, smem_blk, ctx.stream>>>(G, k, shift_coef, R, Rinv, zero_flag, ctx.d_status);
+    else
+      chol_inv_kernel<<<1, 512, smem, ctx.stream>>>(G, k, shift_coef, R, Rinv, zero_flag, ctx.d_status);
   });
 }
 
