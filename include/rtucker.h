@@ -52,7 +52,7 @@ typedef enum {
   RT_ECUDA = -4,        /* CUDA runtime error (message in rt_last_error) */
   RT_ENCCL = -5,        /* NCCL error or NCCL unavailable */
   RT_ENUMERIC = -6,     /* device-detected breakdown (reported by rt_sync) */
-  RT_EUNSUPPORTED = -7  /* valid but not implemented (e.g. K_n > 256) */
+  RT_EUNSUPPORTED = -7  /* valid but not implemented (e.g. K_n > 128) */
 } rt_status;
 
 typedef enum { RT_F32 = 0, RT_F64 = 1 } rt_dtype;
@@ -103,7 +103,7 @@ rt_status rt_sync(rt_handle* h);
  * matrices (Gaussian Omega, the Khatri-Rao factors, R-PET's Omega~) is exactly representable in
  * tf32 (e.g. rounded on the host before it is given to both the oracle and this library); the
  * tensor-core products with them then skip the A_hi*Omega_lo product of the 3xTF32 split.  RT_OPT_TC_SEGMENT: contraction chunks (of 32) accumulated in TMEM before the fp32
- * accumulator is drained to registers (default 8, i.e. 256 elements; the tensor core's fp32
+ * accumulator is drained to registers (default 16, i.e. 512 elements; the tensor core's fp32
  * accumulation error grows with this length, tests/test_gpu_tc.py).  RT_OPT_TC_SKEW: tuning of
  * the split-K chunk order (rotation per row tile; default 0).  RT_OPT_QR_FALLBACK is reserved. */
 typedef enum { RT_OPT_TTM_IMPL = 0, RT_OPT_PROFILE = 1, RT_OPT_QR_FALLBACK = 2, RT_OPT_OMEGA_TF32 = 3,
@@ -147,7 +147,7 @@ rt_status rtucker_sketch(rt_handle* h, const rt_tensor* X, int mode, rt_omega_ki
  * Y: col-major m x k (RT_F32 or RT_F64), read-only.  Q: fp64 col-major m x k (ldq).
  * R: fp64 col-major k x k, nullable.  rows_distributed != 0: m is the local row count and
  * the Gram matrices are allreduced over the handle's communicator.  All-zero Y gives
- * Q = I[:, :k], R = 0 (reading R7).  Requires m >= k (global), k <= 256. */
+ * Q = I[:, :k], R = 0 (reading R7).  Requires m >= k (global), k <= 128. */
 rt_status rtucker_qr(rt_handle* h, int64_t m, int64_t k, rt_dtype dtype, const void* Y, int64_t ldy,
                      double* Q, int64_t ldq, double* R, int rows_distributed);
 
