@@ -18,6 +18,7 @@ RT_F32, RT_F64 = 0, 1
 RT_OMEGA_GAUSS, RT_OMEGA_KRON, RT_OMEGA_KR, RT_OMEGA_COUNT = 0, 1, 2, 3
 RT_OPT_TTM_IMPL, RT_OPT_PROFILE, RT_OPT_QR_FALLBACK, RT_OPT_OMEGA_TF32, RT_OPT_TC_SEGMENT, RT_OPT_TC_SKEW = 0, 1, 2, 3, 4, 5
 RT_OPT_FORCE_COLLECTIVES = 6
+RT_OPT_TC_ABLATE = 100          # profiling / A-B switches (210/211: fp16-split power product off/on)
 
 EXPORTS = ["rt_get_unique_id", "rt_create", "rt_loopback_group_create", "rt_loopback_group_destroy",
            "rt_create_loopback", "rt_destroy", "rt_last_error", "rt_sync", "rt_set_option", "rt_profile_read",

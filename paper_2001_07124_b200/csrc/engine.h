@@ -36,6 +36,11 @@ class Engine {
   Arena& ws;
   Comm* comm;
   bool dist() const { return comm && (comm->nranks() > 1 || ctx.force_dist); }
+  // fp16-split power products: the scale s of X (x_scale_h16) in a slot owned by the driver that
+  // outlives the per-mode sketches, computed once per tensor (xs_key = the data it was taken of)
+  float* xs_slot = nullptr;
+  const void* xs_key = nullptr;
+  const float* x_scale(const float* data, int64_t n);
 
   // (1) sketch of mode n incl. q power iterations; Yt: fp64 I_n(local) x K, ld I_n(local).
   template <typename T>
@@ -50,7 +55,7 @@ class Engine {
   // orthonormalize the tall Z of the power iteration in place (shifted CholeskyQR, fp64 Gram)
   template <typename T>
   bool qr_z(T* Z, int64_t m, int64_t ldz, int64_t m_glob, int k, bool rows_dist, int64_t row0, T* Z2 = nullptr,
-            int64_t ldz2 = 0);
+            int64_t ldz2 = 0, int split = 1);
   // (3) core G~ = X x_n Qt_n^T (all n) -> fp64 Gt (replicated)
   template <typename T>
   void core(const TView& X, const T* data, const double* const* Qt, const int64_t* ldq, const int64_t* K,

@@ -42,17 +42,28 @@ void count_sketch(const Ctx& ctx, Arena& ws, const T* X, Box box, const int32_t*
 // MN-major operand.  b_tf32_exact drops the A_hi*B_lo product.
 // b_presplit: B holds rows [B_hi (tc_split_width(K) columns, zero padded) | B_lo (same)] written by
 // ttm_t_tc(split_out) -- no split work in the kernel.
+// b_presplit with xscale (device scalar from x_scale_h16): fp16 split instead (ttm_s_h16_kernel):
+// B rows are [B_hi (tc_npad(K) halves) | B_lo (same)] written by ttm_t_tc(split_out = 2), ldb in
+// halves (a multiple of 8), |B| <= 1; X is scaled by *xscale before its fp16 split.
 bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Bm, int64_t ldb, bool b_tf32_exact,
-              int K, double* Y, int64_t ldy, bool b_presplit = false);
+              int K, double* Y, int64_t ldy, bool b_presplit = false, const float* xscale = nullptr,
+              unsigned int* amax = nullptr);
+// amax (tf32 kernels): also atomicMax max|X| of the tiles read into *amax (float bits; caller zeroes)
+// *s = 2^(15 - e) with 2^(e-1) <= max|X| < 2^e over the n elements of X (1 if max|X| is 0 or not
+// finite): max |s X| in [2^14, 2^15), inside the fp16 range with 11 significant bits kept
+void x_scale_h16(const Ctx& ctx, Arena& ws, const float* X, int64_t n, float* s);
+// the same scale from a max|X| already gathered (ttm_s_tc amax)
+void x_scale_from_amax(const Ctx& ctx, const unsigned int* amax, float* s);
 // whether ttm_s_tc would run (same shape/alignment rules, no launch)
 bool ttm_s_tc_ok(const Ctx& ctx, const float* X, Box box, int K);
 int tc_npad(int K);
 int tc_split_width(int K);
 // out(alpha,c,beta) = sum_i X(alpha,i,beta) Q(i,c), Q col-major (any ld; split into a [hi | lo]
 // workspace copy).  split_out: each output row (so_c == 1) is written as [hi | lo] halves of
-// tc_split_width(C) columns each (the pre-split B operand of ttm_s_tc).
+// tc_split_width(C) columns each (the pre-split B operand of ttm_s_tc); split_out = 2: as fp16
+// [hi (tc_npad(C)) | lo (tc_npad(C))] rows, out then points to halves and so_a / so_b count halves.
 bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
-              int64_t so_a, int64_t so_c, int64_t so_b, bool split_out = false, bool q_tf32_exact = false);
+              int64_t so_a, int64_t so_c, int64_t so_b, int split_out = 0, bool q_tf32_exact = false);
 
 // Gram A^T A of an m x k matrix (fp64 out, k x k), partials reduced in fixed order.  A col-major
 // (element (r,c) at r + lda*c) or, with rowmajor, at r*lda + c.

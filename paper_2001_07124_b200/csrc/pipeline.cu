@@ -30,14 +30,17 @@ int64_t pad4(int64_t x) { return (x + 3) & ~int64_t(3); }
 
 // Y = X_(n) B (B row-major, row pitch ldb: Omega or Z): tcgen05 3xTF32 kernel for fp32 data when
 // the shape fits the TMA path, else the SIMT kernel.
-void ttm_s_dispatch(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B, int64_t ldb, bool exact,
-                    int K, double* Y, int64_t ldy) {
-  if (ctx.ttm_impl != 1 && ttm_s_tc(ctx, ws, X, box, B, ldb, exact, K, Y, ldy)) return;
+// amax: also gather max|X| there (tensor-core kernel only; the return value says whether it did)
+bool ttm_s_dispatch(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B, int64_t ldb, bool exact,
+                    int K, double* Y, int64_t ldy, unsigned int* amax = nullptr) {
+  if (ctx.ttm_impl != 1 && ttm_s_tc(ctx, ws, X, box, B, ldb, exact, K, Y, ldy, false, nullptr, amax)) return amax != nullptr;
   ttm_s<float>(ctx, ws, X, box, B, ldb, 1, K, Y, ldy);
+  return false;
 }
-void ttm_s_dispatch(const Ctx& ctx, Arena& ws, const double* X, Box box, const double* B, int64_t ldb, bool,
-                    int K, double* Y, int64_t ldy) {
+bool ttm_s_dispatch(const Ctx& ctx, Arena& ws, const double* X, Box box, const double* B, int64_t ldb, bool,
+                    int K, double* Y, int64_t ldy, unsigned int* = nullptr) {
   ttm_s<double>(ctx, ws, X, box, B, ldb, 1, K, Y, ldy);
+  return false;
 }
 // out(alpha,c,beta) = sum_i X(alpha,i,beta) Q(i,c), Q col-major (ldq)
 // q_tf32_exact: Q holds tf32-representable values (a host-rounded test matrix, reading R18): the
@@ -125,12 +128,18 @@ void Engine::qr_y(const double* Y, int64_t m, int64_t m_glob, int k, int64_t ldy
   qr_rows<double>(Y, m, m_glob, k, ldy, Q, ldq, R, rows_dist, row0);
 }
 
+const float* Engine::x_scale(const float* data, int64_t n) {
+  RT_REQUIRE(xs_slot != nullptr, kEINVAL, "x_scale: no scale slot");
+  if (xs_key != data) { x_scale_h16(ctx, ws, data, n, xs_slot); xs_key = data; }   // a separate max|X| pass
+  return xs_slot;
+}
+
 // Z only conditions the next product Y = X_(n) Z (span(X Z R^-1) = span(X Z)); a single
 // CholeskyQR step with a small safety shift keeps it well conditioned.  Z is row-major
-// (m x k, row pitch ldz).
+// (m x k, row pitch ldz).  split: form of the Z2 copy (1 tf32 [hi | lo], 2 fp16 [hi | lo]).
 template <typename T>
 bool Engine::qr_z(T* Z, int64_t m, int64_t ldz, int64_t m_glob, int k, bool rows_dist, int64_t row0, T* Z2,
-                  int64_t ldz2) {
+                  int64_t ldz2, int split) {
   const auto mk = ws.mark();
   double* G = ws.alloc_n<double>(int64_t(k) * k);
   double* Rr = ws.alloc_n<double>(int64_t(k) * k);
@@ -162,7 +171,7 @@ bool Engine::qr_z(T* Z, int64_t m, int64_t ldz, int64_t m_glob, int k, bool rows
       const float* RiT = working_copy<float>(ctx, ws, Ri, k, k, k, ldr);
       LabelScope ls(ctx, "zapply_tc");
       // Z2 requested: Z R^{-1} written as the pre-split [hi | lo] operand of the next product
-      if (Z2) done_apply = ttm_t_tc(ctx, ws, Z, zb, RiT, ldr, k, Z2, 0, 1, ldz2, /*split_out=*/true);
+      if (Z2) done_apply = ttm_t_tc(ctx, ws, Z, zb, RiT, ldr, k, Z2, 0, 1, ldz2, /*split_out=*/split);
       else done_apply = ttm_t_tc(ctx, ws, Z, zb, RiT, ldr, k, Z, 0, 1, ldz);
     }
   }
@@ -179,11 +188,22 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
   const Box bx = X.box(n);
   const bool last = (n == N - 1);
   const int64_t In = bx.I;
+  // fp16-split power products (fp32 data): X's scale in a slot that outlives this sketch (the
+  // driver's, else one taken here); gathered by the first pass over X when that is a tf32 sketch
+  bool own_slot = false;
+  if constexpr (std::is_same<T, float>::value) {
+    if (q > 0 && ctx.tc_h16 && !xs_slot) { xs_slot = ws.alloc_n<float>(1); xs_key = nullptr; own_slot = true; }
+  }
   int K;
   if (kind == 0) {
     K = int(omega_cols[n]);
     const T* om = static_cast<const T*>(omega[n]);
     int64_t ld = omega_ld[n];
+    unsigned int* am = nullptr;
+    if (std::is_same<T, float>::value && q > 0 && ctx.tc_h16 && xs_key != data) {
+      am = ws.alloc_n<unsigned int>(1);
+      RT_CUDA(cudaMemsetAsync(am, 0, sizeof(unsigned int), ctx.stream));
+    }
     const auto mo = ws.mark();
     if (std::is_same<T, float>::value && ctx.ttm_impl != 1 && (ld % 4) != 0) {
       // the TMA path needs a 16-byte row pitch: repack Omega (J x K, small next to X) with ld = pad4(K)
@@ -193,7 +213,10 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
       om = c;
       ld = ldp;
     }
-    ttm_s_dispatch(ctx, ws, data, bx, om, ld, ctx.omega_tf32 != 0, K, Yt, In);
+    if (ttm_s_dispatch(ctx, ws, data, bx, om, ld, ctx.omega_tf32 != 0, K, Yt, In, am)) {
+      x_scale_from_amax(ctx, am, xs_slot);
+      xs_key = data;
+    }
     ws.rewind(mo);
   } else if (kind == 3) {
     // count sketch: hash, group, sign and sum the columns of X_(n); no multiplications
@@ -284,8 +307,17 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
   // (row pitch 2 * tc_split_width(K)) so the product Y = X_(n) Z does no split work per tile
   T* Z2 = nullptr;
   int64_t ldz2 = 0;
+  int zsplit = 0;
+  const float* xsc = nullptr;
   if constexpr (std::is_same<T, float>::value) {
-    if (ctx.tc_presplit_z && ttm_s_tc_ok(ctx, data, bx, K) && ldz == K) {
+    if (ctx.tc_h16 && ctx.ttm_impl != 1 && ttm_s_tc_ok(ctx, data, bx, K) && ldz == K) {
+      // fp16 split (ttm_s_h16_kernel): Z R^-1 written as fp16 [hi | lo] rows of 2 tc_npad(K) halves
+      zsplit = 2;
+      ldz2 = 2 * int64_t(tc_npad(K));
+      Z2 = reinterpret_cast<T*>(ws.alloc_n<uint16_t>(Jl * ldz2));
+      xsc = x_scale(data, X.size());
+    } else if (ctx.tc_presplit_z && ttm_s_tc_ok(ctx, data, bx, K) && ldz == K) {
+      zsplit = 1;
       ldz2 = 2 * int64_t(tc_split_width(K));
       Z2 = ws.alloc_n<T>(Jl * ldz2);
     }
@@ -311,12 +343,12 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
       for (int k = n + 1; k < N - 1; ++k) bp *= X.d[k];
       zrow0 = bx.a * bp * X.off;
     }
-    const bool pre = qr_z<T>(Z, Jl, ldz, X.Jg(n), K, !last && dist(), zrow0, Z2, ldz2);
+    const bool pre = qr_z<T>(Z, Jl, ldz, X.Jg(n), K, !last && dist(), zrow0, Z2, ldz2, zsplit);
     {
       LabelScope ls(ctx, "ttm_s_tc_pow");
       bool done = false;
       if constexpr (std::is_same<T, float>::value) {
-        if (pre) done = ttm_s_tc(ctx, ws, data, bx, Z2, ldz2, false, K, Yt, In, /*b_presplit=*/true);
+        if (pre) done = ttm_s_tc(ctx, ws, data, bx, Z2, ldz2, false, K, Yt, In, /*b_presplit=*/true, xsc);
       }
       RT_REQUIRE(!pre || done, kEUNSUPPORTED, "pre-split power product not launched");
       if (!done) ttm_s_dispatch(ctx, ws, data, bx, Z, ldz, false, K, Yt, In);
@@ -324,6 +356,7 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
     allreduce(comm, !last && dist(), Yt, In * K, ctx.stream);                     // C1
   }
   ws.rewind(mk);
+  if (own_slot) { xs_slot = nullptr; xs_key = nullptr; }
 }
 
 // ---------------------------------------------------------------------- core (a5)
@@ -496,6 +529,8 @@ void Engine::hosvd(const TView& X, const int64_t* R, int q, int kind, const void
   const int N = X.N;
   const T* data = static_cast<const T*>(X.data);
   const auto mk = ws.mark();
+  xs_slot = ws.alloc_n<float>(1);      // X's fp16 scale, taken once for all modes' power products
+  xs_key = nullptr;
   int64_t K[5], ldq[5];
   double* Qt[5];
   for (int n = 0; n < N; ++n) {
@@ -520,6 +555,7 @@ void Engine::hosvd(const TView& X, const int64_t* R, int q, int kind, const void
   truncate(X, Gt, K, Qt, ldq, R, Q_out, G_out);
   if (E || Eg) rel_error<T>(X, data, G_out, R, Q_out, E, Eg);
   ws.rewind(mk);
+  xs_slot = nullptr;
 }
 
 // -------------------------------------------------------------- STHOSVD (Alg.8)
@@ -532,6 +568,8 @@ void Engine::sthosvd(const TView& X, const int64_t* R, int q, int kind, const vo
                      double* G_out, double* E, double* Eg) {
   const int N = X.N;
   const auto mk = ws.mark();
+  xs_slot = ws.alloc_n<float>(1);
+  xs_key = nullptr;
   TView S = X;                         // working tensor S (reading R8: S = X)
   const double* sd = nullptr;          // fp64 S after the first shrink
   int64_t total = 1;
@@ -604,6 +642,7 @@ void Engine::sthosvd(const TView& X, const int64_t* R, int q, int kind, const vo
   }
   if (E || Eg) rel_error<T>(X, static_cast<const T*>(X.data), G_out, R, Q_out, E, Eg);
   ws.rewind(mk);
+  xs_slot = nullptr;
 }
 
 // --------------------------------------------------------------- R-PET (Alg.9)
@@ -797,8 +836,8 @@ template void Engine::sketch<float>(const TView&, const float*, int, int, const 
                                     const int64_t*, int, double*);
 template void Engine::sketch<double>(const TView&, const double*, int, int, const void* const*, const int64_t*,
                                      const int64_t*, int, double*);
-template bool Engine::qr_z<float>(float*, int64_t, int64_t, int64_t, int, bool, int64_t, float*, int64_t);
-template bool Engine::qr_z<double>(double*, int64_t, int64_t, int64_t, int, bool, int64_t, double*, int64_t);
+template bool Engine::qr_z<float>(float*, int64_t, int64_t, int64_t, int, bool, int64_t, float*, int64_t, int);
+template bool Engine::qr_z<double>(double*, int64_t, int64_t, int64_t, int, bool, int64_t, double*, int64_t, int);
 template void Engine::qr_rows<float>(const float*, int64_t, int64_t, int, int64_t, double*, int64_t, double*,
                                      bool, int64_t);
 template void Engine::qr_rows<double>(const double*, int64_t, int64_t, int, int64_t, double*, int64_t, double*,

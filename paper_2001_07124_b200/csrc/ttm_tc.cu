@@ -17,6 +17,8 @@
 // accumulators drained every `seg` stages into fp32 registers: the tensor core's fp32 accumulation
 // error grows with the accumulation length (7.5e-6 relative after 1024 terms, 2.6e-5 after 3.5K;
 // 1.4e-6 when drained every 128, tests/test_gpu_tc.py).
+#include <cuda_fp16.h>
+
 #include <cstdio>
 #include <cstring>
 #include <vector>
@@ -152,17 +154,23 @@ __device__ __forceinline__ uint64_t bdesc(uint32_t saddr, int kk) {
 // Splitter: read this thread's row of the raw X tile, write hi/lo tf32 to its TMEM lane.
 //   AMN  : tile [KC][BM] (row r is a column): element (r, k) at k*BM + r
 //   !AMN : tile [BM][KC] with 128B swizzle: 16B chunk c of row r at ((c ^ (r&7)) << 4)
-template <bool AMN>
-__device__ __forceinline__ void split_row_to_tmem(const float* xs, int r, uint32_t t_hi) {
+// AMAX: also fold max |x| of the row into m (the fp16 scale of X, taken during a tf32 pass)
+template <bool AMN, bool AMAX = false>
+__device__ __forceinline__ void split_row_to_tmem(const float* xs, int r, uint32_t t_hi, float* m = nullptr) {
   uint32_t hi[32], lo[32];
   if (AMN) {
 #pragma unroll
-    for (int q = 0; q < 32; ++q) split_tf32(xs[q * BM + r], hi[q], lo[q]);
+    for (int q = 0; q < 32; ++q) {
+      const float v = xs[q * BM + r];
+      if (AMAX) *m = fmaxf(*m, fabsf(v));
+      split_tf32(v, hi[q], lo[q]);
+    }
   } else {
     const float* row = xs + r * KC;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const float4 v = *reinterpret_cast<const float4*>(row + ((c ^ (r & 7)) << 2));
+      if (AMAX) *m = fmaxf(fmaxf(*m, fmaxf(fabsf(v.x), fabsf(v.y))), fmaxf(fabsf(v.z), fabsf(v.w)));
       split_tf32(v.x, hi[4 * c + 0], lo[4 * c + 0]);
       split_tf32(v.y, hi[4 * c + 1], lo[4 * c + 1]);
       split_tf32(v.z, hi[4 * c + 2], lo[4 * c + 2]);
@@ -282,6 +290,7 @@ struct SParams {
   int ablate;         // profiling only: 1 = no MMA, 2 = no split work (results invalid)
   int skew;           // chunk-order rotation per M-tile (decorrelates the rows' DRAM addresses)
   float* part;        // [split][K][I]
+  unsigned int* amax; // optional: max |X| over the tiles read (as the bits of a non-negative float)
   unsigned long long* tim;   // diagnostics (RT_OPT_TC_ABLATE = 1000): per-CTA role wait cycles, else null
   long long* trace;          // diagnostics (RT_OPT_TC_ABLATE = 2000): per-chunk event clocks of CTA (0,0)
 };
@@ -433,15 +442,20 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
     const uint32_t lane_base = tmem + (uint32_t(32 * q4) << 16);
     const int t = threadIdx.x - 64;
     unsigned long long* tim = (warp == 2) ? p.tim : nullptr;   // warp-uniform (aligned tcgen05 ops inside)
+    float xmax = 0.f;
     Ring rx;
     for (int it = 0; it < nch; ++it, rx.next<NX>()) {
       const int g = it / CPS, c = it % CPS, sl = st_slot(g), bs = it % L::NBS;
       RT_TIMED(tim, 10, mbar_wait(&b.x_full[rx.s], rx.ph));
       if (c == 0 && g >= NB) RT_TIMED(tim, 11, mbar_wait(&b.tfree[sl], st_par(g) ^ 1));   // stage's TMEM slot free
       RT_TIMED(tim, 12, {
-        if (p.ablate != 2)
-          split_row_to_tmem<AMN>(reinterpret_cast<const float*>(smem + L::off_x + rx.s * L::kX), r,
-                                 lane_base + L::a_slot(sl) + 64u * c);
+        const float* xs = reinterpret_cast<const float*>(smem + L::off_x + rx.s * L::kX);
+        if (p.ablate == 2) {
+        } else if (p.amax) {
+          split_row_to_tmem<AMN, true>(xs, r, lane_base + L::a_slot(sl) + 64u * c, &xmax);
+        } else {
+          split_row_to_tmem<AMN>(xs, r, lane_base + L::a_slot(sl) + 64u * c);
+        }
       });
       mbar_arrive(&b.x_free[rx.s]);
       RT_TIMED(tim, 13, mbar_wait(&b.b_full[bs], uint32_t(it / L::NBS) & 1u));
@@ -455,6 +469,11 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
         tc_fence_before();
         mbar_arrive(&b.ready[sl]);
       }
+    }
+    if (p.amax) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) xmax = fmaxf(xmax, __shfl_xor_sync(0xffffffffu, xmax, o));
+      if (lane == 0) atomicMax(p.amax, __float_as_uint(xmax));
     }
   } else if (warp >= 8) {                              // ---------------- epilogue: drain segments
     const int q4 = warp & 3;
@@ -481,6 +500,249 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
+// ================================================================ ttm_s, fp16 split
+// The power product Y = X_(n) Q_z with Q_z = Z R^-1 pre-split by the zapply epilogue into fp16
+// rows [Q_hi (NPAD) | Q_lo (NPAD)] of 2^14 Q_z (|Q_z| <= 1: inside the fp16 range).  X is scaled by the power of two s
+// (xscale, from max|X|, so max|sX| is in [2^14, 2^15)) and split x s = x_hi + x_lo in fp16 by the
+// splitters; D0 += A_hi [Q_hi | Q_lo] (issuer 0, N = 2 NPAD), D1 += A_lo Q_hi (issuer 1); the
+// epilogue multiplies by 1/s.  Same 22 significant bits per operand as the 3xTF32 form; fp16 runs
+// K = 16 per instruction at twice the tf32 rate, so the stage needs half the MMA instructions and
+// half the tensor time, and the A slot is half as wide (32 TMEM columns per chunk).
+// Q_z is stored times 2^14: its entries are <= 1 in magnitude but typically ~J^-1/2 (5e-4 at
+// J = 2048^2), whose lo parts would otherwise fall into the fp16 subnormals (11 bits lost)
+constexpr float kQScale = 16384.f;
+
+template <int NPAD>
+struct PlanH {
+  static constexpr int CPS = 2;
+  static constexpr int NBX = (2 * NPAD + 63) / 64;       // 64-wide MN atoms of the [hi | lo] B rows
+  static constexpr uint32_t kB = uint32_t(NBX) * 4096u;  // 32 k-rows x 128 B per atom column
+  static constexpr uint32_t kBS = kB;
+  static constexpr int NI = 2;
+  static constexpr int NBUF = 1;
+  static constexpr uint32_t acc_cols = 3u * NPAD;
+  static constexpr uint32_t a_base = (acc_cols + 63u) & ~63u;
+  static constexpr int NB_fit = int((512u - a_base) / (32u * CPS));
+  static constexpr int NB = NB_fit > 6 ? 6 : NB_fit;
+  static_assert(NB >= 2, "TMEM plan leaves fewer than two A stages");
+  static_assert(2 * NPAD <= 256 && NPAD % 16 == 0, "f16 operand shape");
+  __host__ __device__ static constexpr uint32_t acc(int q, int) { return q == 0 ? 0u : uint32_t(2 * NPAD); }
+  __host__ __device__ static constexpr uint32_t a_slot(int s) { return a_base + 32u * CPS * uint32_t(s); }
+  static constexpr uint32_t kX = uint32_t(BM) * KC * 4;
+  static constexpr uint32_t budget = 224u * 1024u;
+  static constexpr int NBS = NB * CPS;
+  static constexpr int NX_fit = int((budget - NBS * kBS) / kX);
+  static constexpr int NX = NX_fit > 10 ? 10 : NX_fit;
+  static constexpr uint32_t off_x = 0;
+  static constexpr uint32_t off_b = off_x + NX * kX;
+  static constexpr uint32_t off_bar = off_b + NBS * kBS;
+  static constexpr int nbar = 2 * NX + 2 * NBS + 2 * 8 + 4;
+  static constexpr uint32_t bytes = off_bar + 8 * nbar + 16;
+  static_assert(NX >= 4, "X ring too shallow");
+  static_assert(NB <= 8 && NBS <= 16, "barrier plan");
+};
+
+// MN-major fp16 SWIZZLE_128B operand (tools/f16_probe.cu): atoms of 8 k-rows x 128 B (64 n);
+// LBO = 4 KB between 64-wide atom columns (32 k-rows each), SBO = 1 KB between 8-row k groups;
+// the K = 16 step kk starts 2 KB further.
+__device__ __forceinline__ uint64_t bdesc_h16(uint32_t saddr, int kk) {
+  return sdesc(saddr + 2048u * uint32_t(kk), 4096u, 1024u) | (uint64_t(2) << 61);
+}
+
+// Splitter (fp16): this thread's row of the raw X tile, scaled by s, as packed fp16 hi/lo pairs
+template <bool AMN>
+__device__ __forceinline__ void split_row_to_tmem_h16(const float* xs, int r, float s, uint32_t t_hi) {
+  float v[32];
+  if (AMN) {
+#pragma unroll
+    for (int q = 0; q < 32; ++q) v[q] = xs[q * BM + r] * s;
+  } else {
+    const float* row = xs + r * KC;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const float4 w = *reinterpret_cast<const float4*>(row + ((c ^ (r & 7)) << 2));
+      v[4 * c + 0] = w.x * s; v[4 * c + 1] = w.y * s; v[4 * c + 2] = w.z * s; v[4 * c + 3] = w.w * s;
+    }
+  }
+  uint32_t hi[16], lo[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) split_h16x2(v[2 * c], v[2 * c + 1], hi[c], lo[c]);
+  tmem_st16(t_hi, hi);
+  tmem_st16(t_hi + 16, lo);
+}
+
+struct HParams {
+  SParams s;
+  const float* xscale;   // device: s (a power of two)
+};
+
+template <int NPAD, bool AMN>
+__global__ void __launch_bounds__(NT_TTM, 1)
+ttm_s_h16_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb, const HParams hp) {
+  using L = PlanH<NPAD>;
+  const SParams& p = hp.s;
+  constexpr int NX = L::NX, CPS = L::CPS, NB = L::NB;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const Bars b = bars_of<L>(smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t z = blockIdx.y, S = gridDim.y;
+  const int64_t i0 = int64_t(blockIdx.x) * BM;
+  const int64_t per = (p.nchunks + S - 1) / S;
+  const int64_t cbeg = z * per;
+  const int nch = cbeg < p.nchunks ? int(min(per, p.nchunks - cbeg)) : 0;
+  const int nst = (nch + CPS - 1) / CPS;
+  const int rot = nch ? int((int64_t(blockIdx.x) * p.skew) % nch) : 0;
+  auto chunk_of = [&](int it) { int c = it + rot; return cbeg + (c >= nch ? c - nch : c); };
+  auto st_slot = [](int g) { return g % NB; };
+  auto st_par = [](int g) { return uint32_t(g / NB) & 1u; };
+
+  if (threadIdx.x == 0) {
+    init_bars<L>(b);
+    tma_prefetch(&tmx);
+    tma_prefetch(&tmb);
+  }
+  if (warp == 1) tmem_alloc(b.tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *b.tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {                                   // ---------------- X producer
+      Ring rx;
+      const uint64_t pol = policy_evict_first();
+      for (int it = 0; it < nch; ++it, rx.next<NX>()) {
+        if (it >= NX) mbar_wait(&b.x_free[rx.s], rx.ph ^ 1);
+        int64_t a0, beta, j0;
+        chunk_coords<AMN>(p, chunk_of(it), a0, beta, j0);
+        mbar_expect_tx(&b.x_full[rx.s], L::kX);
+        void* xs = smem + L::off_x + rx.s * L::kX;
+        if (AMN) tma_load_2d_hint(xs, &tmx, &b.x_full[rx.s], int(i0), int(j0), pol);
+        else tma_load_3d_hint(xs, &tmx, &b.x_full[rx.s], int(a0), int(i0), int(beta), pol);
+      }
+    }
+  } else if (warp == 6) {
+    if (lane == 0) {                                   // ---------------- B producer (one slot per chunk)
+      const uint64_t pol = policy_evict_last();
+      for (int it = 0; it < nch; ++it) {
+        const int g = it / CPS, bs = it % L::NBS;
+        if (g >= NB) mbar_wait(&b.tfree[st_slot(g)], st_par(g) ^ 1);
+        int64_t a0, beta, j0;
+        chunk_coords<AMN>(p, chunk_of(it), a0, beta, j0);
+        mbar_expect_tx(&b.b_full[bs], L::kB);
+#pragma unroll
+        for (int x = 0; x < L::NBX; ++x)
+          tma_load_2d_hint(smem + L::off_b + bs * L::kBS + x * 4096, &tmb, &b.b_full[bs], 64 * x, int(j0), pol);
+      }
+    }
+  } else if (warp == 1 || warp == 7) {
+    const int q = warp == 1 ? 0 : 1;                   // ---------------- MMA issuers (whole warp)
+    const uint32_t idesc = idesc_f16(BM, q == 0 ? 2 * NPAD : NPAD, 1);
+    const uint32_t d = tmem + L::acc(q, 0);
+    const int spg = (p.seg + CPS - 1) / CPS;
+    int64_t u = 0;
+    int pos = 0;
+    for (int g = 0; g < nst; ++g) {
+      const bool first = pos == 0;
+      const bool last = (pos == spg - 1) || (g == nst - 1);
+      const int sl = st_slot(g);
+      if (first) wait_acc_free<L>(b, u);
+      mbar_wait(&b.ready[sl], st_par(g));               // A split and B landed
+      tc_fence_after();
+      const int c0 = g * CPS;
+      const int cn = (nch - c0) < CPS ? (nch - c0) : CPS;
+#pragma unroll
+      for (int c = 0; c < CPS; ++c) {
+        if (c < cn) {
+          const uint32_t a = tmem + L::a_slot(sl) + 32u * c + (q == 0 ? 0u : 16u);
+          const uint32_t bsa = smem_u32(smem + L::off_b + ((c0 + c) % L::NBS) * L::kBS);
+#pragma unroll
+          for (int kk = 0; kk < KC / 16; ++kk)
+            mma_f16_ts_w(d, a + 8 * kk, bdesc_h16(bsa, kk), idesc, (first && c == 0 && kk == 0) ? 0u : 1u);
+        }
+      }
+      mma_commit_w(&b.tfree[sl]);
+      if (last) { mma_commit_w(&b.acc_full[0]); ++u; pos = 0; } else { ++pos; }
+    }
+  } else if (warp >= 2 && warp <= 5) {                 // ---------------- splitters
+    const int q4 = warp & 3;
+    const int r = 32 * q4 + lane;
+    const uint32_t lane_base = tmem + (uint32_t(32 * q4) << 16);
+    const float sc = *hp.xscale;
+    Ring rx;
+    for (int it = 0; it < nch; ++it, rx.next<NX>()) {
+      const int g = it / CPS, c = it % CPS, sl = st_slot(g), bs = it % L::NBS;
+      mbar_wait(&b.x_full[rx.s], rx.ph);
+      if (c == 0 && g >= NB) mbar_wait(&b.tfree[sl], st_par(g) ^ 1);   // stage's TMEM slot free
+      split_row_to_tmem_h16<AMN>(reinterpret_cast<const float*>(smem + L::off_x + rx.s * L::kX), r, sc,
+                                 lane_base + L::a_slot(sl) + 32u * c);
+      mbar_arrive(&b.x_free[rx.s]);
+      if (c == CPS - 1 || it == nch - 1) {             // stage complete (B landed too)
+        mbar_wait(&b.b_full[bs], uint32_t(it / L::NBS) & 1u);
+        if (c == 1) mbar_wait(&b.b_full[bs - 1], uint32_t((it - 1) / L::NBS) & 1u);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&b.ready[sl]);
+      }
+    }
+  } else if (warp >= 8) {                              // ---------------- epilogue: drain segments
+    const int q4 = warp & 3;
+    const int r = 32 * q4 + lane;
+    const uint32_t lane_base = tmem + (uint32_t(32 * q4) << 16);
+    float sums[NPAD];
+#pragma unroll
+    for (int k = 0; k < NPAD; ++k) sums[k] = 0.f;
+    const int spg = (p.seg + CPS - 1) / CPS;
+    const int64_t nseg = (nst + spg - 1) / spg;
+    for (int64_t u = 0; u < nseg; ++u) {
+      mbar_wait(&b.acc_full[0], uint32_t(u) & 1u);
+      tc_fence_after();
+      add_cols<NPAD>(lane_base + L::acc(0, 0), sums);            // A_hi Q_hi
+      add_cols<NPAD>(lane_base + L::acc(0, 0) + NPAD, sums);     // A_hi Q_lo
+      add_cols<NPAD>(lane_base + L::acc(1, 0), sums);            // A_lo Q_hi
+      tc_fence_before();
+      mbar_arrive(&b.acc_empty[0]);
+    }
+    const float inv = 1.0f / (*hp.xscale * kQScale);  // exact: both scales are powers of two
+    const int64_t i = i0 + r;                         // partial tile -> part[split][k][i]
+    if (i < p.I) {
+      float* dst = p.part + z * p.K * p.I;
+#pragma unroll
+      for (int k = 0; k < NPAD; ++k)
+        if (k < p.K) dst[int64_t(k) * p.I + i] = sums[k] * inv;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+// max |X| -> s = 2^(14 - e), e = floor(log2 max|X|) (s = 1 for max|X| = 0 or non-finite), so
+// that max |s X| lies in [2^14, 2^15) below the fp16 maximum
+__global__ void __launch_bounds__(256) absmax_kernel(const float4* __restrict__ x, int64_t n4, const float* __restrict__ tail,
+                                                     int ntail, unsigned int* __restrict__ amax) {
+  float m = 0.f;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n4; e += int64_t(gridDim.x) * blockDim.x) {
+    const float4 v = __ldcs(x + e);
+    m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+  }
+  if (blockIdx.x == 0 && int(threadIdx.x) < ntail) m = fmaxf(m, fabsf(tail[threadIdx.x]));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(amax, __float_as_uint(m));   // non-negative floats order as integers
+}
+__global__ void xscale_kernel(const unsigned int* __restrict__ amax, float* __restrict__ s) {
+  const float m = __uint_as_float(*amax);
+  float r = 1.f;
+  if (m > 0.f && isfinite(m)) {
+    int e;
+    frexpf(m, &e);                                      // m = f 2^e, f in [0.5, 1): floor(log2 m) = e - 1
+    r = ldexpf(1.f, min(15 - e, 127));
+  }
+  *s = r;
+}
+
 // ====================================================================== ttm_t
 struct TParams {
   int64_t a, I, b;
@@ -492,7 +754,8 @@ struct TParams {
   float* out;
   int64_t so_a, so_c, so_b;
   bool vec4;          // so_c == 1 and every output row 16-byte aligned with C % 4 == 0
-  bool split_out;     // write each output row as [hi (NHO) | lo (NHO)] tf32 halves (vec4 layout)
+  int split_out;      // 1: each output row as [hi (NHO) | lo (NHO)] tf32 halves (vec4 layout);
+                      // 2: as fp16 [hi (NPAD) | lo (NPAD)] (out points to halves, so_* count halves)
   bool tma_out;       // output tiles staged in shared memory and written by TMA stores (tmo)
 };
 
@@ -643,7 +906,21 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
           bulk_commit();
         }
       } else if (valid) {
-        if (p.split_out) {                                   // [hi | lo] rows for a pre-split B operand
+        if (p.split_out == 2) {                              // fp16 [hi | lo] rows (ttm_s_h16_kernel B)
+          uint4* oh = reinterpret_cast<uint4*>(reinterpret_cast<__half*>(p.out) + ob);
+          uint4* ol = reinterpret_cast<uint4*>(reinterpret_cast<__half*>(p.out) + ob + NPAD);
+#pragma unroll
+          for (int k = 0; k < NPAD / 8; ++k) {
+            uint32_t h[4], l[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int c0 = 8 * k + 2 * e, c1 = c0 + 1;
+              split_h16x2(c0 < p.C ? sums[c0] * kQScale : 0.f, c1 < p.C ? sums[c1] * kQScale : 0.f, h[e], l[e]);
+            }
+            oh[k] = make_uint4(h[0], h[1], h[2], h[3]);
+            ol[k] = make_uint4(l[0], l[1], l[2], l[3]);
+          }
+        } else if (p.split_out) {                            // [hi | lo] rows for a pre-split B operand
           constexpr int NHO = ((NPAD + 31) / 32) * 32;
           float4* oh = reinterpret_cast<float4*>(p.out + ob);
           float4* ol = reinterpret_cast<float4*>(p.out + ob + NHO);
@@ -699,7 +976,8 @@ EncodeFn encode_fn() {
 }
 
 bool make_map(CUtensorMap* m, const void* ptr, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
-              const uint32_t* box, bool swz128, CUtensorMapSwizzle swz_override = CU_TENSOR_MAP_SWIZZLE_NONE) {
+              const uint32_t* box, bool swz128, CUtensorMapSwizzle swz_override = CU_TENSOR_MAP_SWIZZLE_NONE,
+              CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32) {
   EncodeFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t d[5], s[4];
@@ -707,7 +985,7 @@ bool make_map(CUtensorMap* m, const void* ptr, int rank, const uint64_t* dims, c
   for (int i = 0; i < rank; ++i) { d[i] = dims[i]; b[i] = box[i]; e[i] = 1; }
   for (int i = 0; i < rank - 1; ++i) s[i] = strides_bytes[i];
   std::memset(m, 0, sizeof(*m));
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, cuuint32_t(rank), const_cast<void*>(ptr), d, s, b, e,
+  CUresult r = fn(m, dt, cuuint32_t(rank), const_cast<void*>(ptr), d, s, b, e,
                   CU_TENSOR_MAP_INTERLEAVE_NONE,
                   swz_override != CU_TENSOR_MAP_SWIZZLE_NONE ? swz_override
                                                              : (swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE),
@@ -756,6 +1034,16 @@ void dispatch_s(const Ctx& ctx, bool amn, int bmode, const CUtensorMap& tx, cons
   if (bmode == 0) { if (amn) launch_s<NPAD, false, true, false>(ctx, tx, tb, p, g); else launch_s<NPAD, false, false, false>(ctx, tx, tb, p, g); }
   else if (bmode == 1) { if (amn) launch_s<NPAD, true, true, false>(ctx, tx, tb, p, g); else launch_s<NPAD, true, false, false>(ctx, tx, tb, p, g); }
   else { if (amn) launch_s<NPAD, true, true, true>(ctx, tx, tb, p, g); else launch_s<NPAD, true, false, true>(ctx, tx, tb, p, g); }
+}
+
+template <int NPAD, bool AMN>
+void launch_h(const Ctx& ctx, const CUtensorMap& tx, const CUtensorMap& tb, const HParams& p, dim3 grid) {
+  using L = PlanH<NPAD>;
+  static bool attr = false;
+  if (!attr) { set_smem(ttm_s_h16_kernel<NPAD, AMN>, L::bytes); attr = true; }
+  launch(ctx, ctx.label ? ctx.label : "ttm_s_h16", [&] {
+    ttm_s_h16_kernel<NPAD, AMN><<<grid, NT_TTM, L::bytes, ctx.stream>>>(tx, tb, p);
+  });
 }
 
 template <int NPAD, bool AKM, bool BSPLIT>
@@ -845,9 +1133,26 @@ bool ttm_s_tc_ok(const Ctx& ctx, const float* X, Box box, int K) {
   return !(box.a > INT32_MAX || box.I > INT32_MAX || box.b > INT32_MAX || J > INT32_MAX);
 }
 
+void x_scale_from_amax(const Ctx& ctx, const unsigned int* amax, float* s) {
+  launch(ctx, "xscale", [&] { xscale_kernel<<<1, 1, 0, ctx.stream>>>(amax, s); });
+}
+
+void x_scale_h16(const Ctx& ctx, Arena& ws, const float* X, int64_t n, float* s) {
+  RT_REQUIRE(aligned(X, 16), kEINVAL, "x_scale_h16: X must be 16-byte aligned");
+  unsigned int* amax = ws.alloc_n<unsigned int>(1);
+  RT_CUDA(cudaMemsetAsync(amax, 0, sizeof(unsigned int), ctx.stream));
+  const int64_t n4 = n / 4;
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(cdiv(n4, 256), int64_t(ctx.num_sms) * 8));
+  launch(ctx, "absmax", [&] {
+    absmax_kernel<<<unsigned(blocks), 256, 0, ctx.stream>>>(reinterpret_cast<const float4*>(X), n4, X + 4 * n4,
+                                                            int(n - 4 * n4), amax);
+  });
+  launch(ctx, "xscale", [&] { xscale_kernel<<<1, 1, 0, ctx.stream>>>(amax, s); });
+}
+
 // Returns false (nothing launched) when the shape/alignment is not supported by the TMA path.
 bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Bm, int64_t ldb, bool b_tf32_exact,
-              int K, double* Y, int64_t ldy, bool b_presplit) {
+              int K, double* Y, int64_t ldy, bool b_presplit, const float* xscale, unsigned int* amax) {
   const int npad = tc_npad(K);
   if (npad < 0) return false;
   const int64_t J = box.J();
@@ -867,7 +1172,16 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
     const uint32_t bx[3] = {KC, BM, 1};
     if (!make_map(&tx, X, 3, d, s, bx, true)) return false;
   }
-  if (!make_b_map_rm(&tb, Bm, J, b_presplit ? 2 * nh : K, ldb)) return false;
+  const bool h16 = b_presplit && xscale != nullptr;
+  if (h16) {
+    // fp16 [hi (npad) | lo (npad)] rows, row pitch ldb halves: (64 cols, 32 rows) SWIZZLE_128B boxes
+    if (!aligned(Bm, 16) || (ldb % 8) || ldb < 2 * npad) return false;
+    const uint64_t d[2] = {uint64_t(2 * npad), uint64_t(J)}, st[1] = {uint64_t(ldb) * 2};
+    const uint32_t bx[2] = {64, KC};
+    if (!make_map(&tb, Bm, 2, d, st, bx, true, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_DATA_TYPE_FLOAT16)) return false;
+  } else if (!make_b_map_rm(&tb, Bm, J, b_presplit ? 2 * nh : K, ldb)) {
+    return false;
+  }
   SParams p;
   p.a = box.a; p.I = box.I; p.b = box.b; p.K = K;
   p.cpb = amn ? 1 : cdiv(box.a, KC);
@@ -880,6 +1194,7 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
   p.ablate = ctx.tc_ablate;
   p.skew = ctx.tc_skew >= 0 ? ctx.tc_skew : 0;
   p.part = ws.alloc_n<float>(splits * K * box.I);
+  p.amax = h16 ? nullptr : amax;
   p.tim = nullptr;
   p.trace = nullptr;
   const dim3 grid{unsigned(mtiles), unsigned(splits), 1u};
@@ -892,9 +1207,15 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
     RT_CUDA(cudaMemsetAsync(p.tim, 0, sizeof(unsigned long long) * mtiles * splits * 24, ctx.stream));
   }
   const int bmode = b_presplit ? 2 : (b_tf32_exact ? 0 : 1);
-#define RT_S_CASE(NP)                                       \
-  case NP:                                                  \
-    dispatch_s<NP>(ctx, amn, bmode, tx, tb, p, grid);       \
+#define RT_S_CASE(NP)                                                                 \
+  case NP:                                                                            \
+    if (h16) {                                                                        \
+      const HParams hp{p, xscale};                                                    \
+      if (amn) launch_h<NP, true>(ctx, tx, tb, hp, grid);                             \
+      else launch_h<NP, false>(ctx, tx, tb, hp, grid);                                \
+    } else {                                                                          \
+      dispatch_s<NP>(ctx, amn, bmode, tx, tb, p, grid);                               \
+    }                                                                                 \
     break;
   switch (npad) {
     RT_S_CASE(16) RT_S_CASE(32) RT_S_CASE(48) RT_S_CASE(64) RT_S_CASE(80) RT_S_CASE(96) RT_S_CASE(128)
@@ -939,7 +1260,7 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
 }
 
 bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
-              int64_t so_a, int64_t so_c, int64_t so_b, bool split_out, bool q_tf32_exact) {
+              int64_t so_a, int64_t so_c, int64_t so_b, int split_out, bool q_tf32_exact) {
   const int npad = tc_npad(C);
   if (npad < 0) return false;
   const bool akm = (box.a == 1);
@@ -981,6 +1302,7 @@ bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q
   p.split_out = split_out;
   RT_REQUIRE(!split_out || (so_c == 1 && (so_a % 4) == 0 && (so_b % 4) == 0 && aligned(out, 16)), kEINVAL,
              "split output needs 16-byte aligned row-major rows");
+  RT_REQUIRE(split_out != 2 || ((so_a % 8) == 0 && (so_b % 8) == 0), kEINVAL, "fp16 split rows need 16-byte pitch");
   // TMA-stored output tiles: row-major rows (so_c == 1) with one row pitch across the whole
   // output (mode 0: rows j = beta, pitch so_b; a > 1: rows alpha + a beta with so_b = a so_a and
   // whole 128-row tiles per beta)

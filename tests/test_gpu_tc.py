@@ -125,6 +125,34 @@ def test_tc_power_iteration(P, htc, q):
     htc.sync()
 
 
+@pytest.mark.parametrize("scale", [1.0, 3e-12, 1e12])
+@pytest.mark.parametrize("h16", [True, False])
+def test_tc_power_iteration_h16(P, scale, h16):
+    """The power product on the fp16-split kernel (ttm_s_h16, X scaled by a power of two taken from
+    max|X|) against the 3xTF32 kernel and the oracle, at data scales far outside the fp16 range;
+    ragged shapes, several K (tc_npad 16 .. 128)."""
+    from paper_2001_07124_b200 import _lib as L
+    h = _handle(P, 2, omega_tf32=True)
+    h.set_option(L.RT_OPT_TC_ABLATE, 211 if h16 else 210)
+    try:
+        for dims, K in [((130, 100, 84), 16), ((256, 150, 70), 20), ((96, 140, 200), 48), ((140, 130, 150), 80),
+                        ((200, 160, 130), 128)]:
+            x = np.asfortranarray((np.random.default_rng(9).standard_normal(dims) * scale).astype(np.float32))
+            X = dev(x)
+            rng = np.random.default_rng(10)
+            for n in range(3):
+                om = synth.round_tf32(rng.standard_normal((x.size // dims[n], K)).astype(np.float32))
+                y = mat(P.rtucker_sketch(h, X, n, om_dev(om), q=1))
+                _, yo = oracle.sketch_gauss(x, n, om, 1)
+                assert np.all(np.isfinite(y))
+                # span(Y) = span(X_(n) X_(n)^T Q_y) does not depend on R_z (nor on its shift)
+                sub = M.subspace(np.linalg.qr(y)[0], np.linalg.qr(yo)[0])
+                assert sub <= 1e-5, (dims, K, n, sub)
+        h.sync()
+    finally:
+        h.close()
+
+
 @pytest.mark.parametrize("dims,C", [((128, 96, 64), (80, 16, 32)), ((500, 500, 40), (30, 30, 20))])
 def test_tc_core_parity(P, htc, dims, C):
     x = np.asfortranarray(np.random.default_rng(7).standard_normal(dims).astype(np.float32))
