@@ -63,7 +63,10 @@ int tc_split_width(int K);
 // tc_split_width(C) columns each (the pre-split B operand of ttm_s_tc); split_out = 2: as fp16
 // [hi (tc_npad(C)) | lo (tc_npad(C))] rows, out then points to halves and so_a / so_b count halves.
 bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
-              int64_t so_a, int64_t so_c, int64_t so_b, int split_out = 0, bool q_tf32_exact = false);
+              int64_t so_a, int64_t so_c, int64_t so_b, int split_out = 0, bool q_tf32_exact = false,
+              const float* xscale = nullptr);
+// xscale (device scale of X from x_scale_h16 / x_scale_from_amax, |Q| <= 1 required): the fp16
+// split form (ttm_t_tc_kernel<H16>) instead of 3xTF32; ignored with q_tf32_exact
 
 // Gram A^T A of an m x k matrix (fp64 out, k x k), partials reduced in fixed order.  A col-major
 // (element (r,c) at r + lda*c) or, with rowmajor, at r*lda + c.

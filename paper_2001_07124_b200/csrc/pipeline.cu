@@ -45,20 +45,21 @@ bool ttm_s_dispatch(const Ctx& ctx, Arena& ws, const double* X, Box box, const d
 // out(alpha,c,beta) = sum_i X(alpha,i,beta) Q(i,c), Q col-major (ldq)
 // q_tf32_exact: Q holds tf32-representable values (a host-rounded test matrix, reading R18): the
 // tensor-core kernel then runs 2 products instead of the 3 of the split form
+// xscale: X's fp16 scale when known (an orthonormal Q): the fp16-split kernel instead of 3xTF32
 void ttm_t_dispatch(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
-                    int64_t so_a, int64_t so_c, int64_t so_b, bool q_tf32_exact = false) {
+                    int64_t so_a, int64_t so_c, int64_t so_b, bool q_tf32_exact = false, const float* xscale = nullptr) {
   if (ctx.ttm_impl != 1) {
     if (C <= 128) {
-      if (ttm_t_tc(ctx, ws, X, box, Q, ldq, C, out, so_a, so_c, so_b, false, q_tf32_exact)) return;
+      if (ttm_t_tc(ctx, ws, X, box, Q, ldq, C, out, so_a, so_c, so_b, 0, q_tf32_exact, xscale)) return;
     } else {
       // wider than one TMEM tile (e.g. the R-PET core sketch, S_n = 2K_n + 1): balanced column
       // chunks of <= 128, one X pass each, each writing its slice of the output
       const int nch = int(cdiv(C, 128));
       const int cw = int(cdiv(C, nch) + 3) & ~3;
-      if (ttm_t_tc(ctx, ws, X, box, Q, ldq, cw, out, so_a, so_c, so_b, false, q_tf32_exact)) {
+      if (ttm_t_tc(ctx, ws, X, box, Q, ldq, cw, out, so_a, so_c, so_b, 0, q_tf32_exact, xscale)) {
         for (int c0 = cw; c0 < C; c0 += cw)
           RT_REQUIRE(ttm_t_tc(ctx, ws, X, box, Q + int64_t(c0) * ldq, ldq, std::min(cw, C - c0), out + c0 * so_c, so_a,
-                              so_c, so_b, false, q_tf32_exact),
+                              so_c, so_b, 0, q_tf32_exact, xscale),
                      kEINVAL, "ttm_t: tensor-core chunk rejected after the first");   // same shape: unreachable
         return;
       }
@@ -67,7 +68,7 @@ void ttm_t_dispatch(const Ctx& ctx, Arena& ws, const float* X, Box box, const fl
   ttm_t<float, float, float>(ctx, X, box, Q, 1, ldq, C, out, so_a, so_c, so_b);
 }
 void ttm_t_dispatch(const Ctx& ctx, Arena&, const double* X, Box box, const double* Q, int64_t ldq, int C, double* out,
-                    int64_t so_a, int64_t so_c, int64_t so_b, bool = false) {
+                    int64_t so_a, int64_t so_c, int64_t so_b, bool = false, const float* = nullptr) {
   ttm_t<double, double, double>(ctx, X, box, Q, 1, ldq, C, out, so_a, so_c, so_b);
 }
 
@@ -332,7 +333,7 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
     // so_a = ldz, so_c = 1, so_b = a ldz
     {
       LabelScope ls(ctx, "ttm_t_tc_pow");
-      ttm_t_dispatch(ctx, ws, data, bx, QyT, ldqt, K, Z, ldz, 1, bx.a * ldz);
+      ttm_t_dispatch(ctx, ws, data, bx, QyT, ldqt, K, Z, ldz, 1, bx.a * ldz, false, xsc);
     }
     ws.rewind(mq);
     allreduce(comm, last && dist(), Z, Jl * ldz, ctx.stream);                    // C3
@@ -388,7 +389,12 @@ void Engine::core(const TView& X, const T* data, const double* const* Qt, const 
     } else {
       T* dst = ws.alloc_n<T>(b.a * K[n] * b.b);
       LabelScope ls(ctx, s2 == 0 ? "core_first" : "core_mid");
-      ttm_t_dispatch(ctx, ws, src, b, QT[n], ld, int(K[n]), dst, 1, b.a, b.a * K[n]);
+      // the first stage streams X: fp16 split when X's scale is already known (a driver's sketches)
+      const float* xsc = nullptr;
+      if constexpr (std::is_same<T, float>::value) {
+        if (s2 == 0 && ctx.tc_h16 && xs_slot && xs_key == data) xsc = xs_slot;
+      }
+      ttm_t_dispatch(ctx, ws, src, b, QT[n], ld, int(K[n]), dst, 1, b.a, b.a * K[n], false, xsc);
       src = dst;
     }
     cur[n] = K[n];

@@ -21,6 +21,7 @@
 
 #include <cstdio>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "kernels.h"
@@ -512,9 +513,10 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
 // J = 2048^2), whose lo parts would otherwise fall into the fp16 subnormals (11 bits lost)
 constexpr float kQScale = 16384.f;
 
-template <int NPAD>
+template <int NPAD, int CPS_ = 2, uint32_t OUTB = 0>
 struct PlanH {
-  static constexpr int CPS = 2;
+  static constexpr int CPS = CPS_;
+  static constexpr int NH = NPAD;                        // D0 = [hi block | lo block]
   static constexpr int NBX = (2 * NPAD + 63) / 64;       // 64-wide MN atoms of the [hi | lo] B rows
   static constexpr uint32_t kB = uint32_t(NBX) * 4096u;  // 32 k-rows x 128 B per atom column
   static constexpr uint32_t kBS = kB;
@@ -531,11 +533,12 @@ struct PlanH {
   static constexpr uint32_t kX = uint32_t(BM) * KC * 4;
   static constexpr uint32_t budget = 224u * 1024u;
   static constexpr int NBS = NB * CPS;
-  static constexpr int NX_fit = int((budget - NBS * kBS) / kX);
+  static constexpr int NX_fit = int((budget - NBS * kBS - OUTB) / kX);
   static constexpr int NX = NX_fit > 10 ? 10 : NX_fit;
   static constexpr uint32_t off_x = 0;
   static constexpr uint32_t off_b = off_x + NX * kX;
-  static constexpr uint32_t off_bar = off_b + NBS * kBS;
+  static constexpr uint32_t off_o = off_b + NBS * kBS;  // output staging (ttm_t), OUTB bytes
+  static constexpr uint32_t off_bar = off_o + OUTB;
   static constexpr int nbar = 2 * NX + 2 * NBS + 2 * 8 + 4;
   static constexpr uint32_t bytes = off_bar + 8 * nbar + 16;
   static_assert(NX >= 4, "X ring too shallow");
@@ -757,6 +760,7 @@ struct TParams {
   int split_out;      // 1: each output row as [hi (NHO) | lo (NHO)] tf32 halves (vec4 layout);
                       // 2: as fp16 [hi (NPAD) | lo (NPAD)] (out points to halves, so_* count halves)
   bool tma_out;       // output tiles staged in shared memory and written by TMA stores (tmo)
+  const float* xscale;   // H16 kernels: device scale s of X (the output is divided by s 2^14)
 };
 
 // AKM: mode 0 (a == 1), X tile K-major [BM j][KC i].  BSPLIT: Q = Q_hi + Q_lo pre-split (an fp64
@@ -766,11 +770,14 @@ struct TParams {
 template <int NPAD>
 constexpr uint32_t t_outb() { return uint32_t(BM) * ((NPAD + 31) / 32) * 128u; }
 
-template <int NPAD, bool AKM, bool BSPLIT>
+// H16: the fp16 split (see ttm_s_h16_kernel): B = [2^14 Q_hi | 2^14 Q_lo] fp16 rows (row-major
+// I x 2 NPAD, MN-major atoms), X scaled by s and split by the splitters, 2 K = 16 steps per chunk.
+template <int NPAD, bool AKM, bool BSPLIT, bool H16 = false>
 __global__ void __launch_bounds__(NT_TTM, 1)
 ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb,
                 const __grid_constant__ CUtensorMap tmo, const TParams p) {
-  using L = Plan<NPAD, BSPLIT, false, 1, t_outb<NPAD>()>;
+  static_assert(!H16 || BSPLIT, "the fp16 form always carries Q_lo");
+  using L = std::conditional_t<H16, PlanH<NPAD, 1, t_outb<NPAD>()>, Plan<NPAD, BSPLIT, false, 1, t_outb<NPAD>()>>;
   constexpr int NX = L::NX;
   extern __shared__ __align__(1024) uint8_t smem[];
   const Bars b = bars_of<L>(smem);
@@ -819,14 +826,20 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
         for (int c = 0; c < p.nic; ++c, ++it, rb.next<L::NBS>()) {
           if (it >= L::NBS) mbar_wait(&b.b_free[rb.s], rb.ph ^ 1);
           mbar_expect_tx(&b.b_full[rb.s], L::kBS);
-          tma_load_2d_hint(smem + L::off_b + rb.s * L::kBS, &tmb, &b.b_full[rb.s], c * KC, 0, pol);
+          if constexpr (H16) {
+#pragma unroll
+            for (int x = 0; x < L::NBX; ++x)
+              tma_load_2d_hint(smem + L::off_b + rb.s * L::kBS + x * 4096, &tmb, &b.b_full[rb.s], 64 * x, c * KC, pol);
+          } else {
+            tma_load_2d_hint(smem + L::off_b + rb.s * L::kBS, &tmb, &b.b_full[rb.s], c * KC, 0, pol);
+          }
         }
     }
   } else if (warp == 1 || warp == 7) {
     const int q = warp == 1 ? 0 : 1;
     if (q < L::NI) {                                   // ---------------- MMA issuers (whole warp)
-      const uint32_t idesc0 = idesc_tf32(BM, BSPLIT ? L::NH + NPAD : NPAD, 0);
-      const uint32_t idesc1 = idesc_tf32(BM, NPAD, 0);
+      const uint32_t idesc0 = H16 ? idesc_f16(BM, 2 * NPAD, 1) : idesc_tf32(BM, BSPLIT ? L::NH + NPAD : NPAD, 0);
+      const uint32_t idesc1 = H16 ? idesc_f16(BM, NPAD, 1) : idesc_tf32(BM, NPAD, 0);
       Ring rt, rb;
       int64_t g = 0;                                   // global segment counter
       for (int64_t u = 0; u < my_tiles; ++u) {
@@ -837,8 +850,17 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
           if (first) wait_acc_free<L>(b, g);
           mbar_wait(&b.ready[rt.s], rt.ph);                // A split and B landed
           tc_fence_after();
-          issue_stage<L, BSPLIT, false>(tmem, q, acc_buf<L>(g), L::a_slot(rt.s),
-                                        smem_u32(smem + L::off_b + rb.s * L::kBS), idesc0, idesc1, first);
+          if constexpr (H16) {
+            const uint32_t d = tmem + L::acc(q, 0);
+            const uint32_t a = tmem + L::a_slot(rt.s) + (q == 0 ? 0u : 16u);
+            const uint32_t bsa = smem_u32(smem + L::off_b + rb.s * L::kBS);
+#pragma unroll
+            for (int kk = 0; kk < KC / 16; ++kk)
+              mma_f16_ts_w(d, a + 8 * kk, bdesc_h16(bsa, kk), q == 0 ? idesc0 : idesc1, (first && kk == 0) ? 0u : 1u);
+          } else {
+            issue_stage<L, BSPLIT, false>(tmem, q, acc_buf<L>(g), L::a_slot(rt.s),
+                                          smem_u32(smem + L::off_b + rb.s * L::kBS), idesc0, idesc1, first);
+          }
           mma_commit_w(&b.tfree[rt.s]);
           if (last) { mma_commit_w(&b.acc_full[acc_buf<L>(g)]); ++g; pos = 0; } else { ++pos; }
         }
@@ -850,12 +872,17 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
     const uint32_t lane_base = tmem + (uint32_t(32 * q4) << 16);
     Ring rx, rt;
     int it = 0;
+    const float sc = H16 ? *p.xscale : 1.f;
     for (int64_t u = 0; u < my_tiles; ++u) {
       for (int c = 0; c < p.nic; ++c, ++it, rx.next<NX>(), rt.next<L::NB>()) {
         mbar_wait(&b.x_full[rx.s], rx.ph);
         if (it >= L::NB) mbar_wait(&b.tfree[rt.s], rt.ph ^ 1);
-        split_row_to_tmem<!AKM>(reinterpret_cast<const float*>(smem + L::off_x + rx.s * L::kX), r,
-                                lane_base + L::a_slot(rt.s));
+        if constexpr (H16)
+          split_row_to_tmem_h16<!AKM>(reinterpret_cast<const float*>(smem + L::off_x + rx.s * L::kX), r, sc,
+                                      lane_base + L::a_slot(rt.s));
+        else
+          split_row_to_tmem<!AKM>(reinterpret_cast<const float*>(smem + L::off_x + rx.s * L::kX), r,
+                                  lane_base + L::a_slot(rt.s));
         mbar_arrive(&b.x_free[rx.s]);
         mbar_wait(&b.b_full[rt.s], rt.ph);
         tmem_wait_st();
@@ -871,10 +898,27 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
 #pragma unroll
     for (int k = 0; k < NPAD; ++k) sums[k] = 0.f;
     const int segs_per_tile = (p.nic + p.seg - 1) / p.seg;
+    const float inv = H16 ? 1.0f / (*p.xscale * kQScale) : 1.f;   // exact: powers of two
     int64_t g = 0;
     for (int64_t u = 0; u < my_tiles; ++u) {
       const int64_t tile = blockIdx.x + u * gridDim.x;
-      for (int sgi = 0; sgi < segs_per_tile; ++sgi, ++g) drain_acc<L, NPAD, BSPLIT>(b, lane_base, g, sums);
+      for (int sgi = 0; sgi < segs_per_tile; ++sgi, ++g) {
+        if constexpr (H16) {
+          mbar_wait(&b.acc_full[0], uint32_t(g) & 1u);
+          tc_fence_after();
+          add_cols<NPAD>(lane_base + L::acc(0, 0), sums);            // A_hi Q_hi
+          add_cols<NPAD>(lane_base + L::acc(0, 0) + NPAD, sums);     // A_hi Q_lo
+          add_cols<NPAD>(lane_base + L::acc(1, 0), sums);            // A_lo Q_hi
+          tc_fence_before();
+          mbar_arrive(&b.acc_empty[0]);
+        } else {
+          drain_acc<L, NPAD, BSPLIT>(b, lane_base, g, sums);
+        }
+      }
+      if constexpr (H16) {
+#pragma unroll
+        for (int k = 0; k < NPAD; ++k) sums[k] *= inv;
+      }
       int64_t a0, beta;
       tile_coords(tile, a0, beta);
       bool valid;
@@ -1046,14 +1090,14 @@ void launch_h(const Ctx& ctx, const CUtensorMap& tx, const CUtensorMap& tb, cons
   });
 }
 
-template <int NPAD, bool AKM, bool BSPLIT>
+template <int NPAD, bool AKM, bool BSPLIT, bool H16 = false>
 void launch_t(const Ctx& ctx, const CUtensorMap& tx, const CUtensorMap& tb, const CUtensorMap& to, const TParams& p,
               dim3 grid) {
-  using L = Plan<NPAD, BSPLIT, false, 1, t_outb<NPAD>()>;
+  using L = std::conditional_t<H16, PlanH<NPAD, 1, t_outb<NPAD>()>, Plan<NPAD, BSPLIT, false, 1, t_outb<NPAD>()>>;
   static bool attr = false;
-  if (!attr) { set_smem(ttm_t_tc_kernel<NPAD, AKM, BSPLIT>, L::bytes); attr = true; }
-  launch(ctx, ctx.label ? ctx.label : "ttm_t_tc", [&] {
-    ttm_t_tc_kernel<NPAD, AKM, BSPLIT><<<grid, NT_TTM, L::bytes, ctx.stream>>>(tx, tb, to, p);
+  if (!attr) { set_smem(ttm_t_tc_kernel<NPAD, AKM, BSPLIT, H16>, L::bytes); attr = true; }
+  launch(ctx, ctx.label ? ctx.label : (H16 ? "ttm_t_h16" : "ttm_t_tc"), [&] {
+    ttm_t_tc_kernel<NPAD, AKM, BSPLIT, H16><<<grid, NT_TTM, L::bytes, ctx.stream>>>(tx, tb, to, p);
   });
 }
 
@@ -1105,6 +1149,21 @@ __global__ void split_q_kernel(const float* __restrict__ Q, int64_t I, int C, in
   split_tf32(v, h, l);
   Q2[i + ld2 * c] = __uint_as_float(h);
   Q2[i + ld2 * (npad + c)] = __uint_as_float(l);
+}
+
+// Q (I x C, col-major ldq) -> Q2 row-major I x 2 npad fp16 (row pitch 2 npad): [2^14 Q_hi | 2^14 Q_lo],
+// columns >= C zero (the B operand of ttm_t_tc_kernel<H16>)
+__global__ void split_q_h16_kernel(const float* __restrict__ Q, int64_t I, int C, int64_t ldq, int npad,
+                                   uint32_t* __restrict__ Q2) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;   // one pair of columns of one row
+  const int hp = npad / 2;
+  if (e >= I * hp) return;
+  const int64_t i = e / hp;
+  const int c0 = 2 * int(e % hp), c1 = c0 + 1;
+  uint32_t h, l;
+  split_h16x2(c0 < C ? Q[i + ldq * c0] * kQScale : 0.f, c1 < C ? Q[i + ldq * c1] * kQScale : 0.f, h, l);
+  Q2[i * npad + c0 / 2] = h;
+  Q2[i * npad + hp + c0 / 2] = l;
 }
 
 }  // namespace
@@ -1260,9 +1319,10 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
 }
 
 bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
-              int64_t so_a, int64_t so_c, int64_t so_b, int split_out, bool q_tf32_exact) {
+              int64_t so_a, int64_t so_c, int64_t so_b, int split_out, bool q_tf32_exact, const float* xscale) {
   const int npad = tc_npad(C);
   if (npad < 0) return false;
+  const bool h16 = xscale != nullptr && !q_tf32_exact;
   const bool akm = (box.a == 1);
   if (!aligned(X, 16)) return false;
   if (akm ? (box.I % 4) : (box.a % 4)) return false;
@@ -1279,7 +1339,16 @@ bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q
     if (!make_map(&tx, X, 3, d, s, bx, false)) return false;
   }
   const bool bsplit = !q_tf32_exact || !aligned(Q, 16) || (ldq % 4) != 0;
-  if (bsplit) {
+  if (h16) {
+    // fp16 [2^14 Q_hi | 2^14 Q_lo] rows (I x 2 npad halves): (64 cols, 32 rows) SWIZZLE_128B boxes
+    uint32_t* Q2 = ws.alloc_n<uint32_t>(box.I * npad);
+    const uint64_t d[2] = {uint64_t(2 * npad), uint64_t(box.I)}, st[1] = {uint64_t(npad) * 4};
+    const uint32_t bx[2] = {64, KC};
+    if (!make_map(&tb, Q2, 2, d, st, bx, true, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_DATA_TYPE_FLOAT16)) return false;
+    launch(ctx, "split_q", [&] {
+      split_q_h16_kernel<<<unsigned(cdiv(box.I * (npad / 2), 256)), 256, 0, ctx.stream>>>(Q, box.I, C, ldq, npad, Q2);
+    });
+  } else if (bsplit) {
     // pre-split [Q_hi | Q_lo] (I x 2 npad): the kernel loads it as one [2 npad][32] K-major slot
     const int64_t ld2 = (box.I + 3) & ~int64_t(3);
     float* Q2 = ws.alloc_n<float>(ld2 * 2 * npad);
@@ -1300,6 +1369,7 @@ bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q
   p.out = out; p.so_a = so_a; p.so_c = so_c; p.so_b = so_b;
   p.vec4 = so_c == 1 && (so_a % 4) == 0 && (so_b % 4) == 0 && (C % 4) == 0 && aligned(out, 16);
   p.split_out = split_out;
+  p.xscale = h16 ? xscale : nullptr;
   RT_REQUIRE(!split_out || (so_c == 1 && (so_a % 4) == 0 && (so_b % 4) == 0 && aligned(out, 16)), kEINVAL,
              "split output needs 16-byte aligned row-major rows");
   RT_REQUIRE(split_out != 2 || ((so_a % 8) == 0 && (so_b % 8) == 0), kEINVAL, "fp16 split rows need 16-byte pitch");
@@ -1322,7 +1392,10 @@ bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q
   const int64_t grid = std::min<int64_t>(p.ntiles, ctx.num_sms);
 #define RT_T_CASE(NP)                                                     \
   case NP:                                                                \
-    if (bsplit) {                                                        \
+    if (h16) {                                                           \
+      if (akm) launch_t<NP, true, true, true>(ctx, tx, tb, to, p, dim3(unsigned(grid)));  \
+      else launch_t<NP, false, true, true>(ctx, tx, tb, to, p, dim3(unsigned(grid)));     \
+    } else if (bsplit) {                                                 \
       if (akm) launch_t<NP, true, true>(ctx, tx, tb, to, p, dim3(unsigned(grid)));  \
       else launch_t<NP, false, true>(ctx, tx, tb, to, p, dim3(unsigned(grid)));     \
     } else {                                                             \

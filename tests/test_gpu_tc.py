@@ -195,6 +195,31 @@ def test_tc_hosvd_parity(P, htc, name, dims, core, ranks):
     assert abs(e - ref["E"]) / ref["E"] <= 1e-5
 
 
+@pytest.mark.parametrize("scale", [3e-12, 1.0, 1e12])
+def test_tc_hosvd_h16_scales(P, htc, scale):
+    """HOSVD with q = 1 on the fp16-split kernels (power products Z = X^T Q_y, Y = X Q_z and the
+    first core stage; X's scale gathered in the first sketch pass: the 'xscale' launch) at data
+    scales far outside the fp16 range: parity with the oracle on the same scaled tensor."""
+    cfg = synth.CONFIGS["cfg2"].scaled((200, 180, 160), (20, 20, 20), (20, 20, 20))
+    x = np.asfortranarray((synth.make_tensor(cfg).astype(np.float64) * scale).astype(np.float32))
+    oms = [synth.gaussian_omega(cfg, n) for n in range(3)]
+    ref = oracle.hosvd(x, cfg.ranks, oms, q=1)
+    htc.set_option(1, 1)
+    res = P.rtucker_hosvd(htc, dev(x), cfg.ranks, cfg.p, 1, [om_dev(o) for o in oms])
+    htc.sync()
+    htc.set_option(1, 0)
+    names = {n for n, _, _ in htc.profile_read()[0]}
+    assert "xscale" in names and "absmax" not in names, names      # scale from the first pass, no extra pass
+    qg = [mat(q) for q in res["Q"]]
+    gg = P.core_to_numpy(res["G"])
+    for n in range(3):
+        assert M.subspace(qg[n], ref["Q"][n]) <= 1e-5, (n, M.subspace(qg[n], ref["Q"][n]))
+    assert M.core_in_oracle_basis(gg, qg, ref["G"], ref["Q"]) <= 1e-5
+    assert M.recon(gg, qg, ref["G"], ref["Q"]) <= 1e-5
+    e = mat(res["err"])[0]
+    assert abs(e - ref["E"]) / ref["E"] <= 1e-5
+
+
 def test_tc_sthosvd_shrink(P, htc):
     cfg = dataclasses.replace(synth.CONFIGS["cfg2"].scaled((96, 80, 64), (8, 8, 8), (8, 8, 8)), q=0)
     x = synth.make_tensor(cfg)
