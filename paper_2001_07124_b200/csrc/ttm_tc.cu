@@ -33,7 +33,7 @@ using namespace tc;
 
 constexpr int KC = 32;           // contraction elements per stage
 constexpr int BM = 128;          // tile rows = TMEM lanes
-constexpr int NTHREADS = 192;    // residual kernel
+constexpr int NTHREADS = 224;    // residual kernel: TMA, 2 MMA issuers, 4 split/epilogue warps
 constexpr int NT_TTM = 384;      // TTM kernels: X producer, MMA issuer, 4 splitters, B producer, 2nd issuer,
                                  // 4 epilogue warps (warp w accesses TMEM lanes 32 (w % 4) ..)
 
@@ -1367,7 +1367,7 @@ bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q
   p.nic = int(cdiv(box.I, KC));
   p.seg = std::max(1, ctx.tc_seg);
   p.out = out; p.so_a = so_a; p.so_c = so_c; p.so_b = so_b;
-  p.vec4 = so_c == 1 && (so_a % 4) == 0 && (so_b % 4) == 0 && (C % 4) == 0 && aligned(out, 16);
+  p.vec4 = so_c == 1 && (akm || (so_a % 4) == 0) && (so_b % 4) == 0 && (C % 4) == 0 && aligned(out, 16);   // a == 1: so_a unused
   p.split_out = split_out;
   p.xscale = h16 ? xscale : nullptr;
   RT_REQUIRE(!split_out || (so_c == 1 && (so_a % 4) == 0 && (so_b % 4) == 0 && aligned(out, 16)), kEINVAL,
@@ -1464,18 +1464,22 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constan
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2 * RNS + 8);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t my_tiles = (p.ntiles > blockIdx.x) ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  // TMEM: accumulator buffers at 0 / 2 RNB, each [hi.hi | hi.lo + lo.hi] (2 RNB columns: the B
-  // operand of the wide MMA is the concatenated [Q_hi | Q_lo] chunk); A hi at kA, A lo at kA + RP
+  // TMEM: accumulator buffers at 0 / 2 RNB, each [hi.hi | hi.lo] (2 RNB columns: the B operand of
+  // the wide MMA is the concatenated [Q_hi | Q_lo] chunk), issued by warp 1; the lo.hi products in
+  // their own buffers at kAcc1 + RNB ab, issued by warp 6 (MMAs from two warps overlap, one warp's
+  // complete one after another); A hi at kA, A lo at kA + RP
   constexpr uint32_t kAcc = 2 * RNB;
-  constexpr uint32_t kA = 2 * kAcc;
+  constexpr uint32_t kAcc1 = 2 * kAcc;
+  constexpr uint32_t kA = kAcc1 + 2 * RNB;
+  static_assert(kA + 2 * RP <= 512, "residual TMEM plan");
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < RNS; ++s) { mbar_init(&st_full[s], 1); mbar_init(&st_free[s], 128); }
     mbar_init(p_full, 1);
     mbar_init(p_free, 128);
     mbar_init(a_ready, 128);
-    mbar_init(a_free, 1);
-    for (int b = 0; b < 2; ++b) { mbar_init(&acc_full[b], 1); mbar_init(&acc_empty[b], 128); }
+    mbar_init(a_free, 2);
+    for (int b = 0; b < 2; ++b) { mbar_init(&acc_full[b], 2); mbar_init(&acc_empty[b], 128); }
     fence_barrier_init();
     tma_prefetch(&tmx); tma_prefetch(&tmp); tma_prefetch(&tqh); tma_prefetch(&tql);
   }
@@ -1507,9 +1511,10 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constan
         }
       }
     }
-  } else if (warp == 1) {                             // ---------------- MMA issuer (whole warp)
+  } else if (warp == 1 || warp == 6) {                // ---------------- MMA issuers (whole warps)
+    const bool wide = warp == 1;
     const uint32_t idesc_w = idesc_tf32(BM, 2 * RNB, 0);   // A_hi [Q_hi | Q_lo]
-    const uint32_t idesc_n = idesc_tf32(BM, RNB, 0);       // A_lo Q_hi -> correction columns
+    const uint32_t idesc_n = idesc_tf32(BM, RNB, 0);       // A_lo Q_hi
     Ring rg;
     int64_t g = 0;
     for (int64_t u = 0; u < my_tiles; ++u) {
@@ -1521,22 +1526,21 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constan
         mbar_wait(&st_full[rg.s], rg.ph);
         tc_fence_after();
         const uint32_t st = smem_u32(smem + L::off_st + rg.s * L::per_stage);
-        const uint32_t acc = tmem + uint32_t(ab) * kAcc;
+        const uint32_t acc = tmem + (wide ? uint32_t(ab) * kAcc : kAcc1 + uint32_t(ab) * RNB);
 #pragma unroll
         for (int c = 0; c < NCH; ++c)
 #pragma unroll
           for (int kk = 0; kk < KC / 8; ++kk) {
             const uint32_t a_hi = tmem + kA + c * KC + 8 * kk;
-            const uint32_t a_lo = a_hi + RP;
             const uint64_t bq = bdesc_sw128(st + (2 * c) * L::kQ, kk);
-            mma_tf32_ts_w(acc, a_hi, bq, idesc_w, (c == 0 && kk == 0) ? 0u : 1u);
-            mma_tf32_ts_w(acc + RNB, a_lo, bq, idesc_n, 1u);
+            if (wide) mma_tf32_ts_w(acc, a_hi, bq, idesc_w, (c == 0 && kk == 0) ? 0u : 1u);
+            else mma_tf32_ts_w(acc, a_hi + RP, bq, idesc_n, (c == 0 && kk == 0) ? 0u : 1u);
           }
         mma_commit_w(&acc_full[ab]);
       }
       mma_commit_w(a_free);
     }
-  } else {                                             // ---------------- split A / epilogue
+  } else if (warp >= 2 && warp <= 5) {                 // ---------------- split A / epilogue
     const int q4 = warp & 3;
     const int r = 32 * q4 + lane;
     const uint32_t lane_base = tmem + (uint32_t(32 * q4) << 16);
@@ -1571,14 +1575,15 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constan
         float tr = 0.f, tx = 0.f;
 #pragma unroll
         for (int cb = 0; cb < RNB / 16; ++cb) {
-          uint32_t v[16], w[16];
+          uint32_t v[16], w[16], z[16];
           tmem_ld16(lane_base + uint32_t(ab) * kAcc + 16 * cb, v);           // A_hi Q_hi
-          tmem_ld16(lane_base + uint32_t(ab) * kAcc + RNB + 16 * cb, w);     // A_hi Q_lo + A_lo Q_hi
+          tmem_ld16(lane_base + uint32_t(ab) * kAcc + RNB + 16 * cb, w);     // A_hi Q_lo
+          tmem_ld16(lane_base + kAcc1 + uint32_t(ab) * RNB + 16 * cb, z);    // A_lo Q_hi
           tmem_wait_ld();
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
             const float x = xt[(16 * cb + q) * BM + r];
-            const float d = x - (__uint_as_float(v[q]) + __uint_as_float(w[q]));
+            const float d = x - (__uint_as_float(v[q]) + (__uint_as_float(w[q]) + __uint_as_float(z[q])));
             tr = fmaf(d, d, tr);
             tx = fmaf(x, x, tx);
           }
