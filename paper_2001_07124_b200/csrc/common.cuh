@@ -75,6 +75,7 @@ struct Ctx {
   mutable const char* label = nullptr;   // profiler name override for the next TC launches
   int tc_presplit_z = 0;        // power iteration: write Z R^-1 pre-split [hi | lo] (ablation 200 toggles)
   int tc_h16 = 1;               // power product on the fp16-split kernel (ttm_s_h16; ablation 210/211 toggles)
+  int hooi_tc = 1;              // RP-HOOI: X pass of the S chain on the tensor cores (ablation 220/221 toggles)
 };
 
 // Launch a kernel (given as a lambda issuing <<<...>>> on ctx.stream) with optional

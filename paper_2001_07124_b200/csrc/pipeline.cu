@@ -772,7 +772,25 @@ void Engine::multi_ttm_skip(const TView& X, const T* data, const double* const* 
     const int p = ps[i];
     const Box b = TView::box_of(cur, N, p);
     double* dst = (i == np_ - 1) ? out : ws.alloc_n<double>(b.a * C[p] * b.b);
-    if (i == 0)
+    bool done = false;
+    if constexpr (std::is_same<T, float>::value) {
+      // the X pass on the tensor cores (fp32-accurate products, fp32 out), the rest of the chain in fp64
+      if (i == 0 && ctx.hooi_tc && ctx.ttm_impl != 1 && C[p] <= 128) {
+        const auto mq = ws.mark();
+        int64_t ldt;
+        const float* qt = working_copy<float>(ctx, ws, Q[p], cur[p], C[p], ldq[p], ldt);
+        float* d32 = ws.alloc_n<float>(b.a * C[p] * b.b);
+        const float* xsc = (ctx.tc_h16 && xs_slot) ? x_scale(data, X.size()) : nullptr;
+        LabelScope ls(ctx, "hooi_first");
+        if (ttm_t_tc(ctx, ws, data, b, qt, ldt, int(C[p]), d32, 1, b.a, b.a * C[p], 0, false, xsc)) {
+          convert2d<float, double>(ctx, d32, b.a * C[p] * b.b, 1, b.a * C[p] * b.b, dst, b.a * C[p] * b.b);
+          done = true;
+        }
+        ws.rewind(mq);
+      }
+    }
+    if (done) {
+    } else if (i == 0)
       ttm_t<T, double, double>(ctx, data, b, Q[p], 1, ldq[p], int(C[p]), dst, 1, b.a, b.a * C[p]);
     else
       ttm_t<double, double, double>(ctx, src, b, Q[p], 1, ldq[p], int(C[p]), dst, 1, b.a, b.a * C[p]);
@@ -794,6 +812,8 @@ void Engine::rp_hooi(const TView& X, const int64_t* R, int sweeps, const double*
   const int N = X.N;
   const T* data = static_cast<const T*>(X.data);
   const auto mk = ws.mark();
+  xs_slot = ws.alloc_n<float>(1);      // X's fp16 scale (one max|X| pass), shared by all S chains and the core
+  xs_key = nullptr;
   int64_t ldq[5];
   for (int n = 0; n < N; ++n) {
     ldq[n] = X.d[n];
@@ -826,6 +846,7 @@ void Engine::rp_hooi(const TView& X, const int64_t* R, int sweeps, const double*
   core<T>(X, data, Q_out, ldq, R, G_out);                                                // line 7
   if (E || Eg) rel_error<T>(X, data, G_out, R, Q_out, E, Eg);
   ws.rewind(mk);
+  xs_slot = nullptr;
 }
 
 template void Engine::rp_hooi<float>(const TView&, const int64_t*, int, const double* const*, const double* const*,

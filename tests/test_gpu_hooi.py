@@ -1,7 +1,10 @@
 """GPU parity of RP-HOOI (Alg.7) through the C-ABI
 (`rtucker_rp_hooi`) against the fp64 oracle `oracle.rp_hooi` on the same seeded inputs (the same
 starting factors, the oracle's RP-HOSVD output, and the same per-sweep Omega^(n)).  Metrics and
-tolerances as for the HOSVD path (M2, M4-M6 <= 1e-5; orthonormality <= 1e-12)."""
+tolerances as for the HOSVD path (M2, M4, M5 <= 1e-5; orthonormality <= 1e-12).  E: the default
+path streams X on the tensor cores (fp32-accurate), so E is held to DESIGN.md reading R30,
+|E_gpu - E_o| <= max(1e-5 E_o, 4u) with u = 2^-24; the fp64 X pass (RT_OPT_TC_ABLATE 220, reading
+R25) is held to the plain relative 1e-5 bar on the same cases."""
 import dataclasses
 import threading
 
@@ -32,6 +35,22 @@ def h(P):
     hh.close()
 
 
+@pytest.fixture(scope="module")
+def h64(P):
+    hh = P.Handle()
+    hh.set_option(100, 220)                 # RT_OPT_TC_ABLATE 220: fp64 X pass of the S chains (R25)
+    yield hh
+    hh.close()
+
+
+U32 = 2.0 ** -24
+
+
+def _e_ok(e, e_ref, strict):
+    """R30 (tensor-core X pass): max(1e-5 E, 4u) absolute floor; R25 (fp64 X pass): relative 1e-5."""
+    return abs(e - e_ref) <= (1e-5 * e_ref if strict else max(1e-5 * e_ref, 4 * U32))
+
+
 def _dev(x):
     return torch.from_numpy(synth.to_device_layout(x)).cuda()
 
@@ -45,7 +64,7 @@ def _start(cfg, x):
     return oracle.hosvd(x, cfg.ranks, oms, q=0)["Q"]
 
 
-def _check(P, res, ref, tol=1e-5):
+def _check(P, res, ref, tol=1e-5, strict=False):
     qg = [q.cpu().numpy() for q in res["Q"]]
     gg = P.core_to_numpy(res["G"])
     for n, q in enumerate(qg):
@@ -54,7 +73,7 @@ def _check(P, res, ref, tol=1e-5):
     assert M.core_in_oracle_basis(gg, qg, ref["G"], ref["Q"]) <= tol
     assert M.recon(gg, qg, ref["G"], ref["Q"]) <= tol
     e = float(res["err"][0])
-    assert abs(e - ref["E"]) / ref["E"] <= tol, (e, ref["E"])
+    assert _e_ok(e, ref["E"], strict), (e, ref["E"], abs(e - ref["E"]) / ref["E"])
 
 
 CASES = {
@@ -67,16 +86,18 @@ CASES = {
 }
 
 
+@pytest.mark.parametrize("strict", [False, True])
 @pytest.mark.parametrize("name", list(CASES))
-def test_rp_hooi_parity(P, h, name):
+def test_rp_hooi_parity(P, h, h64, name, strict):
     cfg, sweeps = CASES[name]
     x = synth.make_tensor(cfg)
     q0 = _start(cfg, x)
     oms = synth.hooi_omegas(cfg, sweeps)
     ref = oracle.rp_hooi(x, cfg.ranks, q0, oms)
-    res = P.rtucker_rp_hooi(h, _dev(x), cfg.ranks, [_t(q) for q in q0], [[_t(o) for o in s] for s in oms])
-    h.sync()
-    _check(P, res, ref)
+    hh = h64 if strict else h
+    res = P.rtucker_rp_hooi(hh, _dev(x), cfg.ranks, [_t(q) for q in q0], [[_t(o) for o in s] for s in oms])
+    hh.sync()
+    _check(P, res, ref, strict=strict)
 
 
 def test_rp_hooi_zero_sweeps_is_core_of_start(P, h):
@@ -127,8 +148,9 @@ def test_rp_hooi_invalid_arguments(P, h):
     h.sync()
 
 
+@pytest.mark.parametrize("strict", [False, True])
 @pytest.mark.parametrize("nranks", [2, 3])
-def test_rp_hooi_loopback_multirank(P, nranks):
+def test_rp_hooi_loopback_multirank(P, nranks, strict):
     """Slab-parallel RP-HOOI on one GPU (loopback communicator): S for n < N-1 contracts the
     distributed last mode (allreduced partial sums); Q^(N-1) is row-distributed (TSQR gather)."""
     cfg = synth.CONFIGS["cfg5"].scaled((48, 40, 36), (6, 6, 6), (6, 6, 6))
@@ -147,6 +169,8 @@ def test_rp_hooi_loopback_multirank(P, nranks):
             s = torch.cuda.Stream()
             with torch.cuda.stream(s):
                 hh = P.Handle(stream=s, loopback_group=grp, rank=r)
+                if strict:
+                    hh.set_option(100, 220)
                 lo, hi = int(cuts[r]), int(cuts[r + 1])
                 xs = _dev(np.asfortranarray(x[:, :, lo:hi]))
                 ql = [_t(q0[0]), _t(q0[1]), _t(q0[2][lo:hi])]
@@ -171,4 +195,4 @@ def test_rp_hooi_loopback_multirank(P, nranks):
         assert M.orth(qg[n]) <= 1e-12
         assert M.subspace(qg[n], ref["Q"][n]) <= 1e-5
     assert M.recon(out[0]["G"], qg, ref["G"], ref["Q"]) <= 1e-5
-    assert abs(out[0]["err"][0] - ref["E"]) / ref["E"] <= 1e-5
+    assert _e_ok(out[0]["err"][0], ref["E"], strict), (out[0]["err"][0], ref["E"])

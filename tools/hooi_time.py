@@ -10,9 +10,12 @@ from paper_2001_07124_b200 import api
 ap = argparse.ArgumentParser()
 ap.add_argument("--cfg", default="cfg5")
 ap.add_argument("--sweeps", type=int, default=1)
+ap.add_argument("--ablate", type=int, default=0, help="RT_OPT_TC_ABLATE switch (220/221: S-chain X pass on TC off/on)")
 a = ap.parse_args()
 cfg = synth.CONFIGS[a.cfg]
 h = api.Handle()
+if a.ablate:
+    h.set_option(100, a.ablate)
 X = synth.make_tensor_device(cfg, "cuda")
 if isinstance(X, tuple):
     X = X[0]
