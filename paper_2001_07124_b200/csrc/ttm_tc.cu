@@ -930,23 +930,47 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
         uint8_t* stage = smem + L::off_o;
         if (u > 0 && r == 0) bulk_wait_read0();              // the previous tile's stores have read it
         named_bar(1, 128);
+        if (p.split_out == 2) {
+          // fp16 [2^14 hi | 2^14 lo] rows (2 NPAD halves = the same bytes as NPAD floats): half e of
+          // the row in box e / 64, 16-byte chunk (e % 64) / 8
 #pragma unroll
-        for (int bx = 0; bx < NBX; ++bx)
+          for (int k = 0; k < NPAD / 8; ++k) {
+            uint32_t h[4], l[4];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int c = 32 * bx + 4 * q;
-            const float4 v = make_float4(c < NPAD ? sums[c % NPAD] : 0.f, c + 1 < NPAD ? sums[(c + 1) % NPAD] : 0.f,
-                                         c + 2 < NPAD ? sums[(c + 2) % NPAD] : 0.f,
-                                         c + 3 < NPAD ? sums[(c + 3) % NPAD] : 0.f);
-            *reinterpret_cast<float4*>(stage + bx * (BM * 128) + r * 128 + ((q ^ (r & 7)) << 4)) = v;
+            for (int e = 0; e < 4; ++e) {
+              const int c0 = 8 * k + 2 * e, c1 = c0 + 1;
+              split_h16x2(c0 < p.C ? sums[c0] * kQScale : 0.f, c1 < p.C ? sums[c1] * kQScale : 0.f, h[e], l[e]);
+            }
+            const int eh = 8 * k, el = NPAD + 8 * k;
+            *reinterpret_cast<uint4*>(stage + (eh >> 6) * (BM * 128) + r * 128 + ((((eh & 63) >> 3) ^ (r & 7)) << 4)) =
+                make_uint4(h[0], h[1], h[2], h[3]);
+            *reinterpret_cast<uint4*>(stage + (el >> 6) * (BM * 128) + r * 128 + ((((el & 63) >> 3) ^ (r & 7)) << 4)) =
+                make_uint4(l[0], l[1], l[2], l[3]);
           }
+        } else {
+#pragma unroll
+          for (int bx = 0; bx < NBX; ++bx)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const int c = 32 * bx + 4 * q;
+              const float4 v = make_float4(c < NPAD ? sums[c % NPAD] : 0.f, c + 1 < NPAD ? sums[(c + 1) % NPAD] : 0.f,
+                                           c + 2 < NPAD ? sums[(c + 2) % NPAD] : 0.f,
+                                           c + 3 < NPAD ? sums[(c + 3) % NPAD] : 0.f);
+              *reinterpret_cast<float4*>(stage + bx * (BM * 128) + r * 128 + ((q ^ (r & 7)) << 4)) = v;
+            }
+        }
         fence_proxy_async();
         named_bar(1, 128);
         if (r == 0) {
           const int row0 = AKM ? int(beta) : int(a0 + p.a * beta);
 #pragma unroll
-          for (int bx = 0; bx < NBX; ++bx)
-            if (32 * bx < p.C) tma_store_2d(&tmo, stage + bx * (BM * 128), 32 * bx, row0);
+          for (int bx = 0; bx < NBX; ++bx) {
+            if (p.split_out == 2) {
+              if (64 * bx < 2 * NPAD) tma_store_2d(&tmo, stage + bx * (BM * 128), 64 * bx, row0);
+            } else if (32 * bx < p.C) {
+              tma_store_2d(&tmo, stage + bx * (BM * 128), 32 * bx, row0);
+            }
+          }
           bulk_commit();
         }
       } else if (valid) {
@@ -1388,6 +1412,11 @@ bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q
       const uint32_t bx[2] = {32, uint32_t(BM)};
       p.tma_out = make_map(&to, out, 2, d, st, bx, true);
     }
+  } else if (split_out == 2 && akm && box.b <= INT32_MAX && !getenv("RT_TC_NO_TMA_OUT")) {
+    // fp16 [hi | lo] rows of 2 npad halves, pitch so_b halves: (64, 128) SWIZZLE_128B boxes
+    const uint64_t d[2] = {uint64_t(2 * npad), uint64_t(box.b)}, st[1] = {uint64_t(so_b) * 2};
+    const uint32_t bx[2] = {64, uint32_t(BM)};
+    p.tma_out = make_map(&to, out, 2, d, st, bx, true, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
   }
   const int64_t grid = std::min<int64_t>(p.ntiles, ctx.num_sms);
 #define RT_T_CASE(NP)                                                     \
