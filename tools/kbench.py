@@ -24,11 +24,18 @@ ap.add_argument("--seg", type=int, default=0)
 ap.add_argument("--tf32", type=int, default=0)
 ap.add_argument("--ablate", type=int, default=0)
 ap.add_argument("--skew", type=int, default=-1)
+ap.add_argument("--synth", default="", help="take X from gen.synth.make_tensor_device(CONFIGS[name]) instead of randn")
 a = ap.parse_args()
 
 dims = a.dims
 N = len(dims)
-X = torch.randn(tuple(reversed(dims)), device="cuda", dtype=torch.float32)
+if a.synth:
+    from gen import synth
+    X = synth.make_tensor_device(synth.CONFIGS[a.synth], "cuda")[0]
+    dims = synth.CONFIGS[a.synth].dims
+    N = len(dims)
+else:
+    X = torch.randn(tuple(reversed(dims)), device="cuda", dtype=torch.float32)
 xbytes = X.numel() * 4
 h = P.Handle()
 h.set_option(L.RT_OPT_TTM_IMPL, a.impl)
