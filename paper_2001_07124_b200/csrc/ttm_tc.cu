@@ -1457,7 +1457,7 @@ namespace {
 using namespace tc;
 
 constexpr int RNB = 64;                      // i columns per block (MMA N)
-constexpr int RNS = 2;                       // block pipeline depth
+constexpr int RNS = 3;                       // block pipeline depth (3 x 64 KB + the 32 KB P tile)
 
 template <int RP>
 struct RSmem {
