@@ -55,7 +55,7 @@ class Engine {
   // orthonormalize the tall Z of the power iteration in place (shifted CholeskyQR, fp64 Gram)
   template <typename T>
   bool qr_z(T* Z, int64_t m, int64_t ldz, int64_t m_glob, int k, bool rows_dist, int64_t row0, T* Z2 = nullptr,
-            int64_t ldz2 = 0, int split = 1);
+            int64_t ldz2 = 0, int split = 1, const float* xsc = nullptr);
   // (3) core G~ = X x_n Qt_n^T (all n) -> fp64 Gt (replicated)
   template <typename T>
   void core(const TView& X, const T* data, const double* const* Qt, const int64_t* ldq, const int64_t* K,

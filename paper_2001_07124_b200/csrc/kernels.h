@@ -47,13 +47,17 @@ void count_sketch(const Ctx& ctx, Arena& ws, const T* X, Box box, const int32_t*
 // halves (a multiple of 8), |B| <= 1; X is scaled by *xscale before its fp16 split.
 bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Bm, int64_t ldb, bool b_tf32_exact,
               int K, double* Y, int64_t ldy, bool b_presplit = false, const float* xscale = nullptr,
-              unsigned int* amax = nullptr);
-// amax (tf32 kernels): also atomicMax max|X| of the tiles read into *amax (float bits; caller zeroes)
+              unsigned int* amax = nullptr, const float* Bfb = nullptr, int64_t ldbfb = 0);
+// Bfb (required with xscale): the fp32 B (row-major, ldbfb) of the tf32 twin launch that runs
+// instead when *xscale == 0 (X's dynamic range too wide for one fp16 scale, R29)
+// amax (tf32 kernels): X statistics of the tiles read: amax[0] = max|X| (float bits, atomicMax),
+// ((double*)amax)[1] = sum |x| (16 bytes, caller zeroes)
 // *s = 2^(15 - e) with 2^(e-1) <= max|X| < 2^e over the n elements of X (1 if max|X| is 0 or not
 // finite): max |s X| in [2^14, 2^15), inside the fp16 range with 11 significant bits kept
 void x_scale_h16(const Ctx& ctx, Arena& ws, const float* X, int64_t n, float* s);
-// the same scale from a max|X| already gathered (ttm_s_tc amax)
-void x_scale_from_amax(const Ctx& ctx, const unsigned int* amax, float* s);
+// the same scale from statistics already gathered (ttm_s_tc amax) over the n elements of X;
+// s = 0 when max|X| > 2^16 mean|X| (the fp16 kernels then stand down for their tf32 twins)
+void x_scale_from_amax(const Ctx& ctx, const unsigned int* amax, int64_t n, float* s);
 // whether ttm_s_tc would run (same shape/alignment rules, no launch)
 bool ttm_s_tc_ok(const Ctx& ctx, const float* X, Box box, int K);
 int tc_npad(int K);
@@ -64,7 +68,9 @@ int tc_split_width(int K);
 // [hi (tc_npad(C)) | lo (tc_npad(C))] rows, out then points to halves and so_a / so_b count halves.
 bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
               int64_t so_a, int64_t so_c, int64_t so_b, int split_out = 0, bool q_tf32_exact = false,
-              const float* xscale = nullptr);
+              const float* xscale = nullptr, const float* run_if_zero = nullptr);
+// run_if_zero (tf32 form only): the launch does its work only if *run_if_zero == 0 (device-side
+// gate: the fallback of an fp16-split step whose X scale came out 0, R29)
 // xscale (device scale of X from x_scale_h16 / x_scale_from_amax, |Q| <= 1 required): the fp16
 // split form (ttm_t_tc_kernel<H16>) instead of 3xTF32; ignored with q_tf32_exact
 

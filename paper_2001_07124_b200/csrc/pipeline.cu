@@ -140,7 +140,7 @@ const float* Engine::x_scale(const float* data, int64_t n) {
 // (m x k, row pitch ldz).  split: form of the Z2 copy (1 tf32 [hi | lo], 2 fp16 [hi | lo]).
 template <typename T>
 bool Engine::qr_z(T* Z, int64_t m, int64_t ldz, int64_t m_glob, int k, bool rows_dist, int64_t row0, T* Z2,
-                  int64_t ldz2, int split) {
+                  int64_t ldz2, int split, const float* xsc) {
   const auto mk = ws.mark();
   double* G = ws.alloc_n<double>(int64_t(k) * k);
   double* Rr = ws.alloc_n<double>(int64_t(k) * k);
@@ -173,6 +173,11 @@ bool Engine::qr_z(T* Z, int64_t m, int64_t ldz, int64_t m_glob, int k, bool rows
       LabelScope ls(ctx, "zapply_tc");
       // Z2 requested: Z R^{-1} written as the pre-split [hi | lo] operand of the next product
       if (Z2) done_apply = ttm_t_tc(ctx, ws, Z, zb, RiT, ldr, k, Z2, 0, 1, ldz2, /*split_out=*/split);
+      // fp16 Z2 with a device-side fallback (X scale 0, R29): the tf32 twin of the power product
+      // reads the fp32 Z R^-1, applied in place by a launch gated on the same scale
+      if (Z2 && split == 2 && xsc)
+        RT_REQUIRE(ttm_t_tc(ctx, ws, Z, zb, RiT, ldr, k, Z, 0, 1, ldz, 0, false, nullptr, xsc), kEINVAL,
+                   "qr_z: gated in-place apply not launched");
       else done_apply = ttm_t_tc(ctx, ws, Z, zb, RiT, ldr, k, Z, 0, 1, ldz);
     }
   }
@@ -202,8 +207,8 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
     int64_t ld = omega_ld[n];
     unsigned int* am = nullptr;
     if (std::is_same<T, float>::value && q > 0 && ctx.tc_h16 && xs_key != data) {
-      am = ws.alloc_n<unsigned int>(1);
-      RT_CUDA(cudaMemsetAsync(am, 0, sizeof(unsigned int), ctx.stream));
+      am = ws.alloc_n<unsigned int>(4);                 // {max|X| bits, pad, sum |x| (f64)}
+      RT_CUDA(cudaMemsetAsync(am, 0, 16, ctx.stream));
     }
     const auto mo = ws.mark();
     if (std::is_same<T, float>::value && ctx.ttm_impl != 1 && (ld % 4) != 0) {
@@ -215,7 +220,7 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
       ld = ldp;
     }
     if (ttm_s_dispatch(ctx, ws, data, bx, om, ld, ctx.omega_tf32 != 0, K, Yt, In, am)) {
-      x_scale_from_amax(ctx, am, xs_slot);
+      x_scale_from_amax(ctx, am, X.size(), xs_slot);
       xs_key = data;
     }
     ws.rewind(mo);
@@ -344,12 +349,13 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
       for (int k = n + 1; k < N - 1; ++k) bp *= X.d[k];
       zrow0 = bx.a * bp * X.off;
     }
-    const bool pre = qr_z<T>(Z, Jl, ldz, X.Jg(n), K, !last && dist(), zrow0, Z2, ldz2, zsplit);
+    const bool pre = qr_z<T>(Z, Jl, ldz, X.Jg(n), K, !last && dist(), zrow0, Z2, ldz2, zsplit, xsc);
     {
       LabelScope ls(ctx, "ttm_s_tc_pow");
       bool done = false;
       if constexpr (std::is_same<T, float>::value) {
-        if (pre) done = ttm_s_tc(ctx, ws, data, bx, Z2, ldz2, false, K, Yt, In, /*b_presplit=*/true, xsc);
+        if (pre) done = ttm_s_tc(ctx, ws, data, bx, Z2, ldz2, false, K, Yt, In, /*b_presplit=*/true, xsc, nullptr,
+                                 xsc ? Z : nullptr, ldz);
       }
       RT_REQUIRE(!pre || done, kEUNSUPPORTED, "pre-split power product not launched");
       if (!done) ttm_s_dispatch(ctx, ws, data, bx, Z, ldz, false, K, Yt, In);
@@ -863,8 +869,10 @@ template void Engine::sketch<float>(const TView&, const float*, int, int, const 
                                     const int64_t*, int, double*);
 template void Engine::sketch<double>(const TView&, const double*, int, int, const void* const*, const int64_t*,
                                      const int64_t*, int, double*);
-template bool Engine::qr_z<float>(float*, int64_t, int64_t, int64_t, int, bool, int64_t, float*, int64_t, int);
-template bool Engine::qr_z<double>(double*, int64_t, int64_t, int64_t, int, bool, int64_t, double*, int64_t, int);
+template bool Engine::qr_z<float>(float*, int64_t, int64_t, int64_t, int, bool, int64_t, float*, int64_t, int,
+                                  const float*);
+template bool Engine::qr_z<double>(double*, int64_t, int64_t, int64_t, int, bool, int64_t, double*, int64_t, int,
+                                   const float*);
 template void Engine::qr_rows<float>(const float*, int64_t, int64_t, int, int64_t, double*, int64_t, double*,
                                      bool, int64_t);
 template void Engine::qr_rows<double>(const double*, int64_t, int64_t, int, int64_t, double*, int64_t, double*,

@@ -155,15 +155,17 @@ __device__ __forceinline__ uint64_t bdesc(uint32_t saddr, int kk) {
 // Splitter: read this thread's row of the raw X tile, write hi/lo tf32 to its TMEM lane.
 //   AMN  : tile [KC][BM] (row r is a column): element (r, k) at k*BM + r
 //   !AMN : tile [BM][KC] with 128B swizzle: 16B chunk c of row r at ((c ^ (r&7)) << 4)
-// AMAX: also fold max |x| of the row into m (the fp16 scale of X, taken during a tf32 pass)
+// AMAX: also fold max |x| and sum |x| of the row into m, sq (the fp16 scale of X, R29, taken
+// during a tf32 pass)
 template <bool AMN, bool AMAX = false>
-__device__ __forceinline__ void split_row_to_tmem(const float* xs, int r, uint32_t t_hi, float* m = nullptr) {
+__device__ __forceinline__ void split_row_to_tmem(const float* xs, int r, uint32_t t_hi, float* m = nullptr,
+                                                  float* sq = nullptr) {
   uint32_t hi[32], lo[32];
   if (AMN) {
 #pragma unroll
     for (int q = 0; q < 32; ++q) {
       const float v = xs[q * BM + r];
-      if (AMAX) *m = fmaxf(*m, fabsf(v));
+      if (AMAX) { *m = fmaxf(*m, fabsf(v)); *sq += fabsf(v); }
       split_tf32(v, hi[q], lo[q]);
     }
   } else {
@@ -171,7 +173,10 @@ __device__ __forceinline__ void split_row_to_tmem(const float* xs, int r, uint32
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const float4 v = *reinterpret_cast<const float4*>(row + ((c ^ (r & 7)) << 2));
-      if (AMAX) *m = fmaxf(fmaxf(*m, fmaxf(fabsf(v.x), fabsf(v.y))), fmaxf(fabsf(v.z), fabsf(v.w)));
+      if (AMAX) {
+        *m = fmaxf(fmaxf(*m, fmaxf(fabsf(v.x), fabsf(v.y))), fmaxf(fabsf(v.z), fabsf(v.w)));
+        *sq += (fabsf(v.x) + fabsf(v.y)) + (fabsf(v.z) + fabsf(v.w));
+      }
       split_tf32(v.x, hi[4 * c + 0], lo[4 * c + 0]);
       split_tf32(v.y, hi[4 * c + 1], lo[4 * c + 1]);
       split_tf32(v.z, hi[4 * c + 2], lo[4 * c + 2]);
@@ -281,6 +286,17 @@ __device__ __forceinline__ void drain_acc(const Bars& b, uint32_t lane_base, int
   mbar_arrive(&b.acc_empty[ab]);
 }
 
+__device__ __forceinline__ void xstat_add(unsigned int* stat, float m, float sq) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(stat, __float_as_uint(m));                // non-negative floats order as integers
+    atomicAdd(reinterpret_cast<double*>(stat + 2), double(sq));   // sum |x|
+  }
+}
 // ====================================================================== ttm_s
 struct SParams {
   int64_t a, I, b;
@@ -291,7 +307,8 @@ struct SParams {
   int ablate;         // profiling only: 1 = no MMA, 2 = no split work (results invalid)
   int skew;           // chunk-order rotation per M-tile (decorrelates the rows' DRAM addresses)
   float* part;        // [split][K][I]
-  unsigned int* amax; // optional: max |X| over the tiles read (as the bits of a non-negative float)
+  unsigned int* amax; // optional: X statistics of the tiles read (xstat_add: max |X| bits, sum |x|)
+  const float* gate;  // optional: run only if *gate == 0 (the tf32 fallback of an fp16-split launch)
   unsigned long long* tim;   // diagnostics (RT_OPT_TC_ABLATE = 1000): per-CTA role wait cycles, else null
   long long* trace;          // diagnostics (RT_OPT_TC_ABLATE = 2000): per-chunk event clocks of CTA (0,0)
 };
@@ -347,6 +364,7 @@ template <int NPAD, bool BSPLIT, bool AMN, bool BPRE>
 __global__ void __launch_bounds__(NT_TTM, 1)
 ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb, const SParams p) {
   static_assert(!BPRE || BSPLIT, "pre-split B implies the split product form");
+  if (p.gate && *p.gate != 0.f) return;                // fp16-split launch in charge (R29)
   using L = Plan<NPAD, BSPLIT, true, sketch_cps<NPAD, BSPLIT, true>()>;
   constexpr int NX = L::NX, CPS = L::CPS, NB = L::NB;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -443,7 +461,7 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
     const uint32_t lane_base = tmem + (uint32_t(32 * q4) << 16);
     const int t = threadIdx.x - 64;
     unsigned long long* tim = (warp == 2) ? p.tim : nullptr;   // warp-uniform (aligned tcgen05 ops inside)
-    float xmax = 0.f;
+    float xmax = 0.f, xsq = 0.f;
     Ring rx;
     for (int it = 0; it < nch; ++it, rx.next<NX>()) {
       const int g = it / CPS, c = it % CPS, sl = st_slot(g), bs = it % L::NBS;
@@ -453,7 +471,7 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
         const float* xs = reinterpret_cast<const float*>(smem + L::off_x + rx.s * L::kX);
         if (p.ablate == 2) {
         } else if (p.amax) {
-          split_row_to_tmem<AMN, true>(xs, r, lane_base + L::a_slot(sl) + 64u * c, &xmax);
+          split_row_to_tmem<AMN, true>(xs, r, lane_base + L::a_slot(sl) + 64u * c, &xmax, &xsq);
         } else {
           split_row_to_tmem<AMN>(xs, r, lane_base + L::a_slot(sl) + 64u * c);
         }
@@ -471,11 +489,7 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
         mbar_arrive(&b.ready[sl]);
       }
     }
-    if (p.amax) {
-#pragma unroll
-      for (int o = 16; o; o >>= 1) xmax = fmaxf(xmax, __shfl_xor_sync(0xffffffffu, xmax, o));
-      if (lane == 0) atomicMax(p.amax, __float_as_uint(xmax));
-    }
+    if (p.amax) xstat_add(p.amax, xmax, xsq);
   } else if (warp >= 8) {                              // ---------------- epilogue: drain segments
     const int q4 = warp & 3;
     const int r = 32 * q4 + lane;
@@ -584,6 +598,7 @@ __global__ void __launch_bounds__(NT_TTM, 1)
 ttm_s_h16_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb, const HParams hp) {
   using L = PlanH<NPAD, CPS_>;
   const SParams& p = hp.s;
+  if (*hp.xscale == 0.f) return;                       // dynamic range too wide: the tf32 launch runs
   constexpr int NX = L::NX, CPS = L::CPS, NB = L::NB;
   extern __shared__ __align__(1024) uint8_t smem[];
   const Bars b = bars_of<L>(smem);
@@ -721,27 +736,31 @@ ttm_s_h16_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant_
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
-// max |X| -> s = 2^(14 - e), e = floor(log2 max|X|) (s = 1 for max|X| = 0 or non-finite), so
-// that max |s X| lies in [2^14, 2^15) below the fp16 maximum
+// X statistics for the fp16 scale: stat = {max|X| as float bits (u32), pad, sum |x| (f64)}.
+// s = 2^(15 - e), 2^(e-1) <= max|X| < 2^e, so max |s X| lies in [2^14, 2^15) below the fp16 maximum;
+// s = 0 ("use the tf32 kernels") when max|X| > 2^16 mean|X|: the bulk of such a tensor (a few huge
+// outliers) would sit so far below the scale that its fp16 lo parts turn subnormal (R29).  mean|X|
+// (not the rms, which a few outliers dominate) tracks the bulk.
 __global__ void __launch_bounds__(256) absmax_kernel(const float4* __restrict__ x, int64_t n4, const float* __restrict__ tail,
-                                                     int ntail, unsigned int* __restrict__ amax) {
-  float m = 0.f;
+                                                     int ntail, unsigned int* __restrict__ stat) {
+  float m = 0.f, sq = 0.f;
   for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n4; e += int64_t(gridDim.x) * blockDim.x) {
     const float4 v = __ldcs(x + e);
     m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    sq += (fabsf(v.x) + fabsf(v.y)) + (fabsf(v.z) + fabsf(v.w));
   }
-  if (blockIdx.x == 0 && int(threadIdx.x) < ntail) m = fmaxf(m, fabsf(tail[threadIdx.x]));
-#pragma unroll
-  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(amax, __float_as_uint(m));   // non-negative floats order as integers
+  if (blockIdx.x == 0 && int(threadIdx.x) < ntail) { const float v = tail[threadIdx.x]; m = fmaxf(m, fabsf(v)); sq += fabsf(v); }
+  xstat_add(stat, m, sq);
 }
-__global__ void xscale_kernel(const unsigned int* __restrict__ amax, float* __restrict__ s) {
-  const float m = __uint_as_float(*amax);
+__global__ void xscale_kernel(const unsigned int* __restrict__ stat, double n, float* __restrict__ s) {
+  const float m = __uint_as_float(stat[0]);
+  const double mean_abs = *reinterpret_cast<const double*>(stat + 2) / n;
   float r = 1.f;
   if (m > 0.f && isfinite(m)) {
     int e;
     frexpf(m, &e);                                      // m = f 2^e, f in [0.5, 1): floor(log2 m) = e - 1
     r = ldexpf(1.f, min(15 - e, 127));
+    if (double(m) > 65536.0 * mean_abs) r = 0.f;       // too wide a dynamic range: tf32 kernels
   }
   *s = r;
 }
@@ -761,6 +780,7 @@ struct TParams {
                       // 2: as fp16 [hi (NPAD) | lo (NPAD)] (out points to halves, so_* count halves)
   bool tma_out;       // output tiles staged in shared memory and written by TMA stores (tmo)
   const float* xscale;   // H16 kernels: device scale s of X (the output is divided by s 2^14)
+  const float* gate;     // tf32 kernels: run only if *gate == 0 (fallback of an fp16-split launch)
 };
 
 // AKM: mode 0 (a == 1), X tile K-major [BM j][KC i].  BSPLIT: Q = Q_hi + Q_lo pre-split (an fp64
@@ -777,6 +797,7 @@ __global__ void __launch_bounds__(NT_TTM, 1)
 ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb,
                 const __grid_constant__ CUtensorMap tmo, const TParams p) {
   static_assert(!H16 || BSPLIT, "the fp16 form always carries Q_lo");
+  if (H16 ? (*p.xscale == 0.f) : (p.gate != nullptr && *p.gate != 0.f)) return;   // one of the pair runs (R29)
   using L = std::conditional_t<H16, PlanH<NPAD, 1, t_outb<NPAD>()>, Plan<NPAD, BSPLIT, false, 1, t_outb<NPAD>()>>;
   constexpr int NX = L::NX;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -1221,26 +1242,27 @@ bool ttm_s_tc_ok(const Ctx& ctx, const float* X, Box box, int K) {
   return !(box.a > INT32_MAX || box.I > INT32_MAX || box.b > INT32_MAX || J > INT32_MAX);
 }
 
-void x_scale_from_amax(const Ctx& ctx, const unsigned int* amax, float* s) {
-  launch(ctx, "xscale", [&] { xscale_kernel<<<1, 1, 0, ctx.stream>>>(amax, s); });
+void x_scale_from_amax(const Ctx& ctx, const unsigned int* amax, int64_t n, float* s) {
+  launch(ctx, "xscale", [&] { xscale_kernel<<<1, 1, 0, ctx.stream>>>(amax, double(n), s); });
 }
 
 void x_scale_h16(const Ctx& ctx, Arena& ws, const float* X, int64_t n, float* s) {
   RT_REQUIRE(aligned(X, 16), kEINVAL, "x_scale_h16: X must be 16-byte aligned");
-  unsigned int* amax = ws.alloc_n<unsigned int>(1);
-  RT_CUDA(cudaMemsetAsync(amax, 0, sizeof(unsigned int), ctx.stream));
+  unsigned int* stat = ws.alloc_n<unsigned int>(4);
+  RT_CUDA(cudaMemsetAsync(stat, 0, 16, ctx.stream));
   const int64_t n4 = n / 4;
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(cdiv(n4, 256), int64_t(ctx.num_sms) * 8));
   launch(ctx, "absmax", [&] {
     absmax_kernel<<<unsigned(blocks), 256, 0, ctx.stream>>>(reinterpret_cast<const float4*>(X), n4, X + 4 * n4,
-                                                            int(n - 4 * n4), amax);
+                                                            int(n - 4 * n4), stat);
   });
-  launch(ctx, "xscale", [&] { xscale_kernel<<<1, 1, 0, ctx.stream>>>(amax, s); });
+  x_scale_from_amax(ctx, stat, n, s);
 }
 
 // Returns false (nothing launched) when the shape/alignment is not supported by the TMA path.
 bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Bm, int64_t ldb, bool b_tf32_exact,
-              int K, double* Y, int64_t ldy, bool b_presplit, const float* xscale, unsigned int* amax) {
+              int K, double* Y, int64_t ldy, bool b_presplit, const float* xscale, unsigned int* amax,
+              const float* Bfb, int64_t ldbfb) {
   const int npad = tc_npad(K);
   if (npad < 0) return false;
   const int64_t J = box.J();
@@ -1270,6 +1292,11 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
   } else if (!make_b_map_rm(&tb, Bm, J, b_presplit ? 2 * nh : K, ldb)) {
     return false;
   }
+  // the fp16-split launch comes with its tf32 twin on the fp32 B (split in the kernel), gated on the
+  // device by s == 0 (R29): both write the same split-K partials, exactly one of them runs
+  CUtensorMap tbf;
+  RT_REQUIRE(!h16 || Bfb != nullptr, kEINVAL, "ttm_s_tc: the fp16 form needs the fp32 B of its tf32 twin");
+  if (h16 && !make_b_map_rm(&tbf, Bfb, J, K, ldbfb)) return false;
   SParams p;
   p.a = box.a; p.I = box.I; p.b = box.b; p.K = K;
   p.cpb = amn ? 1 : cdiv(box.a, KC);
@@ -1283,6 +1310,7 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
   p.skew = ctx.tc_skew >= 0 ? ctx.tc_skew : 0;
   p.part = ws.alloc_n<float>(splits * K * box.I);
   p.amax = h16 ? nullptr : amax;
+  p.gate = nullptr;
   p.tim = nullptr;
   p.trace = nullptr;
   const dim3 grid{unsigned(mtiles), unsigned(splits), 1u};
@@ -1301,6 +1329,9 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
       const HParams hp{p, xscale};                                                    \
       if (amn) launch_h<NP, true>(ctx, tx, tb, hp, grid);                             \
       else launch_h<NP, false>(ctx, tx, tb, hp, grid);                                \
+      SParams pf = p;                                                                 \
+      pf.gate = xscale;                                                               \
+      dispatch_s<NP>(ctx, amn, 1, tx, tbf, pf, grid);                                 \
     } else {                                                                          \
       dispatch_s<NP>(ctx, amn, bmode, tx, tb, p, grid);                               \
     }                                                                                 \
@@ -1348,7 +1379,8 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
 }
 
 bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
-              int64_t so_a, int64_t so_c, int64_t so_b, int split_out, bool q_tf32_exact, const float* xscale) {
+              int64_t so_a, int64_t so_c, int64_t so_b, int split_out, bool q_tf32_exact, const float* xscale,
+              const float* run_if_zero) {
   const int npad = tc_npad(C);
   if (npad < 0) return false;
   const bool h16 = xscale != nullptr && !q_tf32_exact;
@@ -1368,17 +1400,20 @@ bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q
     if (!make_map(&tx, X, 3, d, s, bx, false)) return false;
   }
   const bool bsplit = !q_tf32_exact || !aligned(Q, 16) || (ldq % 4) != 0;
+  CUtensorMap tbh;   // fp16 [2^14 Q_hi | 2^14 Q_lo] operand of the H16 kernel (with h16)
   if (h16) {
-    // fp16 [2^14 Q_hi | 2^14 Q_lo] rows (I x 2 npad halves): (64 cols, 32 rows) SWIZZLE_128B boxes
+    // fp16 rows (I x 2 npad halves): (64 cols, 32 rows) SWIZZLE_128B boxes
     uint32_t* Q2 = ws.alloc_n<uint32_t>(box.I * npad);
     const uint64_t d[2] = {uint64_t(2 * npad), uint64_t(box.I)}, st[1] = {uint64_t(npad) * 4};
     const uint32_t bx[2] = {64, KC};
-    if (!make_map(&tb, Q2, 2, d, st, bx, true, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_DATA_TYPE_FLOAT16)) return false;
+    if (!make_map(&tbh, Q2, 2, d, st, bx, true, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_DATA_TYPE_FLOAT16)) return false;
     launch(ctx, "split_q", [&] {
       split_q_h16_kernel<<<unsigned(cdiv(box.I * (npad / 2), 256)), 256, 0, ctx.stream>>>(Q, box.I, C, ldq, npad, Q2);
     });
-  } else if (bsplit) {
+  }
+  if (bsplit) {
     // pre-split [Q_hi | Q_lo] (I x 2 npad): the kernel loads it as one [2 npad][32] K-major slot
+    // (with h16 this is the operand of the tf32 twin that runs instead when s == 0, R29)
     const int64_t ld2 = (box.I + 3) & ~int64_t(3);
     float* Q2 = ws.alloc_n<float>(ld2 * 2 * npad);
     if (!make_b_map(&tb, Q2, box.I, 2 * npad, ld2, 2 * npad)) return false;
@@ -1399,6 +1434,7 @@ bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q
   p.vec4 = so_c == 1 && (akm || (so_a % 4) == 0) && (so_b % 4) == 0 && (C % 4) == 0 && aligned(out, 16);   // a == 1: so_a unused
   p.split_out = split_out;
   p.xscale = h16 ? xscale : nullptr;
+  p.gate = h16 ? nullptr : run_if_zero;
   RT_REQUIRE(!split_out || (so_c == 1 && (so_a % 4) == 0 && (so_b % 4) == 0 && aligned(out, 16)), kEINVAL,
              "split output needs 16-byte aligned row-major rows");
   RT_REQUIRE(split_out != 2 || ((so_a % 8) == 0 && (so_b % 8) == 0), kEINVAL, "fp16 split rows need 16-byte pitch");
@@ -1427,8 +1463,15 @@ bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q
 #define RT_T_CASE(NP)                                                     \
   case NP:                                                                \
     if (h16) {                                                           \
-      if (akm) launch_t<NP, true, true, true>(ctx, tx, tb, to, p, dim3(unsigned(grid)));  \
-      else launch_t<NP, false, true, true>(ctx, tx, tb, to, p, dim3(unsigned(grid)));     \
+      TParams pf = p;                                                    \
+      pf.gate = xscale;                                                  \
+      if (akm) {                                                         \
+        launch_t<NP, true, true, true>(ctx, tx, tbh, to, p, dim3(unsigned(grid)));  \
+        launch_t<NP, true, true>(ctx, tx, tb, to, pf, dim3(unsigned(grid)));        \
+      } else {                                                           \
+        launch_t<NP, false, true, true>(ctx, tx, tbh, to, p, dim3(unsigned(grid))); \
+        launch_t<NP, false, true>(ctx, tx, tb, to, pf, dim3(unsigned(grid)));       \
+      }                                                                  \
     } else if (bsplit) {                                                 \
       if (akm) launch_t<NP, true, true>(ctx, tx, tb, to, p, dim3(unsigned(grid)));  \
       else launch_t<NP, false, true>(ctx, tx, tb, to, p, dim3(unsigned(grid)));     \
