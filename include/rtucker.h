@@ -105,11 +105,15 @@ rt_status rt_sync(rt_handle* h);
  * tensor-core products with them then skip the A_hi*Omega_lo product of the 3xTF32 split.  RT_OPT_TC_SEGMENT: contraction chunks (of 32) accumulated in TMEM before the fp32
  * accumulator is drained to registers (default 16, i.e. 512 elements; the tensor core's fp32
  * accumulation error grows with this length, tests/test_gpu_tc.py).  RT_OPT_TC_SKEW: tuning of
- * the split-K chunk order (rotation per row tile; default 0).  RT_OPT_QR_FALLBACK is reserved. */
+ * the split-K chunk order (rotation per row tile; default 0).  RT_OPT_QR_FALLBACK is reserved.
+ * RT_OPT_TC_ABLATE: profiling ablations (values 1, 2, 1000, 2000 give invalid results) and valid
+ * A/B switches of the product path: 210 / 211 = the fp16-split form of the X passes that multiply
+ * an orthonormal Q (power products, first core stage; R29) off / on (default on);
+ * 220 / 221 = RP-HOOI's X pass on the fp64 warp MMA / on the tensor cores (default, R30). */
 typedef enum { RT_OPT_TTM_IMPL = 0, RT_OPT_PROFILE = 1, RT_OPT_QR_FALLBACK = 2, RT_OPT_OMEGA_TF32 = 3,
                RT_OPT_TC_SEGMENT = 4, RT_OPT_TC_SKEW = 5,
                RT_OPT_FORCE_COLLECTIVES = 6 /* tests: run the slab exchanges even on a 1-rank communicator */,
-               RT_OPT_TC_ABLATE = 100 /* profiling only: invalid results */ } rt_option;
+               RT_OPT_TC_ABLATE = 100 /* profiling ablations and A/B switches, see above */ } rt_option;
 rt_status rt_set_option(rt_handle* h, rt_option opt, int64_t value);
 
 /* Profile of the launches recorded since the last read (synchronizes the stream).
