@@ -79,10 +79,12 @@ def work_model(cfg, nranks=1):
     r_flops = 2 * xl * cfg.ranks[-1]
     total_flops = s_flops + t_flops + r_flops
     # hardware tensor flops of the ttm_s class: the Omega sketch runs 2 tf32 products (tf32-exact
-    # Omega, reading R18), the power product Y = X Z 3 (3xTF32)
-    s_hw = sum(2 * xl * K[n] * (2 + 3 * cfg.q) for n in range(N))
+    # Omega, reading R18); the power product Y = X Q_z runs 3 fp16 products (fp16 split, R29)
+    s_hw_tf32 = sum(2 * xl * K[n] * 2 for n in range(N))
+    s_hw_f16 = sum(2 * xl * K[n] * 3 * cfg.q for n in range(N))
     return {"ttm_s": (s_bytes, s_flops, s_n), "ttm_t": (t_bytes, t_flops, t_n), "residual": (r_bytes, r_flops, 1),
-            "total_flops": total_flops, "x_bytes_local": xl * esz, "ttm_s_hw_flops": s_hw}
+            "total_flops": total_flops, "x_bytes_local": xl * esz, "ttm_s_hw_tf32": s_hw_tf32,
+            "ttm_s_hw_f16": s_hw_f16}
 
 
 # --------------------------------------------------------------------- clocks
@@ -395,12 +397,15 @@ def main():
                 "share_of_step": per_step_ms / ms,
                 "tflops": f / (per_step_ms * 1e-3) / 1e12}
         if cls == "ttm_s":
-            # tensor pipe: hardware tf32 flops against the tf32 peak = measured bf16 peak x 1/2
-            # (nominal tf32:bf16 ratio, B200_PROFILING.md); the class is co-limited by both
-            tf32_peak = bf16 / 2.0
-            hw = wm["ttm_s_hw_flops"] / (per_step_ms * 1e-3) / 1e12
-            roof["tensor"] = {"hw_tflops": hw, "peak_tflops": tf32_peak, "frac": hw / tf32_peak,
-                              "peak_source": f"{peak_src} bf16 x 1/2"}
+            # tensor pipe: hardware flops of the class (tf32 Omega sketches + fp16-split power
+            # products) and the fraction of the class time the pipe needs at the measured peaks
+            # (fp16 = measured dense bf16; tf32 = bf16 x 1/2, the nominal ratio of B200_PROFILING.md)
+            tf32_peak, f16_peak = bf16 / 2.0, bf16
+            t_s = per_step_ms * 1e-3
+            busy = (wm["ttm_s_hw_tf32"] / (tf32_peak * 1e12) + wm["ttm_s_hw_f16"] / (f16_peak * 1e12)) / t_s
+            roof["tensor"] = {"hw_tflops": (wm["ttm_s_hw_tf32"] + wm["ttm_s_hw_f16"]) / t_s / 1e12, "frac": busy,
+                              "peak_tflops": {"tf32": tf32_peak, "f16": f16_peak},
+                              "peak_source": f"{peak_src} bf16 (f16), x 1/2 (tf32)"}
     line = {"metric": METRIC, "value": value * 1.0, "unit": UNIT, "n_gpus": r["world"], "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config,
