@@ -108,7 +108,8 @@ rt_status rt_sync(rt_handle* h);
  * the split-K chunk order (rotation per row tile; default 0).  RT_OPT_QR_FALLBACK is reserved.
  * RT_OPT_TC_ABLATE: profiling ablations (values 1, 2, 1000, 2000 give invalid results) and valid
  * A/B switches of the product path: 210 / 211 = the fp16-split form of the X passes that multiply
- * an orthonormal Q (power products, first core stage; R29) off / on (default on);
+ * an orthonormal Q (power products, first core stage; R29) off / on (default on), 212 =
+ * on with its device-side range gate forced closed (the tf32 twin launches do the work; tests);
  * 220 / 221 = RP-HOOI's X pass on the fp64 warp MMA / on the tensor cores (default, R30). */
 typedef enum { RT_OPT_TTM_IMPL = 0, RT_OPT_PROFILE = 1, RT_OPT_QR_FALLBACK = 2, RT_OPT_OMEGA_TF32 = 3,
                RT_OPT_TC_SEGMENT = 4, RT_OPT_TC_SKEW = 5,

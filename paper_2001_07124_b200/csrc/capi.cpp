@@ -223,7 +223,7 @@ rt_status rt_set_option(rt_handle* h, rt_option opt, int64_t value) {
     case RT_OPT_TC_SEGMENT: h->ctx.tc_seg = int(value > 0 ? value : 16); return RT_OK;
     case RT_OPT_TC_ABLATE:
       if (value == 200 || value == 201) { h->ctx.tc_presplit_z = int(value == 201); return RT_OK; }
-      if (value == 210 || value == 211) { h->ctx.tc_h16 = int(value == 211); return RT_OK; }
+      if (value >= 210 && value <= 212) { h->ctx.tc_h16 = int(value - 210); return RT_OK; }
       if (value == 220 || value == 221) { h->ctx.hooi_tc = int(value == 221); return RT_OK; }
       h->ctx.tc_ablate = int(value);
       return RT_OK;

@@ -74,7 +74,8 @@ struct Ctx {
   int force_dist = 0;           // run the slab exchanges on a 1-rank communicator (tests)
   mutable const char* label = nullptr;   // profiler name override for the next TC launches
   int tc_presplit_z = 0;        // power iteration: write Z R^-1 pre-split [hi | lo] (ablation 200 toggles)
-  int tc_h16 = 1;               // power product on the fp16-split kernel (ttm_s_h16; ablation 210/211 toggles)
+  int tc_h16 = 1;               // fp16-split X passes (R29; ablation 210/211 toggles; 212 = on with the
+                                // device gate forced closed, so the tf32 twins run: tests)
   int hooi_tc = 1;              // RP-HOOI: X pass of the S chain on the tensor cores (ablation 220/221 toggles)
 };
 

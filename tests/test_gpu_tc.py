@@ -195,6 +195,34 @@ def test_tc_hosvd_parity(P, htc, name, dims, core, ranks):
     assert abs(e - ref["E"]) / ref["E"] <= 1e-5
 
 
+@pytest.mark.parametrize("mode", [211, 212])
+def test_tc_hosvd_h16_gate(P, mode):
+    """R29's device-side gate: with the scale forced to 0 (option 212) every fp16-split launch stands
+    down and its tf32 twin (launched beside it, gated on the same scale) produces the result --
+    the same parity as the fp16 path (211) on the same inputs."""
+    from paper_2001_07124_b200 import _lib as L
+    h = _handle(P, 2, omega_tf32=True)
+    h.set_option(L.RT_OPT_TC_ABLATE, mode)
+    try:
+        # K = R + p = 32 (a multiple of 4): the power products take the fp16 / twin kernels too
+        cfg = synth.CONFIGS["cfg2"].scaled((200, 180, 160), (22, 22, 22), (22, 22, 22))
+        x = synth.make_tensor(cfg)
+        oms = [synth.round_tf32(synth.gaussian_omega(cfg, n)) for n in range(3)]
+        ref = oracle.hosvd(x, cfg.ranks, oms, q=1)
+        res = P.rtucker_hosvd(h, dev(x), cfg.ranks, cfg.p, 1, [om_dev(o) for o in oms])
+        h.sync()
+        qg = [mat(q) for q in res["Q"]]
+        gg = P.core_to_numpy(res["G"])
+        for n in range(3):
+            assert M.subspace(qg[n], ref["Q"][n]) <= 1e-5, (mode, n, M.subspace(qg[n], ref["Q"][n]))
+        assert M.core_in_oracle_basis(gg, qg, ref["G"], ref["Q"]) <= 1e-5
+        assert M.recon(gg, qg, ref["G"], ref["Q"]) <= 1e-5
+        e = mat(res["err"])[0]
+        assert abs(e - ref["E"]) / ref["E"] <= 1e-5
+    finally:
+        h.close()
+
+
 @pytest.mark.parametrize("scale", [3e-12, 1.0, 1e12])
 def test_tc_hosvd_h16_scales(P, htc, scale):
     """HOSVD with q = 1 on the fp16-split kernels (power products Z = X^T Q_y, Y = X Q_z and the
