@@ -46,7 +46,7 @@ def _peaks():
 
 
 # ----------------------------------------------------------------- work model
-def work_model(cfg, nranks=1):
+def work_model(cfg, nranks=1, omega_products=2):
     """Algorithmic bytes / flops per rank per step, by kernel class.
 
     ttm_s (sketch & power products Y = X_(n) B): per launch reads X_local and B (J_n x K_n);
@@ -80,7 +80,7 @@ def work_model(cfg, nranks=1):
     total_flops = s_flops + t_flops + r_flops
     # hardware tensor flops of the ttm_s class: the Omega sketch runs 2 tf32 products (tf32-exact
     # Omega, reading R18); the power product Y = X Q_z runs 3 fp16 products (fp16 split, R29)
-    s_hw_tf32 = sum(2 * xl * K[n] * 2 for n in range(N))
+    s_hw_tf32 = sum(2 * xl * K[n] * omega_products for n in range(N))
     s_hw_f16 = sum(2 * xl * K[n] * 3 * cfg.q for n in range(N))
     return {"ttm_s": (s_bytes, s_flops, s_n), "ttm_t": (t_bytes, t_flops, t_n), "residual": (r_bytes, r_flops, 1),
             "total_flops": total_flops, "x_bytes_local": xl * esz, "ttm_s_hw_tf32": s_hw_tf32,
@@ -207,12 +207,14 @@ def run_gpu(args, cfg):
         for n in range(N):
             rows = partition.omega_rows(cfg.dims, n, lo, hi)
             if rows is not None:
-                oms.append(synth.gaussian_omega_device(cfg, n, dev, row0=rows[0], rows=rows[1], tf32=True))
+                oms.append(synth.gaussian_omega_device(cfg, n, dev, row0=rows[0], rows=rows[1],
+                                                       tf32=args.omega == "tf32"))
             else:
-                oms.append(synth.gaussian_omega_device(cfg, n, dev, tf32=True))
+                oms.append(synth.gaussian_omega_device(cfg, n, dev, tf32=args.omega == "tf32"))
         torch.cuda.synchronize()
         h = P.Handle(stream=stream, nccl_id=nid, nranks=world, rank=rank)
-        h.set_option(3, 1)                  # RT_OPT_OMEGA_TF32: Omega is host/device-rounded to tf32
+        if args.omega == "tf32":
+            h.set_option(3, 1)              # RT_OPT_OMEGA_TF32: Omega is device-rounded to tf32
 
         def step():
             return P.rtucker_hosvd(h, X, cfg.ranks, cfg.p, cfg.q, oms, last_offset=lo, last_global=I_last)
@@ -338,15 +340,31 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-elems", type=float, default=5.0e8)
+    ap.add_argument("--omega", default="tf32", choices=["tf32", "general"],
+                    help="tf32: Gaussian Omega rounded to tf32 before the call (RT_OPT_OMEGA_TF32, reading R18, "
+                         "2 tensor products per sketch); general: fp32 Gaussian Omega (3 products)")
     args = ap.parse_args()
     cfg = synth.CONFIGS[args.config]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        # not launched by torchrun: start one rank per GPU ourselves (same command line)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if args.impl != "reference" and world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
     workload = (f"{cfg.name}: {'x'.join(map(str, cfg.dims))} {cfg.dtype} randomized "
                 f"{'HOSVD (Alg.6)' if cfg.algo == 'hosvd' else 'STHOSVD (Alg.8)'}, rank {cfg.ranks}, "
                 f"p={cfg.p}, q={cfg.q}, Gaussian Omega, +relative error")
     config = {"workload": workload, "dims": list(cfg.dims), "ranks": list(cfg.ranks), "p": cfg.p, "q": cfg.q,
-              "parallelism": f"slab{args.gpus}" if args.gpus > 1 else "single",
+              "parallelism": f"slab{world}" if world > 1 else "single",
+              "omega": ("Gaussian, tf32-rounded on the device before the call (RT_OPT_OMEGA_TF32, reading R18)"
+                        if args.omega == "tf32" else "Gaussian fp32 (general Omega: 3xTF32 sketch)"),
               "l2": "inputs larger than L2 (X 32 GiB >> 126 MB; no flush needed)",
               "step": "rtucker_hosvd incl. residual pass for E"}
 
@@ -374,7 +392,7 @@ def main():
     xbytes = cfg.nbytes
     ms = r["ms"] / args.steps
     value = xbytes / (ms * 1e-3) / 1e9
-    wm = work_model(cfg, r["world"])
+    wm = work_model(cfg, r["world"], 2 if args.omega == "tf32" else 3)
     # dominant kernel class by measured device time: the X-streaming launches of one TTM shape
     # (ttm_s_tc = Omega sketch + power product Y = X Z; ttm_t_tc = Z = X^T Q + first core stage)
     prof = sorted(r["prof"], key=lambda e: -e[2])

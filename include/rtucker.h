@@ -98,7 +98,10 @@ const char* rt_last_error(const rt_handle* h);
 rt_status rt_sync(rt_handle* h);
 
 /* Options.  RT_OPT_TTM_IMPL: 0 / 2 tcgen05 where the shape fits the TMA path (fp32 data,
- * 16-byte aligned strides), CUDA-core (SIMT) kernels elsewhere; 1 CUDA-core TTM kernels only.  RT_OPT_PROFILE: 1 records a CUDA event pair around every launch (read with
+ * 16-byte aligned strides), CUDA-core (SIMT) kernels elsewhere; 1 CUDA-core TTM kernels only; 3 the
+ * strict reference-precision mode: CUDA-core kernels whose X passes (sketches, power products, core
+ * stages, residual) accumulate in fp64 (fp32 data widened exactly), for parity at the relative 1e-5
+ * bar where fp32 accumulation is first-order visible (R-PET, RP-HOOI E; R28/R30).  RT_OPT_PROFILE: 1 records a CUDA event pair around every launch (read with
  * rt_profile_read).  RT_OPT_OMEGA_TF32: 1 = the caller guarantees every entry of the random test
  * matrices (Gaussian Omega, the Khatri-Rao factors, R-PET's Omega~) is exactly representable in
  * tf32 (e.g. rounded on the host before it is given to both the oracle and this library); the
@@ -119,7 +122,10 @@ rt_status rt_set_option(rt_handle* h, rt_option opt, int64_t value);
 
 /* Profile of the launches recorded since the last read (synchronizes the stream).
  * Fills up to `cap` entries: kernel class name (NUL-terminated, <= 47 chars), launch
- * count, total device milliseconds.  *n = number of classes; *launches = total. */
+ * count, total device milliseconds.  *n = number of classes; *launches = total.  Two extra
+ * entries (ms = 0) count the gated pairs of R29 whose work was done since the last read, recorded
+ * on the device whether or not RT_OPT_PROFILE is on: "h16_ran" (fp16-split X passes) and
+ * "tf32_twin_ran" (their tf32 twins, which run instead when X's scale comes out 0). */
 typedef struct { char name[48]; int64_t count; double ms; } rt_profile_entry;
 rt_status rt_profile_read(rt_handle* h, rt_profile_entry* out, int cap, int* n, int64_t* launches);
 

@@ -17,6 +17,7 @@ struct rt_handle {
   std::string err;
   int device = 0;
   int* d_status = nullptr;
+  unsigned int* d_runs = nullptr;   // [2] fp16-split / tf32-twin run counters (rt_profile_read)
 };
 
 namespace {
@@ -152,6 +153,14 @@ static rt_status create_common(rt_handle** h, void* stream) {
   }
   cudaMemset(hh->d_status, 0, sizeof(int));
   hh->ctx.d_status = hh->d_status;
+  if (cudaMalloc(&hh->d_runs, 2 * sizeof(unsigned int)) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(hh->d_status);
+    delete hh;
+    return fail(nullptr, RT_ECUDA, "cudaMalloc(run counters) failed");
+  }
+  cudaMemset(hh->d_runs, 0, 2 * sizeof(unsigned int));
+  hh->ctx.d_runs = hh->d_runs;
   hh->ctx.prof = &hh->prof;
   *h = hh;
   return RT_OK;
@@ -192,6 +201,7 @@ rt_status rt_destroy(rt_handle* h) {
   if (h->ctx.stream) cudaStreamSynchronize(h->ctx.stream); else cudaDeviceSynchronize();
   h->comm.reset();
   if (h->d_status) cudaFree(h->d_status);
+  if (h->d_runs) cudaFree(h->d_runs);
   delete h;
   return RT_OK;
 }
@@ -257,6 +267,20 @@ rt_status rt_profile_read(rt_handle* h, rt_profile_entry* out, int cap, int* n, 
       P.pool.push_back(r.b);
     }
     P.recs.clear();
+    // device run counters of the fp16-split X passes and their tf32 twins (R29): which one of each
+    // gated pair did the work since the last read
+    unsigned int runs[2] = {0, 0};
+    RT_CUDA(cudaMemcpy(runs, h->d_runs, sizeof(runs), cudaMemcpyDeviceToHost));
+    RT_CUDA(cudaMemset(h->d_runs, 0, sizeof(runs)));
+    const char* rn[2] = {"h16_ran", "tf32_twin_ran"};
+    for (int k = 0; k < 2; ++k) {
+      if (runs[k] == 0 || cnt >= cap) continue;
+      std::memset(out[cnt].name, 0, sizeof(out[cnt].name));
+      std::strncpy(out[cnt].name, rn[k], sizeof(out[cnt].name) - 1);
+      out[cnt].count = int64_t(runs[k]);
+      out[cnt].ms = 0;
+      ++cnt;
+    }
     if (n) *n = cnt;
     if (launches) *launches = P.launches;
     P.launches = 0;
@@ -301,27 +325,28 @@ rt_status rtucker_qr(rt_handle* h, int64_t m, int64_t k, rt_dtype dtype, const v
     RT_REQUIRE(k <= 128, rt::kEUNSUPPORTED, "k > 128 not supported");
     rt::Engine eng(h->ctx, h->ws, h->comm.get());
     const bool dist = rows_distributed && eng.dist();
-    int64_t m_glob = m, row0 = 0;
+    double* shift_dev = nullptr;
+    int64_t* row0_dev = nullptr;
     if (dist) {
-      // global row count and this rank's first row: allgather of local counts (host-visible)
+      // global row count and this rank's first row from an allgather of the local counts, kept on
+      // the device (enqueue-only: no host sync).  A global m < k makes the Cholesky break down
+      // (RT_ENUMERIC at rt_sync).
       double* cnt = h->ws.alloc_n<double>(1);
       double* all = h->ws.alloc_n<double>(eng.comm->nranks());
-      const double md = double(m);
-      RT_CUDA(cudaMemcpyAsync(cnt, &md, sizeof(double), cudaMemcpyHostToDevice, h->ctx.stream));
+      shift_dev = h->ws.alloc_n<double>(1);
+      row0_dev = h->ws.alloc_n<int64_t>(1);
+      rt::fill_value(h->ctx, cnt, double(m));
       eng.comm->allgather(cnt, all, 1, h->ctx.stream);
-      std::unique_ptr<double[]> host(new double[eng.comm->nranks()]);
-      RT_CUDA(cudaMemcpyAsync(host.get(), all, sizeof(double) * eng.comm->nranks(), cudaMemcpyDeviceToHost,
-                              h->ctx.stream));
-      RT_CUDA(cudaStreamSynchronize(h->ctx.stream));
-      m_glob = 0;
-      for (int r = 0; r < eng.comm->nranks(); ++r) {
-        if (r < eng.comm->rank()) row0 += int64_t(host[r]);
-        m_glob += int64_t(host[r]);
-      }
+      rt::dist_rows_info(h->ctx, all, eng.comm->nranks(), eng.comm->rank(), int(k), shift_dev, row0_dev);
+    } else {
+      RT_REQUIRE(m >= k, rt::kERANK, "thin QR needs m >= k");
     }
-    RT_REQUIRE(m_glob >= k, rt::kERANK, "thin QR needs m >= k");
-    if (dtype == RT_F64) eng.qr_rows<double>(static_cast<const double*>(Y), m, m_glob, int(k), ldy, Q, ldq, R, dist, row0);
-    else if (dtype == RT_F32) eng.qr_rows<float>(static_cast<const float*>(Y), m, m_glob, int(k), ldy, Q, ldq, R, dist, row0);
+    // m_glob = max(m, k) only passes the host-side check when distributed; the device values rule
+    const int64_t mg = std::max<int64_t>(m, k);
+    if (dtype == RT_F64)
+      eng.qr_rows<double>(static_cast<const double*>(Y), m, mg, int(k), ldy, Q, ldq, R, dist, 0, shift_dev, row0_dev);
+    else if (dtype == RT_F32)
+      eng.qr_rows<float>(static_cast<const float*>(Y), m, mg, int(k), ldy, Q, ldq, R, dist, 0, shift_dev, row0_dev);
     else throw rt::Error(rt::kEINVAL, "bad dtype");
   });
 }

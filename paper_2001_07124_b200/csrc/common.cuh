@@ -66,7 +66,10 @@ struct Ctx {
   int* d_status = nullptr;      // device status latch
   Profiler* prof = nullptr;
   int num_sms = 148;
-  int ttm_impl = 0;             // 0 auto, 1 SIMT, 2 tcgen05 (error if unavailable)
+  int ttm_impl = 0;             // 0 auto, 1 SIMT, 2 tcgen05 (error if unavailable), 3 SIMT with fp64
+                                // accumulation of every X pass (the strict reference-precision mode)
+  bool simt() const { return ttm_impl == 1 || ttm_impl == 3; }
+  bool acc64() const { return ttm_impl == 3; }
   int omega_tf32 = 0;           // caller asserts Gaussian Omega entries are tf32-representable
   int tc_seg = 16;              // tcgen05: 32-element chunks per TMEM accumulator segment (drained to fp32 regs)
   int tc_ablate = 0;            // profiling only (RT_OPT_TC_ABLATE): 1 no MMA, 2 no split; results invalid
@@ -77,6 +80,8 @@ struct Ctx {
   int tc_h16 = 1;               // fp16-split X passes (R29; ablation 210/211 toggles; 212 = on with the
                                 // device gate forced closed, so the tf32 twins run: tests)
   int hooi_tc = 1;              // RP-HOOI: X pass of the S chain on the tensor cores (ablation 220/221 toggles)
+  unsigned int* d_runs = nullptr;  // device counters: [0] fp16-split X passes that did their work,
+                                   // [1] tf32 twins that ran in their place (R29; rt_profile_read)
 };
 
 // Launch a kernel (given as a lambda issuing <<<...>>> on ctx.stream) with optional

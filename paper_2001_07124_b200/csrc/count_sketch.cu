@@ -407,7 +407,7 @@ void prep(const Ctx& ctx, const int32_t* code, int64_t J, int64_t Jpad, int K, i
 // TMA path for fp32 a > 1; false (nothing launched) when it does not apply
 bool count_sketch_tma(const Ctx& ctx, Arena& ws, const float* X, Box box, const int32_t* code, int K, double* Y,
                       int64_t ldy, int sms, size_t budget) {
-  if (ctx.ttm_impl == 1 || box.a % 4 != 0 || (reinterpret_cast<uintptr_t>(X) % 16) != 0 ||
+  if (ctx.simt() || box.a % 4 != 0 || (reinterpret_cast<uintptr_t>(X) % 16) != 0 ||
       box.a >= (int64_t(1) << 31) || box.I >= (int64_t(1) << 31) || box.b >= (int64_t(1) << 31))
     return false;
   // TI rows (lane = row), NB boxes of 32 alpha per stage, as many stages as fit.  Default
@@ -466,7 +466,7 @@ bool count_sketch_tma(const Ctx& ctx, Arena& ws, const float* X, Box box, const 
 bool count_sketch_rows_tma(const Ctx& ctx, Arena& ws, const float* X, Box box, const int32_t* code, int K,
                            double* Y, int64_t ldy, int sms, size_t budget) {
   const int64_t I = box.I, J = box.J();
-  if (ctx.ttm_impl == 1 || I % 4 != 0 || (reinterpret_cast<uintptr_t>(X) % 16) != 0 || I >= (int64_t(1) << 31) ||
+  if (ctx.simt() || I % 4 != 0 || (reinterpret_cast<uintptr_t>(X) % 16) != 0 || I >= (int64_t(1) << 31) ||
       J >= (int64_t(1) << 31))
     return false;
   constexpr int TI = 256;

@@ -51,7 +51,7 @@ class Engine {
             double* R, bool rows_dist, int64_t row0);
   template <typename T>
   void qr_rows(const T* Y, int64_t m, int64_t m_glob, int k, int64_t ldy, double* Q, int64_t ldq, double* R,
-               bool rows_dist, int64_t row0);
+               bool rows_dist, int64_t row0, const double* shift_dev = nullptr, const int64_t* row0_dev = nullptr);
   // orthonormalize the tall Z of the power iteration in place (shifted CholeskyQR, fp64 Gram)
   template <typename T>
   bool qr_z(T* Z, int64_t m, int64_t ldz, int64_t m_glob, int k, bool rows_dist, int64_t row0, T* Z2 = nullptr,
@@ -87,7 +87,7 @@ class Engine {
   // slab partial sums are allreduced when the last mode is contracted
   template <typename T>
   void multi_ttm_skip(const TView& X, const T* data, const double* const* Q, const int64_t* ldq, const int64_t* C,
-                      int skip, double* out);
+                      int skip, double* out, const bool* ortho = nullptr);
 
  private:
   void canon(double* Qn, int64_t m, int r, int64_t ld, int64_t row0, bool dist_rows, double* U, int ku);

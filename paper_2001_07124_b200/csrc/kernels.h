@@ -81,8 +81,13 @@ void gram(const Ctx& ctx, Arena& ws, const T* A, int64_t m, int k, int64_t lda, 
 
 // Cholesky of (G + shift*I) (k x k) -> R (upper, col-major) and Rinv.  shift_coef * trace(G)
 // is the shift.  zero_flag[0] = 1 if trace(G) == 0 (all-zero input, reading R7).
+// shift_dev (nullable): device shift coefficient used instead of shift_coef
 void chol_inv(const Ctx& ctx, const double* G, int k, double shift_coef, double* R, double* Rinv,
-              int* zero_flag);
+              int* zero_flag, const double* shift_dev = nullptr);
+// row-distributed QR: first global row of this rank and the shifted-CholeskyQR coefficient with the
+// global row count, from the allgathered local row counts (device only)
+void dist_rows_info(const Ctx& ctx, const double* counts, int nranks, int rank, int k, double* shift_coef,
+                    int64_t* row0);
 
 // C(m x n) = A(m x k) * B(k x n); A col-major (lda) of TA, B fp64 col-major (ldb), C of TC (ldc).
 // rowmajor: A and C are row-major (row pitches lda, ldc).
@@ -91,7 +96,7 @@ void chol_inv(const Ctx& ctx, const double* G, int k, double shift_coef, double*
 template <typename TA, typename TC>
 void gemm_tall(const Ctx& ctx, const TA* A, int64_t m, int k, int64_t lda, const double* B, int n,
                int64_t ldb, TC* C, int64_t ldc, const int* zero_flag = nullptr, int64_t row0 = 0,
-               bool rowmajor = false);
+               bool rowmajor = false, const int64_t* row0_dev = nullptr);
 
 // Small dense fp64 GEMM C = op(A) op(B) (col-major), for k x k triangular products.
 void gemm_small(const Ctx& ctx, bool ta, bool tb, int m, int n, int k, const double* A, int lda,
@@ -126,12 +131,12 @@ void transpose_copy(const Ctx& ctx, const T* in, int64_t m, int64_t n, int64_t l
 // P, X of type T; Q of type T.  Writes 2 fp64 sums to out2 (deterministic partials).
 template <typename T>
 void residual(const Ctx& ctx, Arena& ws, const T* X, int64_t J, int64_t In, const T* P, int R,
-              const T* Q, int64_t ldq, double* out2);
+              const T* Q, int64_t ldq, double* out2, const float* rscale = nullptr);
 
 // tcgen05 residual (ttm_tc.cu): same sums with Xhat = P Q^T built on the tensor cores (fp32 data,
 // R <= 64, J % 4 == 0, ldp % 4 == 0).  Returns false (nothing launched) when not applicable.
 bool residual_tc(const Ctx& ctx, Arena& ws, const float* X, int64_t J, int64_t In, const float* P, int64_t ldp,
-                 int R, const float* Q, int64_t ldq, double* out2);
+                 int R, const float* Q, int64_t ldq, double* out2, const float* rscale = nullptr);
 // out2 = fixed-order sums of n (a, b) pairs
 void reduce_pairs(const Ctx& ctx, const double* part, int n, double* out2);
 
@@ -139,9 +144,14 @@ void reduce_pairs(const Ctx& ctx, const double* part, int n, double* out2);
 void sumsq(const Ctx& ctx, Arena& ws, const double* x, int64_t n, double* out);
 
 // E = sqrt(res/xx), E_gram = sqrt(max(0, 1 - gg/xx)) (0 when xx == 0).
-void finalize_err(const Ctx& ctx, const double* sums /*res, xx*/, const double* gg, double* E, double* Eg);
+// rscale (nullable): the power-of-two scale the residual sums were taken at (resid_scale)
+void finalize_err(const Ctx& ctx, const double* sums /*res, xx*/, const double* gg, double* E, double* Eg,
+                  const float* rscale = nullptr);
+// *s = 2^-e with rms = sqrt(gg / numel) in [2^(e-1), 2^e): the residual pass works on s X (exact)
+void resid_scale(const Ctx& ctx, const double* gg, double numel, float* s);
 
 void fill_zero(const Ctx& ctx, void* p, size_t bytes);
+void fill_value(const Ctx& ctx, double* p, double v);   // *p = v, stream-ordered (no host staging)
 void set_status_if_nonfinite(const Ctx& ctx, const double* x, int64_t n);
 
 }  // namespace rt

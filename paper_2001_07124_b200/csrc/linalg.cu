@@ -109,7 +109,7 @@ __device__ inline int tri(int i, int c) { return i * (i + 1) / 2 + c; }
 
 __global__ void __launch_bounds__(512) chol_inv_kernel(const double* __restrict__ G, int k, double shift_coef,
                                                         double* __restrict__ R, double* __restrict__ Rinv,
-                                                        int* zero_flag, int* status) {
+                                                        int* zero_flag, int* status, const double* shift_dev) {
   extern __shared__ double sm[];
   double* L = sm;                        // k(k+1)/2
   double* W = sm + k * (k + 1) / 2;      // k(k+1)/2
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(512) chol_inv_kernel(const double* __restrict_
   tr = block_sum(tr, red);
   if (t == 0) {
     s_tr = tr;
-    s_shift = shift_coef * tr;
+    s_shift = (shift_dev ? *shift_dev : shift_coef) * tr;
     s_bad = 0;
     if (!(tr == tr) || tr > DBL_MAX) latch(status, kStatusNonFinite);
     if (zero_flag) *zero_flag = (tr == 0.0) ? 1 : 0;
@@ -191,7 +191,7 @@ constexpr int NBK = 16;
 
 __global__ void __launch_bounds__(256) chol_inv_blk_kernel(const double* __restrict__ G, int k, double shift_coef,
                                                            double* __restrict__ R, double* __restrict__ Rinv,
-                                                           int* zero_flag, int* status) {
+                                                           int* zero_flag, int* status, const double* shift_dev) {
   extern __shared__ double sm[];
   const int ld = k + 1;
   double* A = sm;                          // k x ld, L in the lower part
@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(256) chol_inv_blk_kernel(const double* __restr
   tr = block_sum(tr, red);
   if (t == 0) {
     s_tr = tr;
-    s_shift = shift_coef * tr;
+    s_shift = (shift_dev ? *shift_dev : shift_coef) * tr;
     s_bad = 0;
     if (!(tr == tr) || tr > DBL_MAX) latch(status, kStatusNonFinite);
     if (zero_flag) *zero_flag = (tr == 0.0) ? 1 : 0;
@@ -325,7 +325,7 @@ template <typename TA, typename TC>
 __global__ void __launch_bounds__(256) gemm_tall_kernel(const TA* A, int64_t m, int k, int64_t lda,
                                                          const double* __restrict__ B, int n, int64_t ldb,
                                                          TC* C, int64_t ldc, const int* zero_flag,
-                                                         int64_t grow0, bool rm) {
+                                                         int64_t grow0, bool rm, const int64_t* grow0_dev) {
   // element (row, c): col-major at row + ld*c, row-major (rm) at row*ld + c
   const int64_t ars = rm ? lda : 1, acs = rm ? 1 : lda, crs = rm ? ldc : 1, ccs = rm ? 1 : ldc;
   extern __shared__ double sm[];
@@ -336,6 +336,7 @@ __global__ void __launch_bounds__(256) gemm_tall_kernel(const TA* A, int64_t m, 
   const int64_t r0 = int64_t(blockIdx.x) * BR;
   const bool zero = zero_flag && *zero_flag;
   if (zero) {
+    if (grow0_dev) grow0 = *grow0_dev;
     for (int e = t; e < BR * n; e += 256) {
       const int rl = e % BR, c = e / BR;
       const int64_t row = r0 + rl;
@@ -560,11 +561,12 @@ __global__ void unfold_copy_kernel(const T* __restrict__ Tt, int64_t a, int64_t 
 }
 
 // Residual: tiles of 128 (j) x 64 (i); R in chunks of BR; grid-stride over tiles.
-template <typename T>
+template <typename T, typename Tacc = typename AccOf<T>::type>
 __global__ void __launch_bounds__(256) residual_kernel(const T* __restrict__ X, int64_t J, int64_t In,
                                                         const T* __restrict__ P, int R, const T* __restrict__ Q,
-                                                        int64_t ldq, double* __restrict__ part) {
-  using Tacc = typename AccOf<T>::type;
+                                                        int64_t ldq, double* __restrict__ part,
+                                                        const float* __restrict__ rscale) {
+  const Tacc sc = rscale ? Tacc(*rscale) : Tacc(1);
   constexpr int BM = 128, BN = 64, BR = 16;
   __shared__ Tacc Ps[BR][BM];
   __shared__ Tacc Qs[BR][BN + 1];
@@ -614,8 +616,8 @@ __global__ void __launch_bounds__(256) residual_kernel(const T* __restrict__ X, 
       for (int r = 0; r < 4; ++r) {
         const int64_t j = j0 + tx + 32 * r;
         if (j >= J) continue;
-        const Tacc x = Tacc(X[j + J * i]);
-        const Tacc d = x - acc[r][c];
+        const Tacc x = Tacc(X[j + J * i]) * sc;
+        const Tacc d = x - acc[r][c] * sc;
         tres = fma(d, d, tres);
         txx = fma(x, x, txx);
       }
@@ -651,10 +653,26 @@ __global__ void sumsq_kernel(const double* __restrict__ x, int64_t n, double* __
   if (threadIdx.x == 0) *out = s;
 }
 
-__global__ void finalize_err_kernel(const double* sums, const double* gg, double* E, double* Eg) {
-  const double res = sums[0], xx = sums[1];
-  if (E) *E = xx > 0 ? sqrt(res / xx) : 0.0;
-  if (Eg) *Eg = xx > 0 ? sqrt(fmax(0.0, 1.0 - *gg / xx)) : 0.0;
+__global__ void finalize_err_kernel(const double* sums, const double* gg, double* E, double* Eg,
+                                    const float* rscale) {
+  const double res = sums[0], xx = sums[1];            // sums of the scaled residual / data
+  const double s = rscale ? double(*rscale) : 1.0;
+  if (E) *E = xx > 0 ? sqrt(res / xx) : 0.0;           // the power-of-two scale cancels exactly
+  if (Eg) *Eg = xx > 0 ? sqrt(fmax(0.0, 1.0 - (*gg * s * s) / xx)) : 0.0;
+}
+
+// Power-of-two scale of the residual pass: rms(X) ~ ||G|| / sqrt(numel) (orthonormal factors) is
+// brought near 1 so the fp32 squares of the data and of the residual neither underflow (|x| <
+// 1e-19) nor overflow (|x| > 1e19).  1 when ||G|| is 0 or not finite.
+__global__ void resid_scale_kernel(const double* gg, double numel, float* s) {
+  float r = 1.f;
+  const double rms = sqrt(*gg / numel);
+  if (rms > 0.0 && isfinite(rms)) {
+    int e;
+    frexp(rms, &e);                                    // rms in [2^(e-1), 2^e)
+    r = ldexpf(1.f, max(-120, min(120, -e)));
+  }
+  *s = r;
 }
 
 __global__ void nonfinite_kernel(const double* __restrict__ x, int64_t n, int* status) {
@@ -681,7 +699,7 @@ template void gram<float>(const Ctx&, Arena&, const float*, int64_t, int, int64_
 template void gram<double>(const Ctx&, Arena&, const double*, int64_t, int, int64_t, double*, bool);
 
 void chol_inv(const Ctx& ctx, const double* G, int k, double shift_coef, double* R, double* Rinv,
-              int* zero_flag) {
+              int* zero_flag, const double* shift_dev) {
   const size_t smem = sizeof(double) * size_t(k) * (k + 1);
   RT_REQUIRE(smem <= 220 * 1024, kEUNSUPPORTED, "chol_inv: k too large");
   const size_t smem_blk = sizeof(double) * (2 * size_t(k) * (k + 1) + size_t(k) * NBK + size_t(k));
@@ -693,15 +711,17 @@ void chol_inv(const Ctx& ctx, const double* G, int k, double shift_coef, double*
   }
   launch(ctx, "chol_inv", [&] {
     if (smem_blk <= 220 * 1024 && !getenv("RT_CHOL_UNBLOCKED"))
-      chol_inv_blk_kernel<<<1, 256, smem_blk, ctx.stream>>>(G, k, shift_coef, R, Rinv, zero_flag, ctx.d_status);
+      chol_inv_blk_kernel<<<1, 256, smem_blk, ctx.stream>>>(G, k, shift_coef, R, Rinv, zero_flag, ctx.d_status,
+                                                            shift_dev);
     else
-      chol_inv_kernel<<<1, 512, smem, ctx.stream>>>(G, k, shift_coef, R, Rinv, zero_flag, ctx.d_status);
+      chol_inv_kernel<<<1, 512, smem, ctx.stream>>>(G, k, shift_coef, R, Rinv, zero_flag, ctx.d_status, shift_dev);
   });
 }
 
 template <typename TA, typename TC>
 void gemm_tall(const Ctx& ctx, const TA* A, int64_t m, int k, int64_t lda, const double* B, int n,
-               int64_t ldb, TC* C, int64_t ldc, const int* zero_flag, int64_t row0, bool rowmajor) {
+               int64_t ldb, TC* C, int64_t ldc, const int* zero_flag, int64_t row0, bool rowmajor,
+               const int64_t* row0_dev) {
   if (m == 0 || n == 0) return;
   const size_t smem = sizeof(double) * (size_t(k) * n + 32 * size_t(k + 1));
   RT_REQUIRE(smem <= 220 * 1024, kEUNSUPPORTED, "gemm_tall: k*n too large");
@@ -712,15 +732,15 @@ void gemm_tall(const Ctx& ctx, const TA* A, int64_t m, int k, int64_t lda, const
   }
   launch(ctx, "gemm_tall", [&] {
     gemm_tall_kernel<TA, TC><<<unsigned(cdiv(m, 32)), 256, smem, ctx.stream>>>(A, m, k, lda, B, n, ldb, C, ldc,
-                                                                               zero_flag, row0, rowmajor);
+                                                                               zero_flag, row0, rowmajor, row0_dev);
   });
 }
 template void gemm_tall<double, double>(const Ctx&, const double*, int64_t, int, int64_t, const double*, int,
-                                        int64_t, double*, int64_t, const int*, int64_t, bool);
+                                        int64_t, double*, int64_t, const int*, int64_t, bool, const int64_t*);
 template void gemm_tall<float, float>(const Ctx&, const float*, int64_t, int, int64_t, const double*, int,
-                                      int64_t, float*, int64_t, const int*, int64_t, bool);
+                                      int64_t, float*, int64_t, const int*, int64_t, bool, const int64_t*);
 template void gemm_tall<float, double>(const Ctx&, const float*, int64_t, int, int64_t, const double*, int,
-                                       int64_t, double*, int64_t, const int*, int64_t, bool);
+                                       int64_t, double*, int64_t, const int*, int64_t, bool, const int64_t*);
 
 void gemm_small(const Ctx& ctx, bool ta, bool tb, int m, int n, int k, const double* A, int lda,
                 const double* B, int ldb, double* C, int ldc) {
@@ -819,18 +839,19 @@ template void unfold_copy<double>(const Ctx&, const double*, Box, double*, int64
 
 template <typename T>
 void residual(const Ctx& ctx, Arena& ws, const T* X, int64_t J, int64_t In, const T* P, int R, const T* Q,
-              int64_t ldq, double* out2) {
+              int64_t ldq, double* out2, const float* rscale) {
   const int nblk = 4 * ctx.num_sms;
   double* part = ws.alloc_n<double>(2 * nblk);
   launch(ctx, "residual_simt", [&] {
-    residual_kernel<T><<<nblk, 256, 0, ctx.stream>>>(X, J, In, P, R, Q, ldq, part);
+    if (ctx.acc64()) residual_kernel<T, double><<<nblk, 256, 0, ctx.stream>>>(X, J, In, P, R, Q, ldq, part, rscale);
+    else residual_kernel<T><<<nblk, 256, 0, ctx.stream>>>(X, J, In, P, R, Q, ldq, part, rscale);
   });
   launch(ctx, "reduce_pairs", [&] { reduce_pairs_kernel<<<1, 256, 0, ctx.stream>>>(part, nblk, out2); });
 }
 template void residual<float>(const Ctx&, Arena&, const float*, int64_t, int64_t, const float*, int, const float*,
-                              int64_t, double*);
+                              int64_t, double*, const float*);
 template void residual<double>(const Ctx&, Arena&, const double*, int64_t, int64_t, const double*, int,
-                               const double*, int64_t, double*);
+                               const double*, int64_t, double*, const float*);
 
 void reduce_pairs(const Ctx& ctx, const double* part, int n, double* out2) {
   launch(ctx, "reduce_pairs", [&] { reduce_pairs_kernel<<<1, 256, 0, ctx.stream>>>(part, n, out2); });
@@ -840,8 +861,31 @@ void sumsq(const Ctx& ctx, Arena&, const double* x, int64_t n, double* out) {
   launch(ctx, "sumsq", [&] { sumsq_kernel<<<1, 512, 0, ctx.stream>>>(x, n, out); });
 }
 
-void finalize_err(const Ctx& ctx, const double* sums, const double* gg, double* E, double* Eg) {
-  launch(ctx, "finalize_err", [&] { finalize_err_kernel<<<1, 1, 0, ctx.stream>>>(sums, gg, E, Eg); });
+void finalize_err(const Ctx& ctx, const double* sums, const double* gg, double* E, double* Eg, const float* rscale) {
+  launch(ctx, "finalize_err", [&] { finalize_err_kernel<<<1, 1, 0, ctx.stream>>>(sums, gg, E, Eg, rscale); });
+}
+// Row-distributed thin QR bookkeeping on the device (no host sync): from the allgathered local
+// row counts, this rank's first global row and the shift coefficient 11 (m k + k (k + 1)) u of
+// shifted CholeskyQR with the global row count m.
+__global__ void dist_rows_info_kernel(const double* counts, int nranks, int rank, int k, double* shift_coef,
+                                      int64_t* row0) {
+  double m = 0.0, r0 = 0.0;
+  for (int r = 0; r < nranks; ++r) { if (r < rank) r0 += counts[r]; m += counts[r]; }
+  *row0 = int64_t(r0);
+  *shift_coef = 11.0 * (m * k + double(k) * (k + 1)) * 1.1102230246251565e-16;
+}
+__global__ void fill_value_kernel(double* p, double v) { *p = v; }
+void fill_value(const Ctx& ctx, double* p, double v) {
+  launch(ctx, "fill_value", [&] { fill_value_kernel<<<1, 1, 0, ctx.stream>>>(p, v); });
+}
+void dist_rows_info(const Ctx& ctx, const double* counts, int nranks, int rank, int k, double* shift_coef,
+                    int64_t* row0) {
+  launch(ctx, "dist_rows_info", [&] {
+    dist_rows_info_kernel<<<1, 1, 0, ctx.stream>>>(counts, nranks, rank, k, shift_coef, row0);
+  });
+}
+void resid_scale(const Ctx& ctx, const double* gg, double numel, float* s) {
+  launch(ctx, "resid_scale", [&] { resid_scale_kernel<<<1, 1, 0, ctx.stream>>>(gg, numel, s); });
 }
 
 void fill_zero(const Ctx& ctx, void* p, size_t bytes) { RT_CUDA(cudaMemsetAsync(p, 0, bytes, ctx.stream)); }

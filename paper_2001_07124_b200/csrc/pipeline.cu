@@ -33,7 +33,7 @@ int64_t pad4(int64_t x) { return (x + 3) & ~int64_t(3); }
 // amax: also gather max|X| there (tensor-core kernel only; the return value says whether it did)
 bool ttm_s_dispatch(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B, int64_t ldb, bool exact,
                     int K, double* Y, int64_t ldy, unsigned int* amax = nullptr) {
-  if (ctx.ttm_impl != 1 && ttm_s_tc(ctx, ws, X, box, B, ldb, exact, K, Y, ldy, false, nullptr, amax)) return amax != nullptr;
+  if (!ctx.simt() && ttm_s_tc(ctx, ws, X, box, B, ldb, exact, K, Y, ldy, false, nullptr, amax)) return amax != nullptr;
   ttm_s<float>(ctx, ws, X, box, B, ldb, 1, K, Y, ldy);
   return false;
 }
@@ -48,7 +48,7 @@ bool ttm_s_dispatch(const Ctx& ctx, Arena& ws, const double* X, Box box, const d
 // xscale: X's fp16 scale when known (an orthonormal Q): the fp16-split kernel instead of 3xTF32
 void ttm_t_dispatch(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
                     int64_t so_a, int64_t so_c, int64_t so_b, bool q_tf32_exact = false, const float* xscale = nullptr) {
-  if (ctx.ttm_impl != 1) {
+  if (!ctx.simt()) {
     if (C <= 128) {
       if (ttm_t_tc(ctx, ws, X, box, Q, ldq, C, out, so_a, so_c, so_b, 0, q_tf32_exact, xscale)) return;
     } else {
@@ -90,9 +90,11 @@ T* working_copy(const Ctx& ctx, Arena& ws, const double* Q, int64_t m, int64_t k
 // ------------------------------------------------------------------ QR (a4)
 // Shifted CholeskyQR3 (sCQR3): step 1 with shift 11(mk + k(k+1)) u trace(G), steps 2-3 plain
 // CholeskyQR; R = R3 R2 R1, R_ii >= 0 by construction (reading R5).  Gram in fp64.
+// shift_dev / row0_dev (nullable): the shift coefficient and this rank's first global row on the
+// device (rtucker_qr's row-distributed form, which learns m_glob from an allgather without a host sync)
 template <typename T>
 void Engine::qr_rows(const T* Y, int64_t m, int64_t m_glob, int k, int64_t ldy, double* Q, int64_t ldq,
-                     double* R, bool rows_dist, int64_t row0) {
+                     double* R, bool rows_dist, int64_t row0, const double* shift_dev, const int64_t* row0_dev) {
   RT_REQUIRE(m_glob >= k, kERANK, "qr: needs m >= k");
   const auto mk = ws.mark();
   double* G = ws.alloc_n<double>(int64_t(k) * k);
@@ -106,8 +108,8 @@ void Engine::qr_rows(const T* Y, int64_t m, int64_t m_glob, int k, int64_t ldy, 
   gram<T>(ctx, ws, Y, m, k, ldy, G);
   allreduce(comm, dist_g, G, int64_t(k) * k, ctx.stream);
   const double shift = 11.0 * (double(m_glob) * k + double(k) * (k + 1)) * kU;
-  chol_inv(ctx, G, k, shift, Rs[0], Ri, zero);
-  gemm_tall<T, double>(ctx, Y, m, k, ldy, Ri, k, k, Q1, m, zero, row0);
+  chol_inv(ctx, G, k, shift, Rs[0], Ri, zero, shift_dev);
+  gemm_tall<T, double>(ctx, Y, m, k, ldy, Ri, k, k, Q1, m, zero, row0, false, row0_dev);
   // steps 2, 3
   for (int s = 1; s < 3; ++s) {
     gram<double>(ctx, ws, Q1, m, k, m, G);
@@ -149,7 +151,7 @@ bool Engine::qr_z(T* Z, int64_t m, int64_t ldz, int64_t m_glob, int k, bool rows
   // fp32 Z on the tensor cores: view Z as the 2-way tensor [a=1, I=k, b=m] (element (c, j) at c + k j);
   // its mode-0 "sketch" with B = Z is Z^T Z, and its mode-0 TTM with R^{-1} is Z R^{-1} (in place:
   // every 128-row tile is read completely before it is written, by the one CTA that owns it).
-  const bool tc = std::is_same<T, float>::value && ctx.ttm_impl != 1 && ldz == k;
+  const bool tc = std::is_same<T, float>::value && !ctx.simt() && ldz == k;
   const Box zb{1, k, m};
   bool done_gram = false;
   if constexpr (std::is_same<T, float>::value) {
@@ -211,7 +213,7 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
       RT_CUDA(cudaMemsetAsync(am, 0, 16, ctx.stream));
     }
     const auto mo = ws.mark();
-    if (std::is_same<T, float>::value && ctx.ttm_impl != 1 && (ld % 4) != 0) {
+    if (std::is_same<T, float>::value && !ctx.simt() && (ld % 4) != 0) {
       // the TMA path needs a 16-byte row pitch: repack Omega (J x K, small next to X) with ld = pad4(K)
       const int64_t ldp = pad4(K);
       T* c = ws.alloc_n<T>(bx.J() * ldp);
@@ -316,7 +318,7 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
   int zsplit = 0;
   const float* xsc = nullptr;
   if constexpr (std::is_same<T, float>::value) {
-    if (ctx.tc_h16 && ctx.ttm_impl != 1 && ttm_s_tc_ok(ctx, data, bx, K) && ldz == K) {
+    if (ctx.tc_h16 && !ctx.simt() && ttm_s_tc_ok(ctx, data, bx, K) && ldz == K) {
       // fp16 split (ttm_s_h16_kernel): Z R^-1 written as fp16 [hi | lo] rows of 2 tc_npad(K) halves
       zsplit = 2;
       ldz2 = 2 * int64_t(tc_npad(K));
@@ -525,11 +527,15 @@ void Engine::rel_error(const TView& X, const T* data, const double* G, const int
   }
   int64_t J = 1;
   for (int k = 0; k < N - 1; ++k) J *= X.d[k];
+  // the sums are taken of s X and s X^ (s a power of two from ||G||: rms(X) near 1), so fp32
+  // squares of data at any scale stay in range; E is unchanged, E_gram rescales exactly
+  float* rs = ws.alloc_n<float>(1);
+  resid_scale(ctx, gg, double(X.size()) * double(X.glob) / double(X.d[N - 1]), rs);
   bool done = false;
-  if constexpr (std::is_same<T, float>::value) done = residual_tc(ctx, ws, data, J, Il, P, J, Rl, QL, Il, sums);
-  if (!done) residual<T>(ctx, ws, data, J, Il, P, Rl, QL, Il, sums);
+  if constexpr (std::is_same<T, float>::value) done = residual_tc(ctx, ws, data, J, Il, P, J, Rl, QL, Il, sums, rs);
+  if (!done) residual<T>(ctx, ws, data, J, Il, P, Rl, QL, Il, sums, rs);
   allreduce(comm, dist(), sums, 2, ctx.stream);                                    // C5
-  finalize_err(ctx, sums, gg, E, Eg);
+  finalize_err(ctx, sums, gg, E, Eg, rs);
   ws.rewind(mk);
 }
 
@@ -706,17 +712,25 @@ void Engine::pet(const TView& X, const int64_t* R, const void* const* omega, con
     int64_t cur[5];
     for (int k = 0; k < N; ++k) cur[k] = X.d[k];
     const Box b0 = TView::box_of(cur, N, 0);
-    int64_t ld0;
-    const T* w0 = working_copy<T>(ctx, ws, Wt[0], X.d[0], Sp[0], ldw[0], ld0);
-    T* h1 = ws.alloc_n<T>(b0.a * Sp[0] * b0.b);
-    ttm_t_dispatch(ctx, ws, data, b0, w0, ld0, int(Sp[0]), h1, 1, b0.a, b0.a * Sp[0], ctx.omega_tf32 != 0);
+    T* h1 = nullptr;
+    double* h1d = nullptr;
+    if (ctx.acc64()) {
+      // strict mode: the X stage accumulates in fp64 and keeps its output in fp64 (no fp32 rounding of H)
+      h1d = ws.alloc_n<double>(b0.a * Sp[0] * b0.b);
+      ttm_t<T, double, double>(ctx, data, b0, Wt[0], 1, ldw[0], int(Sp[0]), h1d, 1, b0.a, b0.a * Sp[0]);
+    } else {
+      int64_t ld0;
+      const T* w0 = working_copy<T>(ctx, ws, Wt[0], X.d[0], Sp[0], ldw[0], ld0);
+      h1 = ws.alloc_n<T>(b0.a * Sp[0] * b0.b);
+      ttm_t_dispatch(ctx, ws, data, b0, w0, ld0, int(Sp[0]), h1, 1, b0.a, b0.a * Sp[0], ctx.omega_tf32 != 0);
+    }
     cur[0] = Sp[0];
-    const double* src = nullptr;
+    const double* src = h1d;
     for (int n = 1; n < N; ++n) {
       const Box b = TView::box_of(cur, N, n);
       double* dst = (n == N - 1) ? H : ws.alloc_n<double>(b.a * Sp[n] * b.b);
       LabelScope ls(ctx, "pet_hchain");
-      if (n == 1) ttm_t<T, double, double>(ctx, h1, b, Wt[n], 1, ldw[n], int(Sp[n]), dst, 1, b.a, b.a * Sp[n]);
+      if (n == 1 && h1) ttm_t<T, double, double>(ctx, h1, b, Wt[n], 1, ldw[n], int(Sp[n]), dst, 1, b.a, b.a * Sp[n]);
       else ttm_t<double, double, double>(ctx, src, b, Wt[n], 1, ldw[n], int(Sp[n]), dst, 1, b.a, b.a * Sp[n]);
       src = dst;
       cur[n] = Sp[n];
@@ -764,9 +778,12 @@ void Engine::pet(const TView& X, const int64_t* R, const void* const* omega, con
 // Reading R25: every stage accumulates in fp64 (CUDA cores) with fp64 intermediates and the fp64
 // factors as stored.  W = S_(n) Omega^(n) has no oversampling, so span(W) is conditioned by
 // kappa(W) ~ 1e1-1e2 and the fp32-accumulated tensor-core chain moved E by ~2e-5 on cfg2-small.
+// ortho (nullable = all): which Q_p this call produced by a QR (orthonormal, |q| <= 1).  The fp16
+// split of the X pass scales Q by 2^14 and needs |q| < 4 (R29): a caller's start factor (Alg.7 allows
+// a random Gaussian one) takes the 3xTF32 form instead.
 template <typename T>
 void Engine::multi_ttm_skip(const TView& X, const T* data, const double* const* Q, const int64_t* ldq,
-                            const int64_t* C, int skip, double* out) {
+                            const int64_t* C, int skip, double* out, const bool* ortho) {
   const int N = X.N;
   const auto mk = ws.mark();
   int ps[5], np_ = 0;
@@ -781,12 +798,13 @@ void Engine::multi_ttm_skip(const TView& X, const T* data, const double* const* 
     bool done = false;
     if constexpr (std::is_same<T, float>::value) {
       // the X pass on the tensor cores (fp32-accurate products, fp32 out), the rest of the chain in fp64
-      if (i == 0 && ctx.hooi_tc && ctx.ttm_impl != 1 && C[p] <= 128) {
+      if (i == 0 && ctx.hooi_tc && !ctx.simt() && C[p] <= 128) {
         const auto mq = ws.mark();
         int64_t ldt;
         const float* qt = working_copy<float>(ctx, ws, Q[p], cur[p], C[p], ldq[p], ldt);
         float* d32 = ws.alloc_n<float>(b.a * C[p] * b.b);
-        const float* xsc = (ctx.tc_h16 && xs_slot) ? x_scale(data, X.size()) : nullptr;
+        const bool q_ok = ortho == nullptr || ortho[p];
+        const float* xsc = (ctx.tc_h16 && xs_slot && q_ok) ? x_scale(data, X.size()) : nullptr;
         LabelScope ls(ctx, "hooi_first");
         if (ttm_t_tc(ctx, ws, data, b, qt, ldt, int(C[p]), d32, 1, b.a, b.a * C[p], 0, false, xsc)) {
           convert2d<float, double>(ctx, d32, b.a * C[p] * b.b, 1, b.a * C[p] * b.b, dst, b.a * C[p] * b.b);
@@ -821,6 +839,7 @@ void Engine::rp_hooi(const TView& X, const int64_t* R, int sweeps, const double*
   xs_slot = ws.alloc_n<float>(1);      // X's fp16 scale (one max|X| pass), shared by all S chains and the core
   xs_key = nullptr;
   int64_t ldq[5];
+  bool ortho[5] = {false, false, false, false, false};   // Q_out[n] produced by this call's QR yet
   for (int n = 0; n < N; ++n) {
     ldq[n] = X.d[n];
     if (Q_out[n] != Q_init[n])
@@ -835,13 +854,14 @@ void Engine::rp_hooi(const TView& X, const int64_t* R, int sweeps, const double*
       int64_t sz = 1;
       for (int k = 0; k < N; ++k) sz *= cur[k];
       double* S = ws.alloc_n<double>(sz);
-      multi_ttm_skip<T>(X, data, Q_out, ldq, R, n, S);                                   // line 4
+      multi_ttm_skip<T>(X, data, Q_out, ldq, R, n, S, ortho);                            // line 4
       const int64_t In = X.d[n];
       double* W = ws.alloc_n<double>(In * R[n]);
       ttm_s<double>(ctx, ws, S, TView::box_of(cur, N, n), omega[it * N + n], omega_ld[it * N + n], 1, int(R[n]), W,
                     In);                                                                  // line 5
       const bool last = (n == N - 1);
       qr_y(W, In, X.Ig(n), int(R[n]), In, Q_out[n], In, nullptr, last && dist(), last ? X.off : 0);   // line 6
+      ortho[n] = true;
       ws.rewind(ms);
     }
   }
@@ -874,9 +894,9 @@ template bool Engine::qr_z<float>(float*, int64_t, int64_t, int64_t, int, bool, 
 template bool Engine::qr_z<double>(double*, int64_t, int64_t, int64_t, int, bool, int64_t, double*, int64_t, int,
                                    const float*);
 template void Engine::qr_rows<float>(const float*, int64_t, int64_t, int, int64_t, double*, int64_t, double*,
-                                     bool, int64_t);
+                                     bool, int64_t, const double*, const int64_t*);
 template void Engine::qr_rows<double>(const double*, int64_t, int64_t, int, int64_t, double*, int64_t, double*,
-                                      bool, int64_t);
+                                      bool, int64_t, const double*, const int64_t*);
 template void Engine::core<float>(const TView&, const float*, const double* const*, const int64_t*,
                                   const int64_t*, double*);
 template void Engine::core<double>(const TView&, const double*, const double* const*, const int64_t*,

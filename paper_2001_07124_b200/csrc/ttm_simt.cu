@@ -31,10 +31,11 @@ template <typename A, typename B, typename C> struct Acc3 {
 // ------------------------------------------------------------------ ttm_s
 // Block tile: BM = 128 rows i, BJ contraction columns j per stage, BN = 16*TN sketch cols.
 // 256 threads = 16 (k) x 16 (i); thread owns i in {ty + 16 r}, k in {tx + 16 c}.
-template <typename T, int TN, bool GRAM>
+// A: accumulator (and partial) type -- T, or fp64 for fp32 data in the strict mode (ttm_impl 3).
+template <typename T, int TN, bool GRAM, typename A = T>
 __global__ void __launch_bounds__(256)
 ttm_s_kernel(const T* __restrict__ X, int64_t a, int64_t I, const T* __restrict__ Bm, int64_t bs_j,
-             int64_t bs_k, int K, int64_t J, int64_t jps, T* __restrict__ part) {
+             int64_t bs_k, int K, int64_t J, int64_t jps, A* __restrict__ part) {
   constexpr int BM = 128;
   constexpr int BJ = sizeof(T) == 8 ? 16 : 32;
   constexpr int BN = 16 * TN;
@@ -46,11 +47,11 @@ ttm_s_kernel(const T* __restrict__ X, int64_t a, int64_t I, const T* __restrict_
   const int64_t jb = int64_t(blockIdx.z) * jps;
   const int64_t je = min(J, jb + jps);
   const int64_t aI = a * I;
-  T acc[8][TN];
+  A acc[8][TN];
 #pragma unroll
   for (int r = 0; r < 8; ++r)
 #pragma unroll
-    for (int c = 0; c < TN; ++c) acc[r][c] = T(0);
+    for (int c = 0; c < TN; ++c) acc[r][c] = A(0);
 
   for (int64_t jc = jb; jc < je; jc += BJ) {
     if (a == 1) {                       // mode 0: X_(n)(i,j) = X[i + I*j], contiguous in i
@@ -109,11 +110,11 @@ ttm_s_kernel(const T* __restrict__ X, int64_t a, int64_t I, const T* __restrict_
 #pragma unroll
       for (int r = 0; r < 8; ++r)
 #pragma unroll
-        for (int c = 0; c < TN; ++c) acc[r][c] = fma(xr[r], br[c], acc[r][c]);
+        for (int c = 0; c < TN; ++c) acc[r][c] = fma(A(xr[r]), A(br[c]), acc[r][c]);
     }
     __syncthreads();
   }
-  T* dst = part + int64_t(blockIdx.z) * K * I;
+  A* dst = part + int64_t(blockIdx.z) * K * I;
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
     const int64_t i = i0 + ty + 16 * r;
@@ -138,7 +139,7 @@ __global__ void splitk_reduce_kernel(const T* __restrict__ part, int64_t I, int 
   Y[i + ldy * k] = s;
 }
 
-template <typename T, int TN>
+template <typename T, int TN, typename A = T>
 void launch_ttm_s(const Ctx& ctx, Arena& ws, const T* X, Box box, const T* Bm, int64_t bs_j,
                   int64_t bs_k, int K, double* Y, int64_t ldy, bool gram) {
   constexpr int BJ = sizeof(T) == 8 ? 16 : 32;
@@ -152,19 +153,19 @@ void launch_ttm_s(const Ctx& ctx, Arena& ws, const T* X, Box box, const T* Bm, i
   splits = std::min<int64_t>(splits, 65535);
   int64_t jps = cdiv(cdiv(J, splits), BJ) * BJ;
   splits = cdiv(J, jps);
-  T* part = ws.alloc_n<T>(splits * K * box.I);
+  A* part = ws.alloc_n<A>(splits * K * box.I);
   const dim3 grid((unsigned)itiles, (unsigned)ktiles, (unsigned)splits);
   if (gram)
     launch(ctx, "ttm_s_gram_simt", [&] {
-      ttm_s_kernel<T, TN, true><<<grid, 256, 0, ctx.stream>>>(X, box.a, box.I, Bm, bs_j, bs_k, K, J, jps, part);
+      ttm_s_kernel<T, TN, true, A><<<grid, 256, 0, ctx.stream>>>(X, box.a, box.I, Bm, bs_j, bs_k, K, J, jps, part);
     });
   else
     launch(ctx, "ttm_s_simt", [&] {
-      ttm_s_kernel<T, TN, false><<<grid, 256, 0, ctx.stream>>>(X, box.a, box.I, Bm, bs_j, bs_k, K, J, jps, part);
+      ttm_s_kernel<T, TN, false, A><<<grid, 256, 0, ctx.stream>>>(X, box.a, box.I, Bm, bs_j, bs_k, K, J, jps, part);
     });
   const int64_t n = box.I * K;
   launch(ctx, "splitk_reduce", [&] {
-    splitk_reduce_kernel<T><<<unsigned(cdiv(n, 256)), 256, 0, ctx.stream>>>(part, box.I, K, int(splits), Y, ldy);
+    splitk_reduce_kernel<A><<<unsigned(cdiv(n, 256)), 256, 0, ctx.stream>>>(part, box.I, K, int(splits), Y, ldy);
   });
 }
 
@@ -431,6 +432,12 @@ void ttm_s(const Ctx& ctx, Arena& ws, const T* X, Box box, const T* Bm, int64_t 
     return;
   }
   if (gram) RT_REQUIRE(box.I <= 128 && K == box.I, kEUNSUPPORTED, "gram mode needs I <= 128");
+  if (std::is_same<T, float>::value && ctx.acc64()) {    // strict mode: fp64 products and sums
+    if (K <= 32)       launch_ttm_s<T, 2, double>(ctx, ws, X, box, Bm, bs_j, bs_k, K, Y, ldy, gram);
+    else if (K <= 64)  launch_ttm_s<T, 4, double>(ctx, ws, X, box, Bm, bs_j, bs_k, K, Y, ldy, gram);
+    else               launch_ttm_s<T, 8, double>(ctx, ws, X, box, Bm, bs_j, bs_k, K, Y, ldy, gram);
+    return;
+  }
   if (K <= 16)       launch_ttm_s<T, 1>(ctx, ws, X, box, Bm, bs_j, bs_k, K, Y, ldy, gram);
   else if (K <= 32)  launch_ttm_s<T, 2>(ctx, ws, X, box, Bm, bs_j, bs_k, K, Y, ldy, gram);
   else if (K <= 48)  launch_ttm_s<T, 3>(ctx, ws, X, box, Bm, bs_j, bs_k, K, Y, ldy, gram);
@@ -448,7 +455,7 @@ void ttm_t(const Ctx& ctx, const Tin* X, Box box, const Tm* Mm, int64_t ms_i, in
     throw Error(kEINVAL, "ttm_t with empty contraction");
   }
   using Tacc = typename Acc3<Tin, Tm, Tout>::type;
-  if (std::is_same<Tacc, double>::value && C > 16 && ctx.ttm_impl != 1) {
+  if ((std::is_same<Tacc, double>::value && C > 16 && ctx.ttm_impl != 1) || ctx.acc64()) {
     // fp64 accumulation: the fp64 warp MMA (fewer shared-memory operand reads per FMA)
     launch_ttm_t_dmma<Tin, Tm, Tout>(ctx, X, box, Mm, ms_i, ms_c, C, out, so_a, so_c, so_b);
     return;

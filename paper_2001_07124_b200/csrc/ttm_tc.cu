@@ -309,6 +309,7 @@ struct SParams {
   float* part;        // [split][K][I]
   unsigned int* amax; // optional: X statistics of the tiles read (xstat_add: max |X| bits, sum |x|)
   const float* gate;  // optional: run only if *gate == 0 (the tf32 fallback of an fp16-split launch)
+  unsigned int* runs; // optional: run counters ([0] fp16 split, [1] tf32 twin), bumped by CTA (0, 0)
   unsigned long long* tim;   // diagnostics (RT_OPT_TC_ABLATE = 1000): per-CTA role wait cycles, else null
   long long* trace;          // diagnostics (RT_OPT_TC_ABLATE = 2000): per-chunk event clocks of CTA (0,0)
 };
@@ -365,6 +366,7 @@ __global__ void __launch_bounds__(NT_TTM, 1)
 ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb, const SParams p) {
   static_assert(!BPRE || BSPLIT, "pre-split B implies the split product form");
   if (p.gate && *p.gate != 0.f) return;                // fp16-split launch in charge (R29)
+  if (p.gate && p.runs && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) atomicAdd(&p.runs[1], 1u);
   using L = Plan<NPAD, BSPLIT, true, sketch_cps<NPAD, BSPLIT, true>()>;
   constexpr int NX = L::NX, CPS = L::CPS, NB = L::NB;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -599,6 +601,7 @@ ttm_s_h16_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant_
   using L = PlanH<NPAD, CPS_>;
   const SParams& p = hp.s;
   if (*hp.xscale == 0.f) return;                       // dynamic range too wide: the tf32 launch runs
+  if (p.runs && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) atomicAdd(&p.runs[0], 1u);
   constexpr int NX = L::NX, CPS = L::CPS, NB = L::NB;
   extern __shared__ __align__(1024) uint8_t smem[];
   const Bars b = bars_of<L>(smem);
@@ -759,7 +762,9 @@ __global__ void xscale_kernel(const unsigned int* __restrict__ stat, double n, f
   if (m > 0.f && isfinite(m)) {
     int e;
     frexpf(m, &e);                                      // m = f 2^e, f in [0.5, 1): floor(log2 m) = e - 1
-    r = ldexpf(1.f, min(15 - e, 127));
+    // s 2^14 (the epilogue divides by it) must stay a finite fp32 power of two: s <= 2^113, i.e.
+    // max|X| >= 2^-98; tinier data take the tf32 kernels
+    r = (15 - e > 113) ? 0.f : ldexpf(1.f, 15 - e);
     if (double(m) > 65536.0 * mean_abs) r = 0.f;       // too wide a dynamic range: tf32 kernels
   }
   *s = force_zero ? 0.f : r;                            // tests: the tf32 twins take over
@@ -781,6 +786,7 @@ struct TParams {
   bool tma_out;       // output tiles staged in shared memory and written by TMA stores (tmo)
   const float* xscale;   // H16 kernels: device scale s of X (the output is divided by s 2^14)
   const float* gate;     // tf32 kernels: run only if *gate == 0 (fallback of an fp16-split launch)
+  unsigned int* runs;    // optional run counters (see SParams)
 };
 
 // AKM: mode 0 (a == 1), X tile K-major [BM j][KC i].  BSPLIT: Q = Q_hi + Q_lo pre-split (an fp64
@@ -798,6 +804,7 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
                 const __grid_constant__ CUtensorMap tmo, const TParams p) {
   static_assert(!H16 || BSPLIT, "the fp16 form always carries Q_lo");
   if (H16 ? (*p.xscale == 0.f) : (p.gate != nullptr && *p.gate != 0.f)) return;   // one of the pair runs (R29)
+  if ((H16 || p.gate != nullptr) && p.runs && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&p.runs[H16 ? 0 : 1], 1u);
   using L = std::conditional_t<H16, PlanH<NPAD, 1, t_outb<NPAD>()>, Plan<NPAD, BSPLIT, false, 1, t_outb<NPAD>()>>;
   constexpr int NX = L::NX;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -1234,7 +1241,7 @@ int tc_split_width(int K) {
 }
 
 bool ttm_s_tc_ok(const Ctx& ctx, const float* X, Box box, int K) {
-  if (ctx.ttm_impl == 1 || tc_npad(K) < 0) return false;
+  if (ctx.simt() || tc_npad(K) < 0) return false;
   const int64_t J = box.J();
   if (box.I < 1 || J < KC || !aligned(X, 16)) return false;
   const bool amn = (box.a == 1);
@@ -1311,6 +1318,7 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
   p.part = ws.alloc_n<float>(splits * K * box.I);
   p.amax = h16 ? nullptr : amax;
   p.gate = nullptr;
+  p.runs = ctx.d_runs;
   p.tim = nullptr;
   p.trace = nullptr;
   const dim3 grid{unsigned(mtiles), unsigned(splits), 1u};
@@ -1435,6 +1443,7 @@ bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q
   p.split_out = split_out;
   p.xscale = h16 ? xscale : nullptr;
   p.gate = h16 ? nullptr : run_if_zero;
+  p.runs = ctx.d_runs;
   RT_REQUIRE(!split_out || (so_c == 1 && (so_a % 4) == 0 && (so_b % 4) == 0 && aligned(out, 16)), kEINVAL,
              "split output needs 16-byte aligned row-major rows");
   RT_REQUIRE(split_out != 2 || ((so_a % 8) == 0 && (so_b % 8) == 0), kEINVAL, "fp16 split rows need 16-byte pitch");
@@ -1520,6 +1529,7 @@ struct RParams {
   int64_t ntiles;     // j tiles of 128
   int nblk;           // i blocks of 64
   double* part;       // [grid][2]
+  const float* rscale;   // power-of-two scale applied to x and x^ (resid_scale), nullable
 };
 
 template <int RP>
@@ -1622,6 +1632,7 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constan
     const int r = 32 * q4 + lane;
     const uint32_t lane_base = tmem + (uint32_t(32 * q4) << 16);
     double res = 0.0, xx = 0.0;
+    const float sc = p.rscale ? *p.rscale : 1.f;
     Ring rg;
     int64_t g = 0;
     for (int64_t u = 0; u < my_tiles; ++u) {
@@ -1659,8 +1670,8 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constan
           tmem_wait_ld();
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
-            const float x = xt[(16 * cb + q) * BM + r];
-            const float d = x - (__uint_as_float(v[q]) + (__uint_as_float(w[q]) + __uint_as_float(z[q])));
+            const float x = xt[(16 * cb + q) * BM + r] * sc;
+            const float d = x - (__uint_as_float(v[q]) + (__uint_as_float(w[q]) + __uint_as_float(z[q]))) * sc;
             tr = fmaf(d, d, tr);
             tx = fmaf(x, x, tx);
           }
@@ -1718,8 +1729,8 @@ __global__ void split_transpose_kernel(const float* __restrict__ Q, int64_t In, 
 }  // namespace
 
 bool residual_tc(const Ctx& ctx, Arena& ws, const float* X, int64_t J, int64_t In, const float* P, int64_t ldp,
-                 int R, const float* Q, int64_t ldq, double* part_out2) {
-  if (ctx.ttm_impl == 1 || R < 1 || R > 64) return false;
+                 int R, const float* Q, int64_t ldq, double* part_out2, const float* rscale) {
+  if (ctx.simt() || R < 1 || R > 64) return false;
   if (!aligned(X, 16) || !aligned(P, 16) || (J % 4) || (ldp % 4) || J > INT32_MAX || In > INT32_MAX) return false;
   const int rp = R <= 32 ? 32 : 64;
   CUtensorMap tx, tp, th, tl;
@@ -1746,6 +1757,7 @@ bool residual_tc(const Ctx& ctx, Arena& ws, const float* X, int64_t J, int64_t I
   p.nblk = int(cdiv(In, RNB));
   const int grid = int(std::min<int64_t>(p.ntiles, ctx.num_sms));
   p.part = ws.alloc_n<double>(2 * grid);
+  p.rscale = rscale;
   if (rp == 32) launch_r<32>(ctx, tx, tp, th, tl, p, grid);
   else launch_r<64>(ctx, tx, tp, th, tl, p, grid);
   // fixed-order final reduction of the per-CTA pairs

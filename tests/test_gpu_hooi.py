@@ -100,6 +100,25 @@ def test_rp_hooi_parity(P, h, h64, name, strict):
     _check(P, res, ref, strict=strict)
 
 
+@pytest.mark.parametrize("strict", [False, True])
+def test_rp_hooi_gaussian_start(P, h, h64, strict):
+    """Alg.7 line 1 allows a random start: unnormalized Gaussian Q_init (entries |q| >= 4 occur,
+    outside the fp16 split's range once scaled by 2^14).  A caller's start factor takes the 3xTF32
+    X pass (R29 applies only to factors this call orthonormalized); parity with the oracle from the
+    same start."""
+    cfg = synth.CONFIGS["cfg2"].scaled((150, 140, 130), (12, 12, 12), (12, 12, 12))
+    x = synth.make_tensor(cfg)
+    q0 = [synth.rng_for(4242, 7, n).standard_normal((cfg.dims[n], cfg.ranks[n])) * 3.0 for n in range(3)]
+    assert max(np.abs(q).max() for q in q0) >= 4.0
+    oms = synth.hooi_omegas(cfg, 2)
+    ref = oracle.rp_hooi(x, cfg.ranks, q0, oms)
+    hh = h64 if strict else h
+    res = P.rtucker_rp_hooi(hh, _dev(x), cfg.ranks, [_t(q) for q in q0], [[_t(o) for o in s] for s in oms])
+    hh.sync()
+    assert all(np.isfinite(q.cpu().numpy()).all() for q in res["Q"])
+    _check(P, res, ref, strict=strict)
+
+
 def test_rp_hooi_zero_sweeps_is_core_of_start(P, h):
     """sweeps = 0: the factors are the (sign-canonicalized) starting factors and G their core."""
     cfg = synth.CONFIGS["cfg2"].scaled((60, 50, 40), (5, 5, 5), (5, 5, 5))

@@ -224,6 +224,26 @@ def test_hosvd_parity(P, h, name):
     _check_result(res, ref, cfg)
 
 
+@pytest.mark.parametrize("name", list(SMALL))
+def test_hosvd_parity_strict_fp64_accumulation(P, name):
+    """The strict reference-precision mode (RT_OPT_TTM_IMPL = 3: every X pass accumulates in fp64)
+    on the same cases: same metrics, and the sketches to 1e-12 of the oracle's."""
+    cfg = SMALL[name]
+    x = synth.make_tensor(cfg)
+    oms = _omegas_for(cfg)
+    ref = oracle.hosvd(x, cfg.ranks, oms, q=cfg.q)
+    hh = P.Handle()
+    hh.set_option(0, 3)
+    try:
+        res = P.rtucker_hosvd(hh, dev(x), cfg.ranks, cfg.p, cfg.q, _to_dev_omegas(oms, "gauss"))
+        y0 = P.rtucker_sketch(hh, dev(x), 0, om_dev(oms[0]))
+        hh.sync()
+        _check_result(res, ref, cfg)
+        assert M.rel_fro(mat(y0), ref["Y0"][0]) <= 1e-12
+    finally:
+        hh.close()
+
+
 def test_sthosvd_kron_parity(P, h):
     cfg = synth.CONFIGS["cfg3"].scaled((40, 36, 32, 30), (6, 6, 6, 6), (6, 6, 6, 6))
     x = synth.make_tensor(cfg)

@@ -53,11 +53,22 @@ def _inputs(cfg):
 U32 = 2.0 ** -24
 
 
-def _e_ok(e, e_ref, tol=1e-5):
-    return abs(e - e_ref) <= max(tol * e_ref, 4 * U32)
+def _e_ok(e, e_ref, tol=1e-5, strict=False):
+    """R28 (tensor-core X passes): max(1e-5 E, 4u); strict (RT_OPT_TTM_IMPL 3, fp64-accumulating X
+    passes): the plain relative 1e-5 bar of north_star."""
+    return abs(e - e_ref) <= (tol * e_ref if strict else max(tol * e_ref, 4 * U32))
 
 
-def _check(P, res, ref, tol=1e-5):
+@pytest.fixture(scope="module")
+def h64(P):
+    """Strict reference-precision mode: every X pass accumulates in fp64 (RT_OPT_TTM_IMPL = 3)."""
+    hh = P.Handle()
+    hh.set_option(0, 3)
+    yield hh
+    hh.close()
+
+
+def _check(P, res, ref, tol=1e-5, strict=False):
     qg = [q.cpu().numpy() for q in res["Q"]]
     gg = P.core_to_numpy(res["G"])
     for n, q in enumerate(qg):
@@ -66,7 +77,7 @@ def _check(P, res, ref, tol=1e-5):
     assert M.core_in_oracle_basis(gg, qg, ref["G"], ref["Q"]) <= tol
     assert M.recon(gg, qg, ref["G"], ref["Q"]) <= tol
     e = float(res["err"][0])
-    assert _e_ok(e, ref["E"], tol), (e, ref["E"])
+    assert _e_ok(e, ref["E"], tol, strict), (e, ref["E"], abs(e - ref["E"]) / ref["E"])
 
 
 CASES = {
@@ -77,15 +88,17 @@ CASES = {
 }
 
 
+@pytest.mark.parametrize("strict", [False, True])
 @pytest.mark.parametrize("name", list(CASES))
-def test_pet_parity(P, h, name):
+def test_pet_parity(P, h, h64, name, strict):
     cfg = CASES[name]
     x = synth.make_tensor(cfg)
     oms, omt = _inputs(cfg)
     ref = oracle.pet(x, cfg.ranks, oms, omt)
-    res = P.rtucker_pet(h, _dev(x), cfg.ranks, [_t(o) for o in oms], [_t(o) for o in omt])
-    h.sync()
-    _check(P, res, ref)
+    hh = h64 if strict else h
+    res = P.rtucker_pet(hh, _dev(x), cfg.ranks, [_t(o) for o in oms], [_t(o) for o in omt])
+    hh.sync()
+    _check(P, res, ref, strict=strict)
 
 
 def test_pet_exact_rank_fp64(P, h):
@@ -128,8 +141,9 @@ def test_pet_invalid_arguments(P, h):
     h.sync()
 
 
+@pytest.mark.parametrize("strict", [False, True])
 @pytest.mark.parametrize("nranks", [2, 3])
-def test_pet_loopback_multirank(P, nranks):
+def test_pet_loopback_multirank(P, nranks, strict):
     """Slab-parallel R-PET on one GPU (loopback communicator): the line-1 sketches of modes
     n < N-1, the core sketch H and Omega~_{N-1} Q^(N-1) are slab partial sums (allreduced), the
     last factor is row-distributed; the gathered result equals the oracle."""
@@ -148,6 +162,8 @@ def test_pet_loopback_multirank(P, nranks):
             s = torch.cuda.Stream()
             with torch.cuda.stream(s):
                 hh = P.Handle(stream=s, loopback_group=grp, rank=r)
+                if strict:
+                    hh.set_option(0, 3)                  # RT_OPT_TTM_IMPL 3: fp64-accumulating X passes
                 lo, hi = int(cuts[r]), int(cuts[r + 1])
                 xs = _dev(np.asfortranarray(x[:, :, lo:hi]))
                 # local rows of Omega_0 / Omega_1 (j = alpha + a beta: the slab's beta block), full Omega_2
@@ -173,7 +189,7 @@ def test_pet_loopback_multirank(P, nranks):
     for n in range(3):
         assert M.subspace(qg[n], ref["Q"][n]) <= 1e-5
     assert M.recon(out[0]["G"], qg, ref["G"], ref["Q"]) <= 1e-5
-    assert _e_ok(out[0]["err"][0], ref["E"]), (out[0]["err"][0], ref["E"])
+    assert _e_ok(out[0]["err"][0], ref["E"], strict=strict), (out[0]["err"][0], ref["E"])
 
 
 def test_pet_tf32_exact_omega_tilde(P):

@@ -211,6 +211,11 @@ def test_tc_hosvd_h16_gate(P, mode):
         ref = oracle.hosvd(x, cfg.ranks, oms, q=1)
         res = P.rtucker_hosvd(h, dev(x), cfg.ranks, cfg.p, 1, [om_dev(o) for o in oms])
         h.sync()
+        runs = _runs(h)
+        if mode == 211:   # 3 Z = X^T Q_y + 3 Y = X Q_z + the first core stage, all fp16 split
+            assert runs.get("h16_ran", 0) >= 7 and runs.get("tf32_twin_ran", 0) == 0, runs
+        else:             # gate forced closed: every fp16 launch stood down, the twins did the work
+            assert runs.get("h16_ran", 0) == 0 and runs.get("tf32_twin_ran", 0) >= 7, runs
         qg = [mat(q) for q in res["Q"]]
         gg = P.core_to_numpy(res["G"])
         for n in range(3):
@@ -223,21 +228,38 @@ def test_tc_hosvd_h16_gate(P, mode):
         h.close()
 
 
-@pytest.mark.parametrize("scale", [3e-12, 1.0, 1e12])
+def _runs(h):
+    """Device run counters of the gated fp16 / tf32-twin pairs since the last read (rt_profile_read)."""
+    return {n: c for n, c, _ in h.profile_read()[0] if n in ("h16_ran", "tf32_twin_ran")}
+
+
+@pytest.mark.parametrize("scale", [1e-31, 1e-30, 3e-12, 1.0, 1e12, 1e30])
 def test_tc_hosvd_h16_scales(P, htc, scale):
     """HOSVD with q = 1 on the fp16-split kernels (power products Z = X^T Q_y, Y = X Q_z and the
     first core stage; X's scale gathered in the first sketch pass: the 'xscale' launch) at data
-    scales far outside the fp16 range: parity with the oracle on the same scaled tensor."""
-    cfg = synth.CONFIGS["cfg2"].scaled((200, 180, 160), (20, 20, 20), (20, 20, 20))
+    scales far outside the fp16 range: parity with the oracle on the same scaled tensor.  K = R + p
+    = 32 (a multiple of 4, so the power products take the fp16 kernels); the device run counters
+    prove which kernel of each gated pair did the work: the fp16 split at every scale down to
+    max|X| >= 2^-98, the tf32 twins below (1e-31: s 2^14 would not be a finite fp32, R29).  The
+    residual sums are taken at a power-of-two scale, so E holds at every scale."""
+    cfg = synth.CONFIGS["cfg2"].scaled((200, 180, 160), (22, 22, 22), (22, 22, 22))
+    assert cfg.ranks[0] + cfg.p == 32
     x = np.asfortranarray((synth.make_tensor(cfg).astype(np.float64) * scale).astype(np.float32))
     oms = [synth.gaussian_omega(cfg, n) for n in range(3)]
     ref = oracle.hosvd(x, cfg.ranks, oms, q=1)
+    _runs(htc)
     htc.set_option(1, 1)
     res = P.rtucker_hosvd(htc, dev(x), cfg.ranks, cfg.p, 1, [om_dev(o) for o in oms])
     htc.sync()
     htc.set_option(1, 0)
-    names = {n for n, _, _ in htc.profile_read()[0]}
+    prof = htc.profile_read()[0]
+    names = {n for n, _, _ in prof}
+    runs = {n: c for n, c, _ in prof if n in ("h16_ran", "tf32_twin_ran")}
     assert "xscale" in names and "absmax" not in names, names      # scale from the first pass, no extra pass
+    if scale >= 1e-30:
+        assert runs.get("h16_ran", 0) >= 7 and runs.get("tf32_twin_ran", 0) == 0, runs
+    else:
+        assert runs.get("h16_ran", 0) == 0 and runs.get("tf32_twin_ran", 0) >= 7, runs
     qg = [mat(q) for q in res["Q"]]
     gg = P.core_to_numpy(res["G"])
     for n in range(3):

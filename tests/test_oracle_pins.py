@@ -276,6 +276,16 @@ def test_P8_P9_pythagoras_and_subpro():
     res = oracle.hosvd(x, ranks, oms, q=1)
     e2 = res["E"] ** 2
     assert abs(e2 - (1 - oracle.fro(res["G"]) ** 2 / oracle.fro(x) ** 2)) < 1e-13
+    # the oracle's E_gram diagnostic is this identity: equal to the direct residual E
+    # (a dropped square or sqrt in rel_error_gram fails here: E ~ 0.3 is far from E^2 and sqrt(E))
+    assert abs(res["E_gram"] - res["E"]) < 1e-12
+    assert abs(oracle.rel_error_gram(x, res["G"]) - res["E"]) < 1e-12
+    # closed forms: ||X|| = 5, ||G|| = 3 -> sqrt(1 - 9/25) = 0.8; ||G|| >= ||X|| -> 0; X = 0 -> 0
+    x5 = np.zeros((2, 2, 2)); x5[0, 0, 0], x5[1, 1, 1] = 3.0, 4.0
+    g3 = np.zeros((1, 1, 1)); g3[0, 0, 0] = 3.0
+    assert abs(oracle.rel_error_gram(x5, g3) - 0.8) < 1e-15
+    assert oracle.rel_error_gram(x5, 2 * g3) == 0.0
+    assert oracle.rel_error_gram(np.zeros((2, 2, 2)), g3) == 0.0
     bound = 0.0
     for n, qn in enumerate(res["Q"]):
         xn = oracle.unfold(x, n)
