@@ -40,7 +40,8 @@ class Engine {
   // outlives the per-mode sketches, computed once per tensor (xs_key = the data it was taken of)
   float* xs_slot = nullptr;
   const void* xs_key = nullptr;
-  const float* x_scale(const float* data, int64_t n);
+  const float* x_scale(const float* data, int64_t n, int64_t n_glob = 0);
+  void finish_scale(const unsigned int* stat, int64_t n_local, int64_t n_glob);
 
   // (1) sketch of mode n incl. q power iterations; Yt: fp64 I_n(local) x K, ld I_n(local).
   template <typename T>

@@ -58,6 +58,13 @@ void x_scale_h16(const Ctx& ctx, Arena& ws, const float* X, int64_t n, float* s)
 // the same scale from statistics already gathered (ttm_s_tc amax) over the n elements of X;
 // s = 0 when max|X| > 2^16 mean|X| (the fp16 kernels then stand down for their tf32 twins)
 void x_scale_from_amax(const Ctx& ctx, const unsigned int* amax, int64_t n, float* s);
+// s is float[2]: s[0] the fp16-split scale above, s[1] = 2^-e (2^(e-1) <= max|X| < 2^e, clamped to
+// 2^+-120; 1 for an all-zero X): the normalizing scale of the power iteration's Z
+// distributed form: every rank's stats as a (max, sum) double pair (x_stat_pair), allgathered
+void x_stat_pair(const Ctx& ctx, const unsigned int* amax, double* pair);
+void x_scale_from_gathered(const Ctx& ctx, const double* pairs, int nranks, int64_t n_glob, float* s);
+// max |X| and sum |x| of n elements into stat (16 bytes, zeroed here): one streaming pass
+void x_absmax_stats(const Ctx& ctx, Arena& ws, const float* X, int64_t n, unsigned int* stat);
 // whether ttm_s_tc would run (same shape/alignment rules, no launch)
 bool ttm_s_tc_ok(const Ctx& ctx, const float* X, Box box, int K);
 int tc_npad(int K);
@@ -68,7 +75,8 @@ int tc_split_width(int K);
 // [hi (tc_npad(C)) | lo (tc_npad(C))] rows, out then points to halves and so_a / so_b count halves.
 bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
               int64_t so_a, int64_t so_c, int64_t so_b, int split_out = 0, bool q_tf32_exact = false,
-              const float* xscale = nullptr, const float* run_if_zero = nullptr);
+              const float* xscale = nullptr, const float* run_if_zero = nullptr, const float* oscale = nullptr);
+// oscale (nullable): device scale multiplied into every output (the power iteration's Z = sn X^T Q)
 // run_if_zero (tf32 form only): the launch does its work only if *run_if_zero == 0 (device-side
 // gate: the fallback of an fp16-split step whose X scale came out 0, R29)
 // xscale (device scale of X from x_scale_h16 / x_scale_from_amax, |Q| <= 1 required): the fp16

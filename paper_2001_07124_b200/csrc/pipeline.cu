@@ -46,11 +46,14 @@ bool ttm_s_dispatch(const Ctx& ctx, Arena& ws, const double* X, Box box, const d
 // q_tf32_exact: Q holds tf32-representable values (a host-rounded test matrix, reading R18): the
 // tensor-core kernel then runs 2 products instead of the 3 of the split form
 // xscale: X's fp16 scale when known (an orthonormal Q): the fp16-split kernel instead of 3xTF32
+// oscale: device scale of the output (tensor-core kernels; the SIMT fallback leaves it unscaled,
+// which only the power iteration's Z uses, whose span it does not change)
 void ttm_t_dispatch(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
-                    int64_t so_a, int64_t so_c, int64_t so_b, bool q_tf32_exact = false, const float* xscale = nullptr) {
+                    int64_t so_a, int64_t so_c, int64_t so_b, bool q_tf32_exact = false, const float* xscale = nullptr,
+                    const float* oscale = nullptr) {
   if (!ctx.simt()) {
     if (C <= 128) {
-      if (ttm_t_tc(ctx, ws, X, box, Q, ldq, C, out, so_a, so_c, so_b, 0, q_tf32_exact, xscale)) return;
+      if (ttm_t_tc(ctx, ws, X, box, Q, ldq, C, out, so_a, so_c, so_b, 0, q_tf32_exact, xscale, nullptr, oscale)) return;
     } else {
       // wider than one TMEM tile (e.g. the R-PET core sketch, S_n = 2K_n + 1): balanced column
       // chunks of <= 128, one X pass each, each writing its slice of the output
@@ -68,7 +71,8 @@ void ttm_t_dispatch(const Ctx& ctx, Arena& ws, const float* X, Box box, const fl
   ttm_t<float, float, float>(ctx, X, box, Q, 1, ldq, C, out, so_a, so_c, so_b);
 }
 void ttm_t_dispatch(const Ctx& ctx, Arena&, const double* X, Box box, const double* Q, int64_t ldq, int C, double* out,
-                    int64_t so_a, int64_t so_c, int64_t so_b, bool = false, const float* = nullptr) {
+                    int64_t so_a, int64_t so_c, int64_t so_b, bool = false, const float* = nullptr,
+                    const float* = nullptr) {
   ttm_t<double, double, double>(ctx, X, box, Q, 1, ldq, C, out, so_a, so_c, so_b);
 }
 
@@ -131,9 +135,29 @@ void Engine::qr_y(const double* Y, int64_t m, int64_t m_glob, int k, int64_t ldy
   qr_rows<double>(Y, m, m_glob, k, ldy, Q, ldq, R, rows_dist, row0);
 }
 
-const float* Engine::x_scale(const float* data, int64_t n) {
+// X's scales (xs_slot[0] fp16 split, [1] normalizing) from its |x| statistics; on a slab the
+// statistics of all ranks are gathered first, so every rank holds the same scales (the partial sums
+// of the slab exchanges must agree on them).  n_glob: element count of the whole tensor.
+void Engine::finish_scale(const unsigned int* stat, int64_t n_local, int64_t n_glob) {
+  if (dist()) {
+    double* pair = ws.alloc_n<double>(2);
+    double* all = ws.alloc_n<double>(2 * comm->nranks());
+    x_stat_pair(ctx, stat, pair);
+    comm->allgather(pair, all, 2, ctx.stream);
+    x_scale_from_gathered(ctx, all, comm->nranks(), n_glob, xs_slot);
+  } else {
+    x_scale_from_amax(ctx, stat, n_local, xs_slot);
+  }
+}
+
+const float* Engine::x_scale(const float* data, int64_t n, int64_t n_glob) {
   RT_REQUIRE(xs_slot != nullptr, kEINVAL, "x_scale: no scale slot");
-  if (xs_key != data) { x_scale_h16(ctx, ws, data, n, xs_slot); xs_key = data; }   // a separate max|X| pass
+  if (xs_key != data) {                                   // a separate max|X| pass
+    unsigned int* stat = ws.alloc_n<unsigned int>(4);
+    x_absmax_stats(ctx, ws, data, n, stat);
+    finish_scale(stat, n, n_glob > 0 ? n_glob : n);
+    xs_key = data;
+  }
   return xs_slot;
 }
 
@@ -199,8 +223,9 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
   // fp16-split power products (fp32 data): X's scale in a slot that outlives this sketch (the
   // driver's, else one taken here); gathered by the first pass over X when that is a tf32 sketch
   bool own_slot = false;
+  const int64_t n_glob = X.size() / X.d[N - 1] * X.glob;
   if constexpr (std::is_same<T, float>::value) {
-    if (q > 0 && ctx.tc_h16 && !xs_slot) { xs_slot = ws.alloc_n<float>(1); xs_key = nullptr; own_slot = true; }
+    if (q > 0 && !xs_slot) { xs_slot = ws.alloc_n<float>(2); xs_key = nullptr; own_slot = true; }
   }
   int K;
   if (kind == 0) {
@@ -208,7 +233,7 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
     const T* om = static_cast<const T*>(omega[n]);
     int64_t ld = omega_ld[n];
     unsigned int* am = nullptr;
-    if (std::is_same<T, float>::value && q > 0 && ctx.tc_h16 && xs_key != data) {
+    if (std::is_same<T, float>::value && q > 0 && xs_key != data) {
       am = ws.alloc_n<unsigned int>(4);                 // {max|X| bits, pad, sum |x| (f64)}
       RT_CUDA(cudaMemsetAsync(am, 0, 16, ctx.stream));
     }
@@ -222,7 +247,7 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
       ld = ldp;
     }
     if (ttm_s_dispatch(ctx, ws, data, bx, om, ld, ctx.omega_tf32 != 0, K, Yt, In, am)) {
-      x_scale_from_amax(ctx, am, X.size(), xs_slot);
+      finish_scale(am, X.size(), n_glob);
       xs_key = data;
     }
     ws.rewind(mo);
@@ -317,13 +342,15 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
   int64_t ldz2 = 0;
   int zsplit = 0;
   const float* xsc = nullptr;
+  const float* zsc = nullptr;       // Z = sn X^T Q: normalizing power of two of X (fp32 Gram of Z in range)
   if constexpr (std::is_same<T, float>::value) {
+    if (!ctx.simt()) zsc = x_scale(data, X.size(), n_glob) + 1;
     if (ctx.tc_h16 && !ctx.simt() && ttm_s_tc_ok(ctx, data, bx, K) && ldz == K) {
       // fp16 split (ttm_s_h16_kernel): Z R^-1 written as fp16 [hi | lo] rows of 2 tc_npad(K) halves
       zsplit = 2;
       ldz2 = 2 * int64_t(tc_npad(K));
       Z2 = reinterpret_cast<T*>(ws.alloc_n<uint16_t>(Jl * ldz2));
-      xsc = x_scale(data, X.size());
+      xsc = x_scale(data, X.size(), n_glob);
     } else if (ctx.tc_presplit_z && ttm_s_tc_ok(ctx, data, bx, K) && ldz == K) {
       zsplit = 1;
       ldz2 = 2 * int64_t(tc_split_width(K));
@@ -340,7 +367,7 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
     // so_a = ldz, so_c = 1, so_b = a ldz
     {
       LabelScope ls(ctx, "ttm_t_tc_pow");
-      ttm_t_dispatch(ctx, ws, data, bx, QyT, ldqt, K, Z, ldz, 1, bx.a * ldz, false, xsc);
+      ttm_t_dispatch(ctx, ws, data, bx, QyT, ldqt, K, Z, ldz, 1, bx.a * ldz, false, xsc, zsc);
     }
     ws.rewind(mq);
     allreduce(comm, last && dist(), Z, Jl * ldz, ctx.stream);                    // C3
@@ -547,7 +574,7 @@ void Engine::hosvd(const TView& X, const int64_t* R, int q, int kind, const void
   const int N = X.N;
   const T* data = static_cast<const T*>(X.data);
   const auto mk = ws.mark();
-  xs_slot = ws.alloc_n<float>(1);      // X's fp16 scale, taken once for all modes' power products
+  xs_slot = ws.alloc_n<float>(2);      // X's fp16 scale, taken once for all modes' power products
   xs_key = nullptr;
   int64_t K[5], ldq[5];
   double* Qt[5];
@@ -586,7 +613,7 @@ void Engine::sthosvd(const TView& X, const int64_t* R, int q, int kind, const vo
                      double* G_out, double* E, double* Eg) {
   const int N = X.N;
   const auto mk = ws.mark();
-  xs_slot = ws.alloc_n<float>(1);
+  xs_slot = ws.alloc_n<float>(2);
   xs_key = nullptr;
   TView S = X;                         // working tensor S (reading R8: S = X)
   const double* sd = nullptr;          // fp64 S after the first shrink
@@ -804,7 +831,8 @@ void Engine::multi_ttm_skip(const TView& X, const T* data, const double* const* 
         const float* qt = working_copy<float>(ctx, ws, Q[p], cur[p], C[p], ldq[p], ldt);
         float* d32 = ws.alloc_n<float>(b.a * C[p] * b.b);
         const bool q_ok = ortho == nullptr || ortho[p];
-        const float* xsc = (ctx.tc_h16 && xs_slot && q_ok) ? x_scale(data, X.size()) : nullptr;
+        const float* xsc =
+            (ctx.tc_h16 && xs_slot && q_ok) ? x_scale(data, X.size(), X.size() / X.d[N - 1] * X.glob) : nullptr;
         LabelScope ls(ctx, "hooi_first");
         if (ttm_t_tc(ctx, ws, data, b, qt, ldt, int(C[p]), d32, 1, b.a, b.a * C[p], 0, false, xsc)) {
           convert2d<float, double>(ctx, d32, b.a * C[p] * b.b, 1, b.a * C[p] * b.b, dst, b.a * C[p] * b.b);
@@ -836,7 +864,7 @@ void Engine::rp_hooi(const TView& X, const int64_t* R, int sweeps, const double*
   const int N = X.N;
   const T* data = static_cast<const T*>(X.data);
   const auto mk = ws.mark();
-  xs_slot = ws.alloc_n<float>(1);      // X's fp16 scale (one max|X| pass), shared by all S chains and the core
+  xs_slot = ws.alloc_n<float>(2);      // X's fp16 scale (one max|X| pass), shared by all S chains and the core
   xs_key = nullptr;
   int64_t ldq[5];
   bool ortho[5] = {false, false, false, false, false};   // Q_out[n] produced by this call's QR yet

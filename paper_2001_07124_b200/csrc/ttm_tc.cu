@@ -755,19 +755,38 @@ __global__ void __launch_bounds__(256) absmax_kernel(const float4* __restrict__ 
   if (blockIdx.x == 0 && int(threadIdx.x) < ntail) { const float v = tail[threadIdx.x]; m = fmaxf(m, fabsf(v)); sq += fabsf(v); }
   xstat_add(stat, m, sq);
 }
-__global__ void xscale_kernel(const unsigned int* __restrict__ stat, double n, float* __restrict__ s, int force_zero) {
-  const float m = __uint_as_float(stat[0]);
-  const double mean_abs = *reinterpret_cast<const double*>(stat + 2) / n;
-  float r = 1.f;
-  if (m > 0.f && isfinite(m)) {
+// s[0] = the fp16-split scale (0: the tf32 twins run), s[1] = sn = 2^-e, the normalizing scale of
+// the power iteration's Z = sn X^T Q (any scale spans the same space; sn keeps Z's fp32 Gram on the
+// tensor cores clear of underflow / overflow at any data scale).  stat: max |X| (double), sum |x|
+// over n elements (all ranks).
+__device__ void xscale_of(double m, double sum_abs, double n, float* __restrict__ s, int force_zero) {
+  const double mean_abs = sum_abs / n;
+  float r = 1.f, sn = 1.f;
+  if (m > 0.0 && isfinite(m)) {
     int e;
-    frexpf(m, &e);                                      // m = f 2^e, f in [0.5, 1): floor(log2 m) = e - 1
+    frexp(m, &e);                                       // m = f 2^e, f in [0.5, 1): floor(log2 m) = e - 1
     // s 2^14 (the epilogue divides by it) must stay a finite fp32 power of two: s <= 2^113, i.e.
     // max|X| >= 2^-98; tinier data take the tf32 kernels
     r = (15 - e > 113) ? 0.f : ldexpf(1.f, 15 - e);
-    if (double(m) > 65536.0 * mean_abs) r = 0.f;       // too wide a dynamic range: tf32 kernels
+    if (m > 65536.0 * mean_abs) r = 0.f;               // too wide a dynamic range: tf32 kernels
+    sn = ldexpf(1.f, max(-120, min(120, -e)));
   }
-  *s = force_zero ? 0.f : r;                            // tests: the tf32 twins take over
+  s[0] = force_zero ? 0.f : r;                          // tests: the tf32 twins take over
+  s[1] = sn;
+}
+__global__ void xscale_kernel(const unsigned int* __restrict__ stat, double n, float* __restrict__ s, int force_zero) {
+  xscale_of(double(__uint_as_float(stat[0])), *reinterpret_cast<const double*>(stat + 2), n, s, force_zero);
+}
+// distributed: stats of every rank gathered as (max, sum) double pairs
+__global__ void stat_pair_kernel(const unsigned int* __restrict__ stat, double* __restrict__ pair) {
+  pair[0] = double(__uint_as_float(stat[0]));
+  pair[1] = *reinterpret_cast<const double*>(stat + 2);
+}
+__global__ void xscale_gathered_kernel(const double* __restrict__ pairs, int nranks, double n, float* __restrict__ s,
+                                       int force_zero) {
+  double m = 0.0, sum = 0.0;
+  for (int r = 0; r < nranks; ++r) { m = fmax(m, pairs[2 * r]); sum += pairs[2 * r + 1]; }
+  xscale_of(m, sum, n, s, force_zero);
 }
 
 // ====================================================================== ttm_t
@@ -787,6 +806,7 @@ struct TParams {
   const float* xscale;   // H16 kernels: device scale s of X (the output is divided by s 2^14)
   const float* gate;     // tf32 kernels: run only if *gate == 0 (fallback of an fp16-split launch)
   unsigned int* runs;    // optional run counters (see SParams)
+  const float* oscale;   // optional device scale of the output (the power iteration's Z = sn X^T Q)
 };
 
 // AKM: mode 0 (a == 1), X tile K-major [BM j][KC i].  BSPLIT: Q = Q_hi + Q_lo pre-split (an fp64
@@ -926,7 +946,9 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
 #pragma unroll
     for (int k = 0; k < NPAD; ++k) sums[k] = 0.f;
     const int segs_per_tile = (p.nic + p.seg - 1) / p.seg;
-    const float inv = H16 ? 1.0f / (*p.xscale * kQScale) : 1.f;   // exact: powers of two
+    // exact: powers of two (the H16 unscaling and the optional output scale)
+    const float inv = (H16 ? 1.0f / (*p.xscale * kQScale) : 1.f) * (p.oscale ? *p.oscale : 1.f);
+    const bool rescale = H16 || p.oscale != nullptr;
     int64_t g = 0;
     for (int64_t u = 0; u < my_tiles; ++u) {
       const int64_t tile = blockIdx.x + u * gridDim.x;
@@ -943,7 +965,7 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
           drain_acc<L, NPAD, BSPLIT>(b, lane_base, g, sums);
         }
       }
-      if constexpr (H16) {
+      if (rescale) {
 #pragma unroll
         for (int k = 0; k < NPAD; ++k) sums[k] *= inv;
       }
@@ -1252,10 +1274,17 @@ bool ttm_s_tc_ok(const Ctx& ctx, const float* X, Box box, int K) {
 void x_scale_from_amax(const Ctx& ctx, const unsigned int* amax, int64_t n, float* s) {
   launch(ctx, "xscale", [&] { xscale_kernel<<<1, 1, 0, ctx.stream>>>(amax, double(n), s, ctx.tc_h16 == 2); });
 }
+void x_stat_pair(const Ctx& ctx, const unsigned int* amax, double* pair) {
+  launch(ctx, "xstat_pair", [&] { stat_pair_kernel<<<1, 1, 0, ctx.stream>>>(amax, pair); });
+}
+void x_scale_from_gathered(const Ctx& ctx, const double* pairs, int nranks, int64_t n, float* s) {
+  launch(ctx, "xscale", [&] {
+    xscale_gathered_kernel<<<1, 1, 0, ctx.stream>>>(pairs, nranks, double(n), s, ctx.tc_h16 == 2);
+  });
+}
 
-void x_scale_h16(const Ctx& ctx, Arena& ws, const float* X, int64_t n, float* s) {
-  RT_REQUIRE(aligned(X, 16), kEINVAL, "x_scale_h16: X must be 16-byte aligned");
-  unsigned int* stat = ws.alloc_n<unsigned int>(4);
+void x_absmax_stats(const Ctx& ctx, Arena& ws, const float* X, int64_t n, unsigned int* stat) {
+  RT_REQUIRE(aligned(X, 16), kEINVAL, "x_absmax_stats: X must be 16-byte aligned");
   RT_CUDA(cudaMemsetAsync(stat, 0, 16, ctx.stream));
   const int64_t n4 = n / 4;
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(cdiv(n4, 256), int64_t(ctx.num_sms) * 8));
@@ -1263,6 +1292,11 @@ void x_scale_h16(const Ctx& ctx, Arena& ws, const float* X, int64_t n, float* s)
     absmax_kernel<<<unsigned(blocks), 256, 0, ctx.stream>>>(reinterpret_cast<const float4*>(X), n4, X + 4 * n4,
                                                             int(n - 4 * n4), stat);
   });
+}
+
+void x_scale_h16(const Ctx& ctx, Arena& ws, const float* X, int64_t n, float* s) {
+  unsigned int* stat = ws.alloc_n<unsigned int>(4);
+  x_absmax_stats(ctx, ws, X, n, stat);
   x_scale_from_amax(ctx, stat, n, s);
 }
 
@@ -1388,7 +1422,7 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
 
 bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
               int64_t so_a, int64_t so_c, int64_t so_b, int split_out, bool q_tf32_exact, const float* xscale,
-              const float* run_if_zero) {
+              const float* run_if_zero, const float* oscale) {
   const int npad = tc_npad(C);
   if (npad < 0) return false;
   const bool h16 = xscale != nullptr && !q_tf32_exact;
@@ -1444,6 +1478,7 @@ bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q
   p.xscale = h16 ? xscale : nullptr;
   p.gate = h16 ? nullptr : run_if_zero;
   p.runs = ctx.d_runs;
+  p.oscale = oscale;
   RT_REQUIRE(!split_out || (so_c == 1 && (so_a % 4) == 0 && (so_b % 4) == 0 && aligned(out, 16)), kEINVAL,
              "split output needs 16-byte aligned row-major rows");
   RT_REQUIRE(split_out != 2 || ((so_a % 8) == 0 && (so_b % 8) == 0), kEINVAL, "fp16 split rows need 16-byte pitch");

@@ -643,3 +643,27 @@ def test_P31_count_sketch_hosvd_exact_rank_recovery():
     oms = [synth.count_codes(cfg, n, K=r + 3) for n in range(3)]
     out = oracle.hosvd(x, (r,) * 3, oms, q=0, kind="count")
     assert out["E"] < 1e-10
+
+
+# --------------------------------------------------------- P18 (slab-wise oracle)
+@pytest.mark.parametrize("dims,ranks,K,q,slab", [((14, 12, 11), (3, 4, 2), (6, 7, 5), 0, 4),
+                                                 ((14, 12, 11), (3, 4, 2), (6, 7, 5), 1, 5),
+                                                 ((9, 8, 7, 10), (2, 3, 2, 3), (4, 5, 4, 5), 2, 3),
+                                                 ((13, 15), (3, 4), (5, 6), 1, 4)])
+def test_P18_slabwise_oracle_equals_oracle_hosvd(dims, ranks, K, q, slab):
+    """P18: oracle.slabbed.hosvd_slabs (the cfg5-size evaluation of the oracle, tests/
+    test_gpu_fullsize.py) splits every sum over the last mode into slab partial sums -- a
+    reassociation only, so it equals oracle.hosvd to rounding on any input (ragged last slab)."""
+    from oracle.slabbed import hosvd_slabs
+    rng = _rng(18)
+    x, _, _ = _low_rank(rng, dims, ranks, noise=0.2)
+    oms = _omegas(rng, dims, K)
+    got = hosvd_slabs(np.asfortranarray(x.astype(np.float32)).astype(np.float64), ranks, oms, q=q, slab=slab)
+    ref = oracle.hosvd(np.asfortranarray(x.astype(np.float32)).astype(np.float64), ranks, oms, q=q)
+    for n in range(len(dims)):
+        np.testing.assert_allclose(got["Y0"][n], ref["Y0"][n], rtol=0, atol=1e-12 * np.abs(ref["Y0"][n]).max())
+        np.testing.assert_allclose(got["Qt"][n], ref["Qt"][n], rtol=0, atol=1e-11)
+        np.testing.assert_allclose(got["Q"][n], ref["Q"][n], rtol=0, atol=1e-11)
+    np.testing.assert_allclose(got["G"], ref["G"], rtol=0, atol=1e-11 * np.abs(ref["G"]).max())
+    assert abs(got["E"] - ref["E"]) <= 1e-12 * ref["E"]
+    assert abs(got["E_gram"] - ref["E_gram"]) <= 1e-10
