@@ -88,7 +88,7 @@ class Engine {
   // slab partial sums are allreduced when the last mode is contracted
   template <typename T>
   void multi_ttm_skip(const TView& X, const T* data, const double* const* Q, const int64_t* ldq, const int64_t* C,
-                      int skip, double* out, const bool* ortho = nullptr);
+                      int skip, double* out);
 
  private:
   void canon(double* Qn, int64_t m, int r, int64_t ld, int64_t row0, bool dist_rows, double* U, int ku);

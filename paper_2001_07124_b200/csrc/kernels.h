@@ -63,6 +63,9 @@ void x_scale_from_amax(const Ctx& ctx, const unsigned int* amax, int64_t n, floa
 // distributed form: every rank's stats as a (max, sum) double pair (x_stat_pair), allgathered
 void x_stat_pair(const Ctx& ctx, const unsigned int* amax, double* pair);
 void x_scale_from_gathered(const Ctx& ctx, const double* pairs, int nranks, int64_t n_glob, float* s);
+// out = xs with out[0] = 0 unless max|Q| < 2 (Q fp32 col-major m x r, ld): the fp16 split of an X pass
+// with Q (2^14 Q must stay inside the fp16 range) then stands down for its tf32 twin
+void q_gate_scale(const Ctx& ctx, const float* Q, int64_t m, int r, int64_t ld, const float* xs, float* out);
 // max |X| and sum |x| of n elements into stat (16 bytes, zeroed here): one streaming pass
 void x_absmax_stats(const Ctx& ctx, Arena& ws, const float* X, int64_t n, unsigned int* stat);
 // whether ttm_s_tc would run (same shape/alignment rules, no launch)

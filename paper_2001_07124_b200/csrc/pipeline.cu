@@ -805,12 +805,12 @@ void Engine::pet(const TView& X, const int64_t* R, const void* const* omega, con
 // Reading R25: every stage accumulates in fp64 (CUDA cores) with fp64 intermediates and the fp64
 // factors as stored.  W = S_(n) Omega^(n) has no oversampling, so span(W) is conditioned by
 // kappa(W) ~ 1e1-1e2 and the fp32-accumulated tensor-core chain moved E by ~2e-5 on cfg2-small.
-// ortho (nullable = all): which Q_p this call produced by a QR (orthonormal, |q| <= 1).  The fp16
-// split of the X pass scales Q by 2^14 and needs |q| < 4 (R29): a caller's start factor (Alg.7 allows
-// a random Gaussian one) takes the 3xTF32 form instead.
+// The fp16 split of the X pass scales Q by 2^14 and needs |q| < 4 (R29): the launch is gated on the
+// device by max|Q| < 2 as well as by X's scale (qgate), so a caller's wide start factor (Alg.7
+// allows a random Gaussian one) sends the work to the 3xTF32 twin.
 template <typename T>
 void Engine::multi_ttm_skip(const TView& X, const T* data, const double* const* Q, const int64_t* ldq,
-                            const int64_t* C, int skip, double* out, const bool* ortho) {
+                            const int64_t* C, int skip, double* out) {
   const int N = X.N;
   const auto mk = ws.mark();
   int ps[5], np_ = 0;
@@ -830,9 +830,12 @@ void Engine::multi_ttm_skip(const TView& X, const T* data, const double* const* 
         int64_t ldt;
         const float* qt = working_copy<float>(ctx, ws, Q[p], cur[p], C[p], ldq[p], ldt);
         float* d32 = ws.alloc_n<float>(b.a * C[p] * b.b);
-        const bool q_ok = ortho == nullptr || ortho[p];
-        const float* xsc =
-            (ctx.tc_h16 && xs_slot && q_ok) ? x_scale(data, X.size(), X.size() / X.d[N - 1] * X.glob) : nullptr;
+        const float* xsc = nullptr;
+        if (ctx.tc_h16 && xs_slot) {
+          float* xq = ws.alloc_n<float>(2);
+          q_gate_scale(ctx, qt, cur[p], int(C[p]), ldt, x_scale(data, X.size(), X.size() / X.d[N - 1] * X.glob), xq);
+          xsc = xq;
+        }
         LabelScope ls(ctx, "hooi_first");
         if (ttm_t_tc(ctx, ws, data, b, qt, ldt, int(C[p]), d32, 1, b.a, b.a * C[p], 0, false, xsc)) {
           convert2d<float, double>(ctx, d32, b.a * C[p] * b.b, 1, b.a * C[p] * b.b, dst, b.a * C[p] * b.b);
@@ -867,7 +870,6 @@ void Engine::rp_hooi(const TView& X, const int64_t* R, int sweeps, const double*
   xs_slot = ws.alloc_n<float>(2);      // X's fp16 scale (one max|X| pass), shared by all S chains and the core
   xs_key = nullptr;
   int64_t ldq[5];
-  bool ortho[5] = {false, false, false, false, false};   // Q_out[n] produced by this call's QR yet
   for (int n = 0; n < N; ++n) {
     ldq[n] = X.d[n];
     if (Q_out[n] != Q_init[n])
@@ -882,14 +884,13 @@ void Engine::rp_hooi(const TView& X, const int64_t* R, int sweeps, const double*
       int64_t sz = 1;
       for (int k = 0; k < N; ++k) sz *= cur[k];
       double* S = ws.alloc_n<double>(sz);
-      multi_ttm_skip<T>(X, data, Q_out, ldq, R, n, S, ortho);                            // line 4
+      multi_ttm_skip<T>(X, data, Q_out, ldq, R, n, S);                                   // line 4
       const int64_t In = X.d[n];
       double* W = ws.alloc_n<double>(In * R[n]);
       ttm_s<double>(ctx, ws, S, TView::box_of(cur, N, n), omega[it * N + n], omega_ld[it * N + n], 1, int(R[n]), W,
                     In);                                                                  // line 5
       const bool last = (n == N - 1);
       qr_y(W, In, X.Ig(n), int(R[n]), In, Q_out[n], In, nullptr, last && dist(), last ? X.off : 0);   // line 6
-      ortho[n] = true;
       ws.rewind(ms);
     }
   }

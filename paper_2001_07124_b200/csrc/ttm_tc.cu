@@ -1274,6 +1274,21 @@ bool ttm_s_tc_ok(const Ctx& ctx, const float* X, Box box, int K) {
 void x_scale_from_amax(const Ctx& ctx, const unsigned int* amax, int64_t n, float* s) {
   launch(ctx, "xscale", [&] { xscale_kernel<<<1, 1, 0, ctx.stream>>>(amax, double(n), s, ctx.tc_h16 == 2); });
 }
+__global__ void __launch_bounds__(256) q_gate_kernel(const float* __restrict__ Q, int64_t m, int r, int64_t ld,
+                                                     const float* __restrict__ xs, float* __restrict__ out) {
+  __shared__ int wide;
+  if (threadIdx.x == 0) wide = 0;
+  __syncthreads();
+  for (int64_t e = threadIdx.x; e < m * r; e += blockDim.x) {
+    const float v = Q[(e % m) + ld * (e / m)];
+    if (!(fabsf(v) < 2.f)) wide = 1;                  // benign race: any writer stores 1
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) { out[0] = wide ? 0.f : xs[0]; out[1] = xs[1]; }
+}
+void q_gate_scale(const Ctx& ctx, const float* Q, int64_t m, int r, int64_t ld, const float* xs, float* out) {
+  launch(ctx, "q_gate", [&] { q_gate_kernel<<<1, 256, 0, ctx.stream>>>(Q, m, r, ld, xs, out); });
+}
 void x_stat_pair(const Ctx& ctx, const unsigned int* amax, double* pair) {
   launch(ctx, "xstat_pair", [&] { stat_pair_kernel<<<1, 1, 0, ctx.stream>>>(amax, pair); });
 }

@@ -103,9 +103,10 @@ def test_rp_hooi_parity(P, h, h64, name, strict):
 @pytest.mark.parametrize("strict", [False, True])
 def test_rp_hooi_gaussian_start(P, h, h64, strict):
     """Alg.7 line 1 allows a random start: unnormalized Gaussian Q_init (entries |q| >= 4 occur,
-    outside the fp16 split's range once scaled by 2^14).  A caller's start factor takes the 3xTF32
-    X pass (R29 applies only to factors this call orthonormalized); parity with the oracle from the
-    same start."""
+    outside the fp16 split's range once scaled by 2^14).  The fp16-split X pass is gated on the
+    device by max|Q| < 2 as well as X's scale, so the wide start factors send sweep 0's first
+    stages to the 3xTF32 twin (the run counters show both kinds ran); parity with the oracle from
+    the same start."""
     cfg = synth.CONFIGS["cfg2"].scaled((150, 140, 130), (12, 12, 12), (12, 12, 12))
     x = synth.make_tensor(cfg)
     q0 = [synth.rng_for(4242, 7, n).standard_normal((cfg.dims[n], cfg.ranks[n])) * 3.0 for n in range(3)]
@@ -113,8 +114,12 @@ def test_rp_hooi_gaussian_start(P, h, h64, strict):
     oms = synth.hooi_omegas(cfg, 2)
     ref = oracle.rp_hooi(x, cfg.ranks, q0, oms)
     hh = h64 if strict else h
+    hh.profile_read()
     res = P.rtucker_rp_hooi(hh, _dev(x), cfg.ranks, [_t(q) for q in q0], [[_t(o) for o in s] for s in oms])
     hh.sync()
+    runs = {n: c for n, c, _ in hh.profile_read()[0] if n in ("h16_ran", "tf32_twin_ran")}
+    if not strict:
+        assert runs.get("tf32_twin_ran", 0) >= 1 and runs.get("h16_ran", 0) >= 1, runs
     assert all(np.isfinite(q.cpu().numpy()).all() for q in res["Q"])
     _check(P, res, ref, strict=strict)
 
