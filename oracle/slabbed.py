@@ -20,6 +20,9 @@ this module against ``oracle.hosvd``):
 """
 from __future__ import annotations
 
+import os
+import sys
+import time
 from typing import Sequence
 
 import numpy as np
@@ -41,6 +44,15 @@ def hosvd_slabs(x: np.ndarray, ranks: Sequence[int], omegas, q: int = 0, slab: i
     dims = x.shape
     last = dims[-1]
     sl = _slabs(last, slab)
+    # middle modes 0 < n < N-1: single-index slabs, whose unfolding of an F-ordered x is a strided
+    # view (no copy of the slab per product); the first and last modes take the wide slabs
+    sl1 = _slabs(last, 1)
+    verbose = bool(os.environ.get("RT_ORACLE_VERBOSE"))
+    t0 = time.perf_counter()
+
+    def tick(what):
+        if verbose:
+            print(f"[hosvd_slabs] {what}: {time.perf_counter() - t0:.1f} s", file=sys.stderr, flush=True)
 
     def xs_of(k0, k1):
         return np.asarray(x[..., k0:k1], dtype=np.float64)
@@ -55,14 +67,17 @@ def hosvd_slabs(x: np.ndarray, ranks: Sequence[int], omegas, q: int = 0, slab: i
         return _zero_result(dims, ranks)
     omegas = [np.asarray(o, dtype=np.float64) for o in omegas]
 
+    def slabs_for(n):
+        return sl1 if 0 < n < N - 1 else sl
+
     def x_times(n, b):                       # X_(n) B
         if n < N - 1:
-            return sum(unfold(xs_of(k0, k1), n) @ b[rows(n, k0, k1)] for k0, k1 in sl)
+            return sum(unfold(xs_of(k0, k1), n) @ b[rows(n, k0, k1)] for k0, k1 in slabs_for(n))
         return np.concatenate([unfold(xs_of(k0, k1), n) @ b for k0, k1 in sl], axis=0)
 
     def xt_times(n, qm):                     # X_(n)^T Q
         if n < N - 1:
-            return np.concatenate([unfold(xs_of(k0, k1), n).T @ qm for k0, k1 in sl], axis=0)
+            return np.concatenate([unfold(xs_of(k0, k1), n).T @ qm for k0, k1 in slabs_for(n)], axis=0)
         return sum(unfold(xs_of(k0, k1), n).T @ qm[k0:k1] for k0, k1 in sl)
 
     y0s, qts = [], []
@@ -78,11 +93,14 @@ def hosvd_slabs(x: np.ndarray, ranks: Sequence[int], omegas, q: int = 0, slab: i
         qt, _ = qr_plus(y)                   # Alg.6 line 4
         y0s.append(y0)
         qts.append(qt)
+        tick(f"mode {n} sketch + {q} power iterations + QR")
     gt = sum(core(xs_of(k0, k1), qts[:-1] + [qts[-1][k0:k1]]) for k0, k1 in sl)   # line 5
+    tick("core")
     g, qs = truncate_hosvd(gt, qts, ranks)                                        # reading R1
     out = dict(Q=qs, G=g, Qt=qts, Gt=gt, Y0=y0s)
     if with_error:
         res2 = sum(fro(xs_of(k0, k1) - reconstruct(g, qs[:-1] + [qs[-1][k0:k1]])) ** 2 for k0, k1 in sl)
+        tick("residual")
         out["E"] = float(np.sqrt(res2 / nx2))
         out["E_gram"] = rel_error_gram(np.array([np.sqrt(nx2)]), g)   # only ||X|| enters the identity
     return out

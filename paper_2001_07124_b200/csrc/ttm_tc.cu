@@ -66,7 +66,16 @@ constexpr int sketch_cps() {
   return (512 - abase) / 128 >= 2 ? 2 : 1;
 }
 
-template <int NPAD, bool BSPLIT, bool BMN, int CPS_ = 1, uint32_t OUTB = 0>
+// X stage geometry.  XW = 1: one chunk per stage, the [BM rows][KC] tile with the 128 B swizzle
+// (one 128 B piece of every X row per TMA box).  XW > 1 ("wide rows", strided modes n > 0): XW
+// chunks per stage in one unswizzled box of BM rows x (KC XW + 4) elements, so every X row is read
+// as one contiguous (KC XW + 4) x 4 B run (512 B + 16 at XW = 4; the 16 B overlap with the next
+// stage is never used).  The 4-element pad makes the row pitch 4 words mod 32: the splitters' 16 B
+// row reads hit 8 distinct bank groups per warp (4 wavefronts, the minimum for 512 B).
+template <int XW>
+constexpr uint32_t x_pitch() { return XW == 1 ? uint32_t(KC) * 4u : uint32_t(KC * XW + 4) * 4u; }
+
+template <int NPAD, bool BSPLIT, bool BMN, int CPS_ = 1, uint32_t OUTB = 0, int XW = 1>
 struct Plan {
   // CPS chunks (of KC contraction elements) per pipeline stage: one ready wait, one commit and
   // one A slot of 64 CPS columns per stage -- the issuer warps' per-stage overhead (barrier wait,
@@ -83,28 +92,31 @@ struct Plan {
   static constexpr uint32_t acc_cols = BSPLIT ? uint32_t(NH + 2 * NPAD) : uint32_t(NI * NPAD);
   static constexpr uint32_t a_base = (acc_cols + 63u) & ~63u;
   static constexpr int NB_fit = int((512u - a_base) / (64u * CPS));
-  static constexpr int NB = NB_fit > 6 ? 6 : NB_fit;   // stages in the TMEM A ring
-  static_assert(NB >= 2, "TMEM plan leaves fewer than two A stages");
+  // wide X stages: leave room for two of them in shared memory
+  static constexpr int NB_smem = XW == 1 ? 6 : int((224u * 1024u - 2u * BM * x_pitch<XW>() - OUTB) / (CPS * (BSPLIT ? 2u : 1u) * kB));
+  static constexpr int NB = NB_fit < NB_smem ? (NB_fit > 6 ? 6 : NB_fit) : (NB_smem > 6 ? 6 : NB_smem);   // A ring stages
   static_assert(!BSPLIT || NH + NPAD <= 256, "concatenated B operand wider than 256");
   __host__ __device__ static constexpr uint32_t acc(int q, int b) {
     return BSPLIT ? (q == 0 ? 0u : uint32_t(NH + NPAD)) : uint32_t((NBUF * q + b) * NPAD);
   }
   __host__ __device__ static constexpr uint32_t a_slot(int s) { return a_base + 64u * CPS * uint32_t(s); }
   // shared memory
-  static constexpr uint32_t kX = uint32_t(BM) * KC * 4;
+  static constexpr uint32_t kX = uint32_t(BM) * x_pitch<XW>();   // one X stage (XW chunks)
   static constexpr uint32_t budget = 224u * 1024u;
   // One stage = one A slot + one B slot, released together by a single tcgen05.commit per issuer
   // (every commit stalls the issuing warp's MMA stream, so there is one per stage).
   static constexpr int NBS = NB * CPS;                  // B slots (one per chunk)
   static constexpr int NX_fit = int((budget - NBS * kBS - OUTB) / kX);
   static constexpr int NX = NX_fit > 10 ? 10 : NX_fit;
+  static_assert(kX % 1024 == 0, "X stages keep the 1 KB alignment of the swizzled B slots");
   static constexpr uint32_t off_x = 0;
   static constexpr uint32_t off_b = off_x + NX * kX;
   static constexpr uint32_t off_o = off_b + NBS * kBS;  // output staging (1024-aligned), OUTB bytes
   static constexpr uint32_t off_bar = off_o + OUTB;
   static constexpr int nbar = 2 * NX + 2 * NBS + 2 * 8 + 4;
   static constexpr uint32_t bytes = off_bar + 8 * nbar + 16;
-  static_assert(NX >= 4, "X ring too shallow");
+  // feasible plan (checked by the kernels; the host picks a feasible X stage width)
+  static constexpr bool ok = NB >= 2 && NX >= (XW == 1 ? 4 : 2);
 };
 
 struct Bars {
@@ -184,6 +196,30 @@ __device__ __forceinline__ void split_row_to_tmem(const float* xs, int r, uint32
     }
   }
   // all smem reads of the X stage are done once the values are in registers
+  tmem_st16(t_hi, *reinterpret_cast<const uint32_t(*)[16]>(&hi[0]));
+  tmem_st16(t_hi + 16, *reinterpret_cast<const uint32_t(*)[16]>(&hi[16]));
+  tmem_st16(t_hi + 32, *reinterpret_cast<const uint32_t(*)[16]>(&lo[0]));
+  tmem_st16(t_hi + 48, *reinterpret_cast<const uint32_t(*)[16]>(&lo[16]));
+}
+
+// Wide-row X stage (XW > 1): this thread's row is contiguous (pitch x_pitch<XW>, 4 words mod 32:
+// conflict-free 16 B reads); `row` points at the chunk's 32 elements.
+template <bool AMAX = false>
+__device__ __forceinline__ void split_wrow_to_tmem(const float* row, uint32_t t_hi, float* m = nullptr,
+                                                   float* sq = nullptr) {
+  uint32_t hi[32], lo[32];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const float4 v = *reinterpret_cast<const float4*>(row + 4 * c);
+    if (AMAX) {
+      *m = fmaxf(fmaxf(*m, fmaxf(fabsf(v.x), fabsf(v.y))), fmaxf(fabsf(v.z), fabsf(v.w)));
+      *sq += (fabsf(v.x) + fabsf(v.y)) + (fabsf(v.z) + fabsf(v.w));
+    }
+    split_tf32(v.x, hi[4 * c + 0], lo[4 * c + 0]);
+    split_tf32(v.y, hi[4 * c + 1], lo[4 * c + 1]);
+    split_tf32(v.z, hi[4 * c + 2], lo[4 * c + 2]);
+    split_tf32(v.w, hi[4 * c + 3], lo[4 * c + 3]);
+  }
   tmem_st16(t_hi, *reinterpret_cast<const uint32_t(*)[16]>(&hi[0]));
   tmem_st16(t_hi + 16, *reinterpret_cast<const uint32_t(*)[16]>(&hi[16]));
   tmem_st16(t_hi + 32, *reinterpret_cast<const uint32_t(*)[16]>(&lo[0]));
@@ -303,6 +339,7 @@ struct SParams {
   int K;
   int64_t cpb;        // chunks per beta (a > 1)
   int64_t nchunks;    // total j-chunks
+  int64_t per;        // chunks per split (a multiple of the X stage width)
   int seg;            // chunks per accumulator segment
   int ablate;         // profiling only: 1 = no MMA, 2 = no split work (results invalid)
   int skew;           // chunk-order rotation per M-tile (decorrelates the rows' DRAM addresses)
@@ -361,13 +398,17 @@ __device__ __forceinline__ void chunk_coords(const SParams& p, int64_t c, int64_
 // rows) run in the same wave and in near lockstep: B comes from DRAM once and from L2 for the rest.
 // BPRE (with BSPLIT): B is pre-split in global memory, row j = [hi (NH columns) | lo (NH columns)],
 // and is loaded as the whole [B_hi | B_lo] slot; nothing is split in the kernel.
-template <int NPAD, bool BSPLIT, bool AMN, bool BPRE>
+// XW > 1: wide-row X stages (see x_pitch), strided modes only; the CTA's chunk range is a multiple
+// of XW chunks within one beta (the host checks a % (KC XW) == 0).
+template <int NPAD, bool BSPLIT, bool AMN, bool BPRE, int XW = 1>
 __global__ void __launch_bounds__(NT_TTM, 1)
 ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb, const SParams p) {
   static_assert(!BPRE || BSPLIT, "pre-split B implies the split product form");
+  static_assert(XW == 1 || !AMN, "wide X rows are for the strided modes");
   if (p.gate && *p.gate != 0.f) return;                // fp16-split launch in charge (R29)
   if (p.gate && p.runs && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) atomicAdd(&p.runs[1], 1u);
-  using L = Plan<NPAD, BSPLIT, true, sketch_cps<NPAD, BSPLIT, true>()>;
+  using L = Plan<NPAD, BSPLIT, true, sketch_cps<NPAD, BSPLIT, true>(), 0, XW>;
+  static_assert(L::ok, "infeasible TMEM / shared-memory plan");
   constexpr int NX = L::NX, CPS = L::CPS, NB = L::NB;
   extern __shared__ __align__(1024) uint8_t smem[];
   const Bars b = bars_of<L>(smem);
@@ -376,11 +417,12 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
   const int64_t i0 = int64_t(blockIdx.x) * BM;
   // contiguous chunk range per split: consecutive TMA boxes of a CTA continue the same rows, which
   // keeps DRAM pages (and 256 B L2 promotions) useful on the strided last-mode rows
-  const int64_t per = (p.nchunks + S - 1) / S;
+  const int64_t per = p.per;                           // contiguous chunks per split (host)
+  (void)S;
   const int64_t cbeg = z * per;
   const int nch = cbeg < p.nchunks ? int(min(per, p.nchunks - cbeg)) : 0;
   const int nst = (nch + CPS - 1) / CPS;               // stages
-  const int rot = nch ? int((int64_t(blockIdx.x) * p.skew) % nch) : 0;
+  const int rot = (nch && XW == 1) ? int((int64_t(blockIdx.x) * p.skew) % nch) : 0;
   auto chunk_of = [&](int it) { int c = it + rot; return cbeg + (c >= nch ? c - nch : c); };
   // stage g -> ring slot and round parity
   auto st_slot = [](int g) { return g % NB; };
@@ -398,11 +440,12 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
   const uint32_t tmem = *b.tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {                                   // ---------------- X producer
+    if (lane == 0) {                                   // ---------------- X producer (one box per XW chunks)
       Ring rx;
       const uint64_t pol = policy_evict_first();
-      for (int it = 0; it < nch; ++it, rx.next<NX>()) {
-        if (it >= NX) RT_TIMED(p.tim, 0, mbar_wait(&b.x_free[rx.s], rx.ph ^ 1));
+      int xi = 0;
+      for (int it = 0; it < nch; it += XW, ++xi, rx.next<NX>()) {
+        if (xi >= NX) RT_TIMED(p.tim, 0, mbar_wait(&b.x_free[rx.s], rx.ph ^ 1));
         int64_t a0, beta, j0;
         chunk_coords<AMN>(p, chunk_of(it), a0, beta, j0);
         mbar_expect_tx(&b.x_full[rx.s], L::kX);
@@ -465,20 +508,26 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
     unsigned long long* tim = (warp == 2) ? p.tim : nullptr;   // warp-uniform (aligned tcgen05 ops inside)
     float xmax = 0.f, xsq = 0.f;
     Ring rx;
-    for (int it = 0; it < nch; ++it, rx.next<NX>()) {
+    for (int it = 0; it < nch; ++it) {
       const int g = it / CPS, c = it % CPS, sl = st_slot(g), bs = it % L::NBS;
-      RT_TIMED(tim, 10, mbar_wait(&b.x_full[rx.s], rx.ph));
+      const int cx = XW == 1 ? 0 : it % XW;             // chunk within the X stage
+      if (cx == 0) RT_TIMED(tim, 10, mbar_wait(&b.x_full[rx.s], rx.ph));
       if (c == 0 && g >= NB) RT_TIMED(tim, 11, mbar_wait(&b.tfree[sl], st_par(g) ^ 1));   // stage's TMEM slot free
       RT_TIMED(tim, 12, {
         const float* xs = reinterpret_cast<const float*>(smem + L::off_x + rx.s * L::kX);
+        const uint32_t ta = lane_base + L::a_slot(sl) + 64u * c;
         if (p.ablate == 2) {
+        } else if constexpr (XW > 1) {
+          const float* row = xs + r * (KC * XW + 4) + KC * cx;
+          if (p.amax) split_wrow_to_tmem<true>(row, ta, &xmax, &xsq);
+          else split_wrow_to_tmem(row, ta);
         } else if (p.amax) {
-          split_row_to_tmem<AMN, true>(xs, r, lane_base + L::a_slot(sl) + 64u * c, &xmax, &xsq);
+          split_row_to_tmem<AMN, true>(xs, r, ta, &xmax, &xsq);
         } else {
-          split_row_to_tmem<AMN>(xs, r, lane_base + L::a_slot(sl) + 64u * c);
+          split_row_to_tmem<AMN>(xs, r, ta);
         }
       });
-      mbar_arrive(&b.x_free[rx.s]);
+      if (cx == XW - 1 || it == nch - 1) { mbar_arrive(&b.x_free[rx.s]); rx.next<NX>(); }
       RT_TIMED(tim, 13, mbar_wait(&b.b_full[bs], uint32_t(it / L::NBS) & 1u));
       if (BSPLIT && !BPRE) {
         float* bsp = reinterpret_cast<float*>(smem + L::off_b + bs * L::kBS);
@@ -529,7 +578,7 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
 // J = 2048^2), whose lo parts would otherwise fall into the fp16 subnormals (11 bits lost)
 constexpr float kQScale = 16384.f;
 
-template <int NPAD, int CPS_ = 2, uint32_t OUTB = 0>
+template <int NPAD, int CPS_ = 2, uint32_t OUTB = 0, int XW = 1>
 struct PlanH {
   static constexpr int CPS = CPS_;
   static constexpr int NH = NPAD;                        // D0 = [hi block | lo block]
@@ -541,12 +590,12 @@ struct PlanH {
   static constexpr uint32_t acc_cols = 3u * NPAD;
   static constexpr uint32_t a_base = (acc_cols + 63u) & ~63u;
   static constexpr int NB_fit = int((512u - a_base) / (32u * CPS));
-  static constexpr int NB = NB_fit > 6 ? 6 : NB_fit;
-  static_assert(NB >= 2, "TMEM plan leaves fewer than two A stages");
+  static constexpr int NB_smem = XW == 1 ? 6 : int((224u * 1024u - 2u * BM * x_pitch<XW>() - OUTB) / (CPS * kB));
+  static constexpr int NB = NB_fit < NB_smem ? (NB_fit > 6 ? 6 : NB_fit) : (NB_smem > 6 ? 6 : NB_smem);
   static_assert(2 * NPAD <= 256 && NPAD % 16 == 0, "f16 operand shape");
   __host__ __device__ static constexpr uint32_t acc(int q, int) { return q == 0 ? 0u : uint32_t(2 * NPAD); }
   __host__ __device__ static constexpr uint32_t a_slot(int s) { return a_base + 32u * CPS * uint32_t(s); }
-  static constexpr uint32_t kX = uint32_t(BM) * KC * 4;
+  static constexpr uint32_t kX = uint32_t(BM) * x_pitch<XW>();   // one X stage (XW chunks)
   static constexpr uint32_t budget = 224u * 1024u;
   static constexpr int NBS = NB * CPS;
   static constexpr int NX_fit = int((budget - NBS * kBS - OUTB) / kX);
@@ -557,8 +606,9 @@ struct PlanH {
   static constexpr uint32_t off_bar = off_o + OUTB;
   static constexpr int nbar = 2 * NX + 2 * NBS + 2 * 8 + 4;
   static constexpr uint32_t bytes = off_bar + 8 * nbar + 16;
-  static_assert(NX >= 4, "X ring too shallow");
+  static_assert(kX % 1024 == 0, "X stages keep the 1 KB alignment of the swizzled B slots");
   static_assert(NB <= 8 && NBS <= 16, "barrier plan");
+  static constexpr bool ok = NB >= 2 && NX >= (XW == 1 ? 4 : 2);
 };
 
 // MN-major fp16 SWIZZLE_128B operand (tools/f16_probe.cu): atoms of 8 k-rows x 128 B (64 n);
@@ -590,15 +640,31 @@ __device__ __forceinline__ void split_row_to_tmem_h16(const float* xs, int r, fl
   tmem_st16(t_hi + 16, lo);
 }
 
+__device__ __forceinline__ void split_wrow_to_tmem_h16(const float* row, float s, uint32_t t_hi) {
+  float v[32];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const float4 w = *reinterpret_cast<const float4*>(row + 4 * c);
+    v[4 * c + 0] = w.x * s; v[4 * c + 1] = w.y * s; v[4 * c + 2] = w.z * s; v[4 * c + 3] = w.w * s;
+  }
+  uint32_t hi[16], lo[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) split_h16x2(v[2 * c], v[2 * c + 1], hi[c], lo[c]);
+  tmem_st16(t_hi, hi);
+  tmem_st16(t_hi + 16, lo);
+}
+
 struct HParams {
   SParams s;
   const float* xscale;   // device: s (a power of two)
 };
 
-template <int NPAD, bool AMN, int CPS_ = 2>
+template <int NPAD, bool AMN, int CPS_ = 2, int XW = 1>
 __global__ void __launch_bounds__(NT_TTM, 1)
 ttm_s_h16_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb, const HParams hp) {
-  using L = PlanH<NPAD, CPS_>;
+  static_assert(XW == 1 || !AMN, "wide X rows are for the strided modes");
+  using L = PlanH<NPAD, CPS_, 0, XW>;
+  static_assert(L::ok, "infeasible TMEM / shared-memory plan");
   const SParams& p = hp.s;
   if (*hp.xscale == 0.f) return;                       // dynamic range too wide: the tf32 launch runs
   if (p.runs && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) atomicAdd(&p.runs[0], 1u);
@@ -608,11 +674,12 @@ ttm_s_h16_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant_
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t z = blockIdx.y, S = gridDim.y;
   const int64_t i0 = int64_t(blockIdx.x) * BM;
-  const int64_t per = (p.nchunks + S - 1) / S;
+  const int64_t per = p.per;                           // contiguous chunks per split (host)
+  (void)S;
   const int64_t cbeg = z * per;
   const int nch = cbeg < p.nchunks ? int(min(per, p.nchunks - cbeg)) : 0;
   const int nst = (nch + CPS - 1) / CPS;
-  const int rot = nch ? int((int64_t(blockIdx.x) * p.skew) % nch) : 0;
+  const int rot = (nch && XW == 1) ? int((int64_t(blockIdx.x) * p.skew) % nch) : 0;
   auto chunk_of = [&](int it) { int c = it + rot; return cbeg + (c >= nch ? c - nch : c); };
   auto st_slot = [](int g) { return g % NB; };
   auto st_par = [](int g) { return uint32_t(g / NB) & 1u; };
@@ -629,11 +696,12 @@ ttm_s_h16_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant_
   const uint32_t tmem = *b.tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {                                   // ---------------- X producer
+    if (lane == 0) {                                   // ---------------- X producer (one box per XW chunks)
       Ring rx;
       const uint64_t pol = policy_evict_first();
-      for (int it = 0; it < nch; ++it, rx.next<NX>()) {
-        if (it >= NX) mbar_wait(&b.x_free[rx.s], rx.ph ^ 1);
+      int xi = 0;
+      for (int it = 0; it < nch; it += XW, ++xi, rx.next<NX>()) {
+        if (xi >= NX) mbar_wait(&b.x_free[rx.s], rx.ph ^ 1);
         int64_t a0, beta, j0;
         chunk_coords<AMN>(p, chunk_of(it), a0, beta, j0);
         mbar_expect_tx(&b.x_full[rx.s], L::kX);
@@ -691,13 +759,17 @@ ttm_s_h16_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant_
     const uint32_t lane_base = tmem + (uint32_t(32 * q4) << 16);
     const float sc = *hp.xscale;
     Ring rx;
-    for (int it = 0; it < nch; ++it, rx.next<NX>()) {
+    for (int it = 0; it < nch; ++it) {
       const int g = it / CPS, c = it % CPS, sl = st_slot(g), bs = it % L::NBS;
-      mbar_wait(&b.x_full[rx.s], rx.ph);
+      const int cx = XW == 1 ? 0 : it % XW;             // chunk within the X stage
+      if (cx == 0) mbar_wait(&b.x_full[rx.s], rx.ph);
       if (c == 0 && g >= NB) mbar_wait(&b.tfree[sl], st_par(g) ^ 1);   // stage's TMEM slot free
-      split_row_to_tmem_h16<AMN>(reinterpret_cast<const float*>(smem + L::off_x + rx.s * L::kX), r, sc,
-                                 lane_base + L::a_slot(sl) + 32u * c);
-      mbar_arrive(&b.x_free[rx.s]);
+      const float* xs = reinterpret_cast<const float*>(smem + L::off_x + rx.s * L::kX);
+      if constexpr (XW > 1)
+        split_wrow_to_tmem_h16(xs + r * (KC * XW + 4) + KC * cx, sc, lane_base + L::a_slot(sl) + 32u * c);
+      else
+        split_row_to_tmem_h16<AMN>(xs, r, sc, lane_base + L::a_slot(sl) + 32u * c);
+      if (cx == XW - 1 || it == nch - 1) { mbar_arrive(&b.x_free[rx.s]); rx.next<NX>(); }
       if (c == CPS - 1 || it == nch - 1) {             // stage complete (B landed too)
         mbar_wait(&b.b_full[bs], uint32_t(it / L::NBS) & 1u);
         if (c == 1) mbar_wait(&b.b_full[bs - 1], uint32_t((it - 1) / L::NBS) & 1u);
@@ -826,6 +898,7 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
   if (H16 ? (*p.xscale == 0.f) : (p.gate != nullptr && *p.gate != 0.f)) return;   // one of the pair runs (R29)
   if ((H16 || p.gate != nullptr) && p.runs && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&p.runs[H16 ? 0 : 1], 1u);
   using L = std::conditional_t<H16, PlanH<NPAD, 1, t_outb<NPAD>()>, Plan<NPAD, BSPLIT, false, 1, t_outb<NPAD>()>>;
+  static_assert(L::ok, "infeasible TMEM / shared-memory plan");
   constexpr int NX = L::NX;
   extern __shared__ __align__(1024) uint8_t smem[];
   const Bars b = bars_of<L>(smem);
@@ -1135,37 +1208,69 @@ void set_smem(Kern kernel, uint32_t bytes) {
   RT_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
 }
 
-template <int NPAD, bool BSPLIT, bool AMN, bool BPRE>
+template <int NPAD, bool BSPLIT, bool AMN, bool BPRE, int XW = 1>
 void launch_s(const Ctx& ctx, const CUtensorMap& tx, const CUtensorMap& tb, const SParams& p, dim3 grid) {
-  using L = Plan<NPAD, BSPLIT, true, sketch_cps<NPAD, BSPLIT, true>()>;
+  using L = Plan<NPAD, BSPLIT, true, sketch_cps<NPAD, BSPLIT, true>(), 0, XW>;
   static bool attr = false;
-  if (!attr) { set_smem(ttm_s_tc_kernel<NPAD, BSPLIT, AMN, BPRE>, L::bytes); attr = true; }
+  if (!attr) { set_smem(ttm_s_tc_kernel<NPAD, BSPLIT, AMN, BPRE, XW>, L::bytes); attr = true; }
   launch(ctx, ctx.label ? ctx.label : "ttm_s_tc", [&] {
-    ttm_s_tc_kernel<NPAD, BSPLIT, AMN, BPRE><<<grid, NT_TTM, L::bytes, ctx.stream>>>(tx, tb, p);
+    ttm_s_tc_kernel<NPAD, BSPLIT, AMN, BPRE, XW><<<grid, NT_TTM, L::bytes, ctx.stream>>>(tx, tb, p);
   });
 }
 
-// b: 0 tf32-exact B, 1 split in the kernel, 2 pre-split in global memory
+// widest feasible X stage width <= want for the strided-mode sketch kernels of this shape
 template <int NPAD>
-void dispatch_s(const Ctx& ctx, bool amn, int bmode, const CUtensorMap& tx, const CUtensorMap& tb, const SParams& p,
-                dim3 g) {
-  if (bmode == 0) { if (amn) launch_s<NPAD, false, true, false>(ctx, tx, tb, p, g); else launch_s<NPAD, false, false, false>(ctx, tx, tb, p, g); }
-  else if (bmode == 1) { if (amn) launch_s<NPAD, true, true, false>(ctx, tx, tb, p, g); else launch_s<NPAD, true, false, false>(ctx, tx, tb, p, g); }
-  else { if (amn) launch_s<NPAD, true, true, true>(ctx, tx, tb, p, g); else launch_s<NPAD, true, false, true>(ctx, tx, tb, p, g); }
+int xw_feasible(int bmode, bool h16, int want) {
+  auto ok_s = [&](auto xwc) {
+    constexpr int XW = decltype(xwc)::value;
+    if (h16) return PlanH<NPAD, 2, 0, XW>::ok;
+    if (bmode == 0) return Plan<NPAD, false, true, sketch_cps<NPAD, false, true>(), 0, XW>::ok;
+    return Plan<NPAD, true, true, sketch_cps<NPAD, true, true>(), 0, XW>::ok;
+  };
+  if (want >= 4 && ok_s(std::integral_constant<int, 4>())) return 4;
+  if (want >= 2 && ok_s(std::integral_constant<int, 2>())) return 2;
+  return 1;
 }
 
-template <int NPAD, bool AMN, int CPS = 2>
+// b: 0 tf32-exact B, 1 split in the kernel, 2 pre-split in global memory; xw: X stage width
+template <int NPAD>
+void dispatch_s(const Ctx& ctx, bool amn, int bmode, int xw, const CUtensorMap& tx, const CUtensorMap& tb,
+                const SParams& p, dim3 g) {
+  if (amn) {
+    if (bmode == 0) launch_s<NPAD, false, true, false>(ctx, tx, tb, p, g);
+    else if (bmode == 1) launch_s<NPAD, true, true, false>(ctx, tx, tb, p, g);
+    else launch_s<NPAD, true, true, true>(ctx, tx, tb, p, g);
+  } else if (xw == 4) {
+    if (bmode == 0) { if constexpr (Plan<NPAD, false, true, sketch_cps<NPAD, false, true>(), 0, 4>::ok) launch_s<NPAD, false, false, false, 4>(ctx, tx, tb, p, g); }
+    else if (bmode == 1) { if constexpr (Plan<NPAD, true, true, sketch_cps<NPAD, true, true>(), 0, 4>::ok) launch_s<NPAD, true, false, false, 4>(ctx, tx, tb, p, g); }
+    else { if constexpr (Plan<NPAD, true, true, sketch_cps<NPAD, true, true>(), 0, 4>::ok) launch_s<NPAD, true, false, true, 4>(ctx, tx, tb, p, g); }
+  } else if (xw == 2) {
+    if (bmode == 0) { if constexpr (Plan<NPAD, false, true, sketch_cps<NPAD, false, true>(), 0, 2>::ok) launch_s<NPAD, false, false, false, 2>(ctx, tx, tb, p, g); }
+    else if (bmode == 1) { if constexpr (Plan<NPAD, true, true, sketch_cps<NPAD, true, true>(), 0, 2>::ok) launch_s<NPAD, true, false, false, 2>(ctx, tx, tb, p, g); }
+    else { if constexpr (Plan<NPAD, true, true, sketch_cps<NPAD, true, true>(), 0, 2>::ok) launch_s<NPAD, true, false, true, 2>(ctx, tx, tb, p, g); }
+  } else {
+    if (bmode == 0) launch_s<NPAD, false, false, false>(ctx, tx, tb, p, g);
+    else if (bmode == 1) launch_s<NPAD, true, false, false>(ctx, tx, tb, p, g);
+    else launch_s<NPAD, true, false, true>(ctx, tx, tb, p, g);
+  }
+}
+
+template <int NPAD, bool AMN, int CPS = 2, int XW = 1>
 void launch_h1(const Ctx& ctx, const CUtensorMap& tx, const CUtensorMap& tb, const HParams& p, dim3 grid) {
-  using L = PlanH<NPAD, CPS>;
+  using L = PlanH<NPAD, CPS, 0, XW>;
   static bool attr = false;
-  if (!attr) { set_smem(ttm_s_h16_kernel<NPAD, AMN, CPS>, L::bytes); attr = true; }
+  if (!attr) { set_smem(ttm_s_h16_kernel<NPAD, AMN, CPS, XW>, L::bytes); attr = true; }
   launch(ctx, ctx.label ? ctx.label : "ttm_s_h16", [&] {
-    ttm_s_h16_kernel<NPAD, AMN, CPS><<<grid, NT_TTM, L::bytes, ctx.stream>>>(tx, tb, p);
+    ttm_s_h16_kernel<NPAD, AMN, CPS, XW><<<grid, NT_TTM, L::bytes, ctx.stream>>>(tx, tb, p);
   });
 }
 // 2 chunks per stage (1 chunk per stage measured the same: 6.0-6.3 ms per cfg5 pass either way)
 template <int NPAD, bool AMN>
-void launch_h(const Ctx& ctx, const CUtensorMap& tx, const CUtensorMap& tb, const HParams& p, dim3 grid) {
+void launch_h(const Ctx& ctx, int xw, const CUtensorMap& tx, const CUtensorMap& tb, const HParams& p, dim3 grid) {
+  if constexpr (!AMN) {
+    if constexpr (PlanH<NPAD, 2, 0, 4>::ok) { if (xw == 4) { launch_h1<NPAD, AMN, 2, 4>(ctx, tx, tb, p, grid); return; } }
+    if constexpr (PlanH<NPAD, 2, 0, 2>::ok) { if (xw == 2) { launch_h1<NPAD, AMN, 2, 2>(ctx, tx, tb, p, grid); return; } }
+  }
   launch_h1<NPAD, AMN, 2>(ctx, tx, tb, p, grid);
 }
 
@@ -1327,18 +1432,43 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
   if (amn ? (box.I % 4) : (box.a % 4)) return false;
   if (box.a > INT32_MAX || box.I > INT32_MAX || box.b > INT32_MAX || J > INT32_MAX) return false;
   const int nh = tc_split_width(K);
-  CUtensorMap tx, tb;
-  if (amn) {
-    const uint64_t d[2] = {uint64_t(box.I), uint64_t(box.b)}, s[1] = {uint64_t(box.I) * 4};
-    const uint32_t bx[2] = {BM, KC};
-    if (!make_map(&tx, X, 2, d, s, bx, false)) return false;
-  } else {
-    const uint64_t d[3] = {uint64_t(box.a), uint64_t(box.I), uint64_t(box.b)};
-    const uint64_t s[2] = {uint64_t(box.a) * 4, uint64_t(box.a) * box.I * 4};
-    const uint32_t bx[3] = {KC, BM, 1};
-    if (!make_map(&tx, X, 3, d, s, bx, true)) return false;
-  }
   const bool h16 = b_presplit && xscale != nullptr;
+  const int bmode = b_presplit ? 2 : (b_tf32_exact ? 0 : 1);
+  // X stage width of the strided modes: wide rows (xw chunks per unswizzled box) when a is a
+  // multiple of KC xw (the chunk groups stay inside one beta) and the kernel's plan fits
+  // (RT_OPT_TC_ABLATE 231 / 232 / 234 cap it at 1 / 2 / 4).  The fp16 kernel and its tf32 twin may
+  // get different widths (the twin splits B in shared memory: fewer bytes left for X stages).
+  auto pick_xw = [&](int bm, bool hh) {
+    if (amn) return 1;
+    int want = ctx.tc_xw;
+    switch (npad) {
+      case 16: want = xw_feasible<16>(bm, hh, want); break;
+      case 32: want = xw_feasible<32>(bm, hh, want); break;
+      case 48: want = xw_feasible<48>(bm, hh, want); break;
+      case 64: want = xw_feasible<64>(bm, hh, want); break;
+      case 80: want = xw_feasible<80>(bm, hh, want); break;
+      case 96: want = xw_feasible<96>(bm, hh, want); break;
+      default: want = xw_feasible<128>(bm, hh, want); break;
+    }
+    while (want >= 2 && !(box.a % (int64_t(KC) * want) == 0 && box.a >= int64_t(KC) * want + 4)) want /= 2;
+    return want >= 2 ? want : 1;
+  };
+  const int xw = pick_xw(h16 ? 2 : bmode, h16);           // the launch in charge
+  const int xw_t = h16 ? pick_xw(1, false) : xw;           // its tf32 twin (h16 only)
+  auto make_x = [&](CUtensorMap* m, int w) {
+    if (amn) {
+      const uint64_t d[2] = {uint64_t(box.I), uint64_t(box.b)}, st[1] = {uint64_t(box.I) * 4};
+      const uint32_t bx[2] = {BM, KC};
+      return make_map(m, X, 2, d, st, bx, false);
+    }
+    const uint64_t d[3] = {uint64_t(box.a), uint64_t(box.I), uint64_t(box.b)};
+    const uint64_t st[2] = {uint64_t(box.a) * 4, uint64_t(box.a) * box.I * 4};
+    const uint32_t bx[3] = {w > 1 ? uint32_t(KC * w + 4) : uint32_t(KC), BM, 1};
+    return make_map(m, X, 3, d, st, bx, w == 1);
+  };
+  CUtensorMap tx, txt, tb;
+  if (!make_x(&tx, xw)) return false;
+  if (xw_t != xw) { if (!make_x(&txt, xw_t)) return false; } else { txt = tx; }
   if (h16) {
     // fp16 [hi (npad) | lo (npad)] rows, row pitch ldb halves: (64 cols, 32 rows) SWIZZLE_128B boxes
     if (!aligned(Bm, 16) || (ldb % 8) || ldb < 2 * npad) return false;
@@ -1361,6 +1491,10 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
   int64_t splits = std::max<int64_t>(1, (int64_t(ctx.num_sms) * 4 + mtiles - 1) / mtiles);
   splits = std::min<int64_t>(splits, std::max<int64_t>(1, p.nchunks / 8));
   splits = std::min<int64_t>(splits, 65535);
+  // contiguous chunk range per split, a whole number of X stages
+  const int xwl = std::max(xw, xw_t);                     // 1, 2, 4: a multiple of both widths
+  p.per = cdiv(cdiv(p.nchunks, splits), xwl) * xwl;
+  splits = cdiv(p.nchunks, p.per);
   p.seg = std::max(1, ctx.tc_seg);
   p.ablate = ctx.tc_ablate;
   p.skew = ctx.tc_skew >= 0 ? ctx.tc_skew : 0;
@@ -1379,18 +1513,17 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
     p.tim = ws.alloc_n<unsigned long long>(mtiles * splits * 24);
     RT_CUDA(cudaMemsetAsync(p.tim, 0, sizeof(unsigned long long) * mtiles * splits * 24, ctx.stream));
   }
-  const int bmode = b_presplit ? 2 : (b_tf32_exact ? 0 : 1);
 #define RT_S_CASE(NP)                                                                 \
   case NP:                                                                            \
     if (h16) {                                                                        \
       const HParams hp{p, xscale};                                                    \
-      if (amn) launch_h<NP, true>(ctx, tx, tb, hp, grid);                             \
-      else launch_h<NP, false>(ctx, tx, tb, hp, grid);                                \
+      if (amn) launch_h<NP, true>(ctx, xw, tx, tb, hp, grid);                         \
+      else launch_h<NP, false>(ctx, xw, tx, tb, hp, grid);                            \
       SParams pf = p;                                                                 \
       pf.gate = xscale;                                                               \
-      dispatch_s<NP>(ctx, amn, 1, tx, tbf, pf, grid);                                 \
+      dispatch_s<NP>(ctx, amn, 1, xw_t, txt, tbf, pf, grid);                          \
     } else {                                                                          \
-      dispatch_s<NP>(ctx, amn, bmode, tx, tb, p, grid);                               \
+      dispatch_s<NP>(ctx, amn, bmode, xw, tx, tb, p, grid);                           \
     }                                                                                 \
     break;
   switch (npad) {

@@ -107,7 +107,8 @@ def test_rp_hooi_gaussian_start(P, h, h64, strict):
     device by max|Q| < 2 as well as X's scale, so the wide start factors send sweep 0's first
     stages to the 3xTF32 twin (the run counters show both kinds ran); parity with the oracle from
     the same start."""
-    cfg = synth.CONFIGS["cfg2"].scaled((150, 140, 130), (12, 12, 12), (12, 12, 12))
+    # dims multiples of 4: the first S-chain stage takes the tensor-core path (16-byte TMA strides)
+    cfg = synth.CONFIGS["cfg2"].scaled((152, 144, 128), (12, 12, 12), (12, 12, 12))
     x = synth.make_tensor(cfg)
     q0 = [synth.rng_for(4242, 7, n).standard_normal((cfg.dims[n], cfg.ranks[n])) * 3.0 for n in range(3)]
     assert max(np.abs(q).max() for q in q0) >= 4.0
