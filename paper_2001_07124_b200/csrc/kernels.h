@@ -78,8 +78,11 @@ int tc_split_width(int K);
 // [hi (tc_npad(C)) | lo (tc_npad(C))] rows, out then points to halves and so_a / so_b count halves.
 bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
               int64_t so_a, int64_t so_c, int64_t so_b, int split_out = 0, bool q_tf32_exact = false,
-              const float* xscale = nullptr, const float* run_if_zero = nullptr, const float* oscale = nullptr);
-// oscale (nullable): device scale multiplied into every output (the power iteration's Z = sn X^T Q)
+              const float* xscale = nullptr, const float* run_if_zero = nullptr, const float* oscale = nullptr,
+              float omul = 1.f, bool no_twin = false);
+// oscale (nullable): device scale multiplied into every output (the power iteration's Z = sn X^T Q);
+// omul: a host power-of-two factor as well; no_twin (with xscale): launch the fp16-split kernel only
+// (the caller launches its tf32 twin itself, e.g. with another output format)
 // run_if_zero (tf32 form only): the launch does its work only if *run_if_zero == 0 (device-side
 // gate: the fallback of an fp16-split step whose X scale came out 0, R29)
 // xscale (device scale of X from x_scale_h16 / x_scale_from_amax, |Q| <= 1 required): the fp16

@@ -363,13 +363,42 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
     const auto mq = ws.mark();
     int64_t ldqt;
     const T* QyT = working_copy<T>(ctx, ws, Qy, In, K, In, ldqt);
+    // Reading R31 (fp32 data, fp16-split power products, Z rows local): Z is not orthonormalized.
+    // span(X_(n) Z R^-1) = span(X_(n) Z) for any invertible R, and Z = X_(n)^T Q_y ~ V_K Sigma_K has
+    // near-orthogonal columns, so the product's column errors are those of an orthonormalized Z; a
+    // power of two s_z = sn 2^-(ceil(log2 sqrt(I_n)) + 1) bounds |s_z Z| < 1/2 (|z_jc| <= sqrt(I_n)
+    // max|X|), and the Z pass writes s_z Z straight into the fp16 [hi | lo] rows of the product's B
+    // operand: no Gram / Cholesky / apply passes over Z.  Its tf32 twin (gated on X's fp16 scale
+    // being 0) writes the fp32 s_z Z that the product's tf32 twin reads.
+    bool r31 = false;
+    if constexpr (std::is_same<T, float>::value) r31 = zsplit == 2 && !ctx.power_qrz && !(last && dist());
     // Z(j, c) = sum_i X_(n)(i, j) Q(i, c), written row-major J x K (j = alpha + a beta):
     // so_a = ldz, so_c = 1, so_b = a ldz
-    {
+    if constexpr (std::is_same<T, float>::value) {
+      if (r31) {
+        LabelScope ls(ctx, "ttm_t_tc_pow");
+        const int ez = int(std::ceil(0.5 * std::log2(double(X.Ig(n)))));
+        const float hz = std::ldexp(1.0f, -(ez + 1));
+        RT_REQUIRE(ttm_t_tc(ctx, ws, data, bx, QyT, ldqt, K, reinterpret_cast<float*>(Z2), ldz2, 1, bx.a * ldz2,
+                            /*split_out=*/2, false, xsc, nullptr, zsc, hz, /*no_twin=*/true) &&
+                       ttm_t_tc(ctx, ws, data, bx, QyT, ldqt, K, Z, ldz, 1, bx.a * ldz, 0, false, nullptr, xsc, zsc, hz),
+                   kEUNSUPPORTED, "power iteration: Z pass rejected by the tensor-core path");
+      }
+    }
+    if (!r31) {
       LabelScope ls(ctx, "ttm_t_tc_pow");
       ttm_t_dispatch(ctx, ws, data, bx, QyT, ldqt, K, Z, ldz, 1, bx.a * ldz, false, xsc, zsc);
     }
     ws.rewind(mq);
+    if constexpr (std::is_same<T, float>::value) {
+      if (r31) {
+        LabelScope ls(ctx, "ttm_s_tc_pow");
+        RT_REQUIRE(ttm_s_tc(ctx, ws, data, bx, Z2, ldz2, false, K, Yt, In, /*b_presplit=*/true, xsc, nullptr, Z, ldz),
+                   kEUNSUPPORTED, "pre-split power product not launched");
+        allreduce(comm, !last && dist(), Yt, In * K, ctx.stream);                   // C1
+        continue;
+      }
+    }
     allreduce(comm, last && dist(), Z, Jl * ldz, ctx.stream);                    // C3
     // local Z rows: for n < N-1 the slab's j's are the contiguous block starting at a*b'*off
     int64_t zrow0 = 0;

@@ -879,6 +879,7 @@ struct TParams {
   const float* gate;     // tf32 kernels: run only if *gate == 0 (fallback of an fp16-split launch)
   unsigned int* runs;    // optional run counters (see SParams)
   const float* oscale;   // optional device scale of the output (the power iteration's Z = sn X^T Q)
+  float omul;            // host power-of-two factor of the output (1 = none)
 };
 
 // AKM: mode 0 (a == 1), X tile K-major [BM j][KC i].  BSPLIT: Q = Q_hi + Q_lo pre-split (an fp64
@@ -1020,8 +1021,8 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
     for (int k = 0; k < NPAD; ++k) sums[k] = 0.f;
     const int segs_per_tile = (p.nic + p.seg - 1) / p.seg;
     // exact: powers of two (the H16 unscaling and the optional output scale)
-    const float inv = (H16 ? 1.0f / (*p.xscale * kQScale) : 1.f) * (p.oscale ? *p.oscale : 1.f);
-    const bool rescale = H16 || p.oscale != nullptr;
+    const float inv = (H16 ? 1.0f / (*p.xscale * kQScale) : 1.f) * (p.oscale ? *p.oscale : 1.f) * p.omul;
+    const bool rescale = H16 || p.oscale != nullptr || p.omul != 1.f;
     int64_t g = 0;
     for (int64_t u = 0; u < my_tiles; ++u) {
       const int64_t tile = blockIdx.x + u * gridDim.x;
@@ -1570,7 +1571,7 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
 
 bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
               int64_t so_a, int64_t so_c, int64_t so_b, int split_out, bool q_tf32_exact, const float* xscale,
-              const float* run_if_zero, const float* oscale) {
+              const float* run_if_zero, const float* oscale, float omul, bool no_twin) {
   const int npad = tc_npad(C);
   if (npad < 0) return false;
   const bool h16 = xscale != nullptr && !q_tf32_exact;
@@ -1627,6 +1628,7 @@ bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q
   p.gate = h16 ? nullptr : run_if_zero;
   p.runs = ctx.d_runs;
   p.oscale = oscale;
+  p.omul = omul;
   RT_REQUIRE(!split_out || (so_c == 1 && (so_a % 4) == 0 && (so_b % 4) == 0 && aligned(out, 16)), kEINVAL,
              "split output needs 16-byte aligned row-major rows");
   RT_REQUIRE(split_out != 2 || ((so_a % 8) == 0 && (so_b % 8) == 0), kEINVAL, "fp16 split rows need 16-byte pitch");
@@ -1645,11 +1647,18 @@ bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q
       const uint32_t bx[2] = {32, uint32_t(BM)};
       p.tma_out = make_map(&to, out, 2, d, st, bx, true);
     }
-  } else if (split_out == 2 && akm && box.b <= INT32_MAX && !getenv("RT_TC_NO_TMA_OUT")) {
-    // fp16 [hi | lo] rows of 2 npad halves, pitch so_b halves: (64, 128) SWIZZLE_128B boxes
-    const uint64_t d[2] = {uint64_t(2 * npad), uint64_t(box.b)}, st[1] = {uint64_t(so_b) * 2};
-    const uint32_t bx[2] = {64, uint32_t(BM)};
-    p.tma_out = make_map(&to, out, 2, d, st, bx, true, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+  } else if (split_out == 2 && !getenv("RT_TC_NO_TMA_OUT")) {
+    // fp16 [hi | lo] rows of 2 npad halves, one row pitch across the output (mode 0: rows j = beta,
+    // pitch so_b; a > 1: rows alpha + a beta, pitch so_a, whole 128-row tiles per beta): (64, 128)
+    // SWIZZLE_128B boxes
+    const int64_t pitch = akm ? so_b : so_a;
+    const int64_t rows = akm ? box.b : box.a * box.b;
+    const bool rowsok = akm || (box.a % BM == 0 && so_b == box.a * so_a);
+    if (rowsok && rows <= INT32_MAX) {
+      const uint64_t d[2] = {uint64_t(2 * npad), uint64_t(rows)}, st[1] = {uint64_t(pitch) * 2};
+      const uint32_t bx[2] = {64, uint32_t(BM)};
+      p.tma_out = make_map(&to, out, 2, d, st, bx, true, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+    }
   }
   const int64_t grid = std::min<int64_t>(p.ntiles, ctx.num_sms);
 #define RT_T_CASE(NP)                                                     \
@@ -1659,10 +1668,10 @@ bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q
       pf.gate = xscale;                                                  \
       if (akm) {                                                         \
         launch_t<NP, true, true, true>(ctx, tx, tbh, to, p, dim3(unsigned(grid)));  \
-        launch_t<NP, true, true>(ctx, tx, tb, to, pf, dim3(unsigned(grid)));        \
+        if (!no_twin) launch_t<NP, true, true>(ctx, tx, tb, to, pf, dim3(unsigned(grid)));  \
       } else {                                                           \
         launch_t<NP, false, true, true>(ctx, tx, tbh, to, p, dim3(unsigned(grid))); \
-        launch_t<NP, false, true>(ctx, tx, tb, to, pf, dim3(unsigned(grid)));       \
+        if (!no_twin) launch_t<NP, false, true>(ctx, tx, tb, to, pf, dim3(unsigned(grid))); \
       }                                                                  \
     } else if (bsplit) {                                                 \
       if (akm) launch_t<NP, true, true>(ctx, tx, tb, to, p, dim3(unsigned(grid)));  \
