@@ -47,7 +47,15 @@ void count_sketch(const Ctx& ctx, Arena& ws, const T* X, Box box, const int32_t*
 // halves (a multiple of 8), |B| <= 1; X is scaled by *xscale before its fp16 split.
 bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Bm, int64_t ldb, bool b_tf32_exact,
               int K, double* Y, int64_t ldy, bool b_presplit = false, const float* xscale = nullptr,
-              unsigned int* amax = nullptr, const float* Bfb = nullptr, int64_t ldbfb = 0);
+              unsigned int* amax = nullptr, const float* Bfb = nullptr, int64_t ldbfb = 0,
+              float binv = 1.f / 16384.f);
+// binv (fp16 form): 1 / the power-of-two scale of the pre-split B rows (2^-14 for Q_z / Z, 2^-11 for
+// Omega from omega_h16)
+// Omega (J x K fp32 row-major, pitch ld) -> *O2: fp16 rows [2^11 hi | 2^11 lo] (pitch *ld2 halves) for an
+// fp16-split Omega sketch; returns the device scale pair to pass as xscale: X's (xs) with the fp16
+// scale zeroed when Omega has an entry outside |omega| < 16 (its tf32 twin then runs on Om)
+const float* omega_h16(const Ctx& ctx, Arena& ws, const float* Om, int64_t J, int K, int64_t ld, const float* xs,
+                       uint16_t** O2, int64_t* ld2);
 // Bfb (required with xscale): the fp32 B (row-major, ldbfb) of the tf32 twin launch that runs
 // instead when *xscale == 0 (X's dynamic range too wide for one fp16 scale, R29)
 // amax (tf32 kernels): X statistics of the tiles read: amax[0] = max|X| (float bits, atomicMax),

@@ -246,7 +246,21 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
       om = c;
       ld = ldp;
     }
-    if (ttm_s_dispatch(ctx, ws, data, bx, om, ld, ctx.omega_tf32 != 0, K, Yt, In, am)) {
+    bool done = false;
+    if constexpr (std::is_same<T, float>::value) {
+      // X's scale already known (a previous mode's sketch of this call gathered it): the fp16 split
+      // (R29) on Omega converted once to fp16 [hi | lo] rows (R34)
+      if (xs_slot && xs_key == data && ctx.tc_h16 && !ctx.simt() && !ctx.omega_h16_off &&
+          ttm_s_tc_ok(ctx, data, bx, K)) {
+        uint16_t* o2;
+        int64_t ld2;
+        const float* xso = omega_h16(ctx, ws, om, bx.J(), K, ld, xs_slot, &o2, &ld2);
+        LabelScope ls(ctx, "ttm_s_tc");
+        done = ttm_s_tc(ctx, ws, data, bx, reinterpret_cast<const float*>(o2), ld2, false, K, Yt, In,
+                        /*b_presplit=*/true, xso, nullptr, om, ld, 1.f / 2048.f);
+      }
+    }
+    if (!done && ttm_s_dispatch(ctx, ws, data, bx, om, ld, ctx.omega_tf32 != 0, K, Yt, In, am)) {
       finish_scale(am, X.size(), n_glob);
       xs_key = data;
     }
