@@ -238,6 +238,7 @@ rt_status rt_set_option(rt_handle* h, rt_option opt, int64_t value) {
       if (value == 231 || value == 232 || value == 234) { h->ctx.tc_xw = int(value - 230); return RT_OK; }
       if (value == 240 || value == 241) { h->ctx.power_qrz = int(value == 240); return RT_OK; }
       if (value == 250 || value == 251) { h->ctx.omega_h16_off = int(value == 250); return RT_OK; }
+      if (value == 260 || value == 261) { h->ctx.jacobi_v1 = int(value == 260); return RT_OK; }
       h->ctx.tc_ablate = int(value);
       return RT_OK;
     case RT_OPT_TC_SKEW: h->ctx.tc_skew = int(value); return RT_OK;

@@ -1401,20 +1401,33 @@ void q_gate_scale(const Ctx& ctx, const float* Q, int64_t m, int r, int64_t ld, 
 // the fp16 range with room (a Gaussian test matrix of 3.4e8 entries peaks near 6); an entry with
 // |2^11 omega| >= 2^15 or a non-finite one sets *flag (the fp16 launch then stands down for its
 // tf32 twin).  A tf32-rounded Omega is exact in the hi part (lo = 0).
+// one thread per 8 consecutive columns of a row: two 16 B loads (vec4: K and ld multiples of 4 and a
+// 16 B aligned Omega), one 16 B store each of the hi and lo halves
 __global__ void omega_h16_kernel(const float* __restrict__ Om, int64_t J, int K, int64_t ld, int npad,
-                                 uint32_t* __restrict__ O2, int* __restrict__ flag) {
-  const int hp = npad / 2;
+                                 uint32_t* __restrict__ O2, int* __restrict__ flag, bool vec4) {
+  const int g8 = npad / 8, hp = npad / 2;
   bool bad = false;
-  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < J * hp; e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t j = e / hp;
-    const int c0 = 2 * int(e % hp), c1 = c0 + 1;
-    const float v0 = c0 < K ? Om[j * ld + c0] * 2048.f : 0.f;
-    const float v1 = c1 < K ? Om[j * ld + c1] * 2048.f : 0.f;
-    bad |= !(fabsf(v0) < 32768.f) || !(fabsf(v1) < 32768.f);
-    uint32_t h, l;
-    split_h16x2(v0, v1, h, l);
-    O2[j * npad + c0 / 2] = h;
-    O2[j * npad + hp + c0 / 2] = l;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < J * g8; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t j = e / g8;
+    const int c0 = 8 * int(e % g8);
+    float v[8];
+    const float* row = Om + j * ld + c0;
+    if (vec4 && c0 + 8 <= K) {
+      const float4 a = __ldcs(reinterpret_cast<const float4*>(row)), b = __ldcs(reinterpret_cast<const float4*>(row + 4));
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = (c0 + q < K) ? row[q] : 0.f;
+    }
+    uint32_t h[4], l[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float v0 = v[2 * q] * 2048.f, v1 = v[2 * q + 1] * 2048.f;
+      bad |= !(fabsf(v0) < 32768.f) || !(fabsf(v1) < 32768.f);
+      split_h16x2(v0, v1, h[q], l[q]);
+    }
+    *reinterpret_cast<uint4*>(O2 + j * npad + c0 / 2) = make_uint4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<uint4*>(O2 + j * npad + hp + c0 / 2) = make_uint4(l[0], l[1], l[2], l[3]);
   }
   if (bad) atomicOr(flag, 1);
 }
@@ -1431,10 +1444,12 @@ const float* omega_h16(const Ctx& ctx, Arena& ws, const float* Om, int64_t J, in
   int* flag = ws.alloc_n<int>(1);
   float* xo = ws.alloc_n<float>(2);
   RT_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), ctx.stream));
-  const int64_t n = J * (npad / 2);
+  const int64_t n = J * (npad / 8);
+  const bool vec4 = (K % 4) == 0 && (ld % 4) == 0 && aligned(Om, 16);
   const unsigned blocks = unsigned(std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), int64_t(ctx.num_sms) * 16)));
   launch(ctx, "omega_h16", [&] {
-    omega_h16_kernel<<<blocks, 256, 0, ctx.stream>>>(Om, J, K, ld, npad, reinterpret_cast<uint32_t*>(*O2), flag);
+    omega_h16_kernel<<<blocks, 256, 0, ctx.stream>>>(Om, J, K, ld, npad, reinterpret_cast<uint32_t*>(*O2), flag,
+                                                     vec4);
   });
   launch(ctx, "omega_gate", [&] { omega_gate_kernel<<<1, 1, 0, ctx.stream>>>(flag, xs, xo); });
   return xo;
