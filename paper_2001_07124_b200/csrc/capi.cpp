@@ -12,6 +12,9 @@
 struct rt_handle {
   rt::Ctx ctx;
   rt::Arena ws;
+  rt::Arena ws_side;                 // workspace of the side stream (overlapped QRs)
+  rt::EventPool events;
+  cudaStream_t side = nullptr;
   rt::Profiler prof;
   std::unique_ptr<rt::Comm> comm;
   std::string err;
@@ -36,6 +39,8 @@ rt_status guard(rt_handle* h, F&& f) {
     if (h) {
       cudaSetDevice(h->device);
       h->ws.begin_call();
+      h->ws_side.begin_call();
+      h->events.reset();
     }
     f();
     return RT_OK;
@@ -161,6 +166,16 @@ static rt_status create_common(rt_handle** h, void* stream) {
   }
   cudaMemset(hh->d_runs, 0, 2 * sizeof(unsigned int));
   hh->ctx.d_runs = hh->d_runs;
+  // side stream (highest priority: its latency-bound QR kernels take SMs ahead of the X passes)
+  int lo_prio = 0, hi_prio = 0;
+  cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+  if (cudaStreamCreateWithPriority(&hh->side, cudaStreamNonBlocking, hi_prio) != cudaSuccess) {
+    cudaGetLastError();
+    hh->side = nullptr;               // no overlap: every step on the main stream
+  }
+  hh->ctx.side_stream = hh->side;
+  hh->ctx.side_ws = &hh->ws_side;
+  hh->ctx.events = &hh->events;
   hh->ctx.prof = &hh->prof;
   *h = hh;
   return RT_OK;
@@ -200,6 +215,7 @@ rt_status rt_destroy(rt_handle* h) {
   cudaSetDevice(h->device);
   if (h->ctx.stream) cudaStreamSynchronize(h->ctx.stream); else cudaDeviceSynchronize();
   h->comm.reset();
+  if (h->side) { cudaStreamSynchronize(h->side); cudaStreamDestroy(h->side); }
   if (h->d_status) cudaFree(h->d_status);
   if (h->d_runs) cudaFree(h->d_runs);
   delete h;
@@ -238,7 +254,7 @@ rt_status rt_set_option(rt_handle* h, rt_option opt, int64_t value) {
       if (value == 231 || value == 232 || value == 234) { h->ctx.tc_xw = int(value - 230); return RT_OK; }
       if (value == 240 || value == 241) { h->ctx.power_qrz = int(value == 240); return RT_OK; }
       if (value == 250 || value == 251) { h->ctx.omega_h16_off = int(value == 250); return RT_OK; }
-      if (value == 260 || value == 261) { h->ctx.jacobi_v1 = int(value == 260); return RT_OK; }
+      if (value == 270 || value == 271) { h->ctx.overlap = int(value == 271); return RT_OK; }
       h->ctx.tc_ablate = int(value);
       return RT_OK;
     case RT_OPT_TC_SKEW: h->ctx.tc_skew = int(value); return RT_OK;

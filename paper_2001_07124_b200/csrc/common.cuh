@@ -60,6 +60,24 @@ struct Profiler {
   }
 };
 
+class Arena;
+
+// Pool of reusable CUDA events (fork / join of the side stream); reset at the start of every call.
+struct EventPool {
+  std::vector<cudaEvent_t> ev;
+  size_t next = 0;
+  cudaEvent_t get() {
+    if (next == ev.size()) {
+      cudaEvent_t e;
+      RT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ev.push_back(e);
+    }
+    return ev[next++];
+  }
+  void reset() { next = 0; }
+  ~EventPool() { for (auto e : ev) cudaEventDestroy(e); }
+};
+
 // ---------------------------------------------------------------- launch context
 struct Ctx {
   cudaStream_t stream = nullptr;
@@ -83,9 +101,13 @@ struct Ctx {
   int power_qrz = 0;            // power iteration: orthonormalize Z (shifted CholeskyQR) instead of R31's
                                 // power-of-two scale (ablation 240 / 241 toggle)
   int omega_h16_off = 0;        // Omega sketches of later modes: 1 = keep tf32 (ablation 250 / 251 toggle)
-  int jacobi_v1 = 0;            // 1: the 512-thread three-barrier Jacobi round (ablation 260 / 261 toggle)
   int tc_xw = 2;                // ttm_s strided modes: chunks per wide-row X stage (1 = swizzled 128 B rows;
                                 // ablation 231/232/234 select 1/2/4; cfg5 modes 1/2: 2 is fastest)
+  cudaStream_t side_stream = nullptr;   // second stream of the handle (high priority): overlapped QRs
+  Arena* side_ws = nullptr;             // its workspace arena
+  EventPool* events = nullptr;          // fork / join events
+  int overlap = 1;              // HOSVD: thin QRs on the side stream (ablation 270 / 271 toggle)
+  int sm_reserve = 0;           // SMs the persistent X-pass grids leave free (set while side work is pending)
   unsigned int* d_runs = nullptr;  // device counters: [0] fp16-split X passes that did their work,
                                    // [1] tf32 twins that ran in their place (R29; rt_profile_read)
 };

@@ -46,7 +46,13 @@ class Engine {
   // (1) sketch of mode n incl. q power iterations; Yt: fp64 I_n(local) x K, ld I_n(local).
   template <typename T>
   void sketch(const TView& X, const T* data, int n, int kind, const void* const* omega,
-              const int64_t* omega_cols, const int64_t* omega_ld, int q, double* Yt);
+              const int64_t* omega_cols, const int64_t* omega_ld, int q, double* Yt, bool first_only = false);
+  // one power step of reading R31 (fp32 data, tensor cores): Yt = X_(n) s_z X_(n)^T Qy; false if n/a
+  bool power_step_r31(const TView& X, const float* data, int n, int K, const double* Qy, double* Yt);
+  // HOSVD (Gaussian Omega) with the thin QRs on the handle's side stream; false (nothing launched) if n/a
+  bool hosvd_overlap(const TView& X, const float* data, const int64_t* R, int q, const void* const* omega,
+                     const int64_t* omega_cols, const int64_t* omega_ld, double* const* Q_out, double* G_out,
+                     double* E, double* Eg);
   // (2) thin QR of the fp64 Y side (shifted CholeskyQR3); R nullable.
   void qr_y(const double* Y, int64_t m, int64_t m_glob, int k, int64_t ldy, double* Q, int64_t ldq,
             double* R, bool rows_dist, int64_t row0);

@@ -495,121 +495,6 @@ __global__ void __launch_bounds__(512) jacobi_kernel(EigBatch bt, double* Vscrat
   }
 }
 
-// Leaner cyclic Jacobi (same rotations, same ordering, same convergence test as jacobi_kernel):
-// 256 threads per matrix, every warp owns a fixed share of the kk/2 disjoint rotation pairs of a
-// round, computes their (c, s) itself (one lane per pair, in parallel) and applies their row and
-// column rotations: two block barriers per round instead of three, and no phase in which only a
-// few threads of the CTA compute while the others wait.
-__global__ void __launch_bounds__(256) jacobi2_kernel(EigBatch bt, double* Vscratch, int v_in_smem, int64_t stride_scr) {
-  extern __shared__ double sm[];
-  const int k = bt.k[blockIdx.x];
-  const int kk = k + (k & 1);
-  const int ld = kk + 1;
-  double* A = sm;                                   // kk x ld (row-major A[i*ld + j])
-  double* V = v_in_smem ? (sm + kk * ld) : (Vscratch + blockIdx.x * stride_scr);
-  double* cs = (v_in_smem ? sm + 2 * kk * ld : sm + kk * ld);   // kk/2 pairs: c, s
-  __shared__ double red[32];
-  __shared__ int s_done;
-  const double* Ab = bt.A[blockIdx.x];
-  double* W = bt.W[blockIdx.x];
-  double* Vout = bt.V[blockIdx.x];
-  const int t = threadIdx.x, nt = blockDim.x;
-  const int warp = t >> 5, lane = t & 31, nw = nt >> 5;
-  for (int i = warp; i < kk; i += nw)
-    for (int j = lane; j < kk; j += 32) {
-      A[i * ld + j] = (i < k && j < k) ? 0.5 * (Ab[i + int64_t(k) * j] + Ab[j + int64_t(k) * i]) : 0.0;
-      V[i * ld + j] = (i == j) ? 1.0 : 0.0;
-    }
-  __syncthreads();
-  const int npairs = kk / 2;
-  auto pair_of = [&](int round, int pi, int& p, int& q) {
-    if (pi == 0) { p = round; q = kk - 1; }
-    else {
-      p = round + pi; if (p >= kk - 1) p -= kk - 1;
-      q = round - pi; if (q < 0) q += kk - 1;
-    }
-    if (p > q) { const int tmp = p; p = q; q = tmp; }
-  };
-  for (int sweep = 0; sweep < 40; ++sweep) {
-    double off = 0.0, dia = 0.0;
-    for (int i = warp; i < kk; i += nw)
-      for (int j = lane; j < kk; j += 32) {
-        const double v = A[i * ld + j];
-        if (i != j) off += v * v; else dia += v * v;
-      }
-    off = block_sum(off, red);
-    __syncthreads();
-    dia = block_sum(dia, red);
-    const double tol = double(k) * 1.1102230246251565e-16;
-    if (t == 0) s_done = (off <= tol * tol * dia) || (dia == 0.0);
-    __syncthreads();
-    if (s_done) break;
-    for (int round = 0; round < kk - 1; ++round) {
-      // this warp's pairs: pi = warp + nw * j; lane j computes the rotation of its j-th pair
-      double cl = 1.0, sl = 0.0;
-      {
-        const int pi = warp + nw * lane;
-        if (pi < npairs) {
-          int p, q;
-          pair_of(round, pi, p, q);
-          const double apq = A[p * ld + q];
-          if (apq != 0.0) {
-            const double tau = (A[q * ld + q] - A[p * ld + p]) / (2.0 * apq);
-            const double tt = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-            cl = 1.0 / sqrt(1.0 + tt * tt);
-            sl = tt * cl;
-          }
-          cs[2 * pi] = cl;
-          cs[2 * pi + 1] = sl;
-        }
-      }
-      // rows: A <- J^T A
-      for (int j = 0; warp + nw * j < npairs; ++j) {
-        const int pi = warp + nw * j;
-        const double c = __shfl_sync(0xffffffffu, cl, j), s = __shfl_sync(0xffffffffu, sl, j);
-        if (s == 0.0) continue;
-        int p, q;
-        pair_of(round, pi, p, q);
-        for (int l = lane; l < kk; l += 32) {
-          const double ap = A[p * ld + l], aq = A[q * ld + l];
-          A[p * ld + l] = c * ap - s * aq;
-          A[q * ld + l] = s * ap + c * aq;
-        }
-      }
-      __syncthreads();
-      // columns: A <- A J, V <- V J
-      for (int j = 0; warp + nw * j < npairs; ++j) {
-        const int pi = warp + nw * j;
-        const double c = cs[2 * pi], s = cs[2 * pi + 1];
-        if (s == 0.0) continue;
-        int p, q;
-        pair_of(round, pi, p, q);
-        for (int l = lane; l < kk; l += 32) {
-          const double ap = A[l * ld + p], aq = A[l * ld + q];
-          A[l * ld + p] = c * ap - s * aq;
-          A[l * ld + q] = s * ap + c * aq;
-          const double vp = V[l * ld + p], vq = V[l * ld + q];
-          V[l * ld + p] = c * vp - s * vq;
-          V[l * ld + q] = s * vp + c * vq;
-        }
-        __syncwarp();
-        if (lane == 0) { A[p * ld + q] = 0.0; A[q * ld + p] = 0.0; }
-      }
-      __syncthreads();
-    }
-  }
-  for (int i = t; i < k; i += nt) {
-    const double wi = A[i * ld + i];
-    int rank = 0;
-    for (int j = 0; j < k; ++j) {
-      const double wj = A[j * ld + j];
-      rank += (wj > wi) || (wj == wi && j < i);
-    }
-    W[rank] = wi;
-    for (int l = 0; l < k; ++l) Vout[l + int64_t(k) * rank] = V[l * ld + i];
-  }
-}
-
 // ------------------------------------------------------------ sign canon
 __global__ void colmax_kernel(const double* __restrict__ Q, int64_t m, int64_t ld, int64_t row0,
                               double* __restrict__ cand) {
@@ -888,14 +773,10 @@ void eig_sym_batch(const Ctx& ctx, Arena& ws, int count, const double* const* A,
   static bool attr = false;
   if (!attr) {
     RT_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    RT_CUDA(cudaFuncSetAttribute(jacobi2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     attr = true;
   }
   launch(ctx, "jacobi_eig", [&] {
-    if (ctx.jacobi_v1)
-      jacobi_kernel<<<count, 512, smem, ctx.stream>>>(bt, scratch, v_in_smem, stride_scr);
-    else
-      jacobi2_kernel<<<count, 256, smem, ctx.stream>>>(bt, scratch, v_in_smem, stride_scr);
+    jacobi_kernel<<<count, 512, smem, ctx.stream>>>(bt, scratch, v_in_smem, stride_scr);
   });
 }
 

@@ -213,9 +213,11 @@ bool Engine::qr_z(T* Z, int64_t m, int64_t ldz, int64_t m_glob, int k, bool rows
 }
 
 // ---------------------------------------------------------------- sketch (a1-a3)
+// first_only: the first sketch Y^(0) only (C1 and the non-finite check included), with X's scale
+// gathered as for q > 0 -- the driver that overlaps the QRs runs the power steps itself
 template <typename T>
 void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* const* omega,
-                    const int64_t* omega_cols, const int64_t* omega_ld, int q, double* Yt) {
+                    const int64_t* omega_cols, const int64_t* omega_ld, int q, double* Yt, bool first_only) {
   const int N = X.N;
   const Box bx = X.box(n);
   const bool last = (n == N - 1);
@@ -224,6 +226,7 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
   // driver's, else one taken here); gathered by the first pass over X when that is a tf32 sketch
   bool own_slot = false;
   const int64_t n_glob = X.size() / X.d[N - 1] * X.glob;
+  if (first_only) q = std::max(q, 1);
   if constexpr (std::is_same<T, float>::value) {
     if (q > 0 && !xs_slot) { xs_slot = ws.alloc_n<float>(2); xs_key = nullptr; own_slot = true; }
   }
@@ -342,7 +345,10 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
   }
   allreduce(comm, !last && dist(), Yt, In * K, ctx.stream);                       // C1
   set_status_if_nonfinite(ctx, Yt, In * K);
-  if (q <= 0) return;
+  if (q <= 0 || first_only) {
+    if (own_slot) { xs_slot = nullptr; xs_key = nullptr; }
+    return;
+  }
   // power iterations (reading R2): Q = qr(Y); Z = qr(X_(n)^T Q); Y = X_(n) Z
   const auto mk = ws.mark();
   const int64_t Jl = bx.J();
@@ -436,6 +442,129 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
   }
   ws.rewind(mk);
   if (own_slot) { xs_slot = nullptr; xs_key = nullptr; }
+}
+
+// One power step of reading R31 for mode n: Yt = X_(n) (s_z X_(n)^T Q_y), Q_y fp64 In x K orthonormal
+// (the same launches as the R31 branch of sketch, for the driver that overlaps the QRs).  False
+// (nothing launched) when the fp16-split form does not apply.
+bool Engine::power_step_r31(const TView& X, const float* data, int n, int K, const double* Qy, double* Yt) {
+  const int N = X.N;
+  const Box bx = X.box(n);
+  const bool last = (n == N - 1);
+  if (!ctx.tc_h16 || ctx.simt() || ctx.power_qrz || (last && dist()) || (K % 4) != 0 ||
+      !ttm_s_tc_ok(ctx, data, bx, K) || !xs_slot || xs_key != data)
+    return false;
+  const int64_t In = bx.I, Jl = bx.J(), ldz = K;
+  const auto mk = ws.mark();
+  const int64_t ldz2 = 2 * int64_t(tc_npad(K));
+  float* Z = ws.alloc_n<float>(Jl * ldz);
+  float* Z2 = reinterpret_cast<float*>(ws.alloc_n<uint16_t>(Jl * ldz2));
+  int64_t ldqt;
+  const float* QyT = working_copy<float>(ctx, ws, Qy, In, K, In, ldqt);
+  const float* xsc = xs_slot;
+  const float* zsc = xs_slot + 1;
+  const int ez = int(std::ceil(0.5 * std::log2(double(X.Ig(n)))));
+  const float hz = std::ldexp(1.0f, -(ez + 1));
+  {
+    LabelScope ls(ctx, "ttm_t_tc_pow");
+    RT_REQUIRE(ttm_t_tc(ctx, ws, data, bx, QyT, ldqt, K, Z2, ldz2, 1, bx.a * ldz2, 2, false, xsc, nullptr, zsc, hz, true) &&
+                   ttm_t_tc(ctx, ws, data, bx, QyT, ldqt, K, Z, ldz, 1, bx.a * ldz, 0, false, nullptr, xsc, zsc, hz),
+               kEUNSUPPORTED, "power iteration: Z pass rejected by the tensor-core path");
+  }
+  {
+    LabelScope ls(ctx, "ttm_s_tc_pow");
+    RT_REQUIRE(ttm_s_tc(ctx, ws, data, bx, Z2, ldz2, false, K, Yt, In, true, xsc, nullptr, Z, ldz), kEUNSUPPORTED,
+               "pre-split power product not launched");
+  }
+  allreduce(comm, !last && dist(), Yt, In * K, ctx.stream);                         // C1
+  ws.rewind(mk);
+  return true;
+}
+
+// HOSVD with the thin QRs on a second stream (SURVEY.md H7 / reading R9: the modes are independent):
+// every QR of a replicated sketch runs on the handle's side stream while the main stream streams X
+// for the next mode's sketch or power step; the main stream waits for a QR only when it needs its
+// Q.  Order: the first sketches of all modes, then the power steps mode by mode (iteration outer),
+// then core, truncation and error.  The slab mode of a distributed run (row-distributed QR with
+// collectives) runs entirely on the main stream.  The side stream's allocations come from the
+// handle's second arena, so the main stream's scoped reuse never touches them.
+bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, int q, const void* const* omega,
+                           const int64_t* omega_cols, const int64_t* omega_ld, double* const* Q_out, double* G_out,
+                           double* E, double* Eg) {
+  const int N = X.N;
+  if (!ctx.side_stream || !ctx.side_ws || !ctx.events || ctx.simt()) return false;
+  int64_t K[5];
+  for (int n = 0; n < N; ++n) {
+    K[n] = omega_cols[n * N + n];
+    const bool main_only = dist() && n == N - 1;
+    // every power step must take the R31 form (checked before anything is launched)
+    if (q > 0 && !main_only &&
+        (!ctx.tc_h16 || ctx.power_qrz || (K[n] % 4) != 0 || !ttm_s_tc_ok(ctx, data, X.box(n), int(K[n]))))
+      return false;
+  }
+  const auto mk = ws.mark();
+  xs_slot = ws.alloc_n<float>(2);
+  xs_key = nullptr;
+  Ctx sctx = ctx;
+  sctx.stream = ctx.side_stream;
+  sctx.label = nullptr;
+  Engine se(sctx, *ctx.side_ws, comm);
+  double* Yt[5];
+  double* Qy[5];
+  double* Qt[5];
+  int64_t ldq[5];
+  cudaEvent_t done_q[5];
+  auto fork_qr = [&](int n, double* Q) {      // side stream: Q = qr(Yt[n]) after the work enqueued so far
+    cudaEvent_t e = ctx.events->get();
+    RT_CUDA(cudaEventRecord(e, ctx.stream));
+    RT_CUDA(cudaStreamWaitEvent(sctx.stream, e, 0));
+    se.qr_y(Yt[n], X.d[n], X.Ig(n), int(K[n]), X.d[n], Q, X.d[n], nullptr, false, 0);
+    done_q[n] = ctx.events->get();
+    RT_CUDA(cudaEventRecord(done_q[n], sctx.stream));
+  };
+  auto wait_q = [&](int n) { RT_CUDA(cudaStreamWaitEvent(ctx.stream, done_q[n], 0)); };
+  const int saved_reserve = ctx.sm_reserve;
+  ctx.sm_reserve = 2;                         // persistent X-pass grids leave SMs for the side stream
+  for (int n = 0; n < N; ++n) {
+    const int64_t In = X.d[n];
+    Yt[n] = ws.alloc_n<double>(In * K[n]);
+    Qy[n] = ws.alloc_n<double>(In * K[n]);
+    Qt[n] = ws.alloc_n<double>(In * K[n]);
+    ldq[n] = In;
+    done_q[n] = nullptr;
+  }
+  for (int n = 0; n < N; ++n) {                // first sketches; their QRs on the side stream
+    const void* const* om = omega + n * N;
+    const int64_t* oc = omega_cols + n * N;
+    const int64_t* ol = omega_ld + n * N;
+    const bool last = n == N - 1;
+    if (dist() && last) {                      // slab mode: the whole mode on the main stream
+      sketch<float>(X, data, n, 0, om, oc, ol, q, Yt[n]);
+      qr_y(Yt[n], X.d[n], X.Ig(n), int(K[n]), X.d[n], Qt[n], X.d[n], nullptr, true, X.off);
+      continue;
+    }
+    sketch<float>(X, data, n, 0, om, oc, ol, q, Yt[n], /*first_only=*/true);
+    fork_qr(n, q > 0 ? Qy[n] : Qt[n]);
+  }
+  for (int it = 0; it < q; ++it)                // power steps (R31), each QR forked again
+    for (int n = 0; n < N; ++n) {
+      if (dist() && n == N - 1) continue;
+      wait_q(n);
+      RT_REQUIRE(power_step_r31(X, data, n, int(K[n]), Qy[n], Yt[n]), kEUNSUPPORTED, "power step not launched");
+      fork_qr(n, it == q - 1 ? Qt[n] : Qy[n]);
+    }
+  for (int n = 0; n < N; ++n)
+    if (done_q[n]) wait_q(n);                  // join
+  ctx.sm_reserve = saved_reserve;
+  int64_t gsz = 1;
+  for (int n = 0; n < N; ++n) gsz *= K[n];
+  double* Gt = ws.alloc_n<double>(gsz);
+  core<float>(X, data, Qt, ldq, K, Gt);
+  truncate(X, Gt, K, Qt, ldq, R, Q_out, G_out);
+  if (E || Eg) rel_error<float>(X, data, G_out, R, Q_out, E, Eg);
+  ws.rewind(mk);
+  xs_slot = nullptr;
+  return true;
 }
 
 // ---------------------------------------------------------------------- core (a5)
@@ -616,6 +745,11 @@ void Engine::hosvd(const TView& X, const int64_t* R, int q, int kind, const void
                    double* Eg) {
   const int N = X.N;
   const T* data = static_cast<const T*>(X.data);
+  if constexpr (std::is_same<T, float>::value) {
+    if (kind == 0 && ctx.overlap &&
+        hosvd_overlap(X, data, R, q, omega, omega_cols, omega_ld, Q_out, G_out, E, Eg))
+      return;
+  }
   const auto mk = ws.mark();
   xs_slot = ws.alloc_n<float>(2);      // X's fp16 scale, taken once for all modes' power products
   xs_key = nullptr;
@@ -958,9 +1092,9 @@ template void Engine::pet<double>(const TView&, const int64_t*, const void* cons
                                   const void* const*, const int64_t*, const int64_t*, double* const*, double*, double*,
                                   double*);
 template void Engine::sketch<float>(const TView&, const float*, int, int, const void* const*, const int64_t*,
-                                    const int64_t*, int, double*);
+                                    const int64_t*, int, double*, bool);
 template void Engine::sketch<double>(const TView&, const double*, int, int, const void* const*, const int64_t*,
-                                     const int64_t*, int, double*);
+                                     const int64_t*, int, double*, bool);
 template bool Engine::qr_z<float>(float*, int64_t, int64_t, int64_t, int, bool, int64_t, float*, int64_t, int,
                                   const float*);
 template bool Engine::qr_z<double>(double*, int64_t, int64_t, int64_t, int, bool, int64_t, double*, int64_t, int,

@@ -1719,7 +1719,7 @@ bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q
       p.tma_out = make_map(&to, out, 2, d, st, bx, true, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
     }
   }
-  const int64_t grid = std::min<int64_t>(p.ntiles, ctx.num_sms);
+  const int64_t grid = std::min<int64_t>(p.ntiles, std::max(1, ctx.num_sms - ctx.sm_reserve));
 #define RT_T_CASE(NP)                                                     \
   case NP:                                                                \
     if (h16) {                                                           \
