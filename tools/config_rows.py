@@ -101,6 +101,7 @@ def main():
     ap.add_argument("--configs", nargs="+", default=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--oracle-elems", type=float, default=6.0e7)
+    ap.add_argument("--profile", action="store_true", help="top kernel classes of each run to stderr")
     a = ap.parse_args()
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
     for name in a.configs:
@@ -129,6 +130,15 @@ def main():
                              sthosvd_bytes(cfg, cfg.q)))
         for label, algo, fn, nbytes in runs:
             ms, res = timed(h, fn, a.reps)
+            if a.profile:
+                h.profile_read()
+                h.set_option(1, 1)
+                fn()
+                h.sync()
+                h.set_option(1, 0)
+                prof = sorted(h.profile_read()[0], key=lambda e: -e[2])
+                print(f"[{name} {label}] " + ", ".join(f"{n}:{c}x {t:.3f}" for n, c, t in prof[:16]), file=sys.stderr,
+                      flush=True)
             # the residual pass (a8) timed apart: E of the same factors through rtucker_core
             ms_e, _ = timed(h, lambda: P.rtucker_core(h, X, res["Q"], with_error=True), a.reps)
             ms_c, _ = timed(h, lambda: P.rtucker_core(h, X, res["Q"], with_error=False), a.reps)
