@@ -340,6 +340,7 @@ struct SParams {
   int64_t cpb;        // chunks per beta (a > 1)
   int64_t nchunks;    // total j-chunks
   int64_t per;        // chunks per split (a multiple of the X stage width)
+  int xfirst;         // wide rows: 1 = X tiles with L2::evict_first like the 1-chunk stages (A/B option)
   int seg;            // chunks per accumulator segment
   int ablate;         // profiling only: 1 = no MMA, 2 = no split work (results invalid)
   int skew;           // chunk-order rotation per M-tile (decorrelates the rows' DRAM addresses)
@@ -442,7 +443,9 @@ ttm_s_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
   if (warp == 0) {
     if (lane == 0) {                                   // ---------------- X producer (one box per XW chunks)
       Ring rx;
-      const uint64_t pol = policy_evict_first();
+      // wide rows: the 16 B pad sector is read again by the next stage, so X lines keep the normal
+      // L2 priority there (evict_first sends the re-read to DRAM)
+      const uint64_t pol = (XW > 1 && !p.xfirst) ? policy_evict_normal() : policy_evict_first();
       int xi = 0;
       for (int it = 0; it < nch; it += XW, ++xi, rx.next<NX>()) {
         if (xi >= NX) RT_TIMED(p.tim, 0, mbar_wait(&b.x_free[rx.s], rx.ph ^ 1));
@@ -699,7 +702,9 @@ ttm_s_h16_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant_
   if (warp == 0) {
     if (lane == 0) {                                   // ---------------- X producer (one box per XW chunks)
       Ring rx;
-      const uint64_t pol = policy_evict_first();
+      // wide rows: the 16 B pad sector is read again by the next stage, so X lines keep the normal
+      // L2 priority there (evict_first sends the re-read to DRAM)
+      const uint64_t pol = (XW > 1 && !p.xfirst) ? policy_evict_normal() : policy_evict_first();
       int xi = 0;
       for (int it = 0; it < nch; it += XW, ++xi, rx.next<NX>()) {
         if (xi >= NX) mbar_wait(&b.x_free[rx.s], rx.ph ^ 1);
@@ -1558,6 +1563,7 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
   p.seg = std::max(1, ctx.tc_seg);
   p.ablate = ctx.tc_ablate;
   p.skew = ctx.tc_skew >= 0 ? ctx.tc_skew : 0;
+  p.xfirst = ctx.tc_xfirst;
   p.part = ws.alloc_n<float>(splits * K * box.I);
   p.amax = h16 ? nullptr : amax;
   p.gate = nullptr;
