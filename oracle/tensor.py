@@ -59,4 +59,5 @@ def reconstruct(g: np.ndarray, factors) -> np.ndarray:
 
 
 def fro(x: np.ndarray) -> float:
-    return float(np.linalg.norm(np.asarray(x, dtype=np.float64).ravel()))
+    """Frobenius norm sqrt(sum x^2), read in memory order (no copy of a strided view)."""
+    return float(np.linalg.norm(np.asarray(x, dtype=np.float64).ravel(order="K")))
