@@ -66,7 +66,7 @@ class Engine {
   // (3) core G~ = X x_n Qt_n^T (all n) -> fp64 Gt (replicated)
   template <typename T>
   void core(const TView& X, const T* data, const double* const* Qt, const int64_t* ldq, const int64_t* K,
-            double* Gt);
+            double* Gt, const T* stage0 = nullptr);
   // (a6) truncation of the oversampled core: Q_out, G_out from Gt, Qt
   void truncate(const TView& X, const double* Gt, const int64_t* K, const double* const* Qt,
                 const int64_t* ldq, const int64_t* R, double* const* Q_out, double* G_out);

@@ -71,6 +71,13 @@ void x_scale_from_amax(const Ctx& ctx, const unsigned int* amax, int64_t n, floa
 // distributed form: every rank's stats as a (max, sum) double pair (x_stat_pair), allgathered
 void x_stat_pair(const Ctx& ctx, const unsigned int* amax, double* pair);
 void x_scale_from_gathered(const Ctx& ctx, const double* pairs, int nranks, int64_t n_glob, float* s);
+// Fused pass (fp32 X, fp16 split): the mode-1 Omega sketch Y = X_(1) Omega_1 and the first core stage
+// out = X x_1 Q~_0^T share one read of X (sketch1_core0_kernel).  b1 / b0: X as the mode-1 / mode-0
+// box; Om row-major J x K1 (ld), Q0 col-major I_0 x K0 (ld, orthonormal); xs: X's scale pair; Y fp64
+// I_1 x K1 (ldy); out: the core stage rows (K0 floats per row j of the mode-0 unfolding).  False
+// (nothing launched) when the shape is outside the fused kernel.
+bool sketch1_core0(const Ctx& ctx, Arena& ws, const float* X, Box b1, Box b0, const float* Om, int64_t ldom, int K1,
+                   const float* Q0, int64_t ldq0, int K0, const float* xs, double* Y, int64_t ldy, float* out);
 // out = xs with out[0] = 0 unless max|Q| < 2 (Q fp32 col-major m x r, ld): the fp16 split of an X pass
 // with Q (2^14 Q must stay inside the fp16 range) then stands down for its tf32 twin
 void q_gate_scale(const Ctx& ctx, const float* Q, int64_t m, int r, int64_t ld, const float* xs, float* out);

@@ -483,11 +483,14 @@ bool Engine::power_step_r31(const TView& X, const float* data, int n, int K, con
 
 // HOSVD with the thin QRs on a second stream (SURVEY.md H7 / reading R9: the modes are independent):
 // every QR of a replicated sketch runs on the handle's side stream while the main stream streams X
-// for the next mode's sketch or power step; the main stream waits for a QR only when it needs its
-// Q.  Order: the first sketches of all modes, then the power steps mode by mode (iteration outer),
-// then core, truncation and error.  The slab mode of a distributed run (row-distributed QR with
-// collectives) runs entirely on the main stream.  The side stream's allocations come from the
-// handle's second arena, so the main stream's scoped reuse never touches them.
+// for another mode's sketch or power step; the main stream waits for a QR only when it needs its
+// Q.  The slab mode of a distributed run (row-distributed QR with collectives) runs entirely on the
+// main stream.  The side stream's allocations come from the handle's second arena, so the main
+// stream's scoped reuse never touches them.
+// With q > 0 the first core stage G1 = X x_1 Q~_0^T shares its pass over X with the mode-1 Omega sketch
+// (sketch1_core0: 10 instead of 11 passes over X for a 3-way tensor): mode 0 is finished first, the
+// other modes' power steps hide its last QR, then the fused pass, then mode 1's power steps.
+// Order (q = 1, N = 3): S0, S2, P0, P2, [S1 + G1], P1 (S = first sketch, P = Z pass + power product).
 bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, int q, const void* const* omega,
                            const int64_t* omega_cols, const int64_t* omega_ld, double* const* Q_out, double* G_out,
                            double* E, double* Eg) {
@@ -502,6 +505,9 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
         (!ctx.tc_h16 || ctx.power_qrz || (K[n] % 4) != 0 || !ttm_s_tc_ok(ctx, data, X.box(n), int(K[n]))))
       return false;
   }
+  // fused mode-1 sketch + first core stage: needs X's scale (q > 0) and mode 1 off the slab
+  const bool try_fuse = q > 0 && N >= 2 && !ctx.fuse_off && ctx.tc_h16 && !(dist() && N - 1 == 1) &&
+                        (omega_ld[1 * N + 1] % 4) == 0;
   const auto mk = ws.mark();
   xs_slot = ws.alloc_n<float>(2);
   xs_key = nullptr;
@@ -533,33 +539,71 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
     ldq[n] = In;
     done_q[n] = nullptr;
   }
-  for (int n = 0; n < N; ++n) {                // first sketches; their QRs on the side stream
+  int it_done[5] = {0, 0, 0, 0, 0};            // power steps taken per mode
+  auto first_sketch = [&](int n) {
     const void* const* om = omega + n * N;
     const int64_t* oc = omega_cols + n * N;
     const int64_t* ol = omega_ld + n * N;
-    const bool last = n == N - 1;
-    if (dist() && last) {                      // slab mode: the whole mode on the main stream
+    if (dist() && n == N - 1) {               // slab mode: the whole mode on the main stream
       sketch<float>(X, data, n, 0, om, oc, ol, q, Yt[n]);
       qr_y(Yt[n], X.d[n], X.Ig(n), int(K[n]), X.d[n], Qt[n], X.d[n], nullptr, true, X.off);
-      continue;
+      it_done[n] = q;
+      return;
     }
     sketch<float>(X, data, n, 0, om, oc, ol, q, Yt[n], /*first_only=*/true);
     fork_qr(n, q > 0 ? Qy[n] : Qt[n]);
-  }
-  for (int it = 0; it < q; ++it)                // power steps (R31), each QR forked again
-    for (int n = 0; n < N; ++n) {
-      if (dist() && n == N - 1) continue;
+  };
+  auto power_all = [&](int n) {               // the remaining power steps of mode n
+    if (dist() && n == N - 1) return;
+    for (; it_done[n] < q; ++it_done[n]) {
       wait_q(n);
       RT_REQUIRE(power_step_r31(X, data, n, int(K[n]), Qy[n], Yt[n]), kEUNSUPPORTED, "power step not launched");
-      fork_qr(n, it == q - 1 ? Qt[n] : Qy[n]);
+      fork_qr(n, it_done[n] == q - 1 ? Qt[n] : Qy[n]);
     }
+  };
+  float* g1 = nullptr;                         // the first core stage from the fused pass
+  if (try_fuse) {
+    first_sketch(0);
+    for (int n = 2; n < N; ++n) first_sketch(n);
+    power_all(0);                              // Q~_0 after its last QR
+    for (int n = 2; n < N; ++n) power_all(n);  // hides that QR
+    wait_q(0);
+    const Box b1 = X.box(1), b0 = X.box(0);
+    int64_t ld0;
+    const float* q0 = working_copy<float>(ctx, ws, Qt[0], X.d[0], K[0], ldq[0], ld0);
+    float* g = ws.alloc_n<float>(b0.b * K[0]);
+    bool fused;
+    {
+      LabelScope ls(ctx, "sketch1_core0");
+      fused = sketch1_core0(ctx, ws, data, b1, b0, static_cast<const float*>(omega[1 * N + 1]), omega_ld[1 * N + 1],
+                            int(K[1]), q0, ld0, int(K[0]), xs_slot, Yt[1], X.d[1], g);
+    }
+    if (fused) {
+      allreduce(comm, N - 1 != 1 && dist(), Yt[1], X.d[1] * K[1], ctx.stream);   // C1
+      set_status_if_nonfinite(ctx, Yt[1], X.d[1] * K[1]);
+      fork_qr(1, Qy[1]);
+      g1 = g;
+    } else {
+      first_sketch(1);
+    }
+    power_all(1);
+  } else {
+    for (int n = 0; n < N; ++n) first_sketch(n);
+    for (int it = 0; it < q; ++it)           // power steps, iteration outer
+      for (int n = 0; n < N; ++n) {
+        if (dist() && n == N - 1) continue;
+        wait_q(n);
+        RT_REQUIRE(power_step_r31(X, data, n, int(K[n]), Qy[n], Yt[n]), kEUNSUPPORTED, "power step not launched");
+        fork_qr(n, it == q - 1 ? Qt[n] : Qy[n]);
+      }
+  }
   for (int n = 0; n < N; ++n)
     if (done_q[n]) wait_q(n);                  // join
   ctx.sm_reserve = saved_reserve;
   int64_t gsz = 1;
   for (int n = 0; n < N; ++n) gsz *= K[n];
   double* Gt = ws.alloc_n<double>(gsz);
-  core<float>(X, data, Qt, ldq, K, Gt);
+  core<float>(X, data, Qt, ldq, K, Gt, g1);
   truncate(X, Gt, K, Qt, ldq, R, Q_out, G_out);
   if (E || Eg) rel_error<float>(X, data, G_out, R, Q_out, E, Eg);
   ws.rewind(mk);
@@ -568,9 +612,10 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
 }
 
 // ---------------------------------------------------------------------- core (a5)
+// stage0 (nullable): the first stage X x_1 Q~_0^T already computed (the fused pass of hosvd_overlap)
 template <typename T>
 void Engine::core(const TView& X, const T* data, const double* const* Qt, const int64_t* ldq, const int64_t* K,
-                  double* Gt) {
+                  double* Gt, const T* stage0) {
   const int N = X.N;
   const auto mk = ws.mark();
   const T* QT[5];
@@ -593,6 +638,8 @@ void Engine::core(const TView& X, const T* data, const double* const* Qt, const 
     if (s2 == N - 1) {
       LabelScope ls(ctx, "core_last");
       ttm_t<T, T, double>(ctx, src, b, QT[n], 1, ld, int(K[n]), Gt, 1, b.a, b.a * K[n]);
+    } else if (s2 == 0 && stage0) {
+      src = stage0;
     } else {
       T* dst = ws.alloc_n<T>(b.a * K[n] * b.b);
       LabelScope ls(ctx, s2 == 0 ? "core_first" : "core_mid");
@@ -1104,9 +1151,9 @@ template void Engine::qr_rows<float>(const float*, int64_t, int64_t, int, int64_
 template void Engine::qr_rows<double>(const double*, int64_t, int64_t, int, int64_t, double*, int64_t, double*,
                                       bool, int64_t, const double*, const int64_t*);
 template void Engine::core<float>(const TView&, const float*, const double* const*, const int64_t*,
-                                  const int64_t*, double*);
+                                  const int64_t*, double*, const float*);
 template void Engine::core<double>(const TView&, const double*, const double* const*, const int64_t*,
-                                   const int64_t*, double*);
+                                   const int64_t*, double*, const double*);
 template void Engine::rel_error<float>(const TView&, const float*, const double*, const int64_t*,
                                        const double* const*, double*, double*);
 template void Engine::rel_error<double>(const TView&, const double*, const double*, const int64_t*,

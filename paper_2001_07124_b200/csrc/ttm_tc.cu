@@ -1153,6 +1153,285 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
+// ================================================= fused mode-1 sketch + mode-0 core stage (fp16)
+// One pass over X feeds two contractions that read the same A tile.  In the mode-1 view
+// [a = I_0, I = I_1, b = the later modes] a chunk is X(alpha0..alpha0+31, i1 tile, beta):
+//   the Omega sketch of mode 1:  Y_1(i1, k)       += sum_alpha X(alpha, i1, beta) Omega_1(alpha + a beta, k)
+//   the first core stage:        G1(c, i1, beta)  += sum_alpha X(alpha, i1, beta) Q~_0(alpha, c)
+// (the core contracts mode 0 first, Eq. Core; the sketch is Alg.6 line 3 P:556 for n = 1).
+// X is split once per chunk into fp16 hi/lo A operands in TMEM (R29); B is one K-major 128 B-swizzled
+// slot per chunk pair holding [2^14 Q_hi^T | 2^11 Omega^T | 2^14 Q_lo^T] (3 NPAD rows x 64 K):
+//   issuer 0: A_hi [Q_hi | Omega | Q_lo] -> TMEM [C0 | S0 | C1a]   (N = 3 NPAD)
+//   issuer 1: A_lo [Q_hi | Omega]        -> TMEM [C1b | S1]        (N = 2 NPAD)
+// with Omega tf32-exact (RT_OPT_OMEGA_TF32: exact in fp16 at 2^11, no Omega_lo).  The sketch sums S0 + S1
+// over the whole chunk range of the CTA (split-K partials, as ttm_s); the core rows C0 + C1a + C1b
+// are complete after the cpb chunks of one beta and leave through TMA stores.
+struct FParams {
+  int64_t a, I, b;
+  int K, C;            // sketch width (mode 1), core width (mode 0)
+  int64_t cpb;         // chunks per beta (a / 32)
+  int64_t nchunks, per;
+  int seg;             // chunks per accumulator segment (divides cpb)
+  float* part;         // [split][K][I] sketch partials
+  const float* xscale; // device s (0: the tf32 twins run)
+  float binv_s, binv_c;
+  unsigned int* runs;
+};
+
+template <int NPAD>
+struct PlanF {
+  static constexpr int XW = 2, NB = 3, NBB = 2;
+  static constexpr uint32_t c0 = 0, s0 = NPAD, c1a = 2 * NPAD, c1b = 3 * NPAD, s1 = 4 * NPAD;
+  static constexpr uint32_t a_base = (5u * NPAD + 31u) & ~31u;
+  static_assert(a_base + 32u * NB <= 512u, "fused TMEM plan");
+  __host__ __device__ static constexpr uint32_t a_slot(int s) { return a_base + 32u * uint32_t(s); }
+  static constexpr uint32_t kX = uint32_t(BM) * x_pitch<XW>();
+  static constexpr uint32_t kB = 3u * NPAD * 128u;                   // one chunk pair: 64 K x 3 NPAD rows
+  static constexpr uint32_t kO = uint32_t(BM) * ((NPAD + 31) / 32) * 128u;   // core output staging
+  static constexpr uint32_t budget = 224u * 1024u;
+  static constexpr int NX_fit = int((budget - NBB * kB - kO) / kX);
+  static constexpr int NX = NX_fit > 4 ? 4 : NX_fit;
+  static constexpr uint32_t off_x = 0, off_b = off_x + NX * kX, off_o = off_b + NBB * kB, off_bar = off_o + kO;
+  static constexpr int nbar = 2 * NX + 2 * NBB + 2 * NB + 4;
+  static constexpr uint32_t bytes = off_bar + 8 * nbar + 16;
+  static_assert(NX >= 2 && kB % 1024 == 0 && kX % 1024 == 0, "fused smem plan");
+};
+
+template <int NPAD>
+__global__ void __launch_bounds__(NT_TTM, 1)
+sketch1_core0_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmq,
+                     const __grid_constant__ CUtensorMap tmw, const __grid_constant__ CUtensorMap tmc,
+                     const FParams p) {
+  using L = PlanF<NPAD>;
+  constexpr int NX = L::NX, NB = L::NB, NBB = L::NBB, XW = L::XW;
+  if (*p.xscale == 0.f) return;                        // the tf32 twins run instead (R29)
+  if (p.runs && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) atomicAdd(&p.runs[0], 1u);
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::off_bar);
+  uint64_t* x_full = bar;
+  uint64_t* x_free = bar + NX;
+  uint64_t* b_full = bar + 2 * NX;
+  uint64_t* b_free = bar + 2 * NX + NBB;
+  uint64_t* ready = bar + 2 * NX + 2 * NBB;
+  uint64_t* tfree = ready + NB;
+  uint64_t* acc_full = tfree + NB;
+  uint64_t* acc_empty = acc_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + L::nbar);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t z = blockIdx.y;
+  const int64_t i0 = int64_t(blockIdx.x) * BM;
+  const int64_t cbeg = z * p.per;
+  const int nch = cbeg < p.nchunks ? int(min(p.per, p.nchunks - cbeg)) : 0;   // a multiple of cpb
+  auto coords = [&](int it, int64_t& a0, int64_t& beta) {
+    const int64_t c = cbeg + it;
+    beta = c / p.cpb;
+    a0 = (c % p.cpb) * KC;
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NX; ++s) { mbar_init(&x_full[s], 1); mbar_init(&x_free[s], 128); }
+    for (int s = 0; s < NBB; ++s) { mbar_init(&b_full[s], 1); mbar_init(&b_free[s], 2); }
+    for (int s = 0; s < NB; ++s) { mbar_init(&ready[s], 128); mbar_init(&tfree[s], 2); }
+    mbar_init(acc_full, 2);
+    mbar_init(acc_empty, 128);
+    fence_barrier_init();
+    tma_prefetch(&tmx); tma_prefetch(&tmq); tma_prefetch(&tmw); tma_prefetch(&tmc);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {                                   // ---------------- X producer (XW chunks per box)
+      Ring rx;
+      const uint64_t pol = policy_evict_normal();
+      int xi = 0;
+      for (int it = 0; it < nch; it += XW, ++xi, rx.next<NX>()) {
+        if (xi >= NX) mbar_wait(&x_free[rx.s], rx.ph ^ 1);
+        int64_t a0, beta;
+        coords(it, a0, beta);
+        mbar_expect_tx(&x_full[rx.s], L::kX);
+        tma_load_3d_hint(smem + L::off_x + rx.s * L::kX, &tmx, &x_full[rx.s], int(a0), int(i0), int(beta), pol);
+      }
+    }
+  } else if (warp == 6) {
+    if (lane == 0) {                                   // ---------------- B producer (one slot per chunk pair)
+      Ring rb;
+      const uint64_t pol = policy_evict_last();
+      int bi = 0;
+      for (int it = 0; it < nch; it += 2, ++bi, rb.next<NBB>()) {
+        if (bi >= NBB) mbar_wait(&b_free[rb.s], rb.ph ^ 1);
+        int64_t a0, beta;
+        coords(it, a0, beta);
+        uint8_t* dst = smem + L::off_b + rb.s * L::kB;
+        mbar_expect_tx(&b_full[rb.s], L::kB);
+        tma_load_2d_hint(dst, &tmq, &b_full[rb.s], int(a0), 0, pol);                              // 2^14 Q_hi^T
+        tma_load_2d_hint(dst + NPAD * 128, &tmw, &b_full[rb.s], int(a0 + p.a * beta), 0, pol);    // 2^11 Omega^T
+        tma_load_2d_hint(dst + 2 * NPAD * 128, &tmq, &b_full[rb.s], int(a0), NPAD, pol);          // 2^14 Q_lo^T
+      }
+    }
+  } else if (warp == 1 || warp == 7) {
+    const int q = warp == 1 ? 0 : 1;                   // ---------------- MMA issuers (whole warp)
+    const uint32_t idesc = idesc_f16(BM, q == 0 ? 3 * NPAD : 2 * NPAD, 0);
+    const uint32_t d = tmem + (q == 0 ? L::c0 : L::c1b);
+    int64_t u = 0;
+    int pos = 0;
+    for (int it = 0; it < nch; ++it) {
+      const bool first = pos == 0;
+      const bool last = (pos == p.seg - 1) || (it == nch - 1);
+      const int sl = it % NB;
+      if (first && u >= 1) mbar_wait(acc_empty, uint32_t(u - 1) & 1u);
+      mbar_wait(&ready[sl], uint32_t(it / NB) & 1u);   // A split, B pair landed
+      tc_fence_after();
+      const uint32_t bsa = smem_u32(smem + L::off_b + ((it / 2) % NBB) * L::kB);
+      const uint32_t a = tmem + L::a_slot(sl) + (q == 0 ? 0u : 16u);
+#pragma unroll
+      for (int kk = 0; kk < KC / 16; ++kk)
+        mma_f16_ts_w(d, a + 8 * kk, bdesc_sw128(bsa, 2 * (it & 1) + kk), idesc, (first && kk == 0) ? 0u : 1u);
+      mma_commit_w(&tfree[sl]);
+      if (it & 1) mma_commit_w(&b_free[(it / 2) % NBB]);
+      if (last) { mma_commit_w(acc_full); ++u; pos = 0; } else { ++pos; }
+    }
+  } else if (warp >= 2 && warp <= 5) {                 // ---------------- splitters
+    const int q4 = warp & 3;
+    const int r = 32 * q4 + lane;
+    const uint32_t lane_base = tmem + (uint32_t(32 * q4) << 16);
+    const float sc = *p.xscale;
+    Ring rx;
+    for (int it = 0; it < nch; ++it) {
+      const int sl = it % NB, cx = it % XW;
+      if (cx == 0) mbar_wait(&x_full[rx.s], rx.ph);
+      if (it >= NB) mbar_wait(&tfree[sl], (uint32_t(it / NB) & 1u) ^ 1u);   // the A slot's MMAs done
+      const float* xs = reinterpret_cast<const float*>(smem + L::off_x + rx.s * L::kX);
+      split_wrow_to_tmem_h16(xs + r * (KC * XW + 4) + KC * cx, sc, lane_base + L::a_slot(sl));
+      if (cx == XW - 1 || it == nch - 1) { mbar_arrive(&x_free[rx.s]); rx.next<NX>(); }
+      mbar_wait(&b_full[(it / 2) % NBB], uint32_t((it / 2) / NBB) & 1u);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&ready[sl]);
+    }
+  } else if (warp >= 8) {                              // ---------------- epilogue
+    const int q4 = warp & 3;
+    const int r = 32 * q4 + lane;
+    const uint32_t lane_base = tmem + (uint32_t(32 * q4) << 16);
+    float sums[NPAD];
+#pragma unroll
+    for (int k = 0; k < NPAD; ++k) sums[k] = 0.f;
+    const float inv_c = p.binv_c / *p.xscale;           // exact: powers of two
+    const int spb = int(p.cpb / p.seg);                 // segments per beta
+    const int nseg = nch / p.seg;
+    uint8_t* stage = smem + L::off_o;
+    for (int u = 0; u < nseg; ++u) {
+      const int ub = u % spb;
+      if (ub == 0 && u > 0) {                          // the previous beta's stores have read the staging
+        if (r == 0) bulk_wait_read0();
+        named_bar(1, 128);
+      }
+      mbar_wait(acc_full, uint32_t(u) & 1u);
+      tc_fence_after();
+      add_cols<NPAD>(lane_base + L::s0, sums);          // A_hi Omega
+      add_cols<NPAD>(lane_base + L::s1, sums);          // A_lo Omega
+      const bool fin = ub == spb - 1;
+#pragma unroll
+      for (int c0 = 0; c0 < NPAD; c0 += 16) {
+        uint32_t v0[16], v1[16], v2[16];
+        tmem_ld16(lane_base + L::c0 + c0, v0);
+        tmem_ld16(lane_base + L::c1a + c0, v1);
+        tmem_ld16(lane_base + L::c1b + c0, v2);
+        tmem_wait_ld();
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const int c = c0 + 4 * g;
+          float4* dst = reinterpret_cast<float4*>(stage + (c >> 5) * (BM * 128) + r * 128 + ((((c & 31) >> 2) ^ (r & 7)) << 4));
+          float4 v;
+          v.x = __uint_as_float(v0[4 * g + 0]) + (__uint_as_float(v1[4 * g + 0]) + __uint_as_float(v2[4 * g + 0]));
+          v.y = __uint_as_float(v0[4 * g + 1]) + (__uint_as_float(v1[4 * g + 1]) + __uint_as_float(v2[4 * g + 1]));
+          v.z = __uint_as_float(v0[4 * g + 2]) + (__uint_as_float(v1[4 * g + 2]) + __uint_as_float(v2[4 * g + 2]));
+          v.w = __uint_as_float(v0[4 * g + 3]) + (__uint_as_float(v1[4 * g + 3]) + __uint_as_float(v2[4 * g + 3]));
+          if (ub > 0) {
+            const float4 o = *dst;
+            v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+          }
+          if (fin) { v.x *= inv_c; v.y *= inv_c; v.z *= inv_c; v.w *= inv_c; }
+          *dst = v;
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(acc_empty);
+      if (fin) {                                       // beta complete: rows i1 + I beta of the core stage
+        fence_proxy_async();
+        named_bar(1, 128);
+        if (r == 0) {
+          int64_t a0, beta;
+          coords(u * p.seg, a0, beta);
+          const int row0 = int(i0 + p.I * beta);
+#pragma unroll
+          for (int bx = 0; bx < (NPAD + 31) / 32; ++bx)
+            if (32 * bx < p.C) tma_store_2d(&tmc, stage + bx * (BM * 128), 32 * bx, row0);
+          bulk_commit();
+        }
+      }
+    }
+    if (r == 0) bulk_wait0();
+    const float inv_s = p.binv_s / *p.xscale;
+    const int64_t i = i0 + r;
+    if (i < p.I) {
+      float* dst = p.part + z * p.K * p.I;
+#pragma unroll
+      for (int k = 0; k < NPAD; ++k)
+        if (k < p.K) dst[int64_t(k) * p.I + i] = sums[k] * inv_s;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+// Q (I x C fp32, col-major ldq) -> QT (fp16, 2 NPAD rows x ldt): rows c < C = 2^14 Q_hi[:, c]^T,
+// rows NPAD + c = 2^14 Q_lo[:, c]^T, other rows zero
+__global__ void qt16_kernel(const float* __restrict__ Q, int64_t I, int C, int64_t ldq, int npad,
+                            __half* __restrict__ QT, int64_t ldt) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= ldt * npad) return;
+  const int64_t i = e % ldt;
+  const int c = int(e / ldt);
+  const float v = (i < I && c < C) ? Q[i + ldq * c] * 16384.f : 0.f;
+  const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+  QT[int64_t(c) * ldt + i] = __float2half_rn(h);
+  QT[int64_t(npad + c) * ldt + i] = __float2half_rn(v - h);
+}
+
+// Omega (J x K fp32, row-major ld) -> WT (fp16, NPAD rows x ldw): row k = 2^11 Omega[:, k]^T (rows >= K
+// zero).  *flag = 1 if an entry is not exactly an fp16 at 2^11 (not tf32-exact, or out of range):
+// the fused kernel then stands down for its twins.  64 j-rows per block through shared memory.
+__global__ void __launch_bounds__(256) omega_t16_kernel(const float* __restrict__ Om, int64_t J, int K, int64_t ld,
+                                                        int npad, __half* __restrict__ WT, int64_t ldw,
+                                                        int* __restrict__ flag) {
+  __shared__ float t[64][129];
+  const int64_t j0 = int64_t(blockIdx.x) * 64;
+  bool bad = false;
+  for (int e = threadIdx.x; e < 64 * npad; e += blockDim.x) {
+    const int jl = e / npad, k = e % npad;
+    const int64_t j = j0 + jl;
+    t[jl][k] = (j < J && k < K) ? Om[j * ld + k] : 0.f;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 64 * npad; e += blockDim.x) {
+    const int k = e / 64, jl = e % 64;
+    const int64_t j = j0 + jl;
+    if (j >= ldw) continue;
+    const float v = t[jl][k] * 2048.f;
+    const __half hv = __float2half_rn(v);
+    // an entry in the fp16 normal range must be exact (a tf32-rounded Omega is); entries below it round
+    // with an absolute error <= 2^-25 (2^-36 of |Omega|): immaterial next to fp32
+    bad |= !(fabsf(v) < 32768.f) || (fabsf(v) >= 6.103515625e-05f && __half2float(hv) != v);
+    WT[int64_t(k) * ldw + j] = hv;
+  }
+  if (bad) atomicOr(flag, 1);
+}
+
 // ================================================================ host side
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -1751,6 +2030,118 @@ bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q
     default: return false;
   }
 #undef RT_T_CASE
+  return true;
+}
+
+
+// Fused mode-1 Omega sketch + mode-0 core stage (sketch1_core0_kernel); false (nothing launched) when
+// the shape / precision is outside it.  b1: X as the mode-1 box [I_0, I_1, rest]; b0: the mode-0 box.
+// Om: the fp32 Omega_1 (J x K1 row-major, ld ldom; tf32-exact for the fused form, else the flag sends
+// the work to the twins); Q0: Q~_0 fp32 col-major (I_0 x K0, ld ldq0, orthonormal); xs: X's scale pair.
+// Outputs: Y (fp64 I_1 x K1, ld ldy) and out (the core stage: rows j = i1 + I_1 beta of K0 floats).
+bool sketch1_core0(const Ctx& ctx, Arena& ws, const float* X, Box b1, Box b0, const float* Om, int64_t ldom, int K1,
+                   const float* Q0, int64_t ldq0, int K0, const float* xs, double* Y, int64_t ldy, float* out) {
+  if (ctx.simt() || !ctx.tc_h16 || ctx.fuse_off) return false;
+  const int npad = tc_npad(std::max(K0, K1));
+  if (npad < 0 || npad > 80) return false;
+  if (b1.a % 512 || b1.I % BM || (K0 % 4) || (ldom % 4) || !aligned(X, 16) || !aligned(Om, 16) || !aligned(out, 16))
+    return false;
+  const int64_t J = b1.J();
+  if (b1.a > INT32_MAX || b1.I > INT32_MAX || b1.b > INT32_MAX || J > INT32_MAX || b0.b > INT32_MAX) return false;
+  // B sources: 2^14 [Q_hi^T ; Q_lo^T] and 2^11 Omega^T in fp16, rows padded to npad
+  const int64_t ldt = (b1.a + 7) & ~int64_t(7), ldw = (J + 7) & ~int64_t(7);
+  __half* QT = ws.alloc_n<__half>(2 * npad * ldt);
+  __half* WT = ws.alloc_n<__half>(int64_t(npad) * ldw);
+  int* flag = ws.alloc_n<int>(1);
+  float* xso = ws.alloc_n<float>(2);
+  RT_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), ctx.stream));
+  launch(ctx, "qt16", [&] {
+    qt16_kernel<<<unsigned(cdiv(ldt * npad, 256)), 256, 0, ctx.stream>>>(Q0, b1.a, K0, ldq0, npad, QT, ldt);
+  });
+  launch(ctx, "omega_t16", [&] {
+    omega_t16_kernel<<<unsigned(cdiv(ldw, 64)), 256, 0, ctx.stream>>>(Om, J, K1, ldom, npad, WT, ldw, flag);
+  });
+  launch(ctx, "omega_gate", [&] { omega_gate_kernel<<<1, 1, 0, ctx.stream>>>(flag, xs, xso); });
+  CUtensorMap tx, tq, tw, tc;
+  {
+    const uint64_t d[3] = {uint64_t(b1.a), uint64_t(b1.I), uint64_t(b1.b)};
+    const uint64_t st[2] = {uint64_t(b1.a) * 4, uint64_t(b1.a) * b1.I * 4};
+    const uint32_t bx[3] = {uint32_t(KC * 2 + 4), BM, 1};
+    if (!make_map(&tx, X, 3, d, st, bx, false)) return false;
+  }
+  {
+    const uint64_t d[2] = {uint64_t(ldt), uint64_t(2 * npad)}, st[1] = {uint64_t(ldt) * 2};
+    const uint32_t bx[2] = {64, uint32_t(npad)};
+    if (!make_map(&tq, QT, 2, d, st, bx, true, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_DATA_TYPE_FLOAT16)) return false;
+  }
+  {
+    const uint64_t d[2] = {uint64_t(ldw), uint64_t(npad)}, st[1] = {uint64_t(ldw) * 2};
+    const uint32_t bx[2] = {64, uint32_t(npad)};
+    if (!make_map(&tw, WT, 2, d, st, bx, true, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_DATA_TYPE_FLOAT16)) return false;
+  }
+  {
+    const uint64_t d[2] = {uint64_t(K0), uint64_t(b0.b)}, st[1] = {uint64_t(K0) * 4};
+    const uint32_t bx[2] = {32, uint32_t(BM)};
+    if (!make_map(&tc, out, 2, d, st, bx, true)) return false;
+  }
+  FParams p;
+  p.a = b1.a; p.I = b1.I; p.b = b1.b; p.K = K1; p.C = K0;
+  p.cpb = b1.a / KC;
+  p.nchunks = p.cpb * b1.b;
+  p.seg = int(std::min<int64_t>(16, p.cpb));
+  const int64_t mtiles = b1.I / BM;
+  const int64_t want = std::max<int64_t>(1, (int64_t(ctx.num_sms) * 4 + mtiles - 1) / mtiles);
+  const int64_t bper = cdiv(b1.b, std::min<int64_t>(want, b1.b));      // whole betas per split
+  p.per = bper * p.cpb;
+  const int64_t splits = cdiv(p.nchunks, p.per);
+  p.part = ws.alloc_n<float>(splits * K1 * b1.I);
+  p.xscale = xso;
+  p.binv_s = 1.f / 2048.f;
+  p.binv_c = 1.f / kQScale;
+  p.runs = ctx.d_runs;
+  const dim3 grid{unsigned(mtiles), unsigned(splits), 1u};
+  // tf32 twins, gated on the same scale (s == 0: X's range or Omega's precision outside the fp16
+  // form): the plain sketch kernel on the fp32 Omega and the tf32 core stage
+  const int bmode_t = ctx.omega_tf32 ? 0 : 1;
+  SParams pf{};
+  pf.a = b1.a; pf.I = b1.I; pf.b = b1.b; pf.K = K1;
+  pf.cpb = p.cpb; pf.nchunks = p.nchunks; pf.per = p.per;
+  pf.seg = std::max(1, ctx.tc_seg);
+  pf.xfirst = ctx.tc_xfirst;
+  pf.part = p.part;
+  pf.gate = xso;
+  pf.runs = ctx.d_runs;
+  CUtensorMap tbf, txt;
+  if (!make_b_map_rm(&tbf, Om, J, K1, ldom)) return false;
+#define RT_F_CASE(NP)                                                                                    \
+  case NP: {                                                                                             \
+    using L = PlanF<NP>;                                                                                 \
+    static bool attr = false;                                                                            \
+    if (!attr) { set_smem(sketch1_core0_kernel<NP>, L::bytes); attr = true; }                            \
+    launch(ctx, ctx.label ? ctx.label : "sketch1_core0", [&] {                                           \
+      sketch1_core0_kernel<NP><<<grid, NT_TTM, L::bytes, ctx.stream>>>(tx, tq, tw, tc, p);              \
+    });                                                                                                  \
+    int xw_t = xw_feasible<NP>(bmode_t, false, 2);                                                       \
+    {                                                                                                    \
+      const uint64_t d[3] = {uint64_t(b1.a), uint64_t(b1.I), uint64_t(b1.b)};                            \
+      const uint64_t st[2] = {uint64_t(b1.a) * 4, uint64_t(b1.a) * b1.I * 4};                            \
+      const uint32_t bx[3] = {xw_t > 1 ? uint32_t(KC * xw_t + 4) : uint32_t(KC), BM, 1};                 \
+      if (!make_map(&txt, X, 3, d, st, bx, xw_t == 1)) return false;                                    \
+    }                                                                                                    \
+    dispatch_s<NP>(ctx, false, bmode_t, xw_t, txt, tbf, pf, grid);                                       \
+    break;                                                                                               \
+  }
+  switch (npad) {
+    RT_F_CASE(16) RT_F_CASE(32) RT_F_CASE(48) RT_F_CASE(64) RT_F_CASE(80)
+    default: return false;
+  }
+#undef RT_F_CASE
+  RT_REQUIRE(ttm_t_tc(ctx, ws, X, b0, Q0, ldq0, K0, out, 1, 1, K0, 0, false, nullptr, xso), kEUNSUPPORTED,
+             "sketch1_core0: tf32 twin of the core stage rejected");
+  const int64_t n = b1.I * K1;
+  launch(ctx, "splitk_reduce", [&] {
+    splitk_reduce_f32_kernel<<<unsigned(cdiv(n, 32)), 256, 0, ctx.stream>>>(p.part, b1.I, K1, int(splits), Y, ldy);
+  });
   return true;
 }
 

@@ -287,3 +287,43 @@ def test_tc_sthosvd_shrink(P, htc):
     for n in range(3):
         assert M.subspace(qg[n], ref["Q"][n]) <= 1e-5
     assert abs(mat(res["err"])[0] - ref["E"]) / ref["E"] <= 1e-5
+
+
+@pytest.mark.parametrize("dims,rank,p,q", [((512, 256, 48), 20, 12, 1),      # K = 32
+                                           ((1024, 128, 40), 16, 8, 2),      # K = 24 (npad 32)
+                                           ((512, 256, 6, 8), 12, 8, 1),     # order 4
+                                           ((512, 384), 20, 12, 1)])         # order 2
+def test_fused_sketch1_core0(P, dims, rank, p, q):
+    """The fused pass (sketch1_core0_kernel: the mode-1 Omega sketch and the first core stage
+    X x_1 Q~_0^T from one read of X, 10 instead of 11 passes for a 3-way tensor) in bench.py's
+    configuration (tf32-rounded Omega), on shapes it accepts (I_0 % 512 == 0, I_1 % 128 == 0): parity
+    with the oracle, the fused launch seen in the profile, and the same result as the unfused path
+    (option 290) to fp32 rounding."""
+    from paper_2001_07124_b200 import _lib as L
+    N = len(dims)
+    cfg = dataclasses.replace(synth.CONFIGS["cfg5"].scaled(dims, (rank,) * N, (rank,) * N), p=p, q=q)
+    x = synth.make_tensor(cfg)
+    oms = [synth.round_tf32(synth.gaussian_omega(cfg, n)) for n in range(N)]
+    ref = oracle.hosvd(x, cfg.ranks, oms, q=q)
+    res = {}
+    for opt in (291, 290):
+        h = _handle(P, 0, omega_tf32=True)
+        h.set_option(L.RT_OPT_TC_ABLATE, opt)
+        h.set_option(L.RT_OPT_PROFILE, 1)
+        r = P.rtucker_hosvd(h, dev(x), cfg.ranks, cfg.p, q, [om_dev(o) for o in oms])
+        h.sync()
+        names = {n for n, _, _ in h.profile_read()[0]}
+        assert ("sketch1_core0" in names) == (opt == 291), (opt, names)
+        res[opt] = r
+        qg = [mat(t) for t in r["Q"]]
+        gg = P.core_to_numpy(r["G"])
+        for n in range(N):
+            assert M.orth(qg[n]) <= 1e-12
+            assert M.subspace(qg[n], ref["Q"][n]) <= 1e-5, (opt, n, M.subspace(qg[n], ref["Q"][n]))
+        assert M.core_in_oracle_basis(gg, qg, ref["G"], ref["Q"]) <= 1e-5
+        assert M.recon(gg, qg, ref["G"], ref["Q"]) <= 1e-5
+        e = mat(r["err"])[0]
+        assert abs(e - ref["E"]) / ref["E"] <= 1e-5, (opt, e, ref["E"])
+        h.close()
+    for n in range(N):
+        assert M.subspace(mat(res[291]["Q"][n]), mat(res[290]["Q"][n])) <= 2e-6
