@@ -1412,22 +1412,35 @@ __global__ void __launch_bounds__(256) omega_t16_kernel(const float* __restrict_
   __shared__ float t[64][129];
   const int64_t j0 = int64_t(blockIdx.x) * 64;
   bool bad = false;
-  for (int e = threadIdx.x; e < 64 * npad; e += blockDim.x) {
-    const int jl = e / npad, k = e % npad;
+  for (int e = threadIdx.x; e < 16 * npad; e += blockDim.x) {        // float4 per thread
+    const int jl = e / (npad / 4), k4 = 4 * (e % (npad / 4));
     const int64_t j = j0 + jl;
-    t[jl][k] = (j < J && k < K) ? Om[j * ld + k] : 0.f;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (j < J) {
+      if (k4 + 4 <= K) v = __ldcs(reinterpret_cast<const float4*>(Om + j * ld + k4));
+      else {
+        if (k4 + 0 < K) v.x = Om[j * ld + k4 + 0];
+        if (k4 + 1 < K) v.y = Om[j * ld + k4 + 1];
+        if (k4 + 2 < K) v.z = Om[j * ld + k4 + 2];
+      }
+    }
+    t[jl][k4] = v.x; t[jl][k4 + 1] = v.y; t[jl][k4 + 2] = v.z; t[jl][k4 + 3] = v.w;
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < 64 * npad; e += blockDim.x) {
-    const int k = e / 64, jl = e % 64;
-    const int64_t j = j0 + jl;
-    if (j >= ldw) continue;
-    const float v = t[jl][k] * 2048.f;
-    const __half hv = __float2half_rn(v);
-    // an entry in the fp16 normal range must be exact (a tf32-rounded Omega is); entries below it round
-    // with an absolute error <= 2^-25 (2^-36 of |Omega|): immaterial next to fp32
-    bad |= !(fabsf(v) < 32768.f) || (fabsf(v) >= 6.103515625e-05f && __half2float(hv) != v);
-    WT[int64_t(k) * ldw + j] = hv;
+  // 8 consecutive j of one row k per thread: one 16-byte store (ldw and j0 are multiples of 8)
+  for (int e = threadIdx.x; e < 8 * npad; e += blockDim.x) {
+    const int k = e / 8, jl0 = 8 * (e % 8);
+    if (j0 + jl0 >= ldw) continue;
+    __align__(16) __half hv[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float v = t[jl0 + q][k] * 2048.f;
+      hv[q] = __float2half_rn(v);
+      // an entry in the fp16 normal range must be exact (a tf32-rounded Omega is); entries below it
+      // round with an absolute error <= 2^-25 (2^-36 of |Omega|): immaterial next to fp32
+      bad |= !(fabsf(v) < 32768.f) || (fabsf(v) >= 6.103515625e-05f && __half2float(hv[q]) != v);
+    }
+    *reinterpret_cast<uint4*>(WT + int64_t(k) * ldw + j0 + jl0) = *reinterpret_cast<const uint4*>(hv);
   }
   if (bad) atomicOr(flag, 1);
 }
