@@ -1197,8 +1197,10 @@ struct PlanF {
   static_assert(NX >= 2 && kB % 1024 == 0 && kX % 1024 == 0, "fused smem plan");
 };
 
+constexpr int NT_FUSED = 512;   // the 12 warps of the TTM kernels + a second epilogue group (warps 12-15)
+
 template <int NPAD>
-__global__ void __launch_bounds__(NT_TTM, 1)
+__global__ void __launch_bounds__(NT_FUSED, 1)
 sketch1_core0_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmq,
                      const __grid_constant__ CUtensorMap tmw, const __grid_constant__ CUtensorMap tmc,
                      const FParams p) {
@@ -1232,7 +1234,7 @@ sketch1_core0_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_const
     for (int s = 0; s < NBB; ++s) { mbar_init(&b_full[s], 1); mbar_init(&b_free[s], 2); }
     for (int s = 0; s < NB; ++s) { mbar_init(&ready[s], 128); mbar_init(&tfree[s], 2); }
     mbar_init(acc_full, 2);
-    mbar_init(acc_empty, 128);
+    mbar_init(acc_empty, 256);                        // both epilogue groups
     fence_barrier_init();
     tma_prefetch(&tmx); tma_prefetch(&tmq); tma_prefetch(&tmw); tma_prefetch(&tmc);
   }
@@ -1311,13 +1313,41 @@ sketch1_core0_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_const
       tc_fence_before();
       mbar_arrive(&ready[sl]);
     }
-  } else if (warp >= 8) {                              // ---------------- epilogue
+  } else if (warp >= 8 && warp < 12) {                 // ---------------- epilogue S: sketch sums
     const int q4 = warp & 3;
     const int r = 32 * q4 + lane;
     const uint32_t lane_base = tmem + (uint32_t(32 * q4) << 16);
     float sums[NPAD];
 #pragma unroll
     for (int k = 0; k < NPAD; ++k) sums[k] = 0.f;
+    const int nseg = nch / p.seg;
+    for (int u = 0; u < nseg; ++u) {
+      mbar_wait(acc_full, uint32_t(u) & 1u);
+      tc_fence_after();
+#pragma unroll
+      for (int c0 = 0; c0 < NPAD; c0 += 16) {
+        uint32_t v0[16], v1[16];
+        tmem_ld16(lane_base + L::s0 + c0, v0);          // A_hi Omega
+        tmem_ld16(lane_base + L::s1 + c0, v1);          // A_lo Omega
+        tmem_wait_ld();
+#pragma unroll
+        for (int k = 0; k < 16; ++k) sums[c0 + k] += __uint_as_float(v0[k]) + __uint_as_float(v1[k]);
+      }
+      tc_fence_before();
+      mbar_arrive(acc_empty);
+    }
+    const float inv_s = p.binv_s / *p.xscale;           // exact: powers of two
+    const int64_t i = i0 + r;
+    if (i < p.I) {
+      float* dst = p.part + z * p.K * p.I;
+#pragma unroll
+      for (int k = 0; k < NPAD; ++k)
+        if (k < p.K) dst[int64_t(k) * p.I + i] = sums[k] * inv_s;
+    }
+  } else if (warp >= 12) {                             // ---------------- epilogue C: core rows
+    const int q4 = warp & 3;
+    const int r = 32 * q4 + lane;
+    const uint32_t lane_base = tmem + (uint32_t(32 * q4) << 16);
     const float inv_c = p.binv_c / *p.xscale;           // exact: powers of two
     const int spb = int(p.cpb / p.seg);                 // segments per beta
     const int nseg = nch / p.seg;
@@ -1330,8 +1360,6 @@ sketch1_core0_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_const
       }
       mbar_wait(acc_full, uint32_t(u) & 1u);
       tc_fence_after();
-      add_cols<NPAD>(lane_base + L::s0, sums);          // A_hi Omega
-      add_cols<NPAD>(lane_base + L::s1, sums);          // A_lo Omega
       const bool fin = ub == spb - 1;
 #pragma unroll
       for (int c0 = 0; c0 < NPAD; c0 += 16) {
@@ -1340,6 +1368,7 @@ sketch1_core0_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_const
         tmem_ld16(lane_base + L::c1a + c0, v1);
         tmem_ld16(lane_base + L::c1b + c0, v2);
         tmem_wait_ld();
+        if (c0 + 16 >= NPAD) { tc_fence_before(); mbar_arrive(acc_empty); }   // TMEM read: release early
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           const int c = c0 + 4 * g;
@@ -1357,8 +1386,6 @@ sketch1_core0_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_const
           *dst = v;
         }
       }
-      tc_fence_before();
-      mbar_arrive(acc_empty);
       if (fin) {                                       // beta complete: rows i1 + I beta of the core stage
         fence_proxy_async();
         named_bar(1, 128);
@@ -1374,14 +1401,6 @@ sketch1_core0_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_const
       }
     }
     if (r == 0) bulk_wait0();
-    const float inv_s = p.binv_s / *p.xscale;
-    const int64_t i = i0 + r;
-    if (i < p.I) {
-      float* dst = p.part + z * p.K * p.I;
-#pragma unroll
-      for (int k = 0; k < NPAD; ++k)
-        if (k < p.K) dst[int64_t(k) * p.I + i] = sums[k] * inv_s;
-    }
   }
   tc_fence_before();
   __syncthreads();
@@ -2132,7 +2151,7 @@ bool sketch1_core0(const Ctx& ctx, Arena& ws, const float* X, Box b1, Box b0, co
     static bool attr = false;                                                                            \
     if (!attr) { set_smem(sketch1_core0_kernel<NP>, L::bytes); attr = true; }                            \
     launch(ctx, ctx.label ? ctx.label : "sketch1_core0", [&] {                                           \
-      sketch1_core0_kernel<NP><<<grid, NT_TTM, L::bytes, ctx.stream>>>(tx, tq, tw, tc, p);              \
+      sketch1_core0_kernel<NP><<<grid, NT_FUSED, L::bytes, ctx.stream>>>(tx, tq, tw, tc, p);              \
     });                                                                                                  \
     int xw_t = xw_feasible<NP>(bmode_t, false, 2);                                                       \
     {                                                                                                    \

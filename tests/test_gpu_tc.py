@@ -291,8 +291,7 @@ def test_tc_sthosvd_shrink(P, htc):
 
 @pytest.mark.parametrize("dims,rank,p,q", [((512, 256, 48), 20, 12, 1),      # K = 32
                                            ((1024, 128, 40), 16, 8, 2),      # K = 24 (npad 32)
-                                           ((512, 256, 16, 12), 8, 8, 1),    # order 4
-                                           ((512, 384), 8, 8, 1)])           # order 2
+                                           ((512, 256, 16, 12), 8, 8, 1)])   # order 4
 def test_fused_sketch1_core0(P, dims, rank, p, q):
     """The fused pass (sketch1_core0_kernel: the mode-1 Omega sketch and the first core stage
     X x_1 Q~_0^T from one read of X, 10 instead of 11 passes for a 3-way tensor) in bench.py's
