@@ -1178,9 +1178,9 @@ struct FParams {
   unsigned int* runs;
 };
 
-template <int NPAD>
+template <int NPAD, int NBB_ = 2>
 struct PlanF {
-  static constexpr int XW = 2, NB = 3, NBB = 2;
+  static constexpr int XW = 2, NB = 3, NBB = NBB_;
   static constexpr uint32_t c0 = 0, s0 = NPAD, c1a = 2 * NPAD, c1b = 3 * NPAD, s1 = 4 * NPAD;
   static constexpr uint32_t a_base = (5u * NPAD + 31u) & ~31u;
   static_assert(a_base + 32u * NB <= 512u, "fused TMEM plan");
@@ -1199,12 +1199,12 @@ struct PlanF {
 
 constexpr int NT_FUSED = 512;   // the 12 warps of the TTM kernels + a second epilogue group (warps 12-15)
 
-template <int NPAD>
+template <int NPAD, int NBB_ = 2>
 __global__ void __launch_bounds__(NT_FUSED, 1)
 sketch1_core0_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmq,
                      const __grid_constant__ CUtensorMap tmw, const __grid_constant__ CUtensorMap tmc,
                      const FParams p) {
-  using L = PlanF<NPAD>;
+  using L = PlanF<NPAD, NBB_>;
   constexpr int NX = L::NX, NB = L::NB, NBB = L::NBB, XW = L::XW;
   if (*p.xscale == 0.f) return;                        // the tf32 twins run instead (R29)
   if (p.runs && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) atomicAdd(&p.runs[0], 1u);
@@ -1269,7 +1269,7 @@ sketch1_core0_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_const
         uint8_t* dst = smem + L::off_b + rb.s * L::kB;
         mbar_expect_tx(&b_full[rb.s], L::kB);
         tma_load_2d_hint(dst, &tmq, &b_full[rb.s], int(a0), 0, pol);                              // 2^14 Q_hi^T
-        tma_load_2d_hint(dst + NPAD * 128, &tmw, &b_full[rb.s], int(a0 + p.a * beta), 0, pol);    // 2^11 Omega^T
+        tma_load_3d_hint(dst + NPAD * 128, &tmw, &b_full[rb.s], 0, 0, int((a0 + p.a * beta) / 64), pol);   // 2^11 Omega^T
         tma_load_2d_hint(dst + 2 * NPAD * 128, &tmq, &b_full[rb.s], int(a0), NPAD, pol);          // 2^14 Q_lo^T
       }
     }
@@ -1422,9 +1422,10 @@ __global__ void qt16_kernel(const float* __restrict__ Q, int64_t I, int C, int64
   QT[int64_t(npad + c) * ldt + i] = __float2half_rn(v - h);
 }
 
-// Omega (J x K fp32, row-major ld) -> WT (fp16, NPAD rows x ldw): row k = 2^11 Omega[:, k]^T (rows >= K
-// zero).  *flag = 1 if an entry is not exactly an fp16 at 2^11 (not tf32-exact, or out of range):
-// the fused kernel then stands down for its twins.  64 j-rows per block through shared memory.
+// Omega (J x K fp32, row-major ld) -> WT (fp16) in 64-column blocks: WT[jb][k][jl] = 2^11 Omega[64 jb + jl][k]
+// (rows k >= K zero), so the B box of a chunk pair (NPAD rows x 64 j) is one contiguous 128 NPAD-byte
+// run.  *flag = 1 if an entry is not exactly an fp16 at 2^11 (not tf32-exact, or out of range): the
+// fused kernel then stands down for its twins.  64 j-rows per block through shared memory.
 __global__ void __launch_bounds__(256) omega_t16_kernel(const float* __restrict__ Om, int64_t J, int K, int64_t ld,
                                                         int npad, __half* __restrict__ WT, int64_t ldw,
                                                         int* __restrict__ flag) {
@@ -1449,7 +1450,7 @@ __global__ void __launch_bounds__(256) omega_t16_kernel(const float* __restrict_
   // 8 consecutive j of one row k per thread: one 16-byte store (ldw and j0 are multiples of 8)
   for (int e = threadIdx.x; e < 8 * npad; e += blockDim.x) {
     const int k = e / 8, jl0 = 8 * (e % 8);
-    if (j0 + jl0 >= ldw) continue;
+
     __align__(16) __half hv[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -1459,7 +1460,8 @@ __global__ void __launch_bounds__(256) omega_t16_kernel(const float* __restrict_
       // round with an absolute error <= 2^-25 (2^-36 of |Omega|): immaterial next to fp32
       bad |= !(fabsf(v) < 32768.f) || (fabsf(v) >= 6.103515625e-05f && __half2float(hv[q]) != v);
     }
-    *reinterpret_cast<uint4*>(WT + int64_t(k) * ldw + j0 + jl0) = *reinterpret_cast<const uint4*>(hv);
+    *reinterpret_cast<uint4*>(WT + (j0 / 64) * (int64_t(npad) * 64) + int64_t(k) * 64 + jl0) =
+        *reinterpret_cast<const uint4*>(hv);
   }
   if (bad) atomicOr(flag, 1);
 }
@@ -2081,7 +2083,7 @@ bool sketch1_core0(const Ctx& ctx, Arena& ws, const float* X, Box b1, Box b0, co
   const int64_t J = b1.J();
   if (b1.a > INT32_MAX || b1.I > INT32_MAX || b1.b > INT32_MAX || J > INT32_MAX || b0.b > INT32_MAX) return false;
   // B sources: 2^14 [Q_hi^T ; Q_lo^T] and 2^11 Omega^T in fp16, rows padded to npad
-  const int64_t ldt = (b1.a + 7) & ~int64_t(7), ldw = (J + 7) & ~int64_t(7);
+  const int64_t ldt = (b1.a + 7) & ~int64_t(7), ldw = (J + 63) & ~int64_t(63);
   __half* QT = ws.alloc_n<__half>(2 * npad * ldt);
   __half* WT = ws.alloc_n<__half>(int64_t(npad) * ldw);
   int* flag = ws.alloc_n<int>(1);
@@ -2107,9 +2109,9 @@ bool sketch1_core0(const Ctx& ctx, Arena& ws, const float* X, Box b1, Box b0, co
     if (!make_map(&tq, QT, 2, d, st, bx, true, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_DATA_TYPE_FLOAT16)) return false;
   }
   {
-    const uint64_t d[2] = {uint64_t(ldw), uint64_t(npad)}, st[1] = {uint64_t(ldw) * 2};
-    const uint32_t bx[2] = {64, uint32_t(npad)};
-    if (!make_map(&tw, WT, 2, d, st, bx, true, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_DATA_TYPE_FLOAT16)) return false;
+    const uint64_t d[3] = {64, uint64_t(npad), uint64_t(ldw / 64)}, st[2] = {128, uint64_t(npad) * 128};
+    const uint32_t bx[3] = {64, uint32_t(npad), 1};
+    if (!make_map(&tw, WT, 3, d, st, bx, true, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_DATA_TYPE_FLOAT16)) return false;
   }
   {
     const uint64_t d[2] = {uint64_t(K0), uint64_t(b0.b)}, st[1] = {uint64_t(K0) * 4};
@@ -2147,12 +2149,21 @@ bool sketch1_core0(const Ctx& ctx, Arena& ws, const float* X, Box b1, Box b0, co
   if (!make_b_map_rm(&tbf, Om, J, K1, ldom)) return false;
 #define RT_F_CASE(NP)                                                                                    \
   case NP: {                                                                                             \
-    using L = PlanF<NP>;                                                                                 \
-    static bool attr = false;                                                                            \
-    if (!attr) { set_smem(sketch1_core0_kernel<NP>, L::bytes); attr = true; }                            \
-    launch(ctx, ctx.label ? ctx.label : "sketch1_core0", [&] {                                           \
-      sketch1_core0_kernel<NP><<<grid, NT_FUSED, L::bytes, ctx.stream>>>(tx, tq, tw, tc, p);              \
-    });                                                                                                  \
+    if (ctx.fused_nbb == 3) {                                                                            \
+      using L = PlanF<NP, 3>;                                                                            \
+      static bool attr = false;                                                                          \
+      if (!attr) { set_smem(sketch1_core0_kernel<NP, 3>, L::bytes); attr = true; }                       \
+      launch(ctx, ctx.label ? ctx.label : "sketch1_core0", [&] {                                         \
+        sketch1_core0_kernel<NP, 3><<<grid, NT_FUSED, L::bytes, ctx.stream>>>(tx, tq, tw, tc, p);        \
+      });                                                                                                \
+    } else {                                                                                             \
+      using L = PlanF<NP, 2>;                                                                            \
+      static bool attr = false;                                                                          \
+      if (!attr) { set_smem(sketch1_core0_kernel<NP, 2>, L::bytes); attr = true; }                       \
+      launch(ctx, ctx.label ? ctx.label : "sketch1_core0", [&] {                                         \
+        sketch1_core0_kernel<NP, 2><<<grid, NT_FUSED, L::bytes, ctx.stream>>>(tx, tq, tw, tc, p);        \
+      });                                                                                                \
+    }                                                                                                    \
     int xw_t = xw_feasible<NP>(bmode_t, false, 2);                                                       \
     {                                                                                                    \
       const uint64_t d[3] = {uint64_t(b1.a), uint64_t(b1.I), uint64_t(b1.b)};                            \
