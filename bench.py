@@ -393,37 +393,44 @@ def main():
     ms = r["ms"] / args.steps
     value = xbytes / (ms * 1e-3) / 1e9
     wm = work_model(cfg, r["world"], 2 if args.omega == "tf32" else 3)
-    # dominant kernel class by measured device time: the X-streaming launches of one TTM shape
-    # (ttm_s_tc = Omega sketch + power product Y = X Z; ttm_t_tc = Z = X^T Q + first core stage)
+    # roofline of the X-streaming kernels (the dominant work: every launch that reads X in the
+    # sketch+QR+core pipeline; the residual pass a8 is reported apart): algorithmic bytes of those
+    # passes (|X| per pass + the test / power matrices and the core stage written)
+    # over their device time, CUDA events on the launching stream (RT_OPT_PROFILE)
     prof = sorted(r["prof"], key=lambda e: -e[2])
-    classes = {"ttm_s": ("ttm_s_tc", "ttm_s_tc_pow"), "ttm_t": ("ttm_t_tc", "ttm_t_tc_pow", "core_first"),
-               "residual": ("residual_tc",)}
-    cls_ms = {c: sum(t for nm, _, t in prof if nm in names) for c, names in classes.items()}
-    cls = max(cls_ms, key=cls_ms.get) if prof else None
-    top = (classes[cls][0], 0, cls_ms[cls]) if cls else ("?", 0, 0.0)
+    xlabels = ("ttm_s_tc", "ttm_s_tc_pow", "ttm_t_tc_pow", "core_first", "sketch1_core0")
+    fused = any(nm == "sketch1_core0" for nm, _, _ in prof)
+    x_ms = sum(t for nm, _, t in prof if nm in xlabels) / args.steps
+    xl = wm["x_bytes_local"]
+    npass = wm["ttm_s"][2] + wm["ttm_t"][2] - (1 if fused else 0)
+    cls_bytes = wm["ttm_s"][0] + wm["ttm_t"][0] - (xl if fused else 0)
+    cls_flops = wm["ttm_s"][1] + wm["ttm_t"][1]
     roof = None
-    if cls and cls_ms[cls] > 0:
-        b, f, n = wm[cls]
-        per_step_ms = top[2] / args.steps
-        achieved = b / (per_step_ms * 1e-3) / 1e9
+    if x_ms > 0:
+        achieved = cls_bytes / (x_ms * 1e-3) / 1e9
         traffic = None
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp):
-            traffic = json.load(open(tp)).get(top[0])
-        roof = {"bound": "hbm", "kernel": "+".join(classes[cls]), "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
-                "share_of_step": per_step_ms / ms,
-                "tflops": f / (per_step_ms * 1e-3) / 1e12}
-        if cls == "ttm_s":
-            # tensor pipe: hardware flops of the class (tf32 Omega sketches + fp16-split power
-            # products) and the fraction of the class time the pipe needs at the measured peaks
-            # (fp16 = measured dense bf16; tf32 = bf16 x 1/2, the nominal ratio of B200_PROFILING.md)
-            tf32_peak, f16_peak = bf16 / 2.0, bf16
-            t_s = per_step_ms * 1e-3
-            busy = (wm["ttm_s_hw_tf32"] / (tf32_peak * 1e12) + wm["ttm_s_hw_f16"] / (f16_peak * 1e12)) / t_s
-            roof["tensor"] = {"hw_tflops": (wm["ttm_s_hw_tf32"] + wm["ttm_s_hw_f16"]) / t_s / 1e12, "frac": busy,
-                              "peak_tflops": {"tf32": tf32_peak, "f16": f16_peak},
-                              "peak_source": f"{peak_src} bf16 (f16), x 1/2 (tf32)"}
+            traffic = json.load(open(tp)).get("ttm_s_h16")
+        roof = {"bound": "hbm", "kernel": "X passes: " + "+".join(xlabels), "achieved": achieved, "peak": hbm,
+                "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
+                "traffic_note": "ncu dram bytes read+write per launch of ttm_s_h16_kernel (the most frequent X pass)",
+                "algorithmic_bytes_per_pass": cls_bytes / npass, "x_passes_per_step": npass + 1,
+                "peak_source": peak_src, "share_of_step": x_ms / ms,
+                "tflops": cls_flops / (x_ms * 1e-3) / 1e12}
+        # tensor pipe: hardware flops (the first Omega sketch: 2 tf32 products; every other X pass: the
+        # 3 fp16-split products, the fused pass 5 per column of its [sketch | core]) against the
+        # measured peaks (f16 = measured dense bf16; tf32 = bf16 x 1/2, B200_PROFILING.md's ratio)
+        tf32_peak, f16_peak = bf16 / 2.0, bf16
+        K0 = cfg.K(0)
+        first = 2 * (xl // 4) * K0
+        hw_tf32 = 2 * first if args.omega == "tf32" else 3 * first
+        hw_f16 = 3 * (cls_flops - first)
+        t_s = x_ms * 1e-3
+        roof["tensor"] = {"hw_tflops": (hw_tf32 + hw_f16) / t_s / 1e12,
+                          "frac": (hw_tf32 / (tf32_peak * 1e12) + hw_f16 / (f16_peak * 1e12)) / t_s,
+                          "peak_tflops": {"tf32": tf32_peak, "f16": f16_peak},
+                          "peak_source": f"{peak_src} bf16 (f16), x 1/2 (tf32)"}
     line = {"metric": METRIC, "value": value * 1.0, "unit": UNIT, "n_gpus": r["world"], "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config,

@@ -15,6 +15,7 @@ struct rt_handle {
   rt::Arena ws_side;                 // workspace of the side stream (overlapped QRs)
   rt::EventPool events;
   cudaStream_t side = nullptr;
+  cudaStream_t cstream = nullptr;   // C3 overlap (distributed HOSVD)
   rt::Profiler prof;
   std::unique_ptr<rt::Comm> comm;
   std::string err;
@@ -174,6 +175,11 @@ static rt_status create_common(rt_handle** h, void* stream) {
     hh->side = nullptr;               // no overlap: every step on the main stream
   }
   hh->ctx.side_stream = hh->side;
+  if (cudaStreamCreateWithFlags(&hh->cstream, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    hh->cstream = nullptr;
+  }
+  hh->ctx.comm_stream = hh->cstream;
   hh->ctx.side_ws = &hh->ws_side;
   hh->ctx.events = &hh->events;
   hh->ctx.prof = &hh->prof;
@@ -214,8 +220,11 @@ rt_status rt_destroy(rt_handle* h) {
   if (!h) return RT_OK;
   cudaSetDevice(h->device);
   if (h->ctx.stream) cudaStreamSynchronize(h->ctx.stream); else cudaDeviceSynchronize();
+  if (h->side) cudaStreamSynchronize(h->side);
+  if (h->cstream) cudaStreamSynchronize(h->cstream);
   h->comm.reset();
-  if (h->side) { cudaStreamSynchronize(h->side); cudaStreamDestroy(h->side); }
+  if (h->side) cudaStreamDestroy(h->side);
+  if (h->cstream) cudaStreamDestroy(h->cstream);
   if (h->d_status) cudaFree(h->d_status);
   if (h->d_runs) cudaFree(h->d_runs);
   delete h;

@@ -28,6 +28,7 @@ struct NcclApi {
   ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, void*) = nullptr;   // optional (NCCL >= 2.18)
 };
 
 NcclApi& nccl() {
@@ -48,6 +49,7 @@ NcclApi& nccl() {
     api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(h, "ncclAllReduce"));
     api.AllGather = reinterpret_cast<decltype(api.AllGather)>(dlsym(h, "ncclAllGather"));
     api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+    api.CommSplit = reinterpret_cast<decltype(api.CommSplit)>(dlsym(h, "ncclCommSplit"));
     if (!api.GetUniqueId || !api.CommInitRank || !api.AllReduce || !api.AllGather) {
       api.err = "libnccl is missing required symbols";
       return;
@@ -66,10 +68,19 @@ void nccl_check(ncclResult_t r, const char* what) {
 
 class NcclComm final : public Comm {
  public:
-  NcclComm(ncclComm_t c, int n, int r) : comm_(c), n_(n), r_(r) {}
+  NcclComm(ncclComm_t c, int n, int r, bool make_side = true) : comm_(c), n_(n), r_(r) {
+    // the side communicator (same ranks, color 0): every rank splits at construction, so the
+    // collective split happens at the same point everywhere
+    if (make_side && n > 1 && nccl().CommSplit) {
+      ncclComm_t sc = nullptr;
+      if (nccl().CommSplit(comm_, 0, r, &sc, nullptr) == 0 && sc) side_.reset(new NcclComm(sc, n, r, false));
+    }
+  }
   ~NcclComm() override {
+    side_.reset();
     if (comm_ && nccl().CommDestroy) nccl().CommDestroy(comm_);
   }
+  Comm* side() override { return side_.get(); }
   int nranks() const override { return n_; }
   int rank() const override { return r_; }
   void allreduce_sum(double* b, size_t n, cudaStream_t s) override {
@@ -85,6 +96,7 @@ class NcclComm final : public Comm {
  private:
   ncclComm_t comm_;
   int n_, r_;
+  std::unique_ptr<NcclComm> side_;
 };
 }  // namespace
 
@@ -133,6 +145,7 @@ struct LoopbackGroup {
   int64_t gen = 0;
   std::vector<const void*> ptr;
   std::vector<cudaEvent_t> ev;
+  LoopbackGroup* side = nullptr;       // the group of the side communicators (Comm::side)
   explicit LoopbackGroup(int nn) : n(nn), ptr(nn, nullptr), ev(nn, nullptr) {}
   void barrier() {
     std::unique_lock<std::mutex> lk(mu);
@@ -149,9 +162,14 @@ struct LoopbackGroup {
 
 LoopbackGroup* loopback_group_create(int nranks) {
   if (nranks < 1 || nranks > kMaxLoop) throw Error(kEINVAL, "loopback group: 1 <= nranks <= 8");
-  return new LoopbackGroup(nranks);
+  LoopbackGroup* g = new LoopbackGroup(nranks);
+  g->side = new LoopbackGroup(nranks);
+  return g;
 }
-void loopback_group_destroy(LoopbackGroup* g) { delete g; }
+void loopback_group_destroy(LoopbackGroup* g) {
+  if (g) delete g->side;
+  delete g;
+}
 
 namespace {
 class LoopbackComm final : public Comm {
@@ -159,7 +177,9 @@ class LoopbackComm final : public Comm {
   LoopbackComm(LoopbackGroup* g, int r) : g_(g), r_(r) {
     RT_CUDA(cudaEventCreateWithFlags(&ready_, cudaEventDisableTiming));
     RT_CUDA(cudaEventCreateWithFlags(&done_, cudaEventDisableTiming));
+    if (g->side) side_.reset(new LoopbackComm(g->side, r));
   }
+  Comm* side() override { return side_.get(); }
   ~LoopbackComm() override {
     cudaEventDestroy(ready_);
     cudaEventDestroy(done_);
@@ -225,6 +245,7 @@ class LoopbackComm final : public Comm {
   cudaEvent_t ready_ = nullptr, done_ = nullptr;
   void* tmp_ = nullptr;
   size_t tmp_bytes_ = 0;
+  std::unique_ptr<LoopbackComm> side_;
 };
 }  // namespace
 

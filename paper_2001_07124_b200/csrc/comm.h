@@ -28,6 +28,9 @@ class Comm {
   virtual void allreduce_sum(float* buf, size_t n, cudaStream_t s) = 0;
   // recv[r*n .. r*n+n) = send of rank r
   virtual void allgather(const double* send, double* recv, size_t n, cudaStream_t s) = 0;
+  // a second communicator over the same ranks whose collectives may run concurrently with this
+  // one's on another stream (NCCL: ncclCommSplit; loopback: the group's side group); nullptr if none
+  virtual Comm* side() { return nullptr; }
 };
 
 int nccl_get_unique_id(uint8_t id[128]);   // 0 ok, else error (message via nccl_last_error)

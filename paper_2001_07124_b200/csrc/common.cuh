@@ -107,6 +107,7 @@ struct Ctx {
   int tc_xw = 2;                // ttm_s strided modes: chunks per wide-row X stage (1 = swizzled 128 B rows;
                                 // ablation 231/232/234 select 1/2/4; cfg5 modes 1/2: 2 is fastest)
   cudaStream_t side_stream = nullptr;   // second stream of the handle (high priority): overlapped QRs
+  cudaStream_t comm_stream = nullptr;   // third stream: the slab mode's Z allreduce (C3) on the side communicator
   Arena* side_ws = nullptr;             // its workspace arena
   EventPool* events = nullptr;          // fork / join events
   int overlap = 1;              // HOSVD: thin QRs on the side stream (ablation 270 / 271 toggle)

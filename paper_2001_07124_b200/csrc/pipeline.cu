@@ -540,11 +540,73 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
     done_q[n] = nullptr;
   }
   int it_done[5] = {0, 0, 0, 0, 0};            // power steps taken per mode
+  // Slab mode of a distributed run: its power step sums Z = X_(N-1)^T Q over the
+  // slabs (C3, J x K: 1.34 GB at cfg5).  C3 overlap (H7): the slab mode's first sketch, QR and Z pass
+  // run first, the allreduce of Z goes to a third stream on the side communicator while the main
+  // stream processes the other modes, and the slab mode's product Y = X_(N-1) s_z Z (R31) follows
+  // once Z is summed; later power iterations of the slab mode allreduce on the main stream.
+  const int ns = N - 1;
+  const int64_t Jls = X.box(ns).J();
+  const bool c3ovl = dist() && q > 0 && comm->side() && ctx.comm_stream && !ctx.power_qrz && (K[ns] % 4) == 0 &&
+                     ctx.tc_h16 && ttm_s_tc_ok(ctx, data, X.box(ns), int(K[ns]));
+  float* Zs = c3ovl ? ws.alloc_n<float>(Jls * K[ns]) : nullptr;
+  cudaEvent_t c3_done = nullptr;
+  // the slab mode's Z pass: Zs = s_z X_(N-1)^T Qy (fp32 partial sums of this slab), h16 pair
+  auto slab_zpass = [&]() {
+    const Box bx = X.box(ns);
+    const auto mz = ws.mark();
+    int64_t ldqt;
+    const float* QyT = working_copy<float>(ctx, ws, Qy[ns], X.d[ns], K[ns], X.d[ns], ldqt);
+    const int ez = int(std::ceil(0.5 * std::log2(double(X.Ig(ns)))));
+    LabelScope ls(ctx, "ttm_t_tc_pow");
+    RT_REQUIRE(ttm_t_tc(ctx, ws, data, bx, QyT, ldqt, int(K[ns]), Zs, K[ns], 1, bx.a * K[ns], 0, false, xs_slot, nullptr,
+                        xs_slot + 1, std::ldexp(1.0f, -(ez + 1))),
+               kEUNSUPPORTED, "slab mode: Z pass rejected by the tensor-core path");
+    ws.rewind(mz);
+  };
+  // the slab mode's product from the summed Zs: Yt = X_(N-1) Zs (fp16 split rows), then its QR
+  auto slab_product = [&](bool final_qr) {
+    const Box bx = X.box(ns);
+    const auto mz = ws.mark();
+    const int64_t ldz2 = 2 * int64_t(tc_npad(int(K[ns])));
+    uint16_t* Z2 = ws.alloc_n<uint16_t>(Jls * ldz2);
+    split_rows_h16(ctx, Zs, Jls, int(K[ns]), K[ns], Z2);
+    {
+      LabelScope ls(ctx, "ttm_s_tc_pow");
+      RT_REQUIRE(ttm_s_tc(ctx, ws, data, bx, reinterpret_cast<const float*>(Z2), ldz2, false, int(K[ns]), Yt[ns],
+                          X.d[ns], true, xs_slot, nullptr, Zs, K[ns]),
+                 kEUNSUPPORTED, "slab mode: power product not launched");
+    }
+    ws.rewind(mz);
+    qr_y(Yt[ns], X.d[ns], X.Ig(ns), int(K[ns]), X.d[ns], final_qr ? Qt[ns] : Qy[ns], X.d[ns], nullptr, true, X.off);
+  };
+  if (c3ovl) {
+    sketch<float>(X, data, ns, 0, omega + ns * N, omega_cols + ns * N, omega_ld + ns * N, q, Yt[ns], true);
+    qr_y(Yt[ns], X.d[ns], X.Ig(ns), int(K[ns]), X.d[ns], Qy[ns], X.d[ns], nullptr, true, X.off);   // C2
+    slab_zpass();
+    cudaEvent_t e = ctx.events->get();
+    RT_CUDA(cudaEventRecord(e, ctx.stream));
+    RT_CUDA(cudaStreamWaitEvent(ctx.comm_stream, e, 0));
+    comm->side()->allreduce_sum(Zs, size_t(Jls * K[ns]), ctx.comm_stream);                           // C3
+    c3_done = ctx.events->get();
+    RT_CUDA(cudaEventRecord(c3_done, ctx.comm_stream));
+  }
+  auto finish_slab = [&]() {                   // after the other modes: the slab mode's remaining steps
+    if (!c3ovl) return;
+    RT_CUDA(cudaStreamWaitEvent(ctx.stream, c3_done, 0));
+    slab_product(q == 1);
+    for (int it = 1; it < q; ++it) {
+      slab_zpass();
+      allreduce(comm, true, Zs, Jls * K[ns], ctx.stream);                                           // C3
+      slab_product(it == q - 1);
+    }
+  };
   auto first_sketch = [&](int n) {
     const void* const* om = omega + n * N;
     const int64_t* oc = omega_cols + n * N;
     const int64_t* ol = omega_ld + n * N;
     if (dist() && n == N - 1) {               // slab mode: the whole mode on the main stream
+      if (c3ovl) return;                       // (overlapped: started above, finished by finish_slab)
       sketch<float>(X, data, n, 0, om, oc, ol, q, Yt[n]);
       qr_y(Yt[n], X.d[n], X.Ig(n), int(K[n]), X.d[n], Qt[n], X.d[n], nullptr, true, X.off);
       it_done[n] = q;
@@ -597,6 +659,7 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
         fork_qr(n, it == q - 1 ? Qt[n] : Qy[n]);
       }
   }
+  finish_slab();
   for (int n = 0; n < N; ++n)
     if (done_q[n]) wait_q(n);                  // join
   ctx.sm_reserve = saved_reserve;

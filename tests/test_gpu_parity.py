@@ -381,7 +381,7 @@ def test_slab_partial_sums_equal_unsharded(P, h):
     h.sync()
 
 
-def _run_loopback(P, x, cfg, oms, nranks, bounds):
+def _run_loopback(P, x, cfg, oms, nranks, bounds, options=()):
     grp = P.LoopbackGroup(nranks)
     out = [None] * nranks
     errs = []
@@ -392,6 +392,8 @@ def _run_loopback(P, x, cfg, oms, nranks, bounds):
             s = torch.cuda.Stream()
             with torch.cuda.stream(s):
                 hh = P.Handle(stream=s, loopback_group=grp, rank=r)
+                for o, v in options:
+                    hh.set_option(o, v)
                 lo, hi = bounds[r]
                 xs = dev(np.asfortranarray(x[:, :, lo:hi]))
                 loc = []
@@ -437,5 +439,33 @@ def test_loopback_multirank_hosvd(P, h, nranks):
     qg = out[0]["Q"][:2] + [q_last]
     for n in range(3):
         assert M.subspace(qg[n], ref["Q"][n]) <= 1e-5
+    assert M.recon(out[0]["G"], qg, ref["G"], ref["Q"]) <= 1e-5
+    assert abs(out[0]["err"][0] - ref["E"]) / ref["E"] <= 1e-5
+
+
+@pytest.mark.parametrize("nranks,opts", [(2, ()), (3, ()), (2, ((100, 270),)), (3, ((3, 1),))])
+def test_loopback_overlapped_hosvd(P, nranks, opts):
+    """The overlapped distributed schedule (K_n % 4 == 0 so every power step takes reading R31): the
+    replicated modes' QRs on the side stream, the slab mode's Z allreduce (C3) on the side
+    communicator and a third stream while the other modes proceed, then its product from the summed
+    Z.  2 and 3 emulated ranks (loopback), with the overlap off (option 270) and with tf32-rounded
+    Omega (option 3): the gathered result equals the oracle; replicated outputs agree bit for bit."""
+    cfg = dataclasses.replace(synth.CONFIGS["cfg5"].scaled((48, 40, 36), (6, 6, 6), (6, 6, 6)), q=1, p=10)
+    assert all(cfg.K(n) % 4 == 0 for n in range(3))
+    x = synth.make_tensor(cfg)
+    oms = [synth.gaussian_omega(cfg, n) for n in range(3)]
+    if any(o == 3 for o, _ in opts):
+        oms = [synth.round_tf32(o) for o in oms]
+    ref = oracle.hosvd(x, cfg.ranks, oms, q=1)
+    cuts = np.linspace(0, cfg.dims[2], nranks + 1).astype(int)
+    out = _run_loopback(P, x, cfg, oms, nranks, [(int(cuts[r]), int(cuts[r + 1])) for r in range(nranks)], opts)
+    for r in range(1, nranks):
+        np.testing.assert_array_equal(out[r]["G"], out[0]["G"])
+        for n in range(2):
+            np.testing.assert_array_equal(out[r]["Q"][n], out[0]["Q"][n])
+    qg = out[0]["Q"][:2] + [np.concatenate([out[r]["Q"][2] for r in range(nranks)], axis=0)]
+    for n in range(3):
+        assert M.orth(qg[n]) <= 1e-12
+        assert M.subspace(qg[n], ref["Q"][n]) <= 1e-5, (n, M.subspace(qg[n], ref["Q"][n]))
     assert M.recon(out[0]["G"], qg, ref["G"], ref["Q"]) <= 1e-5
     assert abs(out[0]["err"][0] - ref["E"]) / ref["E"] <= 1e-5
