@@ -73,7 +73,7 @@ class Engine {
   // (a8) residual pass: E and E_gram from X, G (R_1..R_N), Q (I_n(local) x R_n, ld I_n(local))
   template <typename T>
   void rel_error(const TView& X, const T* data, const double* G, const int64_t* R, const double* const* Q,
-                 double* E, double* Eg);
+                 double* E, double* Eg, bool ortho_q = false);
   // drivers
   template <typename T>
   void hosvd(const TView& X, const int64_t* R, int q, int kind, const void* const* omega,

@@ -167,7 +167,10 @@ void residual(const Ctx& ctx, Arena& ws, const T* X, int64_t J, int64_t In, cons
 // tcgen05 residual (ttm_tc.cu): same sums with Xhat = P Q^T built on the tensor cores (fp32 data,
 // R <= 64, J % 4 == 0, ldp % 4 == 0).  Returns false (nothing launched) when not applicable.
 bool residual_tc(const Ctx& ctx, Arena& ws, const float* X, int64_t J, int64_t In, const float* P, int64_t ldp,
-                 int R, const float* Q, int64_t ldq, double* out2, const float* rscale = nullptr);
+                 int R, const float* Q, int64_t ldq, double* out2, const float* rscale = nullptr,
+                 const float* pscale = nullptr);
+// pscale (nullable): device fp16 scale of P (resid_scale s[1]): the fp16-split residual
+// (residual_h16_kernel) with the tf32 kernel as its gated twin (runs when *pscale == 0)
 // out2 = fixed-order sums of n (a, b) pairs
 void reduce_pairs(const Ctx& ctx, const double* part, int n, double* out2);
 
@@ -178,7 +181,8 @@ void sumsq(const Ctx& ctx, Arena& ws, const double* x, int64_t n, double* out);
 // rscale (nullable): the power-of-two scale the residual sums were taken at (resid_scale)
 void finalize_err(const Ctx& ctx, const double* sums /*res, xx*/, const double* gg, double* E, double* Eg,
                   const float* rscale = nullptr);
-// *s = 2^-e with rms = sqrt(gg / numel) in [2^(e-1), 2^e): the residual pass works on s X (exact)
+// s[0] = 2^-e with rms = sqrt(gg / numel) in [2^(e-1), 2^e): the residual pass works on s X (exact);
+// s[1] = the fp16 scale of P for the fp16-split residual (0: the tf32 residual)
 void resid_scale(const Ctx& ctx, const double* gg, double numel, float* s);
 
 void fill_zero(const Ctx& ctx, void* p, size_t bytes);

@@ -664,15 +664,26 @@ __global__ void finalize_err_kernel(const double* sums, const double* gg, double
 // Power-of-two scale of the residual pass: rms(X) ~ ||G|| / sqrt(numel) (orthonormal factors) is
 // brought near 1 so the fp32 squares of the data and of the residual neither underflow (|x| <
 // 1e-19) nor overflow (|x| > 1e19).  1 when ||G|| is 0 or not finite.
+// s[1] = the fp16 scale of P (the core expanded over all but the last mode) for the fp16-split
+// residual: every |P_jr| <= ||P||_F = ||G||_F (orthonormal factors), so s[1] = 2^(14 - e_G) with
+// ||G|| in [2^(e_G-1), 2^e_G) keeps |s[1] P| < 2^14, inside the fp16 range; 0 (the tf32 residual
+// runs) when ||G|| is 0 or not finite.
 __global__ void resid_scale_kernel(const double* gg, double numel, float* s) {
-  float r = 1.f;
+  float r = 1.f, sp = 0.f;
   const double rms = sqrt(*gg / numel);
   if (rms > 0.0 && isfinite(rms)) {
     int e;
     frexp(rms, &e);                                    // rms in [2^(e-1), 2^e)
     r = ldexpf(1.f, max(-120, min(120, -e)));
   }
-  *s = r;
+  const double ng = sqrt(*gg);
+  if (ng > 0.0 && isfinite(ng)) {
+    int e;
+    frexp(ng, &e);
+    if (14 - e >= -120 && 14 - e <= 113) sp = ldexpf(1.f, 14 - e);
+  }
+  s[0] = r;
+  s[1] = sp;
 }
 
 __global__ void nonfinite_kernel(const double* __restrict__ x, int64_t n, int* status) {

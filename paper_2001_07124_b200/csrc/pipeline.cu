@@ -668,7 +668,7 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
   double* Gt = ws.alloc_n<double>(gsz);
   core<float>(X, data, Qt, ldq, K, Gt, g1);
   truncate(X, Gt, K, Qt, ldq, R, Q_out, G_out);
-  if (E || Eg) rel_error<float>(X, data, G_out, R, Q_out, E, Eg);
+  if (E || Eg) rel_error<float>(X, data, G_out, R, Q_out, E, Eg, true);
   ws.rewind(mk);
   xs_slot = nullptr;
   return true;
@@ -778,9 +778,12 @@ void Engine::truncate(const TView& X, const double* Gt, const int64_t* K, const 
 }
 
 // ------------------------------------------------------------- residual (a8)
+// ortho_q: the factors are orthonormal (the drivers' own output), so ||P||_F = ||G||_F bounds P's
+// entries and the fp16-split residual may scale P from ||G||; a caller's factors (rtucker_core) take
+// the tf32 residual
 template <typename T>
 void Engine::rel_error(const TView& X, const T* data, const double* G, const int64_t* R, const double* const* Q,
-                       double* E, double* Eg) {
+                       double* E, double* Eg, bool ortho_q) {
   const int N = X.N;
   const auto mk = ws.mark();
   double* sums = ws.alloc_n<double>(2);
@@ -838,10 +841,13 @@ void Engine::rel_error(const TView& X, const T* data, const double* G, const int
   for (int k = 0; k < N - 1; ++k) J *= X.d[k];
   // the sums are taken of s X and s X^ (s a power of two from ||G||: rms(X) near 1), so fp32
   // squares of data at any scale stay in range; E is unchanged, E_gram rescales exactly
-  float* rs = ws.alloc_n<float>(1);
+  float* rs = ws.alloc_n<float>(2);
   resid_scale(ctx, gg, double(X.size()) * double(X.glob) / double(X.d[N - 1]), rs);
   bool done = false;
-  if constexpr (std::is_same<T, float>::value) done = residual_tc(ctx, ws, data, J, Il, P, J, Rl, QL, Il, sums, rs);
+  if constexpr (std::is_same<T, float>::value) {
+    // the fp16-split residual (R29) with P at the power-of-two scale rs[1] from ||G||
+    done = residual_tc(ctx, ws, data, J, Il, P, J, Rl, QL, Il, sums, rs, ortho_q ? rs + 1 : nullptr);
+  }
   if (!done) residual<T>(ctx, ws, data, J, Il, P, Rl, QL, Il, sums, rs);
   allreduce(comm, dist(), sums, 2, ctx.stream);                                    // C5
   finalize_err(ctx, sums, gg, E, Eg, rs);
@@ -885,7 +891,7 @@ void Engine::hosvd(const TView& X, const int64_t* R, int q, int kind, const void
   double* Gt = ws.alloc_n<double>(gsz);
   core<T>(X, data, Qt, ldq, K, Gt);
   truncate(X, Gt, K, Qt, ldq, R, Q_out, G_out);
-  if (E || Eg) rel_error<T>(X, data, G_out, R, Q_out, E, Eg);
+  if (E || Eg) rel_error<T>(X, data, G_out, R, Q_out, E, Eg, true);
   ws.rewind(mk);
   xs_slot = nullptr;
 }
@@ -972,7 +978,7 @@ void Engine::sthosvd(const TView& X, const int64_t* R, int q, int kind, const vo
     S.d[n] = R[n];
     if (n == N - 1) { S.glob = R[n]; S.off = 0; }      // the last mode is now replicated
   }
-  if (E || Eg) rel_error<T>(X, static_cast<const T*>(X.data), G_out, R, Q_out, E, Eg);
+  if (E || Eg) rel_error<T>(X, static_cast<const T*>(X.data), G_out, R, Q_out, E, Eg, true);
   ws.rewind(mk);
   xs_slot = nullptr;
 }
@@ -1084,7 +1090,7 @@ void Engine::pet(const TView& X, const int64_t* R, const void* const* omega, con
     cur[n] = k;
   }
   truncate(X, Sc, K, Qt, ldq, R, Q_out, G_out);                                   // line 5 (R1)
-  if (E || Eg) rel_error<T>(X, data, G_out, R, Q_out, E, Eg);
+  if (E || Eg) rel_error<T>(X, data, G_out, R, Q_out, E, Eg, true);
   ws.rewind(mk);
 }
 
@@ -1186,7 +1192,7 @@ void Engine::rp_hooi(const TView& X, const int64_t* R, int sweeps, const double*
     canon(Q_out[n], X.d[n], int(R[n]), X.d[n], n == N - 1 ? X.off : 0, n == N - 1, U, int(R[n]));
   }
   core<T>(X, data, Q_out, ldq, R, G_out);                                                // line 7
-  if (E || Eg) rel_error<T>(X, data, G_out, R, Q_out, E, Eg);
+  if (E || Eg) rel_error<T>(X, data, G_out, R, Q_out, E, Eg, true);
   ws.rewind(mk);
   xs_slot = nullptr;
 }
@@ -1218,9 +1224,9 @@ template void Engine::core<float>(const TView&, const float*, const double* cons
 template void Engine::core<double>(const TView&, const double*, const double* const*, const int64_t*,
                                    const int64_t*, double*, const double*);
 template void Engine::rel_error<float>(const TView&, const float*, const double*, const int64_t*,
-                                       const double* const*, double*, double*);
+                                       const double* const*, double*, double*, bool);
 template void Engine::rel_error<double>(const TView&, const double*, const double*, const int64_t*,
-                                        const double* const*, double*, double*);
+                                        const double* const*, double*, double*, bool);
 template void Engine::hosvd<float>(const TView&, const int64_t*, int, int, const void* const*, const int64_t*,
                                    const int64_t*, double* const*, double*, double*, double*);
 template void Engine::hosvd<double>(const TView&, const int64_t*, int, int, const void* const*, const int64_t*,

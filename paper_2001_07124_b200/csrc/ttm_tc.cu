@@ -2243,6 +2243,7 @@ struct RParams {
   int nblk;           // i blocks of 64
   double* part;       // [grid][2]
   const float* rscale;   // power-of-two scale applied to x and x^ (resid_scale), nullable
+  const float* gate;     // tf32 kernel: run only if *gate == 0 (twin of the fp16-split residual)
 };
 
 template <int RP>
@@ -2251,6 +2252,7 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constan
                    const __grid_constant__ CUtensorMap tqh, const __grid_constant__ CUtensorMap tql, const RParams p) {
   using L = RSmem<RP>;
   constexpr int NCH = RP / KC;                 // r chunks
+  if (p.gate && *p.gate != 0.f) return;       // the fp16-split residual ran (R29)
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::off_bar);
   uint64_t* st_full = bar;                     // [RNS] Q chunks + X tile landed
@@ -2415,6 +2417,199 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constan
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
+// fp16-split residual (R29 applied to a8): X^ = P Q_N^T with P (the core expanded over all but the
+// last mode; |P_jr| <= ||G||, scale s from resid_scale) split as s P = P_hi + P_lo in fp16 (A in TMEM, 64 r = 32 + 32 columns) and
+// Q^T as fp16 [2^14 Q_hi | 2^14 Q_lo] K-major rows (64 r = 128 B, one box per 64 i each): wide issuer
+// A_hi [Q_hi | Q_lo] (N = 128), narrow issuer A_lo Q_hi (N = 64), 4 K = 16 steps per i block -- half
+// the MMA instructions and half the B bytes of the 3xTF32 form per X tile.  X^ = (v + w + z) / (s 2^14).
+// Gated on s: it stands down (s == 0: ||G|| zero or not finite) for residual_tc_kernel.
+struct RSmemH {
+  static constexpr int RP = 64;
+  static constexpr uint32_t kP = uint32_t(RP) * BM * 4;          // raw P tile [64 r][128 j]
+  static constexpr uint32_t kQ = uint32_t(RNB) * 128;            // one [64 i][64 r] fp16 box (8 KB)
+  static constexpr uint32_t kXt = uint32_t(BM) * RNB * 4;        // X tile [64 i][128 j]
+  static constexpr int NS = 4;
+  static constexpr uint32_t per_stage = 2 * kQ + kXt;
+  static constexpr uint32_t off_p = 0;
+  static constexpr uint32_t off_st = kP;
+  static constexpr uint32_t off_bar = off_st + NS * per_stage;
+  static constexpr uint32_t bytes = off_bar + 8 * (2 * NS + 8) + 16;
+};
+
+__global__ void __launch_bounds__(NTHREADS, 1)
+residual_h16_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmp,
+                    const __grid_constant__ CUtensorMap tqh, const __grid_constant__ CUtensorMap tql, const RParams p,
+                    const float* __restrict__ pscale) {
+  using L = RSmemH;
+  constexpr int RP = L::RP, NS = L::NS;
+  if (*pscale == 0.f) return;                          // the tf32 residual runs instead (R29)
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::off_bar);
+  uint64_t* st_full = bar;
+  uint64_t* st_free = bar + NS;
+  uint64_t* p_full = bar + 2 * NS;
+  uint64_t* p_free = bar + 2 * NS + 1;
+  uint64_t* a_ready = bar + 2 * NS + 2;
+  uint64_t* a_free = bar + 2 * NS + 3;
+  uint64_t* acc_full = bar + 2 * NS + 4;
+  uint64_t* acc_empty = bar + 2 * NS + 6;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2 * NS + 8);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t my_tiles = (p.ntiles > blockIdx.x) ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  constexpr uint32_t kAcc = 2 * RNB;                  // [hi.hi | hi.lo] per buffer (wide issuer)
+  constexpr uint32_t kAcc1 = 2 * kAcc;                // lo.hi buffers (narrow issuer)
+  constexpr uint32_t kA = kAcc1 + 2 * RNB;            // A hi (32 columns), then A lo (32 columns)
+  static_assert(kA + RP <= 512, "residual TMEM plan");
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) { mbar_init(&st_full[s], 1); mbar_init(&st_free[s], 128); }
+    mbar_init(p_full, 1);
+    mbar_init(p_free, 128);
+    mbar_init(a_ready, 128);
+    mbar_init(a_free, 2);
+    for (int b = 0; b < 2; ++b) { mbar_init(&acc_full[b], 2); mbar_init(&acc_empty[b], 128); }
+    fence_barrier_init();
+    tma_prefetch(&tmx); tma_prefetch(&tmp); tma_prefetch(&tqh); tma_prefetch(&tql);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (warp == 0) {
+    if (lane == 0) {                                   // ---------------- TMA producer
+      Ring rg;
+      int it = 0;
+      const uint64_t pol = policy_evict_first();
+      const uint64_t pq = policy_evict_last();
+      for (int64_t u = 0; u < my_tiles; ++u) {
+        const int j0 = int((blockIdx.x + u * gridDim.x) * BM);
+        if (u >= 1) mbar_wait(p_free, uint32_t(u - 1) & 1);
+        mbar_expect_tx(p_full, L::kP);
+        for (int c = 0; c < RP / KC; ++c) tma_load_2d(smem + L::off_p + c * (BM * KC * 4), &tmp, p_full, j0, c * KC);
+        for (int b = 0; b < p.nblk; ++b, ++it, rg.next<NS>()) {
+          if (it >= NS) mbar_wait(&st_free[rg.s], rg.ph ^ 1);
+          uint8_t* st = smem + L::off_st + rg.s * L::per_stage;
+          mbar_expect_tx(&st_full[rg.s], L::per_stage);
+          tma_load_2d_hint(st, &tqh, &st_full[rg.s], 0, b * RNB, pq);            // [Q_hi | Q_lo] adjacent:
+          tma_load_2d_hint(st + L::kQ, &tql, &st_full[rg.s], 0, b * RNB, pq);    // one N = 128 operand
+          tma_load_2d_hint(st + 2 * L::kQ, &tmx, &st_full[rg.s], j0, b * RNB, pol);
+        }
+      }
+    }
+  } else if (warp == 1 || warp == 6) {                // ---------------- MMA issuers (whole warps)
+    const bool wide = warp == 1;
+    const uint32_t idesc = idesc_f16(BM, wide ? 2 * RNB : RNB, 0);
+    Ring rg;
+    int64_t g = 0;
+    for (int64_t u = 0; u < my_tiles; ++u) {
+      mbar_wait(a_ready, uint32_t(u) & 1);
+      tc_fence_after();
+      for (int b = 0; b < p.nblk; ++b, ++g, rg.next<NS>()) {
+        const int ab = int(g & 1);
+        if (g >= 2) mbar_wait(&acc_empty[ab], uint32_t((g >> 1) - 1) & 1);
+        mbar_wait(&st_full[rg.s], rg.ph);
+        tc_fence_after();
+        const uint32_t st = smem_u32(smem + L::off_st + rg.s * L::per_stage);
+        const uint32_t acc = tmem + (wide ? uint32_t(ab) * kAcc : kAcc1 + uint32_t(ab) * RNB);
+#pragma unroll
+        for (int kk = 0; kk < RP / 16; ++kk) {
+          const uint32_t a = tmem + kA + (wide ? 0u : 32u) + 8 * kk;
+          mma_f16_ts_w(acc, a, bdesc_sw128(st, kk), idesc, kk == 0 ? 0u : 1u);
+        }
+        mma_commit_w(&acc_full[ab]);
+      }
+      mma_commit_w(a_free);
+    }
+  } else if (warp >= 2 && warp <= 5) {                 // ---------------- split P / epilogue
+    const int q4 = warp & 3;
+    const int r = 32 * q4 + lane;
+    const uint32_t lane_base = tmem + (uint32_t(32 * q4) << 16);
+    const float sc = *pscale;                            // |sc P| < 2^14 (resid_scale)
+    const float inv = 1.0f / (sc * kQScale);             // exact: powers of two
+    const float rs = p.rscale ? *p.rscale : 1.f;
+    const float invr = inv * rs;
+    double res = 0.0, xx = 0.0;
+    Ring rg;
+    int64_t g = 0;
+    for (int64_t u = 0; u < my_tiles; ++u) {
+      mbar_wait(p_full, uint32_t(u) & 1);
+      if (u >= 1) mbar_wait(a_free, uint32_t(u - 1) & 1);
+      tc_fence_after();
+      const float* ps = reinterpret_cast<const float*>(smem + L::off_p);
+      float v[RP];
+#pragma unroll
+      for (int q = 0; q < RP; ++q) v[q] = ps[(q / KC) * (BM * KC) + (q % KC) * BM + r] * sc;
+      uint32_t hi[32], lo[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) split_h16x2(v[2 * c], v[2 * c + 1], hi[c], lo[c]);
+      tmem_st16(lane_base + kA, *reinterpret_cast<const uint32_t(*)[16]>(&hi[0]));
+      tmem_st16(lane_base + kA + 16, *reinterpret_cast<const uint32_t(*)[16]>(&hi[16]));
+      tmem_st16(lane_base + kA + 32, *reinterpret_cast<const uint32_t(*)[16]>(&lo[0]));
+      tmem_st16(lane_base + kA + 48, *reinterpret_cast<const uint32_t(*)[16]>(&lo[16]));
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(p_free);
+      mbar_arrive(a_ready);
+      for (int b = 0; b < p.nblk; ++b, ++g, rg.next<NS>()) {
+        const int ab = int(g & 1);
+        mbar_wait(&st_full[rg.s], rg.ph);
+        mbar_wait(&acc_full[ab], uint32_t(g >> 1) & 1);
+        tc_fence_after();
+        const float* xt = reinterpret_cast<const float*>(smem + L::off_st + rg.s * L::per_stage + 2 * L::kQ);
+        float tr = 0.f, tx = 0.f;
+#pragma unroll
+        for (int cb = 0; cb < RNB / 16; ++cb) {
+          uint32_t a0[16], a1[16], a2[16];
+          tmem_ld16(lane_base + uint32_t(ab) * kAcc + 16 * cb, a0);           // A_hi Q_hi
+          tmem_ld16(lane_base + uint32_t(ab) * kAcc + RNB + 16 * cb, a1);     // A_hi Q_lo
+          tmem_ld16(lane_base + kAcc1 + uint32_t(ab) * RNB + 16 * cb, a2);    // A_lo Q_hi
+          tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const float x = xt[(16 * cb + q) * BM + r] * rs;
+            const float d = x - (__uint_as_float(a0[q]) + (__uint_as_float(a1[q]) + __uint_as_float(a2[q]))) * invr;
+            tr = fmaf(d, d, tr);
+            tx = fmaf(x, x, tx);
+          }
+        }
+        res += double(tr);
+        xx += double(tx);
+        tc_fence_before();
+        mbar_arrive(&acc_empty[ab]);
+        mbar_arrive(&st_free[rg.s]);
+      }
+    }
+    __shared__ double red[2][4];
+    for (int o = 16; o; o >>= 1) {
+      res += __shfl_xor_sync(0xffffffffu, res, o);
+      xx += __shfl_xor_sync(0xffffffffu, xx, o);
+    }
+    if (lane == 0) { red[0][q4] = res; red[1][q4] = xx; }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (threadIdx.x == 64) {
+      p.part[2 * blockIdx.x] = red[0][0] + red[0][1] + red[0][2] + red[0][3];
+      p.part[2 * blockIdx.x + 1] = red[1][0] + red[1][1] + red[1][2] + red[1][3];
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+// Q (In x R fp32, col-major ldq) -> fp16 [In rows][64] rows of 2^14 Q_hi and of 2^14 Q_lo (r >= R zero)
+__global__ void qsplit_rows_h16_kernel(const float* __restrict__ Q, int64_t In, int R, int64_t ldq,
+                                       __half* __restrict__ qh, __half* __restrict__ ql) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= In * 64) return;
+  const int64_t i = e / 64;
+  const int r = int(e % 64);
+  const float v = r < R ? Q[i + ldq * r] * kQScale : 0.f;
+  const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+  qh[e] = __float2half_rn(h);
+  ql[e] = __float2half_rn(v - h);
+}
+
 template <int RP>
 void launch_r(const Ctx& ctx, const CUtensorMap& tx, const CUtensorMap& tp, const CUtensorMap& th,
               const CUtensorMap& tl, const RParams& p, int grid) {
@@ -2442,7 +2637,7 @@ __global__ void split_transpose_kernel(const float* __restrict__ Q, int64_t In, 
 }  // namespace
 
 bool residual_tc(const Ctx& ctx, Arena& ws, const float* X, int64_t J, int64_t In, const float* P, int64_t ldp,
-                 int R, const float* Q, int64_t ldq, double* part_out2, const float* rscale) {
+                 int R, const float* Q, int64_t ldq, double* part_out2, const float* rscale, const float* pscale) {
   if (ctx.simt() || R < 1 || R > 64) return false;
   if (!aligned(X, 16) || !aligned(P, 16) || (J % 4) || (ldp % 4) || J > INT32_MAX || In > INT32_MAX) return false;
   const int rp = R <= 32 ? 32 : 64;
@@ -2471,6 +2666,27 @@ bool residual_tc(const Ctx& ctx, Arena& ws, const float* X, int64_t J, int64_t I
   const int grid = int(std::min<int64_t>(p.ntiles, ctx.num_sms));
   p.part = ws.alloc_n<double>(2 * grid);
   p.rscale = rscale;
+  p.gate = nullptr;
+  if (pscale && ctx.tc_h16 && !ctx.resid_tf32) {
+    // fp16-split form (its tf32 twin below runs instead when X's scale is 0)
+    __half* qh = ws.alloc_n<__half>(In * 64);
+    __half* ql = ws.alloc_n<__half>(In * 64);
+    launch(ctx, "split_transpose", [&] {
+      qsplit_rows_h16_kernel<<<unsigned(cdiv(In * 64, 256)), 256, 0, ctx.stream>>>(Q, In, R, ldq, qh, ql);
+    });
+    CUtensorMap hh, hl;
+    const uint64_t d[2] = {64, uint64_t(In)}, st[1] = {128};
+    const uint32_t bx[2] = {64, uint32_t(RNB)};
+    if (make_map(&hh, qh, 2, d, st, bx, true, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_DATA_TYPE_FLOAT16) &&
+        make_map(&hl, ql, 2, d, st, bx, true, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_DATA_TYPE_FLOAT16)) {
+      static bool attr = false;
+      if (!attr) { set_smem(residual_h16_kernel, RSmemH::bytes); attr = true; }
+      launch(ctx, "residual_tc", [&] {
+        residual_h16_kernel<<<grid, NTHREADS, RSmemH::bytes, ctx.stream>>>(tx, tp, hh, hl, p, pscale);
+      });
+      p.gate = pscale;
+    }
+  }
   if (rp == 32) launch_r<32>(ctx, tx, tp, th, tl, p, grid);
   else launch_r<64>(ctx, tx, tp, th, tl, p, grid);
   // fixed-order final reduction of the per-CTA pairs
