@@ -4,7 +4,8 @@ reading R18).
 
 * cfg2 (500^3) and cfg3 (128^4 STHOSVD, Kronecker): element-wise metrics M2/M4-M7 against the
   fp64 oracle on the same inputs (the oracle finishes these in seconds).
-* cfg4 (2048x2048x256, noise-free): X = G x_1 U_1 x_2 U_2 x_3 U_3 with orthonormal U_n, so the
+* cfg4 (2048x2048x256, noise-free): the unmodified oracle.hosvd on the same device bytes (8.6 GB
+  in fp64); and a second, independent check: X = G x_1 U_1 x_2 U_2 x_3 U_3 with orthonormal U_n, so the
   randomized HOSVD of X is the lifted randomized HOSVD of the small core G with the reduced test
   matrices Omega'_n = (kron_{k!=n} U_k)^T Omega_n (exact algebra of Eq.(2)): the oracle
   runs on the 200x200x100 core and its factors are lifted by U_n.  Compared with the
@@ -118,6 +119,25 @@ def _reduce_omega(om, dims, n, us):
     for pos, k in enumerate(other):
         t = ttm(t, us[k].T, pos)
     return np.reshape(t, (-1, K), order="F")
+
+
+def test_cfg4_full_vs_oracle(P, hb):
+    """cfg4 at full size (2048 x 2048 x 256, q = 2) against the unmodified fp64 oracle.hosvd on the same
+    device bytes of X and Omega (8.6 GB in fp64: fits the host)."""
+    cfg = synth.CONFIGS["cfg4"]
+    X, _ = synth.make_tensor_device(cfg, "cuda")
+    N = cfg.order
+    om_dev = [synth.gaussian_omega_device(cfg, n, "cuda", tf32=True) for n in range(N)]
+    res = P.rtucker_hosvd(hb, X, cfg.ranks, cfg.p, cfg.q, om_dev)
+    hb.sync()
+    x64 = np.asfortranarray(_np(X).transpose(2, 1, 0)).astype(np.float64)
+    oms = [_np(o).astype(np.float64) for o in om_dev]
+    ref = oracle.hosvd(x64, cfg.ranks, oms, q=cfg.q)
+    del x64
+    for n in range(N):
+        assert M.rel_fro(_np(P.rtucker_sketch(hb, X, n, om_dev[n])), ref["Y0"][n]) <= 1e-5
+    hb.sync()
+    _check_vs_oracle(P, res, ref)
 
 
 def test_cfg4_full_vs_reduced_oracle(P, hb):
