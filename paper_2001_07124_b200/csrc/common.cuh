@@ -105,6 +105,7 @@ struct Ctx {
   int fuse_off = 0;             // HOSVD: 1 = no fused mode-1 sketch + mode-0 core pass (ablation 290 / 291)
   int fused_nbb = 3;            // fused pass: B slots (chunk pairs) 2 or 3 (ablation 292 / 293)
   int resid_tf32 = 0;           // residual pass: 1 = the 3xTF32 kernel only (ablation 294 / 295)
+  int tc_waves = 4;             // ttm_s split-K grids: CTA waves over the SMs (ablation 301..308)
   int tc_xw = 2;                // ttm_s strided modes: chunks per wide-row X stage (1 = swizzled 128 B rows;
                                 // ablation 231/232/234 select 1/2/4; cfg5 modes 1/2: 2 is fastest)
   cudaStream_t side_stream = nullptr;   // second stream of the handle (high priority): overlapped QRs

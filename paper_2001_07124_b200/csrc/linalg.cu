@@ -442,7 +442,10 @@ __global__ void __launch_bounds__(512) jacobi_kernel(EigBatch bt, double* Vscrat
         if (p > q) { const int tmp = p; p = q; q = tmp; }
         const double apq = A[p * ld + q];
         double c = 1.0, s = 0.0;
-        if (apq != 0.0) {
+        // threshold Jacobi: a pair whose |a_pq| is below k u sqrt(|a_pp a_qq|) is skipped (its rotation
+        // would move the diagonal by less than the convergence tolerance): the late sweeps skip most
+        // pairs and their row / column updates
+        if (fabs(apq) > double(k) * 1.1102230246251565e-16 * sqrt(fabs(A[p * ld + p] * A[q * ld + q]))) {
           const double tau = (A[q * ld + q] - A[p * ld + p]) / (2.0 * apq);
           const double tt = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
           c = 1.0 / sqrt(1.0 + tt * tt);

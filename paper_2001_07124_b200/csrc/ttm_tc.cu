@@ -1888,7 +1888,10 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
   p.cpb = amn ? 1 : cdiv(box.a, KC);
   p.nchunks = amn ? cdiv(box.b, KC) : p.cpb * box.b;
   const int64_t mtiles = cdiv(box.I, BM);
-  int64_t splits = std::max<int64_t>(1, (int64_t(ctx.num_sms) * 4 + mtiles - 1) / mtiles);
+  // split count: tc_waves CTA waves over the SMs (1: one CTA per SM for the whole pass, no wave
+  // quantization; the SMs left over when mtiles does not divide the SM count serve the side stream)
+  int64_t splits = ctx.tc_waves == 1 ? std::max<int64_t>(1, int64_t(ctx.num_sms - ctx.sm_reserve) / mtiles)
+                                     : std::max<int64_t>(1, (int64_t(ctx.num_sms) * ctx.tc_waves + mtiles - 1) / mtiles);
   splits = std::min<int64_t>(splits, std::max<int64_t>(1, p.nchunks / 8));
   splits = std::min<int64_t>(splits, 65535);
   // contiguous chunk range per split, a whole number of X stages
