@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(512) jacobi_kernel(EigBatch bt, double* Vscrat
   double* V = v_in_smem ? (sm + kk * ld) : (Vscratch + blockIdx.x * stride_scr);
   double* cs = (v_in_smem ? sm + 2 * kk * ld : sm + kk * ld);   // kk/2 pairs: c, s, p, q
   __shared__ double red[32];
-  __shared__ int s_done;
+  __shared__ int s_done, s_rot;
   const double* Ab = bt.A[blockIdx.x];
   double* W = bt.W[blockIdx.x];
   double* Vout = bt.V[blockIdx.x];
@@ -428,7 +428,8 @@ __global__ void __launch_bounds__(512) jacobi_kernel(EigBatch bt, double* Vscrat
     // converged when ||offdiag||_F <= k u ||diag||_F (u = 2^-53): below this the rotations only
     // shuffle rounding noise
     const double tol = double(k) * 1.1102230246251565e-16;
-    if (t == 0) s_done = (off <= tol * tol * dia) || (dia == 0.0);
+    // converged: off-diagonal norm below tolerance, or the previous sweep rotated no pair
+    if (t == 0) { s_done = (off <= tol * tol * dia) || (dia == 0.0) || (sweep > 0 && !s_rot); s_rot = 0; }
     __syncthreads();
     if (s_done) break;
     for (int round = 0; round < kk - 1; ++round) {
@@ -451,6 +452,7 @@ __global__ void __launch_bounds__(512) jacobi_kernel(EigBatch bt, double* Vscrat
           c = 1.0 / sqrt(1.0 + tt * tt);
           s = tt * c;
         }
+        if (s != 0.0) s_rot = 1;                      // benign race: every writer stores 1
         cs[4 * pi + 0] = c; cs[4 * pi + 1] = s;
         cs[4 * pi + 2] = p; cs[4 * pi + 3] = q;
       }
