@@ -320,11 +320,15 @@ def run_gpu(args, cfg):
     return out
 
 
+# the kernels of the residual pass (a8): P chain, residual kernel(s), reductions
+RESIDUAL_LABELS = ("residual_tc", "residual_simt", "pchain", "reduce_pairs", "finalize_err", "sumsq", "resid_scale",
+                   "split_transpose")
+
+
 def _pipeline(prof, ms, steps, xbytes):
     """throughput of sketch+QR+core (first sketch to truncated G) with the
     residual pass (a8: P chain + residual kernel) timed and reported separately."""
-    res_ms = sum(t for nm, _, t in prof if nm in ("residual_tc", "residual_simt", "pchain", "reduce_pairs",
-                                                   "finalize_err", "sumsq")) / steps
+    res_ms = sum(t for nm, _, t in prof if nm in RESIDUAL_LABELS) / steps
     pm = ms - res_ms
     return {"value": xbytes / (pm * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": pm, "residual_ms": res_ms}
 
