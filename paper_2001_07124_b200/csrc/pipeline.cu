@@ -451,10 +451,11 @@ bool Engine::power_step_r31(const TView& X, const float* data, int n, int K, con
   const int N = X.N;
   const Box bx = X.box(n);
   const bool last = (n == N - 1);
-  if (!ctx.tc_h16 || ctx.simt() || ctx.power_qrz || (last && dist()) || (K % 4) != 0 ||
-      !ttm_s_tc_ok(ctx, data, bx, K) || !xs_slot || xs_key != data)
+  if (!ctx.tc_h16 || ctx.simt() || ctx.power_qrz || (last && dist()) || !ttm_s_tc_ok(ctx, data, bx, K) || !xs_slot ||
+      xs_key != data)
     return false;
-  const int64_t In = bx.I, Jl = bx.J(), ldz = K;
+  // the fp32 Z of the tf32 twin: 16-byte row pitch (columns >= K are never read)
+  const int64_t In = bx.I, Jl = bx.J(), ldz = pad4(K);
   const auto mk = ws.mark();
   const int64_t ldz2 = 2 * int64_t(tc_npad(K));
   float* Z = ws.alloc_n<float>(Jl * ldz);
@@ -502,7 +503,7 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
     const bool main_only = dist() && n == N - 1;
     // every power step must take the R31 form (checked before anything is launched)
     if (q > 0 && !main_only &&
-        (!ctx.tc_h16 || ctx.power_qrz || (K[n] % 4) != 0 || !ttm_s_tc_ok(ctx, data, X.box(n), int(K[n]))))
+        (!ctx.tc_h16 || ctx.power_qrz || !ttm_s_tc_ok(ctx, data, X.box(n), int(K[n]))))
       return false;
   }
   // fused mode-1 sketch + first core stage: needs X's scale (q > 0) and mode 1 off the slab
@@ -547,9 +548,11 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
   // once Z is summed; later power iterations of the slab mode allreduce on the main stream.
   const int ns = N - 1;
   const int64_t Jls = X.box(ns).J();
-  const bool c3ovl = dist() && q > 0 && comm->side() && ctx.comm_stream && !ctx.power_qrz && (K[ns] % 4) == 0 &&
-                     ctx.tc_h16 && ttm_s_tc_ok(ctx, data, X.box(ns), int(K[ns]));
-  float* Zs = c3ovl ? ws.alloc_n<float>(Jls * K[ns]) : nullptr;
+  const bool c3ovl = dist() && q > 0 && comm->side() && ctx.comm_stream && !ctx.power_qrz && ctx.tc_h16 &&
+                     ttm_s_tc_ok(ctx, data, X.box(ns), int(K[ns]));
+  const int64_t ldzs = pad4(K[ns]);            // 16-byte row pitch of the slab mode's fp32 Z
+  float* Zs = c3ovl ? ws.alloc_n<float>(Jls * ldzs) : nullptr;
+  if (Zs && ldzs != K[ns]) fill_zero(ctx, Zs, sizeof(float) * Jls * ldzs);   // pad columns (summed by C3)
   cudaEvent_t c3_done = nullptr;
   // the slab mode's Z pass: Zs = s_z X_(N-1)^T Qy (fp32 partial sums of this slab), h16 pair
   auto slab_zpass = [&]() {
@@ -559,7 +562,7 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
     const float* QyT = working_copy<float>(ctx, ws, Qy[ns], X.d[ns], K[ns], X.d[ns], ldqt);
     const int ez = int(std::ceil(0.5 * std::log2(double(X.Ig(ns)))));
     LabelScope ls(ctx, "ttm_t_tc_pow");
-    RT_REQUIRE(ttm_t_tc(ctx, ws, data, bx, QyT, ldqt, int(K[ns]), Zs, K[ns], 1, bx.a * K[ns], 0, false, xs_slot, nullptr,
+    RT_REQUIRE(ttm_t_tc(ctx, ws, data, bx, QyT, ldqt, int(K[ns]), Zs, ldzs, 1, bx.a * ldzs, 0, false, xs_slot, nullptr,
                         xs_slot + 1, std::ldexp(1.0f, -(ez + 1))),
                kEUNSUPPORTED, "slab mode: Z pass rejected by the tensor-core path");
     ws.rewind(mz);
@@ -570,11 +573,11 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
     const auto mz = ws.mark();
     const int64_t ldz2 = 2 * int64_t(tc_npad(int(K[ns])));
     uint16_t* Z2 = ws.alloc_n<uint16_t>(Jls * ldz2);
-    split_rows_h16(ctx, Zs, Jls, int(K[ns]), K[ns], Z2);
+    split_rows_h16(ctx, Zs, Jls, int(K[ns]), ldzs, Z2);
     {
       LabelScope ls(ctx, "ttm_s_tc_pow");
       RT_REQUIRE(ttm_s_tc(ctx, ws, data, bx, reinterpret_cast<const float*>(Z2), ldz2, false, int(K[ns]), Yt[ns],
-                          X.d[ns], true, xs_slot, nullptr, Zs, K[ns]),
+                          X.d[ns], true, xs_slot, nullptr, Zs, ldzs),
                  kEUNSUPPORTED, "slab mode: power product not launched");
     }
     ws.rewind(mz);
@@ -587,7 +590,7 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
     cudaEvent_t e = ctx.events->get();
     RT_CUDA(cudaEventRecord(e, ctx.stream));
     RT_CUDA(cudaStreamWaitEvent(ctx.comm_stream, e, 0));
-    comm->side()->allreduce_sum(Zs, size_t(Jls * K[ns]), ctx.comm_stream);                           // C3
+    comm->side()->allreduce_sum(Zs, size_t(Jls * ldzs), ctx.comm_stream);                            // C3
     c3_done = ctx.events->get();
     RT_CUDA(cudaEventRecord(c3_done, ctx.comm_stream));
   }
@@ -597,7 +600,7 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
     slab_product(q == 1);
     for (int it = 1; it < q; ++it) {
       slab_zpass();
-      allreduce(comm, true, Zs, Jls * K[ns], ctx.stream);                                           // C3
+      allreduce(comm, true, Zs, Jls * ldzs, ctx.stream);                                            // C3
       slab_product(it == q - 1);
     }
   };
