@@ -106,6 +106,7 @@ struct Ctx {
   int fused_nbb = 3;            // fused pass: B slots (chunk pairs) 2 or 3 (ablation 292 / 293)
   int resid_tf32 = 0;           // residual pass: 1 = the 3xTF32 kernel only (ablation 294 / 295)
   int tc_waves = 4;             // ttm_s split-K grids: CTA waves over the SMs (ablation 301..308)
+  int fused_seg = 16;           // fused pass: chunks per accumulator segment (ablation 316 / 332: 16 / 32)
   int tc_xw = 2;                // ttm_s strided modes: chunks per wide-row X stage (1 = swizzled 128 B rows;
                                 // ablation 231/232/234 select 1/2/4; cfg5 modes 1/2: 2 is fastest)
   cudaStream_t side_stream = nullptr;   // second stream of the handle (high priority): overlapped QRs

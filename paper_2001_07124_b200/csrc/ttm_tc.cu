@@ -2147,7 +2147,8 @@ bool sketch1_core0(const Ctx& ctx, Arena& ws, const float* X, Box b1, Box b0, co
   p.a = b1.a; p.I = b1.I; p.b = b1.b; p.K = K1; p.C = K0;
   p.cpb = b1.a / KC;
   p.nchunks = p.cpb * b1.b;
-  p.seg = int(std::min<int64_t>(16, p.cpb));
+  p.seg = int(std::min<int64_t>(ctx.fused_seg, p.cpb));
+  while (p.cpb % p.seg) --p.seg;
   const int64_t mtiles = b1.I / BM;
   const int64_t want = std::max<int64_t>(1, (int64_t(ctx.num_sms) * 4 + mtiles - 1) / mtiles);
   const int64_t bper = cdiv(b1.b, std::min<int64_t>(want, b1.b));      // whole betas per split
