@@ -23,7 +23,8 @@
 //    columns and transposes it through a 32x33 shared tile.
 //
 // fp32 accumulators hold at most ~512 terms (a CTA's column range is <= 512 K columns); the
-// per-CTA partials are added into the fp64 Y with fp64 atomics (one per (row, group) per CTA).
+// each CTA writes its partials to its own slice, and a reduce kernel adds the slices into the fp64 Y
+// in a fixed order: bitwise reproducible run to run for float data too.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -77,14 +78,28 @@ __device__ __forceinline__ void cs_quad(unsigned char* rowb, int4 o, float4 s, A
   }
 }
 
+// the CTA's partial sums go to its own slice part[blockIdx.y][c][i] (no atomics): cs_reduce adds
+// the slices in blockIdx.y order, so the result is bitwise reproducible for any data
 template <typename A>
-__device__ inline void cs_flush(const A* acc, int K, int TI, int64_t i0, int64_t I, double* Y, int64_t ldy) {
+__device__ inline void cs_flush(const A* acc, int K, int TI, int64_t i0, int64_t I, A* part) {
+  part += size_t(blockIdx.y) * K * I;
   for (int e = threadIdx.x; e < K * TI; e += blockDim.x) {
     const int c = e / TI, r = e - c * TI;
     const int64_t i = i0 + r;
-    const A v = acc[e];
-    if (i < I && v != A(0)) atomicAdd(&Y[i + c * ldy], double(v));
+    if (i < I) part[i + c * I] = acc[e];
   }
+}
+
+// Y[i, c] = sum_y part[y][c][i] in fp64, y ascending
+template <typename A>
+__global__ void cs_reduce_kernel(const A* __restrict__ part, int64_t ny, int64_t KI, int64_t I,
+                                 double* __restrict__ Y, int64_t ldy) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= KI) return;
+  double s = 0.0;
+  for (int64_t y = 0; y < ny; ++y) s += double(part[e + y * KI]);
+  const int64_t c = e / I, i = e - c * I;
+  Y[i + c * ldy] = s;
 }
 
 // ---------------------------------------------------------------- a == 1: X_(0) columns contiguous
@@ -92,7 +107,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) cs_rows_kernel(const T* __restrict__ X, int64_t I, int64_t J, int64_t Jpad,
                                                       const uint32_t* __restrict__ off,
                                                       const float* __restrict__ sgn, int K, int64_t jchunk,
-                                                      double* __restrict__ Y, int64_t ldy) {
+                                                      typename CsAcc<T>::type* __restrict__ part) {
   using A = typename CsAcc<T>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   A* acc = reinterpret_cast<A*>(smem_raw);                  // [K + 1][TI], row K = trash
@@ -117,7 +132,7 @@ __global__ void __launch_bounds__(256) cs_rows_kernel(const T* __restrict__ X, i
       cs_quad<A>(rowb, __ldg(oq + q), __ldg(sq + q), A(x[4 * q]), A(x[4 * q + 1]), A(x[4 * q + 2]), A(x[4 * q + 3]));
   }
   __syncthreads();
-  cs_flush(acc, K, TI, i0, I, Y, ldy);
+  cs_flush(acc, K, TI, i0, I, part);
 }
 
 // ---------------------------------------------------------------- a > 1: transpose per warp
@@ -125,7 +140,7 @@ template <typename T, int U>
 __global__ void __launch_bounds__(256) cs_mid_kernel(const T* __restrict__ X, int64_t a, int64_t I, int64_t J,
                                                      int64_t Jpad, const uint32_t* __restrict__ off,
                                                      const float* __restrict__ sgn, int K, int64_t jchunk,
-                                                     double* __restrict__ Y, int64_t ldy) {
+                                                     typename CsAcc<T>::type* __restrict__ part) {
   using A = typename CsAcc<T>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int TI = blockDim.x;
@@ -168,7 +183,7 @@ __global__ void __launch_bounds__(256) cs_mid_kernel(const T* __restrict__ X, in
     }
   }
   __syncthreads();
-  cs_flush(acc, K, TI, i0, I, Y, ldy);
+  cs_flush(acc, K, TI, i0, I, part);
 }
 
 // ---------------------------------------------------------------- a > 1, fp32: TMA pipeline
@@ -183,8 +198,7 @@ struct CsTmaParams {
   int64_t tiles_per_cta;  // tau range per CTA (blockIdx.y)
   int64_t ntiles;         // nat * b
   int K, stages;
-  double* Y;
-  int64_t ldy;
+  float* part;      // [gridDim.y][K][I] partial sums
 };
 
 template <int NB, int W>
@@ -279,7 +293,7 @@ __global__ void __launch_bounds__(32 * W + 32, 1) cs_mid_tma_kernel(const __grid
     }
   }
   __syncthreads();
-  cs_flush(acc, p.K, TI, i0, p.I, p.Y, p.ldy);
+  cs_flush(acc, p.K, TI, i0, p.I, p.part);
 }
 
 // ---------------------------------------------------------------- a == 1, fp32: TMA pipeline
@@ -295,8 +309,7 @@ struct CsRowsParams {
   int64_t I, J;
   int64_t tiles_per_cta, ntiles;   // tiles of 32 columns
   int K, stages;
-  double* Y;
-  int64_t ldy;
+  float* part;      // [gridDim.y][K][I] partial sums
 };
 
 __global__ void __launch_bounds__(96, 1) cs_rows_tma_kernel(const __grid_constant__ CUtensorMap tx,
@@ -382,7 +395,7 @@ __global__ void __launch_bounds__(96, 1) cs_rows_tma_kernel(const __grid_constan
     }
   }
   __syncthreads();
-  cs_flush(acc, p.K, TI, i0, p.I, p.Y, p.ldy);
+  cs_flush(acc, p.K, TI, i0, p.I, p.part);
 }
 
 // column range per CTA (multiple of blk >= 32): <= 512 K columns (fp32 accumulator length bound)
@@ -394,6 +407,14 @@ int64_t pick_jchunk(int64_t J, int64_t gx, int K, int64_t blk, int sms) {
   if (cdiv(J, jc) > 65535) jc = cdiv(J, 65535);
   jc = cdiv(jc, blk) * blk;
   return jc < blk ? blk : jc;
+}
+
+template <typename A>
+void reduce_parts(const Ctx& ctx, const A* part, int64_t ny, int K, int64_t I, double* Y, int64_t ldy) {
+  const int64_t KI = int64_t(K) * I;
+  launch(ctx, "count_reduce", [&] {
+    cs_reduce_kernel<A><<<unsigned(cdiv(KI, 256)), 256, 0, ctx.stream>>>(part, ny, KI, I, Y, ldy);
+  });
 }
 
 void prep(const Ctx& ctx, const int32_t* code, int64_t J, int64_t Jpad, int K, int row_bytes, uint32_t* off,
@@ -429,7 +450,7 @@ bool count_sketch_tma(const Ctx& ctx, Arena& ws, const float* X, Box box, const 
   const uint32_t bx[3] = {32, uint32_t(TIt), 1};
   if (!tc::encode_f32_map(&tx, X, 3, d, st, bx, true)) return false;
   CsTmaParams p;
-  p.a = box.a; p.I = box.I; p.K = K; p.stages = stages; p.Y = Y; p.ldy = ldy;
+  p.a = box.a; p.I = box.I; p.K = K; p.stages = stages; 
   p.nat = cdiv(box.a, int64_t(32) * NB);
   p.ntiles = p.nat * box.b;
   const int64_t gx = cdiv(box.I, TIt);
@@ -445,6 +466,7 @@ bool count_sketch_tma(const Ctx& ctx, Arena& ws, const float* X, Box box, const 
   prep(ctx, code, J, Jp4, K, TIt * 4, off, sgn);
   const size_t sm = tneed(stages);
   const dim3 grid(unsigned(gx), unsigned(cdiv(p.ntiles, tpc)));
+  p.part = ws.alloc_n<float>(int64_t(grid.y) * K * box.I);
   auto go = [&](auto kern, int threads) {
     RT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
     kern<<<grid, threads, sm, ctx.stream>>>(tx, off, sgn, p);
@@ -458,6 +480,7 @@ bool count_sketch_tma(const Ctx& ctx, Arena& ws, const float* X, Box box, const 
     else if (TIt == 128 && NB == 4) go(cs_mid_tma_kernel<4, 4>, 160);
     else ok = false;
   });
+  if (ok) reduce_parts(ctx, p.part, grid.y, K, box.I, Y, ldy);
   ws.rewind(mk);
   if (!ok) throw Error(kEINVAL, "RT_CS_TILE: unsupported tile");
   return true;
@@ -481,7 +504,7 @@ bool count_sketch_rows_tma(const Ctx& ctx, Arena& ws, const float* X, Box box, c
   const uint32_t bx[2] = {uint32_t(TI), 32};
   if (!tc::encode_f32_map(&tx, X, 2, d, st, bx, false)) return false;
   CsRowsParams p;
-  p.I = I; p.J = J; p.K = K; p.stages = stages; p.Y = Y; p.ldy = ldy;
+  p.I = I; p.J = J; p.K = K; p.stages = stages; 
   p.ntiles = cdiv(J, int64_t(32));
   const int64_t gx = cdiv(I, int64_t(TI));
   int64_t tpc = std::max<int64_t>(1, (int64_t(512) * K) / 32);          // <= 512 K columns per CTA
@@ -496,10 +519,12 @@ bool count_sketch_rows_tma(const Ctx& ctx, Arena& ws, const float* X, Box box, c
   prep(ctx, code, J, Jp4, K, TI * 4, off, sgn);
   const size_t sm = tneed(stages);
   const dim3 grid(unsigned(gx), unsigned(cdiv(p.ntiles, tpc)));
+  p.part = ws.alloc_n<float>(int64_t(grid.y) * K * I);
   launch(ctx, "count_sketch", [&] {
     RT_CUDA(cudaFuncSetAttribute(cs_rows_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
     cs_rows_tma_kernel<<<grid, 96, sm, ctx.stream>>>(tx, off, sgn, p);
   });
+  reduce_parts(ctx, p.part, grid.y, K, I, Y, ldy);
   ws.rewind(mk);
   return true;
 }
@@ -542,17 +567,19 @@ void count_sketch(const Ctx& ctx, Arena& ws, const T* X, Box box, const int32_t*
   prep(ctx, code, J, Jpad, K, int(TI * sizeof(A)), off, sgn);
   const int64_t jc = pick_jchunk(J, gx, K, blk, sms);
   const dim3 grid(unsigned(gx), unsigned(cdiv(Jpad, jc)));
+  A* part = ws.alloc_n<A>(int64_t(grid.y) * K * I);
   if (!mid) {
     launch(ctx, "count_sketch", [&] {
       RT_CUDA(cudaFuncSetAttribute(cs_rows_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-      cs_rows_kernel<T><<<grid, TI, sm, ctx.stream>>>(X, I, J, Jpad, off, sgn, K, jc, Y, ldy);
+      cs_rows_kernel<T><<<grid, TI, sm, ctx.stream>>>(X, I, J, Jpad, off, sgn, K, jc, part);
     });
   } else {
     launch(ctx, "count_sketch", [&] {
       RT_CUDA(cudaFuncSetAttribute(cs_mid_kernel<T, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-      cs_mid_kernel<T, U><<<grid, TI, sm, ctx.stream>>>(X, box.a, I, J, Jpad, off, sgn, K, jc, Y, ldy);
+      cs_mid_kernel<T, U><<<grid, TI, sm, ctx.stream>>>(X, box.a, I, J, Jpad, off, sgn, K, jc, part);
     });
   }
+  reduce_parts(ctx, part, grid.y, K, I, Y, ldy);
   ws.rewind(mk);
 }
 

@@ -47,8 +47,13 @@ class Engine {
   template <typename T>
   void sketch(const TView& X, const T* data, int n, int kind, const void* const* omega,
               const int64_t* omega_cols, const int64_t* omega_ld, int q, double* Yt, bool first_only = false);
-  // one power step of reading R31 (fp32 data, tensor cores): Yt = X_(n) s_z X_(n)^T Qy; false if n/a
-  bool power_step_r31(const TView& X, const float* data, int n, int K, const double* Qy, double* Yt);
+  // one power step of reading R31 (fp32 data, tensor cores): Yt = X_(n) s_z X_(n)^T Qy; false if n/a.
+  // unmixed: Qy already went through unmix_q (the overlapped driver does it on the side stream)
+  bool power_step_r31(const TView& X, const float* data, int n, int K, const double* Qy, double* Yt,
+                      bool unmixed = false);
+  // reading R31': Qp = Qy R_S^-1 D (ws allocation, In x K, ld In) with R_S the Cholesky factor of the
+  // Gram of a row sample of Z = X_(n)^T Qy, so that Z' = X_(n)^T Qp has near-orthogonal columns
+  double* unmix_q(const TView& X, const float* data, int n, int K, const double* Qy, double* out = nullptr);
   // HOSVD (Gaussian Omega) with the thin QRs on the handle's side stream; false (nothing launched) if n/a
   bool hosvd_overlap(const TView& X, const float* data, const int64_t* R, int q, const void* const* omega,
                      const int64_t* omega_cols, const int64_t* omega_ld, double* const* Q_out, double* G_out,

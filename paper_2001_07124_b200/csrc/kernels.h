@@ -129,6 +129,16 @@ void gemm_tall(const Ctx& ctx, const TA* A, int64_t m, int k, int64_t lda, const
                int64_t ldb, TC* C, int64_t ldc, const int* zero_flag = nullptr, int64_t row0 = 0,
                bool rowmajor = false, const int64_t* row0_dev = nullptr);
 
+// Power-step unmixing (reading R31', pipeline.cu unmix_q): Z_S = X_(n)[:, S]^T Q over 32 nblk sampled
+// columns (blocks of 32 consecutive j spread evenly over J), fp64, col-major (ldz >= 32 nblk);
+// Qp = Q Rinv diag(d) with d_c the power of two that puts ||Rinv[:, c]|| d_c in [1/2, 1) (Rinv upper
+// triangular k x k; the identity when *zero).
+template <typename T>
+void zsample(const Ctx& ctx, const T* X, Box box, int nblk, const double* Q, int64_t ldq, int K, double* Zs,
+             int64_t ldz);
+void unmix_cols(const Ctx& ctx, const double* Q, int64_t m, int K, int64_t ldq, const double* Ri, const int* zero,
+                double* Qp, int64_t ldp);
+
 // Small dense fp64 GEMM C = op(A) op(B) (col-major), for k x k triangular products.
 void gemm_small(const Ctx& ctx, bool ta, bool tb, int m, int n, int k, const double* A, int lda,
                 const double* B, int ldb, double* C, int ldc);

@@ -696,6 +696,75 @@ __global__ void nonfinite_kernel(const double* __restrict__ x, int64_t n, int* s
   if (e < n && !isfinite(x[e])) latch(status, kStatusNonFinite);
 }
 
+
+// ------------------------------------------------------------ power-step unmixing (reading R31')
+// Z_S(s, c) = sum_i X_(n)(i, j_s) Q(i, c) for 32 nblk sampled columns: block b takes the 32
+// consecutive j from j0 = 32 floor(b ceil(J/32) / nblk) (rows past J are zero).  Lane = j (consecutive
+// alpha: coalesced for a >= 32), warp = c mod 8; fp64 products and sums.
+template <typename T>
+__global__ void __launch_bounds__(256) zsample_kernel(const T* __restrict__ X, Box box, int nblk,
+                                                      const double* __restrict__ Q, int64_t ldq, int K,
+                                                      double* __restrict__ Zs, int64_t ldz) {
+  constexpr int CPT = 16;                                   // K <= 128 columns, c = warp + 8 t
+  const int64_t J = box.a * box.b, nj32 = (J + 31) / 32;
+  const int64_t j0 = ((int64_t(blockIdx.x) * nj32) / nblk) * 32;
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int64_t j = j0 + lane;
+  const bool live = j < J;
+  const int64_t al = live ? j % box.a : 0, be = live ? j / box.a : 0;
+  const T* xp = X + al + box.a * box.I * be;
+  double acc[CPT];
+#pragma unroll
+  for (int t = 0; t < CPT; ++t) acc[t] = 0.0;
+  for (int64_t i = 0; i < box.I; ++i) {
+    const double x = live ? double(xp[box.a * i]) : 0.0;
+#pragma unroll
+    for (int t = 0; t < CPT; ++t) {
+      const int c = wp + 8 * t;
+      if (c < K) acc[t] = fma(x, __ldg(&Q[i + ldq * c]), acc[t]);
+    }
+  }
+  const int64_t row = int64_t(blockIdx.x) * 32 + lane;
+#pragma unroll
+  for (int t = 0; t < CPT; ++t) {
+    const int c = wp + 8 * t;
+    if (c < K) Zs[row + ldz * c] = acc[t];
+  }
+}
+
+// Qp[:, c] = d_c Q Rinv[:, c] (Rinv upper triangular; the identity when *zero), d_c = 2^-e with
+// ||Rinv[:, c]|| in [2^(e-1), 2^e): ||Qp[:, c]|| in [1/2, 1) for an orthonormal Q, from the
+// replicated Rinv alone (the same scale on every rank of a row-distributed Q).  One CTA per column.
+__global__ void __launch_bounds__(256) unmix_cols_kernel(const double* __restrict__ Q, int64_t m, int K,
+                                                         int64_t ldq, const double* __restrict__ Ri,
+                                                         const int* zero, double* __restrict__ Qp, int64_t ldp) {
+  __shared__ double rc[128];
+  __shared__ double s_d;
+  const int c = blockIdx.x;
+  const bool z = zero && *zero;
+  if (threadIdx.x < 32) {
+    double ss = 0.0;
+    for (int l = threadIdx.x; l <= c; l += 32) {
+      const double v = z ? (l == c ? 1.0 : 0.0) : Ri[l + int64_t(K) * c];
+      ss = fma(v, v, ss);
+    }
+    for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (threadIdx.x == 0) {
+      int e = 0;
+      frexp(sqrt(ss), &e);
+      s_d = (ss > 0.0 && ss <= DBL_MAX) ? ldexp(1.0, -e) : 1.0;
+    }
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l <= c; l += blockDim.x) rc[l] = (z ? (l == c ? 1.0 : 0.0) : Ri[l + int64_t(K) * c]) * s_d;
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+    double v = 0.0;
+    for (int l = 0; l <= c; ++l) v = fma(Q[i + ldq * l], rc[l], v);
+    Qp[i + ldp * c] = v;
+  }
+}
+
 }  // namespace
 
 // ======================================================================= host
@@ -911,6 +980,21 @@ void set_status_if_nonfinite(const Ctx& ctx, const double* x, int64_t n) {
   launch(ctx, "nonfinite_check", [&] {
     nonfinite_kernel<<<unsigned(cdiv(n, 256)), 256, 0, ctx.stream>>>(x, n, ctx.d_status);
   });
+}
+
+template <typename T>
+void zsample(const Ctx& ctx, const T* X, Box box, int nblk, const double* Q, int64_t ldq, int K, double* Zs,
+             int64_t ldz) {
+  RT_REQUIRE(K >= 1 && K <= 128 && nblk >= 1, kEUNSUPPORTED, "zsample: K outside [1, 128]");
+  launch(ctx, "zsample", [&] { zsample_kernel<T><<<nblk, 256, 0, ctx.stream>>>(X, box, nblk, Q, ldq, K, Zs, ldz); });
+}
+template void zsample<float>(const Ctx&, const float*, Box, int, const double*, int64_t, int, double*, int64_t);
+template void zsample<double>(const Ctx&, const double*, Box, int, const double*, int64_t, int, double*, int64_t);
+
+void unmix_cols(const Ctx& ctx, const double* Q, int64_t m, int K, int64_t ldq, const double* Ri, const int* zero,
+                double* Qp, int64_t ldp) {
+  RT_REQUIRE(K >= 1 && K <= 128, kEUNSUPPORTED, "unmix_cols: K outside [1, 128]");
+  launch(ctx, "unmix_cols", [&] { unmix_cols_kernel<<<K, 256, 0, ctx.stream>>>(Q, m, K, ldq, Ri, zero, Qp, ldp); });
 }
 
 }  // namespace rt

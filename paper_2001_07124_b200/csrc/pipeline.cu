@@ -381,8 +381,14 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
   for (int it = 0; it < q; ++it) {
     qr_y(Yt, In, X.Ig(n), K, In, Qy, In, nullptr, last && dist(), last ? row0_last : 0);
     const auto mq = ws.mark();
+    bool r31 = false;
+    if constexpr (std::is_same<T, float>::value) r31 = zsplit == 2 && !ctx.power_qrz && !(last && dist());
+    const double* Qsrc = Qy;
+    if constexpr (std::is_same<T, float>::value) {
+      if (r31) Qsrc = unmix_q(X, data, n, K, Qy);                                   // R31'
+    }
     int64_t ldqt;
-    const T* QyT = working_copy<T>(ctx, ws, Qy, In, K, In, ldqt);
+    const T* QyT = working_copy<T>(ctx, ws, Qsrc, In, K, In, ldqt);
     // Reading R31 (fp32 data, fp16-split power products, Z rows local): Z is not orthonormalized.
     // span(X_(n) Z R^-1) = span(X_(n) Z) for any invertible R, and Z = X_(n)^T Q_y ~ V_K Sigma_K has
     // near-orthogonal columns, so the product's column errors are those of an orthonormalized Z; a
@@ -390,8 +396,6 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
     // max|X|), and the Z pass writes s_z Z straight into the fp16 [hi | lo] rows of the product's B
     // operand: no Gram / Cholesky / apply passes over Z.  Its tf32 twin (gated on X's fp16 scale
     // being 0) writes the fp32 s_z Z that the product's tf32 twin reads.
-    bool r31 = false;
-    if constexpr (std::is_same<T, float>::value) r31 = zsplit == 2 && !ctx.power_qrz && !(last && dist());
     // Z(j, c) = sum_i X_(n)(i, j) Q(i, c), written row-major J x K (j = alpha + a beta):
     // so_a = ldz, so_c = 1, so_b = a ldz
     if constexpr (std::is_same<T, float>::value) {
@@ -444,10 +448,45 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
   if (own_slot) { xs_slot = nullptr; xs_key = nullptr; }
 }
 
+// Reading R31' (the unmixing of Q_y before an R31 power step).  Z = X_(n)^T Q_y is not orthonormalized
+// in R31, and its columns are mixtures of the strong and weak singular directions (Q_y spans the sketch
+// in no particular basis); the product X_(n) Z then carries rounding errors of the size of the strong
+// directions in every column, which swamp the weak ones (the order-2 test with sigma_1 / sigma_K ~ 400
+// lost a factor 20 against the QR of Z).  Orthogonalizing the columns of Z before the product removes
+// that, and it can be done on Q_y: with R_S the Cholesky factor of the Gram of a row sample Z_S =
+// X_(n)[:, S]^T Q_y (32 blocks of 32 consecutive columns spread over J, the whole Z when J <= 1024),
+// Z' = X_(n)^T (Q_y R_S^-1) has near-orthogonal columns (a row sample of a tall matrix gives its Gram
+// to a few per cent).  span(X Z') = span(X Z): the result is the oracle's power step; no pass over
+// Z.  Columns are scaled by powers of two so that ||Qp[:, c]|| < 1 (the R31 fp16 bound on s_z Z holds
+// unchanged).  Collectives: the slab mode's Z_S is a partial sum over the slabs (allreduce), the
+// other modes' samples are local rows (allreduce of the Gram).
+double* Engine::unmix_q(const TView& X, const float* data, int n, int K, const double* Qy, double* out) {
+  const Box bx = X.box(n);
+  const bool last = n == X.N - 1;
+  const int64_t In = bx.I;
+  double* Qp = out ? out : ws.alloc_n<double>(In * K);
+  const auto mk = ws.mark();
+  const int nblk = int(std::max<int64_t>(1, std::min<int64_t>(32, cdiv(bx.J(), int64_t(32)))));
+  const int64_t S = int64_t(nblk) * 32;
+  double* Zs = ws.alloc_n<double>(S * K);
+  double* G = ws.alloc_n<double>(int64_t(K) * K);
+  double* Ri = ws.alloc_n<double>(int64_t(K) * K);
+  int* zero = ws.alloc_n<int>(1);
+  zsample<float>(ctx, data, bx, nblk, Qy, In, K, Zs, S);
+  allreduce(comm, last && dist(), Zs, S * K, ctx.stream);
+  gram<double>(ctx, ws, Zs, S, K, S, G);
+  allreduce(comm, !last && dist(), G, int64_t(K) * K, ctx.stream);
+  chol_inv(ctx, G, K, 1e-10, nullptr, Ri, zero);
+  unmix_cols(ctx, Qy, In, K, In, Ri, zero, Qp, In);
+  ws.rewind(mk);
+  return Qp;
+}
+
 // One power step of reading R31 for mode n: Yt = X_(n) (s_z X_(n)^T Q_y), Q_y fp64 In x K orthonormal
 // (the same launches as the R31 branch of sketch, for the driver that overlaps the QRs).  False
 // (nothing launched) when the fp16-split form does not apply.
-bool Engine::power_step_r31(const TView& X, const float* data, int n, int K, const double* Qy, double* Yt) {
+bool Engine::power_step_r31(const TView& X, const float* data, int n, int K, const double* Qy, double* Yt,
+                            bool unmixed) {
   const int N = X.N;
   const Box bx = X.box(n);
   const bool last = (n == N - 1);
@@ -461,7 +500,8 @@ bool Engine::power_step_r31(const TView& X, const float* data, int n, int K, con
   float* Z = ws.alloc_n<float>(Jl * ldz);
   float* Z2 = reinterpret_cast<float*>(ws.alloc_n<uint16_t>(Jl * ldz2));
   int64_t ldqt;
-  const float* QyT = working_copy<float>(ctx, ws, Qy, In, K, In, ldqt);
+  const double* Qu = unmixed ? Qy : unmix_q(X, data, n, K, Qy);                    // R31'
+  const float* QyT = working_copy<float>(ctx, ws, Qu, In, K, In, ldqt);
   const float* xsc = xs_slot;
   const float* zsc = xs_slot + 1;
   const int ez = int(std::ceil(0.5 * std::log2(double(X.Ig(n)))));
@@ -518,6 +558,7 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
   Engine se(sctx, *ctx.side_ws, comm);
   double* Yt[5];
   double* Qy[5];
+  double* Qu[5];                               // Qy after the R31' unmixing (side stream, !dist())
   double* Qt[5];
   int64_t ldq[5];
   cudaEvent_t done_q[5];
@@ -526,6 +567,7 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
     RT_CUDA(cudaEventRecord(e, ctx.stream));
     RT_CUDA(cudaStreamWaitEvent(sctx.stream, e, 0));
     se.qr_y(Yt[n], X.d[n], X.Ig(n), int(K[n]), X.d[n], Q, X.d[n], nullptr, false, 0);
+    if (Q == Qy[n] && !dist()) se.unmix_q(X, data, n, int(K[n]), Qy[n], Qu[n]);   // R31' off the main stream
     done_q[n] = ctx.events->get();
     RT_CUDA(cudaEventRecord(done_q[n], sctx.stream));
   };
@@ -536,6 +578,7 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
     const int64_t In = X.d[n];
     Yt[n] = ws.alloc_n<double>(In * K[n]);
     Qy[n] = ws.alloc_n<double>(In * K[n]);
+    Qu[n] = ws.alloc_n<double>(In * K[n]);
     Qt[n] = ws.alloc_n<double>(In * K[n]);
     ldq[n] = In;
     done_q[n] = nullptr;
@@ -559,7 +602,8 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
     const Box bx = X.box(ns);
     const auto mz = ws.mark();
     int64_t ldqt;
-    const float* QyT = working_copy<float>(ctx, ws, Qy[ns], X.d[ns], K[ns], X.d[ns], ldqt);
+    const double* Qu = unmix_q(X, data, ns, int(K[ns]), Qy[ns]);                    // R31'
+    const float* QyT = working_copy<float>(ctx, ws, Qu, X.d[ns], K[ns], X.d[ns], ldqt);
     const int ez = int(std::ceil(0.5 * std::log2(double(X.Ig(ns)))));
     LabelScope ls(ctx, "ttm_t_tc_pow");
     RT_REQUIRE(ttm_t_tc(ctx, ws, data, bx, QyT, ldqt, int(K[ns]), Zs, ldzs, 1, bx.a * ldzs, 0, false, xs_slot, nullptr,
@@ -622,7 +666,7 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
     if (dist() && n == N - 1) return;
     for (; it_done[n] < q; ++it_done[n]) {
       wait_q(n);
-      RT_REQUIRE(power_step_r31(X, data, n, int(K[n]), Qy[n], Yt[n]), kEUNSUPPORTED, "power step not launched");
+      RT_REQUIRE(power_step_r31(X, data, n, int(K[n]), dist() ? Qy[n] : Qu[n], Yt[n], !dist()), kEUNSUPPORTED, "power step not launched");
       fork_qr(n, it_done[n] == q - 1 ? Qt[n] : Qy[n]);
     }
   };
@@ -658,7 +702,7 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
       for (int n = 0; n < N; ++n) {
         if (dist() && n == N - 1) continue;
         wait_q(n);
-        RT_REQUIRE(power_step_r31(X, data, n, int(K[n]), Qy[n], Yt[n]), kEUNSUPPORTED, "power step not launched");
+        RT_REQUIRE(power_step_r31(X, data, n, int(K[n]), dist() ? Qy[n] : Qu[n], Yt[n], !dist()), kEUNSUPPORTED, "power step not launched");
         fork_qr(n, it == q - 1 ? Qt[n] : Qy[n]);
       }
   }

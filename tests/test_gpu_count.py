@@ -92,6 +92,22 @@ def test_count_sketch_exact_integers(P, h):
     h.sync()
 
 
+@pytest.mark.parametrize("dims", [(2048, 96, 80), (96, 2048, 80), (64, 48, 4000)])
+def test_count_sketch_bitwise_reproducible(P, h, dims):
+    """Gaussian fp32 data (inexact partial sums): two calls give bit-identical sketches on every
+    mode (per-CTA partial slices added in a fixed order, no floating-point atomics),
+    across several CTAs per row block (each shape splits the columns over > 1 CTA)."""
+    rng = np.random.default_rng(44)
+    x = np.asfortranarray(rng.standard_normal(dims).astype(np.float32))
+    X = _dev(x)
+    for n in range(3):
+        J = x.size // dims[n]
+        codes = _c(_codes(rng, J, 24))
+        ys = [P.rtucker_sketch(h, X, n, (codes, 24), kind="count").cpu().numpy() for _ in range(3)]
+        assert np.array_equal(ys[0], ys[1]) and np.array_equal(ys[0], ys[2]), n
+    h.sync()
+
+
 @pytest.mark.parametrize("q", [0, 1])
 def test_count_hosvd_parity(P, h, q):
     import dataclasses

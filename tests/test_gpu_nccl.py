@@ -1,7 +1,7 @@
 """The NCCL backend on a real GPU: a 1-rank NCCL communicator (ncclGetUniqueId / ncclCommInitRank
 through the run-time loaded libnccl) with RT_OPT_FORCE_COLLECTIVES, so that every slab exchange of
 the drivers (C1-C5 allreduces, the sign-candidate allgather, TSQR Grams) goes through ncclAllReduce /
-ncclAllGather.  One rank: the results must equal the communicator-free run (and the oracle).
+ncclAllGather.  One rank: the results must equal the communicator-free run to rounding (and the oracle at 1e-5).
 Several ranks cannot share one GPU under NCCL; the multi-rank exchanges are covered by the
 loopback-communicator tests and the gloo replay (tests/test_dist_gloo.py)."""
 import numpy as np
@@ -55,7 +55,11 @@ def test_nccl_one_rank_hosvd_matches_plain_and_oracle(P, q):
     hn.sync()
     for n in range(3):
         qa, qb = res["Q"][n].cpu().numpy(), plain["Q"][n].cpu().numpy()
-        assert M.subspace(qa, qb) <= 1e-7          # metric floor ~1e-8 (fp64 cancellation)
+        # q = 0: the same launches (metric floor ~1e-8, fp64 cancellation).  q = 1: the slab mode of a
+        # distributed call takes the C3 form (fp32 partial Z, allreduce, then the fp16
+        # [hi | lo] split) where the plain call splits the accumulator directly, and its QR is the
+        # row-distributed one: two roundings of the same 22-bit product, ~1e-7 apart
+        assert M.subspace(qa, qb) <= (1e-7 if q == 0 else 1e-6), (n, M.subspace(qa, qb))
         assert M.subspace(qa, ref["Q"][n]) <= 1e-5
     assert abs(float(res["err"][0]) - ref["E"]) / ref["E"] <= 1e-5
     hn.close()

@@ -326,3 +326,36 @@ def test_fused_sketch1_core0(P, dims, rank, p, q):
         h.close()
     for n in range(N):
         assert M.subspace(mat(res[291]["Q"][n]), mat(res[290]["Q"][n])) <= 2e-6
+
+
+@pytest.mark.parametrize("dims,rank", [((300, 200), 12), ((320, 256, 96), 12), ((2048, 96, 80), 10)])
+def test_r31_unmix_steep_spectrum(P, dims, rank):
+    """Reading R31': an R31 power step on Q_y unmixed by a sampled R_S (the default) against the QR of
+    Z (option 240, the oracle's form) on spectra that fall steeply inside the sketch (sigma_1 / sigma_K
+    ~ 400 for the order-2 case, which R31 without the unmixing missed at 1.07e-5): both within 2e-6
+    of the oracle and of each other, with the fp16 power products seen running (device counters)."""
+    from paper_2001_07124_b200 import _lib as L
+    N = len(dims)
+    cfg = dataclasses.replace(synth.CONFIGS["cfg2"].scaled(dims, (rank,) * N, (rank,) * N), q=1)
+    x = synth.make_tensor(cfg)
+    oms = [synth.gaussian_omega(cfg, n) for n in range(N)]
+    ref = oracle.hosvd(x, cfg.ranks, oms, q=1)
+    out = {}
+    for opt in (241, 240):
+        h = _handle(P, 0)
+        h.set_option(L.RT_OPT_TC_ABLATE, opt)
+        h.set_option(L.RT_OPT_PROFILE, 1)
+        r = P.rtucker_hosvd(h, dev(x), cfg.ranks, cfg.p, 1, [om_dev(o) for o in oms])
+        h.sync()
+        prof = h.profile_read()[0]
+        names = {n for n, _, _ in prof}
+        runs = {n: c for n, c, _ in prof if n in ("h16_ran", "tf32_twin_ran")}
+        assert ("zsample" in names) == (opt == 241), names
+        assert runs.get("h16_ran", 0) >= N and runs.get("tf32_twin_ran", 0) == 0, runs
+        out[opt] = [mat(q) for q in r["Q"]]
+        for n in range(N):
+            assert M.subspace(out[opt][n], ref["Q"][n]) <= 2e-6, (opt, n, M.subspace(out[opt][n], ref["Q"][n]))
+        assert abs(mat(r["err"])[0] - ref["E"]) / ref["E"] <= 1e-5
+        h.close()
+    for n in range(N):
+        assert M.subspace(out[241][n], out[240][n]) <= 2e-6
