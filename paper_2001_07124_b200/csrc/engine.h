@@ -79,6 +79,10 @@ class Engine {
   template <typename T>
   void rel_error(const TView& X, const T* data, const double* G, const int64_t* R, const double* const* Q,
                  double* E, double* Eg, bool ortho_q = false);
+  // the residual sums of rel_error without the finalization (sums[2], gg = ||G||^2, rs[2] the scales)
+  template <typename T>
+  void resid_sums(const TView& X, const T* data, const double* G, const int64_t* R, const double* const* Q,
+                  double* sums, double* gg, float* rs, bool ortho_q);
   // drivers
   template <typename T>
   void hosvd(const TView& X, const int64_t* R, int q, int kind, const void* const* omega,

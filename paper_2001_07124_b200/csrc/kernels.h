@@ -130,12 +130,12 @@ void gemm_tall(const Ctx& ctx, const TA* A, int64_t m, int k, int64_t lda, const
                bool rowmajor = false, const int64_t* row0_dev = nullptr);
 
 // Power-step unmixing (reading R31', pipeline.cu unmix_q): Z_S = X_(n)[:, S]^T Q over 32 nblk sampled
-// columns (blocks of 32 consecutive j spread evenly over J), fp64, col-major (ldz >= 32 nblk);
+// columns (blocks of 32 consecutive j spread evenly over J), fp64, col-major (ld 32 nblk);
 // Qp = Q Rinv diag(d) with d_c the power of two that puts ||Rinv[:, c]|| d_c in [1/2, 1) (Rinv upper
 // triangular k x k; the identity when *zero).
 template <typename T>
-void zsample(const Ctx& ctx, const T* X, Box box, int nblk, const double* Q, int64_t ldq, int K, double* Zs,
-             int64_t ldz);
+void zsample(const Ctx& ctx, Arena& ws, const T* X, Box box, int nblk, const double* Q, int64_t ldq, int K,
+             double* Zs);
 void unmix_cols(const Ctx& ctx, const double* Q, int64_t m, int K, int64_t ldq, const double* Ri, const int* zero,
                 double* Qp, int64_t ldp);
 
@@ -174,8 +174,14 @@ template <typename T>
 void residual(const Ctx& ctx, Arena& ws, const T* X, int64_t J, int64_t In, const T* P, int R,
               const T* Q, int64_t ldq, double* out2, const float* rscale = nullptr);
 
+// the SIMT residual's per-CTA (res, xx) pairs into part[2 nblk] (no reduction), run only if *gate == 0
+// (nullable gate): the twin of the fp16-split residual for R > 64
+void residual_part(const Ctx& ctx, const float* X, int64_t J, int64_t In, const float* P, int R, const float* Q,
+                   int64_t ldq, double* part, int nblk, const float* rscale, const float* gate);
+
 // tcgen05 residual (ttm_tc.cu): same sums with Xhat = P Q^T built on the tensor cores (fp32 data,
-// R <= 64, J % 4 == 0, ldp % 4 == 0).  Returns false (nothing launched) when not applicable.
+// R <= 128 (R > 64: fp16 split only), J % 4 == 0, ldp % 4 == 0).  Returns false (nothing launched)
+// when not applicable.  The persistent grid leaves ctx.sm_reserve SMs free.
 bool residual_tc(const Ctx& ctx, Arena& ws, const float* X, int64_t J, int64_t In, const float* P, int64_t ldp,
                  int R, const float* Q, int64_t ldq, double* out2, const float* rscale = nullptr,
                  const float* pscale = nullptr);
@@ -191,6 +197,9 @@ void sumsq(const Ctx& ctx, Arena& ws, const double* x, int64_t n, double* out);
 // rscale (nullable): the power-of-two scale the residual sums were taken at (resid_scale)
 void finalize_err(const Ctx& ctx, const double* sums /*res, xx*/, const double* gg, double* E, double* Eg,
                   const float* rscale = nullptr);
+// reading R35: E from the rank-K residual sums plus the truncated energy ||G~||^2 - ||G||^2 (ggK, ggR)
+void finalize_err_split(const Ctx& ctx, const double* sums, const double* ggK, const double* ggR, double* E, double* Eg,
+                        const float* rscale);
 // s[0] = 2^-e with rms = sqrt(gg / numel) in [2^(e-1), 2^e): the residual pass works on s X (exact);
 // s[1] = the fp16 scale of P for the fp16-split residual (0: the tf32 residual)
 void resid_scale(const Ctx& ctx, const double* gg, double numel, float* s);

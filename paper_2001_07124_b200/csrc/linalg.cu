@@ -457,32 +457,32 @@ __global__ void __launch_bounds__(512) jacobi_kernel(EigBatch bt, double* Vscrat
         cs[4 * pi + 2] = p; cs[4 * pi + 3] = q;
       }
       __syncthreads();
-      // rows: A <- J^T A   (one warp per pair, lanes over columns)
-      for (int pi = warp; pi < npairs; pi += nw) {
-        const double c = cs[4 * pi], s = cs[4 * pi + 1];
-        if (s == 0.0) continue;
-        const int p = int(cs[4 * pi + 2]), q = int(cs[4 * pi + 3]);
-        for (int l = lane; l < kk; l += 32) {
-          const double ap = A[p * ld + l], aq = A[q * ld + l];
-          A[p * ld + l] = c * ap - s * aq;
-          A[q * ld + l] = s * ap + c * aq;
-        }
+      // A <- J^T A J in one phase: the rotations of a round act on disjoint index pairs, so the
+      // 2x2 block (rows of pair u, columns of pair v) of the result depends only on the same block
+      // of A and on the two rotations; one thread per block, in place.  V <- V J likewise.
+      for (int e = t; e < npairs * npairs; e += nt) {
+        const int u = e / npairs, v = e - u * npairs;
+        const double cu = cs[4 * u], su = cs[4 * u + 1], cv = cs[4 * v], sv = cs[4 * v + 1];
+        if (su == 0.0 && sv == 0.0) continue;
+        const int pu = int(cs[4 * u + 2]), qu = int(cs[4 * u + 3]);
+        const int pv = int(cs[4 * v + 2]), qv = int(cs[4 * v + 3]);
+        const double app = A[pu * ld + pv], apq = A[pu * ld + qv], aqp = A[qu * ld + pv], aqq = A[qu * ld + qv];
+        const double rpp = cu * app - su * aqp, rpq = cu * apq - su * aqq;     // rows: J_u^T A
+        const double rqp = su * app + cu * aqp, rqq = su * apq + cu * aqq;
+        A[pu * ld + pv] = cv * rpp - sv * rpq;                                 // columns: (.) J_v
+        A[pu * ld + qv] = sv * rpp + cv * rpq;
+        A[qu * ld + pv] = cv * rqp - sv * rqq;
+        A[qu * ld + qv] = sv * rqp + cv * rqq;
+        if (u == v) { A[pu * ld + qv] = 0.0; A[qu * ld + pv] = 0.0; }      // the annihilated pair
       }
-      __syncthreads();
-      // columns: A <- A J, V <- V J
-      for (int pi = warp; pi < npairs; pi += nw) {
-        const double c = cs[4 * pi], s = cs[4 * pi + 1];
-        if (s == 0.0) continue;
-        const int p = int(cs[4 * pi + 2]), q = int(cs[4 * pi + 3]);
-        for (int l = lane; l < kk; l += 32) {
-          const double ap = A[l * ld + p], aq = A[l * ld + q];
-          A[l * ld + p] = c * ap - s * aq;
-          A[l * ld + q] = s * ap + c * aq;
-          const double vp = V[l * ld + p], vq = V[l * ld + q];
-          V[l * ld + p] = c * vp - s * vq;
-          V[l * ld + q] = s * vp + c * vq;
-        }
-        if (lane == 0) { A[p * ld + q] = 0.0; A[q * ld + p] = 0.0; }
+      for (int e = t; e < kk * npairs; e += nt) {
+        const int l = e / npairs, v = e - l * npairs;
+        const double c = cs[4 * v], sn = cs[4 * v + 1];
+        if (sn == 0.0) continue;
+        const int pv = int(cs[4 * v + 2]), qv = int(cs[4 * v + 3]);
+        const double vp = V[l * ld + pv], vq = V[l * ld + qv];
+        V[l * ld + pv] = c * vp - sn * vq;
+        V[l * ld + qv] = sn * vp + c * vq;
       }
       __syncthreads();
     }
@@ -570,7 +570,9 @@ template <typename T, typename Tacc = typename AccOf<T>::type>
 __global__ void __launch_bounds__(256) residual_kernel(const T* __restrict__ X, int64_t J, int64_t In,
                                                         const T* __restrict__ P, int R, const T* __restrict__ Q,
                                                         int64_t ldq, double* __restrict__ part,
-                                                        const float* __restrict__ rscale) {
+                                                        const float* __restrict__ rscale,
+                                                        const float* __restrict__ gate) {
+  if (gate && *gate != 0.f) return;                      // the fp16-split residual ran (twin of R35)
   const Tacc sc = rscale ? Tacc(*rscale) : Tacc(1);
   constexpr int BM = 128, BN = 64, BR = 16;
   __shared__ Tacc Ps[BR][BM];
@@ -666,6 +668,17 @@ __global__ void finalize_err_kernel(const double* sums, const double* gg, double
   if (Eg) *Eg = xx > 0 ? sqrt(fmax(0.0, 1.0 - (*gg * s * s) / xx)) : 0.0;
 }
 
+// Reading R35: res = sum (s x - s x^_K)^2 + s^2 (||G~||^2 - ||G||^2) (the rank-K residual plus the
+// truncated energy, orthogonal parts), E = sqrt(res / xx), E_gram from ||G||^2 as in finalize_err
+__global__ void finalize_err_split_kernel(const double* sums, const double* ggK, const double* ggR, double* E,
+                                          double* Eg, const float* rscale) {
+  const double s = rscale ? double(*rscale) : 1.0;
+  const double xx = sums[1];
+  const double res = sums[0] + fmax(0.0, *ggK - *ggR) * s * s;
+  if (E) *E = xx > 0 ? sqrt(res / xx) : 0.0;
+  if (Eg) *Eg = xx > 0 ? sqrt(fmax(0.0, 1.0 - (*ggR * s * s) / xx)) : 0.0;
+}
+
 // Power-of-two scale of the residual pass: rms(X) ~ ||G|| / sqrt(numel) (orthonormal factors) is
 // brought near 1 so the fp32 squares of the data and of the residual neither underflow (|x| <
 // 1e-19) nor overflow (|x| > 1e19).  1 when ||G|| is 0 or not finite.
@@ -699,37 +712,68 @@ __global__ void nonfinite_kernel(const double* __restrict__ x, int64_t n, int* s
 
 // ------------------------------------------------------------ power-step unmixing (reading R31')
 // Z_S(s, c) = sum_i X_(n)(i, j_s) Q(i, c) for 32 nblk sampled columns: block b takes the 32
-// consecutive j from j0 = 32 floor(b ceil(J/32) / nblk) (rows past J are zero).  Lane = j (consecutive
-// alpha: coalesced for a >= 32), warp = c mod 8; fp64 products and sums.
+// consecutive j from j0 = 32 floor(b ceil(J/32) / nblk) (rows past J are zero).  Grid (nblk, isplit):
+// a CTA stages 32 rows i x the block's 32 columns of X and the matching 32 x K rows of Q in
+// shared memory (coalesced along whichever of i / j is contiguous: a == 1 or a >= 32), then lane = j,
+// warp = c mod 8 accumulate in fp64; partials part[split][s][c], summed in split order by
+// zsample_reduce_kernel (deterministic: no atomics).
+constexpr int ZS_TI = 32;
 template <typename T>
 __global__ void __launch_bounds__(256) zsample_kernel(const T* __restrict__ X, Box box, int nblk,
                                                       const double* __restrict__ Q, int64_t ldq, int K,
-                                                      double* __restrict__ Zs, int64_t ldz) {
+                                                      double* __restrict__ part) {
   constexpr int CPT = 16;                                   // K <= 128 columns, c = warp + 8 t
+  __shared__ double xs[ZS_TI][33];
+  __shared__ double qs[128][ZS_TI + 1];
   const int64_t J = box.a * box.b, nj32 = (J + 31) / 32;
   const int64_t j0 = ((int64_t(blockIdx.x) * nj32) / nblk) * 32;
-  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  const int64_t j = j0 + lane;
-  const bool live = j < J;
-  const int64_t al = live ? j % box.a : 0, be = live ? j / box.a : 0;
-  const T* xp = X + al + box.a * box.I * be;
+  const int64_t i0 = int64_t(blockIdx.y) * ZS_TI;
+  const int ni = box.I - i0 < ZS_TI ? int(box.I - i0) : ZS_TI;
+  const int t = threadIdx.x, lane = t & 31, wp = t >> 5;
+  // X chunk: element (i, jl) at alpha + a i + a I beta, j = j0 + jl = alpha + a beta
+  for (int e = t; e < ZS_TI * 32; e += 256) {
+    int il, jl;
+    if (box.a == 1) { il = e % ZS_TI; jl = e / ZS_TI; }     // i contiguous in memory
+    else            { jl = e % 32; il = e / 32; }           // alpha contiguous
+    const int64_t j = j0 + jl;
+    double v = 0.0;
+    if (il < ni && j < J) {
+      const int64_t al = j % box.a, be = j / box.a;
+      v = double(X[al + box.a * (i0 + il) + box.a * box.I * be]);
+    }
+    xs[il][jl] = v;
+  }
+  for (int e = t; e < ZS_TI * K; e += 256) {
+    const int il = e % ZS_TI, c = e / ZS_TI;
+    qs[c][il] = il < ni ? Q[i0 + il + ldq * c] : 0.0;
+  }
+  __syncthreads();
   double acc[CPT];
 #pragma unroll
-  for (int t = 0; t < CPT; ++t) acc[t] = 0.0;
-  for (int64_t i = 0; i < box.I; ++i) {
-    const double x = live ? double(xp[box.a * i]) : 0.0;
+  for (int u = 0; u < CPT; ++u) acc[u] = 0.0;
+  for (int il = 0; il < ni; ++il) {
+    const double x = xs[il][lane];
 #pragma unroll
-    for (int t = 0; t < CPT; ++t) {
-      const int c = wp + 8 * t;
-      if (c < K) acc[t] = fma(x, __ldg(&Q[i + ldq * c]), acc[t]);
+    for (int u = 0; u < CPT; ++u) {
+      const int c = wp + 8 * u;
+      if (c < K) acc[u] = fma(x, qs[c][il], acc[u]);
     }
   }
+  const int64_t S = int64_t(nblk) * 32;
+  double* dst = part + int64_t(blockIdx.y) * S * K;
   const int64_t row = int64_t(blockIdx.x) * 32 + lane;
 #pragma unroll
-  for (int t = 0; t < CPT; ++t) {
-    const int c = wp + 8 * t;
-    if (c < K) Zs[row + ldz * c] = acc[t];
+  for (int u = 0; u < CPT; ++u) {
+    const int c = wp + 8 * u;
+    if (c < K) dst[row + S * c] = acc[u];
   }
+}
+__global__ void zsample_reduce_kernel(const double* __restrict__ part, int nsplit, int64_t n, double* __restrict__ Zs) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  double s = 0.0;
+  for (int z = 0; z < nsplit; ++z) s += part[e + n * z];
+  Zs[e] = s;
 }
 
 // Qp[:, c] = d_c Q Rinv[:, c] (Rinv upper triangular; the identity when *zero), d_c = 2^-e with
@@ -928,10 +972,17 @@ void residual(const Ctx& ctx, Arena& ws, const T* X, int64_t J, int64_t In, cons
   const int nblk = 4 * ctx.num_sms;
   double* part = ws.alloc_n<double>(2 * nblk);
   launch(ctx, "residual_simt", [&] {
-    if (ctx.acc64()) residual_kernel<T, double><<<nblk, 256, 0, ctx.stream>>>(X, J, In, P, R, Q, ldq, part, rscale);
-    else residual_kernel<T><<<nblk, 256, 0, ctx.stream>>>(X, J, In, P, R, Q, ldq, part, rscale);
+    if (ctx.acc64())
+      residual_kernel<T, double><<<nblk, 256, 0, ctx.stream>>>(X, J, In, P, R, Q, ldq, part, rscale, nullptr);
+    else residual_kernel<T><<<nblk, 256, 0, ctx.stream>>>(X, J, In, P, R, Q, ldq, part, rscale, nullptr);
   });
   launch(ctx, "reduce_pairs", [&] { reduce_pairs_kernel<<<1, 256, 0, ctx.stream>>>(part, nblk, out2); });
+}
+void residual_part(const Ctx& ctx, const float* X, int64_t J, int64_t In, const float* P, int R, const float* Q,
+                   int64_t ldq, double* part, int nblk, const float* rscale, const float* gate) {
+  launch(ctx, "residual_simt", [&] {
+    residual_kernel<float><<<nblk, 256, 0, ctx.stream>>>(X, J, In, P, R, Q, ldq, part, rscale, gate);
+  });
 }
 template void residual<float>(const Ctx&, Arena&, const float*, int64_t, int64_t, const float*, int, const float*,
                               int64_t, double*, const float*);
@@ -969,6 +1020,12 @@ void dist_rows_info(const Ctx& ctx, const double* counts, int nranks, int rank, 
     dist_rows_info_kernel<<<1, 1, 0, ctx.stream>>>(counts, nranks, rank, k, shift_coef, row0);
   });
 }
+void finalize_err_split(const Ctx& ctx, const double* sums, const double* ggK, const double* ggR, double* E, double* Eg,
+                        const float* rscale) {
+  launch(ctx, "finalize_err", [&] {
+    finalize_err_split_kernel<<<1, 1, 0, ctx.stream>>>(sums, ggK, ggR, E, Eg, rscale);
+  });
+}
 void resid_scale(const Ctx& ctx, const double* gg, double numel, float* s) {
   launch(ctx, "resid_scale", [&] { resid_scale_kernel<<<1, 1, 0, ctx.stream>>>(gg, numel, s); });
 }
@@ -983,13 +1040,22 @@ void set_status_if_nonfinite(const Ctx& ctx, const double* x, int64_t n) {
 }
 
 template <typename T>
-void zsample(const Ctx& ctx, const T* X, Box box, int nblk, const double* Q, int64_t ldq, int K, double* Zs,
-             int64_t ldz) {
+void zsample(const Ctx& ctx, Arena& ws, const T* X, Box box, int nblk, const double* Q, int64_t ldq, int K,
+             double* Zs) {
   RT_REQUIRE(K >= 1 && K <= 128 && nblk >= 1, kEUNSUPPORTED, "zsample: K outside [1, 128]");
-  launch(ctx, "zsample", [&] { zsample_kernel<T><<<nblk, 256, 0, ctx.stream>>>(X, box, nblk, Q, ldq, K, Zs, ldz); });
+  const int nsplit = int(cdiv(box.I, int64_t(ZS_TI)));
+  RT_REQUIRE(nsplit <= 65535, kEUNSUPPORTED, "zsample: I_n too large");
+  const int64_t n = int64_t(nblk) * 32 * K;
+  const auto mk = ws.mark();
+  double* part = ws.alloc_n<double>(n * nsplit);
+  launch(ctx, "zsample", [&] {
+    zsample_kernel<T><<<dim3(unsigned(nblk), unsigned(nsplit)), 256, 0, ctx.stream>>>(X, box, nblk, Q, ldq, K, part);
+    zsample_reduce_kernel<<<unsigned(cdiv(n, int64_t(256))), 256, 0, ctx.stream>>>(part, nsplit, n, Zs);
+  });
+  ws.rewind(mk);
 }
-template void zsample<float>(const Ctx&, const float*, Box, int, const double*, int64_t, int, double*, int64_t);
-template void zsample<double>(const Ctx&, const double*, Box, int, const double*, int64_t, int, double*, int64_t);
+template void zsample<float>(Ctx const&, Arena&, const float*, Box, int, const double*, int64_t, int, double*);
+template void zsample<double>(Ctx const&, Arena&, const double*, Box, int, const double*, int64_t, int, double*);
 
 void unmix_cols(const Ctx& ctx, const double* Q, int64_t m, int K, int64_t ldq, const double* Ri, const int* zero,
                 double* Qp, int64_t ldp) {

@@ -472,7 +472,7 @@ double* Engine::unmix_q(const TView& X, const float* data, int n, int K, const d
   double* G = ws.alloc_n<double>(int64_t(K) * K);
   double* Ri = ws.alloc_n<double>(int64_t(K) * K);
   int* zero = ws.alloc_n<int>(1);
-  zsample<float>(ctx, data, bx, nblk, Qy, In, K, Zs, S);
+  zsample<float>(ctx, ws, data, bx, nblk, Qy, In, K, Zs);
   allreduce(comm, last && dist(), Zs, S * K, ctx.stream);
   gram<double>(ctx, ws, Zs, S, K, S, G);
   allreduce(comm, !last && dist(), G, int64_t(K) * K, ctx.stream);
@@ -714,8 +714,34 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
   for (int n = 0; n < N; ++n) gsz *= K[n];
   double* Gt = ws.alloc_n<double>(gsz);
   core<float>(X, data, Qt, ldq, K, Gt, g1);
-  truncate(X, Gt, K, Qt, ldq, R, Q_out, G_out);
-  if (E || Eg) rel_error<float>(X, data, G_out, R, Q_out, E, Eg, true);
+  if ((E || Eg) && !dist() && !ctx.split_resid_off) {
+    // Reading R35: E^2 ||X||^2 = ||X - X^_K||^2 + ||G~||^2 - ||G||^2 with X^_K = G~ x_n Q~_n (the
+    // rank-K reconstruction): the truncation (Jacobi, lift, sign canon, core shrink) runs on the side
+    // stream while the residual pass streams X against X^_K, which does not depend on it
+    double* sums = ws.alloc_n<double>(2);
+    double* ggK = ws.alloc_n<double>(1);
+    double* ggR = ws.alloc_n<double>(1);
+    float* rs = ws.alloc_n<float>(2);
+    cudaEvent_t e = ctx.events->get();
+    RT_CUDA(cudaEventRecord(e, ctx.stream));
+    RT_CUDA(cudaStreamWaitEvent(sctx.stream, e, 0));
+    se.truncate(X, Gt, K, Qt, ldq, R, Q_out, G_out);
+    int64_t gsz = 1;
+    for (int n = 0; n < N; ++n) gsz *= R[n];
+    sumsq(sctx, se.ws, G_out, gsz, ggR);
+    cudaEvent_t done_t = ctx.events->get();
+    RT_CUDA(cudaEventRecord(done_t, sctx.stream));
+    ctx.sm_reserve = 3;                        // the truncation's Jacobi CTAs run beside the residual
+    const double* Qtc[5];
+    for (int n = 0; n < N; ++n) Qtc[n] = Qt[n];
+    resid_sums<float>(X, data, Gt, K, Qtc, sums, ggK, rs, true);
+    ctx.sm_reserve = saved_reserve;
+    RT_CUDA(cudaStreamWaitEvent(ctx.stream, done_t, 0));
+    finalize_err_split(ctx, sums, ggK, ggR, E, Eg, rs);
+  } else {
+    truncate(X, Gt, K, Qt, ldq, R, Q_out, G_out);
+    if (E || Eg) rel_error<float>(X, data, G_out, R, Q_out, E, Eg, true);
+  }
   ws.rewind(mk);
   xs_slot = nullptr;
   return true;
@@ -831,10 +857,22 @@ void Engine::truncate(const TView& X, const double* Gt, const int64_t* K, const 
 template <typename T>
 void Engine::rel_error(const TView& X, const T* data, const double* G, const int64_t* R, const double* const* Q,
                        double* E, double* Eg, bool ortho_q) {
-  const int N = X.N;
   const auto mk = ws.mark();
   double* sums = ws.alloc_n<double>(2);
   double* gg = ws.alloc_n<double>(1);
+  float* rs = ws.alloc_n<float>(2);
+  resid_sums<T>(X, data, G, R, Q, sums, gg, rs, ortho_q);
+  finalize_err(ctx, sums, gg, E, Eg, rs);
+  ws.rewind(mk);
+}
+
+// the residual pass: sums = (sum (s x - s x^)^2, sum (s x)^2) over the whole tensor (C5 included),
+// gg = ||G||^2, rs = the residual scales (resid_scale) for X^ = G x_1 Q_1 ... x_N Q_N
+template <typename T>
+void Engine::resid_sums(const TView& X, const T* data, const double* G, const int64_t* R, const double* const* Q,
+                        double* sums, double* gg, float* rs, bool ortho_q) {
+  const int N = X.N;
+  const auto mk = ws.mark();
   int64_t gsz = 1;
   for (int n = 0; n < N; ++n) gsz *= R[n];
   sumsq(ctx, ws, G, gsz, gg);
@@ -888,7 +926,6 @@ void Engine::rel_error(const TView& X, const T* data, const double* G, const int
   for (int k = 0; k < N - 1; ++k) J *= X.d[k];
   // the sums are taken of s X and s X^ (s a power of two from ||G||: rms(X) near 1), so fp32
   // squares of data at any scale stay in range; E is unchanged, E_gram rescales exactly
-  float* rs = ws.alloc_n<float>(2);
   resid_scale(ctx, gg, double(X.size()) * double(X.glob) / double(X.d[N - 1]), rs);
   bool done = false;
   if constexpr (std::is_same<T, float>::value) {
@@ -897,7 +934,6 @@ void Engine::rel_error(const TView& X, const T* data, const double* G, const int
   }
   if (!done) residual<T>(ctx, ws, data, J, Il, P, Rl, QL, Il, sums, rs);
   allreduce(comm, dist(), sums, 2, ctx.stream);                                    // C5
-  finalize_err(ctx, sums, gg, E, Eg, rs);
   ws.rewind(mk);
 }
 

@@ -2427,26 +2427,39 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constan
 // A_hi [Q_hi | Q_lo] (N = 128), narrow issuer A_lo Q_hi (N = 64), 4 K = 16 steps per i block -- half
 // the MMA instructions and half the B bytes of the 3xTF32 form per X tile.  X^ = (v + w + z) / (s 2^14).
 // Gated on s: it stands down (s == 0: ||G|| zero or not finite) for residual_tc_kernel.
+template <int RPP>
 struct RSmemH {
-  static constexpr int RP = 64;
-  static constexpr uint32_t kP = uint32_t(RP) * BM * 4;          // raw P tile [64 r][128 j]
+  static constexpr int RP = RPP;                                  // P tile rows (64, 96 or 128)
+  static constexpr int NRB = RPP / 64;                            // 64-r B boxes per piece (SW128)
+  static constexpr int HALF = (RPP % 64) ? 1 : 0;                 // + one 32-r box (SW64)
+  static constexpr uint32_t kP = uint32_t(RP) * BM * 4;          // raw P tile [RP r][128 j]
   static constexpr uint32_t kQ = uint32_t(RNB) * 128;            // one [64 i][64 r] fp16 box (8 KB)
   static constexpr uint32_t kXt = uint32_t(BM) * RNB * 4;        // X tile [64 i][128 j]
-  static constexpr int NS = 4;
-  static constexpr uint32_t per_stage = 2 * kQ + kXt;
+  static constexpr uint32_t kBst = 2 * NRB * kQ + HALF * kQ;      // [hi b0 | lo b0 | ... | hi h | lo h]
+  static constexpr uint32_t per_stage = kBst + kXt;
+  static constexpr int NS_fit = int((227u * 1024u - 256u - kP) / per_stage);
+  static constexpr int NS = NS_fit > 4 ? 4 : NS_fit;
   static constexpr uint32_t off_p = 0;
   static constexpr uint32_t off_st = kP;
   static constexpr uint32_t off_bar = off_st + NS * per_stage;
   static constexpr uint32_t bytes = off_bar + 8 * (2 * NS + 8) + 16;
+  static_assert(NS >= 2 && bytes <= 227u * 1024u, "residual smem plan");
 };
 
+// K-major SWIZZLE_64B descriptor of a [rows][32 fp16] box, advanced by j k16-steps (32 B)
+__device__ __forceinline__ uint64_t bdesc_sw64(uint32_t saddr, int j) {
+  return sdesc(saddr + 32u * uint32_t(j), 16u, 512u) | (uint64_t(4) << 61);
+}
+
+template <int RPP>
 __global__ void __launch_bounds__(NTHREADS, 1)
 residual_h16_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmp,
-                    const __grid_constant__ CUtensorMap tqh, const __grid_constant__ CUtensorMap tql, const RParams p,
-                    const float* __restrict__ pscale) {
-  using L = RSmemH;
-  constexpr int RP = L::RP, NS = L::NS;
-  if (*pscale == 0.f) return;                          // the tf32 residual runs instead (R29)
+                    const __grid_constant__ CUtensorMap tqh, const __grid_constant__ CUtensorMap tql,
+                    const __grid_constant__ CUtensorMap tqh2, const __grid_constant__ CUtensorMap tql2,
+                    const RParams p, const float* __restrict__ pscale) {
+  using L = RSmemH<RPP>;
+  constexpr int RP = L::RP, NS = L::NS, NRB = L::NRB, HALF = L::HALF;
+  if (*pscale == 0.f) return;                          // the twin runs instead (R29)
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::off_bar);
   uint64_t* st_full = bar;
@@ -2462,7 +2475,8 @@ residual_h16_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_consta
   const int64_t my_tiles = (p.ntiles > blockIdx.x) ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   constexpr uint32_t kAcc = 2 * RNB;                  // [hi.hi | hi.lo] per buffer (wide issuer)
   constexpr uint32_t kAcc1 = 2 * kAcc;                // lo.hi buffers (narrow issuer)
-  constexpr uint32_t kA = kAcc1 + 2 * RNB;            // A hi (32 columns), then A lo (32 columns)
+  constexpr uint32_t kA = kAcc1 + 2 * RNB;            // A hi (RP/2 columns), then A lo (RP/2 columns)
+  const int nks = (p.R + 15) / 16;                    // k-steps of 16 r (zero steps past R skipped)
   static_assert(kA + RP <= 512, "residual TMEM plan");
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) { mbar_init(&st_full[s], 1); mbar_init(&st_free[s], 128); }
@@ -2494,9 +2508,16 @@ residual_h16_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_consta
           if (it >= NS) mbar_wait(&st_free[rg.s], rg.ph ^ 1);
           uint8_t* st = smem + L::off_st + rg.s * L::per_stage;
           mbar_expect_tx(&st_full[rg.s], L::per_stage);
-          tma_load_2d_hint(st, &tqh, &st_full[rg.s], 0, b * RNB, pq);            // [Q_hi | Q_lo] adjacent:
-          tma_load_2d_hint(st + L::kQ, &tql, &st_full[rg.s], 0, b * RNB, pq);    // one N = 128 operand
-          tma_load_2d_hint(st + 2 * L::kQ, &tmx, &st_full[rg.s], j0, b * RNB, pol);
+#pragma unroll
+          for (int rb = 0; rb < NRB; ++rb) {                                   // [Q_hi | Q_lo] adjacent:
+            tma_load_2d_hint(st + 2 * rb * L::kQ, &tqh, &st_full[rg.s], 64 * rb, b * RNB, pq);   // one N = 128
+            tma_load_2d_hint(st + (2 * rb + 1) * L::kQ, &tql, &st_full[rg.s], 64 * rb, b * RNB, pq);   // operand
+          }
+          if (HALF) {                                                          // r 64 NRB .. + 31 (SW64)
+            tma_load_2d_hint(st + 2 * NRB * L::kQ, &tqh2, &st_full[rg.s], 64 * NRB, b * RNB, pq);
+            tma_load_2d_hint(st + 2 * NRB * L::kQ + L::kQ / 2, &tql2, &st_full[rg.s], 64 * NRB, b * RNB, pq);
+          }
+          tma_load_2d_hint(st + L::kBst, &tmx, &st_full[rg.s], j0, b * RNB, pol);
         }
       }
     }
@@ -2517,8 +2538,11 @@ residual_h16_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_consta
         const uint32_t acc = tmem + (wide ? uint32_t(ab) * kAcc : kAcc1 + uint32_t(ab) * RNB);
 #pragma unroll
         for (int kk = 0; kk < RP / 16; ++kk) {
-          const uint32_t a = tmem + kA + (wide ? 0u : 32u) + 8 * kk;
-          mma_f16_ts_w(acc, a, bdesc_sw128(st, kk), idesc, kk == 0 ? 0u : 1u);
+          if (kk >= nks) break;
+          const uint32_t a = tmem + kA + (wide ? 0u : uint32_t(RP / 2)) + 8 * kk;
+          const uint64_t bd = kk < 4 * NRB ? bdesc_sw128(st + (kk / 4) * 2 * L::kQ, kk % 4)
+                                           : bdesc_sw64(st + 2 * NRB * L::kQ, kk - 4 * NRB);
+          mma_f16_ts_w(acc, a, bd, idesc, kk == 0 ? 0u : 1u);
         }
         mma_commit_w(&acc_full[ab]);
       }
@@ -2543,13 +2567,14 @@ residual_h16_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_consta
       float v[RP];
 #pragma unroll
       for (int q = 0; q < RP; ++q) v[q] = ps[(q / KC) * (BM * KC) + (q % KC) * BM + r] * sc;
-      uint32_t hi[32], lo[32];
+      uint32_t hi[RP / 2], lo[RP / 2];
 #pragma unroll
-      for (int c = 0; c < 32; ++c) split_h16x2(v[2 * c], v[2 * c + 1], hi[c], lo[c]);
-      tmem_st16(lane_base + kA, *reinterpret_cast<const uint32_t(*)[16]>(&hi[0]));
-      tmem_st16(lane_base + kA + 16, *reinterpret_cast<const uint32_t(*)[16]>(&hi[16]));
-      tmem_st16(lane_base + kA + 32, *reinterpret_cast<const uint32_t(*)[16]>(&lo[0]));
-      tmem_st16(lane_base + kA + 48, *reinterpret_cast<const uint32_t(*)[16]>(&lo[16]));
+      for (int c = 0; c < RP / 2; ++c) split_h16x2(v[2 * c], v[2 * c + 1], hi[c], lo[c]);
+#pragma unroll
+      for (int g = 0; g < RP / 32; ++g) {
+        tmem_st16(lane_base + kA + 16 * g, *reinterpret_cast<const uint32_t(*)[16]>(&hi[16 * g]));
+        tmem_st16(lane_base + kA + RP / 2 + 16 * g, *reinterpret_cast<const uint32_t(*)[16]>(&lo[16 * g]));
+      }
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(p_free);
@@ -2559,7 +2584,7 @@ residual_h16_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_consta
         mbar_wait(&st_full[rg.s], rg.ph);
         mbar_wait(&acc_full[ab], uint32_t(g >> 1) & 1);
         tc_fence_after();
-        const float* xt = reinterpret_cast<const float*>(smem + L::off_st + rg.s * L::per_stage + 2 * L::kQ);
+        const float* xt = reinterpret_cast<const float*>(smem + L::off_st + rg.s * L::per_stage + L::kBst);
         float tr = 0.f, tx = 0.f;
 #pragma unroll
         for (int cb = 0; cb < RNB / 16; ++cb) {
@@ -2601,13 +2626,13 @@ residual_h16_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_consta
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
-// Q (In x R fp32, col-major ldq) -> fp16 [In rows][64] rows of 2^14 Q_hi and of 2^14 Q_lo (r >= R zero)
+// Q (In x R fp32, col-major ldq) -> fp16 [In rows][w = 64 NRB] rows of 2^14 Q_hi and of 2^14 Q_lo (r >= R zero)
 __global__ void qsplit_rows_h16_kernel(const float* __restrict__ Q, int64_t In, int R, int64_t ldq,
-                                       __half* __restrict__ qh, __half* __restrict__ ql) {
+                                       __half* __restrict__ qh, __half* __restrict__ ql, int w) {
   const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (e >= In * 64) return;
-  const int64_t i = e / 64;
-  const int r = int(e % 64);
+  if (e >= In * w) return;
+  const int64_t i = e / w;
+  const int r = int(e % w);
   const float v = r < R ? Q[i + ldq * r] * kQScale : 0.f;
   const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
   qh[e] = __float2half_rn(h);
@@ -2642,7 +2667,9 @@ __global__ void split_transpose_kernel(const float* __restrict__ Q, int64_t In, 
 
 bool residual_tc(const Ctx& ctx, Arena& ws, const float* X, int64_t J, int64_t In, const float* P, int64_t ldp,
                  int R, const float* Q, int64_t ldq, double* part_out2, const float* rscale, const float* pscale) {
-  if (ctx.simt() || R < 1 || R > 64) return false;
+  // R <= 64: the fp16-split kernel gated against the tf32 kernel; 64 < R <= 128 (the split residual
+  // of reading R35 runs at the sketch width K): the fp16-split kernel gated against the SIMT kernel
+  if (ctx.simt() || R < 1 || R > 128 || (R > 64 && (!pscale || !ctx.tc_h16 || ctx.resid_tf32))) return false;
   if (!aligned(X, 16) || !aligned(P, 16) || (J % 4) || (ldp % 4) || J > INT32_MAX || In > INT32_MAX) return false;
   const int rp = R <= 32 ? 32 : 64;
   CUtensorMap tx, tp, th, tl;
@@ -2656,43 +2683,65 @@ bool residual_tc(const Ctx& ctx, Arena& ws, const float* X, int64_t J, int64_t I
     const uint32_t bx[2] = {BM, KC};
     if (!make_map(&tp, P, 2, d, s, bx, false)) return false;
   }
-  // Q^T hi / lo, element (r, i) at r + rp*i (pad r >= R zero)
-  float* qh = ws.alloc_n<float>(In * rp);
-  float* ql = ws.alloc_n<float>(In * rp);
-  launch(ctx, "split_transpose", [&] {
-    split_transpose_kernel<<<unsigned(cdiv(In * rp, 256)), 256, 0, ctx.stream>>>(Q, In, R, ldq, qh, ql, rp);
-  });
-  if (!make_b_map(&th, qh, rp, int(In), rp, RNB) || !make_b_map(&tl, ql, rp, int(In), rp, RNB)) return false;
   RParams p;
   p.J = J; p.In = In; p.R = R;
   p.ntiles = cdiv(J, BM);
   p.nblk = int(cdiv(In, RNB));
-  const int grid = int(std::min<int64_t>(p.ntiles, ctx.num_sms));
+  const int grid = int(std::max<int64_t>(1, std::min<int64_t>(p.ntiles, ctx.num_sms - ctx.sm_reserve)));
   p.part = ws.alloc_n<double>(2 * grid);
   p.rscale = rscale;
   p.gate = nullptr;
-  if (pscale && ctx.tc_h16 && !ctx.resid_tf32) {
-    // fp16-split form (its tf32 twin below runs instead when X's scale is 0)
-    __half* qh = ws.alloc_n<__half>(In * 64);
-    __half* ql = ws.alloc_n<__half>(In * 64);
+  if (R <= 64) {
+    // the tf32 kernel's operands first (nothing is launched unless every map is accepted):
+    // Q^T hi / lo, element (r, i) at r + rp*i (pad r >= R zero)
+    float* qh = ws.alloc_n<float>(In * rp);
+    float* ql = ws.alloc_n<float>(In * rp);
+    if (!make_b_map(&th, qh, rp, int(In), rp, RNB) || !make_b_map(&tl, ql, rp, int(In), rp, RNB)) return false;
     launch(ctx, "split_transpose", [&] {
-      qsplit_rows_h16_kernel<<<unsigned(cdiv(In * 64, 256)), 256, 0, ctx.stream>>>(Q, In, R, ldq, qh, ql);
+      split_transpose_kernel<<<unsigned(cdiv(In * rp, 256)), 256, 0, ctx.stream>>>(Q, In, R, ldq, qh, ql, rp);
     });
-    CUtensorMap hh, hl;
-    const uint64_t d[2] = {64, uint64_t(In)}, st[1] = {128};
-    const uint32_t bx[2] = {64, uint32_t(RNB)};
-    if (make_map(&hh, qh, 2, d, st, bx, true, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_DATA_TYPE_FLOAT16) &&
-        make_map(&hl, ql, 2, d, st, bx, true, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_DATA_TYPE_FLOAT16)) {
-      static bool attr = false;
-      if (!attr) { set_smem(residual_h16_kernel, RSmemH::bytes); attr = true; }
-      launch(ctx, "residual_tc", [&] {
-        residual_h16_kernel<<<grid, NTHREADS, RSmemH::bytes, ctx.stream>>>(tx, tp, hh, hl, p, pscale);
-      });
+  }
+  if (pscale && ctx.tc_h16 && !ctx.resid_tf32) {
+    // fp16-split form (its twin below runs instead when the P scale is 0)
+    const int w = R <= 64 ? 64 : (R <= 96 ? 96 : 128);
+    __half* qh = ws.alloc_n<__half>(In * w);
+    __half* ql = ws.alloc_n<__half>(In * w);
+    launch(ctx, "split_transpose", [&] {
+      qsplit_rows_h16_kernel<<<unsigned(cdiv(In * w, 256)), 256, 0, ctx.stream>>>(Q, In, R, ldq, qh, ql, w);
+    });
+    CUtensorMap hh, hl, hh2, hl2;
+    const uint64_t d[2] = {uint64_t(w), uint64_t(In)}, st[1] = {uint64_t(w) * 2};
+    const uint32_t bx[2] = {64, uint32_t(RNB)}, bx2[2] = {32, uint32_t(RNB)};
+    bool mok = make_map(&hh, qh, 2, d, st, bx, true, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_DATA_TYPE_FLOAT16) &&
+               make_map(&hl, ql, 2, d, st, bx, true, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+    hh2 = hh;
+    hl2 = hl;
+    if (mok && w == 96)
+      mok = make_map(&hh2, qh, 2, d, st, bx2, false, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16) &&
+            make_map(&hl2, ql, 2, d, st, bx2, false, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+    if (!mok) {
+      if (R > 64) return false;
+    } else {
+      auto go = [&](auto kern, uint32_t bytes, bool& attr) {
+        if (!attr) { set_smem(kern, bytes); attr = true; }
+        launch(ctx, "residual_tc", [&] {
+          kern<<<grid, NTHREADS, bytes, ctx.stream>>>(tx, tp, hh, hl, hh2, hl2, p, pscale);
+        });
+      };
+      static bool a64 = false, a96 = false, a128 = false;
+      if (R <= 64) go(residual_h16_kernel<64>, RSmemH<64>::bytes, a64);
+      else if (R <= 96) go(residual_h16_kernel<96>, RSmemH<96>::bytes, a96);
+      else go(residual_h16_kernel<128>, RSmemH<128>::bytes, a128);
       p.gate = pscale;
     }
   }
-  if (rp == 32) launch_r<32>(ctx, tx, tp, th, tl, p, grid);
-  else launch_r<64>(ctx, tx, tp, th, tl, p, grid);
+  if (R > 64) {
+    // twin: the SIMT residual into the same per-CTA pairs, run only if the P scale is 0
+    residual_part(ctx, X, J, In, P, R, Q, ldq, p.part, grid, rscale, pscale);
+  } else {
+    if (rp == 32) launch_r<32>(ctx, tx, tp, th, tl, p, grid);
+    else launch_r<64>(ctx, tx, tp, th, tl, p, grid);
+  }
   // fixed-order final reduction of the per-CTA pairs
   reduce_pairs(ctx, p.part, grid, part_out2);
   return true;

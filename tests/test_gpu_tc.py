@@ -359,3 +359,32 @@ def test_r31_unmix_steep_spectrum(P, dims, rank):
         h.close()
     for n in range(N):
         assert M.subspace(out[241][n], out[240][n]) <= 2e-6
+
+
+@pytest.mark.parametrize("rank,p", [(60, 12), (64, 16), (80, 16), (100, 12)])
+def test_split_residual_widths(P, rank, p):
+    """Reading R35 (the default HOSVD driver): E from the rank-K residual pass (fp16-split residual
+    kernel at P-tile widths 96 / 128 for K = 72, 80, 96, 112) plus the truncated core energy, while
+    the truncation runs on the side stream; against the oracle's E (1e-5) and against the rank-R
+    residual after the truncation (option 296) to 1e-6."""
+    from paper_2001_07124_b200 import _lib as L
+    cfg = dataclasses.replace(synth.CONFIGS["cfg5"].scaled((384, 320, 256), (rank,) * 3, (rank,) * 3), p=p, q=1)
+    x = synth.make_tensor(cfg)
+    oms = [synth.round_tf32(synth.gaussian_omega(cfg, n)) for n in range(3)]
+    ref = oracle.hosvd(x, cfg.ranks, oms, q=1)
+    e = {}
+    for opt in (297, 296):
+        h = _handle(P, 0, omega_tf32=True)
+        h.set_option(L.RT_OPT_TC_ABLATE, opt)
+        h.set_option(L.RT_OPT_PROFILE, 1)
+        r = P.rtucker_hosvd(h, dev(x), cfg.ranks, cfg.p, 1, [om_dev(o) for o in oms])
+        h.sync()
+        names = {n for n, _, _ in h.profile_read()[0]}
+        assert "residual_tc" in names, names          # (K > 64: its SIMT twin is launched gated)
+        e[opt] = float(mat(r["err"])[0])
+        assert abs(e[opt] - ref["E"]) / ref["E"] <= 1e-5, (opt, e[opt], ref["E"])
+        qg = [mat(q) for q in r["Q"]]
+        for n in range(3):
+            assert M.subspace(qg[n], ref["Q"][n]) <= 1e-5
+        h.close()
+    assert abs(e[297] - e[296]) / e[296] <= 1e-6
