@@ -402,12 +402,16 @@ def main():
     # passes (|X| per pass + the test / power matrices and the core stage written)
     # over their device time, CUDA events on the launching stream (RT_OPT_PROFILE)
     prof = sorted(r["prof"], key=lambda e: -e[2])
-    xlabels = ("ttm_s_tc", "ttm_s_tc_pow", "ttm_t_tc_pow", "core_first", "sketch1_core0")
-    fused = any(nm == "sketch1_core0" for nm, _, _ in prof)
+    # fused passes (one read of X for two contractions): sketch1_core0 = [S1 + G1] (the one-fusion
+    # schedule), sketch1_z0 = [Z0 + S1] and sketch2_core0 = [G1 + S2] (the 9-pass schedule)
+    fused_labels = ("sketch1_core0", "sketch1_z0", "sketch2_core0")
+    xlabels = ("ttm_s_tc", "ttm_s_tc_pow", "ttm_t_tc_pow", "core_first") + fused_labels
+    names = {nm for nm, _, _ in prof}
+    nfused = sum(1 for f in fused_labels if f in names)
     x_ms = sum(t for nm, _, t in prof if nm in xlabels) / args.steps
     xl = wm["x_bytes_local"]
-    npass = wm["ttm_s"][2] + wm["ttm_t"][2] - (1 if fused else 0)
-    cls_bytes = wm["ttm_s"][0] + wm["ttm_t"][0] - (xl if fused else 0)
+    npass = wm["ttm_s"][2] + wm["ttm_t"][2] - nfused
+    cls_bytes = wm["ttm_s"][0] + wm["ttm_t"][0] - nfused * xl
     cls_flops = wm["ttm_s"][1] + wm["ttm_t"][1]
     roof = None
     if x_ms > 0:

@@ -269,6 +269,7 @@ rt_status rt_set_option(rt_handle* h, rt_option opt, int64_t value) {
       if (value == 292 || value == 293) { h->ctx.fused_nbb = int(value - 290); return RT_OK; }
       if (value == 294 || value == 295) { h->ctx.resid_tf32 = int(value == 294); return RT_OK; }
       if (value == 296 || value == 297) { h->ctx.split_resid_off = int(value == 296); return RT_OK; }
+      if (value == 298 || value == 299) { h->ctx.fuse2_off = int(value == 298); return RT_OK; }
       if (value >= 301 && value <= 308) { h->ctx.tc_waves = int(value - 300); return RT_OK; }
       if (value == 316 || value == 332 || value == 364) { h->ctx.fused_seg = int(value - 300); return RT_OK; }
       h->ctx.tc_ablate = int(value);

@@ -103,6 +103,7 @@ struct Ctx {
   int omega_h16_off = 0;        // Omega sketches of later modes: 1 = keep tf32 (ablation 250 / 251 toggle)
   int tc_xfirst = 0;            // wide X rows with L2::evict_first (ablation 280 / 281: first / normal)
   int fuse_off = 0;             // HOSVD: 1 = no fused mode-1 sketch + mode-0 core pass (ablation 290 / 291)
+  int fuse2_off = 0;            // HOSVD: 1 = one fused pass (S1 + G1) instead of two (Z0 + S1, G1 + S2) (298 / 299)
   int fused_nbb = 3;            // fused pass: B slots (chunk pairs) 2 or 3 (ablation 292 / 293)
   int resid_tf32 = 0;           // residual pass: 1 = the 3xTF32 kernel only (ablation 294 / 295)
   int split_resid_off = 0;      // HOSVD: 1 = truncate, then the rank-R residual (no R35 overlap; 296 / 297)

@@ -49,8 +49,11 @@ class Engine {
               const int64_t* omega_cols, const int64_t* omega_ld, int q, double* Yt, bool first_only = false);
   // one power step of reading R31 (fp32 data, tensor cores): Yt = X_(n) s_z X_(n)^T Qy; false if n/a.
   // unmixed: Qy already went through unmix_q (the overlapped driver does it on the side stream)
+  // parts: 1 = the Z pass only, 2 = the product only (Z from an earlier parts = 1 call in pb), 3 = both;
+  // pb (required unless parts == 3): the Z buffers, allocated on first use from ws and left allocated
+  struct PowerBufs { float* Z = nullptr; float* Z2 = nullptr; };
   bool power_step_r31(const TView& X, const float* data, int n, int K, const double* Qy, double* Yt,
-                      bool unmixed = false);
+                      bool unmixed = false, PowerBufs* pb = nullptr, int parts = 3);
   // reading R31': Qp = Qy R_S^-1 D (ws allocation, In x K, ld In) with R_S the Cholesky factor of the
   // Gram of a row sample of Z = X_(n)^T Qy, so that Z' = X_(n)^T Qp has near-orthogonal columns
   double* unmix_q(const TView& X, const float* data, int n, int K, const double* Qy, double* out = nullptr);

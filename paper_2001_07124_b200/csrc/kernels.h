@@ -76,8 +76,21 @@ void x_scale_from_gathered(const Ctx& ctx, const double* pairs, int nranks, int6
 // box; Om row-major J x K1 (ld), Q0 col-major I_0 x K0 (ld, orthonormal); xs: X's scale pair; Y fp64
 // I_1 x K1 (ldy); out: the core stage rows (K0 floats per row j of the mode-0 unfolding).  False
 // (nothing launched) when the shape is outside the fused kernel.
+// view_last: b1 = [I_0, I_{N-1}, I_1 ... I_{N-2}] (the last mode sketched, rows j = beta + b i of the
+// left output), else b1 = X.box(1).  pre (nullable): Omega^T in fp16 from sketch1_core0_prep (it does
+// not depend on Q0 or X's scale, so it can be launched before the caller waits for Q0).  zo (nullable):
+// the left output is the power-iteration Z of mode 0 in the R31 form instead of core rows (Q0 then
+// the unmixed Q_y of mode 0): zo->Z2 fp16 [hi | lo] rows (ldz2 = 2 tc_npad halves), zo->Z the fp32
+// s_z Z of the tf32 twin (ldz), zo->oscale / omul the R31 scale, zo->xs_x X's scale pair.
+struct F1Prep { uint16_t* WT = nullptr; int64_t ldw = 0; int* flag = nullptr; int npad = 0; };
+struct F1ZOut {
+  float* Z; int64_t ldz; uint16_t* Z2; int64_t ldz2; const float* oscale; float omul; const float* xs_x;
+};
+bool sketch1_core0_prep(const Ctx& ctx, Arena& ws, const float* Om, int64_t J, int K1, int64_t ldom, int npad,
+                        F1Prep* pre);
 bool sketch1_core0(const Ctx& ctx, Arena& ws, const float* X, Box b1, Box b0, const float* Om, int64_t ldom, int K1,
-                   const float* Q0, int64_t ldq0, int K0, const float* xs, double* Y, int64_t ldy, float* out);
+                   const float* Q0, int64_t ldq0, int K0, const float* xs, double* Y, int64_t ldy, float* out,
+                   int view_last = 0, const F1Prep* pre = nullptr, const F1ZOut* zo = nullptr);
 // Z (J x K fp32 row-major, pitch ldz) -> Z2: fp16 rows [2^14 Z_hi | 2^14 Z_lo] of 2 tc_npad(K) halves
 void split_rows_h16(const Ctx& ctx, const float* Z, int64_t J, int K, int64_t ldz, uint16_t* Z2);
 // out = xs with out[0] = 0 unless max|Q| < 2 (Q fp32 col-major m x r, ld): the fp16 split of an X pass

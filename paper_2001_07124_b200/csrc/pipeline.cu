@@ -486,7 +486,7 @@ double* Engine::unmix_q(const TView& X, const float* data, int n, int K, const d
 // (the same launches as the R31 branch of sketch, for the driver that overlaps the QRs).  False
 // (nothing launched) when the fp16-split form does not apply.
 bool Engine::power_step_r31(const TView& X, const float* data, int n, int K, const double* Qy, double* Yt,
-                            bool unmixed) {
+                            bool unmixed, PowerBufs* pb, int parts) {
   const int N = X.N;
   const Box bx = X.box(n);
   const bool last = (n == N - 1);
@@ -497,28 +497,42 @@ bool Engine::power_step_r31(const TView& X, const float* data, int n, int K, con
   const int64_t In = bx.I, Jl = bx.J(), ldz = pad4(K);
   const auto mk = ws.mark();
   const int64_t ldz2 = 2 * int64_t(tc_npad(K));
-  float* Z = ws.alloc_n<float>(Jl * ldz);
-  float* Z2 = reinterpret_cast<float*>(ws.alloc_n<uint16_t>(Jl * ldz2));
-  int64_t ldqt;
-  const double* Qu = unmixed ? Qy : unmix_q(X, data, n, K, Qy);                    // R31'
-  const float* QyT = working_copy<float>(ctx, ws, Qu, In, K, In, ldqt);
+  PowerBufs local;
+  if (!pb) {
+    RT_REQUIRE(parts == 3, kEINVAL, "power_step_r31: split parts need caller buffers");
+    pb = &local;
+  }
+  if (!pb->Z) {                                  // caller's buffers outlive this call (split parts)
+    pb->Z = ws.alloc_n<float>(Jl * ldz);
+    pb->Z2 = reinterpret_cast<float*>(ws.alloc_n<uint16_t>(Jl * ldz2));
+  }
+  const auto mk2 = ws.mark();
+  float* Z = pb->Z;
+  float* Z2 = pb->Z2;
   const float* xsc = xs_slot;
-  const float* zsc = xs_slot + 1;
-  const int ez = int(std::ceil(0.5 * std::log2(double(X.Ig(n)))));
-  const float hz = std::ldexp(1.0f, -(ez + 1));
-  {
+  if (parts & 1) {
+    int64_t ldqt;
+    const double* Qu = unmixed ? Qy : unmix_q(X, data, n, K, Qy);                  // R31'
+    const float* QyT = working_copy<float>(ctx, ws, Qu, In, K, In, ldqt);
+    const float* zsc = xs_slot + 1;
+    const int ez = int(std::ceil(0.5 * std::log2(double(X.Ig(n)))));
+    const float hz = std::ldexp(1.0f, -(ez + 1));
     LabelScope ls(ctx, "ttm_t_tc_pow");
     RT_REQUIRE(ttm_t_tc(ctx, ws, data, bx, QyT, ldqt, K, Z2, ldz2, 1, bx.a * ldz2, 2, false, xsc, nullptr, zsc, hz, true) &&
                    ttm_t_tc(ctx, ws, data, bx, QyT, ldqt, K, Z, ldz, 1, bx.a * ldz, 0, false, nullptr, xsc, zsc, hz),
                kEUNSUPPORTED, "power iteration: Z pass rejected by the tensor-core path");
+    ws.rewind(mk2);
   }
-  {
-    LabelScope ls(ctx, "ttm_s_tc_pow");
-    RT_REQUIRE(ttm_s_tc(ctx, ws, data, bx, Z2, ldz2, false, K, Yt, In, true, xsc, nullptr, Z, ldz), kEUNSUPPORTED,
-               "pre-split power product not launched");
+  if (parts & 2) {
+    {
+      LabelScope ls(ctx, "ttm_s_tc_pow");
+      RT_REQUIRE(ttm_s_tc(ctx, ws, data, bx, Z2, ldz2, false, K, Yt, In, true, xsc, nullptr, Z, ldz), kEUNSUPPORTED,
+                 "pre-split power product not launched");
+    }
+    allreduce(comm, !last && dist(), Yt, In * K, ctx.stream);                       // C1
   }
-  allreduce(comm, !last && dist(), Yt, In * K, ctx.stream);                         // C1
-  ws.rewind(mk);
+  if (pb == &local) ws.rewind(mk);
+  else ws.rewind(mk2);
   return true;
 }
 
@@ -671,11 +685,110 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
     }
   };
   float* g1 = nullptr;                         // the first core stage from the fused pass
-  if (try_fuse) {
+  PowerBufs pbs[5];
+  bool deferred[5] = {false, false, false, false, false};
+  // Two fused passes (N = 3, q = 1, one rank): the mode-0 contraction of X feeds Z_0 (the power step
+  // of mode 0) together with mode 1's Omega sketch, and later the first core stage together with the
+  // last mode's Omega sketch (X viewed with the last mode as rows).  9 passes over X:
+  //   S0, [Z0 + S1], Y0, Z1, [G1 + S2], Y1, Z2, Y2, residual
+  // QR(S0) is exposed (the Omega_1 conversion runs under it); QR(S1) hides under Y0, the last QR of
+  // mode 0 under Z1, QR(S2) under Y1; the final QR of mode 2 closes the sketch phase.
+  const bool try_fuse2 = try_fuse && N == 3 && q == 1 && !dist() && !ctx.fuse2_off && (omega_ld[2 * N + 2] % 4) == 0 &&
+                         X.d[0] % 512 == 0 && X.d[1] % 128 == 0 && X.d[2] % 128 == 0 && K[0] % 4 == 0 &&
+                         K[0] == K[1] && K[0] == K[2] && tc_npad(int(K[0])) > 0 && tc_npad(int(K[0])) <= 80;
+  if (try_fuse2) {
+    const Box b0 = X.box(0), b1 = X.box(1);
+    const Box b2v{X.d[0], X.d[2], X.d[1]};     // [alpha = i0, rows = i2, beta = i1]
+    const int npad = tc_npad(int(K[0]));
+    first_sketch(0);                           // S0: X's scale; QR + unmixing of mode 0 on the side stream
+    F1Prep pre1, pre2;
+    const bool p1 = sketch1_core0_prep(ctx, ws, static_cast<const float*>(omega[1 * N + 1]), b1.J(), int(K[1]),
+                                       omega_ld[1 * N + 1], npad, &pre1);
+    // [Z0 + S1]
+    const int64_t Jl0 = b0.J(), ldz = pad4(K[0]), ldz2 = 2 * int64_t(npad);
+    pbs[0].Z = ws.alloc_n<float>(Jl0 * ldz);
+    pbs[0].Z2 = reinterpret_cast<float*>(ws.alloc_n<uint16_t>(Jl0 * ldz2));
+    wait_q(0);
+    bool fused1;
+    {
+      const auto mz = ws.mark();
+      int64_t ldqt;
+      const float* QyT = working_copy<float>(ctx, ws, Qu[0], X.d[0], K[0], X.d[0], ldqt);
+      const int ez = int(std::ceil(0.5 * std::log2(double(X.Ig(0)))));
+      F1ZOut zo{pbs[0].Z, ldz, reinterpret_cast<uint16_t*>(pbs[0].Z2), ldz2, xs_slot + 1, std::ldexp(1.0f, -(ez + 1)),
+                xs_slot};
+      LabelScope ls(ctx, "sketch1_z0");
+      fused1 = sketch1_core0(ctx, ws, data, b1, b0, static_cast<const float*>(omega[1 * N + 1]), omega_ld[1 * N + 1],
+                             int(K[1]), QyT, ldqt, int(K[0]), xs_slot, Yt[1], X.d[1], nullptr, 0, p1 ? &pre1 : nullptr,
+                             &zo);
+      ws.rewind(mz);
+    }
+    if (fused1) {
+      set_status_if_nonfinite(ctx, Yt[1], X.d[1] * K[1]);
+      fork_qr(1, Qy[1]);
+    } else {
+      RT_REQUIRE(power_step_r31(X, data, 0, int(K[0]), Qu[0], Yt[0], true, &pbs[0], 1), kEUNSUPPORTED,
+                 "power step (Z pass) not launched");
+      first_sketch(1);
+    }
+    // Y0, then Z1 (under it: QR(S1), then the last QR of mode 0)
+    RT_REQUIRE(power_step_r31(X, data, 0, int(K[0]), nullptr, Yt[0], true, &pbs[0], 2), kEUNSUPPORTED,
+               "power step (product) not launched");
+    fork_qr(0, Qt[0]);
+    wait_q(1);
+    RT_REQUIRE(power_step_r31(X, data, 1, int(K[1]), Qu[1], Yt[1], true, &pbs[1], 1), kEUNSUPPORTED,
+               "power step (Z pass) not launched");
+    const bool p2 = sketch1_core0_prep(ctx, ws, static_cast<const float*>(omega[2 * N + 2]), b2v.J(), int(K[2]),
+                                       omega_ld[2 * N + 2], npad, &pre2);
+    wait_q(0);
+    // [G1 + S2]
+    bool fused2;
+    {
+      int64_t ld0;
+      const float* q0 = working_copy<float>(ctx, ws, Qt[0], X.d[0], K[0], ldq[0], ld0);
+      float* g = ws.alloc_n<float>(b0.b * K[0]);
+      {
+        LabelScope ls(ctx, "sketch2_core0");
+        fused2 = sketch1_core0(ctx, ws, data, b2v, b0, static_cast<const float*>(omega[2 * N + 2]),
+                               omega_ld[2 * N + 2], int(K[2]), q0, ld0, int(K[0]), xs_slot, Yt[2], X.d[2], g, 1,
+                               p2 ? &pre2 : nullptr, nullptr);
+      }
+      if (fused2) {
+        set_status_if_nonfinite(ctx, Yt[2], X.d[2] * K[2]);
+        fork_qr(2, Qy[2]);
+        g1 = g;
+      } else {
+        first_sketch(2);
+      }
+    }
+    // Y1 (under it: QR(S2)), Z2, Y2
+    RT_REQUIRE(power_step_r31(X, data, 1, int(K[1]), nullptr, Yt[1], true, &pbs[1], 2), kEUNSUPPORTED,
+               "power step (product) not launched");
+    fork_qr(1, Qt[1]);
+    wait_q(2);
+    RT_REQUIRE(power_step_r31(X, data, 2, int(K[2]), Qu[2], Yt[2], true), kEUNSUPPORTED, "power step not launched");
+    fork_qr(2, Qt[2]);
+  } else if (try_fuse) {
     first_sketch(0);
     for (int n = 2; n < N; ++n) first_sketch(n);
     power_all(0);                              // Q~_0 after its last QR
-    for (int n = 2; n < N; ++n) power_all(n);  // hides that QR
+    // modes 2..N-1: every power step, but the product of the last one waits until after the fused
+    // pass, so that both the last QR of mode 0 (needed by the fused pass) and the QR of the fused
+    // pass's mode-1 sketch (needed by mode 1's Z pass) run under an X pass:
+    //   S0, S2, Z0, Y0, Z2, [S1 + G1], Y2, Z1, Y1
+    for (int n = 2; n < N; ++n) {
+      if (dist() && n == N - 1) continue;
+      for (; it_done[n] < q - 1; ++it_done[n]) {
+        wait_q(n);
+        RT_REQUIRE(power_step_r31(X, data, n, int(K[n]), dist() ? Qy[n] : Qu[n], Yt[n], !dist()), kEUNSUPPORTED,
+                   "power step not launched");
+        fork_qr(n, Qy[n]);
+      }
+      wait_q(n);
+      RT_REQUIRE(power_step_r31(X, data, n, int(K[n]), dist() ? Qy[n] : Qu[n], Yt[n], !dist(), &pbs[n], 1),
+                 kEUNSUPPORTED, "power step (Z pass) not launched");
+      deferred[n] = true;
+    }
     wait_q(0);
     const Box b1 = X.box(1), b0 = X.box(0);
     int64_t ld0;
@@ -694,6 +807,13 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
       g1 = g;
     } else {
       first_sketch(1);
+    }
+    for (int n = 2; n < N; ++n) {              // the deferred products (under them: mode 1's QR)
+      if (!deferred[n]) continue;
+      RT_REQUIRE(power_step_r31(X, data, n, int(K[n]), nullptr, Yt[n], true, &pbs[n], 2), kEUNSUPPORTED,
+                 "power step (product) not launched");
+      fork_qr(n, Qt[n]);
+      it_done[n] = q;
     }
     power_all(1);
   } else {

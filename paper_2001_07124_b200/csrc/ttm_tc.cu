@@ -1176,6 +1176,14 @@ struct FParams {
   const float* xscale; // device s (0: the tf32 twins run)
   float binv_s, binv_c;
   unsigned int* runs;
+  int zout;              // 1: the left output is a power-iteration Z in the R31 form (s_z-scaled fp16 [hi | lo]
+                         //    rows of 2 NPAD halves), 0: fp32 core rows of C floats
+  int view_last;         // 1: X viewed for the last mode (rows i_{N-1}, beta = the middle modes): output
+                         //    row j = beta + b i (3-D stores); 0: mode-1 view, row j = i + I beta
+  const float* oscale;   // zout: device scale of Z (sn, R31)
+  float omul;            // zout: host power of two of Z (2^-(ceil(log2 sqrt I_0) + 1))
+  void* out;             // the left output rows (fp32 core rows or fp16 Z rows)
+  int64_t ldo;           // row pitch in elements (C floats / 2 NPAD halves)
 };
 
 template <int NPAD, int NBB_ = 2>
@@ -1187,7 +1195,7 @@ struct PlanF {
   __host__ __device__ static constexpr uint32_t a_slot(int s) { return a_base + 32u * uint32_t(s); }
   static constexpr uint32_t kX = uint32_t(BM) * x_pitch<XW>();
   static constexpr uint32_t kB = 3u * NPAD * 128u;                   // one chunk pair: 64 K x 3 NPAD rows
-  static constexpr uint32_t kO = uint32_t(BM) * ((NPAD + 31) / 32) * 128u;   // core output staging
+  static constexpr uint32_t kO = 0;         // the left output leaves from registers (no staging)
   static constexpr uint32_t budget = 224u * 1024u;
   static constexpr int NX_fit = int((budget - NBB * kB - kO) / kX);
   static constexpr int NX = NX_fit > 4 ? 4 : NX_fit;
@@ -1202,8 +1210,7 @@ constexpr int NT_FUSED = 512;   // the 12 warps of the TTM kernels + a second ep
 template <int NPAD, int NBB_ = 2>
 __global__ void __launch_bounds__(NT_FUSED, 1)
 sketch1_core0_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmq,
-                     const __grid_constant__ CUtensorMap tmw, const __grid_constant__ CUtensorMap tmc,
-                     const FParams p) {
+                     const __grid_constant__ CUtensorMap tmw, const FParams p) {
   using L = PlanF<NPAD, NBB_>;
   constexpr int NX = L::NX, NB = L::NB, NBB = L::NBB, XW = L::XW;
   if (*p.xscale == 0.f) return;                        // the tf32 twins run instead (R29)
@@ -1236,7 +1243,7 @@ sketch1_core0_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_const
     mbar_init(acc_full, 2);
     mbar_init(acc_empty, 256);                        // both epilogue groups
     fence_barrier_init();
-    tma_prefetch(&tmx); tma_prefetch(&tmq); tma_prefetch(&tmw); tma_prefetch(&tmc);
+    tma_prefetch(&tmx); tma_prefetch(&tmq); tma_prefetch(&tmw);
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
@@ -1344,63 +1351,68 @@ sketch1_core0_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_const
       for (int k = 0; k < NPAD; ++k)
         if (k < p.K) dst[int64_t(k) * p.I + i] = sums[k] * inv_s;
     }
-  } else if (warp >= 12) {                             // ---------------- epilogue C: core rows
+  } else if (warp >= 12) {                             // ---------------- epilogue C: the left output rows
+    // C0 + C1a + C1b of each segment are read out of TMEM 8 columns at a time into the row's fp32
+    // sums (registers, one row per thread), the accumulator is released, and after the cpb chunks of a
+    // beta the finished row leaves straight from the registers (no shared-memory staging: the X ring
+    // gets that space)
     const int q4 = warp & 3;
     const int r = 32 * q4 + lane;
     const uint32_t lane_base = tmem + (uint32_t(32 * q4) << 16);
     const float inv_c = p.binv_c / *p.xscale;           // exact: powers of two
+    const float zmul = p.zout ? inv_c * *p.oscale * p.omul * kQScale : 0.f;   // R31: s_z Z, then x 2^14
     const int spb = int(p.cpb / p.seg);                 // segments per beta
     const int nseg = nch / p.seg;
-    uint8_t* stage = smem + L::off_o;
+    float cs[NPAD];
     for (int u = 0; u < nseg; ++u) {
       const int ub = u % spb;
-      if (ub == 0 && u > 0) {                          // the previous beta's stores have read the staging
-        if (r == 0) bulk_wait_read0();
-        named_bar(1, 128);
+      if (ub == 0) {
+#pragma unroll
+        for (int c = 0; c < NPAD; ++c) cs[c] = 0.f;
       }
       mbar_wait(acc_full, uint32_t(u) & 1u);
       tc_fence_after();
-      const bool fin = ub == spb - 1;
 #pragma unroll
-      for (int c0 = 0; c0 < NPAD; c0 += 16) {
-        uint32_t v0[16], v1[16], v2[16];
-        tmem_ld16(lane_base + L::c0 + c0, v0);
-        tmem_ld16(lane_base + L::c1a + c0, v1);
-        tmem_ld16(lane_base + L::c1b + c0, v2);
+      for (int c0 = 0; c0 < NPAD; c0 += 8) {
+        uint32_t v0[8], v1[8], v2[8];
+        tmem_ld8(lane_base + L::c0 + c0, v0);
+        tmem_ld8(lane_base + L::c1a + c0, v1);
+        tmem_ld8(lane_base + L::c1b + c0, v2);
         tmem_wait_ld();
-        if (c0 + 16 >= NPAD) { tc_fence_before(); mbar_arrive(acc_empty); }   // TMEM read: release early
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          const int c = c0 + 4 * g;
-          float4* dst = reinterpret_cast<float4*>(stage + (c >> 5) * (BM * 128) + r * 128 + ((((c & 31) >> 2) ^ (r & 7)) << 4));
-          float4 v;
-          v.x = __uint_as_float(v0[4 * g + 0]) + (__uint_as_float(v1[4 * g + 0]) + __uint_as_float(v2[4 * g + 0]));
-          v.y = __uint_as_float(v0[4 * g + 1]) + (__uint_as_float(v1[4 * g + 1]) + __uint_as_float(v2[4 * g + 1]));
-          v.z = __uint_as_float(v0[4 * g + 2]) + (__uint_as_float(v1[4 * g + 2]) + __uint_as_float(v2[4 * g + 2]));
-          v.w = __uint_as_float(v0[4 * g + 3]) + (__uint_as_float(v1[4 * g + 3]) + __uint_as_float(v2[4 * g + 3]));
-          if (ub > 0) {
-            const float4 o = *dst;
-            v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
-          }
-          if (fin) { v.x *= inv_c; v.y *= inv_c; v.z *= inv_c; v.w *= inv_c; }
-          *dst = v;
-        }
+        for (int k = 0; k < 8; ++k)
+          cs[c0 + k] += __uint_as_float(v0[k]) + (__uint_as_float(v1[k]) + __uint_as_float(v2[k]));
       }
-      if (fin) {                                       // beta complete: rows i1 + I beta of the core stage
-        fence_proxy_async();
-        named_bar(1, 128);
-        if (r == 0) {
-          int64_t a0, beta;
-          coords(u * p.seg, a0, beta);
-          const int row0 = int(i0 + p.I * beta);
+      tc_fence_before();
+      mbar_arrive(acc_empty);
+      if (ub == spb - 1) {                             // beta complete: this thread's row of the output
+        int64_t a0, beta;
+        coords(u * p.seg, a0, beta);
+        const int64_t row = p.view_last ? beta + p.b * (i0 + r) : i0 + r + p.I * beta;
+        if (p.zout) {
+          // fp16 [2^14 hi | 2^14 lo] row of 2 NPAD halves (columns >= C zero)
+          uint4* oh = reinterpret_cast<uint4*>(static_cast<__half*>(p.out) + row * p.ldo);
+          uint4* ol = reinterpret_cast<uint4*>(static_cast<__half*>(p.out) + row * p.ldo + NPAD);
 #pragma unroll
-          for (int bx = 0; bx < (NPAD + 31) / 32; ++bx)
-            if (32 * bx < p.C) tma_store_2d(&tmc, stage + bx * (BM * 128), 32 * bx, row0);
-          bulk_commit();
+          for (int k = 0; k < NPAD / 8; ++k) {
+            uint32_t h[4], l[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int c0 = 8 * k + 2 * e, c1 = c0 + 1;
+              split_h16x2(c0 < p.C ? cs[c0] * zmul : 0.f, c1 < p.C ? cs[c1] * zmul : 0.f, h[e], l[e]);
+            }
+            oh[k] = make_uint4(h[0], h[1], h[2], h[3]);
+            ol[k] = make_uint4(l[0], l[1], l[2], l[3]);
+          }
+        } else {
+          float4* o4 = reinterpret_cast<float4*>(static_cast<float*>(p.out) + row * p.ldo);
+#pragma unroll
+          for (int k = 0; k < NPAD / 4; ++k)
+            if (4 * k < p.C)
+              o4[k] = make_float4(cs[4 * k] * inv_c, cs[4 * k + 1] * inv_c, cs[4 * k + 2] * inv_c, cs[4 * k + 3] * inv_c);
         }
       }
     }
-    if (r == 0) bulk_wait0();
   }
   tc_fence_before();
   __syncthreads();
@@ -2098,35 +2110,68 @@ bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q
 // Om: the fp32 Omega_1 (J x K1 row-major, ld ldom; tf32-exact for the fused form, else the flag sends
 // the work to the twins); Q0: Q~_0 fp32 col-major (I_0 x K0, ld ldq0, orthonormal); xs: X's scale pair.
 // Outputs: Y (fp64 I_1 x K1, ld ldy) and out (the core stage: rows j = i1 + I_1 beta of K0 floats).
-bool sketch1_core0(const Ctx& ctx, Arena& ws, const float* X, Box b1, Box b0, const float* Om, int64_t ldom, int K1,
-                   const float* Q0, int64_t ldq0, int K0, const float* xs, double* Y, int64_t ldy, float* out) {
-  if (ctx.simt() || !ctx.tc_h16 || ctx.fuse_off) return false;
-  const int npad = tc_npad(std::max(K0, K1));
-  if (npad < 0 || npad > 80) return false;
-  if (b1.a % 512 || b1.I % BM || (K0 % 4) || (ldom % 4) || !aligned(X, 16) || !aligned(Om, 16) || !aligned(out, 16))
+__global__ void omega_gate_inv_kernel(const int* __restrict__ flag, const float* __restrict__ xs, float* __restrict__ out) {
+  out[0] = *flag ? xs[0] : 0.f;                      // the fused pass stood down for Omega, X's scale is fine
+  out[1] = xs[1];
+}
+
+bool sketch1_core0_prep(const Ctx& ctx, Arena& ws, const float* Om, int64_t J, int K1, int64_t ldom, int npad,
+                        F1Prep* pre) {
+  if (ctx.simt() || !ctx.tc_h16 || ctx.fuse_off || npad <= 0 || npad > 80 || (ldom % 4) || !aligned(Om, 16) ||
+      J > INT32_MAX)
     return false;
-  const int64_t J = b1.J();
-  if (b1.a > INT32_MAX || b1.I > INT32_MAX || b1.b > INT32_MAX || J > INT32_MAX || b0.b > INT32_MAX) return false;
-  // B sources: 2^14 [Q_hi^T ; Q_lo^T] and 2^11 Omega^T in fp16, rows padded to npad
-  const int64_t ldt = (b1.a + 7) & ~int64_t(7), ldw = (J + 63) & ~int64_t(63);
-  __half* QT = ws.alloc_n<__half>(2 * npad * ldt);
-  __half* WT = ws.alloc_n<__half>(int64_t(npad) * ldw);
-  int* flag = ws.alloc_n<int>(1);
-  float* xso = ws.alloc_n<float>(2);
-  RT_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), ctx.stream));
-  launch(ctx, "qt16", [&] {
-    qt16_kernel<<<unsigned(cdiv(ldt * npad, 256)), 256, 0, ctx.stream>>>(Q0, b1.a, K0, ldq0, npad, QT, ldt);
-  });
+  pre->npad = npad;
+  pre->ldw = (J + 63) & ~int64_t(63);
+  __half* WT = ws.alloc_n<__half>(int64_t(npad) * pre->ldw);
+  pre->WT = reinterpret_cast<uint16_t*>(WT);
+  pre->flag = ws.alloc_n<int>(1);
+  RT_CUDA(cudaMemsetAsync(pre->flag, 0, sizeof(int), ctx.stream));
+  const int64_t ldw = pre->ldw;
+  int* flag = pre->flag;
   launch(ctx, "omega_t16", [&] {
     omega_t16_kernel<<<unsigned(cdiv(ldw, 64)), 256, 0, ctx.stream>>>(Om, J, K1, ldom, npad, WT, ldw, flag);
   });
+  return true;
+}
+
+bool sketch1_core0(const Ctx& ctx, Arena& ws, const float* X, Box b1, Box b0, const float* Om, int64_t ldom, int K1,
+                   const float* Q0, int64_t ldq0, int K0, const float* xs, double* Y, int64_t ldy, float* out,
+                   int view_last, const F1Prep* pre, const F1ZOut* zo) {
+  if (ctx.simt() || !ctx.tc_h16 || ctx.fuse_off) return false;
+  const int npad = tc_npad(std::max(K0, K1));
+  if (npad < 0 || npad > 80) return false;
+  if (b1.a % 512 || b1.I % BM || (K0 % 4) || (ldom % 4) || !aligned(X, 16) || !aligned(Om, 16) ||
+      (!zo && !aligned(out, 16)))
+    return false;
+  if (pre && pre->npad != npad) return false;
+  const int64_t J = b1.J();
+  if (b1.a > INT32_MAX || b1.I > INT32_MAX || b1.b > INT32_MAX || J > INT32_MAX || b0.b > INT32_MAX) return false;
+  if (zo && (!zo->Z2 || zo->ldz2 != 2 * npad || !aligned(zo->Z2, 16))) return false;
+  // X as [alpha = i_0, rows = i_m, beta]: the mode-1 view is X's memory order; the last-mode view
+  // takes the rows from the slowest dimension and beta (the middle modes) from the middle
+  const uint64_t xd[3] = {uint64_t(b1.a), uint64_t(b1.I), uint64_t(b1.b)};
+  const uint64_t xst[2] = {view_last ? uint64_t(b1.a) * b1.b * 4 : uint64_t(b1.a) * 4,
+                           view_last ? uint64_t(b1.a) * 4 : uint64_t(b1.a) * b1.I * 4};
+  // B sources: 2^14 [Q_hi^T ; Q_lo^T] and 2^11 Omega^T in fp16, rows padded to npad
+  const int64_t ldt = (b1.a + 7) & ~int64_t(7);
+  __half* QT = ws.alloc_n<__half>(2 * npad * ldt);
+  F1Prep own;
+  if (!pre) {
+    if (!sketch1_core0_prep(ctx, ws, Om, J, K1, ldom, npad, &own)) return false;
+    pre = &own;
+  }
+  __half* WT = reinterpret_cast<__half*>(pre->WT);
+  const int64_t ldw = pre->ldw;
+  int* flag = pre->flag;
+  float* xso = ws.alloc_n<float>(2);
+  launch(ctx, "qt16", [&] {
+    qt16_kernel<<<unsigned(cdiv(ldt * npad, 256)), 256, 0, ctx.stream>>>(Q0, b1.a, K0, ldq0, npad, QT, ldt);
+  });
   launch(ctx, "omega_gate", [&] { omega_gate_kernel<<<1, 1, 0, ctx.stream>>>(flag, xs, xso); });
-  CUtensorMap tx, tq, tw, tc;
+  CUtensorMap tx, tq, tw;
   {
-    const uint64_t d[3] = {uint64_t(b1.a), uint64_t(b1.I), uint64_t(b1.b)};
-    const uint64_t st[2] = {uint64_t(b1.a) * 4, uint64_t(b1.a) * b1.I * 4};
     const uint32_t bx[3] = {uint32_t(KC * 2 + 4), BM, 1};
-    if (!make_map(&tx, X, 3, d, st, bx, false)) return false;
+    if (!make_map(&tx, X, 3, xd, xst, bx, false)) return false;
   }
   {
     const uint64_t d[2] = {uint64_t(ldt), uint64_t(2 * npad)}, st[1] = {uint64_t(ldt) * 2};
@@ -2138,11 +2183,9 @@ bool sketch1_core0(const Ctx& ctx, Arena& ws, const float* X, Box b1, Box b0, co
     const uint32_t bx[3] = {64, uint32_t(npad), 1};
     if (!make_map(&tw, WT, 3, d, st, bx, true, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_DATA_TYPE_FLOAT16)) return false;
   }
-  {
-    const uint64_t d[2] = {uint64_t(K0), uint64_t(b0.b)}, st[1] = {uint64_t(K0) * 4};
-    const uint32_t bx[2] = {32, uint32_t(BM)};
-    if (!make_map(&tc, out, 2, d, st, bx, true)) return false;
-  }
+  // the left output: fp32 core rows (K0 floats) or the R31 Z rows (2 npad halves); rows j = i + I beta
+  // (mode-1 view) or j = beta + b i (last-mode view), written from the epilogue's registers
+  if (zo ? !aligned(zo->Z2, 16) : !aligned(out, 16)) return false;
   FParams p;
   p.a = b1.a; p.I = b1.I; p.b = b1.b; p.K = K1; p.C = K0;
   p.cpb = b1.a / KC;
@@ -2159,6 +2202,12 @@ bool sketch1_core0(const Ctx& ctx, Arena& ws, const float* X, Box b1, Box b0, co
   p.binv_s = 1.f / 2048.f;
   p.binv_c = 1.f / kQScale;
   p.runs = ctx.d_runs;
+  p.zout = zo ? 1 : 0;
+  p.view_last = view_last;
+  p.oscale = zo ? zo->oscale : nullptr;
+  p.omul = zo ? zo->omul : 1.f;
+  p.out = zo ? static_cast<void*>(zo->Z2) : static_cast<void*>(out);
+  p.ldo = zo ? int64_t(2 * npad) : int64_t(K0);
   const dim3 grid{unsigned(mtiles), unsigned(splits), 1u};
   // tf32 twins, gated on the same scale (s == 0: X's range or Omega's precision outside the fp16
   // form): the plain sketch kernel on the fp32 Omega and the tf32 core stage
@@ -2180,22 +2229,20 @@ bool sketch1_core0(const Ctx& ctx, Arena& ws, const float* X, Box b1, Box b0, co
       static bool attr = false;                                                                          \
       if (!attr) { set_smem(sketch1_core0_kernel<NP, 3>, L::bytes); attr = true; }                       \
       launch(ctx, ctx.label ? ctx.label : "sketch1_core0", [&] {                                         \
-        sketch1_core0_kernel<NP, 3><<<grid, NT_FUSED, L::bytes, ctx.stream>>>(tx, tq, tw, tc, p);        \
+        sketch1_core0_kernel<NP, 3><<<grid, NT_FUSED, L::bytes, ctx.stream>>>(tx, tq, tw, p);            \
       });                                                                                                \
     } else {                                                                                             \
       using L = PlanF<NP, 2>;                                                                            \
       static bool attr = false;                                                                          \
       if (!attr) { set_smem(sketch1_core0_kernel<NP, 2>, L::bytes); attr = true; }                       \
       launch(ctx, ctx.label ? ctx.label : "sketch1_core0", [&] {                                         \
-        sketch1_core0_kernel<NP, 2><<<grid, NT_FUSED, L::bytes, ctx.stream>>>(tx, tq, tw, tc, p);        \
+        sketch1_core0_kernel<NP, 2><<<grid, NT_FUSED, L::bytes, ctx.stream>>>(tx, tq, tw, p);            \
       });                                                                                                \
     }                                                                                                    \
     int xw_t = xw_feasible<NP>(bmode_t, false, 2);                                                       \
     {                                                                                                    \
-      const uint64_t d[3] = {uint64_t(b1.a), uint64_t(b1.I), uint64_t(b1.b)};                            \
-      const uint64_t st[2] = {uint64_t(b1.a) * 4, uint64_t(b1.a) * b1.I * 4};                            \
       const uint32_t bx[3] = {xw_t > 1 ? uint32_t(KC * xw_t + 4) : uint32_t(KC), BM, 1};                 \
-      if (!make_map(&txt, X, 3, d, st, bx, xw_t == 1)) return false;                                    \
+      if (!make_map(&txt, X, 3, xd, xst, bx, xw_t == 1)) return false;                                  \
     }                                                                                                    \
     dispatch_s<NP>(ctx, false, bmode_t, xw_t, txt, tbf, pf, grid);                                       \
     break;                                                                                               \
@@ -2205,8 +2252,20 @@ bool sketch1_core0(const Ctx& ctx, Arena& ws, const float* X, Box b1, Box b0, co
     default: return false;
   }
 #undef RT_F_CASE
-  RT_REQUIRE(ttm_t_tc(ctx, ws, X, b0, Q0, ldq0, K0, out, 1, 1, K0, 0, false, nullptr, xso), kEUNSUPPORTED,
-             "sketch1_core0: tf32 twin of the core stage rejected");
+  if (!zo) {
+    RT_REQUIRE(ttm_t_tc(ctx, ws, X, b0, Q0, ldq0, K0, out, 1, 1, K0, 0, false, nullptr, xso), kEUNSUPPORTED,
+               "sketch1_core0: tf32 twin of the core stage rejected");
+  } else {
+    // twins of the R31 Z pass: the fp16-split Z pass when only Omega closed the fused gate (gz), and
+    // the tf32 one writing the fp32 s_z Z when X's scale is 0 (the product's tf32 twin reads it)
+    float* gz = ws.alloc_n<float>(2);
+    launch(ctx, "omega_gate", [&] { omega_gate_inv_kernel<<<1, 1, 0, ctx.stream>>>(flag, zo->xs_x, gz); });
+    RT_REQUIRE(ttm_t_tc(ctx, ws, X, b0, Q0, ldq0, K0, reinterpret_cast<float*>(zo->Z2), zo->ldz2, 1, zo->ldz2, 2, false,
+                        gz, nullptr, zo->oscale, zo->omul, true) &&
+                   ttm_t_tc(ctx, ws, X, b0, Q0, ldq0, K0, zo->Z, zo->ldz, 1, zo->ldz, 0, false, nullptr, zo->xs_x,
+                            zo->oscale, zo->omul),
+               kEUNSUPPORTED, "sketch1_core0: twins of the Z pass rejected");
+  }
   const int64_t n = b1.I * K1;
   launch(ctx, "splitk_reduce", [&] {
     splitk_reduce_f32_kernel<<<unsigned(cdiv(n, 32)), 256, 0, ctx.stream>>>(p.part, b1.I, K1, int(splits), Y, ldy);
@@ -2571,9 +2630,9 @@ residual_h16_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_consta
 #pragma unroll
       for (int c = 0; c < RP / 2; ++c) split_h16x2(v[2 * c], v[2 * c + 1], hi[c], lo[c]);
 #pragma unroll
-      for (int g = 0; g < RP / 32; ++g) {
-        tmem_st16(lane_base + kA + 16 * g, *reinterpret_cast<const uint32_t(*)[16]>(&hi[16 * g]));
-        tmem_st16(lane_base + kA + RP / 2 + 16 * g, *reinterpret_cast<const uint32_t(*)[16]>(&lo[16 * g]));
+      for (int gq = 0; gq < RP / 32; ++gq) {
+        tmem_st16(lane_base + kA + 16 * gq, *reinterpret_cast<const uint32_t(*)[16]>(&hi[16 * gq]));
+        tmem_st16(lane_base + kA + RP / 2 + 16 * gq, *reinterpret_cast<const uint32_t(*)[16]>(&lo[16 * gq]));
       }
       tmem_wait_st();
       tc_fence_before();

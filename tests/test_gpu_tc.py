@@ -388,3 +388,47 @@ def test_split_residual_widths(P, rank, p):
             assert M.subspace(qg[n], ref["Q"][n]) <= 1e-5
         h.close()
     assert abs(e[297] - e[296]) / e[296] <= 1e-6
+
+
+@pytest.mark.parametrize("dims,rank,p", [((512, 256, 256), 20, 12),     # K = 32
+                                         ((512, 384, 256), 64, 16),     # K = 80 (the bench width)
+                                         ((1024, 128, 384), 40, 8)])    # K = 48
+def test_two_fused_passes(P, dims, rank, p):
+    """The 9-pass HOSVD schedule (N = 3, q = 1): [Z0 + S1] (the fused pass writing mode 0's power-step
+    Z in the R31 fp16 form beside mode 1's Omega sketch) and [G1 + S2] (the first core stage beside
+    the last mode's Omega sketch, X viewed with the last mode as rows).  Parity with the oracle, both
+    fused launches seen in the profile, and the same result as the one-fusion schedule (option 298)
+    to fp32 rounding."""
+    from paper_2001_07124_b200 import _lib as L
+    cfg = dataclasses.replace(synth.CONFIGS["cfg5"].scaled(dims, (rank,) * 3, (rank,) * 3), p=p, q=1)
+    x = synth.make_tensor(cfg)
+    oms = [synth.round_tf32(synth.gaussian_omega(cfg, n)) for n in range(3)]
+    ref = oracle.hosvd(x, cfg.ranks, oms, q=1)
+    res = {}
+    for opt in (299, 298):
+        h = _handle(P, 0, omega_tf32=True)
+        h.set_option(L.RT_OPT_TC_ABLATE, opt)
+        h.set_option(L.RT_OPT_PROFILE, 1)
+        r = P.rtucker_hosvd(h, dev(x), cfg.ranks, cfg.p, 1, [om_dev(o) for o in oms])
+        h.sync()
+        prof = h.profile_read()[0]
+        names = {n for n, _, _ in prof}
+        if opt == 299:
+            assert "sketch1_z0" in names and "sketch2_core0" in names, names
+            runs = {n: c for n, c, _ in prof if n in ("h16_ran", "tf32_twin_ran")}
+            assert runs.get("tf32_twin_ran", 0) == 0, runs
+        else:
+            assert "sketch1_core0" in names and "sketch1_z0" not in names, names
+        res[opt] = r
+        qg = [mat(t) for t in r["Q"]]
+        gg = P.core_to_numpy(r["G"])
+        for n in range(3):
+            assert M.orth(qg[n]) <= 1e-12
+            assert M.subspace(qg[n], ref["Q"][n]) <= 1e-5, (opt, n, M.subspace(qg[n], ref["Q"][n]))
+        assert M.core_in_oracle_basis(gg, qg, ref["G"], ref["Q"]) <= 1e-5
+        assert M.recon(gg, qg, ref["G"], ref["Q"]) <= 1e-5
+        e = mat(r["err"])[0]
+        assert abs(e - ref["E"]) / ref["E"] <= 1e-5, (opt, e, ref["E"])
+        h.close()
+    for n in range(3):
+        assert M.subspace(mat(res[299]["Q"][n]), mat(res[298]["Q"][n])) <= 2e-6
