@@ -45,7 +45,9 @@ def launches(path, rnd):
     for d in data:
         if d.get("Metric Name") != "gpu__time_duration.sum":
             continue
-        if not any(o in d["Kernel Name"] for o in ours):
+        nm = d["Kernel Name"]
+        if any(t in nm for t in ("at::", "c10::", "cub::", "cublas", "nccl")) or not (
+                any(o in nm for o in ours) or "unnamed>::" in nm or "rt::" in nm):
             continue                        # torch's input-generation kernels (outside the timed region)
         unit = d.get("Metric Unit", unit)
         v = float(d["Metric Value"].replace(",", ""))
