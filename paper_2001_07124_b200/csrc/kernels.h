@@ -123,6 +123,10 @@ bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q
 template <typename T>
 void gram(const Ctx& ctx, Arena& ws, const T* A, int64_t m, int k, int64_t lda, double* G, bool rowmajor = false);
 
+// G = B_(n) B_(n)^T (K x K, fp64) of B viewed as the box [a, K = box.I, b] (the Gram-EVD of the
+// truncation / the STHOSVD step); deterministic (fixed-order partial sums), K <= 128.
+void gram_unfold(const Ctx& ctx, Arena& ws, const double* B, Box box, double* G);
+
 // Cholesky of (G + shift*I) (k x k) -> R (upper, col-major) and Rinv.  shift_coef * trace(G)
 // is the shift.  zero_flag[0] = 1 if trace(G) == 0 (all-zero input, reading R7).
 // shift_dev (nullable): device shift coefficient used instead of shift_coef

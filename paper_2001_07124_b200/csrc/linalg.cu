@@ -809,6 +809,115 @@ __global__ void __launch_bounds__(256) unmix_cols_kernel(const double* __restric
   }
 }
 
+
+// ------------------------------------------------------------ Gram of an unfolding
+// G = B_(n) B_(n)^T for B viewed as [a, K, b] (column j = (alpha, beta) holds B[alpha + a p + a K beta],
+// p < K).  A CTA takes a contiguous range of columns in chunks of 32 staged in shared memory; the
+// upper-triangle 4 x 4 blocks of G are spread over the threads (column groups when there are fewer
+// blocks than threads), fp64 products and sums; the groups are added into the CTA's shared G in a
+// fixed order and the CTA partials are summed in CTA order: deterministic.
+template <int JC, int MB>
+__global__ void __launch_bounds__(256) gram_unfold_kernel(const double* __restrict__ B, int64_t a, int K, int64_t J,
+                                                          int64_t jper, double* __restrict__ part) {
+  constexpr int GU_JC = JC;
+  extern __shared__ double gsm[];
+  double* vs = gsm;                                  // [K][GU_JC + 1]
+  double* G = gsm + size_t(K) * (GU_JC + 1);         // [K][K]
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int nb = (K + 3) / 4, nblk = nb * (nb + 1) / 2;
+  // the lanes of a warp take different blocks of the same column (shared-memory broadcast reads);
+  // a set of wpb warps covers the blocks once, and the 8 / wpb sets take interleaved columns
+  const int wpb = (nblk + 31) / 32;
+  const int groups = wpb <= 8 ? 8 / wpb : 1;
+  const int g = wpb <= 8 ? warp / wpb : 0;
+  const bool active = g < groups;
+  int bp[MB], bq[MB];
+  int nmine = 0;
+  if (active) {
+    for (int idx = (wpb <= 8 ? lane + 32 * (warp % wpb) : t); idx < nblk && nmine < MB; idx += (wpb <= 8 ? nblk : 256)) {
+      int q = 0;
+      while ((q + 1) * (q + 2) / 2 <= idx) ++q;
+      bq[nmine] = q;
+      bp[nmine] = idx - q * (q + 1) / 2;
+      ++nmine;
+    }
+  }
+  double acc[MB][4][4];
+#pragma unroll
+  for (int m = 0; m < MB; ++m)
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[m][u][v] = 0.0;
+  for (int e = t; e < K * K; e += 256) G[e] = 0.0;
+  const int64_t jb = int64_t(blockIdx.x) * jper;
+  const int64_t je = jb + jper < J ? jb + jper : J;
+  for (int64_t j0 = jb; j0 < je; j0 += GU_JC) {
+    __syncthreads();
+    if (a > 1) {
+      // lane = column: one (alpha, beta) split per chunk per thread (256 % 32 == 0)
+      const int jj = t % GU_JC;
+      const int64_t j = j0 + jj;
+      const bool jv = j < je;
+      const int64_t base = jv ? (j % a) + a * K * (j / a) : 0;
+      for (int p = t / GU_JC; p < K; p += 256 / GU_JC) vs[p * (GU_JC + 1) + jj] = jv ? B[base + a * p] : 0.0;
+    } else {
+      const double* src = B + j0 * K;                   // columns contiguous: K doubles each
+      const int64_t nel = (je - j0 < GU_JC ? je - j0 : GU_JC) * int64_t(K);
+      for (int e = t; e < K * GU_JC; e += 256) {
+        const int jj = e / K, p = e - jj * K;
+        vs[p * (GU_JC + 1) + jj] = e < nel ? src[e] : 0.0;
+      }
+    }
+    __syncthreads();
+    for (int jj = g; jj < GU_JC; jj += groups) {
+#pragma unroll
+      for (int m = 0; m < MB; ++m) {
+        if (m >= nmine) break;
+        double vp[4], vq[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int p = 4 * bp[m] + u, q = 4 * bq[m] + u;
+          vp[u] = p < K ? vs[p * (GU_JC + 1) + jj] : 0.0;
+          vq[u] = q < K ? vs[q * (GU_JC + 1) + jj] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[m][u][v] = fma(vp[u], vq[v], acc[m][u][v]);
+      }
+    }
+  }
+  for (int gg = 0; gg < groups; ++gg) {
+    __syncthreads();
+    if (active && g == gg) {
+      for (int m = 0; m < nmine; ++m)
+        for (int u = 0; u < 4; ++u)
+          for (int v = 0; v < 4; ++v) {
+            const int p = 4 * bp[m] + u, q = 4 * bq[m] + v;
+            if (p < K && q < K) {
+              G[p * K + q] += acc[m][u][v];
+              if (bp[m] != bq[m]) G[q * K + p] += acc[m][u][v];
+            }
+          }
+    }
+  }
+  __syncthreads();
+  double* dst = part + int64_t(blockIdx.x) * K * K;
+  for (int e = t; e < K * K; e += 256) dst[e] = G[e];
+}
+// one CTA per element: a fixed strided assignment of the CTA partials to the threads and a fixed
+// tree (deterministic)
+__global__ void __launch_bounds__(128) gram_unfold_reduce_kernel(const double* __restrict__ part, int ncta, int KK,
+                                                                 double* __restrict__ G) {
+  __shared__ double red[32];
+  const int e = blockIdx.x;
+  double s = 0.0;
+  for (int z = threadIdx.x; z < ncta; z += blockDim.x) s += part[int64_t(z) * KK + e];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) G[e] = s;
+}
+
 }  // namespace
 
 // ======================================================================= host
@@ -1061,6 +1170,36 @@ void unmix_cols(const Ctx& ctx, const double* Q, int64_t m, int K, int64_t ldq, 
                 double* Qp, int64_t ldp) {
   RT_REQUIRE(K >= 1 && K <= 128, kEUNSUPPORTED, "unmix_cols: K outside [1, 128]");
   launch(ctx, "unmix_cols", [&] { unmix_cols_kernel<<<K, 256, 0, ctx.stream>>>(Q, m, K, ldq, Ri, zero, Qp, ldp); });
+}
+
+void gram_unfold(const Ctx& ctx, Arena& ws, const double* B, Box box, double* G) {
+  const int K = int(box.I);
+  const int64_t J = box.J();
+  RT_REQUIRE(K >= 1 && K <= 128, kEUNSUPPORTED, "gram_unfold: K outside [1, 128]");
+  if (J == 0) { fill_zero(ctx, G, sizeof(double) * size_t(K) * K); return; }
+  // 128 columns per staged chunk (the loads of a chunk all in flight) when the Gram tile fits beside it
+  const int jc = K <= 64 ? 128 : 32;
+  const int ncta = int(std::max<int64_t>(1, std::min<int64_t>(int64_t(4) * ctx.num_sms, cdiv(J, int64_t(4 * jc)))));
+  const int64_t jper = cdiv(cdiv(J, int64_t(ncta)), int64_t(jc)) * jc;
+  const int nc = int(cdiv(J, jper));
+  const size_t sm = sizeof(double) * (size_t(K) * (jc + 1) + size_t(K) * K);
+  static bool attr = false;
+  if (!attr) {
+    RT_CUDA(cudaFuncSetAttribute(gram_unfold_kernel<32, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    RT_CUDA(cudaFuncSetAttribute(gram_unfold_kernel<128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    RT_CUDA(cudaFuncSetAttribute(gram_unfold_kernel<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  const auto mk = ws.mark();
+  double* part = ws.alloc_n<double>(int64_t(nc) * K * K);
+  launch(ctx, "gram_unfold", [&] {
+    const int nb = (K + 3) / 4, nblk = nb * (nb + 1) / 2;          // 4 x 4 blocks (<= 256 for K <= 88)
+    if (jc == 128 && nblk <= 256) gram_unfold_kernel<128, 1><<<nc, 256, sm, ctx.stream>>>(B, box.a, K, J, jper, part);
+    else if (jc == 128) gram_unfold_kernel<128, 2><<<nc, 256, sm, ctx.stream>>>(B, box.a, K, J, jper, part);
+    else gram_unfold_kernel<32, 3><<<nc, 256, sm, ctx.stream>>>(B, box.a, K, J, jper, part);
+    gram_unfold_reduce_kernel<<<unsigned(K * K), 128, 0, ctx.stream>>>(part, nc, K * K, G);
+  });
+  ws.rewind(mk);
 }
 
 }  // namespace rt

@@ -946,7 +946,7 @@ void Engine::truncate(const TView& X, const double* Gt, const int64_t* K, const 
     V[n] = ws.alloc_n<double>(int64_t(kk[n]) * kk[n]);
     W[n] = ws.alloc_n<double>(kk[n]);
     // M_n = G~_(n) G~_(n)^T (Gram-EVD)
-    ttm_s<double>(ctx, ws, Gt, TView::box_of(K, N, n), nullptr, 0, 0, kk[n], M[n], kk[n], /*gram=*/true);
+    gram_unfold(ctx, ws, Gt, TView::box_of(K, N, n), M[n]);
   }
   eig_sym_batch(ctx, ws, N, M, kk, W, V);
   for (int n = 0; n < N; ++n) {
@@ -1168,7 +1168,7 @@ void Engine::sthosvd(const TView& X, const int64_t* R, int q, int kind, const vo
     double* M = ws.alloc_n<double>(int64_t(K) * K);
     double* V = ws.alloc_n<double>(int64_t(K) * K);
     double* W = ws.alloc_n<double>(K);
-    ttm_s<double>(ctx, ws, B, bb, nullptr, 0, 0, K, M, K, /*gram=*/true);
+    gram_unfold(ctx, ws, B, bb, M);
     allreduce(comm, dist_slab, M, int64_t(K) * K, ctx.stream);
     eig_sym(ctx, ws, M, K, W, V);
     gemm_tall<double, double>(ctx, Qt, In, K, In, V, int(R[n]), K, Q_out[n], In);

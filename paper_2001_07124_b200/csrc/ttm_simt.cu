@@ -301,7 +301,7 @@ void launch_ttm_t(const Ctx& ctx, const Tin* X, Box box, const Tm* Mm, int64_t m
 // owns j in [32 (w % 4), +32) x c in [32 (w / 4), +32): 4 x 4 m8n8 tiles, 16 MMAs per k-step.
 // Fragments (PTX m8n8k4 .f64): A[r][k] at lane 4 r + k; B[k][n] at lane 4 n + k; C[r][2 q + e] at
 // lane 4 r + q.  fp64 pitches = 8 mod 16 doubles: the 4 k-rows of a fragment hit disjoint banks.
-template <typename Tin, typename Tm, typename Tout>
+template <typename Tin, typename Tm, typename Tout, int NF>
 __global__ void __launch_bounds__(256, 2)
 ttm_t_dmma_kernel(const Tin* __restrict__ X, int64_t a, int64_t I, int64_t J, const Tm* __restrict__ Mm,
                   int64_t ms_i, int64_t ms_c, int C, Tout* __restrict__ out, int64_t so_a, int64_t so_c,
@@ -309,7 +309,7 @@ ttm_t_dmma_kernel(const Tin* __restrict__ X, int64_t a, int64_t I, int64_t J, co
   // fp32 X is staged as fp32 (converted when a fragment is read): 32 contraction rows per stage,
   // pitch 132 floats (stores along i and the 4-row fragment reads are at most 2-way conflicted)
   using TX = typename std::conditional<std::is_same<Tin, float>::value, float, double>::type;
-  constexpr int BM = 128, BN = 64, BI = sizeof(TX) == 4 ? 32 : 16;
+  constexpr int BM = 128, BN = 16 * NF, BI = sizeof(TX) == 4 ? 32 : 16;   // NF n-fragments per warp
   constexpr int PX = sizeof(TX) == 4 ? BM + 4 : BM + 8, PM = BN + 8;
   constexpr int XL = BI * BM / 256, ML = BI * BN / 256;
   __shared__ TX Xs[BI][PX];
@@ -318,13 +318,13 @@ ttm_t_dmma_kernel(const Tin* __restrict__ X, int64_t a, int64_t I, int64_t J, co
   const int64_t j0 = int64_t(blockIdx.x) * BM;
   const int c0 = blockIdx.y * BN;
   const int64_t aI = a * I;
-  const int jw = 32 * (w & 3), cw = 32 * (w >> 2);
+  const int jw = 32 * (w & 3), cw = 8 * NF * (w >> 2);
   const int fr = lane >> 2, fk = lane & 3;
-  double acc[4][4][2];
+  double acc[4][NF][2];
 #pragma unroll
   for (int m = 0; m < 4; ++m)
 #pragma unroll
-    for (int n = 0; n < 4; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+    for (int n = 0; n < NF; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
 
   const int jl_b = t % BM;
   const int64_t j_b = j0 + jl_b;
@@ -380,15 +380,15 @@ ttm_t_dmma_kernel(const Tin* __restrict__ X, int64_t a, int64_t I, int64_t J, co
     if (ic + BI < I) load(ic + BI);
 #pragma unroll
     for (int kk = 0; kk < BI / 4; ++kk) {
-      double af[4], bf[4];
+      double af[4], bf[NF];
 #pragma unroll
       for (int m = 0; m < 4; ++m) af[m] = double(Xs[4 * kk + fk][jw + 8 * m + fr]);
 #pragma unroll
-      for (int n = 0; n < 4; ++n) bf[n] = Ms[4 * kk + fk][cw + 8 * n + fr];
+      for (int n = 0; n < NF; ++n) bf[n] = Ms[4 * kk + fk][cw + 8 * n + fr];
 #pragma unroll
       for (int m = 0; m < 4; ++m)
 #pragma unroll
-        for (int n = 0; n < 4; ++n)
+        for (int n = 0; n < NF; ++n)
           asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                        : "+d"(acc[m][n][0]), "+d"(acc[m][n][1])
                        : "d"(af[m]), "d"(bf[n]));
@@ -401,7 +401,7 @@ ttm_t_dmma_kernel(const Tin* __restrict__ X, int64_t a, int64_t I, int64_t J, co
     if (j >= J) continue;
     const int64_t ob = (j % a) * so_a + (j / a) * so_b;
 #pragma unroll
-    for (int n = 0; n < 4; ++n)
+    for (int n = 0; n < NF; ++n)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int c = c0 + cw + 8 * n + 2 * fk + e;
@@ -414,11 +414,17 @@ template <typename Tin, typename Tm, typename Tout>
 void launch_ttm_t_dmma(const Ctx& ctx, const Tin* X, Box box, const Tm* Mm, int64_t ms_i, int64_t ms_c, int C,
                        Tout* out, int64_t so_a, int64_t so_c, int64_t so_b) {
   const int64_t J = box.J();
-  const dim3 grid((unsigned)cdiv(J, 128), (unsigned)cdiv(C, 64));
+  // 32-column tiles for C <= 32 (the STHOSVD shrink at K = 27 used 27 of 64)
+  const int bn = C <= 32 ? 32 : 64;
+  const dim3 grid((unsigned)cdiv(J, 128), (unsigned)cdiv(C, bn));
   RT_REQUIRE(grid.x < (1u << 31) && grid.y < 65536, kEUNSUPPORTED, "ttm_t grid too large");
   launch(ctx, ctx.label ? ctx.label : "ttm_t_dmma", [&] {
-    ttm_t_dmma_kernel<Tin, Tm, Tout><<<grid, 256, 0, ctx.stream>>>(X, box.a, box.I, J, Mm, ms_i, ms_c, C, out,
-                                                                    so_a, so_c, so_b);
+    if (bn == 32)
+      ttm_t_dmma_kernel<Tin, Tm, Tout, 2><<<grid, 256, 0, ctx.stream>>>(X, box.a, box.I, J, Mm, ms_i, ms_c, C, out,
+                                                                         so_a, so_c, so_b);
+    else
+      ttm_t_dmma_kernel<Tin, Tm, Tout, 4><<<grid, 256, 0, ctx.stream>>>(X, box.a, box.I, J, Mm, ms_i, ms_c, C, out,
+                                                                         so_a, so_c, so_b);
   });
 }
 
@@ -447,6 +453,67 @@ void ttm_s(const Ctx& ctx, Arena& ws, const T* X, Box box, const T* Bm, int64_t 
   else               launch_ttm_s<T, 8>(ctx, ws, X, box, Bm, bs_j, bs_k, K, Y, ldy, gram);
 }
 
+// ------------------------------------------------------------ ttm_t, narrow (C <= 8)
+// The Kronecker sketch's chain (L_k = 2-4 columns) and other narrow contractions stream the source
+// once with a handful of fp64 sums per output column j: a > 1: one thread per j (consecutive alpha:
+// coalesced 4 / 8-byte loads per i, 8 loads in flight per thread); a == 1 (i contiguous): one warp
+// per j, lanes over i, warp-shuffle sums.  M (I x C) is read through L1 (every thread reads the same
+// row i).  fp64 products and sums in a fixed order.
+namespace {
+template <typename Tin, typename Tm, typename Tout, int C>
+__global__ void __launch_bounds__(256) ttm_t_narrow_kernel(const Tin* __restrict__ X, int64_t a, int64_t I, int64_t J,
+                                                           const Tm* __restrict__ Mm, int64_t ms_i, int64_t ms_c,
+                                                           Tout* __restrict__ out, int64_t so_a, int64_t so_c,
+                                                           int64_t so_b) {
+  constexpr int TI = 256;                               // rows of M staged per round
+  __shared__ double ms[TI][C];
+  const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool live = j < J;
+  const int64_t al = live ? j % a : 0, be = live ? j / a : 0;
+  const Tin* x = X + al + a * I * be;
+  double acc[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) acc[c] = 0.0;
+  for (int64_t i0 = 0; i0 < I; i0 += TI) {
+    const int ni = I - i0 < TI ? int(I - i0) : TI;
+    __syncthreads();
+    for (int e = threadIdx.x; e < ni * C; e += blockDim.x) {
+      const int il = e / C, c = e - il * C;
+      ms[il][c] = double(Mm[(i0 + il) * ms_i + c * ms_c]);
+    }
+    __syncthreads();
+    if (!live) continue;
+    int il = 0;
+    for (; il + 8 <= ni; il += 8) {
+      double xv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) xv[u] = double(x[a * (i0 + il + u)]);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int c = 0; c < C; ++c) acc[c] = fma(xv[u], ms[il + u][c], acc[c]);
+    }
+    for (; il < ni; ++il) {
+      const double xv = double(x[a * (i0 + il)]);
+#pragma unroll
+      for (int c = 0; c < C; ++c) acc[c] = fma(xv, ms[il][c], acc[c]);
+    }
+  }
+  if (!live) return;
+#pragma unroll
+  for (int c = 0; c < C; ++c) out[al * so_a + c * so_c + be * so_b] = Tout(acc[c]);
+}
+template <typename Tin, typename Tm, typename Tout, int C>
+void launch_narrow(const Ctx& ctx, const Tin* X, Box box, const Tm* Mm, int64_t ms_i, int64_t ms_c, Tout* out,
+                   int64_t so_a, int64_t so_c, int64_t so_b) {
+  const int64_t J = box.J();
+  launch(ctx, ctx.label ? ctx.label : "ttm_t_narrow", [&] {
+    ttm_t_narrow_kernel<Tin, Tm, Tout, C><<<unsigned(cdiv(J, int64_t(256))), 256, 0, ctx.stream>>>(
+        X, box.a, box.I, J, Mm, ms_i, ms_c, out, so_a, so_c, so_b);
+  });
+}
+}  // namespace
+
 template <typename Tin, typename Tm, typename Tout>
 void ttm_t(const Ctx& ctx, const Tin* X, Box box, const Tm* Mm, int64_t ms_i, int64_t ms_c, int C,
            Tout* out, int64_t so_a, int64_t so_c, int64_t so_b) {
@@ -454,8 +521,18 @@ void ttm_t(const Ctx& ctx, const Tin* X, Box box, const Tm* Mm, int64_t ms_i, in
   if (box.I == 0) {
     throw Error(kEINVAL, "ttm_t with empty contraction");
   }
+  if (C <= 4 && (box.a >= 32 || box.a == 1) && ctx.ttm_impl != 1 && cdiv(box.J(), int64_t(256)) < (int64_t(1) << 31)) {
+    // narrow contraction (the Kronecker chain's L_k = 2-4 columns): one thread per output column j,
+    // fp64 sums (the tiled kernel below wastes 5/8 of its 8-column tile here)
+    switch (C) {
+      case 1: launch_narrow<Tin, Tm, Tout, 1>(ctx, X, box, Mm, ms_i, ms_c, out, so_a, so_c, so_b); return;
+      case 2: launch_narrow<Tin, Tm, Tout, 2>(ctx, X, box, Mm, ms_i, ms_c, out, so_a, so_c, so_b); return;
+      case 3: launch_narrow<Tin, Tm, Tout, 3>(ctx, X, box, Mm, ms_i, ms_c, out, so_a, so_c, so_b); return;
+      default: launch_narrow<Tin, Tm, Tout, 4>(ctx, X, box, Mm, ms_i, ms_c, out, so_a, so_c, so_b); return;
+    }
+  }
   using Tacc = typename Acc3<Tin, Tm, Tout>::type;
-  if ((std::is_same<Tacc, double>::value && C > 16 && ctx.ttm_impl != 1) || ctx.acc64()) {
+  if ((std::is_same<Tacc, double>::value && C > 8 && ctx.ttm_impl != 1) || ctx.acc64()) {
     // fp64 accumulation: the fp64 warp MMA (fewer shared-memory operand reads per FMA)
     launch_ttm_t_dmma<Tin, Tm, Tout>(ctx, X, box, Mm, ms_i, ms_c, C, out, so_a, so_c, so_b);
     return;
