@@ -21,7 +21,7 @@ struct rt_handle {
   std::string err;
   int device = 0;
   int* d_status = nullptr;
-  unsigned int* d_runs = nullptr;   // [2] fp16-split / tf32-twin run counters (rt_profile_read)
+  unsigned int* d_runs = nullptr;   // [3] fp16-split / tf32-twin run counters, Jacobi sweeps (rt_profile_read)
 };
 
 namespace {
@@ -159,13 +159,13 @@ static rt_status create_common(rt_handle** h, void* stream) {
   }
   cudaMemset(hh->d_status, 0, sizeof(int));
   hh->ctx.d_status = hh->d_status;
-  if (cudaMalloc(&hh->d_runs, 2 * sizeof(unsigned int)) != cudaSuccess) {
+  if (cudaMalloc(&hh->d_runs, 3 * sizeof(unsigned int)) != cudaSuccess) {
     cudaGetLastError();
     cudaFree(hh->d_status);
     delete hh;
     return fail(nullptr, RT_ECUDA, "cudaMalloc(run counters) failed");
   }
-  cudaMemset(hh->d_runs, 0, 2 * sizeof(unsigned int));
+  cudaMemset(hh->d_runs, 0, 3 * sizeof(unsigned int));
   hh->ctx.d_runs = hh->d_runs;
   // side stream (highest priority: its latency-bound QR kernels take SMs ahead of the X passes)
   int lo_prio = 0, hi_prio = 0;
@@ -306,11 +306,11 @@ rt_status rt_profile_read(rt_handle* h, rt_profile_entry* out, int cap, int* n, 
     P.recs.clear();
     // device run counters of the fp16-split X passes and their tf32 twins (R29): which one of each
     // gated pair did the work since the last read
-    unsigned int runs[2] = {0, 0};
+    unsigned int runs[3] = {0, 0, 0};
     RT_CUDA(cudaMemcpy(runs, h->d_runs, sizeof(runs), cudaMemcpyDeviceToHost));
     RT_CUDA(cudaMemset(h->d_runs, 0, sizeof(runs)));
-    const char* rn[2] = {"h16_ran", "tf32_twin_ran"};
-    for (int k = 0; k < 2; ++k) {
+    const char* rn[3] = {"h16_ran", "tf32_twin_ran", "jacobi_sweeps"};
+    for (int k = 0; k < 3; ++k) {
       if (runs[k] == 0 || cnt >= cap) continue;
       std::memset(out[cnt].name, 0, sizeof(out[cnt].name));
       std::strncpy(out[cnt].name, rn[k], sizeof(out[cnt].name) - 1);

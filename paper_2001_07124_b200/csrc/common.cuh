@@ -118,7 +118,8 @@ struct Ctx {
   int overlap = 1;              // HOSVD: thin QRs on the side stream (ablation 270 / 271 toggle)
   int sm_reserve = 0;           // SMs the persistent X-pass grids leave free (set while side work is pending)
   unsigned int* d_runs = nullptr;  // device counters: [0] fp16-split X passes that did their work,
-                                   // [1] tf32 twins that ran in their place (R29; rt_profile_read)
+                                   // [1] tf32 twins that ran in their place (R29; rt_profile_read),
+                                   // [2] Jacobi sweeps run (all matrices)
 };
 
 // Launch a kernel (given as a lambda issuing <<<...>>> on ctx.stream) with optional

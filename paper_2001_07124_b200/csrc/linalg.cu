@@ -390,6 +390,7 @@ struct EigBatch {
   double* W[8];
   double* V[8];
   int k[8];
+  unsigned int* sweeps;   // nullable: device counter of the sweeps run (rt_profile_read "jacobi_sweeps")
 };
 
 __global__ void __launch_bounds__(512) jacobi_kernel(EigBatch bt, double* Vscratch, int v_in_smem, int64_t stride_scr) {
@@ -403,6 +404,7 @@ __global__ void __launch_bounds__(512) jacobi_kernel(EigBatch bt, double* Vscrat
   double* cs = (v_in_smem ? sm + 2 * kk * ld : sm + kk * ld);   // kk/2 pairs: c, s, p, q
   __shared__ double red[32];
   __shared__ int s_done, s_rot;
+  __shared__ double s_fro2;
   const double* Ab = bt.A[blockIdx.x];
   double* W = bt.W[blockIdx.x];
   double* Vout = bt.V[blockIdx.x];
@@ -429,9 +431,14 @@ __global__ void __launch_bounds__(512) jacobi_kernel(EigBatch bt, double* Vscrat
     // shuffle rounding noise
     const double tol = double(k) * 1.1102230246251565e-16;
     // converged: off-diagonal norm below tolerance, or the previous sweep rotated no pair
-    if (t == 0) { s_done = (off <= tol * tol * dia) || (dia == 0.0) || (sweep > 0 && !s_rot); s_rot = 0; }
+    if (t == 0) {
+      s_done = (off <= tol * tol * dia) || (dia == 0.0) || (sweep > 0 && !s_rot);
+      s_rot = 0;
+      s_fro2 = off + dia;                              // ||A||_F^2 (invariant under the rotations)
+    }
     __syncthreads();
     if (s_done) break;
+    if (t == 0 && bt.sweeps) atomicAdd(bt.sweeps, 1u);
     for (int round = 0; round < kk - 1; ++round) {
       for (int pi = t; pi < npairs; pi += nt) {
         int p, q;
@@ -446,10 +453,19 @@ __global__ void __launch_bounds__(512) jacobi_kernel(EigBatch bt, double* Vscrat
         // threshold Jacobi: a pair whose |a_pq| is below k u sqrt(|a_pp a_qq|) is skipped (its rotation
         // would move the diagonal by less than the convergence tolerance): the late sweeps skip most
         // pairs and their row / column updates
-        if (fabs(apq) > double(k) * 1.1102230246251565e-16 * sqrt(fabs(A[p * ld + p] * A[q * ld + q]))) {
-          const double tau = (A[q * ld + q] - A[p * ld + p]) / (2.0 * apq);
-          const double tt = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-          c = 1.0 / sqrt(1.0 + tt * tt);
+        // (the test squared: no square root), or below the rounding level u ||A||_F of the matrix: a
+        // pair of a large and a tiny eigenvalue (cfg5's Gram spans 6e7) keeps an off-diagonal entry
+        // of the size of the large one's rounding error, which no rotation removes -- without this
+        // bound every sweep rotated such pairs again and the loop ran to its 40-sweep cap
+        const double app = A[p * ld + p], aqq = A[q * ld + q];
+        const double thr = double(k) * 1.1102230246251565e-16;
+        if (apq * apq > thr * thr * fabs(app * aqq) + 1.232595164407831e-32 * s_fro2) {
+          // t = sign(tau) / (|tau| + sqrt(1 + tau^2)) with tau = d / (2 a_pq), d = a_qq - a_pp, multiplied
+          // through by 2 |a_pq| (one square root, one division and one reciprocal square root on the
+          // round's critical path instead of two of each)
+          const double d = aqq - app;
+          const double tt = (d >= 0.0 ? 2.0 : -2.0) * apq / (fabs(d) + sqrt(d * d + 4.0 * apq * apq));
+          c = rsqrt(1.0 + tt * tt);
           s = tt * c;
         }
         if (s != 0.0) s_rot = 1;                      // benign race: every writer stores 1
@@ -995,6 +1011,7 @@ void eig_sym_batch(const Ctx& ctx, Arena& ws, int count, const double* const* A,
   for (int i = 0; i < count; ++i) {
     RT_REQUIRE(k[i] >= 1 && k[i] <= 128, kEUNSUPPORTED, "eig_sym: k must be in [1,128]");
     bt.A[i] = A[i]; bt.W[i] = W[i]; bt.V[i] = V[i]; bt.k[i] = k[i];
+    bt.sweeps = ctx.d_runs ? ctx.d_runs + 2 : nullptr;
     kmax = std::max(kmax, k[i]);
   }
   const int kk = kmax + (kmax & 1), ld = kk + 1;

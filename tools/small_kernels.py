@@ -21,7 +21,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--dims", type=int, nargs=3, default=[512, 512, 512])
 ap.add_argument("--reps", type=int, default=3)
 a = ap.parse_args()
-CLASSES = ("jacobi_eig", "chol_inv", "gram", "gemm_tall", "zsample", "unmix_cols", "splitk_reduce")
+CLASSES = ("jacobi_sweeps", "jacobi_eig", "chol_inv", "gram", "gemm_tall", "zsample", "unmix_cols", "splitk_reduce")
 
 
 def show(tag, prof, reps):
