@@ -142,11 +142,16 @@ def main():
                       flush=True)
             res_ms = sum(t for n, _, t in prof if n in bench.RESIDUAL_LABELS)
             pipe_ms = max(1e-6, ms - res_ms)
+            # a fused pass reads X once for two contractions (DESIGN.md §6f / §6g): one |X| less each
+            names = {n for n, _, _ in prof}
+            nfused = sum(1 for f in ("sketch1_core0", "sketch1_z0", "sketch2_core0") if f in names)
+            if algo == "hosvd":
+                nbytes -= nfused * cfg.nbytes
             gbs = nbytes / (pipe_ms * 1e-3) / 1e9
             line = {"config": name, "op": label, "dims": list(cfg.dims), "dtype": cfg.dtype, "ranks": list(cfg.ranks),
                     "p": cfg.p, "q": cfg.q, "ms": ms, "residual_ms": res_ms, "pipeline_ms": pipe_ms,
                     "x_GB": cfg.nbytes / 1e9, "x_GBps": cfg.nbytes / (ms * 1e-3) / 1e9,
-                    "bytes_model_GB": nbytes / 1e9,
+                    "bytes_model_GB": nbytes / 1e9, "fused_passes": nfused,
                     "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak},
                     "rel_err": float(res["err"][0]),
                     "cpu_baseline": oracle_time(cfg, algo, a.oracle_elems)}
