@@ -109,7 +109,9 @@ int tc_split_width(int K);
 bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
               int64_t so_a, int64_t so_c, int64_t so_b, int split_out = 0, bool q_tf32_exact = false,
               const float* xscale = nullptr, const float* run_if_zero = nullptr, const float* oscale = nullptr,
-              float omul = 1.f, bool no_twin = false);
+              float omul = 1.f, bool no_twin = false, int cw = 0);
+// cw > 0 with C > cw: the C columns in chunks of cw (a multiple of 32, <= 128) within one launch,
+// every chunk re-reading the (small) source from L2 (3xTF32 form only; false otherwise)
 // oscale (nullable): device scale multiplied into every output (the power iteration's Z = sn X^T Q);
 // omul: a host power-of-two factor as well; no_twin (with xscale): launch the fp16-split kernel only
 // (the caller launches its tf32 twin itself, e.g. with another output format)

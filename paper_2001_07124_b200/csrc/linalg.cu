@@ -1119,8 +1119,36 @@ void reduce_pairs(const Ctx& ctx, const double* part, int n, double* out2) {
   launch(ctx, "reduce_pairs", [&] { reduce_pairs_kernel<<<1, 256, 0, ctx.stream>>>(part, n, out2); });
 }
 
-void sumsq(const Ctx& ctx, Arena&, const double* x, int64_t n, double* out) {
-  launch(ctx, "sumsq", [&] { sumsq_kernel<<<1, 512, 0, ctx.stream>>>(x, n, out); });
+// per-CTA partial sums of squares over a fixed strided assignment (then one fixed-order CTA)
+__global__ void sumsq_part_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ part) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    s = fma(x[i], x[i], s);
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+__global__ void sum_parts_kernel(const double* __restrict__ part, int n, double* __restrict__ out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += part[i];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) *out = s;
+}
+void sumsq(const Ctx& ctx, Arena& ws, const double* x, int64_t n, double* out) {
+  // one CTA below 64K elements; above, up to 2 CTAs per SM and a fixed-order sum of their partials
+  const int nb = int(std::max<int64_t>(1, std::min<int64_t>(int64_t(2) * ctx.num_sms, cdiv(n, int64_t(1) << 16))));
+  if (nb == 1) {
+    launch(ctx, "sumsq", [&] { sumsq_kernel<<<1, 512, 0, ctx.stream>>>(x, n, out); });
+    return;
+  }
+  const auto mk = ws.mark();
+  double* part = ws.alloc_n<double>(nb);
+  launch(ctx, "sumsq", [&] {
+    sumsq_part_kernel<<<nb, 512, 0, ctx.stream>>>(x, n, part);
+    sum_parts_kernel<<<1, 512, 0, ctx.stream>>>(part, nb, out);
+  });
+  ws.rewind(mk);
 }
 
 void finalize_err(const Ctx& ctx, const double* sums, const double* gg, double* E, double* Eg, const float* rscale) {

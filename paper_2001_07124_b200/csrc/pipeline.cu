@@ -55,8 +55,13 @@ void ttm_t_dispatch(const Ctx& ctx, Arena& ws, const float* X, Box box, const fl
     if (C <= 128) {
       if (ttm_t_tc(ctx, ws, X, box, Q, ldq, C, out, so_a, so_c, so_b, 0, q_tf32_exact, xscale, nullptr, oscale)) return;
     } else {
-      // wider than one TMEM tile (e.g. the R-PET core sketch, S_n = 2K_n + 1): balanced column
-      // chunks of <= 128, one X pass each, each writing its slice of the output
+      // wider than one TMEM tile (the residual's P chain: C = I_n; the R-PET core sketch, S_n = 2K_n + 1):
+      // column chunks of 128 in one launch (every chunk re-reads the small source from L2)
+      if (!xscale && !q_tf32_exact &&
+          ttm_t_tc(ctx, ws, X, box, Q, ldq, C, out, so_a, so_c, so_b, 0, false, nullptr, nullptr, oscale, 1.f, false,
+                   128))
+        return;
+      // otherwise balanced chunks of <= 128, one launch each, each writing its slice of the output
       const int nch = int(cdiv(C, 128));
       const int cw = int(cdiv(C, nch) + 3) & ~3;
       if (ttm_t_tc(ctx, ws, X, box, Q, ldq, cw, out, so_a, so_c, so_b, 0, q_tf32_exact, xscale)) {

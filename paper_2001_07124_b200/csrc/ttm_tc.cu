@@ -886,6 +886,8 @@ struct TParams {
   unsigned int* runs;    // optional run counters (see SParams)
   const float* oscale;   // optional device scale of the output (the power iteration's Z = sn X^T Q)
   float omul;            // host power-of-two factor of the output (1 = none)
+  int nch = 1;           // column chunks of cw <= NPAD columns (C = the total width); chunk ch's
+  int cw = 0;            //   pre-split B rows start at row 2 NPAD ch of the B map
 };
 
 // AKM: mode 0 (a == 1), X tile K-major [BM j][KC i].  BSPLIT: Q = Q_hi + Q_lo pre-split (an fp64
@@ -910,7 +912,10 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
   extern __shared__ __align__(1024) uint8_t smem[];
   const Bars b = bars_of<L>(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t my_tiles = (p.ntiles > blockIdx.x) ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  // work items: (column chunk, row tile) pairs, chunk-major (p.nch > 1: columns wider than one TMEM
+  // tile, every chunk re-reading the small source from L2)
+  const int64_t nitems = p.ntiles * p.nch;
+  const int64_t my_tiles = (nitems > blockIdx.x) ? (nitems - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
   if (threadIdx.x == 0) {
     init_bars<L>(b);
@@ -935,7 +940,7 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
       int it = 0;
       for (int64_t u = 0; u < my_tiles; ++u) {
         int64_t a0, beta;
-        tile_coords(blockIdx.x + u * gridDim.x, a0, beta);
+        tile_coords((blockIdx.x + u * gridDim.x) % p.ntiles, a0, beta);
         for (int c = 0; c < p.nic; ++c, ++it, rx.next<NX>()) {
           if (it >= NX) mbar_wait(&b.x_free[rx.s], rx.ph ^ 1);
           mbar_expect_tx(&b.x_full[rx.s], L::kX);
@@ -950,7 +955,8 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
       Ring rb;
       const uint64_t pol = policy_evict_last();
       int it = 0;
-      for (int64_t u = 0; u < my_tiles; ++u)
+      for (int64_t u = 0; u < my_tiles; ++u) {
+        const int chunk = int((blockIdx.x + u * gridDim.x) / p.ntiles);
         for (int c = 0; c < p.nic; ++c, ++it, rb.next<L::NBS>()) {
           if (it >= L::NBS) mbar_wait(&b.b_free[rb.s], rb.ph ^ 1);
           mbar_expect_tx(&b.b_full[rb.s], L::kBS);
@@ -959,9 +965,10 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
             for (int x = 0; x < L::NBX; ++x)
               tma_load_2d_hint(smem + L::off_b + rb.s * L::kBS + x * 4096, &tmb, &b.b_full[rb.s], 64 * x, c * KC, pol);
           } else {
-            tma_load_2d_hint(smem + L::off_b + rb.s * L::kBS, &tmb, &b.b_full[rb.s], c * KC, 0, pol);
+            tma_load_2d_hint(smem + L::off_b + rb.s * L::kBS, &tmb, &b.b_full[rb.s], c * KC, chunk * 2 * NPAD, pol);
           }
         }
+      }
     }
   } else if (warp == 1 || warp == 7) {
     const int q = warp == 1 ? 0 : 1;
@@ -1031,7 +1038,10 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
     const bool rescale = H16 || p.oscale != nullptr || p.omul != 1.f;
     int64_t g = 0;
     for (int64_t u = 0; u < my_tiles; ++u) {
-      const int64_t tile = blockIdx.x + u * gridDim.x;
+      const int64_t item = blockIdx.x + u * gridDim.x;
+      const int64_t tile = item % p.ntiles;
+      const int cc0 = int(item / p.ntiles) * p.cw;                 // this chunk's first output column
+      const int Cc = min(p.C - cc0, p.cw);                         // and its width
       for (int sgi = 0; sgi < segs_per_tile; ++sgi, ++g) {
         if constexpr (H16) {
           mbar_wait(&b.acc_full[0], uint32_t(g) & 1u);
@@ -1055,6 +1065,7 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
       int64_t ob;
       if (AKM) { const int64_t j = beta + r; valid = j < p.b; ob = j * p.so_b; }
       else { const int64_t al = a0 + r; valid = al < p.a; ob = al * p.so_a + beta * p.so_b; }
+      ob += int64_t(cc0) * p.so_c;
       if (p.tma_out) {
         constexpr int NBX = (NPAD + 31) / 32;
         uint8_t* stage = smem + L::off_o;
@@ -1069,7 +1080,7 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int c0 = 8 * k + 2 * e, c1 = c0 + 1;
-              split_h16x2(c0 < p.C ? sums[c0] * kQScale : 0.f, c1 < p.C ? sums[c1] * kQScale : 0.f, h[e], l[e]);
+              split_h16x2(c0 < Cc ? sums[c0] * kQScale : 0.f, c1 < Cc ? sums[c1] * kQScale : 0.f, h[e], l[e]);
             }
             const int eh = 8 * k, el = NPAD + 8 * k;
             *reinterpret_cast<uint4*>(stage + (eh >> 6) * (BM * 128) + r * 128 + ((((eh & 63) >> 3) ^ (r & 7)) << 4)) =
@@ -1097,8 +1108,8 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
           for (int bx = 0; bx < NBX; ++bx) {
             if (p.split_out == 2) {
               if (64 * bx < 2 * NPAD) tma_store_2d(&tmo, stage + bx * (BM * 128), 64 * bx, row0);
-            } else if (32 * bx < p.C) {
-              tma_store_2d(&tmo, stage + bx * (BM * 128), 32 * bx, row0);
+            } else if (32 * bx < Cc) {
+              tma_store_2d(&tmo, stage + bx * (BM * 128), cc0 + 32 * bx, row0);
             }
           }
           bulk_commit();
@@ -1113,7 +1124,7 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int c0 = 8 * k + 2 * e, c1 = c0 + 1;
-              split_h16x2(c0 < p.C ? sums[c0] * kQScale : 0.f, c1 < p.C ? sums[c1] * kQScale : 0.f, h[e], l[e]);
+              split_h16x2(c0 < Cc ? sums[c0] * kQScale : 0.f, c1 < Cc ? sums[c1] * kQScale : 0.f, h[e], l[e]);
             }
             oh[k] = make_uint4(h[0], h[1], h[2], h[3]);
             ol[k] = make_uint4(l[0], l[1], l[2], l[3]);
@@ -1126,7 +1137,7 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
           for (int k = 0; k < NHO / 4; ++k) {
             uint32_t h[4], l[4];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) split_tf32((4 * k + e < NPAD && 4 * k + e < p.C) ? sums[(4 * k + e) % NPAD] : 0.f,
+            for (int e = 0; e < 4; ++e) split_tf32((4 * k + e < NPAD && 4 * k + e < Cc) ? sums[(4 * k + e) % NPAD] : 0.f,
                                                    h[e], l[e]);
             oh[k] = make_float4(__uint_as_float(h[0]), __uint_as_float(h[1]), __uint_as_float(h[2]), __uint_as_float(h[3]));
             ol[k] = make_float4(__uint_as_float(l[0]), __uint_as_float(l[1]), __uint_as_float(l[2]), __uint_as_float(l[3]));
@@ -1135,11 +1146,11 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
           float4* o4 = reinterpret_cast<float4*>(p.out + ob);
 #pragma unroll
           for (int k = 0; k < NPAD / 4; ++k)
-            if (4 * k < p.C) o4[k] = make_float4(sums[4 * k], sums[4 * k + 1], sums[4 * k + 2], sums[4 * k + 3]);
+            if (4 * k < Cc) o4[k] = make_float4(sums[4 * k], sums[4 * k + 1], sums[4 * k + 2], sums[4 * k + 3]);
         } else {
 #pragma unroll
           for (int k = 0; k < NPAD; ++k)
-            if (k < p.C) p.out[ob + int64_t(k) * p.so_c] = sums[k];
+            if (k < Cc) p.out[ob + int64_t(k) * p.so_c] = sums[k];
         }
       }
 #pragma unroll
@@ -1654,13 +1665,16 @@ __global__ void __launch_bounds__(256) splitk_reduce_f32_kernel(const float* __r
 
 // Q (I x C, col-major ldq) -> Q2 (I x 2 npad, col-major ld2): columns [0, C) = tf32 hi, columns
 // [npad, npad + C) = lo, the rest zero (the pre-split [B_hi | B_lo] operand of ttm_t_tc)
+// chunk blockIdx.y: columns [cw y, cw y + cw) of Q into rows [2 npad y, 2 npad (y + 1)) of Q2
 __global__ void split_q_kernel(const float* __restrict__ Q, int64_t I, int C, int64_t ldq, int npad,
-                               float* __restrict__ Q2, int64_t ld2) {
+                               float* __restrict__ Q2, int64_t ld2, int cw) {
   const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (e >= ld2 * npad) return;
   const int64_t i = e % ld2;
   const int c = int(e / ld2);
-  const float v = (i < I && c < C) ? Q[i + ldq * c] : 0.f;
+  const int cg = int(blockIdx.y) * cw + c;
+  Q2 += int64_t(blockIdx.y) * 2 * npad * ld2;
+  const float v = (i < I && c < cw && cg < C) ? Q[i + ldq * cg] : 0.f;
   uint32_t h, l;
   split_tf32(v, h, l);
   Q2[i + ld2 * c] = __uint_as_float(h);
@@ -1986,9 +2000,13 @@ bool ttm_s_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* B
 
 bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q, int64_t ldq, int C, float* out,
               int64_t so_a, int64_t so_c, int64_t so_b, int split_out, bool q_tf32_exact, const float* xscale,
-              const float* run_if_zero, const float* oscale, float omul, bool no_twin) {
-  const int npad = tc_npad(C);
+              const float* run_if_zero, const float* oscale, float omul, bool no_twin, int cw) {
+  // cw > 0: C columns in chunks of cw (<= 128) within one launch (3xTF32 form only)
+  const int nch = (cw > 0 && C > cw) ? int(cdiv(C, cw)) : 1;
+  if (nch == 1) cw = C;
+  const int npad = tc_npad(cw);
   if (npad < 0) return false;
+  if (nch > 1 && (xscale != nullptr || split_out || q_tf32_exact)) return false;
   const bool h16 = xscale != nullptr && !q_tf32_exact;
   const bool akm = (box.a == 1);
   if (!aligned(X, 16)) return false;
@@ -2005,7 +2023,7 @@ bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q
     const uint32_t bx[3] = {BM, KC, 1};
     if (!make_map(&tx, X, 3, d, s, bx, false)) return false;
   }
-  const bool bsplit = !q_tf32_exact || !aligned(Q, 16) || (ldq % 4) != 0;
+  const bool bsplit = !q_tf32_exact || !aligned(Q, 16) || (ldq % 4) != 0 || nch > 1;
   CUtensorMap tbh;   // fp16 [2^14 Q_hi | 2^14 Q_lo] operand of the H16 kernel (with h16)
   if (h16) {
     // fp16 rows (I x 2 npad halves): (64 cols, 32 rows) SWIZZLE_128B boxes
@@ -2021,10 +2039,11 @@ bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q
     // pre-split [Q_hi | Q_lo] (I x 2 npad): the kernel loads it as one [2 npad][32] K-major slot
     // (with h16 this is the operand of the tf32 twin that runs instead when s == 0, R29)
     const int64_t ld2 = (box.I + 3) & ~int64_t(3);
-    float* Q2 = ws.alloc_n<float>(ld2 * 2 * npad);
-    if (!make_b_map(&tb, Q2, box.I, 2 * npad, ld2, 2 * npad)) return false;
+    float* Q2 = ws.alloc_n<float>(ld2 * 2 * npad * nch);
+    if (!make_b_map(&tb, Q2, box.I, 2 * npad * nch, ld2, 2 * npad)) return false;
     launch(ctx, "split_q", [&] {
-      split_q_kernel<<<unsigned(cdiv(ld2 * npad, 256)), 256, 0, ctx.stream>>>(Q, box.I, C, ldq, npad, Q2, ld2);
+      split_q_kernel<<<dim3(unsigned(cdiv(ld2 * npad, 256)), unsigned(nch)), 256, 0, ctx.stream>>>(Q, box.I, C, ldq,
+                                                                                                  npad, Q2, ld2, cw);
     });
   } else {
     // tf32-exact Q read in place as a [npad][32] K-major slot (columns >= C read as zero)
@@ -2032,6 +2051,7 @@ bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q
   }
   TParams p;
   p.a = box.a; p.I = box.I; p.b = box.b; p.C = C;
+  p.nch = nch; p.cw = cw;
   p.tpb = akm ? 1 : cdiv(box.a, BM);
   p.ntiles = akm ? cdiv(box.b, BM) : p.tpb * box.b;
   p.nic = int(cdiv(box.I, KC));
@@ -2075,7 +2095,7 @@ bool ttm_t_tc(const Ctx& ctx, Arena& ws, const float* X, Box box, const float* Q
       p.tma_out = make_map(&to, out, 2, d, st, bx, true, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
     }
   }
-  const int64_t grid = std::min<int64_t>(p.ntiles, std::max(1, ctx.num_sms - ctx.sm_reserve));
+  const int64_t grid = std::min<int64_t>(p.ntiles * nch, std::max(1, ctx.num_sms - ctx.sm_reserve));
 #define RT_T_CASE(NP)                                                     \
   case NP:                                                                \
     if (h16) {                                                           \
