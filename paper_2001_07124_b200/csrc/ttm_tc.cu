@@ -1172,10 +1172,11 @@ ttm_t_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__
 // (the core contracts mode 0 first, Eq. Core; the sketch is Alg.6 line 3 P:556 for n = 1).
 // X is split once per chunk into fp16 hi/lo A operands in TMEM (R29); B is one K-major 128 B-swizzled
 // slot per chunk pair holding [2^14 Q_hi^T | 2^11 Omega^T | 2^14 Q_lo^T] (3 NPAD rows x 64 K):
-//   issuer 0: A_hi [Q_hi | Omega | Q_lo] -> TMEM [C0 | S0 | C1a]   (N = 3 NPAD)
-//   issuer 1: A_lo [Q_hi | Omega]        -> TMEM [C1b | S1]        (N = 2 NPAD)
+//   issuer 0: A_hi [Q_hi | Omega] -> TMEM [C0 | S0]                       (N = 2 NPAD)
+//   issuer 1: A_lo [Q_hi | Omega] -> TMEM [C1 | S1], then A_hi Q_lo -> C1  (N = 2 NPAD, NPAD)
+// (the two corrections of the core share C1: 4 NPAD accumulator columns leave room for 4 A slots)
 // with Omega tf32-exact (RT_OPT_OMEGA_TF32: exact in fp16 at 2^11, no Omega_lo).  The sketch sums S0 + S1
-// over the whole chunk range of the CTA (split-K partials, as ttm_s); the core rows C0 + C1a + C1b
+// over the whole chunk range of the CTA (split-K partials, as ttm_s); the core rows C0 + C1
 // are complete after the cpb chunks of one beta and leave through TMA stores.
 struct FParams {
   int64_t a, I, b;
@@ -1199,9 +1200,11 @@ struct FParams {
 
 template <int NPAD, int NBB_ = 2>
 struct PlanF {
-  static constexpr int XW = 2, NB = 3, NBB = NBB_;
-  static constexpr uint32_t c0 = 0, s0 = NPAD, c1a = 2 * NPAD, c1b = 3 * NPAD, s1 = 4 * NPAD;
-  static constexpr uint32_t a_base = (5u * NPAD + 31u) & ~31u;
+  // TMEM: [C0 | S0] (issuer 0: A_hi [Q_hi | Omega]) and [C1 | S1] (issuer 1: A_lo [Q_hi | Omega], then
+  // A_hi Q_lo into C1), then NB A slots of 32 columns (hi 16 | lo 16)
+  static constexpr int XW = 2, NB = 4, NBB = NBB_;
+  static constexpr uint32_t c0 = 0, s0 = NPAD, c1 = 2 * NPAD, s1 = 3 * NPAD;
+  static constexpr uint32_t a_base = (4u * NPAD + 31u) & ~31u;
   static_assert(a_base + 32u * NB <= 512u, "fused TMEM plan");
   __host__ __device__ static constexpr uint32_t a_slot(int s) { return a_base + 32u * uint32_t(s); }
   static constexpr uint32_t kX = uint32_t(BM) * x_pitch<XW>();
@@ -1293,8 +1296,9 @@ sketch1_core0_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_const
     }
   } else if (warp == 1 || warp == 7) {
     const int q = warp == 1 ? 0 : 1;                   // ---------------- MMA issuers (whole warp)
-    const uint32_t idesc = idesc_f16(BM, q == 0 ? 3 * NPAD : 2 * NPAD, 0);
-    const uint32_t d = tmem + (q == 0 ? L::c0 : L::c1b);
+    const uint32_t idesc = idesc_f16(BM, 2 * NPAD, 0);
+    const uint32_t idesc_c = idesc_f16(BM, NPAD, 0);
+    const uint32_t d = tmem + (q == 0 ? L::c0 : L::c1);
     int64_t u = 0;
     int pos = 0;
     for (int it = 0; it < nch; ++it) {
@@ -1307,8 +1311,12 @@ sketch1_core0_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_const
       const uint32_t bsa = smem_u32(smem + L::off_b + ((it / 2) % NBB) * L::kB);
       const uint32_t a = tmem + L::a_slot(sl) + (q == 0 ? 0u : 16u);
 #pragma unroll
-      for (int kk = 0; kk < KC / 16; ++kk)
+      for (int kk = 0; kk < KC / 16; ++kk) {
         mma_f16_ts_w(d, a + 8 * kk, bdesc_sw128(bsa, 2 * (it & 1) + kk), idesc, (first && kk == 0) ? 0u : 1u);
+        if (q == 1)                                    // A_hi Q_lo (B rows 2 NPAD..) into C1, after A_lo Q_hi
+          mma_f16_ts_w(tmem + L::c1, tmem + L::a_slot(sl) + 8 * kk,
+                       bdesc_sw128(bsa + 2u * NPAD * 128u, 2 * (it & 1) + kk), idesc_c, 1u);
+      }
       mma_commit_w(&tfree[sl]);
       if (it & 1) mma_commit_w(&b_free[(it / 2) % NBB]);
       if (last) { mma_commit_w(acc_full); ++u; pos = 0; } else { ++pos; }
@@ -1363,7 +1371,7 @@ sketch1_core0_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_const
         if (k < p.K) dst[int64_t(k) * p.I + i] = sums[k] * inv_s;
     }
   } else if (warp >= 12) {                             // ---------------- epilogue C: the left output rows
-    // C0 + C1a + C1b of each segment are read out of TMEM 8 columns at a time into the row's fp32
+    // C0 + C1 of each segment are read out of TMEM 16 columns at a time into the row's fp32
     // sums (registers, one row per thread), the accumulator is released, and after the cpb chunks of a
     // beta the finished row leaves straight from the registers (no shared-memory staging: the X ring
     // gets that space)
@@ -1384,15 +1392,13 @@ sketch1_core0_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_const
       mbar_wait(acc_full, uint32_t(u) & 1u);
       tc_fence_after();
 #pragma unroll
-      for (int c0 = 0; c0 < NPAD; c0 += 8) {
-        uint32_t v0[8], v1[8], v2[8];
-        tmem_ld8(lane_base + L::c0 + c0, v0);
-        tmem_ld8(lane_base + L::c1a + c0, v1);
-        tmem_ld8(lane_base + L::c1b + c0, v2);
+      for (int c0 = 0; c0 < NPAD; c0 += 16) {
+        uint32_t v0[16], v1[16];
+        tmem_ld16(lane_base + L::c0 + c0, v0);
+        tmem_ld16(lane_base + L::c1 + c0, v1);
         tmem_wait_ld();
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          cs[c0 + k] += __uint_as_float(v0[k]) + (__uint_as_float(v1[k]) + __uint_as_float(v2[k]));
+        for (int k = 0; k < 16; ++k) cs[c0 + k] += __uint_as_float(v0[k]) + __uint_as_float(v1[k]);
       }
       tc_fence_before();
       mbar_arrive(acc_empty);
