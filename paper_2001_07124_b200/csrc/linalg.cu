@@ -319,6 +319,93 @@ __global__ void __launch_bounds__(256) chol_inv_blk_kernel(const double* __restr
   }
 }
 
+
+// One barrier per column (reading R5's CholeskyQR, latency-bound at k <= 128):
+//   Cholesky, right-looking: at column j every thread takes d = a_jj itself and applies the rank-1
+//   update a_ik -= a_ij a_kj / d to its share of the trailing lower triangle, reading column j,
+//   which no thread writes during the step; the scaled column L_ij = a_ij / sqrt(d) goes to L.
+//   Inverse: L = L1 D with L1 unit lower triangular (L1_ij = L_ij / L_jj); W1 = L1^{-1} by
+//   forward substitution without divisions (step j reads row j, which is final, and updates rows
+//   > j), then L^{-1} = D^{-1} W1 (row i divided by L_ii).
+__global__ void __launch_bounds__(256) chol_inv_fast_kernel(const double* __restrict__ G, int k, double shift_coef,
+                                                            double* __restrict__ R, double* __restrict__ Rinv,
+                                                            int* zero_flag, int* status, const double* shift_dev) {
+  extern __shared__ double sm[];
+  const int ld = k + 1;
+  double* A = sm;                          // k x ld: the working matrix, then L (lower)
+  double* W = sm + size_t(k) * ld;         // k x ld: W1, then L^{-1} (lower)
+  double* dg = W + size_t(k) * ld;         // k: sqrt pivots
+  __shared__ double red[32];
+  __shared__ double s_shift, s_tr;
+  __shared__ int s_bad;
+  const int t = threadIdx.x, nt = blockDim.x;
+  double tr = 0.0;
+  for (int i = t; i < k; i += nt) tr += G[i + int64_t(k) * i];
+  tr = block_sum(tr, red);
+  if (t == 0) {
+    s_tr = tr;
+    s_shift = (shift_dev ? *shift_dev : shift_coef) * tr;
+    s_bad = 0;
+    if (!(tr == tr) || tr > DBL_MAX) latch(status, kStatusNonFinite);
+    if (zero_flag) *zero_flag = (tr == 0.0) ? 1 : 0;
+  }
+  __syncthreads();
+  const bool is_zero = (s_tr == 0.0);
+  for (int e = t; e < k * k; e += nt) {
+    const int i = e / k, c = e % k;
+    A[i * ld + c] = (c <= i) ? G[i + int64_t(k) * c] + (i == c ? s_shift : 0.0) : 0.0;
+    W[i * ld + c] = (i == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  if (!is_zero) {
+    for (int j = 0; j < k; ++j) {
+      double d = A[j * ld + j];
+      const bool bad = !(d > 0.0);
+      if (bad) d = 1.0;
+      const double rd = 1.0 / d;
+      if (t == 0) { dg[j] = sqrt(d); if (bad) s_bad = 1; }
+      // trailing update of the lower triangle (i >= c > j)
+      const int m = k - 1 - j;                         // trailing size
+      for (int e = t; e < m * m; e += nt) {
+        const int i = e / m, c = e - i * m;
+        if (c > i) continue;                           // 0 <= c <= i < m
+        const int ii = j + 1 + i, cc = j + 1 + c;
+        A[ii * ld + cc] -= A[ii * ld + j] * A[cc * ld + j] * rd;
+      }
+      __syncthreads();
+    }
+    // L = column j scaled by 1 / sqrt(a_jj) (in place: column j is no longer read)
+    for (int e = t; e < k * k; e += nt) {
+      const int i = e / k, c = e % k;
+      if (c < i) A[i * ld + c] /= dg[c];
+      else if (c == i) A[i * ld + c] = dg[c];
+    }
+    __syncthreads();
+    // W1 = L1^{-1}, L1_ij = L_ij / L_jj
+    for (int j = 0; j < k - 1; ++j) {
+      const int m = k - 1 - j;                         // rows j+1 .. k-1, columns 0 .. j
+      const double rl = 1.0 / dg[j];
+      for (int e = t; e < m * (j + 1); e += nt) {
+        const int i = j + 1 + e / (j + 1), c = e % (j + 1);
+        W[i * ld + c] -= A[i * ld + j] * rl * W[j * ld + c];
+      }
+      __syncthreads();
+    }
+  }
+  if (t == 0 && s_bad) latch(status, kStatusCholBreakdown);
+  // R = L^T (upper), Rinv = (D^{-1} W1)^T; col-major k x k
+  for (int e = t; e < k * k; e += nt) {
+    const int r = e % k, c = e / k;
+    if (is_zero) {
+      if (R) R[e] = 0.0;
+      Rinv[e] = 0.0;
+    } else {
+      if (R) R[e] = (r <= c) ? A[c * ld + r] : 0.0;
+      Rinv[e] = (r <= c) ? W[c * ld + r] / dg[c] : 0.0;
+    }
+  }
+}
+
 // --------------------------------------------------------------- tall GEMM
 // C(m x n) = A(m x k) B(k x n); 32 rows per CTA; B in shared memory; fp64 accumulation.
 template <typename TA, typename TC>
@@ -963,8 +1050,19 @@ void chol_inv(const Ctx& ctx, const double* G, int k, double shift_coef, double*
     RT_CUDA(cudaFuncSetAttribute(chol_inv_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     attr = true;
   }
+  const size_t smem_fast = sizeof(double) * (2 * size_t(k) * (k + 1) + size_t(k));
+  static bool attr_fast = false;
+  if (!attr_fast) {
+    RT_CUDA(cudaFuncSetAttribute(chol_inv_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    attr_fast = true;
+  }
   launch(ctx, "chol_inv", [&] {
-    if (smem_blk <= 220 * 1024 && !getenv("RT_CHOL_UNBLOCKED"))
+    // the one-barrier-per-column kernel wins at small k (tools/qr_time.py: 25 vs 29 us at k = 27;
+    // 84 vs 66 us at k = 60, where the blocked kernel's register-blocked panels pay off)
+    if (k <= 40 && smem_fast <= 220 * 1024 && !getenv("RT_CHOL_BLOCKED") && !getenv("RT_CHOL_UNBLOCKED"))
+      chol_inv_fast_kernel<<<1, 256, smem_fast, ctx.stream>>>(G, k, shift_coef, R, Rinv, zero_flag, ctx.d_status,
+                                                              shift_dev);
+    else if (smem_blk <= 220 * 1024 && !getenv("RT_CHOL_UNBLOCKED"))
       chol_inv_blk_kernel<<<1, 256, smem_blk, ctx.stream>>>(G, k, shift_coef, R, Rinv, zero_flag, ctx.d_status,
                                                             shift_dev);
     else
