@@ -1196,6 +1196,7 @@ struct FParams {
   float omul;            // zout: host power of two of Z (2^-(ceil(log2 sqrt I_0) + 1))
   void* out;             // the left output rows (fp32 core rows or fp16 Z rows)
   int64_t ldo;           // row pitch in elements (C floats / 2 NPAD halves)
+  int ablate;            // profiling only: 1 = no MMA, 2 = no split work (results invalid)
 };
 
 template <int NPAD, int NBB_ = 2>
@@ -1312,6 +1313,7 @@ sketch1_core0_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_const
       const uint32_t a = tmem + L::a_slot(sl) + (q == 0 ? 0u : 16u);
 #pragma unroll
       for (int kk = 0; kk < KC / 16; ++kk) {
+        if (p.ablate == 1) break;
         mma_f16_ts_w(d, a + 8 * kk, bdesc_sw128(bsa, 2 * (it & 1) + kk), idesc, (first && kk == 0) ? 0u : 1u);
         if (q == 1)                                    // A_hi Q_lo (B rows 2 NPAD..) into C1, after A_lo Q_hi
           mma_f16_ts_w(tmem + L::c1, tmem + L::a_slot(sl) + 8 * kk,
@@ -1332,7 +1334,7 @@ sketch1_core0_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_const
       if (cx == 0) mbar_wait(&x_full[rx.s], rx.ph);
       if (it >= NB) mbar_wait(&tfree[sl], (uint32_t(it / NB) & 1u) ^ 1u);   // the A slot's MMAs done
       const float* xs = reinterpret_cast<const float*>(smem + L::off_x + rx.s * L::kX);
-      split_wrow_to_tmem_h16(xs + r * (KC * XW + 4) + KC * cx, sc, lane_base + L::a_slot(sl));
+      if (p.ablate != 2) split_wrow_to_tmem_h16(xs + r * (KC * XW + 4) + KC * cx, sc, lane_base + L::a_slot(sl));
       if (cx == XW - 1 || it == nch - 1) { mbar_arrive(&x_free[rx.s]); rx.next<NX>(); }
       mbar_wait(&b_full[(it / 2) % NBB], uint32_t((it / 2) / NBB) & 1u);
       tmem_wait_st();
@@ -2229,6 +2231,7 @@ bool sketch1_core0(const Ctx& ctx, Arena& ws, const float* X, Box b1, Box b0, co
   p.binv_c = 1.f / kQScale;
   p.runs = ctx.d_runs;
   p.zout = zo ? 1 : 0;
+  p.ablate = ctx.tc_ablate;
   p.view_last = view_last;
   p.oscale = zo ? zo->oscale : nullptr;
   p.omul = zo ? zo->omul : 1.f;
