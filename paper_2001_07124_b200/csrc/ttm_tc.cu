@@ -627,18 +627,19 @@ __device__ __forceinline__ void split_row_to_tmem_h16(const float* xs, int r, fl
   float v[32];
   if (AMN) {
 #pragma unroll
-    for (int q = 0; q < 32; ++q) v[q] = xs[q * BM + r] * s;
+    for (int q = 0; q < 32; ++q) v[q] = xs[q * BM + r];
   } else {
     const float* row = xs + r * KC;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const float4 w = *reinterpret_cast<const float4*>(row + ((c ^ (r & 7)) << 2));
-      v[4 * c + 0] = w.x * s; v[4 * c + 1] = w.y * s; v[4 * c + 2] = w.z * s; v[4 * c + 3] = w.w * s;
+      v[4 * c + 0] = w.x; v[4 * c + 1] = w.y; v[4 * c + 2] = w.z; v[4 * c + 3] = w.w;
     }
   }
+  const uint64_t ss = pack_f32x2(s);
   uint32_t hi[16], lo[16];
 #pragma unroll
-  for (int c = 0; c < 16; ++c) split_h16x2(v[2 * c], v[2 * c + 1], hi[c], lo[c]);
+  for (int c = 0; c < 16; ++c) split_h16x2_s(v[2 * c], v[2 * c + 1], ss, hi[c], lo[c]);
   tmem_st16(t_hi, hi);
   tmem_st16(t_hi + 16, lo);
 }
@@ -648,11 +649,12 @@ __device__ __forceinline__ void split_wrow_to_tmem_h16(const float* row, float s
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
     const float4 w = *reinterpret_cast<const float4*>(row + 4 * c);
-    v[4 * c + 0] = w.x * s; v[4 * c + 1] = w.y * s; v[4 * c + 2] = w.z * s; v[4 * c + 3] = w.w * s;
+    v[4 * c + 0] = w.x; v[4 * c + 1] = w.y; v[4 * c + 2] = w.z; v[4 * c + 3] = w.w;
   }
+  const uint64_t ss = pack_f32x2(s);
   uint32_t hi[16], lo[16];
 #pragma unroll
-  for (int c = 0; c < 16; ++c) split_h16x2(v[2 * c], v[2 * c + 1], hi[c], lo[c]);
+  for (int c = 0; c < 16; ++c) split_h16x2_s(v[2 * c], v[2 * c + 1], ss, hi[c], lo[c]);
   tmem_st16(t_hi, hi);
   tmem_st16(t_hi + 16, lo);
 }
