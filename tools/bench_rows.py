@@ -105,7 +105,7 @@ def main():
           for d, r in zip(cfg.dims, cfg.ranks)]
     hs = [[torch.from_numpy(o).cuda() for o in sw] for sw in synth.hooi_omegas(cfg, 1)]
     emit("rp_hooi 1 sweep", timed(h, lambda: api.rtucker_rp_hooi(h, X, cfg.ranks, q0, hs), a.reps), N + 2,
-         {"note": "N fp64 S-chain passes + core + residual"}, hooi_cpu)
+         {"note": "N S-chain passes (first stage on the tensor cores, R30) + core + residual"}, hooi_cpu)
     h.close()
 
 
