@@ -410,21 +410,175 @@ ttm_t_dmma_kernel(const Tin* __restrict__ X, int64_t a, int64_t I, int64_t J, co
   }
 }
 
+// cp.async form of the fp64 warp-MMA TTM: the stages go global -> shared memory without registers,
+// NSTG deep (one barrier per stage), so the DMMA pipe is not idle while a stage is stored (the
+// register-prefetch kernel above ran the pipe at 50%: its store phase and second barrier were
+// serialized with the MMAs).  Same tile, fragments, fp64 products and sums (same results).
+__device__ __forceinline__ void cp_async4(void* dst, const void* src, bool valid) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(valid ? 4 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(valid ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <typename Tin, typename Tm, typename Tout, int NF, int NSTG, bool AT>
+__global__ void __launch_bounds__(256, 2)
+ttm_t_dmma_async_kernel(const Tin* __restrict__ X, int64_t a, int64_t I, int64_t J, const Tm* __restrict__ Mm,
+                        int64_t ms_i, int64_t ms_c, int C, Tout* __restrict__ out, int64_t so_a, int64_t so_c,
+                        int64_t so_b) {
+  // pitches for conflict-free fragment reads (lane = 4 fr + fk reads row fk, column fr): 32-bit rows at
+  // 8 mod 32 words, 64-bit rows at 4 mod 16 doubles (the 2-wavefront minimum)
+  // AT (a == 1, i contiguous in X): the X tile is kept as [j][i] rows (pitch BI + 4 / BI + 2), so the
+  // cp.async writes along i and the fragment reads (row j = fr, column i = fk) are conflict-free
+  constexpr int BM = 128, BN = 16 * NF, BI = sizeof(Tin) == 4 ? 32 : 16;
+  constexpr int PX = AT ? (sizeof(Tin) == 4 ? BI + 4 : BI + 2) : (sizeof(Tin) == 4 ? BM + 8 : BM + 4);
+  constexpr int PM = BN + (sizeof(Tm) == 4 ? 8 : 4);
+  constexpr int XS = (AT ? BM : BI) * PX, MS = BI * PM;           // elements per stage
+  extern __shared__ __align__(16) unsigned char dsm[];
+  Tin* Xs = reinterpret_cast<Tin*>(dsm);                         // [NSTG][BI][PX]
+  Tm* Ms = reinterpret_cast<Tm*>(dsm + sizeof(Tin) * NSTG * XS);  // [NSTG][BI][PM]
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int64_t j0 = int64_t(blockIdx.x) * BM;
+  const int c0 = blockIdx.y * BN;
+  const int64_t aI = a * I;
+  const int jw = 32 * (w & 3), cw = 8 * NF * (w >> 2);
+  const int fr = lane >> 2, fk = lane & 3;
+  double acc[4][NF][2];
+#pragma unroll
+  for (int m = 0; m < 4; ++m)
+#pragma unroll
+    for (int n = 0; n < NF; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+  // a > 1: thread column jl = t % BM (rows il = t / BM + 2 s); a == 1: row il = t % BI, columns t / BI + k
+  const int jl_b = t % BM;
+  const int64_t j_b = j0 + jl_b;
+  const bool jv_b = j_b < J;
+  const int64_t off_b = jv_b ? (j_b % a) + aI * (j_b / a) : 0;
+  auto issue = [&](int64_t ic, int slot) {
+    Tin* xs = Xs + slot * XS;
+    Tm* ms = Ms + slot * MS;
+    if (a == 1) {
+      const int il = t % BI;
+      const int64_t i = ic + il;
+#pragma unroll
+      for (int s2 = 0; s2 < BI * BM / 256; ++s2) {
+        const int jl = t / BI + (256 / BI) * s2;
+        const int64_t j = j0 + jl;
+        const bool v = j < J && i < I;
+        const Tin* src = X + (v ? i + I * j : 0);
+        Tin* dst = AT ? xs + jl * PX + il : xs + il * PX + jl;
+        if (sizeof(Tin) == 4) cp_async4(dst, src, v); else cp_async8(dst, src, v);
+      }
+    } else {
+#pragma unroll
+      for (int s2 = 0; s2 < BI * BM / 256; ++s2) {
+        const int il = t / BM + (256 / BM) * s2;
+        const int64_t i = ic + il;
+        const bool v = jv_b && i < I;
+        const Tin* src = X + (v ? off_b + a * i : 0);
+        if (sizeof(Tin) == 4) cp_async4(xs + il * PX + jl_b, src, v); else cp_async8(xs + il * PX + jl_b, src, v);
+      }
+    }
+#pragma unroll
+    for (int s2 = 0; s2 < BI * BN / 256; ++s2) {
+      const int e = t + 256 * s2;
+      int il, cl;
+      if (ms_c == 1) { cl = e % BN; il = e / BN; } else { il = e % BI; cl = e / BI; }
+      const int64_t i = ic + il;
+      const int c = c0 + cl;
+      const bool v = i < I && c < C;
+      const Tm* src = Mm + (v ? i * ms_i + int64_t(c) * ms_c : 0);
+      if (sizeof(Tm) == 4) cp_async4(ms + il * PM + cl, src, v); else cp_async8(ms + il * PM + cl, src, v);
+    }
+  };
+  const int64_t nst = (I + BI - 1) / BI;
+#pragma unroll
+  for (int s0 = 0; s0 < NSTG - 1; ++s0) {
+    if (s0 < nst) issue(int64_t(s0) * BI, s0);
+    cp_async_commit();
+  }
+  for (int64_t st = 0; st < nst; ++st) {
+    cp_async_wait<NSTG - 2>();
+    __syncthreads();                                     // stage st landed; stage st - 1 consumed
+    if (st + NSTG - 1 < nst) issue((st + NSTG - 1) * BI, int((st + NSTG - 1) % NSTG));
+    cp_async_commit();
+    const Tin* xs = Xs + int(st % NSTG) * XS;
+    const Tm* ms = Ms + int(st % NSTG) * MS;
+#pragma unroll
+    for (int kk = 0; kk < BI / 4; ++kk) {
+      double af[4], bf[NF];
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+        af[m] = double(AT ? xs[(jw + 8 * m + fr) * PX + 4 * kk + fk] : xs[(4 * kk + fk) * PX + jw + 8 * m + fr]);
+#pragma unroll
+      for (int n = 0; n < NF; ++n) bf[n] = double(ms[(4 * kk + fk) * PM + cw + 8 * n + fr]);
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int n = 0; n < NF; ++n)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(acc[m][n][0]), "+d"(acc[m][n][1])
+                       : "d"(af[m]), "d"(bf[n]));
+    }
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int64_t j = j0 + jw + 8 * m + fr;
+    if (j >= J) continue;
+    const int64_t ob = (j % a) * so_a + (j / a) * so_b;
+#pragma unroll
+    for (int n = 0; n < NF; ++n)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = c0 + cw + 8 * n + 2 * fk + e;
+        if (c < C) out[ob + int64_t(c) * so_c] = Tout(acc[m][n][e]);
+      }
+  }
+}
+
 template <typename Tin, typename Tm, typename Tout>
 void launch_ttm_t_dmma(const Ctx& ctx, const Tin* X, Box box, const Tm* Mm, int64_t ms_i, int64_t ms_c, int C,
                        Tout* out, int64_t so_a, int64_t so_c, int64_t so_b) {
   const int64_t J = box.J();
-  // 32-column tiles for C <= 32 (the STHOSVD shrink at K = 27 used 27 of 64)
-  const int bn = C <= 32 ? 32 : 64;
+  // 16- / 32-column tiles for C <= 16 / 32 (the STHOSVD shrink at K = 27 used 27 of 64, the core
+  // update S <- B x_n U^T at R = 16 used 16 of 32); the register-prefetch fallback has 32 / 64
+  const bool async = !getenv("RT_DMMA_SYNC");
+  const int bn = (C <= 16 && async) ? 16 : (C <= 32 ? 32 : 64);
   const dim3 grid((unsigned)cdiv(J, 128), (unsigned)cdiv(C, bn));
   RT_REQUIRE(grid.x < (1u << 31) && grid.y < 65536, kEUNSUPPORTED, "ttm_t grid too large");
+  constexpr int NSTG = 3;
+  const bool at = box.a == 1;
+  auto smem_of = [at](int bnv) {
+    const int BI = sizeof(Tin) == 4 ? 32 : 16;
+    const int PX = at ? (sizeof(Tin) == 4 ? BI + 4 : BI + 2) : (sizeof(Tin) == 4 ? 136 : 132);
+    const int PM = bnv + (sizeof(Tm) == 4 ? 8 : 4);
+    return size_t(NSTG) * (sizeof(Tin) * size_t(at ? 128 : BI) * PX + sizeof(Tm) * BI * PM);
+  };
   launch(ctx, ctx.label ? ctx.label : "ttm_t_dmma", [&] {
-    if (bn == 32)
+    if (async) {
+      const size_t sm = smem_of(bn);
+      auto go = [&](auto k) {
+        RT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+        k<<<grid, 256, sm, ctx.stream>>>(X, box.a, box.I, J, Mm, ms_i, ms_c, C, out, so_a, so_c, so_b);
+      };
+      if (bn == 16 && at) go(ttm_t_dmma_async_kernel<Tin, Tm, Tout, 1, NSTG, true>);
+      else if (bn == 16) go(ttm_t_dmma_async_kernel<Tin, Tm, Tout, 1, NSTG, false>);
+      else if (bn == 32 && at) go(ttm_t_dmma_async_kernel<Tin, Tm, Tout, 2, NSTG, true>);
+      else if (bn == 32) go(ttm_t_dmma_async_kernel<Tin, Tm, Tout, 2, NSTG, false>);
+      else if (at) go(ttm_t_dmma_async_kernel<Tin, Tm, Tout, 4, NSTG, true>);
+      else go(ttm_t_dmma_async_kernel<Tin, Tm, Tout, 4, NSTG, false>);
+    } else if (bn == 32) {
       ttm_t_dmma_kernel<Tin, Tm, Tout, 2><<<grid, 256, 0, ctx.stream>>>(X, box.a, box.I, J, Mm, ms_i, ms_c, C, out,
                                                                          so_a, so_c, so_b);
-    else
+    } else {
       ttm_t_dmma_kernel<Tin, Tm, Tout, 4><<<grid, 256, 0, ctx.stream>>>(X, box.a, box.I, J, Mm, ms_i, ms_c, C, out,
                                                                          so_a, so_c, so_b);
+    }
   });
 }
 
