@@ -696,7 +696,7 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
   // of mode 0) together with mode 1's Omega sketch, and later the first core stage together with the
   // last mode's Omega sketch (X viewed with the last mode as rows).  9 passes over X:
   //   S0, [Z0 + S1], Y0, Z1, [G1 + S2], Y1, Z2, Y2, residual
-  // QR(S0) is exposed (the Omega_1 conversion runs under it); QR(S1) hides under Y0, the last QR of
+  // QR(S0) is exposed (the Omega_1 and Omega_2 conversions run under it); QR(S1) hides under Y0, the last QR of
   // mode 0 under Z1, QR(S2) under Y1; the final QR of mode 2 closes the sketch phase.
   const bool try_fuse2 = try_fuse && N == 3 && q == 1 && !dist() && !ctx.fuse2_off && (omega_ld[2 * N + 2] % 4) == 0 &&
                          X.d[0] % 512 == 0 && X.d[1] % 128 == 0 && X.d[2] % 128 == 0 && K[0] % 4 == 0 &&
@@ -707,8 +707,11 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
     const int npad = tc_npad(int(K[0]));
     first_sketch(0);                           // S0: X's scale; QR + unmixing of mode 0 on the side stream
     F1Prep pre1, pre2;
+    // both fp16 Omega^T conversions now, on the main stream under QR(S0) (1.2 ms against ~1 ms)
     const bool p1 = sketch1_core0_prep(ctx, ws, static_cast<const float*>(omega[1 * N + 1]), b1.J(), int(K[1]),
                                        omega_ld[1 * N + 1], npad, &pre1);
+    const bool p2 = sketch1_core0_prep(ctx, ws, static_cast<const float*>(omega[2 * N + 2]), b2v.J(), int(K[2]),
+                                       omega_ld[2 * N + 2], npad, &pre2);
     // [Z0 + S1]
     const int64_t Jl0 = b0.J(), ldz = pad4(K[0]), ldz2 = 2 * int64_t(npad);
     pbs[0].Z = ws.alloc_n<float>(Jl0 * ldz);
@@ -743,8 +746,6 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
     wait_q(1);
     RT_REQUIRE(power_step_r31(X, data, 1, int(K[1]), Qu[1], Yt[1], true, &pbs[1], 1), kEUNSUPPORTED,
                "power step (Z pass) not launched");
-    const bool p2 = sketch1_core0_prep(ctx, ws, static_cast<const float*>(omega[2 * N + 2]), b2v.J(), int(K[2]),
-                                       omega_ld[2 * N + 2], npad, &pre2);
     wait_q(0);
     // [G1 + S2]
     bool fused2;
