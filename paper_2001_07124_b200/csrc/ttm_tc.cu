@@ -2526,13 +2526,16 @@ struct RSmemH {
   static constexpr uint32_t kQ = uint32_t(RNB) * 128;            // one [64 i][64 r] fp16 box (8 KB)
   static constexpr uint32_t kXt = uint32_t(BM) * RNB * 4;        // X tile [64 i][128 j]
   static constexpr uint32_t kBst = 2 * NRB * kQ + HALF * kQ;      // [hi b0 | lo b0 | ... | hi h | lo h]
-  static constexpr uint32_t per_stage = kBst + kXt;
-  static constexpr int NS_fit = int((227u * 1024u - 256u - kP) / per_stage);
-  static constexpr int NS = NS_fit > 4 ? 4 : NS_fit;
+  // two rings: B slots (released by the MMAs) and X tiles (released by the epilogue, which holds an
+  // X tile from the MMAs' start to the end of its differences), so the X ring gets the depth
+  static constexpr int NSB = 2;
+  static constexpr int NS_fit = int((227u * 1024u - 512u - kP - NSB * kBst) / kXt);
+  static constexpr int NS = NS_fit > 5 ? 5 : NS_fit;               // X tiles
   static constexpr uint32_t off_p = 0;
-  static constexpr uint32_t off_st = kP;
-  static constexpr uint32_t off_bar = off_st + NS * per_stage;
-  static constexpr uint32_t bytes = off_bar + 8 * (2 * NS + 8) + 16;
+  static constexpr uint32_t off_b = kP;
+  static constexpr uint32_t off_st = off_b + NSB * kBst;
+  static constexpr uint32_t off_bar = off_st + NS * kXt;
+  static constexpr uint32_t bytes = off_bar + 8 * (2 * NS + 2 * NSB + 8) + 16;
   static_assert(NS >= 2 && bytes <= 227u * 1024u, "residual smem plan");
 };
 
@@ -2548,7 +2551,7 @@ residual_h16_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_consta
                     const __grid_constant__ CUtensorMap tqh2, const __grid_constant__ CUtensorMap tql2,
                     const RParams p, const float* __restrict__ pscale) {
   using L = RSmemH<RPP>;
-  constexpr int RP = L::RP, NS = L::NS, NRB = L::NRB, HALF = L::HALF;
+  constexpr int RP = L::RP, NS = L::NS, NRB = L::NRB, HALF = L::HALF, NSB = L::NSB;
   if (*pscale == 0.f) return;                          // the twin runs instead (R29)
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::off_bar);
@@ -2560,7 +2563,9 @@ residual_h16_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_consta
   uint64_t* a_free = bar + 2 * NS + 3;
   uint64_t* acc_full = bar + 2 * NS + 4;
   uint64_t* acc_empty = bar + 2 * NS + 6;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2 * NS + 8);
+  uint64_t* b_full = bar + 2 * NS + 8;
+  uint64_t* b_free = b_full + NSB;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(b_free + NSB);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t my_tiles = (p.ntiles > blockIdx.x) ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   constexpr uint32_t kAcc = 2 * RNB;                  // [hi.hi | hi.lo] per buffer (wide issuer)
@@ -2570,6 +2575,7 @@ residual_h16_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_consta
   static_assert(kA + RP <= 512, "residual TMEM plan");
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) { mbar_init(&st_full[s], 1); mbar_init(&st_free[s], 128); }
+    for (int s = 0; s < NSB; ++s) { mbar_init(&b_full[s], 1); mbar_init(&b_free[s], 2); }
     mbar_init(p_full, 1);
     mbar_init(p_free, 128);
     mbar_init(a_ready, 128);
@@ -2585,7 +2591,7 @@ residual_h16_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_consta
   const uint32_t tmem = *tmem_slot;
   if (warp == 0) {
     if (lane == 0) {                                   // ---------------- TMA producer
-      Ring rg;
+      Ring rg, rbg;
       int it = 0;
       const uint64_t pol = policy_evict_first();
       const uint64_t pq = policy_evict_last();
@@ -2594,37 +2600,40 @@ residual_h16_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_consta
         if (u >= 1) mbar_wait(p_free, uint32_t(u - 1) & 1);
         mbar_expect_tx(p_full, L::kP);
         for (int c = 0; c < RP / KC; ++c) tma_load_2d(smem + L::off_p + c * (BM * KC * 4), &tmp, p_full, j0, c * KC);
-        for (int b = 0; b < p.nblk; ++b, ++it, rg.next<NS>()) {
+        for (int b = 0; b < p.nblk; ++b, ++it, rg.next<NS>(), rbg.next<NSB>()) {
+          // the X tile first (it has the longest way to go), then the B slot
           if (it >= NS) mbar_wait(&st_free[rg.s], rg.ph ^ 1);
-          uint8_t* st = smem + L::off_st + rg.s * L::per_stage;
-          mbar_expect_tx(&st_full[rg.s], L::per_stage);
+          mbar_expect_tx(&st_full[rg.s], L::kXt);
+          tma_load_2d_hint(smem + L::off_st + rg.s * L::kXt, &tmx, &st_full[rg.s], j0, b * RNB, pol);
+          if (it >= NSB) mbar_wait(&b_free[rbg.s], rbg.ph ^ 1);
+          uint8_t* st = smem + L::off_b + rbg.s * L::kBst;
+          mbar_expect_tx(&b_full[rbg.s], L::kBst);
 #pragma unroll
           for (int rb = 0; rb < NRB; ++rb) {                                   // [Q_hi | Q_lo] adjacent:
-            tma_load_2d_hint(st + 2 * rb * L::kQ, &tqh, &st_full[rg.s], 64 * rb, b * RNB, pq);   // one N = 128
-            tma_load_2d_hint(st + (2 * rb + 1) * L::kQ, &tql, &st_full[rg.s], 64 * rb, b * RNB, pq);   // operand
+            tma_load_2d_hint(st + 2 * rb * L::kQ, &tqh, &b_full[rbg.s], 64 * rb, b * RNB, pq);   // one N = 128
+            tma_load_2d_hint(st + (2 * rb + 1) * L::kQ, &tql, &b_full[rbg.s], 64 * rb, b * RNB, pq);   // operand
           }
           if (HALF) {                                                          // r 64 NRB .. + 31 (SW64)
-            tma_load_2d_hint(st + 2 * NRB * L::kQ, &tqh2, &st_full[rg.s], 64 * NRB, b * RNB, pq);
-            tma_load_2d_hint(st + 2 * NRB * L::kQ + L::kQ / 2, &tql2, &st_full[rg.s], 64 * NRB, b * RNB, pq);
+            tma_load_2d_hint(st + 2 * NRB * L::kQ, &tqh2, &b_full[rbg.s], 64 * NRB, b * RNB, pq);
+            tma_load_2d_hint(st + 2 * NRB * L::kQ + L::kQ / 2, &tql2, &b_full[rbg.s], 64 * NRB, b * RNB, pq);
           }
-          tma_load_2d_hint(st + L::kBst, &tmx, &st_full[rg.s], j0, b * RNB, pol);
         }
       }
     }
   } else if (warp == 1 || warp == 6) {                // ---------------- MMA issuers (whole warps)
     const bool wide = warp == 1;
     const uint32_t idesc = idesc_f16(BM, wide ? 2 * RNB : RNB, 0);
-    Ring rg;
+    Ring rbg;
     int64_t g = 0;
     for (int64_t u = 0; u < my_tiles; ++u) {
       mbar_wait(a_ready, uint32_t(u) & 1);
       tc_fence_after();
-      for (int b = 0; b < p.nblk; ++b, ++g, rg.next<NS>()) {
+      for (int b = 0; b < p.nblk; ++b, ++g, rbg.next<NSB>()) {
         const int ab = int(g & 1);
         if (g >= 2) mbar_wait(&acc_empty[ab], uint32_t((g >> 1) - 1) & 1);
-        mbar_wait(&st_full[rg.s], rg.ph);
+        mbar_wait(&b_full[rbg.s], rbg.ph);
         tc_fence_after();
-        const uint32_t st = smem_u32(smem + L::off_st + rg.s * L::per_stage);
+        const uint32_t st = smem_u32(smem + L::off_b + rbg.s * L::kBst);
         const uint32_t acc = tmem + (wide ? uint32_t(ab) * kAcc : kAcc1 + uint32_t(ab) * RNB);
 #pragma unroll
         for (int kk = 0; kk < RP / 16; ++kk) {
@@ -2635,6 +2644,7 @@ residual_h16_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_consta
           mma_f16_ts_w(acc, a, bd, idesc, kk == 0 ? 0u : 1u);
         }
         mma_commit_w(&acc_full[ab]);
+        mma_commit_w(&b_free[rbg.s]);
       }
       mma_commit_w(a_free);
     }
@@ -2674,7 +2684,7 @@ residual_h16_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_consta
         mbar_wait(&st_full[rg.s], rg.ph);
         mbar_wait(&acc_full[ab], uint32_t(g >> 1) & 1);
         tc_fence_after();
-        const float* xt = reinterpret_cast<const float*>(smem + L::off_st + rg.s * L::per_stage + L::kBst);
+        const float* xt = reinterpret_cast<const float*>(smem + L::off_st + rg.s * L::kXt);
         float tr = 0.f, tx = 0.f;
 #pragma unroll
         for (int cb = 0; cb < RNB / 16; ++cb) {
