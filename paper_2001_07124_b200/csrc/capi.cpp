@@ -2,6 +2,8 @@
 // Validation, handle/workspace management and status conversion; no arithmetic.
 #include <cuda_runtime.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -286,9 +288,19 @@ rt_status rt_profile_read(rt_handle* h, rt_profile_entry* out, int cap, int* n, 
     RT_CUDA(cudaStreamSynchronize(h->ctx.stream));
     int cnt = 0;
     auto& P = h->prof;
+    // RT_TIMELINE=<file> (measurement aid, tools/timeline.py): every recorded launch as
+    // "name start_ms end_ms" relative to the first one, whatever stream it ran on
+    FILE* tl = nullptr;
+    if (const char* tp = getenv("RT_TIMELINE")) tl = P.recs.empty() ? nullptr : std::fopen(tp, "a");
+    if (tl) std::fprintf(tl, "# read\n");
     for (auto& r : P.recs) {
       float ms = 0.f;
       RT_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+      if (tl) {
+        float t0 = 0.f;
+        RT_CUDA(cudaEventElapsedTime(&t0, P.recs[0].a, r.a));
+        std::fprintf(tl, "%s %.4f %.4f\n", r.name, t0, t0 + ms);
+      }
       int idx = -1;
       for (int i = 0; i < cnt && i < cap; ++i)
         if (std::strncmp(out[i].name, r.name, sizeof(out[i].name)) == 0) { idx = i; break; }
@@ -304,6 +316,7 @@ rt_status rt_profile_read(rt_handle* h, rt_profile_entry* out, int cap, int* n, 
       P.pool.push_back(r.b);
     }
     P.recs.clear();
+    if (tl) std::fclose(tl);
     // device run counters of the fp16-split X passes and their tf32 twins (R29): which one of each
     // gated pair did the work since the last read
     unsigned int runs[3] = {0, 0, 0};
