@@ -71,7 +71,7 @@ class NcclComm final : public Comm {
   NcclComm(ncclComm_t c, int n, int r, bool make_side = true) : comm_(c), n_(n), r_(r) {
     // the side communicator (same ranks, color 0): every rank splits at construction, so the
     // collective split happens at the same point everywhere
-    if (make_side && n > 1 && nccl().CommSplit) {
+    if (make_side && n >= 1 && nccl().CommSplit) {
       ncclComm_t sc = nullptr;
       if (nccl().CommSplit(comm_, 0, r, &sc, nullptr) == 0 && sc) side_.reset(new NcclComm(sc, n, r, false));
     }

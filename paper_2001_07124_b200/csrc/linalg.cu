@@ -406,6 +406,199 @@ __global__ void __launch_bounds__(256) chol_inv_fast_kernel(const double* __rest
   }
 }
 
+// Register-panel variant of the blocked kernel (k <= 128, the default for k > 40).  Same block
+// algorithm; what changes is the latency-bound part:
+//   diagonal block: warp 0 holds the NBK x NBK block in registers (lane = row), pivots and column
+//     entries travel by shuffles, 1 / sqrt(a_jj) comes from rsqrt() with one correction step for the
+//     square root (no fp64 division or sqrt sequence in the column chain);
+//   D_p = L_pp^{-1} right after it (lane = column, forward substitution in registers), so that
+//   L21 = A21 D_p^T is a product of independent dot products over all threads instead of a
+//     per-row substitution, and the inverse phase finds its diagonal blocks already in W;
+//   trailing update in 2 x 2 register tiles (rows 2t, 2t + 1; columns c, c + h: conflict-free).
+__global__ void __launch_bounds__(256) chol_inv_reg_kernel(const double* __restrict__ G, int k, double shift_coef,
+                                                           double* __restrict__ R, double* __restrict__ Rinv,
+                                                           int* zero_flag, int* status, const double* shift_dev) {
+  extern __shared__ double sm[];
+  const int ld = k + 1;
+  double* A = sm;                          // k x ld, L in the lower part
+  double* W = sm + size_t(k) * ld;         // k x ld, W = L^{-1} (lower part)
+  double* T = W + size_t(k) * ld;          // k x NBK scratch
+  double* rl = T + size_t(k) * NBK;        // 1 / L_jj
+  __shared__ double red[32];
+  __shared__ double s_shift, s_tr;
+  __shared__ int s_bad;
+  const int t = threadIdx.x, nt = blockDim.x;
+  const int warp = t >> 5, lane = t & 31;
+  double tr = 0.0;
+  for (int i = t; i < k; i += nt) tr += G[i + int64_t(k) * i];
+  tr = block_sum(tr, red);
+  if (t == 0) {
+    s_tr = tr;
+    s_shift = (shift_dev ? *shift_dev : shift_coef) * tr;
+    s_bad = 0;
+    if (!(tr == tr) || tr > DBL_MAX) latch(status, kStatusNonFinite);
+    if (zero_flag) *zero_flag = (tr == 0.0) ? 1 : 0;
+  }
+  __syncthreads();
+  const bool is_zero = (s_tr == 0.0);
+  for (int e = t; e < k * k; e += nt) {    // consecutive threads read consecutive rows i of column c
+    const int c = e / k, i = e - c * k;
+    A[i * ld + c] = (c <= i) ? G[i + int64_t(k) * c] + (i == c ? s_shift : 0.0) : 0.0;
+    W[i * ld + c] = 0.0;
+  }
+  __syncthreads();
+  const int np = (k + NBK - 1) / NBK;
+  if (!is_zero) {
+    for (int pb = 0; pb < np; ++pb) {
+      const int c0 = pb * NBK, nb = min(NBK, k - c0);
+      if (warp == 0) {
+        const int i = lane & (NBK - 1);              // lanes 16..31 mirror 0..15 (full-warp shuffles)
+        double a[NBK];
+#pragma unroll
+        for (int c = 0; c < NBK; ++c)
+          a[c] = (i < nb && c <= i) ? A[(c0 + i) * ld + c0 + c] : (c == i ? 1.0 : 0.0);   // identity padding
+        double rsv = 1.0;
+        bool bad = false;
+#pragma unroll
+        for (int j = 0; j < NBK; ++j) {
+          double d = __shfl_sync(0xffffffffu, a[j], j);
+          if (!(d > 0.0)) { bad = true; d = 1.0; }
+          const double rs = rsqrt(d);
+          double sd = d * rs;
+          sd = fma(fma(-sd, sd, d), 0.5 * rs, sd);    // sqrt(d) to the last bit or two
+          const double l = (i == j) ? sd : a[j] * rs;
+          if (i == j) rsv = rs;
+          a[j] = l;
+#pragma unroll
+          for (int c = j + 1; c < NBK; ++c) {
+            const double lc = __shfl_sync(0xffffffffu, l, c);
+            if (i >= c) a[c] = fma(-l, lc, a[c]);
+          }
+        }
+        if (bad && lane == 0) s_bad = 1;
+        if (lane < nb) {
+#pragma unroll
+          for (int c = 0; c < NBK; ++c)
+            if (c <= lane) A[(c0 + lane) * ld + c0 + c] = a[c];
+          rl[c0 + lane] = rsv;
+        }
+        __syncwarp();
+        // D = L11^{-1}: lane = column c, D_cc = 1 / L_cc, D_jc = -(sum_{m = c}^{j-1} L_jm D_mc) / L_jj
+        double dv[NBK];
+#pragma unroll
+        for (int j = 0; j < NBK; ++j) {
+          double v0 = 0.0, v1 = 0.0;
+          if (j < nb) {
+#pragma unroll
+            for (int m = 0; m < j; ++m) {
+              const double ljm = A[(c0 + j) * ld + c0 + m];
+              if (m & 1) v1 = fma(ljm, dv[m], v1); else v0 = fma(ljm, dv[m], v0);
+            }
+          }
+          const double rj = (j < nb) ? rl[c0 + j] : 0.0;
+          dv[j] = (j == i) ? rj : (j > i ? -(v0 + v1) * rj : 0.0);
+        }
+        if (lane < nb) {
+#pragma unroll
+          for (int j = 0; j < NBK; ++j)
+            if (j >= lane && j < nb) W[(c0 + j) * ld + c0 + lane] = dv[j];
+        }
+      }
+      __syncthreads();
+      // L21 = A21 D^T: thread = (row below the panel, half of the panel's columns)
+      const int nrow = k - c0 - nb;                  // <= 112 rows: one item per thread
+      {
+        const int r = t >> 1, half = t & 1;
+        const bool act = r < nrow;
+        double x[NBK];
+        double* ai = A + (c0 + nb + (act ? r : 0)) * ld + c0;
+#pragma unroll
+        for (int m = 0; m < NBK; ++m) x[m] = (act && m < nb) ? ai[m] : 0.0;
+        __syncthreads();
+        if (act) {
+#pragma unroll
+          for (int j8 = 0; j8 < NBK / 2; ++j8) {
+            const int jj = half * (NBK / 2) + j8;
+            if (jj < nb) {
+              const double* dj = W + (c0 + jj) * ld + c0;
+              double v0 = 0.0, v1 = 0.0;
+#pragma unroll
+              for (int m = 0; m < NBK; m += 2) {
+                if (m <= jj) v0 = fma(x[m], dj[m], v0);
+                if (m + 1 <= jj) v1 = fma(x[m + 1], dj[m + 1], v1);
+              }
+              ai[jj] = v0 + v1;
+            }
+          }
+        }
+      }
+      __syncthreads();
+      // A22 -= L21 L21^T (lower part): 2 x 2 tiles, rows (2 ti, 2 ti + 1), columns (tc, tc + h)
+      if (nrow > 0) {
+        const int h = (nrow + 1) >> 1;
+        const double* L21 = A + (c0 + nb) * ld + c0;
+        for (int e = t; e < h * h; e += nt) {
+          const int ti = e / h, tc = e - ti * h;
+          const int i0 = 2 * ti, i1 = i0 + 1, ca = tc, cb = tc + h;
+          if (ca > i1) continue;
+          const bool r1 = i1 < nrow, c1 = cb < nrow && cb <= i1;
+          const double* pa = L21 + i0 * ld;
+          const double* pb2 = L21 + (r1 ? i1 : i0) * ld;
+          const double* qa = L21 + ca * ld;
+          const double* qb = L21 + (c1 ? cb : ca) * ld;
+          double v00 = 0.0, v01 = 0.0, v10 = 0.0, v11 = 0.0;
+#pragma unroll
+          for (int m = 0; m < NBK; ++m) {
+            const double x0 = pa[m], x1 = pb2[m], y0 = qa[m], y1 = qb[m];
+            v00 = fma(x0, y0, v00); v01 = fma(x0, y1, v01);
+            v10 = fma(x1, y0, v10); v11 = fma(x1, y1, v11);
+          }
+          double* o0 = A + (c0 + nb + i0) * ld + c0 + nb;
+          double* o1 = A + (c0 + nb + i1) * ld + c0 + nb;
+          if (ca <= i0) o0[ca] -= v00;
+          if (c1 && cb <= i0) o0[cb] -= v01;
+          if (r1) o1[ca] -= v10;
+          if (r1 && c1) o1[cb] -= v11;
+        }
+      }
+      __syncthreads();
+    }
+    // off-diagonal blocks of W, row block by row block: W_pq = -D_p (sum_{r=q}^{p-1} L_pr W_rq)
+    for (int pb = 1; pb < np; ++pb) {
+      const int r0 = pb * NBK, nr = min(NBK, k - r0);
+      for (int e = t; e < nr * r0; e += nt) {
+        const int i = e / r0, c = e % r0;
+        const double* li = A + (r0 + i) * ld;
+        double v0 = 0.0, v1 = 0.0;
+        int m = c;
+        for (; m + 1 < r0; m += 2) { v0 = fma(li[m], W[m * ld + c], v0); v1 = fma(li[m + 1], W[(m + 1) * ld + c], v1); }
+        if (m < r0) v0 = fma(li[m], W[m * ld + c], v0);
+        T[i * k + c] = v0 + v1;
+      }
+      __syncthreads();
+      for (int e = t; e < nr * r0; e += nt) {
+        const int i = e / r0, c = e % r0;
+        double v = 0.0;
+        for (int m = 0; m <= i; ++m) v = fma(W[(r0 + i) * ld + r0 + m], T[m * k + c], v);
+        W[(r0 + i) * ld + c] = -v;
+      }
+      __syncthreads();
+    }
+  }
+  if (t == 0 && s_bad) latch(status, kStatusCholBreakdown);
+  // R = L^T (upper), Rinv = W^T; col-major k x k
+  for (int e = t; e < k * k; e += nt) {
+    const int r = e % k, c = e / k;
+    if (is_zero) {
+      if (R) R[e] = 0.0;
+      Rinv[e] = 0.0;
+    } else {
+      if (R) R[e] = (r <= c) ? A[c * ld + r] : 0.0;
+      Rinv[e] = (r <= c) ? W[c * ld + r] : 0.0;
+    }
+  }
+}
+
 // --------------------------------------------------------------- tall GEMM
 // C(m x n) = A(m x k) B(k x n); 32 rows per CTA; B in shared memory; fp64 accumulation.
 template <typename TA, typename TC>
@@ -480,7 +673,7 @@ struct EigBatch {
   unsigned int* sweeps;   // nullable: device counter of the sweeps run (rt_profile_read "jacobi_sweeps")
 };
 
-__global__ void __launch_bounds__(512) jacobi_kernel(EigBatch bt, double* Vscratch, int v_in_smem, int64_t stride_scr) {
+__global__ void __launch_bounds__(1024) jacobi_kernel(EigBatch bt, double* Vscratch, int v_in_smem, int64_t stride_scr) {
   extern __shared__ double sm[];
   const int k = bt.k[blockIdx.x];
   const int kk = k + (k & 1);
@@ -488,7 +681,8 @@ __global__ void __launch_bounds__(512) jacobi_kernel(EigBatch bt, double* Vscrat
   const int ld = kmax + 1;
   double* A = sm;                                   // kk x ld (row-major A[i*ld + j])
   double* V = v_in_smem ? (sm + kk * ld) : (Vscratch + blockIdx.x * stride_scr);
-  double* cs = (v_in_smem ? sm + 2 * kk * ld : sm + kk * ld);   // kk/2 pairs: c, s, p, q
+  double* cs = (v_in_smem ? sm + 2 * kk * ld : sm + kk * ld);   // kk/2 pairs: c, s; then their (p, q) as ints
+  int* pq = reinterpret_cast<int*>(cs + 2 * (kk / 2 + 1));
   __shared__ double red[32];
   __shared__ int s_done, s_rot;
   __shared__ double s_fro2;
@@ -547,45 +741,72 @@ __global__ void __launch_bounds__(512) jacobi_kernel(EigBatch bt, double* Vscrat
         const double app = A[p * ld + p], aqq = A[q * ld + q];
         const double thr = double(k) * 1.1102230246251565e-16;
         if (apq * apq > thr * thr * fabs(app * aqq) + 1.232595164407831e-32 * s_fro2) {
-          // t = sign(tau) / (|tau| + sqrt(1 + tau^2)) with tau = d / (2 a_pq), d = a_qq - a_pp, multiplied
-          // through by 2 |a_pq| (one square root, one division and one reciprocal square root on the
-          // round's critical path instead of two of each)
+          // cos 2 theta = |d| / sqrt(d^2 + 4 a_pq^2), sin 2 theta = 2 |a_pq| / sqrt(.) (the same angle as
+          // t = sign(tau) / (|tau| + sqrt(1 + tau^2)), tau = d / (2 a_pq)): with r = rsqrt(d^2 + 4 a_pq^2),
+          // c^2 = (1 + |d| r) / 2 in [1/2, 1] and s = sign(d) a_pq r / c.  Two reciprocal square roots
+          // on the round's critical path, no division or square root; no cancellation at small angles
+          // (s is a product)
           const double d = aqq - app;
-          const double tt = (d >= 0.0 ? 2.0 : -2.0) * apq / (fabs(d) + sqrt(d * d + 4.0 * apq * apq));
-          c = rsqrt(1.0 + tt * tt);
-          s = tt * c;
+          const double r = rsqrt(fma(d, d, 4.0 * apq * apq));
+          const double x = fma(0.5 * fabs(d), r, 0.5);
+          const double ic = rsqrt(x);
+          c = x * ic;
+          s = (d >= 0.0 ? apq : -apq) * r * ic;
         }
         if (s != 0.0) s_rot = 1;                      // benign race: every writer stores 1
-        cs[4 * pi + 0] = c; cs[4 * pi + 1] = s;
-        cs[4 * pi + 2] = p; cs[4 * pi + 3] = q;
+        cs[2 * pi + 0] = c; cs[2 * pi + 1] = s;
+        pq[2 * pi + 0] = p; pq[2 * pi + 1] = q;
       }
       __syncthreads();
       // A <- J^T A J in one phase: the rotations of a round act on disjoint index pairs, so the
       // 2x2 block (rows of pair u, columns of pair v) of the result depends only on the same block
       // of A and on the two rotations; one thread per block, in place.  V <- V J likewise.
+      // (the round is latency-bound: ~1.6 blocks of A and ~3 pairs of V per thread at 1024 threads; the V
+      // items go two at a time, loads first, so that their shared-memory round trips overlap)
       for (int e = t; e < npairs * npairs; e += nt) {
         const int u = e / npairs, v = e - u * npairs;
-        const double cu = cs[4 * u], su = cs[4 * u + 1], cv = cs[4 * v], sv = cs[4 * v + 1];
-        if (su == 0.0 && sv == 0.0) continue;
-        const int pu = int(cs[4 * u + 2]), qu = int(cs[4 * u + 3]);
-        const int pv = int(cs[4 * v + 2]), qv = int(cs[4 * v + 3]);
-        const double app = A[pu * ld + pv], apq = A[pu * ld + qv], aqp = A[qu * ld + pv], aqq = A[qu * ld + qv];
-        const double rpp = cu * app - su * aqp, rpq = cu * apq - su * aqq;     // rows: J_u^T A
-        const double rqp = su * app + cu * aqp, rqq = su * apq + cu * aqq;
-        A[pu * ld + pv] = cv * rpp - sv * rpq;                                 // columns: (.) J_v
-        A[pu * ld + qv] = sv * rpp + cv * rpq;
-        A[qu * ld + pv] = cv * rqp - sv * rqq;
-        A[qu * ld + qv] = sv * rqp + cv * rqq;
-        if (u == v) { A[pu * ld + qv] = 0.0; A[qu * ld + pv] = 0.0; }      // the annihilated pair
+        const double cu = cs[2 * u], su = cs[2 * u + 1], cv = cs[2 * v], sv = cs[2 * v + 1];
+        if (su != 0.0 || sv != 0.0) {
+          const int pu = pq[2 * u], qu = pq[2 * u + 1], pv = pq[2 * v], qv = pq[2 * v + 1];
+          double* ap = A + pu * ld;
+          double* aq = A + qu * ld;
+          const double app = ap[pv], apq = ap[qv], aqp = aq[pv], aqq = aq[qv];
+          const double rpp = cu * app - su * aqp, rpq = cu * apq - su * aqq;     // rows: J_u^T A
+          const double rqp = su * app + cu * aqp, rqq = su * apq + cu * aqq;
+          const bool dg = (u == v);                                              // the annihilated pair
+          ap[pv] = cv * rpp - sv * rpq;                                          // columns: (.) J_v
+          ap[qv] = dg ? 0.0 : sv * rpp + cv * rpq;
+          aq[pv] = dg ? 0.0 : cv * rqp - sv * rqq;
+          aq[qv] = sv * rqp + cv * rqq;
+        }
       }
-      for (int e = t; e < kk * npairs; e += nt) {
-        const int l = e / npairs, v = e - l * npairs;
-        const double c = cs[4 * v], sn = cs[4 * v + 1];
-        if (sn == 0.0) continue;
-        const int pv = int(cs[4 * v + 2]), qv = int(cs[4 * v + 3]);
-        const double vp = V[l * ld + pv], vq = V[l * ld + qv];
-        V[l * ld + pv] = c * vp - sn * vq;
-        V[l * ld + qv] = sn * vp + c * vq;
+      const int nv = kk * npairs;
+      for (int e0 = t; e0 < nv; e0 += 2 * nt) {
+        double c[2], sn[2], vp[2], vq[2];
+        double* pp[2];
+        double* pqv[2];
+        bool act[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int e = e0 + h * nt;
+          act[h] = false;
+          if (e < nv) {
+            const int l = e / npairs, v = e - l * npairs;
+            c[h] = cs[2 * v]; sn[h] = cs[2 * v + 1];
+            if (sn[h] != 0.0) {
+              act[h] = true;
+              pp[h] = V + l * ld + pq[2 * v];
+              pqv[h] = V + l * ld + pq[2 * v + 1];
+              vp[h] = *pp[h]; vq[h] = *pqv[h];
+            }
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (act[h]) {
+            *pp[h] = c[h] * vp[h] - sn[h] * vq[h];
+            *pqv[h] = sn[h] * vp[h] + c[h] * vq[h];
+          }
       }
       __syncthreads();
     }
@@ -1048,6 +1269,7 @@ void chol_inv(const Ctx& ctx, const double* G, int k, double shift_coef, double*
   if (!attr) {
     RT_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     RT_CUDA(cudaFuncSetAttribute(chol_inv_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    RT_CUDA(cudaFuncSetAttribute(chol_inv_reg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     attr = true;
   }
   const size_t smem_fast = sizeof(double) * (2 * size_t(k) * (k + 1) + size_t(k));
@@ -1062,6 +1284,9 @@ void chol_inv(const Ctx& ctx, const double* G, int k, double shift_coef, double*
     if (k <= 40 && smem_fast <= 220 * 1024 && !getenv("RT_CHOL_BLOCKED") && !getenv("RT_CHOL_UNBLOCKED"))
       chol_inv_fast_kernel<<<1, 256, smem_fast, ctx.stream>>>(G, k, shift_coef, R, Rinv, zero_flag, ctx.d_status,
                                                               shift_dev);
+    else if (k <= 128 && smem_blk <= 220 * 1024 && !getenv("RT_CHOL_BLOCKED") && !getenv("RT_CHOL_UNBLOCKED"))
+      chol_inv_reg_kernel<<<1, 256, smem_blk, ctx.stream>>>(G, k, shift_coef, R, Rinv, zero_flag, ctx.d_status,
+                                                            shift_dev);
     else if (smem_blk <= 220 * 1024 && !getenv("RT_CHOL_UNBLOCKED"))
       chol_inv_blk_kernel<<<1, 256, smem_blk, ctx.stream>>>(G, k, shift_coef, R, Rinv, zero_flag, ctx.d_status,
                                                             shift_dev);
@@ -1129,7 +1354,7 @@ void eig_sym_batch(const Ctx& ctx, Arena& ws, int count, const double* const* A,
     attr = true;
   }
   launch(ctx, "jacobi_eig", [&] {
-    jacobi_kernel<<<count, 512, smem, ctx.stream>>>(bt, scratch, v_in_smem, stride_scr);
+    jacobi_kernel<<<count, 1024, smem, ctx.stream>>>(bt, scratch, v_in_smem, stride_scr);
   });
 }
 

@@ -615,6 +615,10 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
   const int64_t ldzs = pad4(K[ns]);            // 16-byte row pitch of the slab mode's fp32 Z
   float* Zs = c3ovl ? ws.alloc_n<float>(Jls * ldzs) : nullptr;
   if (Zs && ldzs != K[ns]) fill_zero(ctx, Zs, sizeof(float) * Jls * ldzs);   // pad columns (summed by C3)
+  // the summed Z as fp16 [hi | lo] rows (the first product's B operand): converted on the C3 stream right
+  // after the allreduce, so the 2 |Z| conversion pass hides under the other modes' X passes too
+  const int64_t ldz2s = c3ovl ? 2 * int64_t(tc_npad(int(K[ns]))) : 0;
+  uint16_t* Z2s = c3ovl ? ws.alloc_n<uint16_t>(Jls * ldz2s) : nullptr;
   cudaEvent_t c3_done = nullptr;
   // the slab mode's Z pass: Zs = s_z X_(N-1)^T Qy (fp32 partial sums of this slab), h16 pair
   auto slab_zpass = [&]() {
@@ -631,12 +635,12 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
     ws.rewind(mz);
   };
   // the slab mode's product from the summed Zs: Yt = X_(N-1) Zs (fp16 split rows), then its QR
-  auto slab_product = [&](bool final_qr) {
+  auto slab_product = [&](bool final_qr, bool presplit) {
     const Box bx = X.box(ns);
     const auto mz = ws.mark();
-    const int64_t ldz2 = 2 * int64_t(tc_npad(int(K[ns])));
-    uint16_t* Z2 = ws.alloc_n<uint16_t>(Jls * ldz2);
-    split_rows_h16(ctx, Zs, Jls, int(K[ns]), ldzs, Z2);
+    const int64_t ldz2 = ldz2s;
+    uint16_t* Z2 = Z2s;
+    if (!presplit) split_rows_h16(ctx, Zs, Jls, int(K[ns]), ldzs, Z2);
     {
       LabelScope ls(ctx, "ttm_s_tc_pow");
       RT_REQUIRE(ttm_s_tc(ctx, ws, data, bx, reinterpret_cast<const float*>(Z2), ldz2, false, int(K[ns]), Yt[ns],
@@ -646,25 +650,14 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
     ws.rewind(mz);
     qr_y(Yt[ns], X.d[ns], X.Ig(ns), int(K[ns]), X.d[ns], final_qr ? Qt[ns] : Qy[ns], X.d[ns], nullptr, true, X.off);
   };
-  if (c3ovl) {
-    sketch<float>(X, data, ns, 0, omega + ns * N, omega_cols + ns * N, omega_ld + ns * N, q, Yt[ns], true);
-    qr_y(Yt[ns], X.d[ns], X.Ig(ns), int(K[ns]), X.d[ns], Qy[ns], X.d[ns], nullptr, true, X.off);   // C2
-    slab_zpass();
-    cudaEvent_t e = ctx.events->get();
-    RT_CUDA(cudaEventRecord(e, ctx.stream));
-    RT_CUDA(cudaStreamWaitEvent(ctx.comm_stream, e, 0));
-    comm->side()->allreduce_sum(Zs, size_t(Jls * ldzs), ctx.comm_stream);                            // C3
-    c3_done = ctx.events->get();
-    RT_CUDA(cudaEventRecord(c3_done, ctx.comm_stream));
-  }
   auto finish_slab = [&]() {                   // after the other modes: the slab mode's remaining steps
     if (!c3ovl) return;
     RT_CUDA(cudaStreamWaitEvent(ctx.stream, c3_done, 0));
-    slab_product(q == 1);
+    slab_product(q == 1, true);
     for (int it = 1; it < q; ++it) {
       slab_zpass();
       allreduce(comm, true, Zs, Jls * ldzs, ctx.stream);                                            // C3
-      slab_product(it == q - 1);
+      slab_product(it == q - 1, false);
     }
   };
   auto first_sketch = [&](int n) {
@@ -689,6 +682,27 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
       fork_qr(n, it_done[n] == q - 1 ? Qt[n] : Qy[n]);
     }
   };
+  bool sketched0 = false;
+  if (c3ovl) {
+    // mode 0's first sketch goes first: its QR (side stream) runs beside the slab mode's sketch and
+    // row-distributed QR (main stream, C2)
+    if (ns != 0) { first_sketch(0); sketched0 = true; }
+    sketch<float>(X, data, ns, 0, omega + ns * N, omega_cols + ns * N, omega_ld + ns * N, q, Yt[ns], true);
+    qr_y(Yt[ns], X.d[ns], X.Ig(ns), int(K[ns]), X.d[ns], Qy[ns], X.d[ns], nullptr, true, X.off);   // C2
+    slab_zpass();
+    cudaEvent_t e = ctx.events->get();
+    RT_CUDA(cudaEventRecord(e, ctx.stream));
+    RT_CUDA(cudaStreamWaitEvent(ctx.comm_stream, e, 0));
+    comm->side()->allreduce_sum(Zs, size_t(Jls * ldzs), ctx.comm_stream);                            // C3
+    {
+      Ctx cctx = ctx;
+      cctx.stream = ctx.comm_stream;
+      cctx.label = nullptr;
+      split_rows_h16(cctx, Zs, Jls, int(K[ns]), ldzs, Z2s);
+    }
+    c3_done = ctx.events->get();
+    RT_CUDA(cudaEventRecord(c3_done, ctx.comm_stream));
+  }
   float* g1 = nullptr;                         // the first core stage from the fused pass
   PowerBufs pbs[5];
   bool deferred[5] = {false, false, false, false, false};
@@ -775,7 +789,7 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
     RT_REQUIRE(power_step_r31(X, data, 2, int(K[2]), Qu[2], Yt[2], true), kEUNSUPPORTED, "power step not launched");
     fork_qr(2, Qt[2]);
   } else if (try_fuse) {
-    first_sketch(0);
+    if (!sketched0) first_sketch(0);
     for (int n = 2; n < N; ++n) first_sketch(n);
     power_all(0);                              // Q~_0 after its last QR
     // modes 2..N-1: every power step, but the product of the last one waits until after the fused
@@ -823,7 +837,8 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
     }
     power_all(1);
   } else {
-    for (int n = 0; n < N; ++n) first_sketch(n);
+    for (int n = 0; n < N; ++n)
+      if (!(n == 0 && sketched0)) first_sketch(n);
     for (int it = 0; it < q; ++it)           // power steps, iteration outer
       for (int n = 0; n < N; ++n) {
         if (dist() && n == N - 1) continue;
@@ -840,7 +855,12 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
   for (int n = 0; n < N; ++n) gsz *= K[n];
   double* Gt = ws.alloc_n<double>(gsz);
   core<float>(X, data, Qt, ldq, K, Gt, g1);
-  if ((E || Eg) && !dist() && !ctx.split_resid_off) {
+  // distributed: the truncation's one collective (the sign candidates of the row-distributed last
+  // factor, canon) goes to the side communicator (C3 finished before the slab mode's product), the
+  // residual pass's C5 stays on the main one: two communicators, two streams
+  Comm* tcomm = dist() ? comm->side() : comm;
+  if ((E || Eg) && (!dist() || tcomm) && !ctx.split_resid_off) {
+    Engine st(sctx, *ctx.side_ws, tcomm);
     // Reading R35: E^2 ||X||^2 = ||X - X^_K||^2 + ||G~||^2 - ||G||^2 with X^_K = G~ x_n Q~_n (the
     // rank-K reconstruction): the truncation (Jacobi, lift, sign canon, core shrink) runs on the side
     // stream while the residual pass streams X against X^_K, which does not depend on it
@@ -851,10 +871,10 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
     cudaEvent_t e = ctx.events->get();
     RT_CUDA(cudaEventRecord(e, ctx.stream));
     RT_CUDA(cudaStreamWaitEvent(sctx.stream, e, 0));
-    se.truncate(X, Gt, K, Qt, ldq, R, Q_out, G_out);
+    st.truncate(X, Gt, K, Qt, ldq, R, Q_out, G_out);
     int64_t gsz = 1;
     for (int n = 0; n < N; ++n) gsz *= R[n];
-    sumsq(sctx, se.ws, G_out, gsz, ggR);
+    sumsq(sctx, st.ws, G_out, gsz, ggR);
     cudaEvent_t done_t = ctx.events->get();
     RT_CUDA(cudaEventRecord(done_t, sctx.stream));
     ctx.sm_reserve = 3;                        // the truncation's Jacobi CTAs run beside the residual
