@@ -92,7 +92,7 @@ bool sketch1_core0(const Ctx& ctx, Arena& ws, const float* X, Box b1, Box b0, co
                    const float* Q0, int64_t ldq0, int K0, const float* xs, double* Y, int64_t ldy, float* out,
                    int view_last = 0, const F1Prep* pre = nullptr, const F1ZOut* zo = nullptr);
 // Z (J x K fp32 row-major, pitch ldz) -> Z2: fp16 rows [2^14 Z_hi | 2^14 Z_lo] of 2 tc_npad(K) halves
-void split_rows_h16(const Ctx& ctx, const float* Z, int64_t J, int K, int64_t ldz, uint16_t* Z2);
+void split_rows_h16(const Ctx& ctx, const float* Z, int64_t J, int K, int64_t ldz, uint16_t* Z2, int max_ctas = 0);
 // out = xs with out[0] = 0 unless max|Q| < 2 (Q fp32 col-major m x r, ld): the fp16 split of an X pass
 // with Q (2^14 Q must stay inside the fp16 range) then stands down for its tf32 twin
 void q_gate_scale(const Ctx& ctx, const float* Q, int64_t m, int r, int64_t ld, const float* xs, float* out);

@@ -7,8 +7,10 @@
 #include <cfloat>
 
 #include <cstdlib>
+#include <cooperative_groups.h>
 #include "kernels.h"
 
+namespace cg = cooperative_groups;
 namespace rt {
 namespace {
 
@@ -824,6 +826,172 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(EigBatch bt, double* Vscra
   }
 }
 
+// Two-CTA (cluster) form of the same Jacobi iteration.  The round is bound by one SM's shared-memory
+// traffic (the A and V updates move the same number of words), so the two updates go to the two CTAs
+// of a cluster: CTA 0 holds A, computes the round's rotations and writes them (c, s and the pair indices)
+// into both CTAs' shared memory (DSMEM stores); CTA 1 holds V and only applies them.  The rotation
+// buffers alternate between rounds, so one cluster barrier per round orders everything: CTA 0 refills
+// a buffer two rounds later, after a barrier CTA 1 reaches only when it has finished reading it.  Same
+// rotations in the same order as jacobi_kernel: same eigenpairs to rounding.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024) jacobi2_kernel(EigBatch bt) {
+  extern __shared__ double sm[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int role = int(cl.block_rank());             // 0: A (rotations, eigenvalues); 1: V (eigenvectors)
+  const int mi = blockIdx.x >> 1;
+  const int k = bt.k[mi];
+  const int kk = k + (k & 1);
+  const int ld = kk + 1;
+  const int npairs = kk / 2;
+  double* M = sm;                                    // kk x ld: A (role 0) or V (role 1), row-major
+  double* csb = sm + kk * ld;                        // 2 buffers of npairs (c, s)
+  int* pqb = reinterpret_cast<int*>(csb + 4 * npairs);   // 2 buffers of npairs (p, q)
+  double* dg = reinterpret_cast<double*>(pqb + 4 * npairs);   // kk: the eigenvalues, for CTA 1's sort
+  __shared__ double red[32];
+  __shared__ int s_done, s_rot;
+  __shared__ double s_fro2;
+  double* r_csb = cl.map_shared_rank(csb, 1);
+  int* r_pqb = cl.map_shared_rank(pqb, 1);
+  int* r_done = cl.map_shared_rank(&s_done, 1);
+  double* r_dg = cl.map_shared_rank(dg, 1);
+  const double* Ab = bt.A[mi];
+  const int t = threadIdx.x, nt = blockDim.x;
+  const int warp = t >> 5, lane = t & 31, nw = nt >> 5;
+  for (int i = warp; i < kk; i += nw)
+    for (int j = lane; j < kk; j += 32) {
+      if (role == 0) M[i * ld + j] = (i < k && j < k) ? 0.5 * (Ab[i + int64_t(k) * j] + Ab[j + int64_t(k) * i]) : 0.0;
+      else M[i * ld + j] = (i == j) ? 1.0 : 0.0;
+    }
+  __syncthreads();
+  int rnd = 0;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    if (role == 0) {
+      double off = 0.0, dia = 0.0;
+      for (int i = warp; i < kk; i += nw)
+        for (int j = lane; j < kk; j += 32) {
+          const double v = M[i * ld + j];
+          if (i != j) off += v * v; else dia += v * v;
+        }
+      off = block_sum(off, red);
+      __syncthreads();
+      dia = block_sum(dia, red);
+      const double tol = double(k) * 1.1102230246251565e-16;
+      if (t == 0) {
+        const int done = (off <= tol * tol * dia) || (dia == 0.0) || (sweep > 0 && !s_rot);
+        s_done = done;
+        *r_done = done;
+        s_rot = 0;
+        s_fro2 = off + dia;
+      }
+    }
+    cl.sync();
+    if (s_done) break;
+    if (role == 0 && t == 0 && bt.sweeps) atomicAdd(bt.sweeps, 1u);
+    for (int round = 0; round < kk - 1; ++round, ++rnd) {
+      const int b = rnd & 1;
+      double* cs = csb + 2 * npairs * b;
+      int* pq = pqb + 2 * npairs * b;
+      if (role == 0 && t < npairs) {
+        const int pi = t;
+        int p, q;
+        if (pi == 0) { p = round; q = kk - 1; }
+        else {
+          p = round + pi; if (p >= kk - 1) p -= kk - 1;
+          q = round - pi; if (q < 0) q += kk - 1;
+        }
+        if (p > q) { const int tmp = p; p = q; q = tmp; }
+        const double apq = M[p * ld + q];
+        double c = 1.0, s = 0.0;
+        const double app = M[p * ld + p], aqq = M[q * ld + q];
+        const double thr = double(k) * 1.1102230246251565e-16;
+        if (apq * apq > thr * thr * fabs(app * aqq) + 1.232595164407831e-32 * s_fro2) {   // as jacobi_kernel
+          const double d = aqq - app;
+          const double r = rsqrt(fma(d, d, 4.0 * apq * apq));
+          const double x = fma(0.5 * fabs(d), r, 0.5);
+          const double ic = rsqrt(x);
+          c = x * ic;
+          s = (d >= 0.0 ? apq : -apq) * r * ic;
+        }
+        if (s != 0.0) s_rot = 1;
+        reinterpret_cast<double2*>(cs)[pi] = make_double2(c, s);
+        reinterpret_cast<int2*>(pq)[pi] = make_int2(p, q);
+        reinterpret_cast<double2*>(r_csb + 2 * npairs * b)[pi] = make_double2(c, s);
+        reinterpret_cast<int2*>(r_pqb + 2 * npairs * b)[pi] = make_int2(p, q);
+      }
+      cl.sync();
+      if (role == 0) {
+        for (int e = t; e < npairs * npairs; e += nt) {
+          const int u = e / npairs, v = e - u * npairs;
+          const double2 ru = reinterpret_cast<const double2*>(cs)[u], rv = reinterpret_cast<const double2*>(cs)[v];
+          const double cu = ru.x, su = ru.y, cv = rv.x, sv = rv.y;
+          if (su != 0.0 || sv != 0.0) {
+            const int2 iu = reinterpret_cast<const int2*>(pq)[u], iv = reinterpret_cast<const int2*>(pq)[v];
+            double* ap = M + iu.x * ld;
+            double* aq = M + iu.y * ld;
+            const double app = ap[iv.x], apq = ap[iv.y], aqp = aq[iv.x], aqq = aq[iv.y];
+            const double rpp = cu * app - su * aqp, rpq = cu * apq - su * aqq;
+            const double rqp = su * app + cu * aqp, rqq = su * apq + cu * aqq;
+            const bool dgl = (u == v);
+            ap[iv.x] = cv * rpp - sv * rpq;
+            ap[iv.y] = dgl ? 0.0 : sv * rpp + cv * rpq;
+            aq[iv.x] = dgl ? 0.0 : cv * rqp - sv * rqq;
+            aq[iv.y] = sv * rqp + cv * rqq;
+          }
+        }
+        __syncthreads();                             // the next round's rotations read A
+      } else {
+        const int nv = kk * npairs;
+        for (int e0 = t; e0 < nv; e0 += 2 * nt) {
+          double c[2], sn[2], vp[2], vq[2];
+          double* pp[2];
+          double* pqv[2];
+          bool act[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int e = e0 + h * nt;
+            act[h] = false;
+            if (e < nv) {
+              const int l = e / npairs, v = e - l * npairs;
+              const double2 rv = reinterpret_cast<const double2*>(cs)[v];
+              c[h] = rv.x; sn[h] = rv.y;
+              if (sn[h] != 0.0) {
+                act[h] = true;
+                const int2 iv = reinterpret_cast<const int2*>(pq)[v];
+                pp[h] = M + l * ld + iv.x;
+                pqv[h] = M + l * ld + iv.y;
+                vp[h] = *pp[h]; vq[h] = *pqv[h];
+              }
+            }
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            if (act[h]) {
+              *pp[h] = c[h] * vp[h] - sn[h] * vq[h];
+              *pqv[h] = sn[h] * vp[h] + c[h] * vq[h];
+            }
+        }
+      }
+    }
+  }
+  // eigenvalues to both CTAs, then CTA 0 writes W and CTA 1 the eigenvectors, sorted descending
+  // (stable on ties: lower index first)
+  if (role == 0)
+    for (int i = t; i < k; i += nt) { const double w = M[i * ld + i]; dg[i] = w; r_dg[i] = w; }
+  cl.sync();
+  for (int i = t; i < k; i += nt) {
+    const double wi = dg[i];
+    int rank = 0;
+    for (int j = 0; j < k; ++j) {
+      const double wj = dg[j];
+      rank += (wj > wi) || (wj == wi && j < i);
+    }
+    if (role == 0) bt.W[mi][rank] = wi;
+    else {
+      double* Vout = bt.V[mi];
+      for (int l = 0; l < k; ++l) Vout[l + int64_t(k) * rank] = M[l * ld + i];
+    }
+  }
+}
+
 // ------------------------------------------------------------ sign canon
 __global__ void colmax_kernel(const double* __restrict__ Q, int64_t m, int64_t ld, int64_t row0,
                               double* __restrict__ cand) {
@@ -1339,6 +1507,19 @@ void eig_sym_batch(const Ctx& ctx, Arena& ws, int count, const double* const* A,
   }
   const int kk = kmax + (kmax & 1), ld = kk + 1;
   const size_t a_bytes = sizeof(double) * size_t(kk) * ld;
+  {
+    // the two-CTA cluster form: A and V in different SMs (RT_JACOBI_1CTA keeps the one-CTA kernel)
+    const size_t smem2 = a_bytes + sizeof(double) * (4 * size_t(kk / 2) + 2 * size_t(kk / 2) + size_t(kk));
+    if (smem2 <= 200 * 1024 && !getenv("RT_JACOBI_1CTA")) {
+      static bool attr2 = false;
+      if (!attr2) {
+        RT_CUDA(cudaFuncSetAttribute(jacobi2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr2 = true;
+      }
+      launch(ctx, "jacobi_eig", [&] { jacobi2_kernel<<<2 * count, 1024, smem2, ctx.stream>>>(bt); });
+      return;
+    }
+  }
   const size_t cs_bytes = sizeof(double) * 4 * size_t(kk / 2 + 1);
   const int v_in_smem = (2 * a_bytes + cs_bytes) <= 200 * 1024;
   const size_t smem = (v_in_smem ? 2 * a_bytes : a_bytes) + cs_bytes;

@@ -258,7 +258,10 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
     if constexpr (std::is_same<T, float>::value) {
       // X's scale already known (a previous mode's sketch of this call gathered it): the fp16 split
       // (R29) on Omega converted once to fp16 [hi | lo] rows (R34)
-      if (xs_slot && xs_key == data && ctx.tc_h16 && !ctx.simt() && !ctx.omega_h16_off &&
+      // (not for a thin slab of the slab mode: its Omega is the whole J x K matrix on every rank, and
+      // converting it costs more than the fp16 form saves once the slab has fewer than ~8 K rows)
+      const bool thin_slab = last && dist() && In < 8 * int64_t(K);
+      if (xs_slot && xs_key == data && ctx.tc_h16 && !ctx.simt() && !ctx.omega_h16_off && !thin_slab &&
           ttm_s_tc_ok(ctx, data, bx, K)) {
         uint16_t* o2;
         int64_t ld2;
@@ -650,8 +653,10 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
     ws.rewind(mz);
     qr_y(Yt[ns], X.d[ns], X.Ig(ns), int(K[ns]), X.d[ns], final_qr ? Qt[ns] : Qy[ns], X.d[ns], nullptr, true, X.off);
   };
+  bool slab_finished = false;
   auto finish_slab = [&]() {                   // after the other modes: the slab mode's remaining steps
-    if (!c3ovl) return;
+    if (!c3ovl || slab_finished) return;
+    slab_finished = true;
     RT_CUDA(cudaStreamWaitEvent(ctx.stream, c3_done, 0));
     slab_product(q == 1, true);
     for (int it = 1; it < q; ++it) {
@@ -698,7 +703,7 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
       Ctx cctx = ctx;
       cctx.stream = ctx.comm_stream;
       cctx.label = nullptr;
-      split_rows_h16(cctx, Zs, Jls, int(K[ns]), ldzs, Z2s);
+      split_rows_h16(cctx, Zs, Jls, int(K[ns]), ldzs, Z2s, /*max_ctas=*/4 * ctx.num_sms);
     }
     c3_done = ctx.events->get();
     RT_CUDA(cudaEventRecord(c3_done, ctx.comm_stream));
@@ -828,6 +833,9 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
     } else {
       first_sketch(1);
     }
+    // slab-parallel: the slab mode's product (C3 has had modes 0's passes and the fused pass to finish)
+    // goes here, so that the QR of mode 1's sketch runs under it instead of holding up mode 1's Z pass
+    finish_slab();
     for (int n = 2; n < N; ++n) {              // the deferred products (under them: mode 1's QR)
       if (!deferred[n]) continue;
       RT_REQUIRE(power_step_r31(X, data, n, int(K[n]), nullptr, Yt[n], true, &pbs[n], 2), kEUNSUPPORTED,

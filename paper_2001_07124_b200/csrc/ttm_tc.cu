@@ -1812,22 +1812,26 @@ const float* omega_h16(const Ctx& ctx, Arena& ws, const float* Om, int64_t J, in
 // operand of ttm_s_h16_kernel; columns >= K zero): the slab mode's power step after its allreduce (C3)
 __global__ void split_rows_h16_kernel(const float* __restrict__ Z, int64_t J, int K, int64_t ldz, int npad,
                                       uint32_t* __restrict__ Z2) {
-  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;   // one pair of columns of one row
   const int hp = npad / 2;
-  if (e >= J * hp) return;
-  const int64_t j = e / hp;
-  const int c0 = 2 * int(e % hp), c1 = c0 + 1;
-  uint32_t h, l;
-  split_h16x2(c0 < K ? Z[j * ldz + c0] * kQScale : 0.f, c1 < K ? Z[j * ldz + c1] * kQScale : 0.f, h, l);
-  Z2[j * npad + c0 / 2] = h;
-  Z2[j * npad + hp + c0 / 2] = l;
+  const int64_t n = J * hp, step = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += step) {   // a pair of columns of a row
+    const int64_t j = e / hp;
+    const int c0 = 2 * int(e % hp), c1 = c0 + 1;
+    uint32_t h, l;
+    split_h16x2(c0 < K ? Z[j * ldz + c0] * kQScale : 0.f, c1 < K ? Z[j * ldz + c1] * kQScale : 0.f, h, l);
+    Z2[j * npad + c0 / 2] = h;
+    Z2[j * npad + hp + c0 / 2] = l;
+  }
 }
-void split_rows_h16(const Ctx& ctx, const float* Z, int64_t J, int K, int64_t ldz, uint16_t* Z2) {
+// max_ctas > 0: a grid of at most that many CTAs (grid-stride); the C3 stream's conversion runs beside the
+// other modes' X passes and must not take the SMs their small kernels are waiting for
+void split_rows_h16(const Ctx& ctx, const float* Z, int64_t J, int K, int64_t ldz, uint16_t* Z2, int max_ctas) {
   const int npad = tc_npad(K);
   RT_REQUIRE(npad > 0, kEUNSUPPORTED, "split_rows_h16: K > 128");
+  int64_t grid = cdiv(J * (npad / 2), 256);
+  if (max_ctas > 0) grid = std::min<int64_t>(grid, max_ctas);
   launch(ctx, "split_rows_h16", [&] {
-    split_rows_h16_kernel<<<unsigned(cdiv(J * (npad / 2), 256)), 256, 0, ctx.stream>>>(Z, J, K, ldz, npad,
-                                                                                       reinterpret_cast<uint32_t*>(Z2));
+    split_rows_h16_kernel<<<unsigned(grid), 256, 0, ctx.stream>>>(Z, J, K, ldz, npad, reinterpret_cast<uint32_t*>(Z2));
   });
 }
 void x_stat_pair(const Ctx& ctx, const unsigned int* amax, double* pair) {

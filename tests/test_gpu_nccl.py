@@ -59,7 +59,9 @@ def test_nccl_one_rank_hosvd_matches_plain_and_oracle(P, q):
         # distributed call takes the C3 form (fp32 partial Z, allreduce, then the fp16
         # [hi | lo] split) where the plain call splits the accumulator directly, and its QR is the
         # row-distributed one: two roundings of the same 22-bit product, ~1e-7 apart
-        assert M.subspace(qa, qb) <= (1e-7 if q == 0 else 1e-6), (n, M.subspace(qa, qb))
+        # (the slab mode of a thin slab, I_N(local) < 8 K, sketches with the tf32 3-product kernel where
+        # the plain call uses the fp16 form of Omega: also two roundings of one product, ~3e-7 apart)
+        assert M.subspace(qa, qb) <= (1e-7 if q == 0 and n < 2 else 1e-6), (n, M.subspace(qa, qb))
         assert M.subspace(qa, ref["Q"][n]) <= 1e-5
     assert abs(float(res["err"][0]) - ref["E"]) / ref["E"] <= 1e-5
     hn.close()
