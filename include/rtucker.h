@@ -113,7 +113,9 @@ rt_status rt_sync(rt_handle* h);
  * A/B switches of the product path: 210 / 211 = the fp16-split form of the X passes that multiply
  * an orthonormal Q (power products, first core stage; R29) off / on (default on), 212 =
  * on with its device-side range gate forced closed (the tf32 twin launches do the work; tests);
- * 220 / 221 = RP-HOOI's X pass on the fp64 warp MMA / on the tensor cores (default, R30). */
+ * 220 / 221 = RP-HOOI's X pass on the fp64 warp MMA / on the tensor cores (default, R30);
+ * 320 / 321 = the slab mode of a thin slab (I_N(local) < 8 K) keeps the fp16 forms of its Omega sketch
+ * and power product / takes the 3xTF32 kernels on the fp32 operands (default). */
 typedef enum { RT_OPT_TTM_IMPL = 0, RT_OPT_PROFILE = 1, RT_OPT_QR_FALLBACK = 2, RT_OPT_OMEGA_TF32 = 3,
                RT_OPT_TC_SEGMENT = 4, RT_OPT_TC_SKEW = 5,
                RT_OPT_FORCE_COLLECTIVES = 6 /* tests: run the slab exchanges even on a 1-rank communicator */,

@@ -260,7 +260,7 @@ void Engine::sketch(const TView& X, const T* data, int n, int kind, const void* 
       // (R29) on Omega converted once to fp16 [hi | lo] rows (R34)
       // (not for a thin slab of the slab mode: its Omega is the whole J x K matrix on every rank, and
       // converting it costs more than the fp16 form saves once the slab has fewer than ~8 K rows)
-      const bool thin_slab = last && dist() && In < 8 * int64_t(K);
+      const bool thin_slab = last && dist() && In < 8 * int64_t(K) && !ctx.thin_slab_off;
       if (xs_slot && xs_key == data && ctx.tc_h16 && !ctx.simt() && !ctx.omega_h16_off && !thin_slab &&
           ttm_s_tc_ok(ctx, data, bx, K)) {
         uint16_t* o2;
@@ -620,8 +620,11 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
   if (Zs && ldzs != K[ns]) fill_zero(ctx, Zs, sizeof(float) * Jls * ldzs);   // pad columns (summed by C3)
   // the summed Z as fp16 [hi | lo] rows (the first product's B operand): converted on the C3 stream right
   // after the allreduce, so the 2 |Z| conversion pass hides under the other modes' X passes too
+  // (a thin slab, I_N(local) < 8 K, skips it: there |Z| is a large part of the product's traffic, and the
+  // 3xTF32 kernel that splits the fp32 Z in flight costs less than a conversion pass plus the fp16 form)
+  const bool thin_slab = X.d[ns] < 8 * K[ns] && !ctx.thin_slab_off;
   const int64_t ldz2s = c3ovl ? 2 * int64_t(tc_npad(int(K[ns]))) : 0;
-  uint16_t* Z2s = c3ovl ? ws.alloc_n<uint16_t>(Jls * ldz2s) : nullptr;
+  uint16_t* Z2s = c3ovl && !thin_slab ? ws.alloc_n<uint16_t>(Jls * ldz2s) : nullptr;
   cudaEvent_t c3_done = nullptr;
   // the slab mode's Z pass: Zs = s_z X_(N-1)^T Qy (fp32 partial sums of this slab), h16 pair
   auto slab_zpass = [&]() {
@@ -643,8 +646,11 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
     const auto mz = ws.mark();
     const int64_t ldz2 = ldz2s;
     uint16_t* Z2 = Z2s;
-    if (!presplit) split_rows_h16(ctx, Zs, Jls, int(K[ns]), ldzs, Z2);
-    {
+    if (!presplit && Z2) split_rows_h16(ctx, Zs, Jls, int(K[ns]), ldzs, Z2);
+    if (!Z2) {
+      LabelScope ls(ctx, "ttm_s_tc_pow");
+      ttm_s_dispatch(ctx, ws, data, bx, Zs, ldzs, false, int(K[ns]), Yt[ns], X.d[ns]);
+    } else {
       LabelScope ls(ctx, "ttm_s_tc_pow");
       RT_REQUIRE(ttm_s_tc(ctx, ws, data, bx, reinterpret_cast<const float*>(Z2), ldz2, false, int(K[ns]), Yt[ns],
                           X.d[ns], true, xs_slot, nullptr, Zs, ldzs),
@@ -699,7 +705,7 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
     RT_CUDA(cudaEventRecord(e, ctx.stream));
     RT_CUDA(cudaStreamWaitEvent(ctx.comm_stream, e, 0));
     comm->side()->allreduce_sum(Zs, size_t(Jls * ldzs), ctx.comm_stream);                            // C3
-    {
+    if (Z2s) {
       Ctx cctx = ctx;
       cctx.stream = ctx.comm_stream;
       cctx.label = nullptr;

@@ -443,13 +443,17 @@ def test_loopback_multirank_hosvd(P, h, nranks):
     assert abs(out[0]["err"][0] - ref["E"]) / ref["E"] <= 1e-5
 
 
-@pytest.mark.parametrize("nranks,opts", [(2, ()), (3, ()), (2, ((100, 270),)), (3, ((3, 1),))])
+@pytest.mark.parametrize("nranks,opts", [(2, ()), (3, ()), (2, ((100, 270),)), (3, ((3, 1),)), (2, ((100, 320),)),
+                                         (3, ((100, 320), (3, 1)))])
 def test_loopback_overlapped_hosvd(P, nranks, opts):
     """The overlapped distributed schedule (K_n % 4 == 0 so every power step takes reading R31): the
     replicated modes' QRs on the side stream, the slab mode's Z allreduce (C3) on the side
     communicator and a third stream while the other modes proceed, then its product from the summed
     Z.  2 and 3 emulated ranks (loopback), with the overlap off (option 270) and with tf32-rounded
-    Omega (option 3): the gathered result equals the oracle; replicated outputs agree bit for bit."""
+    Omega (option 3): the gathered result equals the oracle; replicated outputs agree bit for bit.
+    These slabs are thin (I_3(local) < 8 K): by default the slab mode sketches and multiplies with the
+    3xTF32 kernels on the fp32 Omega / Z; option 320 keeps the fp16 forms a thick slab takes (Omega
+    converted once, the summed Z converted on the C3 stream)."""
     cfg = dataclasses.replace(synth.CONFIGS["cfg5"].scaled((48, 40, 36), (6, 6, 6), (6, 6, 6)), q=1, p=10)
     assert all(cfg.K(n) % 4 == 0 for n in range(3))
     x = synth.make_tensor(cfg)
