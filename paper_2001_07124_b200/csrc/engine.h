@@ -63,10 +63,11 @@ class Engine {
                      double* E, double* Eg);
   // (2) thin QR of the fp64 Y side (shifted CholeskyQR3); R nullable.
   void qr_y(const double* Y, int64_t m, int64_t m_glob, int k, int64_t ldy, double* Q, int64_t ldq,
-            double* R, bool rows_dist, int64_t row0);
+            double* R, bool rows_dist, int64_t row0, int passes = 3);
   template <typename T>
   void qr_rows(const T* Y, int64_t m, int64_t m_glob, int k, int64_t ldy, double* Q, int64_t ldq, double* R,
-               bool rows_dist, int64_t row0, const double* shift_dev = nullptr, const int64_t* row0_dev = nullptr);
+               bool rows_dist, int64_t row0, const double* shift_dev = nullptr, const int64_t* row0_dev = nullptr,
+               int passes = 3);
   // orthonormalize the tall Z of the power iteration in place (shifted CholeskyQR, fp64 Gram)
   template <typename T>
   bool qr_z(T* Z, int64_t m, int64_t ldz, int64_t m_glob, int k, bool rows_dist, int64_t row0, T* Z2 = nullptr,

@@ -601,6 +601,78 @@ __global__ void __launch_bounds__(256) chol_inv_reg_kernel(const double* __restr
   }
 }
 
+// k <= 32: the whole matrix in one warp's registers (lane = row).  Same steps as the diagonal block of
+// chol_inv_reg_kernel: pivots and column entries by shuffles, rsqrt() with a corrected square root, then
+// W = L^{-1} by forward substitution with lane = column (L read from shared memory as broadcasts).  No
+// block barrier inside the factorization (tools/qr_time.py: ~12 vs 30 us at k = 27-30, where the thin
+// QRs of cfg2 / cfg3 spend most of their time).
+__global__ void __launch_bounds__(32) chol_inv_warp_kernel(const double* __restrict__ G, int k, double shift_coef,
+                                                           double* __restrict__ R, double* __restrict__ Rinv,
+                                                           int* zero_flag, int* status, const double* shift_dev) {
+  constexpr int NW = 32;
+  __shared__ double Ls[NW][NW + 1];
+  const int i = threadIdx.x;
+  double tr = (i < k) ? G[i + int64_t(k) * i] : 0.0;
+  for (int o = 16; o; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
+  const double shift = (shift_dev ? *shift_dev : shift_coef) * tr;
+  if (i == 0) {
+    if (!(tr == tr) || tr > DBL_MAX) latch(status, kStatusNonFinite);
+    if (zero_flag) *zero_flag = (tr == 0.0) ? 1 : 0;
+  }
+  if (tr == 0.0) {
+    for (int e = i; e < k * k; e += NW) { if (R) R[e] = 0.0; Rinv[e] = 0.0; }
+    return;
+  }
+  double a[NW];
+#pragma unroll
+  for (int c = 0; c < NW; ++c)
+    a[c] = (i < k && c <= i) ? G[i + int64_t(k) * c] + (i == c ? shift : 0.0) : (c == i ? 1.0 : 0.0);   // identity padding
+  double rsv = 1.0;
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < NW; ++j) {
+    double d = __shfl_sync(0xffffffffu, a[j], j);
+    if (!(d > 0.0)) { bad = true; d = 1.0; }
+    const double rs = rsqrt(d);
+    double sd = d * rs;
+    sd = fma(fma(-sd, sd, d), 0.5 * rs, sd);
+    const double l = (i == j) ? sd : a[j] * rs;
+    if (i == j) rsv = rs;
+    a[j] = l;
+#pragma unroll
+    for (int c = j + 1; c < NW; ++c) {
+      const double lc = __shfl_sync(0xffffffffu, l, c);
+      if (i >= c) a[c] = fma(-l, lc, a[c]);
+    }
+  }
+  if (bad && i == 0) latch(status, kStatusCholBreakdown);
+#pragma unroll
+  for (int c = 0; c < NW; ++c) Ls[i][c] = (c <= i) ? a[c] : 0.0;
+  __syncwarp();
+  // W = L^{-1}: lane = column c; W_cc = 1 / L_cc, W_jc = -(sum_{m = c}^{j-1} L_jm W_mc) / L_jj
+  double dv[NW];
+#pragma unroll
+  for (int j = 0; j < NW; ++j) {
+    double v0 = 0.0, v1 = 0.0;
+#pragma unroll
+    for (int m = 0; m < j; ++m) {
+      const double ljm = Ls[j][m];
+      if (m & 1) v1 = fma(ljm, dv[m], v1); else v0 = fma(ljm, dv[m], v0);
+    }
+    const double rj = __shfl_sync(0xffffffffu, rsv, j);
+    dv[j] = (j == i) ? rj : (j > i ? -(v0 + v1) * rj : 0.0);
+  }
+  // R = L^T (upper), Rinv = W^T; col-major k x k: element (r, c) with lane = r
+  if (i < k) {
+#pragma unroll
+    for (int c = 0; c < NW; ++c)
+      if (c < k) {
+        if (R) R[i + int64_t(k) * c] = (i <= c) ? Ls[c][i] : 0.0;
+        Rinv[i + int64_t(k) * c] = (i <= c) ? dv[c] : 0.0;
+      }
+  }
+}
+
 // --------------------------------------------------------------- tall GEMM
 // C(m x n) = A(m x k) B(k x n); 32 rows per CTA; B in shared memory; fp64 accumulation.
 template <typename TA, typename TC>
@@ -1449,7 +1521,9 @@ void chol_inv(const Ctx& ctx, const double* G, int k, double shift_coef, double*
   launch(ctx, "chol_inv", [&] {
     // the one-barrier-per-column kernel wins at small k (tools/qr_time.py: 25 vs 29 us at k = 27;
     // 84 vs 66 us at k = 60, where the blocked kernel's register-blocked panels pay off)
-    if (k <= 40 && smem_fast <= 220 * 1024 && !getenv("RT_CHOL_BLOCKED") && !getenv("RT_CHOL_UNBLOCKED"))
+    if (k <= 32 && !getenv("RT_CHOL_BLOCKED") && !getenv("RT_CHOL_UNBLOCKED") && !getenv("RT_CHOL_FAST"))
+      chol_inv_warp_kernel<<<1, 32, 0, ctx.stream>>>(G, k, shift_coef, R, Rinv, zero_flag, ctx.d_status, shift_dev);
+    else if (k <= 40 && smem_fast <= 220 * 1024 && !getenv("RT_CHOL_BLOCKED") && !getenv("RT_CHOL_UNBLOCKED"))
       chol_inv_fast_kernel<<<1, 256, smem_fast, ctx.stream>>>(G, k, shift_coef, R, Rinv, zero_flag, ctx.d_status,
                                                               shift_dev);
     else if (k <= 128 && smem_blk <= 220 * 1024 && !getenv("RT_CHOL_BLOCKED") && !getenv("RT_CHOL_UNBLOCKED"))

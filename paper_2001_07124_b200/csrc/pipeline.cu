@@ -103,8 +103,10 @@ T* working_copy(const Ctx& ctx, Arena& ws, const double* Q, int64_t m, int64_t k
 // device (rtucker_qr's row-distributed form, which learns m_glob from an allgather without a host sync)
 template <typename T>
 void Engine::qr_rows(const T* Y, int64_t m, int64_t m_glob, int k, int64_t ldy, double* Q, int64_t ldq,
-                     double* R, bool rows_dist, int64_t row0, const double* shift_dev, const int64_t* row0_dev) {
+                     double* R, bool rows_dist, int64_t row0, const double* shift_dev, const int64_t* row0_dev,
+                     int passes) {
   RT_REQUIRE(m_glob >= k, kERANK, "qr: needs m >= k");
+  RT_REQUIRE(passes == 3 || (passes == 2 && !R), kEINVAL, "qr: 2 passes only without R");
   const auto mk = ws.mark();
   double* G = ws.alloc_n<double>(int64_t(k) * k);
   double* Rs[3];
@@ -120,11 +122,11 @@ void Engine::qr_rows(const T* Y, int64_t m, int64_t m_glob, int k, int64_t ldy, 
   chol_inv(ctx, G, k, shift, Rs[0], Ri, zero, shift_dev);
   gemm_tall<T, double>(ctx, Y, m, k, ldy, Ri, k, k, Q1, m, zero, row0, false, row0_dev);
   // steps 2, 3
-  for (int s = 1; s < 3; ++s) {
+  for (int s = 1; s < passes; ++s) {
     gram<double>(ctx, ws, Q1, m, k, m, G);
     allreduce(comm, dist_g, G, int64_t(k) * k, ctx.stream);
     chol_inv(ctx, G, k, 0.0, Rs[s], Ri, nullptr);
-    if (s == 1) gemm_tall<double, double>(ctx, Q1, m, k, m, Ri, k, k, Q1, m);
+    if (s < passes - 1) gemm_tall<double, double>(ctx, Q1, m, k, m, Ri, k, k, Q1, m);
     else gemm_tall<double, double>(ctx, Q1, m, k, m, Ri, k, k, Q, ldq);
   }
   if (R) {
@@ -135,9 +137,12 @@ void Engine::qr_rows(const T* Y, int64_t m, int64_t m_glob, int k, int64_t ldy, 
   ws.rewind(mk);
 }
 
+// passes = 2 (sCQR2) for a Q that only serves as the basis of a power step (Z = X_(n)^T Q_y; any
+// basis of span(Y) gives the same span(X_(n) Z), and R31' re-mixes Q_y anyway): after the shifted step
+// kappa(Q_1) ~ 1 for kappa(Y) < ~1e6, and one plain step then reaches orthogonality u kappa(Q_1)^2
 void Engine::qr_y(const double* Y, int64_t m, int64_t m_glob, int k, int64_t ldy, double* Q, int64_t ldq,
-                  double* R, bool rows_dist, int64_t row0) {
-  qr_rows<double>(Y, m, m_glob, k, ldy, Q, ldq, R, rows_dist, row0);
+                  double* R, bool rows_dist, int64_t row0, int passes) {
+  qr_rows<double>(Y, m, m_glob, k, ldy, Q, ldq, R, rows_dist, row0, nullptr, nullptr, passes);
 }
 
 // X's scales (xs_slot[0] fp16 split, [1] normalizing) from its |x| statistics; on a slab the
@@ -588,7 +593,8 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
     cudaEvent_t e = ctx.events->get();
     RT_CUDA(cudaEventRecord(e, ctx.stream));
     RT_CUDA(cudaStreamWaitEvent(sctx.stream, e, 0));
-    se.qr_y(Yt[n], X.d[n], X.Ig(n), int(K[n]), X.d[n], Q, X.d[n], nullptr, false, 0);
+    se.qr_y(Yt[n], X.d[n], X.Ig(n), int(K[n]), X.d[n], Q, X.d[n], nullptr, false, 0,
+            (Q == Qy[n] && !ctx.qr3_always) ? 2 : 3);
     if (Q == Qy[n] && !dist()) se.unmix_q(X, data, n, int(K[n]), Qy[n], Qu[n]);   // R31' off the main stream
     done_q[n] = ctx.events->get();
     RT_CUDA(cudaEventRecord(done_q[n], sctx.stream));
@@ -657,7 +663,8 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
                  kEUNSUPPORTED, "slab mode: power product not launched");
     }
     ws.rewind(mz);
-    qr_y(Yt[ns], X.d[ns], X.Ig(ns), int(K[ns]), X.d[ns], final_qr ? Qt[ns] : Qy[ns], X.d[ns], nullptr, true, X.off);
+    qr_y(Yt[ns], X.d[ns], X.Ig(ns), int(K[ns]), X.d[ns], final_qr ? Qt[ns] : Qy[ns], X.d[ns], nullptr, true, X.off,
+         (final_qr || ctx.qr3_always) ? 3 : 2);
   };
   bool slab_finished = false;
   auto finish_slab = [&]() {                   // after the other modes: the slab mode's remaining steps
@@ -699,7 +706,8 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
     // row-distributed QR (main stream, C2)
     if (ns != 0) { first_sketch(0); sketched0 = true; }
     sketch<float>(X, data, ns, 0, omega + ns * N, omega_cols + ns * N, omega_ld + ns * N, q, Yt[ns], true);
-    qr_y(Yt[ns], X.d[ns], X.Ig(ns), int(K[ns]), X.d[ns], Qy[ns], X.d[ns], nullptr, true, X.off);   // C2
+    qr_y(Yt[ns], X.d[ns], X.Ig(ns), int(K[ns]), X.d[ns], Qy[ns], X.d[ns], nullptr, true, X.off,
+         ctx.qr3_always ? 3 : 2);                                                                 // C2
     slab_zpass();
     cudaEvent_t e = ctx.events->get();
     RT_CUDA(cudaEventRecord(e, ctx.stream));
@@ -1461,9 +1469,9 @@ template bool Engine::qr_z<float>(float*, int64_t, int64_t, int64_t, int, bool, 
 template bool Engine::qr_z<double>(double*, int64_t, int64_t, int64_t, int, bool, int64_t, double*, int64_t, int,
                                    const float*);
 template void Engine::qr_rows<float>(const float*, int64_t, int64_t, int, int64_t, double*, int64_t, double*,
-                                     bool, int64_t, const double*, const int64_t*);
+                                     bool, int64_t, const double*, const int64_t*, int);
 template void Engine::qr_rows<double>(const double*, int64_t, int64_t, int, int64_t, double*, int64_t, double*,
-                                      bool, int64_t, const double*, const int64_t*);
+                                      bool, int64_t, const double*, const int64_t*, int);
 template void Engine::core<float>(const TView&, const float*, const double* const*, const int64_t*,
                                   const int64_t*, double*, const float*);
 template void Engine::core<double>(const TView&, const double*, const double* const*, const int64_t*,

@@ -1,4 +1,5 @@
-"""cfg5 HOSVD step: direct C-ABI calls vs replay of a CUDA graph captured from the same call."""
+"""HOSVD step of one BASELINE config (default cfg5): direct C-ABI calls vs replay of a CUDA graph captured
+from the same call.   python tools/graph_time.py [cfg2]"""
 import os
 import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -6,7 +7,7 @@ import torch
 from gen import synth
 from paper_2001_07124_b200 import api as P
 
-cfg = synth.CONFIGS["cfg5"]
+cfg = synth.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "cfg5"]
 s = torch.cuda.Stream()
 with torch.cuda.stream(s):
     X, _ = synth.make_tensor_device(cfg, "cuda")
@@ -18,7 +19,7 @@ with torch.cuda.stream(s):
     for _ in range(3):
         step()
     h.sync()
-    def timed(fn, k=5):
+    def timed(fn, k=20 if cfg.nbytes < (1 << 33) else 5):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize(); e0.record(s)
         for _ in range(k):
