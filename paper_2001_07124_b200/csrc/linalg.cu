@@ -631,6 +631,7 @@ __global__ void __launch_bounds__(32) chol_inv_warp_kernel(const double* __restr
   bool bad = false;
 #pragma unroll
   for (int j = 0; j < NW; ++j) {
+    if (j >= k) break;                               // (uniform: the padding rows need no steps)
     double d = __shfl_sync(0xffffffffu, a[j], j);
     if (!(d > 0.0)) { bad = true; d = 1.0; }
     const double rs = rsqrt(d);
@@ -654,6 +655,7 @@ __global__ void __launch_bounds__(32) chol_inv_warp_kernel(const double* __restr
 #pragma unroll
   for (int j = 0; j < NW; ++j) {
     double v0 = 0.0, v1 = 0.0;
+    if (j >= k) { dv[j] = 0.0; continue; }
 #pragma unroll
     for (int m = 0; m < j; ++m) {
       const double ljm = Ls[j][m];
