@@ -74,13 +74,17 @@ class NcclComm final : public Comm {
     if (make_side && n >= 1 && nccl().CommSplit) {
       ncclComm_t sc = nullptr;
       if (nccl().CommSplit(comm_, 0, r, &sc, nullptr) == 0 && sc) side_.reset(new NcclComm(sc, n, r, false));
+      ncclComm_t sc2 = nullptr;
+      if (side_ && nccl().CommSplit(comm_, 0, r, &sc2, nullptr) == 0 && sc2) side2_.reset(new NcclComm(sc2, n, r, false));
     }
   }
   ~NcclComm() override {
     side_.reset();
+    side2_.reset();
     if (comm_ && nccl().CommDestroy) nccl().CommDestroy(comm_);
   }
   Comm* side() override { return side_.get(); }
+  Comm* side2() override { return side2_.get(); }
   int nranks() const override { return n_; }
   int rank() const override { return r_; }
   void allreduce_sum(double* b, size_t n, cudaStream_t s) override {
@@ -96,7 +100,7 @@ class NcclComm final : public Comm {
  private:
   ncclComm_t comm_;
   int n_, r_;
-  std::unique_ptr<NcclComm> side_;
+  std::unique_ptr<NcclComm> side_, side2_;
 };
 }  // namespace
 
@@ -146,6 +150,7 @@ struct LoopbackGroup {
   std::vector<const void*> ptr;
   std::vector<cudaEvent_t> ev;
   LoopbackGroup* side = nullptr;       // the group of the side communicators (Comm::side)
+  LoopbackGroup* side2 = nullptr;      // and of the third ones (Comm::side2)
   explicit LoopbackGroup(int nn) : n(nn), ptr(nn, nullptr), ev(nn, nullptr) {}
   void barrier() {
     std::unique_lock<std::mutex> lk(mu);
@@ -164,10 +169,11 @@ LoopbackGroup* loopback_group_create(int nranks) {
   if (nranks < 1 || nranks > kMaxLoop) throw Error(kEINVAL, "loopback group: 1 <= nranks <= 8");
   LoopbackGroup* g = new LoopbackGroup(nranks);
   g->side = new LoopbackGroup(nranks);
+  g->side2 = new LoopbackGroup(nranks);
   return g;
 }
 void loopback_group_destroy(LoopbackGroup* g) {
-  if (g) delete g->side;
+  if (g) { delete g->side; delete g->side2; }
   delete g;
 }
 
@@ -178,8 +184,10 @@ class LoopbackComm final : public Comm {
     RT_CUDA(cudaEventCreateWithFlags(&ready_, cudaEventDisableTiming));
     RT_CUDA(cudaEventCreateWithFlags(&done_, cudaEventDisableTiming));
     if (g->side) side_.reset(new LoopbackComm(g->side, r));
+    if (g->side2) side2_.reset(new LoopbackComm(g->side2, r));
   }
   Comm* side() override { return side_.get(); }
+  Comm* side2() override { return side2_.get(); }
   ~LoopbackComm() override {
     cudaEventDestroy(ready_);
     cudaEventDestroy(done_);
@@ -245,7 +253,7 @@ class LoopbackComm final : public Comm {
   cudaEvent_t ready_ = nullptr, done_ = nullptr;
   void* tmp_ = nullptr;
   size_t tmp_bytes_ = 0;
-  std::unique_ptr<LoopbackComm> side_;
+  std::unique_ptr<LoopbackComm> side_, side2_;
 };
 }  // namespace
 

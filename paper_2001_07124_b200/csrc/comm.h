@@ -31,6 +31,9 @@ class Comm {
   // a second communicator over the same ranks whose collectives may run concurrently with this
   // one's on another stream (NCCL: ncclCommSplit; loopback: the group's side group); nullptr if none
   virtual Comm* side() { return nullptr; }
+  // a third one (the side stream's R31' unmixing steps of a slab-parallel call, which run while the C3
+  // allreduce occupies side()); nullptr if none
+  virtual Comm* side2() { return nullptr; }
 };
 
 int nccl_get_unique_id(uint8_t id[128]);   // 0 ok, else error (message via nccl_last_error)

@@ -582,7 +582,12 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
   Ctx sctx = ctx;
   sctx.stream = ctx.side_stream;
   sctx.label = nullptr;
-  Engine se(sctx, *ctx.side_ws, comm);
+  // slab-parallel: the side stream's engine works on the third communicator (its R31' unmixing steps
+  // allreduce a K x K Gram while C3 occupies the side communicator and the main stream's passes the
+  // main one); without one the unmixing stays on the main stream
+  Comm* ucomm = dist() ? comm->side2() : comm;
+  const bool side_unmix = !dist() || ucomm != nullptr;
+  Engine se(sctx, *ctx.side_ws, ucomm ? ucomm : comm);
   double* Yt[5];
   double* Qy[5];
   double* Qu[5];                               // Qy after the R31' unmixing (side stream, !dist())
@@ -595,7 +600,7 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
     RT_CUDA(cudaStreamWaitEvent(sctx.stream, e, 0));
     se.qr_y(Yt[n], X.d[n], X.Ig(n), int(K[n]), X.d[n], Q, X.d[n], nullptr, false, 0,
             (Q == Qy[n] && !ctx.qr3_always) ? 2 : 3);
-    if (Q == Qy[n] && !dist()) se.unmix_q(X, data, n, int(K[n]), Qy[n], Qu[n]);   // R31' off the main stream
+    if (Q == Qy[n] && side_unmix) se.unmix_q(X, data, n, int(K[n]), Qy[n], Qu[n]);   // R31' off the main stream
     done_q[n] = ctx.events->get();
     RT_CUDA(cudaEventRecord(done_q[n], sctx.stream));
   };
@@ -696,7 +701,7 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
     if (dist() && n == N - 1) return;
     for (; it_done[n] < q; ++it_done[n]) {
       wait_q(n);
-      RT_REQUIRE(power_step_r31(X, data, n, int(K[n]), dist() ? Qy[n] : Qu[n], Yt[n], !dist()), kEUNSUPPORTED, "power step not launched");
+      RT_REQUIRE(power_step_r31(X, data, n, int(K[n]), side_unmix ? Qu[n] : Qy[n], Yt[n], side_unmix), kEUNSUPPORTED, "power step not launched");
       fork_qr(n, it_done[n] == q - 1 ? Qt[n] : Qy[n]);
     }
   };
@@ -819,12 +824,12 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
       if (dist() && n == N - 1) continue;
       for (; it_done[n] < q - 1; ++it_done[n]) {
         wait_q(n);
-        RT_REQUIRE(power_step_r31(X, data, n, int(K[n]), dist() ? Qy[n] : Qu[n], Yt[n], !dist()), kEUNSUPPORTED,
+        RT_REQUIRE(power_step_r31(X, data, n, int(K[n]), side_unmix ? Qu[n] : Qy[n], Yt[n], side_unmix), kEUNSUPPORTED,
                    "power step not launched");
         fork_qr(n, Qy[n]);
       }
       wait_q(n);
-      RT_REQUIRE(power_step_r31(X, data, n, int(K[n]), dist() ? Qy[n] : Qu[n], Yt[n], !dist(), &pbs[n], 1),
+      RT_REQUIRE(power_step_r31(X, data, n, int(K[n]), side_unmix ? Qu[n] : Qy[n], Yt[n], side_unmix, &pbs[n], 1),
                  kEUNSUPPORTED, "power step (Z pass) not launched");
       deferred[n] = true;
     }
@@ -865,7 +870,7 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
       for (int n = 0; n < N; ++n) {
         if (dist() && n == N - 1) continue;
         wait_q(n);
-        RT_REQUIRE(power_step_r31(X, data, n, int(K[n]), dist() ? Qy[n] : Qu[n], Yt[n], !dist()), kEUNSUPPORTED, "power step not launched");
+        RT_REQUIRE(power_step_r31(X, data, n, int(K[n]), side_unmix ? Qu[n] : Qy[n], Yt[n], side_unmix), kEUNSUPPORTED, "power step not launched");
         fork_qr(n, it == q - 1 ? Qt[n] : Qy[n]);
       }
   }
