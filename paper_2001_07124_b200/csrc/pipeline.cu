@@ -728,6 +728,7 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
     RT_CUDA(cudaEventRecord(c3_done, ctx.comm_stream));
   }
   float* g1 = nullptr;                         // the first core stage from the fused pass
+  float* g2 = nullptr;                         // and the second (modes 0 and 1 contracted), two-fusion schedule
   PowerBufs pbs[5];
   bool deferred[5] = {false, false, false, false, false};
   // Two fused passes (N = 3, q = 1, one rank): the mode-0 contraction of X feeds Z_0 (the power step
@@ -812,6 +813,23 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
     wait_q(2);
     RT_REQUIRE(power_step_r31(X, data, 2, int(K[2]), Qu[2], Yt[2], true), kEUNSUPPORTED, "power step not launched");
     fork_qr(2, Qt[2]);
+    // While the last QR (mode 2) runs on the side stream, the main stream contracts mode 1 of the first
+    // core stage (Q~_1 has been final since the passes of mode 2 began): G2 = G1 x_2 Q~_1^T, the 1.3 GB
+    // read of the core's second stage.  What waits for Q~_2 is then one small stage on K_0 x K_1 x I_3.
+    // The persistent grid leaves 24 SMs to the QR's kernels.
+    if (g1 && !ctx.core_early_off) {
+      wait_q(1);
+      int64_t ld1;
+      const float* q1 = working_copy<float>(ctx, ws, Qt[1], X.d[1], K[1], ldq[1], ld1);
+      const Box bm{K[0], X.d[1], X.d[2]};
+      g2 = ws.alloc_n<float>(K[0] * K[1] * X.d[2]);
+      ctx.sm_reserve = 24;
+      {
+        LabelScope ls(ctx, "core_mid");
+        ttm_t_dispatch(ctx, ws, g1, bm, q1, ld1, int(K[1]), g2, 1, bm.a, bm.a * K[1]);
+      }
+      ctx.sm_reserve = 2;
+    }
   } else if (try_fuse) {
     if (!sketched0) first_sketch(0);
     for (int n = 2; n < N; ++n) first_sketch(n);
@@ -881,7 +899,16 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
   int64_t gsz = 1;
   for (int n = 0; n < N; ++n) gsz *= K[n];
   double* Gt = ws.alloc_n<double>(gsz);
-  core<float>(X, data, Qt, ldq, K, Gt, g1);
+  if (g2) {
+    // the last stage: G~ = G2 x_3 Q~_2^T (fp64 sums, as core()'s last stage)
+    int64_t ld2;
+    const float* q2 = working_copy<float>(ctx, ws, Qt[2], X.d[2], K[2], ldq[2], ld2);
+    const Box bl{K[0] * K[1], X.d[2], 1};
+    LabelScope ls(ctx, "core_last");
+    ttm_t<float, float, double>(ctx, g2, bl, q2, 1, ld2, int(K[2]), Gt, 1, bl.a, bl.a * K[2]);
+  } else {
+    core<float>(X, data, Qt, ldq, K, Gt, g1);
+  }
   // distributed: the truncation's one collective (the sign candidates of the row-distributed last
   // factor, canon) goes to the side communicator (C3 finished before the slab mode's product), the
   // residual pass's C5 stays on the main one: two communicators, two streams
