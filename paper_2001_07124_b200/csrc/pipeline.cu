@@ -585,7 +585,10 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
   // slab-parallel: the side stream's engine works on the third communicator (its R31' unmixing steps
   // allreduce a K x K Gram while C3 occupies the side communicator and the main stream's passes the
   // main one); without one the unmixing stays on the main stream
-  Comm* ucomm = dist() ? comm->side2() : comm;
+  // (thin slabs only, I_N(local) < 8 K_N: under the long product passes of a thick slab every side-stream
+  // kernel waits for a CTA wave of the pass, and five more of them make the chain outlast the pass --
+  // measured with tools/rank_share.py: P = 2 42.7 -> 45.0 ms, P = 4 24.3 -> 23.6, P = 8 13.6 -> 13.3)
+  Comm* ucomm = dist() ? (X.d[N - 1] < 8 * omega_cols[(N - 1) * N + (N - 1)] && !ctx.thin_slab_off ? comm->side2() : nullptr) : comm;
   const bool side_unmix = !dist() || ucomm != nullptr;
   Engine se(sctx, *ctx.side_ws, ucomm ? ucomm : comm);
   double* Yt[5];
