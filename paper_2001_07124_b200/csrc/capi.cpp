@@ -276,6 +276,7 @@ rt_status rt_set_option(rt_handle* h, rt_option opt, int64_t value) {
       if (value == 320 || value == 321) { h->ctx.thin_slab_off = int(value == 320); return RT_OK; }
       if (value == 330 || value == 331) { h->ctx.qr3_always = int(value == 330); return RT_OK; }
       if (value == 340 || value == 341) { h->ctx.core_early_off = int(value == 340); return RT_OK; }
+      if (value == 350 || value == 351) { h->ctx.resid_slab_off = int(value == 350); return RT_OK; }
       if (value == 316 || value == 332 || value == 364) { h->ctx.fused_seg = int(value - 300); return RT_OK; }
       h->ctx.tc_ablate = int(value);
       return RT_OK;

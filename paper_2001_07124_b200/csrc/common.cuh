@@ -107,6 +107,7 @@ struct Ctx {
   int fused_nbb = 3;            // fused pass: B slots (chunk pairs) 2 or 3 (ablation 292 / 293)
   int resid_tf32 = 0;           // residual pass: 1 = the 3xTF32 kernel only (ablation 294 / 295)
   int split_resid_off = 0;      // HOSVD: 1 = truncate, then the rank-R residual (no R35 overlap; 296 / 297)
+  int resid_slab_off = 0;       // 1: a slab's residual pass keeps the J x R_N form of P (ablation 350)
   int core_early_off = 0;       // 1: the core's second stage waits for every Q~ (ablation 340)
   int qr3_always = 0;           // 1: the power steps' intermediate QRs keep 3 CholeskyQR steps (ablation 330)
   int thin_slab_off = 0;        // 1: thin slabs keep the fp16 forms of the slab mode (ablation 320; tests)

@@ -35,6 +35,9 @@ class Engine {
   Ctx& ctx;
   Arena& ws;
   Comm* comm;
+  // truncate(): recorded on the engine's stream just before the Jacobi launch when set (a driver that runs
+  // a persistent kernel beside it waits for this, so that the two-CTA clusters get their SMs first)
+  cudaEvent_t pre_eig_event = nullptr;
   bool dist() const { return comm && (comm->nranks() > 1 || ctx.force_dist); }
   // fp16-split power products: the scale s of X (x_scale_h16) in a slot owned by the driver that
   // outlives the per-mode sketches, computed once per tensor (xs_key = the data it was taken of)

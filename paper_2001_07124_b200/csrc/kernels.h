@@ -196,14 +196,17 @@ void residual(const Ctx& ctx, Arena& ws, const T* X, int64_t J, int64_t In, cons
 // the SIMT residual's per-CTA (res, xx) pairs into part[2 nblk] (no reduction), run only if *gate == 0
 // (nullable gate): the twin of the fp16-split residual for R > 64
 void residual_part(const Ctx& ctx, const float* X, int64_t J, int64_t In, const float* P, int R, const float* Q,
-                   int64_t ldq, double* part, int nblk, const float* rscale, const float* gate);
+                   int64_t ldq, double* part, int nblk, const float* rscale, const float* gate, int64_t nslice = 1,
+                   int64_t sx = 0, int64_t sp = 0);
 
 // tcgen05 residual (ttm_tc.cu): same sums with Xhat = P Q^T built on the tensor cores (fp32 data,
 // R <= 128 (R > 64: fp16 split only), J % 4 == 0, ldp % 4 == 0).  Returns false (nothing launched)
 // when not applicable.  The persistent grid leaves ctx.sm_reserve SMs free.
 bool residual_tc(const Ctx& ctx, Arena& ws, const float* X, int64_t J, int64_t In, const float* P, int64_t ldp,
                  int R, const float* Q, int64_t ldq, double* out2, const float* rscale = nullptr,
-                 const float* pscale = nullptr);
+                 const float* pscale = nullptr, int64_t nslice = 1, int64_t sx = 0, int64_t sp = 0);
+// nslice > 1 (R > 64 only): a batch of nslice problems X + s sx (J x In, ld J), P + s sp (J x R, ld ldp)
+// with the same Q, summed into one pair -- the slab form of the residual pass
 // pscale (nullable): device fp16 scale of P (resid_scale s[1]): the fp16-split residual
 // (residual_h16_kernel) with the tf32 kernel as its gated twin (runs when *pscale == 0)
 // out2 = fixed-order sums of n (a, b) pairs

@@ -1137,7 +1137,9 @@ __global__ void __launch_bounds__(256) residual_kernel(const T* __restrict__ X, 
                                                         const T* __restrict__ P, int R, const T* __restrict__ Q,
                                                         int64_t ldq, double* __restrict__ part,
                                                         const float* __restrict__ rscale,
-                                                        const float* __restrict__ gate) {
+                                                        const float* __restrict__ gate, int64_t nslice = 1,
+                                                        int64_t sx = 0, int64_t sp = 0) {
+  // nslice > 1: a batch of problems (X + s sx, P + s sp, the same Q): the slab form of resid_sums
   if (gate && *gate != 0.f) return;                      // the fp16-split residual ran (twin of R35)
   const Tacc sc = rscale ? Tacc(*rscale) : Tacc(1);
   constexpr int BM = 128, BN = 64, BR = 16;
@@ -1146,8 +1148,13 @@ __global__ void __launch_bounds__(256) residual_kernel(const T* __restrict__ X, 
   __shared__ double red[32];
   const int t = threadIdx.x, tx = t & 31, ty = t >> 5;
   const int64_t njt = cdiv(J, BM), nit = cdiv(In, BN), ntiles = njt * nit;
+  const T* X0 = X;
+  const T* P0 = P;
   double res = 0.0, xx = 0.0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  for (int64_t tile_s = blockIdx.x; tile_s < ntiles * nslice; tile_s += gridDim.x) {
+    const int64_t tile = tile_s % ntiles, slice = tile_s / ntiles;
+    X = X0 + slice * sx;
+    P = P0 + slice * sp;
     const int64_t j0 = (tile % njt) * BM, i0 = (tile / njt) * BN;
     Tacc acc[4][8];
 #pragma unroll
@@ -1685,9 +1692,10 @@ void residual(const Ctx& ctx, Arena& ws, const T* X, int64_t J, int64_t In, cons
   launch(ctx, "reduce_pairs", [&] { reduce_pairs_kernel<<<1, 256, 0, ctx.stream>>>(part, nblk, out2); });
 }
 void residual_part(const Ctx& ctx, const float* X, int64_t J, int64_t In, const float* P, int R, const float* Q,
-                   int64_t ldq, double* part, int nblk, const float* rscale, const float* gate) {
+                   int64_t ldq, double* part, int nblk, const float* rscale, const float* gate, int64_t nslice,
+                   int64_t sx, int64_t sp) {
   launch(ctx, "residual_simt", [&] {
-    residual_kernel<float><<<nblk, 256, 0, ctx.stream>>>(X, J, In, P, R, Q, ldq, part, rscale, gate);
+    residual_kernel<float><<<nblk, 256, 0, ctx.stream>>>(X, J, In, P, R, Q, ldq, part, rscale, gate, nslice, sx, sp);
   });
 }
 template void residual<float>(const Ctx&, Arena&, const float*, int64_t, int64_t, const float*, int, const float*,

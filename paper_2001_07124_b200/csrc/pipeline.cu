@@ -928,13 +928,21 @@ bool Engine::hosvd_overlap(const TView& X, const float* data, const int64_t* R, 
     cudaEvent_t e = ctx.events->get();
     RT_CUDA(cudaEventRecord(e, ctx.stream));
     RT_CUDA(cudaStreamWaitEvent(sctx.stream, e, 0));
+    cudaEvent_t pre_eig = dist() ? ctx.events->get() : nullptr;
+    st.pre_eig_event = pre_eig;
     st.truncate(X, Gt, K, Qt, ldq, R, Q_out, G_out);
     int64_t gsz = 1;
     for (int n = 0; n < N; ++n) gsz *= R[n];
     sumsq(sctx, st.ws, G_out, gsz, ggR);
     cudaEvent_t done_t = ctx.events->get();
     RT_CUDA(cudaEventRecord(done_t, sctx.stream));
-    ctx.sm_reserve = 3;                        // the truncation's Jacobi CTAs run beside the residual
+    // the truncation's Jacobi CTAs run beside the residual: 3 SMs (its two-CTA clusters then take turns,
+    // still far inside a whole-tensor residual pass); on a slab the residual is short and the Jacobi is
+    // the longer branch: 2 SMs for each of the N clusters
+    ctx.sm_reserve = dist() ? 2 * N : 3;
+    // (on a slab the short residual pass would otherwise take its SMs a moment before the Jacobi is
+    // launched, and scattered leftover SMs cannot host the clusters until it ends)
+    if (pre_eig) RT_CUDA(cudaStreamWaitEvent(ctx.stream, pre_eig, 0));
     const double* Qtc[5];
     for (int n = 0; n < N; ++n) Qtc[n] = Qt[n];
     resid_sums<float>(X, data, Gt, K, Qtc, sums, ggK, rs, true);
@@ -1031,6 +1039,7 @@ void Engine::truncate(const TView& X, const double* Gt, const int64_t* K, const 
     // M_n = G~_(n) G~_(n)^T (Gram-EVD)
     gram_unfold(ctx, ws, Gt, TView::box_of(K, N, n), M[n]);
   }
+  if (pre_eig_event) RT_CUDA(cudaEventRecord(pre_eig_event, ctx.stream));
   eig_sym_batch(ctx, ws, N, M, kk, W, V);
   for (int n = 0; n < N; ++n) {
     const int k = kk[n];
@@ -1079,6 +1088,66 @@ void Engine::resid_sums(const TView& X, const T* data, const double* G, const in
   int64_t gsz = 1;
   for (int n = 0; n < N; ++n) gsz *= R[n];
   sumsq(ctx, ws, G, gsz, gg);
+  if constexpr (std::is_same<T, float>::value) {
+    // Slab form (a thin slab of a slab-parallel call, N >= 3, wide R): the kernel contracts mode N-1
+    // (the second to last) instead of the slab mode.  P' = G x_N Q_N[local rows] x_{k < N-1} Q_k is
+    // J' x R_{N-1} x I_N(local) with J' = I_1 ... I_{N-2}: it shrinks with the slab, where the P of the
+    // form below is the whole J x R_N tensor on every rank (1.34 GB at cfg5, written and read again).
+    // Every slice i_N is one problem X[:, :, i_N] ~ P'[:, :, i_N] Q_{N-1}^T of the same kernel.
+    const int m = N - 2;
+    int64_t Jp = 1;
+    for (int k = 0; k < m; ++k) Jp *= X.d[k];
+    const int64_t Il = X.d[N - 1];
+    if (dist() && N >= 3 && !ctx.resid_slab_off && !ctx.simt() && R[m] > 64 && R[m] <= 128 && (Jp % 4) == 0 &&
+        Il * R[m] * 2 <= X.d[m] * R[N - 1] && Il > 1) {
+      int64_t cur[5];
+      for (int k = 0; k < N; ++k) cur[k] = R[k];
+      // the slab mode first (fp64, small), then modes N-3 .. 0 (the widest stage last, as below)
+      const double* src = G;
+      {
+        const Box b = TView::box_of(cur, N, N - 1);
+        double* dst = ws.alloc_n<double>(b.a * Il * b.b);
+        LabelScope ls(ctx, "pchain");
+        ttm_t<double, double, double>(ctx, src, b, Q[N - 1], Il, 1, int(Il), dst, 1, b.a, b.a * Il);
+        src = dst;
+        cur[N - 1] = Il;
+      }
+      float* Pp = nullptr;
+      for (int n = m - 1; n >= 0; --n) {
+        const Box b = TView::box_of(cur, N, n);
+        const int64_t In = X.d[n];
+        LabelScope ls(ctx, "pchain");
+        if (n == 0) {
+          Pp = ws.alloc_n<float>(b.a * In * b.b);
+          float* sf = ws.alloc_n<float>(b.a * b.I * b.b);
+          float* qf = ws.alloc_n<float>(In * b.I);
+          convert2d<double, float>(ctx, src, b.a * b.I * b.b, 1, b.a * b.I * b.b, sf, b.a * b.I * b.b);
+          convert2d<double, float>(ctx, Q[n], In, b.I, In, qf, In);
+          const int64_t ldt = pad4(b.I);
+          float* qt = ws.alloc_n<float>(ldt * In);
+          if (ldt != b.I) fill_zero(ctx, qt, sizeof(float) * ldt * In);
+          transpose_copy<float>(ctx, qf, b.I, In, In, qt, ldt);
+          ttm_t_dispatch(ctx, ws, sf, b, qt, ldt, int(In), Pp, 1, b.a, b.a * In);
+        } else {
+          double* dst = ws.alloc_n<double>(b.a * In * b.b);
+          ttm_t<double, double, double>(ctx, src, b, Q[n], In, 1, int(In), dst, 1, b.a, b.a * In);
+          src = dst;
+        }
+        cur[n] = In;
+      }
+      const int Rm = int(R[m]);
+      float* qm = ws.alloc_n<float>(X.d[m] * Rm);
+      convert2d<double, float>(ctx, Q[m], X.d[m], Rm, X.d[m], qm, X.d[m]);
+      resid_scale(ctx, gg, double(X.size()) * double(X.glob) / double(X.d[N - 1]), rs);
+      if (residual_tc(ctx, ws, data, Jp, X.d[m], Pp, Jp, Rm, qm, X.d[m], sums, rs, ortho_q ? rs + 1 : nullptr, Il,
+                      Jp * X.d[m], Jp * Rm)) {
+        allreduce(comm, dist(), sums, 2, ctx.stream);                              // C5
+        ws.rewind(mk);
+        return;
+      }
+      ws.rewind(mk);
+    }
+  }
   // P = G x_1 Q_1 ... x_{N-1} Q_{N-1} (all but the last mode), then the residual kernel
   // rebuilds X^ = P x_N Q_N tile by tile against X.  The modes are contracted from N-2 down to 0,
   // so that the widest stage (|P| outputs) contracts mode 0: its new index i_0 is the contiguous

@@ -2342,6 +2342,7 @@ struct RParams {
   double* part;       // [grid][2]
   const float* rscale;   // power-of-two scale applied to x and x^ (resid_scale), nullable
   const float* gate;     // tf32 kernel: run only if *gate == 0 (twin of the fp16-split residual)
+  int64_t tps = 0;       // > 0: sliced form (3-D maps): j tiles per slice; tile t = (slice t / tps, j tile t % tps)
 };
 
 template <int RP>
@@ -2600,15 +2601,21 @@ residual_h16_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_consta
       const uint64_t pol = policy_evict_first();
       const uint64_t pq = policy_evict_last();
       for (int64_t u = 0; u < my_tiles; ++u) {
-        const int j0 = int((blockIdx.x + u * gridDim.x) * BM);
+        const int64_t tile = blockIdx.x + u * gridDim.x;
+        const int slice = p.tps ? int(tile / p.tps) : 0;
+        const int j0 = int((p.tps ? tile % p.tps : tile) * BM);
         if (u >= 1) mbar_wait(p_free, uint32_t(u - 1) & 1);
         mbar_expect_tx(p_full, L::kP);
-        for (int c = 0; c < RP / KC; ++c) tma_load_2d(smem + L::off_p + c * (BM * KC * 4), &tmp, p_full, j0, c * KC);
+        for (int c = 0; c < RP / KC; ++c) {
+          if (p.tps) tma_load_3d(smem + L::off_p + c * (BM * KC * 4), &tmp, p_full, j0, c * KC, slice);
+          else tma_load_2d(smem + L::off_p + c * (BM * KC * 4), &tmp, p_full, j0, c * KC);
+        }
         for (int b = 0; b < p.nblk; ++b, ++it, rg.next<NS>(), rbg.next<NSB>()) {
           // the X tile first (it has the longest way to go), then the B slot
           if (it >= NS) mbar_wait(&st_free[rg.s], rg.ph ^ 1);
           mbar_expect_tx(&st_full[rg.s], L::kXt);
-          tma_load_2d_hint(smem + L::off_st + rg.s * L::kXt, &tmx, &st_full[rg.s], j0, b * RNB, pol);
+          if (p.tps) tma_load_3d_hint(smem + L::off_st + rg.s * L::kXt, &tmx, &st_full[rg.s], j0, b * RNB, slice, pol);
+          else tma_load_2d_hint(smem + L::off_st + rg.s * L::kXt, &tmx, &st_full[rg.s], j0, b * RNB, pol);
           if (it >= NSB) mbar_wait(&b_free[rbg.s], rbg.ph ^ 1);
           uint8_t* st = smem + L::off_b + rbg.s * L::kBst;
           mbar_expect_tx(&b_full[rbg.s], L::kBst);
@@ -2770,26 +2777,31 @@ __global__ void split_transpose_kernel(const float* __restrict__ Q, int64_t In, 
 }  // namespace
 
 bool residual_tc(const Ctx& ctx, Arena& ws, const float* X, int64_t J, int64_t In, const float* P, int64_t ldp,
-                 int R, const float* Q, int64_t ldq, double* part_out2, const float* rscale, const float* pscale) {
+                 int R, const float* Q, int64_t ldq, double* part_out2, const float* rscale, const float* pscale,
+                 int64_t nslice, int64_t sx, int64_t sp) {
+  const bool sliced = nslice > 1;
+  // the sliced form exists for the fp16-split kernel and its SIMT twin (R > 64: R35 runs at the sketch width)
+  if (sliced && (R <= 64 || ldp != J || (sx % 4) || (sp % 4) || nslice > INT32_MAX)) return false;
   // R <= 64: the fp16-split kernel gated against the tf32 kernel; 64 < R <= 128 (the split residual
   // of reading R35 runs at the sketch width K): the fp16-split kernel gated against the SIMT kernel
   if (ctx.simt() || R < 1 || R > 128 || (R > 64 && (!pscale || !ctx.tc_h16 || ctx.resid_tf32))) return false;
   if (!aligned(X, 16) || !aligned(P, 16) || (J % 4) || (ldp % 4) || J > INT32_MAX || In > INT32_MAX) return false;
   const int rp = R <= 32 ? 32 : 64;
   CUtensorMap tx, tp, th, tl;
-  {  // X(j, i) at j + J i: box (128 j, 64 i)
-    const uint64_t d[2] = {uint64_t(J), uint64_t(In)}, s[1] = {uint64_t(J) * 4};
-    const uint32_t bx[2] = {BM, RNB};
-    if (!make_map(&tx, X, 2, d, s, bx, false)) return false;
+  {  // X(j, i) at j + J i: box (128 j, 64 i); sliced: (j, i, s) at j + J i + sx s
+    const uint64_t d[3] = {uint64_t(J), uint64_t(In), uint64_t(nslice)}, s[2] = {uint64_t(J) * 4, uint64_t(sx) * 4};
+    const uint32_t bx[3] = {BM, RNB, 1};
+    if (!make_map(&tx, X, sliced ? 3 : 2, d, s, bx, false)) return false;
   }
   {  // P(j, r) at j + ldp r: box (128 j, 32 r) -> [32 r][128 j]
-    const uint64_t d[2] = {uint64_t(J), uint64_t(R)}, s[1] = {uint64_t(ldp) * 4};
-    const uint32_t bx[2] = {BM, KC};
-    if (!make_map(&tp, P, 2, d, s, bx, false)) return false;
+    const uint64_t d[3] = {uint64_t(J), uint64_t(R), uint64_t(nslice)}, s[2] = {uint64_t(ldp) * 4, uint64_t(sp) * 4};
+    const uint32_t bx[3] = {BM, KC, 1};
+    if (!make_map(&tp, P, sliced ? 3 : 2, d, s, bx, false)) return false;
   }
   RParams p;
   p.J = J; p.In = In; p.R = R;
-  p.ntiles = cdiv(J, BM);
+  p.tps = sliced ? cdiv(J, BM) : 0;
+  p.ntiles = cdiv(J, BM) * nslice;
   p.nblk = int(cdiv(In, RNB));
   const int grid = int(std::max<int64_t>(1, std::min<int64_t>(p.ntiles, ctx.num_sms - ctx.sm_reserve)));
   p.part = ws.alloc_n<double>(2 * grid);
@@ -2841,7 +2853,7 @@ bool residual_tc(const Ctx& ctx, Arena& ws, const float* X, int64_t J, int64_t I
   }
   if (R > 64) {
     // twin: the SIMT residual into the same per-CTA pairs, run only if the P scale is 0
-    residual_part(ctx, X, J, In, P, R, Q, ldq, p.part, grid, rscale, pscale);
+    residual_part(ctx, X, J, In, P, R, Q, ldq, p.part, grid, rscale, pscale, nslice, sx, sp);
   } else {
     if (rp == 32) launch_r<32>(ctx, tx, tp, th, tl, p, grid);
     else launch_r<64>(ctx, tx, tp, th, tl, p, grid);

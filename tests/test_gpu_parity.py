@@ -473,3 +473,28 @@ def test_loopback_overlapped_hosvd(P, nranks, opts):
         assert M.subspace(qg[n], ref["Q"][n]) <= 1e-5, (n, M.subspace(qg[n], ref["Q"][n]))
     assert M.recon(out[0]["G"], qg, ref["G"], ref["Q"]) <= 1e-5
     assert abs(out[0]["err"][0] - ref["E"]) / ref["E"] <= 1e-5
+
+
+@pytest.mark.parametrize("nranks,opts", [(2, ()), (3, ()), (2, ((100, 350),)), (2, ((100, 212),))])
+def test_loopback_slab_residual(P, nranks, opts):
+    """The slab form of the residual pass: with a wide sketch (K = 72 > 64) and
+    a thin slab, a slab-parallel HOSVD rebuilds X^ slice by slice of the slab mode from
+    P' = G x_3 Q_3[local] x_1 Q_1 (J' x K_2 x I_3(local)) with mode 2 contracted in the kernel,
+    instead of from the whole J x K_3 tensor P on every rank.  E against the oracle at 1e-5, with
+    the old form (option 350) and with the fp16 gate closed (option 212: the SIMT twin in its
+    sliced form); replicated outputs agree bit for bit."""
+    cfg = dataclasses.replace(synth.CONFIGS["cfg5"].scaled((96, 88, 80), (64, 64, 64), (64, 64, 64)), q=1, p=8)
+    assert all(cfg.K(n) == 72 for n in range(3))
+    x = synth.make_tensor(cfg)
+    oms = [synth.gaussian_omega(cfg, n) for n in range(3)]
+    ref = oracle.hosvd(x, cfg.ranks, oms, q=1)
+    cuts = np.linspace(0, cfg.dims[2], nranks + 1).astype(int)
+    out = _run_loopback(P, x, cfg, oms, nranks, [(int(cuts[r]), int(cuts[r + 1])) for r in range(nranks)], opts)
+    for r in range(1, nranks):
+        np.testing.assert_array_equal(out[r]["G"], out[0]["G"])
+        np.testing.assert_array_equal(out[r]["err"], out[0]["err"])
+    qg = out[0]["Q"][:2] + [np.concatenate([out[r]["Q"][2] for r in range(nranks)], axis=0)]
+    for n in range(3):
+        assert M.subspace(qg[n], ref["Q"][n]) <= 1e-5, (n, M.subspace(qg[n], ref["Q"][n]))
+    assert M.recon(out[0]["G"], qg, ref["G"], ref["Q"]) <= 1e-5
+    assert abs(out[0]["err"][0] - ref["E"]) / ref["E"] <= 1e-5, (out[0]["err"][0], ref["E"])
