@@ -118,7 +118,8 @@ rt_status rt_sync(rt_handle* h);
  * and power product / takes the 3xTF32 kernels on the fp32 operands (default);
  * 330 / 331 = the intermediate thin QRs of the power steps take three CholeskyQR steps / two (default,
  * DESIGN.md reading R36); 340 / 341 = the core's second stage waits for every factor / runs beside
- * the last QR (default). */
+ * the last QR (default); 350 / 351 = a slab's residual pass keeps the J x R_N form of
+ * P / takes the slab form (default on a thin slab). */
 typedef enum { RT_OPT_TTM_IMPL = 0, RT_OPT_PROFILE = 1, RT_OPT_QR_FALLBACK = 2, RT_OPT_OMEGA_TF32 = 3,
                RT_OPT_TC_SEGMENT = 4, RT_OPT_TC_SKEW = 5,
                RT_OPT_FORCE_COLLECTIVES = 6 /* tests: run the slab exchanges even on a 1-rank communicator */,
