@@ -1259,7 +1259,7 @@ __global__ void finalize_err_split_kernel(const double* sums, const double* ggK,
 // residual: every |P_jr| <= ||P||_F = ||G||_F (orthonormal factors), so s[1] = 2^(14 - e_G) with
 // ||G|| in [2^(e_G-1), 2^e_G) keeps |s[1] P| < 2^14, inside the fp16 range; 0 (the tf32 residual
 // runs) when ||G|| is 0 or not finite.
-__global__ void resid_scale_kernel(const double* gg, double numel, float* s) {
+__global__ void resid_scale_kernel(const double* gg, double numel, float* s, bool force_twin) {
   float r = 1.f, sp = 0.f;
   const double rms = sqrt(*gg / numel);
   if (rms > 0.0 && isfinite(rms)) {
@@ -1274,7 +1274,7 @@ __global__ void resid_scale_kernel(const double* gg, double numel, float* s) {
     if (14 - e >= -120 && 14 - e <= 113) sp = ldexpf(1.f, 14 - e);
   }
   s[0] = r;
-  s[1] = sp;
+  s[1] = force_twin ? 0.f : sp;             // option 212: the gate forced closed, the twin residual runs (tests)
 }
 
 __global__ void nonfinite_kernel(const double* __restrict__ x, int64_t n, int* status) {
@@ -1769,7 +1769,7 @@ void finalize_err_split(const Ctx& ctx, const double* sums, const double* ggK, c
   });
 }
 void resid_scale(const Ctx& ctx, const double* gg, double numel, float* s) {
-  launch(ctx, "resid_scale", [&] { resid_scale_kernel<<<1, 1, 0, ctx.stream>>>(gg, numel, s); });
+  launch(ctx, "resid_scale", [&] { resid_scale_kernel<<<1, 1, 0, ctx.stream>>>(gg, numel, s, ctx.tc_h16 == 2); });
 }
 
 void fill_zero(const Ctx& ctx, void* p, size_t bytes) { RT_CUDA(cudaMemsetAsync(p, 0, bytes, ctx.stream)); }
