@@ -112,7 +112,8 @@ rt_status rt_sync(rt_handle* h);
  * RT_OPT_TC_ABLATE: profiling ablations (values 1, 2, 1000, 2000 give invalid results) and valid
  * A/B switches of the product path: 210 / 211 = the fp16-split form of the X passes that multiply
  * an orthonormal Q (power products, first core stage; R29) off / on (default on), 212 =
- * on with its device-side range gate forced closed (the tf32 twin launches do the work; tests);
+ * on with its device-side range gates forced closed (the twin launches do the work, the residual pass's
+ * included; tests);
  * 220 / 221 = RP-HOOI's X pass on the fp64 warp MMA / on the tensor cores (default, R30);
  * 320 / 321 = the slab mode of a thin slab (I_N(local) < 8 K) keeps the fp16 forms of its Omega sketch
  * and power product / takes the 3xTF32 kernels on the fp32 operands (default);
